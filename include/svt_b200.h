@@ -1,0 +1,207 @@
+/*
+ * svt_b200.h — the C-ABI boundary of the B200-native SVT / R3SVD / R4SVD hot
+ * path (arXiv 1704.05528).  Plain pointers and sizes only; no torch, Eigen or
+ * CUDA types cross this boundary.
+ *
+ * Every entry point replaces one function of the reference's header-only C++
+ * API (`proj/include/svt/` headers, cited per function).  Dense host buffers use
+ * the reference's Eigen::MatrixXd layout (column-major, leading dimension =
+ * rows), so a reference-side binding passes `M.data()` straight through (see
+ * INTEGRATION.md).  Errors are reported as return codes mapping one-to-one
+ * onto the reference's exception types; the message is in svt_last_error().
+ *
+ * Multi-GPU: one process per GPU.  A distributed context owns a row block
+ * [row_begin, row_end) of every sampled matrix; "local" row-indexed arrays
+ * (U, X, Q) cover only that block, n-indexed arrays (V, Omega, B^T) are
+ * replicated.  Collectives are NCCL all-reduces inside the library.
+ */
+#ifndef SVT_B200_H
+#define SVT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define SVT_OK 0
+#define SVT_EINVAL 1   /* std::invalid_argument (shapes, parameters)        */
+#define SVT_EDOMAIN 2  /* std::domain_error (all-zero target)               */
+#define SVT_ERUNTIME 3 /* std::runtime_error                                */
+#define SVT_ECUDA 4    /* CUDA runtime / kernel failure                     */
+#define SVT_ENCCL 5    /* NCCL failure                                      */
+#define SVT_EOOM 6     /* device allocation failed                          */
+
+/* ---- parameter / record structs (mirror the reference structs) --------- */
+
+/* SketchParams, sketch.hpp:20-27 */
+typedef struct svt_sketch_params {
+    int64_t t;
+    int64_t dt;
+    int32_t np;
+    int32_t reserved0;
+    double eps_threshold;
+    uint64_t seed;
+    int64_t p;
+} svt_sketch_params;
+
+/* SvtConfig, solver.hpp:32-43, plus the two Appendix-B harness extensions
+ * (0 = reference behaviour). */
+typedef struct svt_config {
+    double tau;
+    double delta;
+    int32_t maxit;
+    int32_t np;
+    int64_t dt;
+    double eps_stop;
+    double eps_threshold0;
+    double beta;
+    int64_t t0;
+    uint64_t seed;
+    double eps_threshold_min; /* cooling floor: eps <- max(eps*beta, min) */
+    double rel_residual_stop; /* stop when ||P(X-A)||/||P A|| < this      */
+} svt_config;
+
+/* StopRule, solver.hpp:59-67 */
+#define SVT_STOP_TRAIN_MAE 0
+#define SVT_STOP_RESIDUAL 1
+#define SVT_STOP_NONE 2
+typedef struct svt_stop {
+    int32_t kind;
+    int32_t reserved0;
+    double threshold;
+} svt_stop;
+
+/* Backend, solver.hpp:69-78 */
+#define SVT_BACKEND_R4SVD 0
+#define SVT_BACKEND_R3SVD 1
+#define SVT_BACKEND_RSVD_FIXED 2
+#define SVT_BACKEND_FULL_SVD 3
+typedef struct svt_backend {
+    int32_t kind;
+    int32_t reserved0;
+    int64_t fixed_rank;
+} svt_backend;
+
+/* IterationRecord, solver.hpp:49-57 (+ extension columns) */
+typedef struct svt_record {
+    int32_t iter;
+    int32_t extension_rounds;
+    int64_t rank;
+    double residual;
+    double eps_threshold;
+    double train_mae;
+    double sketch_ms;
+    double total_ms;
+    int64_t kept;          /* rank of the shrunk iterate X             */
+    double rel_residual_x; /* ||P_Lambda(X - A)||_F / ||P_Lambda A||_F */
+    double test_mae;       /* held-out MAE (0 without a test set)      */
+    double test_rmse;      /* held-out RMSE (0 without a test set)     */
+} svt_record;
+
+/* IterationObserver, solver.hpp:88.  U is m_local x k, V is n x k
+ * (column-major host copies valid during the call).  Return 0 to stop. */
+typedef int (*svt_observer_fn)(const svt_record* rec, int64_t m_local, int64_t n, int64_t k,
+                               const double* U, const double* sigma, const double* V, void* user);
+
+/* ---- opaque handles ---------------------------------------------------- */
+typedef struct svt_ctx svt_ctx;         /* device, stream, comm, workspaces */
+typedef struct svt_mat svt_mat;         /* SampledMatrix on the device      */
+typedef struct svt_factors svt_factors; /* SketchResult / LowRankFactors    */
+typedef struct svt_solver svt_solver;   /* svt_run_backend state            */
+typedef struct svt_result svt_result;   /* SvtResult                        */
+
+/* ---- context ----------------------------------------------------------- */
+const char* svt_last_error(void);
+int svt_version(void);
+int svt_ctx_create(int device, svt_ctx** out);
+/* One rank of a world: nccl_id is the 128-byte ncclUniqueId of rank 0. */
+int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, svt_ctx** out);
+int svt_nccl_get_unique_id(void* out128);
+int svt_ctx_destroy(svt_ctx* ctx);
+int svt_ctx_sync(svt_ctx* ctx);
+void* svt_ctx_stream(svt_ctx* ctx); /* the cudaStream_t every kernel runs on */
+int svt_ctx_rank(svt_ctx* ctx, int* rank, int* world);
+/* instrumentation: per-kernel-class CUDA-event timing (0 = off) */
+int svt_ctx_set_profiling(svt_ctx* ctx, int on);
+int svt_ctx_reset_stats(svt_ctx* ctx);
+/* class: 0 SpMM, 1 SpMM^T, 2 SDDMM+update, 3 CGS/GEMM passes, 4 RNG, 5 QR, 6 finalize, 7 other */
+int svt_ctx_kernel_stats(svt_ctx* ctx, int cls, int64_t* launches, double* total_ms, double* bytes,
+                         double* flops);
+int64_t svt_ctx_launch_count(svt_ctx* ctx);
+
+/* ---- host-side sample-set construction (SampledMatrix ctor, sampled.hpp:27-62) */
+/* Validates and sorts triplets into CSR; throws-equivalent SVT_EINVAL on
+ * out-of-range, duplicate or non-finite entries. */
+int svt_sampled_build(int64_t m, int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                      const double* vals, int64_t* rowptr_out, int64_t* col_out, double* val_out);
+/* nnz-balanced row partition for `world` ranks: bounds[world+1]. */
+int svt_partition_rows(int64_t m, const int64_t* rowptr, int world, int64_t* bounds);
+
+/* ---- device sample-set matrices --------------------------------------- */
+/* rowptr has (row_end-row_begin+1) entries, offsets into col/val (rowptr[0]
+ * is subtracted).  col is 0-based global column index. */
+int svt_matrix_upload(svt_ctx* ctx, int64_t m, int64_t n, int64_t row_begin, int64_t row_end,
+                      const int64_t* rowptr, const int64_t* col, const double* val, svt_mat** out);
+int svt_matrix_free(svt_mat* mat);
+int svt_matrix_info(svt_mat* mat, int64_t* m, int64_t* n, int64_t* nnz_local, int64_t* row_begin,
+                    int64_t* row_end);
+int svt_matrix_set_values(svt_mat* mat, const double* vals);
+int svt_matrix_get_values(svt_mat* mat, double* vals);
+
+/* ---- primitives (host in/out; dense.hpp / sampled.hpp) ---------------- */
+int svt_gaussian_block(svt_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out); /* dense.hpp:86 */
+int svt_qr_orthonormal(svt_ctx* ctx, int64_t rows, int64_t cols, const double* X, double* Q); /* dense.hpp:103 */
+int svt_small_svd(svt_ctx* ctx, int64_t rows, int64_t cols, const double* B, double* U, double* sigma,
+                  double* V); /* dense.hpp:114; U rows x k, V cols x k, k = min */
+int svt_sp_mult(svt_mat* S, int64_t w, const double* X, double* out);   /* sampled.hpp:113 */
+int svt_sp_mult_t(svt_mat* S, int64_t w, const double* X, double* out); /* sampled.hpp:130 */
+int svt_project_low_rank(svt_mat* pattern, int64_t k, const double* U, const double* sigma, const double* V,
+                         double* out_vals); /* sampled.hpp:148 */
+int svt_sp_axpy(svt_mat* Y, double alpha, const double* d_vals, double* out_vals); /* sampled.hpp:166 */
+int svt_sp_frob_norm_sq(svt_mat* S, double* out);                                 /* sampled.hpp:178 */
+int svt_spectral_norm_est(svt_mat* S, int iters, uint64_t seed, double* out);     /* sampled.hpp:188 */
+int svt_kickstart(svt_mat* A, double tau, double delta, uint64_t seed, double* out_vals); /* solver.hpp:125 */
+
+/* ---- sketch engines (sketch.hpp) -------------------------------------- */
+int svt_rsvd(svt_mat* Y, int64_t k, const svt_sketch_params* p, svt_factors** out);  /* sketch.hpp:165 */
+int svt_r3svd(svt_mat* Y, const svt_sketch_params* p, svt_factors** out);            /* sketch.hpp:188 */
+int svt_r4svd(svt_mat* Y, int64_t s, const double* U_prev, int64_t ldu, const svt_sketch_params* p,
+              svt_factors** out); /* sketch.hpp:207 */
+int svt_factors_info(svt_factors* f, int64_t* m_local, int64_t* n, int64_t* rank, int* saturated,
+                     int* extension_rounds);
+int svt_factors_copy(svt_factors* f, double* U, double* sigma, double* V);
+int svt_factors_free(svt_factors* f);
+
+/* ---- solver (solver.hpp:215-340) -------------------------------------- */
+int svt_default_config(svt_mat* A, svt_config* out); /* solver.hpp:95 */
+int svt_solver_create(svt_mat* A, const svt_config* cfg, svt_stop stop, svt_backend backend, svt_mat* test,
+                      svt_solver** out);
+/* one Bregman iteration; *done = 1 when the run stopped (stop rule/observer
+ * or maxit) — then svt_solver_result() is final. */
+int svt_solver_step(svt_solver* s, svt_observer_fn obs, void* user, svt_record* rec, int* done);
+int svt_solver_result(svt_solver* s, svt_result** out);
+int svt_solver_free(svt_solver* s);
+int svt_run(svt_mat* A, const svt_config* cfg, svt_stop stop, svt_backend backend, svt_mat* test,
+            svt_observer_fn obs, void* user, svt_result** out); /* solver.hpp:215 / 333 / 340 */
+int svt_result_info(svt_result* r, int64_t* n_records, int64_t* m_local, int64_t* n, int64_t* k, int* converged);
+int svt_result_trace(svt_result* r, svt_record* out);
+int svt_result_factors(svt_result* r, double* U, double* sigma, double* V);
+int svt_result_free(svt_result* r);
+
+/* ---- synthetic inputs for the five BASELINE configs (host) ------------- */
+/* Generates the observed (train) triplets and, for configs 3/4, the held-out
+ * test triplets.  Two-phase: call with NULL buffers to get sizes. */
+int svt_synth_config(int config, uint64_t seed, int64_t* m, int64_t* n, int64_t* nnz_train, int64_t* nnz_test,
+                     int64_t* train_rows, int64_t* train_cols, double* train_vals, int64_t* test_rows,
+                     int64_t* test_cols, double* test_vals);
+/* CSR directly (configs too large for triplets, e.g. config 5): rowptr m+1. */
+int svt_synth_config_csr(int config, uint64_t seed, int64_t* m, int64_t* n, int64_t* nnz, int64_t* rowptr,
+                         int64_t* col, double* val);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SVT_B200_H */
