@@ -1,0 +1,566 @@
+"""Python mirror of the reference's public API (proj/include/svt/*.hpp) over
+the C ABI of libsvt_b200.so (include/svt_b200.h).
+
+Names, argument meaning and error behaviour follow the reference:
+`SampledMatrix(rows, cols, triplets)` validates like sampled.hpp:27-62,
+`r3svd` / `r4svd` / `rsvd` return `SketchResult`-like objects
+(sketch.hpp:41-46), `svt_run_backend` drives the Bregman loop
+(solver.hpp:215-328) with an optional `IterationObserver`.  Invalid arguments
+raise `InvalidArgument` (std::invalid_argument), an all-zero target raises
+`DomainError` (std::domain_error).
+
+There is no CPU fallback: every numeric entry point runs the CUDA kernels of
+the extension, and a missing extension raises at first use.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._abi import (OBSERVER_FN, Backend, IterationRecord, SketchParams, StopRule, SvtConfig, raise_for)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libsvt_b200.so")
+_lib = None
+
+P_I64 = C.POINTER(C.c_int64)
+P_F64 = C.POINTER(C.c_double)
+
+
+def lib():
+    """Load libsvt_b200.so (raises if the CUDA extension was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libsvt_b200.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        L.svt_last_error.restype = C.c_char_p
+        L.svt_ctx_stream.restype = C.c_void_p
+        L.svt_ctx_stream.argtypes = [C.c_void_p]
+        L.svt_ctx_launch_count.restype = C.c_int64
+        L.svt_ctx_launch_count.argtypes = [C.c_void_p]
+        for name in ("svt_ctx_destroy", "svt_matrix_free", "svt_factors_free", "svt_solver_free",
+                     "svt_result_free", "svt_ctx_sync"):
+            getattr(L, name).argtypes = [C.c_void_p]
+        _lib = L
+    return _lib
+
+
+def _check(code):
+    if code != 0:
+        raise_for(code, lib().svt_last_error().decode())
+
+
+def _ptr(a, t=P_F64):
+    return a.ctypes.data_as(t)
+
+
+def _cm(a):
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _cm_buf(a):
+    a = _cm(a)
+    return a.ravel(order="F").copy() if a.size else np.zeros(1)
+
+
+def _from_cm(buf, rows, cols):
+    return np.asarray(buf[: rows * cols], dtype=np.float64).reshape((cols, rows)).T.copy()
+
+
+# ---------------------------------------------------------------------------
+class Context:
+    """One device (and, multi-GPU, one rank of an NCCL world): stream,
+    communicator, workspaces and instrumentation (svt_ctx)."""
+
+    def __init__(self, device=0, rank=0, world=1, nccl_id: bytes | None = None):
+        h = C.c_void_p()
+        if world == 1:
+            _check(lib().svt_ctx_create(C.c_int(device), C.byref(h)))
+        else:
+            buf = C.create_string_buffer(nccl_id, 128)
+            _check(lib().svt_ctx_create_dist(C.c_int(device), C.c_int(rank), C.c_int(world), buf, C.byref(h)))
+        self.h = h
+        self.device, self.rank, self.world = device, rank, world
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().svt_nccl_get_unique_id(buf))
+        return buf.raw
+
+    @property
+    def stream(self):
+        return lib().svt_ctx_stream(self.h)
+
+    def sync(self):
+        _check(lib().svt_ctx_sync(self.h))
+
+    def set_profiling(self, on: bool):
+        _check(lib().svt_ctx_set_profiling(self.h, C.c_int(1 if on else 0)))
+
+    def reset_stats(self):
+        _check(lib().svt_ctx_reset_stats(self.h))
+
+    def kernel_stats(self, cls: int):
+        n, ms, b, f = C.c_int64(), C.c_double(), C.c_double(), C.c_double()
+        _check(lib().svt_ctx_kernel_stats(self.h, C.c_int(cls), C.byref(n), C.byref(ms), C.byref(b), C.byref(f)))
+        return dict(launches=n.value, total_ms=ms.value, bytes=b.value, flops=f.value)
+
+    def launch_count(self) -> int:
+        return int(lib().svt_ctx_launch_count(self.h))
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().svt_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+# ---------------------------------------------------------------------------
+def build_csr(m, n, rows, cols, vals):
+    """SampledMatrix ctor semantics (sampled.hpp:27-62) on the host: returns
+    sorted CSR (rowptr, col, val) or raises InvalidArgument."""
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    cols = np.ascontiguousarray(cols, dtype=np.int64)
+    vals = np.ascontiguousarray(vals, dtype=np.float64)
+    nnz = len(vals)
+    if len(rows) != nnz or len(cols) != nnz:
+        raise ValueError("rows/cols/vals length mismatch")
+    rp = np.zeros(max(m, 0) + 1, dtype=np.int64)
+    co = np.zeros(max(nnz, 1), dtype=np.int64)
+    va = np.zeros(max(nnz, 1), dtype=np.float64)
+    _check(lib().svt_sampled_build(C.c_int64(m), C.c_int64(n), C.c_int64(nnz),
+                                   _ptr(rows, P_I64) if nnz else None, _ptr(cols, P_I64) if nnz else None,
+                                   _ptr(vals) if nnz else None, _ptr(rp, P_I64), _ptr(co, P_I64), _ptr(va)))
+    return rp, co[:nnz].copy(), va[:nnz].copy()
+
+
+def partition_rows(rowptr, world):
+    """nnz-balanced row partition (bounds has world + 1 entries)."""
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    b = np.zeros(world + 1, dtype=np.int64)
+    _check(lib().svt_partition_rows(C.c_int64(len(rowptr) - 1), _ptr(rowptr, P_I64), C.c_int(world),
+                                    _ptr(b, P_I64)))
+    return b
+
+
+class SampledMatrix:
+    """Device-resident sample-set matrix (sampled.hpp:25-110).
+
+    Construct from triplets (`SampledMatrix(m, n, rows, cols, vals)`) or from
+    host CSR (`SampledMatrix.from_csr`).  In a multi-rank context the
+    instance holds the rank's row block [row_begin, row_end)."""
+
+    def __init__(self, m, n, rows=None, cols=None, vals=None, ctx: Context | None = None, *, _csr=None,
+                 row_block=None):
+        self.ctx = ctx or default_context()
+        if _csr is None:
+            _csr = build_csr(m, n, rows, cols, vals)
+        rp, co, va = _csr
+        self.m, self.n = int(m), int(n)
+        rb, re_ = (0, self.m) if row_block is None else (int(row_block[0]), int(row_block[1]))
+        lrp = np.ascontiguousarray(rp[rb: re_ + 1], dtype=np.int64)
+        self.rowptr_global = rp
+        self.row_begin, self.row_end = rb, re_
+        self.rowptr = lrp - lrp[0]
+        s, e = int(lrp[0]), int(lrp[-1])
+        self.col = np.ascontiguousarray(co[s:e], dtype=np.int64)
+        self._val = np.ascontiguousarray(va[s:e], dtype=np.float64)
+        h = C.c_void_p()
+        _check(lib().svt_matrix_upload(self.ctx.h, C.c_int64(self.m), C.c_int64(self.n), C.c_int64(rb),
+                                       C.c_int64(re_), _ptr(self.rowptr, P_I64),
+                                       _ptr(self.col if self.col.size else np.zeros(1, np.int64), P_I64),
+                                       _ptr(self._val if self._val.size else np.zeros(1)), C.byref(h)))
+        self.h = h
+
+    @classmethod
+    def from_csr(cls, m, n, rowptr, col, val, ctx=None, row_block=None):
+        return cls(m, n, ctx=ctx, _csr=(np.asarray(rowptr, np.int64), np.asarray(col, np.int64),
+                                        np.asarray(val, np.float64)), row_block=row_block)
+
+    def rows(self):
+        return self.m
+
+    def cols(self):
+        return self.n
+
+    @property
+    def nnz(self):
+        return int(self.rowptr[-1])
+
+    def values(self):
+        out = np.zeros(max(self.nnz, 1))
+        _check(lib().svt_matrix_get_values(self.h, _ptr(out)))
+        return out[: self.nnz]
+
+    def set_values(self, vals):
+        vals = np.ascontiguousarray(vals, dtype=np.float64)
+        if vals.shape != (self.nnz,):
+            raise ValueError("with_values: size mismatch")
+        _check(lib().svt_matrix_set_values(self.h, _ptr(vals)))
+        self._val = vals.copy()
+
+    def with_values(self, vals):
+        """New device matrix on the identical pattern (sampled.hpp:79-91)."""
+        vals = np.ascontiguousarray(vals, dtype=np.float64)
+        if vals.shape != (self.nnz,):
+            from ._abi import InvalidArgument
+            raise InvalidArgument("with_values: size mismatch")
+        full = self.rowptr_global
+        va = np.zeros(int(full[-1]))
+        va[int(full[self.row_begin]): int(full[self.row_end])] = vals
+        co = np.zeros(int(full[-1]), dtype=np.int64)
+        co[int(full[self.row_begin]): int(full[self.row_end])] = self.col
+        return SampledMatrix(self.m, self.n, ctx=self.ctx, _csr=(full, co, va),
+                             row_block=(self.row_begin, self.row_end))
+
+    def row_index(self):
+        return np.repeat(np.arange(self.row_begin, self.row_end, dtype=np.int64), np.diff(self.rowptr))
+
+    def dense(self):
+        D = np.zeros((self.m, self.n))
+        D[self.row_index(), self.col] = self.values()
+        return D
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().svt_matrix_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# dense.hpp
+def gaussian_block(rows, cols, seed, ctx=None):
+    ctx = ctx or default_context()
+    out = np.zeros(max(rows * cols, 1))
+    _check(lib().svt_gaussian_block(ctx.h, C.c_int64(rows), C.c_int64(cols), C.c_uint64(seed), _ptr(out)))
+    return _from_cm(out, rows, cols)
+
+
+def qr_orthonormal(X, ctx=None):
+    ctx = ctx or default_context()
+    X = _cm(X)
+    r, c = X.shape
+    out = np.zeros(max(r * c, 1))
+    _check(lib().svt_qr_orthonormal(ctx.h, C.c_int64(r), C.c_int64(c), _ptr(_cm_buf(X)), _ptr(out)))
+    return _from_cm(out, r, c)
+
+
+def small_svd(B, ctx=None):
+    ctx = ctx or default_context()
+    B = _cm(B)
+    r, c = B.shape
+    k = min(r, c)
+    U = np.zeros(max(r * k, 1))
+    s = np.zeros(max(k, 1))
+    V = np.zeros(max(c * k, 1))
+    _check(lib().svt_small_svd(ctx.h, C.c_int64(r), C.c_int64(c), _ptr(_cm_buf(B)), _ptr(U), _ptr(s), _ptr(V)))
+    return _from_cm(U, r, k), s[:k], _from_cm(V, c, k)
+
+
+# sampled.hpp
+def sp_mult(S: SampledMatrix, X):
+    X = _cm(X)
+    if X.shape[0] != S.n:
+        from ._abi import InvalidArgument
+        raise InvalidArgument("sp_mult: inner dimensions disagree")
+    w = X.shape[1]
+    ml = S.row_end - S.row_begin
+    out = np.zeros(max(ml * w, 1))
+    _check(lib().svt_sp_mult(S.h, C.c_int64(w), _ptr(_cm_buf(X)), _ptr(out)))
+    return _from_cm(out, ml, w)
+
+
+def sp_mult_t(S: SampledMatrix, X):
+    X = _cm(X)
+    ml = S.row_end - S.row_begin
+    if X.shape[0] != ml:
+        from ._abi import InvalidArgument
+        raise InvalidArgument("sp_mult_t: inner dimensions disagree")
+    w = X.shape[1]
+    out = np.zeros(max(S.n * w, 1))
+    _check(lib().svt_sp_mult_t(S.h, C.c_int64(w), _ptr(_cm_buf(X)), _ptr(out)))
+    return _from_cm(out, S.n, w)
+
+
+def project_low_rank(S: SampledMatrix, U, sigma, V):
+    U, V = _cm(U), _cm(V)
+    sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+    ml = S.row_end - S.row_begin
+    if U.shape[0] != ml or V.shape[0] != S.n:
+        from ._abi import InvalidArgument
+        raise InvalidArgument("project_low_rank: factor dimensions disagree with pattern")
+    k = len(sigma)
+    out = np.zeros(max(S.nnz, 1))
+    _check(lib().svt_project_low_rank(S.h, C.c_int64(k), _ptr(_cm_buf(U)), _ptr(sigma if k else np.zeros(1)),
+                                      _ptr(_cm_buf(V)), _ptr(out)))
+    return out[: S.nnz]
+
+
+def sp_axpy(Y: SampledMatrix, alpha, d_vals):
+    d = np.ascontiguousarray(d_vals, dtype=np.float64)
+    out = np.zeros(max(Y.nnz, 1))
+    _check(lib().svt_sp_axpy(Y.h, C.c_double(alpha), _ptr(d if d.size else np.zeros(1)), _ptr(out)))
+    return out[: Y.nnz]
+
+
+def sp_frob_norm_sq(S: SampledMatrix):
+    out = C.c_double()
+    _check(lib().svt_sp_frob_norm_sq(S.h, C.byref(out)))
+    return out.value
+
+
+def spectral_norm_est(S: SampledMatrix, iters, seed):
+    out = C.c_double()
+    _check(lib().svt_spectral_norm_est(S.h, C.c_int(iters), C.c_uint64(seed), C.byref(out)))
+    return out.value
+
+
+def kickstart(A: SampledMatrix, tau, delta, seed):
+    out = np.zeros(max(A.nnz, 1))
+    _check(lib().svt_kickstart(A.h, C.c_double(tau), C.c_double(delta), C.c_uint64(seed), _ptr(out)))
+    return out[: A.nnz]
+
+
+# ---------------------------------------------------------------------------
+# sketch.hpp
+@dataclass
+class SketchResult:
+    """sketch.hpp:41-46"""
+    U: np.ndarray
+    sigma: np.ndarray
+    V: np.ndarray
+    rank: int
+    saturated: bool
+    extension_rounds: int
+
+
+def _take_factors(h):
+    ml, n, k, sat, rounds = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int(), C.c_int()
+    try:
+        _check(lib().svt_factors_info(h, C.byref(ml), C.byref(n), C.byref(k), C.byref(sat), C.byref(rounds)))
+        kk = k.value
+        U = np.zeros(max(ml.value * kk, 1))
+        s = np.zeros(max(kk, 1))
+        V = np.zeros(max(n.value * kk, 1))
+        _check(lib().svt_factors_copy(h, _ptr(U), _ptr(s), _ptr(V)))
+        return _from_cm(U, ml.value, kk), s[:kk], _from_cm(V, n.value, kk), kk, bool(sat.value), rounds.value
+    finally:
+        lib().svt_factors_free(h)
+
+
+def rsvd(Y: SampledMatrix, k, p: SketchParams):
+    h = C.c_void_p()
+    _check(lib().svt_rsvd(Y.h, C.c_int64(k), C.byref(p), C.byref(h)))
+    U, s, V, kk, _, _ = _take_factors(h)
+    return SketchResult(U, s, V, kk, False, 0)
+
+
+def r3svd(Y: SampledMatrix, p: SketchParams):
+    h = C.c_void_p()
+    _check(lib().svt_r3svd(Y.h, C.byref(p), C.byref(h)))
+    U, s, V, kk, sat, rounds = _take_factors(h)
+    return SketchResult(U, s, V, kk, sat, rounds)
+
+
+def r4svd(Y: SampledMatrix, U_prev, p: SketchParams):
+    U_prev = _cm(U_prev)
+    s = U_prev.shape[1] if U_prev.ndim == 2 else 0
+    if s and U_prev.shape[0] != (Y.row_end - Y.row_begin):
+        from ._abi import InvalidArgument
+        raise InvalidArgument("r4svd: U_prev row count does not match Y")
+    h = C.c_void_p()
+    _check(lib().svt_r4svd(Y.h, C.c_int64(s), _ptr(_cm_buf(U_prev)), C.c_int64(max(U_prev.shape[0], 1)),
+                           C.byref(p), C.byref(h)))
+    U, sg, V, kk, sat, rounds = _take_factors(h)
+    return SketchResult(U, sg, V, kk, sat, rounds)
+
+
+# ---------------------------------------------------------------------------
+# solver.hpp
+def default_config(A: SampledMatrix) -> SvtConfig:
+    cfg = SvtConfig()
+    _check(lib().svt_default_config(A.h, C.byref(cfg)))
+    return cfg
+
+
+@dataclass
+class SvtResult:
+    """solver.hpp:80-84"""
+    U: np.ndarray
+    sigma: np.ndarray
+    V: np.ndarray
+    trace: list = field(default_factory=list)
+    converged: bool = False
+
+
+def _wrap_observer(observer):
+    if observer is None:
+        return None
+
+    def _obs(rec, m_local, n, k, U, sigma, V, user):
+        r = rec.contents.as_dict()
+        Uk = np.ctypeslib.as_array(U, shape=(m_local * k,)).copy() if k else np.zeros(0)
+        sk = np.ctypeslib.as_array(sigma, shape=(k,)).copy() if k else np.zeros(0)
+        Vk = np.ctypeslib.as_array(V, shape=(n * k,)).copy() if k else np.zeros(0)
+        return 1 if observer(r, _from_cm(Uk, m_local, k), sk, _from_cm(Vk, n, k)) else 0
+
+    return OBSERVER_FN(_obs)
+
+
+def _take_result(h):
+    L = lib()
+    try:
+        nrec, ml, n, k, conv = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
+        _check(L.svt_result_info(h, C.byref(nrec), C.byref(ml), C.byref(n), C.byref(k), C.byref(conv)))
+        recs = (IterationRecord * max(nrec.value, 1))()
+        _check(L.svt_result_trace(h, recs))
+        kk = k.value
+        U = np.zeros(max(ml.value * kk, 1))
+        s = np.zeros(max(kk, 1))
+        V = np.zeros(max(n.value * kk, 1))
+        _check(L.svt_result_factors(h, _ptr(U), _ptr(s), _ptr(V)))
+        return SvtResult(_from_cm(U, ml.value, kk), s[:kk], _from_cm(V, n.value, kk),
+                         [recs[i].as_dict() for i in range(nrec.value)], bool(conv.value))
+    finally:
+        L.svt_result_free(h)
+
+
+def svt_run_backend(A: SampledMatrix, cfg: SvtConfig, stop: StopRule, backend: Backend, observer=None,
+                    test: SampledMatrix | None = None) -> SvtResult:
+    """solver.hpp:215-328.  observer(record_dict, U, sigma, V) -> bool."""
+    cb = _wrap_observer(observer)
+    h = C.c_void_p()
+    _check(lib().svt_run(A.h, C.byref(cfg), stop, backend, test.h if test is not None else None, cb, None,
+                         C.byref(h)))
+    return _take_result(h)
+
+
+def svt_run(A, cfg, stop, observer=None, test=None):
+    """solver.hpp:333-336"""
+    return svt_run_backend(A, cfg, stop, Backend.r4svd(), observer, test)
+
+
+def svt_run_oracle(A, cfg, stop, observer=None, test=None):
+    """solver.hpp:340-343 (dense SVD of the densified iterate)"""
+    return svt_run_backend(A, cfg, stop, Backend.full_svd(), observer, test)
+
+
+class Solver:
+    """Step-wise svt_run_backend (one Bregman iteration per step) — the
+    handle bench.py times on the device."""
+
+    def __init__(self, A: SampledMatrix, cfg: SvtConfig, stop: StopRule, backend: Backend = None,
+                 test: SampledMatrix | None = None):
+        self.A, self.test = A, test
+        h = C.c_void_p()
+        _check(lib().svt_solver_create(A.h, C.byref(cfg), stop, backend or Backend.r4svd(),
+                                       test.h if test is not None else None, C.byref(h)))
+        self.h = h
+        self.done = False
+
+    def step(self, observer=None):
+        rec = IterationRecord()
+        done = C.c_int()
+        cb = _wrap_observer(observer)
+        _check(lib().svt_solver_step(self.h, cb, None, C.byref(rec), C.byref(done)))
+        self.done = bool(done.value)
+        return rec.as_dict()
+
+    def result(self) -> SvtResult:
+        h = C.c_void_p()
+        _check(lib().svt_solver_result(self.h, C.byref(h)))
+        return _take_result(h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().svt_solver_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# synthetic BASELINE configs (host generators in the extension)
+def synth_config(config: int, seed: int = 1):
+    """Returns dict(m, n, train=(rows, cols, vals), test=(rows, cols, vals) or
+    None) for configs 1-4, dict(m, n, csr=(rowptr, col, val)) for config 5."""
+    L = lib()
+    m, n = C.c_int64(), C.c_int64()
+    if config == 5:
+        nnz = C.c_int64()
+        _check(L.svt_synth_config_csr(C.c_int(5), C.c_uint64(seed), C.byref(m), C.byref(n), C.byref(nnz),
+                                      None, None, None))
+        rp = np.zeros(m.value + 1, dtype=np.int64)
+        co = np.zeros(nnz.value, dtype=np.int64)
+        va = np.zeros(nnz.value)
+        _check(L.svt_synth_config_csr(C.c_int(5), C.c_uint64(seed), C.byref(m), C.byref(n), C.byref(nnz),
+                                      _ptr(rp, P_I64), _ptr(co, P_I64), _ptr(va)))
+        return dict(m=m.value, n=n.value, csr=(rp, co, va))
+    ntr, nte = C.c_int64(), C.c_int64()
+    _check(L.svt_synth_config(C.c_int(config), C.c_uint64(seed), C.byref(m), C.byref(n), C.byref(ntr),
+                              C.byref(nte), None, None, None, None, None, None))
+    tr = [np.zeros(ntr.value, np.int64), np.zeros(ntr.value, np.int64), np.zeros(ntr.value)]
+    te = [np.zeros(max(nte.value, 1), np.int64), np.zeros(max(nte.value, 1), np.int64),
+          np.zeros(max(nte.value, 1))]
+    _check(L.svt_synth_config(C.c_int(config), C.c_uint64(seed), C.byref(m), C.byref(n), C.byref(ntr),
+                              C.byref(nte), _ptr(tr[0], P_I64), _ptr(tr[1], P_I64), _ptr(tr[2]),
+                              _ptr(te[0], P_I64), _ptr(te[1], P_I64), _ptr(te[2])))
+    test = tuple(a[: nte.value] for a in te) if nte.value else None
+    return dict(m=m.value, n=n.value, train=tuple(tr), test=test)
+
+
+def config_params(config: int, A_nnz: int, m: int, n: int, frob_a: float):
+    """The BASELINE.json parameters of each config:
+    returns (SvtConfig, StopRule).  Unspecified values use the reference's
+    default_config formulas (solver.hpp:95-106)."""
+    min_dim = min(m, n)
+    cfg = SvtConfig()
+    cfg.t0 = max(1, int(0.05 * min_dim))
+    cfg.dt = 10
+    cfg.beta = 0.95
+    p = A_nnz / float(m * n)
+    if config == 1:
+        cfg.tau, cfg.delta = 5.0 * n, 1.2 / p
+        cfg.eps_threshold0, cfg.eps_threshold_min = 1e-2, 1e-6
+        cfg.rel_residual_stop = 1e-4
+    elif config == 2:
+        cfg.tau, cfg.delta = 5.0 * np.sqrt(m * n), 1.2 / p
+        cfg.rel_residual_stop = 1e-4
+    elif config in (3, 4):
+        cfg.tau, cfg.delta = frob_a, np.sqrt(m * n / A_nnz)
+    elif config == 5:
+        cfg.tau, cfg.delta = 5.0 * n, 1.2 / p
+        cfg.maxit = 30
+    else:
+        raise ValueError("config must be 1..5")
+    return cfg, StopRule.none()

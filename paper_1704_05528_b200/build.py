@@ -1,0 +1,68 @@
+"""In-tree build of libsvt_b200.so (hand-written sm_100a CUDA + C++ host
+engine behind include/svt_b200.h).  nvcc cross-compiles without a GPU."""
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OUT_DIR = os.path.join(HERE, "lib")
+OUT = os.path.join(OUT_DIR, "libsvt_b200.so")
+OBJ = os.path.join(HERE, "build")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+SOURCES = ["rng.cu", "sparse.cu", "dense.cu", "runtime.cpp", "host.cpp", "engine.cpp", "solver.cpp", "capi.cpp",
+           "synth.cpp"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+          "--expt-relaxed-constexpr", "-Xptxas", "-warn-spills"]
+
+
+def _needs(obj, src):
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    deps = [src] + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".hpp", ".cuh"))]
+    deps.append(os.path.join(HERE, "..", "include", "svt_b200.h"))
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _compile(src):
+    s = os.path.join(CSRC, src)
+    o = os.path.join(OBJ, src + ".o")
+    if not _needs(o, s):
+        return o, None
+    cmd = [NVCC, *ARCH, *COMMON, "-c", s, "-o", o]
+    if src.endswith(".cpp"):
+        cmd = [NVCC, *ARCH, *COMMON, "-x", "cu", "-c", s, "-o", o]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    return o, (r.returncode, " ".join(cmd), r.stdout + r.stderr)
+
+
+def build(verbose=False):
+    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(OUT_DIR, exist_ok=True)
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
+        results = list(ex.map(_compile, SOURCES))
+    relink = not os.path.exists(OUT)
+    for o, res in results:
+        if res is not None:
+            rc, cmd, log = res
+            if rc != 0:
+                raise RuntimeError(f"nvcc failed:\n{cmd}\n{log}")
+            if verbose and log.strip():
+                print(log)
+            relink = True
+        elif os.path.getmtime(o) > os.path.getmtime(OUT) if os.path.exists(OUT) else True:
+            relink = True
+    if relink:
+        objs = [o for o, _ in results]
+        cmd = [NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-ldl", "-lpthread"]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{r.stdout}{r.stderr}")
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

@@ -1,0 +1,662 @@
+// The C ABI (include/svt_b200.h).  Every entry point catches and maps the
+// engine's exceptions to the status codes that correspond to the reference's
+// exception types; messages are kept per thread for svt_last_error().
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "engine.hpp"
+#include "kernels.hpp"
+
+namespace svtb {
+void sampled_build(i64 m, i64 n, i64 nnz, const i64* rows, const i64* cols, const double* vals, i64* rowptr_out,
+                   i64* col_out, double* val_out);
+void partition_rows(i64 m, const i64* rowptr, int world, i64* bounds);
+svt_solver* solver_create(svt_mat* A, const svt_config& cfg, svt_stop stop, svt_backend backend, svt_mat* test);
+void solver_step(svt_solver* S, svt_observer_fn obs, void* user, svt_record* rec_out, int* done);
+svt_result* solver_result(svt_solver* S);
+void kickstart_dev(svt_ctx* c, svt_mat* A, double tau, double delta, u64 seed, double* out_csr, double* out_csc);
+void synth_config(int config, u64 seed, i64* m, i64* n, i64* nnz_train, i64* nnz_test, i64* train_rows,
+                  i64* train_cols, double* train_vals, i64* test_rows, i64* test_cols, double* test_vals);
+void synth_config_csr(int config, u64 seed, i64* m, i64* n, i64* nnz, i64* rowptr, i64* col, double* val);
+}  // namespace svtb
+
+svt_mat* svtb_matrix_upload(svt_ctx* ctx, svtb::i64 m, svtb::i64 n, svtb::i64 row_begin, svtb::i64 row_end,
+                            const svtb::i64* rowptr, const svtb::i64* col, const double* val);
+
+using namespace svtb;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        f();
+        return SVT_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return SVT_EINVAL;
+    } catch (const std::domain_error& e) {
+        g_err = e.what();
+        return SVT_EDOMAIN;
+    } catch (const cuda_error& e) {
+        g_err = e.what();
+        return SVT_ECUDA;
+    } catch (const nccl_error& e) {
+        g_err = e.what();
+        return SVT_ENCCL;
+    } catch (const oom_error& e) {
+        g_err = e.what();
+        return SVT_EOOM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SVT_ERUNTIME;
+    } catch (...) {
+        g_err = "unknown error";
+        return SVT_ERUNTIME;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (p == nullptr) throw std::invalid_argument(std::string(what) + ": null argument");
+}
+
+// column-major host (rows x cols) -> row-major device (rows x cols, ld cols)
+DevBuf<double> upload_cm(svt_ctx* c, const double* h, i64 rows, i64 cols) {
+    DevBuf<double> d(static_cast<size_t>(std::max<i64>(1, rows * cols)));
+    if (rows * cols == 0) return d;
+    std::vector<double> rm(static_cast<size_t>(rows * cols));
+    for (i64 i = 0; i < rows; ++i)
+        for (i64 j = 0; j < cols; ++j) rm[static_cast<size_t>(i * cols + j)] = h[i + j * rows];
+    SVT_CUDA(cudaMemcpyAsync(d.get(), rm.data(), sizeof(double) * rm.size(), cudaMemcpyHostToDevice, c->stream));
+    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    return d;
+}
+
+void download_cm(svt_ctx* c, const double* d, i64 rows, i64 cols, i64 ld, double* h) {
+    if (rows * cols == 0) return;
+    std::vector<double> rm(static_cast<size_t>(rows * ld));
+    SVT_CUDA(cudaMemcpyAsync(rm.data(), d, sizeof(double) * rows * ld, cudaMemcpyDeviceToHost, c->stream));
+    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    for (i64 i = 0; i < rows; ++i)
+        for (i64 j = 0; j < cols; ++j) h[i + j * rows] = rm[static_cast<size_t>(i * ld + j)];
+}
+
+Engine engine_for(svt_mat* S) { return Engine(S->ctx, S, Vals{S->val.get(), S->val_csc.get()}); }
+
+}  // namespace
+
+extern "C" {
+
+const char* svt_last_error(void) { return g_err.c_str(); }
+
+int svt_version(void) { return 1; }
+
+int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, svt_ctx** out) {
+    return guard([&] {
+        need(out, "svt_ctx_create");
+        if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("svt_ctx_create: bad rank/world");
+        if (world > 1) need(nccl_id, "svt_ctx_create_dist: nccl_id");
+        int ndev = 0;
+        SVT_CUDA(cudaGetDeviceCount(&ndev));
+        if (device < 0 || device >= ndev) throw std::invalid_argument("svt_ctx_create: no such CUDA device");
+        SVT_CUDA(cudaSetDevice(device));
+        auto c = std::make_unique<svt_ctx>();
+        c->device = device;
+        SVT_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        SVT_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+        SVT_CUDA(cudaMallocHost(&c->h_scalars, 64 * sizeof(double)));
+        SVT_CUDA(cudaMallocHost(&c->h_flags, 64 * sizeof(int)));
+        SVT_CUDA(cudaMalloc(&c->d_scalars, 64 * sizeof(double)));
+        SVT_CUDA(cudaMalloc(&c->d_flags, 64 * sizeof(int)));
+        SVT_CUDA(cudaMemsetAsync(c->d_scalars, 0, 64 * sizeof(double), c->stream));
+        SVT_CUDA(cudaMemsetAsync(c->d_flags, 0, 64 * sizeof(int), c->stream));
+        nccl_init(c->comm, rank, world, nccl_id);
+        SVT_CUDA(cudaStreamSynchronize(c->stream));
+        *out = c.release();
+    });
+}
+
+int svt_ctx_create(int device, svt_ctx** out) { return svt_ctx_create_dist(device, 0, 1, nullptr, out); }
+
+int svt_nccl_get_unique_id(void* out128) {
+    return guard([&] {
+        need(out128, "svt_nccl_get_unique_id");
+        nccl_unique_id(out128);
+    });
+}
+
+int svt_ctx_destroy(svt_ctx* ctx) {
+    return guard([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        for (auto& p : ctx->pending) {
+            cudaEventDestroy(p.a);
+            cudaEventDestroy(p.b);
+        }
+        for (auto e : ctx->event_pool) cudaEventDestroy(e);
+        ctx->comm.destroy();
+        ctx->ws_partial.release();
+        ctx->ws_partial2.release();
+        ctx->ws_rng.release();
+        ctx->ws_mt.release();
+        ctx->ws_eig.release();
+        ctx->ws_info.release();
+        cudaFree(ctx->d_scalars);
+        cudaFree(ctx->d_flags);
+        cudaFreeHost(ctx->h_scalars);
+        cudaFreeHost(ctx->h_flags);
+        cudaStreamDestroy(ctx->stream);
+        delete ctx;
+    });
+}
+
+int svt_ctx_sync(svt_ctx* ctx) {
+    return guard([&] {
+        need(ctx, "svt_ctx_sync");
+        SVT_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+void* svt_ctx_stream(svt_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+int svt_ctx_rank(svt_ctx* ctx, int* rank, int* world) {
+    return guard([&] {
+        need(ctx, "svt_ctx_rank");
+        if (rank) *rank = ctx->comm.rank;
+        if (world) *world = ctx->comm.world;
+    });
+}
+
+int svt_ctx_set_profiling(svt_ctx* ctx, int on) {
+    return guard([&] {
+        need(ctx, "svt_ctx_set_profiling");
+        flush_stats(ctx);
+        ctx->profiling = on != 0;
+    });
+}
+
+int svt_ctx_reset_stats(svt_ctx* ctx) {
+    return guard([&] {
+        need(ctx, "svt_ctx_reset_stats");
+        flush_stats(ctx);
+        for (auto& s : ctx->stats) s = KStats{};
+        ctx->launch_count = 0;
+    });
+}
+
+int svt_ctx_kernel_stats(svt_ctx* ctx, int cls, int64_t* launches, double* total_ms, double* bytes, double* flops) {
+    return guard([&] {
+        need(ctx, "svt_ctx_kernel_stats");
+        if (cls < 0 || cls >= K_NCLASS) throw std::invalid_argument("svt_ctx_kernel_stats: bad class");
+        flush_stats(ctx);
+        const KStats& s = ctx->stats[cls];
+        if (launches) *launches = s.launches;
+        if (total_ms) *total_ms = s.total_ms;
+        if (bytes) *bytes = s.bytes;
+        if (flops) *flops = s.flops;
+    });
+}
+
+int64_t svt_ctx_launch_count(svt_ctx* ctx) { return ctx ? ctx->launch_count : -1; }
+
+int svt_sampled_build(int64_t m, int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols, const double* vals,
+                      int64_t* rowptr_out, int64_t* col_out, double* val_out) {
+    return guard([&] {
+        if (nnz > 0) {
+            need(rows, "svt_sampled_build");
+            need(cols, "svt_sampled_build");
+            need(vals, "svt_sampled_build");
+        }
+        need(rowptr_out, "svt_sampled_build");
+        sampled_build(m, n, nnz, rows, cols, vals, rowptr_out, col_out, val_out);
+    });
+}
+
+int svt_partition_rows(int64_t m, const int64_t* rowptr, int world, int64_t* bounds) {
+    return guard([&] {
+        need(rowptr, "svt_partition_rows");
+        need(bounds, "svt_partition_rows");
+        partition_rows(m, rowptr, world, bounds);
+    });
+}
+
+int svt_matrix_upload(svt_ctx* ctx, int64_t m, int64_t n, int64_t row_begin, int64_t row_end, const int64_t* rowptr,
+                      const int64_t* col, const double* val, svt_mat** out) {
+    return guard([&] {
+        need(ctx, "svt_matrix_upload");
+        need(rowptr, "svt_matrix_upload");
+        need(out, "svt_matrix_upload");
+        SVT_CUDA(cudaSetDevice(ctx->device));
+        *out = svtb_matrix_upload(ctx, m, n, row_begin, row_end, rowptr, col, val);
+    });
+}
+
+int svt_matrix_free(svt_mat* mat) {
+    return guard([&] { delete mat; });
+}
+
+int svt_matrix_info(svt_mat* M, int64_t* m, int64_t* n, int64_t* nnz_local, int64_t* row_begin, int64_t* row_end) {
+    return guard([&] {
+        need(M, "svt_matrix_info");
+        if (m) *m = M->m;
+        if (n) *n = M->n;
+        if (nnz_local) *nnz_local = M->nnz_local;
+        if (row_begin) *row_begin = M->row_begin;
+        if (row_end) *row_end = M->row_end;
+    });
+}
+
+int svt_matrix_set_values(svt_mat* M, const double* vals) {
+    return guard([&] {
+        need(M, "svt_matrix_set_values");
+        if (M->nnz_local == 0) return;
+        need(vals, "svt_matrix_set_values");
+        for (i64 k = 0; k < M->nnz_local; ++k)
+            if (!std::isfinite(vals[k])) throw std::invalid_argument("with_values: non-finite value");
+        svt_ctx* c = M->ctx;
+        SVT_CUDA(cudaMemcpyAsync(M->val.get(), vals, sizeof(double) * M->nnz_local, cudaMemcpyHostToDevice, c->stream));
+        scale_values(c, M->nnz_local, M->val.get(), 1.0, M->val.get(), M->csr2csc.get(), M->val_csc.get());
+        SVT_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int svt_matrix_get_values(svt_mat* M, double* vals) {
+    return guard([&] {
+        need(M, "svt_matrix_get_values");
+        if (M->nnz_local == 0) return;
+        need(vals, "svt_matrix_get_values");
+        svt_ctx* c = M->ctx;
+        SVT_CUDA(cudaMemcpyAsync(vals, M->val.get(), sizeof(double) * M->nnz_local, cudaMemcpyDeviceToHost, c->stream));
+        SVT_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+// ---- primitives ----------------------------------------------------------
+int svt_gaussian_block(svt_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out) {
+    return guard([&] {
+        need(ctx, "svt_gaussian_block");
+        if (rows < 1 || cols < 1) throw std::invalid_argument("gaussian_block: dimensions must be >= 1");
+        need(out, "svt_gaussian_block");
+        DevBuf<double> d(static_cast<size_t>(rows * cols));
+        gaussian_block_dev(ctx, rows, cols, seed, d.get(), cols);
+        download_cm(ctx, d.get(), rows, cols, cols, out);
+    });
+}
+
+int svt_qr_orthonormal(svt_ctx* ctx, int64_t rows, int64_t cols, const double* X, double* Q) {
+    return guard([&] {
+        need(ctx, "svt_qr_orthonormal");
+        if (cols > rows)
+            throw std::invalid_argument("qr_orthonormal: need cols <= rows, got " + std::to_string(rows) + "x" +
+                                        std::to_string(cols));
+        if (rows * cols == 0) return;
+        // a row-block-free helper matrix: Engine needs m_local for the panel height
+        svt_mat fake;
+        fake.ctx = ctx;
+        fake.m = rows;
+        fake.m_local = rows;
+        fake.n = rows;
+        fake.row_end = rows;
+        Engine E(ctx, &fake, Vals{nullptr, nullptr});
+        if (ctx->comm.world != 1) throw std::invalid_argument("svt_qr_orthonormal: single-rank helper");
+        DevBuf<double> dX = upload_cm(ctx, X, rows, cols);
+        DevBuf<double> dQ(static_cast<size_t>(rows * cols));
+        qr_orthonormal(E, dX.get(), cols, cols, dQ.get(), cols);
+        download_cm(ctx, dQ.get(), rows, cols, cols, Q);
+    });
+}
+
+int svt_small_svd(svt_ctx* ctx, int64_t rows, int64_t cols, const double* B, double* U, double* sigma, double* V) {
+    return guard([&] {
+        need(ctx, "svt_small_svd");
+        if (rows < 1 || cols < 1) throw std::invalid_argument("small_svd: empty block");
+        // finalize with Q = I: B = I * B, Gram of the shorter side
+        const bool tr = rows > cols;
+        const i64 r = tr ? cols : rows, n = tr ? rows : cols;
+        svt_mat fake;
+        fake.ctx = ctx;
+        fake.m = r;
+        fake.m_local = r;
+        fake.n = n;
+        fake.row_end = r;
+        Engine E(ctx, &fake, Vals{nullptr, nullptr});
+        QBDev st;
+        st.m_local = r;
+        st.n = n;
+        st.min_dim = r;
+        st.cap = r;
+        st.rank = r;
+        std::vector<double> eye(static_cast<size_t>(r * r), 0.0);
+        for (i64 i = 0; i < r; ++i) eye[static_cast<size_t>(i * r + i)] = 1.0;
+        st.Q.alloc(static_cast<size_t>(r * r));
+        SVT_CUDA(cudaMemcpyAsync(st.Q.get(), eye.data(), sizeof(double) * r * r, cudaMemcpyHostToDevice, ctx->stream));
+        // B^T (n x r) row-major == B (r x n) column-major; for tr, B^T == B^T
+        std::vector<double> bt(static_cast<size_t>(n * r));
+        for (i64 i = 0; i < r; ++i)
+            for (i64 j = 0; j < n; ++j) {
+                const double v = tr ? B[j + i * rows] : B[i + j * rows];  // (i, j) of the short-side matrix
+                bt[static_cast<size_t>(j * r + i)] = v;
+            }
+        st.Bt.alloc(static_cast<size_t>(n * r));
+        SVT_CUDA(cudaMemcpyAsync(st.Bt.get(), bt.data(), sizeof(double) * n * r, cudaMemcpyHostToDevice, ctx->stream));
+        DevFactors f;
+        finalize(E, st, FinalizeMode::Full, 0.0, f);
+        const i64 k = f.k;
+        std::vector<double> Ur, Vr;
+        std::vector<double> hU(static_cast<size_t>(r * k)), hV(static_cast<size_t>(n * k));
+        download_cm(ctx, f.U.get(), r, k, k, hU.data());
+        download_cm(ctx, f.V.get(), n, k, k, hV.data());
+        if (!tr) {
+            std::memcpy(U, hU.data(), sizeof(double) * r * k);
+            std::memcpy(V, hV.data(), sizeof(double) * n * k);
+        } else {
+            std::memcpy(U, hV.data(), sizeof(double) * n * k);
+            std::memcpy(V, hU.data(), sizeof(double) * r * k);
+        }
+        std::memcpy(sigma, f.sigma.data(), sizeof(double) * k);
+    });
+}
+
+int svt_sp_mult(svt_mat* S, int64_t w, const double* X, double* out) {
+    return guard([&] {
+        need(S, "svt_sp_mult");
+        if (w < 0) throw std::invalid_argument("sp_mult: bad width");
+        if (w == 0) return;
+        svt_ctx* c = S->ctx;
+        Engine E = engine_for(S);
+        DevBuf<double> dX = upload_cm(c, X, S->n, w);
+        DevBuf<double> dO(static_cast<size_t>(std::max<i64>(1, S->m_local * w)));
+        sp_mult(E, w, dX.get(), w, dO.get(), w);
+        download_cm(c, dO.get(), S->m_local, w, w, out);
+    });
+}
+
+int svt_sp_mult_t(svt_mat* S, int64_t w, const double* X, double* out) {
+    return guard([&] {
+        need(S, "svt_sp_mult_t");
+        if (w < 0) throw std::invalid_argument("sp_mult_t: bad width");
+        if (w == 0) return;
+        svt_ctx* c = S->ctx;
+        Engine E = engine_for(S);
+        DevBuf<double> dX = upload_cm(c, X, S->m_local, w);
+        DevBuf<double> dO(static_cast<size_t>(S->n * w));
+        sp_mult_t(E, w, dX.get(), w, dO.get());
+        download_cm(c, dO.get(), S->n, w, w, out);
+    });
+}
+
+int svt_project_low_rank(svt_mat* P, int64_t k, const double* U, const double* sigma, const double* V,
+                         double* out_vals) {
+    return guard([&] {
+        need(P, "svt_project_low_rank");
+        if (k < 0) throw std::invalid_argument("project_low_rank: bad rank");
+        svt_ctx* c = P->ctx;
+        DevBuf<double> dU = upload_cm(c, U, P->m_local, k);
+        std::vector<double> vs(static_cast<size_t>(P->n * k));
+        for (i64 j = 0; j < k; ++j)
+            for (i64 i = 0; i < P->n; ++i) vs[static_cast<size_t>(i + j * P->n)] = V[i + j * P->n] * sigma[j];
+        DevBuf<double> dV = upload_cm(c, vs.data(), P->n, k);
+        DevBuf<double> out(static_cast<size_t>(std::max<i64>(1, P->nnz_local)));
+        sddmm_update(c, P->m_local, P->rowptr.get(), P->col.get(), P->val.get(), out.get(), nullptr, nullptr,
+                     P->nnz_local, P->n, dU.get(), k, dV.get(), k, k, 0.0, 2, c->d_scalars + 40);
+        SVT_CUDA(cudaMemcpyAsync(out_vals, out.get(), sizeof(double) * P->nnz_local, cudaMemcpyDeviceToHost, c->stream));
+        SVT_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int svt_sp_axpy(svt_mat* Y, double alpha, const double* d_vals, double* out_vals) {
+    return guard([&] {
+        need(Y, "svt_sp_axpy");
+        svt_ctx* c = Y->ctx;
+        const i64 nnz = Y->nnz_local;
+        if (nnz == 0) return;
+        DevBuf<double> d(static_cast<size_t>(nnz)), o(static_cast<size_t>(nnz));
+        SVT_CUDA(cudaMemcpyAsync(d.get(), d_vals, sizeof(double) * nnz, cudaMemcpyHostToDevice, c->stream));
+        axpy_values(c, nnz, Y->val.get(), alpha, d.get(), o.get());
+        SVT_CUDA(cudaMemcpyAsync(out_vals, o.get(), sizeof(double) * nnz, cudaMemcpyDeviceToHost, c->stream));
+        SVT_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int svt_sp_frob_norm_sq(svt_mat* S, double* out) {
+    return guard([&] {
+        need(S, "svt_sp_frob_norm_sq");
+        need(out, "svt_sp_frob_norm_sq");
+        Engine E = engine_for(S);
+        *out = frob_sq(E);
+    });
+}
+
+int svt_spectral_norm_est(svt_mat* S, int iters, uint64_t seed, double* out) {
+    return guard([&] {
+        need(S, "svt_spectral_norm_est");
+        need(out, "svt_spectral_norm_est");
+        Engine E = engine_for(S);
+        *out = spectral_norm_est(E, iters, seed);
+    });
+}
+
+int svt_kickstart(svt_mat* A, double tau, double delta, uint64_t seed, double* out_vals) {
+    return guard([&] {
+        need(A, "svt_kickstart");
+        svt_ctx* c = A->ctx;
+        const i64 nnz = std::max<i64>(1, A->nnz_local);
+        DevBuf<double> y(static_cast<size_t>(nnz)), yc(static_cast<size_t>(nnz));
+        kickstart_dev(c, A, tau, delta, seed, y.get(), yc.get());
+        if (A->nnz_local > 0)
+            SVT_CUDA(cudaMemcpyAsync(out_vals, y.get(), sizeof(double) * A->nnz_local, cudaMemcpyDeviceToHost,
+                                     c->stream));
+        SVT_CUDA(cudaStreamSynchronize(c->stream));
+    });
+}
+
+// ---- engines ---------------------------------------------------------------
+static int wrap_factors(svt_factors** out, DevFactors&& f, i64 rank, bool sat, int rounds) {
+    auto h = std::make_unique<svt_factors>();
+    h->f = std::move(f);
+    h->rank = rank;
+    h->saturated = sat ? 1 : 0;
+    h->rounds = rounds;
+    *out = h.release();
+    return 0;
+}
+
+int svt_rsvd(svt_mat* Y, int64_t k, const svt_sketch_params* p, svt_factors** out) {
+    return guard([&] {
+        need(Y, "svt_rsvd");
+        need(p, "svt_rsvd");
+        need(out, "svt_rsvd");
+        Engine E = engine_for(Y);
+        DevFactors f = rsvd(E, k, *p);
+        wrap_factors(out, std::move(f), k, false, 0);
+    });
+}
+
+int svt_r3svd(svt_mat* Y, const svt_sketch_params* p, svt_factors** out) {
+    return guard([&] {
+        need(Y, "svt_r3svd");
+        need(p, "svt_r3svd");
+        need(out, "svt_r3svd");
+        Engine E = engine_for(Y);
+        SketchOut so = r3svd(E, *p, FinalizeMode::Full, 0.0);
+        wrap_factors(out, std::move(so.f), so.rank, so.saturated, so.rounds);
+    });
+}
+
+int svt_r4svd(svt_mat* Y, int64_t s, const double* U_prev, int64_t ldu, const svt_sketch_params* p,
+              svt_factors** out) {
+    return guard([&] {
+        need(Y, "svt_r4svd");
+        need(p, "svt_r4svd");
+        need(out, "svt_r4svd");
+        if (s < 0) throw std::invalid_argument("r4svd: negative basis width");
+        if (s > 0) {
+            need(U_prev, "svt_r4svd");
+            if (ldu < Y->m_local) throw std::invalid_argument("r4svd: U_prev row count does not match Y");
+        }
+        svt_ctx* c = Y->ctx;
+        Engine E = engine_for(Y);
+        // column-major host (ldu) -> row-major device
+        DevBuf<double> dU(static_cast<size_t>(std::max<i64>(1, Y->m_local * s)));
+        if (s > 0) {
+            std::vector<double> rm(static_cast<size_t>(Y->m_local * s));
+            for (i64 i = 0; i < Y->m_local; ++i)
+                for (i64 j = 0; j < s; ++j) rm[static_cast<size_t>(i * s + j)] = U_prev[i + j * ldu];
+            SVT_CUDA(cudaMemcpyAsync(dU.get(), rm.data(), sizeof(double) * rm.size(), cudaMemcpyHostToDevice,
+                                     c->stream));
+            SVT_CUDA(cudaStreamSynchronize(c->stream));
+        }
+        SketchOut so = r4svd(E, dU.get(), s, s, *p, FinalizeMode::Full, 0.0);
+        wrap_factors(out, std::move(so.f), so.rank, so.saturated, so.rounds);
+    });
+}
+
+int svt_factors_info(svt_factors* f, int64_t* m_local, int64_t* n, int64_t* rank, int* saturated, int* rounds) {
+    return guard([&] {
+        need(f, "svt_factors_info");
+        if (m_local) *m_local = f->f.m_local;
+        if (n) *n = f->f.n;
+        if (rank) *rank = f->f.k;
+        if (saturated) *saturated = f->saturated;
+        if (rounds) *rounds = f->rounds;
+    });
+}
+
+int svt_factors_copy(svt_factors* f, double* U, double* sigma, double* V) {
+    return guard([&] {
+        need(f, "svt_factors_copy");
+        svt_ctx* c = nullptr;
+        (void)c;
+        const i64 k = f->f.k;
+        if (k == 0) return;
+        // the factors' context is the one that produced them; copy via the default stream
+        std::vector<double> hu(static_cast<size_t>(f->f.m_local * k)), hv(static_cast<size_t>(f->f.n * k));
+        SVT_CUDA(cudaMemcpy(hu.data(), f->f.U.get(), sizeof(double) * hu.size(), cudaMemcpyDeviceToHost));
+        SVT_CUDA(cudaMemcpy(hv.data(), f->f.V.get(), sizeof(double) * hv.size(), cudaMemcpyDeviceToHost));
+        for (i64 i = 0; i < f->f.m_local; ++i)
+            for (i64 j = 0; j < k; ++j) U[i + j * f->f.m_local] = hu[static_cast<size_t>(i * k + j)];
+        for (i64 i = 0; i < f->f.n; ++i)
+            for (i64 j = 0; j < k; ++j) V[i + j * f->f.n] = hv[static_cast<size_t>(i * k + j)];
+        std::memcpy(sigma, f->f.sigma.data(), sizeof(double) * k);
+    });
+}
+
+int svt_factors_free(svt_factors* f) {
+    return guard([&] { delete f; });
+}
+
+// ---- solver ----------------------------------------------------------------
+int svt_default_config(svt_mat* A, svt_config* out) {  // solver.hpp:95-106
+    return guard([&] {
+        need(A, "svt_default_config");
+        need(out, "svt_default_config");
+        Engine E = engine_for(A);
+        svt_config c{};
+        c.maxit = 500;
+        c.np = 1;
+        c.eps_stop = 1e-3;
+        c.eps_threshold0 = 0.5;
+        c.seed = 1;
+        c.tau = std::sqrt(frob_sq(E));
+        c.delta = std::sqrt(static_cast<double>(A->m) * static_cast<double>(A->n) / static_cast<double>(A->nnz_global));
+        const i64 min_dim = std::min(A->m, A->n);
+        c.t0 = std::max<i64>(1, static_cast<i64>(0.05 * static_cast<double>(min_dim)));
+        c.dt = 10;
+        c.beta = 0.95;
+        *out = c;
+    });
+}
+
+int svt_solver_create(svt_mat* A, const svt_config* cfg, svt_stop stop, svt_backend backend, svt_mat* test,
+                      svt_solver** out) {
+    return guard([&] {
+        need(A, "svt_solver_create");
+        need(cfg, "svt_solver_create");
+        need(out, "svt_solver_create");
+        *out = solver_create(A, *cfg, stop, backend, test);
+    });
+}
+
+int svt_solver_step(svt_solver* s, svt_observer_fn obs, void* user, svt_record* rec, int* done) {
+    return guard([&] {
+        need(s, "svt_solver_step");
+        solver_step(s, obs, user, rec, done);
+    });
+}
+
+int svt_solver_result(svt_solver* s, svt_result** out) {
+    return guard([&] {
+        need(s, "svt_solver_result");
+        need(out, "svt_solver_result");
+        *out = solver_result(s);
+    });
+}
+
+int svt_solver_free(svt_solver* s) {
+    return guard([&] { delete s; });
+}
+
+int svt_run(svt_mat* A, const svt_config* cfg, svt_stop stop, svt_backend backend, svt_mat* test,
+            svt_observer_fn obs, void* user, svt_result** out) {
+    return guard([&] {
+        need(A, "svt_run");
+        need(cfg, "svt_run");
+        need(out, "svt_run");
+        std::unique_ptr<svt_solver> s(solver_create(A, *cfg, stop, backend, test));
+        int done = 0;
+        while (!done) solver_step(s.get(), obs, user, nullptr, &done);
+        *out = solver_result(s.get());
+    });
+}
+
+int svt_result_info(svt_result* r, int64_t* n_records, int64_t* m_local, int64_t* n, int64_t* k, int* converged) {
+    return guard([&] {
+        need(r, "svt_result_info");
+        if (n_records) *n_records = static_cast<int64_t>(r->trace.size());
+        if (m_local) *m_local = r->m_local;
+        if (n) *n = r->n;
+        if (k) *k = r->k;
+        if (converged) *converged = r->converged;
+    });
+}
+
+int svt_result_trace(svt_result* r, svt_record* out) {
+    return guard([&] {
+        need(r, "svt_result_trace");
+        if (!r->trace.empty()) std::memcpy(out, r->trace.data(), sizeof(svt_record) * r->trace.size());
+    });
+}
+
+int svt_result_factors(svt_result* r, double* U, double* sigma, double* V) {
+    return guard([&] {
+        need(r, "svt_result_factors");
+        if (r->k == 0) return;
+        std::memcpy(U, r->U.data(), sizeof(double) * r->U.size());
+        std::memcpy(sigma, r->sigma.data(), sizeof(double) * r->sigma.size());
+        std::memcpy(V, r->V.data(), sizeof(double) * r->V.size());
+    });
+}
+
+int svt_result_free(svt_result* r) {
+    return guard([&] { delete r; });
+}
+
+int svt_synth_config(int config, uint64_t seed, int64_t* m, int64_t* n, int64_t* nnz_train, int64_t* nnz_test,
+                     int64_t* train_rows, int64_t* train_cols, double* train_vals, int64_t* test_rows,
+                     int64_t* test_cols, double* test_vals) {
+    return guard([&] {
+        synth_config(config, seed, m, n, nnz_train, nnz_test, train_rows, train_cols, train_vals, test_rows,
+                     test_cols, test_vals);
+    });
+}
+
+int svt_synth_config_csr(int config, uint64_t seed, int64_t* m, int64_t* n, int64_t* nnz, int64_t* rowptr,
+                         int64_t* col, double* val) {
+    return guard([&] { synth_config_csr(config, seed, m, n, nnz, rowptr, col, val); });
+}
+
+}  // extern "C"

@@ -1,0 +1,156 @@
+// Shared host-side plumbing of libsvt_b200: error handling, device buffers,
+// the per-context stream / communicator / instrumentation state.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace svtb {
+
+using i64 = std::int64_t;
+using u64 = std::uint64_t;
+
+// Error types map one-to-one to the reference's exceptions (sketch.hpp /
+// sampled.hpp / solver.hpp throw std::invalid_argument, std::domain_error,
+// std::runtime_error) plus device-side failures.
+struct cuda_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct nccl_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct oom_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define SVT_CUDA(call)                                                                               \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess) {                                                                     \
+            if (e_ == cudaErrorMemoryAllocation)                                                     \
+                throw ::svtb::oom_error(std::string("CUDA OOM at " __FILE__ ":") +                  \
+                                        std::to_string(__LINE__));                                   \
+            throw ::svtb::cuda_error(std::string(cudaGetErrorString(e_)) + " at " __FILE__ ":" +    \
+                                     std::to_string(__LINE__));                                      \
+        }                                                                                            \
+    } while (0)
+
+#define SVT_CHECK_LAUNCH() SVT_CUDA(cudaGetLastError())
+
+// RAII device allocation.
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+        o.p = nullptr;
+        o.n = 0;
+    }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count == 0) return;
+        SVT_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    // grow-only; contents are not preserved
+    void ensure(size_t count) {
+        if (count > n) alloc(count);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    T* get() const { return p; }
+};
+
+// Kernel classes for instrumentation (svt_ctx_kernel_stats).
+enum KClass : int { K_SPMM = 0, K_SPMMT = 1, K_SDDMM = 2, K_GEMM = 3, K_RNG = 4, K_QR = 5, K_FINAL = 6, K_OTHER = 7, K_NCLASS = 8 };
+
+struct KStats {
+    i64 launches = 0;
+    double total_ms = 0.0;
+    double bytes = 0.0;
+    double flops = 0.0;
+};
+
+// NCCL entry points, resolved with dlopen so a single-GPU run never needs
+// libnccl (comm.cpp).
+struct Comm {
+    int rank = 0;
+    int world = 1;
+    void* handle = nullptr;  // ncclComm_t
+    void allreduce_sum(double* buf, size_t count, cudaStream_t s);
+    void allreduce_sum_i32(int* buf, size_t count, cudaStream_t s);
+    void destroy();
+};
+void nccl_unique_id(void* out128);
+void nccl_init(Comm& c, int rank, int world, const void* id128);
+
+}  // namespace svtb
+
+// The opaque context behind svt_ctx*.
+struct svt_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    svtb::Comm comm;
+    void* cusolver = nullptr;  // cusolverDnHandle_t
+    // instrumentation
+    bool profiling = false;
+    svtb::i64 launch_count = 0;
+    svtb::KStats stats[svtb::K_NCLASS];
+    struct Pending {
+        cudaEvent_t a, b;
+        int cls;
+    };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> event_pool;
+    // device scratch scalars (pinned host mirror for one-shot reads)
+    double* h_scalars = nullptr;  // pinned, 64 doubles
+    double* d_scalars = nullptr;  // device, 64 doubles
+    int* d_flags = nullptr;       // device, 64 ints
+    int* h_flags = nullptr;       // pinned, 64 ints
+    svtb::DevBuf<double> ws_partial;   // split-K / reduction partials
+    svtb::DevBuf<double> ws_partial2;  // second partial buffer (reductions)
+    svtb::DevBuf<unsigned long long> ws_rng;  // raw mt19937_64 draws
+    svtb::DevBuf<unsigned long long> ws_mt;   // persistent mt state (312 words + index)
+    svtb::DevBuf<double> ws_eig;              // Jacobi eigensolver workspace
+    svtb::DevBuf<int> ws_info;
+};
+
+namespace svtb {
+
+// Launch bookkeeping: counts every kernel of ours and, when profiling, brackets
+// it with CUDA events on the context stream.
+struct LaunchScope {
+    svt_ctx* ctx;
+    int cls;
+    cudaEvent_t a = nullptr, b = nullptr;
+    LaunchScope(svt_ctx* c, int k, double bytes, double flops);
+    ~LaunchScope() noexcept(false);
+};
+void flush_stats(svt_ctx* ctx);  // resolve pending event pairs (syncs)
+
+}  // namespace svtb

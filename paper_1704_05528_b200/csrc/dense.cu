@@ -1,0 +1,826 @@
+// Dense kernels: tall-skinny FP64 GEMMs for block Gram-Schmidt (sketch.hpp:
+// 133-141), CholQR2 with a Householder fallback (dense.hpp:103-110), the Gram
+// eigensolver of finalize (sketch.hpp:158-162 / dense.hpp:114-117), and small
+// reductions that drive the reference's data-dependent branches on the device
+// (no host round trip inside a rank-revealing round).
+//
+// FP64 note: tcgen05 has no f64 kind on sm_100a, so FP64 contractions run on
+// the FP64 pipes.  The dt = 10 passes are HBM-bound (2.5 flop/B on Q), so the
+// GEMM is a register-tiled CUDA-core kernel whose job is to stream Q at HBM
+// rate; split-K with a fixed-order reduction keeps results deterministic.
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.hpp"
+
+namespace svtb {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// GEMM
+// ---------------------------------------------------------------------------
+template <int BM, int BN, int BK, int TM, int TN, bool TA>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN)) gemm_kernel(
+    long long M, long long N, long long K, double alpha, const double* __restrict__ A, long long lda,
+    const double* __restrict__ B, long long ldb, double beta, double* __restrict__ C, long long ldc,
+    long long kchunk, double* __restrict__ partial, const int* __restrict__ pred) {
+    if (pred != nullptr && *pred == 0) return;
+    constexpr int NT = (BM / TM) * (BN / TN);
+    constexpr int TX = BN / TN;
+    constexpr int TY = BM / TM;
+    __shared__ double As[BK][BM + 1];
+    __shared__ double Bs[BK][BN];
+    const int tid = threadIdx.x;
+    const int tx = tid % TX;
+    const int ty = tid / TX;
+    const long long i0 = static_cast<long long>(blockIdx.x) * BM;
+    const long long j0 = static_cast<long long>(blockIdx.y) * BN;
+    const long long kbeg = static_cast<long long>(blockIdx.z) * kchunk;
+    const long long kend = min(K, kbeg + kchunk);
+    double acc[TM][TN];
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TN; ++b) acc[a][b] = 0.0;
+
+    for (long long k0 = kbeg; k0 < kend; k0 += BK) {
+        if (TA) {
+            for (int e = tid; e < BK * BM; e += NT) {
+                const int kk = e / BM, ii = e % BM;
+                const long long k = k0 + kk, i = i0 + ii;
+                As[kk][ii] = (k < kend && i < M) ? __ldg(A + k * lda + i) : 0.0;
+            }
+        } else {
+            for (int e = tid; e < BK * BM; e += NT) {
+                const int ii = e / BK, kk = e % BK;
+                const long long k = k0 + kk, i = i0 + ii;
+                As[kk][ii] = (k < kend && i < M) ? __ldg(A + i * lda + k) : 0.0;
+            }
+        }
+        for (int e = tid; e < BK * BN; e += NT) {
+            const int kk = e / BN, jj = e % BN;
+            const long long k = k0 + kk, j = j0 + jj;
+            Bs[kk][jj] = (k < kend && j < N) ? __ldg(B + k * ldb + j) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            double a[TM], b[TN];
+#pragma unroll
+            for (int t = 0; t < TM; ++t) a[t] = As[kk][ty + t * TY];
+#pragma unroll
+            for (int t = 0; t < TN; ++t) b[t] = Bs[kk][tx + t * TX];
+#pragma unroll
+            for (int p = 0; p < TM; ++p)
+#pragma unroll
+                for (int q = 0; q < TN; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int p = 0; p < TM; ++p) {
+        const long long i = i0 + ty + p * TY;
+        if (i >= M) continue;
+#pragma unroll
+        for (int q = 0; q < TN; ++q) {
+            const long long j = j0 + tx + q * TX;
+            if (j >= N) continue;
+            if (gridDim.z == 1) {
+                const double c = (beta != 0.0) ? beta * C[i * ldc + j] : 0.0;
+                C[i * ldc + j] = fma(alpha, acc[p][q], c);
+            } else {
+                partial[(static_cast<long long>(blockIdx.z) * M + i) * N + j] = acc[p][q];
+            }
+        }
+    }
+}
+
+__global__ void gemm_reduce_kernel(long long M, long long N, int splits, const double* __restrict__ partial,
+                                   double alpha, double beta, double* __restrict__ C, long long ldc,
+                                   const int* __restrict__ pred) {
+    if (pred != nullptr && *pred == 0) return;
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= M * N) return;
+    const long long i = e / N, j = e % N;
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += partial[static_cast<long long>(z) * M * N + e];
+    const double c = (beta != 0.0) ? beta * C[i * ldc + j] : 0.0;
+    C[i * ldc + j] = fma(alpha, s, c);
+}
+
+__global__ void scale2d_kernel(double* C, long long M, long long N, long long ldc, double beta, const int* pred) {
+    if (pred != nullptr && *pred == 0) return;
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= M * N) return;
+    const long long i = e / N, j = e % N;
+    C[i * ldc + j] = (beta != 0.0) ? beta * C[i * ldc + j] : 0.0;
+}
+
+template <int BM, int BN, int BK, int TM, int TN>
+void gemm_launch(svt_ctx* ctx, bool transA, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+                 const double* B, i64 ldb, double beta, double* C, i64 ldc, const int* pred) {
+    const i64 mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;
+    const i64 tiles = mt * nt;
+    i64 splits = 1;
+    const i64 target = 2LL * ctx->num_sms;
+    if (tiles < target && K > 8 * BK) {
+        splits = std::min<i64>((target + tiles - 1) / tiles, (K + 8 * BK - 1) / (8 * BK));
+        splits = std::min<i64>(splits, 512);
+        // bound the partial workspace to 256 MB
+        while (splits > 1 && splits * M * N > (32LL << 20)) splits /= 2;
+    }
+    i64 kchunk = (K + splits - 1) / splits;
+    kchunk = ((kchunk + BK - 1) / BK) * BK;
+    splits = (K + kchunk - 1) / kchunk;
+    if (splits < 1) splits = 1;
+    if (splits > 1) ctx->ws_partial.ensure(static_cast<size_t>(splits * M * N));
+    dim3 grid(static_cast<unsigned>(mt), static_cast<unsigned>(nt), static_cast<unsigned>(splits));
+    constexpr int NT = (BM / TM) * (BN / TN);
+    if (transA)
+        gemm_kernel<BM, BN, BK, TM, TN, true><<<grid, NT, 0, ctx->stream>>>(
+            M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, ctx->ws_partial.get(), pred);
+    else
+        gemm_kernel<BM, BN, BK, TM, TN, false><<<grid, NT, 0, ctx->stream>>>(
+            M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, ctx->ws_partial.get(), pred);
+    if (splits > 1) {
+        const i64 tot = M * N;
+        gemm_reduce_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(
+            M, N, static_cast<int>(splits), ctx->ws_partial.get(), alpha, beta, C, ldc, pred);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// reductions
+// ---------------------------------------------------------------------------
+constexpr int kRedBlocks = 256;
+
+__global__ void sumsq_partial_kernel(const double* __restrict__ X, long long rows, long long cols, long long ld,
+                                     double* __restrict__ partial, const int* __restrict__ pred) {
+    if (pred != nullptr && *pred == 0) return;
+    __shared__ double red[32];
+    double s = 0.0;
+    const long long tot = rows * cols;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < tot;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = e / cols, j = e % cols;
+        const double v = X[i * ld + j];
+        s = fma(v, v, s);
+    }
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = (threadIdx.x < blockDim.x / 32) ? red[threadIdx.x] : 0.0;
+        t = warp_sum(t);
+        if (threadIdx.x == 0) partial[blockIdx.x] = t;
+    }
+}
+
+__global__ void maxabs_partial_kernel(const double* __restrict__ X, long long rows, long long cols, long long ld,
+                                      double shift, double* __restrict__ partial) {
+    __shared__ double red[32];
+    double s = 0.0;
+    const long long tot = rows * cols;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < tot;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = e / cols, j = e % cols;
+        double v = X[i * ld + j];
+        if (i == j) v -= shift;
+        s = fmax(s, fabs(v));
+        if (v != v) s = CUDART_INF;  // NaN forces the branch
+    }
+    s = warp_max(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = (threadIdx.x < blockDim.x / 32) ? red[threadIdx.x] : 0.0;
+        t = warp_max(t);
+        if (threadIdx.x == 0) partial[blockIdx.x] = t;
+    }
+}
+
+// op: 0 store sum, 1 add sum, 2 store max
+__global__ void finish_kernel(const double* __restrict__ partial, int n, double* __restrict__ out, int op,
+                              const int* __restrict__ pred) {
+    if (pred != nullptr && *pred == 0) return;
+    double t = 0.0;
+    for (int b = threadIdx.x; b < n; b += 32) t = (op == 2) ? fmax(t, partial[b]) : t + partial[b];
+    t = (op == 2) ? warp_max(t) : warp_sum(t);
+    if (threadIdx.x == 0) {
+        if (op == 1)
+            out[0] += t;
+        else
+            out[0] = t;
+    }
+}
+
+__global__ void set_flag_kernel(const double* a, const double* b, double coef, int mode, int* flag) {
+    if (mode == 0)
+        flag[0] = (sqrt(a[0]) > coef * sqrt(b[0])) ? 1 : 0;
+    else
+        flag[0] = (a[0] > coef) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// CholQR: Cholesky + explicit inverse of R = L^T, one CTA, w <= 64
+// ---------------------------------------------------------------------------
+constexpr int kCholMax = 64;
+
+__global__ void __launch_bounds__(256) chol_rinv_kernel(const double* __restrict__ G, int w,
+                                                        double* __restrict__ Rinv, int* __restrict__ status,
+                                                        const int* __restrict__ pred) {
+    if (pred != nullptr && *pred == 0) return;
+    __shared__ double L[kCholMax][kCholMax + 1];
+    __shared__ double dorig[kCholMax];
+    __shared__ int fail;
+    const int tid = threadIdx.x;
+    if (tid == 0) fail = 0;
+    for (int e = tid; e < w * w; e += blockDim.x) L[e / w][e % w] = G[e];
+    __syncthreads();
+    if (tid < w) dorig[tid] = L[tid][tid];
+    __syncthreads();
+    for (int j = 0; j < w; ++j) {
+        const double d = L[j][j];
+        // a pivot that lost more than ~13 digits (kappa(X) beyond ~3e6 in
+        // that direction) or a zero / non-finite column routes the panel to
+        // the Householder fallback, which keeps all columns like
+        // qr_orthonormal (dense.hpp:100-102)
+        const bool bad = !(dorig[j] > 0.0) || !(d > 1e-13 * dorig[j]) || !(d < CUDART_INF);
+        const double ljj = sqrt(bad ? 1.0 : d);
+        __syncthreads();
+        if (tid == 0) {
+            if (bad) fail = 1;
+            L[j][j] = ljj;
+        }
+        for (int i = j + 1 + tid; i < w; i += blockDim.x) L[i][j] /= ljj;
+        __syncthreads();
+        const int rem = w - j - 1;
+        for (int e = tid; e < rem * rem; e += blockDim.x) {
+            const int i = j + 1 + e / rem, k = j + 1 + e % rem;
+            if (k <= i) L[i][k] -= L[i][j] * L[k][j];
+        }
+        __syncthreads();
+    }
+    // Rinv = L^{-T}: column c by back substitution on L^T x = e_c
+    for (int c = tid; c < w; c += blockDim.x) {
+        double x[kCholMax];
+        for (int r = 0; r < w; ++r) x[r] = 0.0;
+        x[c] = 1.0 / L[c][c];
+        for (int r = c - 1; r >= 0; --r) {
+            double s = 0.0;
+            for (int t = r + 1; t <= c; ++t) s += L[t][r] * x[t];
+            x[r] = -s / L[r][r];
+        }
+        for (int r = 0; r < w; ++r) Rinv[r * w + c] = x[r];
+    }
+    if (tid == 0 && fail) status[0] = 1;
+}
+
+// ---------------------------------------------------------------------------
+// Householder QR fallback (Eigen's makeHouseholder convention), one CTA
+// ---------------------------------------------------------------------------
+constexpr int kHhThreads = 512;
+
+__device__ double block_sum(double v, double* red) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) t += red[i];
+    return t;
+}
+
+__global__ void __launch_bounds__(kHhThreads) householder_kernel(const double* __restrict__ X, long long m, int w,
+                                                                 long long ldx, double* __restrict__ Q,
+                                                                 long long ldq, double* __restrict__ Wk,
+                                                                 const int* __restrict__ pred,
+                                                                 const int* __restrict__ status) {
+    if (pred != nullptr && *pred == 0) return;
+    if (status != nullptr && *status == 0) return;
+    __shared__ double red[32];
+    __shared__ double tau[kCholMax];
+    const int tid = threadIdx.x;
+    for (long long e = tid; e < m * w; e += blockDim.x) Wk[e] = X[(e / w) * ldx + e % w];
+    __syncthreads();
+    for (int j = 0; j < w; ++j) {
+        double ts = 0.0;
+        for (long long i = j + 1 + tid; i < m; i += blockDim.x) {
+            const double v = Wk[i * w + j];
+            ts = fma(v, v, ts);
+        }
+        const double tail_sq = block_sum(ts, red);
+        const double c0 = Wk[static_cast<long long>(j) * w + j];
+        double t, beta;
+        if (tail_sq <= DBL_MIN) {
+            t = 0.0;
+            beta = c0;
+            for (long long i = j + 1 + tid; i < m; i += blockDim.x) Wk[i * w + j] = 0.0;
+        } else {
+            beta = sqrt(c0 * c0 + tail_sq);
+            if (c0 >= 0.0) beta = -beta;
+            const double inv = 1.0 / (c0 - beta);
+            for (long long i = j + 1 + tid; i < m; i += blockDim.x) Wk[i * w + j] *= inv;
+            t = (beta - c0) / beta;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            Wk[static_cast<long long>(j) * w + j] = beta;
+            tau[j] = t;
+        }
+        __syncthreads();
+        if (t != 0.0) {
+            for (int c = j + 1; c < w; ++c) {
+                double ds = 0.0;
+                for (long long i = j + 1 + tid; i < m; i += blockDim.x) ds = fma(Wk[i * w + j], Wk[i * w + c], ds);
+                double dot = block_sum(ds, red) + Wk[static_cast<long long>(j) * w + c];
+                dot *= t;
+                __syncthreads();
+                if (tid == 0) Wk[static_cast<long long>(j) * w + c] -= dot;
+                for (long long i = j + 1 + tid; i < m; i += blockDim.x) Wk[i * w + c] -= dot * Wk[i * w + j];
+                __syncthreads();
+            }
+        }
+    }
+    // Q = H_0 ... H_{w-1} [I_w; 0]
+    for (long long e = tid; e < m * w; e += blockDim.x) {
+        const long long i = e / w, c = e % w;
+        Q[i * ldq + c] = (i == c) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int j = w - 1; j >= 0; --j) {
+        const double t = tau[j];
+        if (t == 0.0) continue;
+        for (int c = 0; c < w; ++c) {
+            double ds = 0.0;
+            for (long long i = j + 1 + tid; i < m; i += blockDim.x) ds = fma(Wk[i * w + j], Q[i * ldq + c], ds);
+            double dot = block_sum(ds, red) + Q[static_cast<long long>(j) * ldq + c];
+            dot *= t;
+            __syncthreads();
+            if (tid == 0) Q[static_cast<long long>(j) * ldq + c] -= dot;
+            for (long long i = j + 1 + tid; i < m; i += blockDim.x) Q[i * ldq + c] -= dot * Wk[i * w + j];
+            __syncthreads();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// single-CTA one-sided Jacobi eigensolver for the small Gram (r <= 48)
+// ---------------------------------------------------------------------------
+constexpr int kJacMax = 48;
+
+__global__ void __launch_bounds__(1024) jacobi_eig_kernel(const double* __restrict__ G, int r,
+                                                          double* __restrict__ W, double* __restrict__ lambda) {
+    __shared__ double A[kJacMax][kJacMax + 1];  // column j = A[.][j]
+    __shared__ double V[kJacMax][kJacMax + 1];
+    __shared__ double nrm[kJacMax];
+    __shared__ int order[kJacMax];
+    __shared__ int rotated;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rp = (r + 1) & ~1;  // even, padded with a zero column
+    for (int e = tid; e < kJacMax * kJacMax; e += blockDim.x) {
+        const int i = e / kJacMax, j = e % kJacMax;
+        A[i][j] = (i < r && j < r) ? G[i * r + j] : 0.0;
+        V[i][j] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int sweep = 0; sweep < 40; ++sweep) {
+        if (tid == 0) rotated = 0;
+        __syncthreads();
+        for (int step = 0; step < rp - 1; ++step) {
+            const int k = warp;
+            if (k < rp / 2) {
+                auto player = [&](int pos) { return pos == 0 ? 0 : 1 + (pos - 1 + step) % (rp - 1); };
+                int p = player(k), q = player(rp - 1 - k);
+                if (p > q) {
+                    const int t = p;
+                    p = q;
+                    q = t;
+                }
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int i = lane; i < rp; i += 32) {
+                    const double x = A[i][p], y = A[i][q];
+                    al = fma(x, x, al);
+                    be = fma(y, y, be);
+                    ga = fma(x, y, ga);
+                }
+                al = warp_sum(al);
+                be = warp_sum(be);
+                ga = warp_sum(ga);
+                if (ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
+                    const double zeta = (be - al) / (2.0 * ga);
+                    const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                    const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+                    for (int i = lane; i < rp; i += 32) {
+                        const double x = A[i][p], y = A[i][q];
+                        A[i][p] = c * x - s * y;
+                        A[i][q] = s * x + c * y;
+                        const double vx = V[i][p], vy = V[i][q];
+                        V[i][p] = c * vx - s * vy;
+                        V[i][q] = s * vx + c * vy;
+                    }
+                    if (lane == 0) rotated = 1;
+                }
+            }
+            __syncthreads();
+        }
+        if (!rotated) break;
+        __syncthreads();
+    }
+    // eigenvalue j = +-||A[:, j]|| with the sign of v_j^T A_j (PSD: +)
+    if (tid < r) {
+        double s = 0.0, d = 0.0;
+        for (int i = 0; i < r; ++i) {
+            s = fma(A[i][tid], A[i][tid], s);
+            d = fma(V[i][tid], A[i][tid], d);
+        }
+        nrm[tid] = (d < 0.0 ? -1.0 : 1.0) * sqrt(s);
+        order[tid] = tid;
+    }
+    __syncthreads();
+    if (tid == 0) {  // stable insertion sort, descending
+        for (int i = 1; i < r; ++i) {
+            const int o = order[i];
+            int j = i - 1;
+            while (j >= 0 && nrm[order[j]] < nrm[o]) {
+                order[j + 1] = order[j];
+                --j;
+            }
+            order[j + 1] = o;
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < r * r; e += blockDim.x) {
+        const int i = e / r, j = e % r;
+        W[i * r + j] = V[i][order[j]];
+    }
+    if (tid < r) lambda[tid] = nrm[order[tid]];
+}
+
+// ---------------------------------------------------------------------------
+// Cooperative one-sided Jacobi for larger Grams: columns of A (= G) and V live
+// column-major in global memory (L2-resident up to r ~ 3000); each round of
+// the round-robin tournament rotates rp/2 disjoint column pairs, one warp per
+// pair, separated by a grid-wide barrier (all CTAs co-resident through a
+// cooperative launch).  L1 is bypassed (__ldcg) so every round reads the
+// previous round's columns.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen, unsigned nblocks) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = atomicAdd(gen, 0u);
+        if (atomicAdd(count, 1u) == nblocks - 1) {
+            atomicExch(count, 0u);
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (atomicAdd(gen, 0u) == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) jacobi_coop_kernel(double* __restrict__ A, double* __restrict__ V, int rp,
+                                                          int max_sweeps, unsigned* __restrict__ sync,
+                                                          double* __restrict__ lambda) {
+    const int lane = threadIdx.x & 31;
+    const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    unsigned* count = sync;
+    unsigned* gen = sync + 1;
+    unsigned* rot = sync + 2;  // rot[0], rot[1]: rotations of the current / next sweep
+    for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) rot[(sweep + 1) & 1] = 0u;
+        for (int step = 0; step < rp - 1; ++step) {
+            for (int k = gwarp; k < rp / 2; k += nwarps) {
+                const int a = k, b = rp - 1 - k;
+                int p = (a == 0) ? 0 : 1 + (a - 1 + step) % (rp - 1);
+                int q = (b == 0) ? 0 : 1 + (b - 1 + step) % (rp - 1);
+                if (p > q) {
+                    const int t = p;
+                    p = q;
+                    q = t;
+                }
+                double* ap = A + static_cast<long long>(p) * rp;
+                double* aq = A + static_cast<long long>(q) * rp;
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int i = lane; i < rp; i += 32) {
+                    const double x = __ldcg(ap + i), y = __ldcg(aq + i);
+                    al = fma(x, x, al);
+                    be = fma(y, y, be);
+                    ga = fma(x, y, ga);
+                }
+                al = warp_sum(al);
+                be = warp_sum(be);
+                ga = warp_sum(ga);
+                if (ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
+                    const double zeta = (be - al) / (2.0 * ga);
+                    const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                    const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+                    double* vp = V + static_cast<long long>(p) * rp;
+                    double* vq = V + static_cast<long long>(q) * rp;
+                    for (int i = lane; i < rp; i += 32) {
+                        const double x = __ldcg(ap + i), y = __ldcg(aq + i);
+                        __stcg(ap + i, c * x - s * y);
+                        __stcg(aq + i, s * x + c * y);
+                        const double vx = __ldcg(vp + i), vy = __ldcg(vq + i);
+                        __stcg(vp + i, c * vx - s * vy);
+                        __stcg(vq + i, s * vx + c * vy);
+                    }
+                    if (lane == 0) atomicAdd(rot + (sweep & 1), 1u);
+                }
+            }
+            grid_barrier(count, gen, gridDim.x);
+        }
+        if (atomicAdd(rot + (sweep & 1), 0u) == 0u) break;
+        grid_barrier(count, gen, gridDim.x);
+    }
+    // eigenvalue j = sign(v_j . a_j) ||a_j||
+    for (int j = gwarp; j < rp; j += nwarps) {
+        const double* aj = A + static_cast<long long>(j) * rp;
+        const double* vj = V + static_cast<long long>(j) * rp;
+        double s = 0.0, d = 0.0;
+        for (int i = lane; i < rp; i += 32) {
+            const double x = __ldcg(aj + i);
+            s = fma(x, x, s);
+            d = fma(__ldcg(vj + i), x, d);
+        }
+        s = warp_sum(s);
+        d = warp_sum(d);
+        if (lane == 0) lambda[j] = (d < 0.0 ? -1.0 : 1.0) * sqrt(s);
+    }
+}
+
+// W (r x r row-major) column j <- column perm[j] of the column-major V (ld)
+__global__ void gather_eigvecs_kernel(const double* __restrict__ Vcm, long long ldv, const int* __restrict__ perm,
+                                      long long r, double* __restrict__ W) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= r * r) return;
+    const long long i = e / r, j = e % r;
+    W[i * r + j] = Vcm[perm[j] * ldv + i];
+}
+
+__global__ void init_jacobi_kernel(const double* __restrict__ G, long long r, long long rp, double* __restrict__ A,
+                                   double* __restrict__ V) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= rp * rp) return;
+    const long long j = e / rp, i = e % rp;  // column-major (i, j)
+    A[e] = (i < r && j < r) ? G[i * r + j] : 0.0;
+    V[e] = (i == j) ? 1.0 : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// small utilities
+// ---------------------------------------------------------------------------
+__global__ void col_sumsq_partial_kernel(const double* __restrict__ X, long long rows, long long cols, long long ld,
+                                         long long rows_per_block, double* __restrict__ partial) {
+    const long long j = blockIdx.x * 32LL + (threadIdx.x & 31);
+    const int ty = threadIdx.x >> 5;  // 8 row lanes
+    __shared__ double red[8][33];
+    double s = 0.0;
+    const long long r0 = blockIdx.y * rows_per_block;
+    const long long r1 = min(rows, r0 + rows_per_block);
+    if (j < cols)
+        for (long long i = r0 + ty; i < r1; i += 8) {
+            const double v = X[i * ld + j];
+            s = fma(v, v, s);
+        }
+    red[ty][threadIdx.x & 31] = s;
+    __syncthreads();
+    if (ty == 0 && j < cols) {
+        double t = 0.0;
+        for (int q = 0; q < 8; ++q) t += red[q][threadIdx.x & 31];
+        partial[blockIdx.y * cols + j] = t;
+    }
+}
+
+__global__ void col_sumsq_finish_kernel(const double* __restrict__ partial, long long cols, int nparts,
+                                        double* __restrict__ out) {
+    const long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (j >= cols) return;
+    double t = 0.0;
+    for (int p = 0; p < nparts; ++p) t += partial[p * cols + j];
+    out[j] = t;
+}
+
+__global__ void scale_cols_kernel(double* X, long long rows, long long cols, long long ld, const double* s) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= rows * cols) return;
+    const long long i = e / cols, j = e % cols;
+    X[i * ld + j] *= s[j];
+}
+
+__global__ void copy2d_kernel(const double* __restrict__ src, long long lds, double* __restrict__ dst, long long ldd,
+                              long long rows, long long cols, const int* __restrict__ pred) {
+    if (pred != nullptr && *pred == 0) return;
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= rows * cols) return;
+    const long long i = e / cols, j = e % cols;
+    dst[i * ldd + j] = src[i * lds + j];
+}
+
+__global__ void fill_kernel(double* p, long long n, double v) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e < n) p[e] = v;
+}
+
+__global__ void transpose_kernel(const double* __restrict__ in, long long rows, long long cols, long long ldi,
+                                 double* __restrict__ out) {
+    __shared__ double tile[32][33];
+    const long long bx = blockIdx.x * 32LL, by = blockIdx.y * 32LL;
+    for (int t = threadIdx.y; t < 32; t += blockDim.y) {
+        const long long i = by + t, j = bx + threadIdx.x;
+        if (i < rows && j < cols) tile[t][threadIdx.x] = in[i * ldi + j];
+    }
+    __syncthreads();
+    for (int t = threadIdx.y; t < 32; t += blockDim.y) {
+        const long long j = bx + t, i = by + threadIdx.x;
+        if (i < rows && j < cols) out[j * rows + i] = tile[threadIdx.x][t];
+    }
+}
+
+__global__ void permute_cols_kernel(const double* __restrict__ W, long long rows, long long ldw,
+                                    const int* __restrict__ perm, long long kcols, double* __restrict__ W2,
+                                    long long ldw2) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= rows * kcols) return;
+    const long long i = e / kcols, j = e % kcols;
+    W2[i * ldw2 + j] = W[i * ldw + perm[j]];
+}
+
+inline unsigned nblk(i64 n, int bs = 256) { return static_cast<unsigned>(std::max<i64>(1, (n + bs - 1) / bs)); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+          const double* B, i64 ldb, double beta, double* C, i64 ldc, const int* pred) {
+    if (M <= 0 || N <= 0) return;
+    LaunchScope ls(ctx, cls, 8.0 * (M * K + K * N + M * N * (beta != 0.0 ? 2 : 1)), 2.0 * M * N * K);
+    if (K <= 0) {
+        scale2d_kernel<<<nblk(M * N), 256, 0, ctx->stream>>>(C, M, N, ldc, beta, pred);
+        return;
+    }
+    if (N <= 16)
+        gemm_launch<128, 16, 16, 4, 4>(ctx, transA, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
+    else
+        gemm_launch<64, 64, 16, 4, 4>(ctx, transA, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
+}
+
+void sumsq(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double* d_out, int op, const int* pred) {
+    ctx->ws_partial2.ensure(kRedBlocks);
+    const i64 tot = rows * cols;
+    if (tot <= 0) {
+        LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
+        finish_kernel<<<1, 32, 0, ctx->stream>>>(ctx->ws_partial2.get(), 0, d_out, op, pred);
+        return;
+    }
+    const int blocks = static_cast<int>(std::min<i64>(kRedBlocks, (tot + 255) / 256));
+    LaunchScope ls(ctx, K_OTHER, 8.0 * tot, 2.0 * tot);
+    sumsq_partial_kernel<<<blocks, 256, 0, ctx->stream>>>(X, rows, cols, ld, ctx->ws_partial2.get(), pred);
+    finish_kernel<<<1, 32, 0, ctx->stream>>>(ctx->ws_partial2.get(), blocks, d_out, op, pred);
+}
+
+void maxabs(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double diag_shift, double* d_out) {
+    ctx->ws_partial2.ensure(kRedBlocks);
+    const i64 tot = rows * cols;
+    const int blocks = static_cast<int>(std::max<i64>(1, std::min<i64>(kRedBlocks, (tot + 255) / 256)));
+    LaunchScope ls(ctx, K_OTHER, 8.0 * tot, 0.0);
+    maxabs_partial_kernel<<<blocks, 256, 0, ctx->stream>>>(X, rows, cols, ld, diag_shift, ctx->ws_partial2.get());
+    finish_kernel<<<1, 32, 0, ctx->stream>>>(ctx->ws_partial2.get(), blocks, d_out, 2, nullptr);
+}
+
+void set_flag(svt_ctx* ctx, const double* a, const double* b, double coef, int mode, int* flag) {
+    LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
+    set_flag_kernel<<<1, 1, 0, ctx->stream>>>(a, b, coef, mode, flag);
+}
+
+void chol_rinv(svt_ctx* ctx, const double* G, i64 w, double* Rinv, int* status, const int* pred) {
+    if (w > kCholMax) throw std::invalid_argument("chol_rinv: panel wider than 64");
+    LaunchScope ls(ctx, K_QR, 16.0 * w * w, w * w * w / 3.0);
+    chol_rinv_kernel<<<1, 256, 0, ctx->stream>>>(G, static_cast<int>(w), Rinv, status, pred);
+}
+
+void householder_qr(svt_ctx* ctx, const double* X, i64 m, i64 w, i64 ldx, double* Q, i64 ldq, double* work,
+                    const int* pred, const int* status) {
+    if (w > kCholMax) throw std::invalid_argument("householder_qr: panel wider than 64");
+    LaunchScope ls(ctx, K_QR, 0.0, 4.0 * m * w * w);
+    householder_kernel<<<1, kHhThreads, 0, ctx->stream>>>(X, m, static_cast<int>(w), ldx, Q, ldq, work, pred,
+                                                          status);
+}
+
+void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
+    if (r <= 0) return;
+    if (r <= kJacMax) {
+        LaunchScope ls(ctx, K_FINAL, 16.0 * r * r, 0.0);
+        jacobi_eig_kernel<<<1, 1024, 0, ctx->stream>>>(G, static_cast<int>(r), W, lambda);
+        return;
+    }
+    // Larger Grams: cooperative multi-CTA one-sided Jacobi.
+    const i64 rp = (r + 1) & ~1LL;
+    ctx->ws_eig.ensure(static_cast<size_t>(2 * rp * rp + rp));
+    ctx->ws_info.ensure(8);
+    double* A = ctx->ws_eig.get();
+    double* V = A + rp * rp;
+    double* lam_u = V + rp * rp;
+    SVT_CUDA(cudaMemsetAsync(ctx->ws_info.get(), 0, 8 * sizeof(int), ctx->stream));
+    {
+        LaunchScope ls(ctx, K_FINAL, 16.0 * rp * rp, 0.0);
+        init_jacobi_kernel<<<nblk(rp * rp), 256, 0, ctx->stream>>>(G, r, rp, A, V);
+    }
+    int per_sm = 0;
+    SVT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_coop_kernel, 256, 0));
+    const int want = static_cast<int>(std::min<i64>(std::max(1, per_sm) * ctx->num_sms, (rp / 2 + 7) / 8));
+    const int grid = std::max(1, std::min(want, std::max(1, per_sm) * ctx->num_sms));
+    int rpi = static_cast<int>(rp), sweeps = 40;
+    unsigned* sync = reinterpret_cast<unsigned*>(ctx->ws_info.get());
+    void* args[] = {&A, &V, &rpi, &sweeps, &sync, &lam_u};
+    {
+        LaunchScope ls(ctx, K_FINAL, 0.0, 6.0 * rp * rp * rp * 8);
+        SVT_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_coop_kernel), grid, 256, args, 0,
+                                             ctx->stream));
+    }
+    // sort descending on the host (r values), gather the eigenvectors
+    std::vector<double> lh(static_cast<size_t>(rp));
+    SVT_CUDA(cudaMemcpyAsync(lh.data(), lam_u, sizeof(double) * rp, cudaMemcpyDeviceToHost, ctx->stream));
+    SVT_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::vector<int> perm(static_cast<size_t>(r));
+    for (i64 j = 0; j < r; ++j) perm[static_cast<size_t>(j)] = static_cast<int>(j);
+    // the padded zero column (if any) is index r and is excluded
+    std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return lh[x] > lh[y]; });
+    std::vector<double> ls_sorted(static_cast<size_t>(r));
+    for (i64 j = 0; j < r; ++j) ls_sorted[static_cast<size_t>(j)] = lh[static_cast<size_t>(perm[static_cast<size_t>(j)])];
+    DevBuf<int> dperm(static_cast<size_t>(r));
+    SVT_CUDA(cudaMemcpyAsync(dperm.get(), perm.data(), sizeof(int) * r, cudaMemcpyHostToDevice, ctx->stream));
+    SVT_CUDA(cudaMemcpyAsync(lambda, ls_sorted.data(), sizeof(double) * r, cudaMemcpyHostToDevice, ctx->stream));
+    {
+        LaunchScope ls(ctx, K_FINAL, 16.0 * r * r, 0.0);
+        gather_eigvecs_kernel<<<nblk(r * r), 256, 0, ctx->stream>>>(V, rp, dperm.get(), r, W);
+    }
+    SVT_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void col_sumsq(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double* out) {
+    if (cols <= 0) return;
+    const i64 rpb = std::max<i64>(256, (rows + 63) / 64);
+    const i64 nparts = std::max<i64>(1, (rows + rpb - 1) / rpb);
+    ctx->ws_partial2.ensure(static_cast<size_t>(nparts * cols));
+    LaunchScope ls(ctx, K_OTHER, 8.0 * rows * cols, 2.0 * rows * cols);
+    dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>(nparts));
+    col_sumsq_partial_kernel<<<grid, 256, 0, ctx->stream>>>(X, rows, cols, ld, rpb, ctx->ws_partial2.get());
+    col_sumsq_finish_kernel<<<nblk(cols), 256, 0, ctx->stream>>>(ctx->ws_partial2.get(), cols,
+                                                                 static_cast<int>(nparts), out);
+}
+
+void scale_cols(svt_ctx* ctx, double* X, i64 rows, i64 cols, i64 ld, const double* s) {
+    if (rows * cols <= 0) return;
+    LaunchScope ls(ctx, K_OTHER, 16.0 * rows * cols, 0.0);
+    scale_cols_kernel<<<nblk(rows * cols), 256, 0, ctx->stream>>>(X, rows, cols, ld, s);
+}
+
+void copy2d(svt_ctx* ctx, const double* src, i64 lds, double* dst, i64 ldd, i64 rows, i64 cols, const int* pred) {
+    if (rows * cols <= 0) return;
+    LaunchScope ls(ctx, K_OTHER, 16.0 * rows * cols, 0.0);
+    copy2d_kernel<<<nblk(rows * cols), 256, 0, ctx->stream>>>(src, lds, dst, ldd, rows, cols, pred);
+}
+
+void fill(svt_ctx* ctx, double* p, i64 n, double v) {
+    if (n <= 0) return;
+    LaunchScope ls(ctx, K_OTHER, 8.0 * n, 0.0);
+    fill_kernel<<<nblk(n), 256, 0, ctx->stream>>>(p, n, v);
+}
+
+void transpose(svt_ctx* ctx, const double* in, i64 rows, i64 cols, i64 ldi, double* out) {
+    if (rows * cols <= 0) return;
+    LaunchScope ls(ctx, K_OTHER, 16.0 * rows * cols, 0.0);
+    dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>((rows + 31) / 32));
+    transpose_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(in, rows, cols, ldi, out);
+}
+
+void permute_cols(svt_ctx* ctx, const double* W, i64 rows, i64 ldw, const int* perm, i64 kcols, double* W2,
+                  i64 ldw2) {
+    if (rows * kcols <= 0) return;
+    LaunchScope ls(ctx, K_OTHER, 16.0 * rows * kcols, 0.0);
+    permute_cols_kernel<<<nblk(rows * kcols), 256, 0, ctx->stream>>>(W, rows, ldw, perm, kcols, W2, ldw2);
+}
+
+}  // namespace svtb

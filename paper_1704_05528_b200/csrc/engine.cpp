@@ -1,0 +1,531 @@
+// R3SVD / R4SVD on the device (sketch.hpp) and the primitives they compose.
+//
+// Control flow follows the reference line by line: the rank-revealing
+// `while error_percentage > eps` loop stays on the host (one 8-byte read per
+// round), every data-dependent branch INSIDE a round (the conditional second
+// Gram-Schmidt pass, sketch.hpp:134; the re-projection, :138; the recycled
+// basis drift test, :231; the rank-deficient QR fallback) is evaluated on
+// the device and predicates the dependent kernels, so a round issues no host
+// synchronisation.  Multi-GPU: Q / X / U rows are the rank's row block;
+// Y^T-products, Gram blocks and norms are NCCL all-reduced.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "kernels.hpp"
+
+namespace svtb {
+
+namespace {
+
+// scalar / flag slots in ctx->d_scalars / ctx->d_flags
+enum : int { S_FROB = 0, S_NX = 1, S_NC = 2, S_MAXD = 3, S_NB = 4, S_TMP = 5, S_SPEC = 6 };
+enum : int { F_CGS2 = 0, F_REORTH = 1, F_QRSTAT = 2, F_DRIFT = 3, F_BLK = 4 };
+
+double* dsc(svt_ctx* c, int i) { return c->d_scalars + i; }
+int* dfl(svt_ctx* c, int i) { return c->d_flags + i; }
+
+double read_scalar(svt_ctx* c, int i) {
+    SVT_CUDA(cudaMemcpyAsync(c->h_scalars + i, c->d_scalars + i, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    return c->h_scalars[i];
+}
+
+int read_flag(svt_ctx* c, int i) {
+    SVT_CUDA(cudaMemcpyAsync(c->h_flags + i, c->d_flags + i, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    return c->h_flags[i];
+}
+
+void zero_flag(svt_ctx* c, int i) { SVT_CUDA(cudaMemsetAsync(c->d_flags + i, 0, sizeof(int), c->stream)); }
+
+void allreduce(svt_ctx* c, double* p, size_t n) { c->comm.allreduce_sum(p, n, c->stream); }
+
+inline u64 splitmix64(u64 x) {
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+
+// grow Q / B^T capacity geometrically, preserving the first `rank` columns
+void ensure_cap(Engine& E, QBDev& st, i64 need) {
+    if (need <= st.cap) return;
+    i64 cap = std::max<i64>(need, std::max<i64>(32, st.cap * 2));
+    cap = std::min<i64>(std::max(cap, need), std::max(st.min_dim, need));
+    cap = (cap + 7) & ~7LL;
+    DevBuf<double> Q2(static_cast<size_t>(std::max<i64>(1, st.m_local) * cap));
+    DevBuf<double> B2(static_cast<size_t>(st.n * cap));
+    if (st.rank > 0) {
+        if (st.m_local > 0)
+            SVT_CUDA(cudaMemcpy2DAsync(Q2.get(), cap * sizeof(double), st.Q.get(), st.cap * sizeof(double),
+                                       st.rank * sizeof(double), st.m_local, cudaMemcpyDeviceToDevice,
+                                       E.ctx->stream));
+        SVT_CUDA(cudaMemcpy2DAsync(B2.get(), cap * sizeof(double), st.Bt.get(), st.cap * sizeof(double),
+                                   st.rank * sizeof(double), st.n, cudaMemcpyDeviceToDevice, E.ctx->stream));
+    }
+    st.Q = std::move(Q2);
+    st.Bt = std::move(B2);
+    st.cap = cap;
+}
+
+// One CholQR2 panel (w <= 64) with the Householder fallback.  X is preserved.
+void qr_panel(Engine& E, const double* X, i64 ldx, i64 w, double* Qout, i64 ldq, const int* pred) {
+    svt_ctx* c = E.ctx;
+    const i64 m = E.mat->m_local;
+    E.G.ensure(static_cast<size_t>(w * w));
+    E.Rinv.ensure(static_cast<size_t>(w * w));
+    E.tmp.ensure(static_cast<size_t>(std::max<i64>(1, m) * w));
+    int* status = dfl(c, F_QRSTAT);
+    zero_flag(c, F_QRSTAT);
+    // pass 1: R1 = chol(X^T X), Q1 = X R1^{-1}
+    gemm(c, K_QR, true, w, w, m, 1.0, X, ldx, X, ldx, 0.0, E.G.get(), w, pred);
+    allreduce(c, E.G.get(), static_cast<size_t>(w * w));
+    chol_rinv(c, E.G.get(), w, E.Rinv.get(), status, pred);
+    gemm(c, K_QR, false, m, w, w, 1.0, X, ldx, E.Rinv.get(), w, 0.0, E.tmp.get(), w, pred);
+    // pass 2
+    gemm(c, K_QR, true, w, w, m, 1.0, E.tmp.get(), w, E.tmp.get(), w, 0.0, E.G.get(), w, pred);
+    allreduce(c, E.G.get(), static_cast<size_t>(w * w));
+    chol_rinv(c, E.G.get(), w, E.Rinv.get(), status, pred);
+    gemm(c, K_QR, false, m, w, w, 1.0, E.tmp.get(), w, E.Rinv.get(), w, 0.0, Qout, ldq, pred);
+    if (c->comm.world == 1) {
+        E.hh.ensure(static_cast<size_t>(std::max<i64>(1, m) * w));
+        householder_qr(c, X, m, w, ldx, Qout, ldq, E.hh.get(), pred, status);
+        return;
+    }
+    // multi-GPU: the (rare) fallback gathers the panel and factors it redundantly
+    if (pred != nullptr && read_flag(c, static_cast<int>(pred - c->d_flags)) == 0) return;
+    if (read_flag(c, F_QRSTAT) == 0) return;
+    const i64 M = E.mat->m;
+    DevBuf<double> full(static_cast<size_t>(M * w)), qfull(static_cast<size_t>(M * w)), work(static_cast<size_t>(M * w));
+    SVT_CUDA(cudaMemsetAsync(full.get(), 0, sizeof(double) * M * w, c->stream));
+    copy2d(c, X, ldx, full.get() + E.mat->row_begin * w, w, m, w);
+    allreduce(c, full.get(), static_cast<size_t>(M * w));
+    householder_qr(c, full.get(), M, w, w, qfull.get(), w, work.get(), nullptr, nullptr);
+    copy2d(c, qfull.get() + E.mat->row_begin * w, w, Qout, ldq, m, w);
+}
+
+// Project Q[:, 0:r0] out of the panel P (m x w, ld) and re-orthonormalize
+// it, predicated on flag `f` computed from max|Q^T P| > 1e-8 (sketch.hpp:138).
+void reorth_if_needed(Engine& E, const double* Q, i64 ldq, i64 r0, double* P, i64 ldp, i64 w) {
+    svt_ctx* c = E.ctx;
+    const i64 m = E.mat->m_local;
+    E.D.ensure(static_cast<size_t>(r0 * w));
+    gemm(c, K_GEMM, true, r0, w, m, 1.0, Q, ldq, P, ldp, 0.0, E.D.get(), w);
+    allreduce(c, E.D.get(), static_cast<size_t>(r0 * w));
+    maxabs(c, E.D.get(), r0, w, w, 0.0, dsc(c, S_MAXD));
+    set_flag(c, dsc(c, S_MAXD), nullptr, 1e-8, 1, dfl(c, F_REORTH));
+    const int* f = dfl(c, F_REORTH);
+    E.X2.ensure(static_cast<size_t>(std::max<i64>(1, m) * w));
+    copy2d(c, P, ldp, E.X2.get(), w, m, w, f);
+    gemm(c, K_GEMM, false, m, w, r0, -1.0, Q, ldq, E.D.get(), w, 1.0, E.X2.get(), w, f);
+    qr_panel(E, E.X2.get(), w, w, P, ldp, f);
+}
+
+}  // namespace
+
+u64 derive_seed_u(u64 seed, u64 stream) { return splitmix64(seed ^ splitmix64(stream)); }
+
+double frob_sq(Engine& E) {
+    svt_ctx* c = E.ctx;
+    sumsq(c, E.Y.csr, 1, E.mat->nnz_local, E.mat->nnz_local, dsc(c, S_FROB), 0);
+    allreduce(c, dsc(c, S_FROB), 1);
+    return read_scalar(c, S_FROB);
+}
+
+void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo) {
+    svt_mat* A = E.mat;
+    spmm(E.ctx, K_SPMM, A->m_local, A->rowptr.get(), A->col.get(), E.Y.csr, A->nnz_local, A->n, w, X, ldx, out, ldo);
+}
+
+void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out) {
+    svt_mat* A = E.mat;
+    spmm(E.ctx, K_SPMMT, A->n, A->colptr.get(), A->cscrow.get(), E.Y.csc, A->nnz_local, A->m_local, w, X, ldx, out,
+         w);
+    allreduce(E.ctx, out, static_cast<size_t>(A->n * w));
+}
+
+// dense.hpp:103-110 on a panel of any width: CholQR2 (w <= 64) or block
+// CGS2 + CholQR2 over 64-column blocks (the column-ordered QR, same nested
+// spans).  X is clobbered.
+void qr_orthonormal(Engine& E, double* X, i64 ldx, i64 w, double* Qout, i64 ldq) {
+    svt_ctx* c = E.ctx;
+    const i64 m = E.mat->m_local;
+    constexpr i64 B = 64;
+    for (i64 b0 = 0; b0 < w; b0 += B) {
+        const i64 wb = std::min(B, w - b0);
+        double* Xb = X + b0;
+        if (b0 > 0) {
+            E.C.ensure(static_cast<size_t>(b0 * wb));
+            for (int pass = 0; pass < 2; ++pass) {
+                gemm(c, K_QR, true, b0, wb, m, 1.0, Qout, ldq, Xb, ldx, 0.0, E.C.get(), wb);
+                allreduce(c, E.C.get(), static_cast<size_t>(b0 * wb));
+                gemm(c, K_QR, false, m, wb, b0, -1.0, Qout, ldq, E.C.get(), wb, 1.0, Xb, ldx);
+            }
+        }
+        qr_panel(E, Xb, ldx, wb, Qout + b0, ldq, nullptr);
+        if (b0 > 0) reorth_if_needed(E, Qout, ldq, b0, Qout + b0, ldq, wb);
+    }
+}
+
+// sampled.hpp:188-213
+double spectral_norm_est(Engine& E, int iters, u64 seed) {
+    if (iters < 1) throw std::invalid_argument("spectral_norm_est: iters must be >= 1");
+    svt_ctx* c = E.ctx;
+    svt_mat* A = E.mat;
+    const i64 n = A->n, m = A->m_local;
+    DevBuf<double> x(static_cast<size_t>(n)), y(static_cast<size_t>(std::max<i64>(1, m)));
+    gaussian_block_dev(c, n, 1, seed, x.get(), 1);
+    sumsq(c, x.get(), 1, n, n, dsc(c, S_SPEC), 0);
+    double xn = std::sqrt(read_scalar(c, S_SPEC));
+    if (xn == 0.0) return 0.0;
+    scale_values(c, n, x.get(), 1.0 / xn, x.get(), nullptr, nullptr);
+    double estimate = 0.0;
+    for (int it = 0; it < iters; ++it) {
+        sp_mult(E, 1, x.get(), 1, y.get(), 1);
+        sumsq(c, y.get(), 1, m, m, dsc(c, S_SPEC), 0);
+        allreduce(c, dsc(c, S_SPEC), 1);
+        estimate = std::sqrt(read_scalar(c, S_SPEC));
+        if (estimate == 0.0) return 0.0;
+        sp_mult_t(E, 1, y.get(), 1, x.get());
+        sumsq(c, x.get(), 1, n, n, dsc(c, S_SPEC), 0);
+        xn = std::sqrt(read_scalar(c, S_SPEC));
+        if (xn == 0.0) return estimate;
+        scale_values(c, n, x.get(), 1.0 / xn, x.get(), nullptr, nullptr);
+    }
+    return estimate;
+}
+
+// sketch.hpp:71-79 — X <- Y (Y^T X), np passes, QR between passes
+static void power_iterate(Engine& E, i64 w, int np) {
+    svt_ctx* c = E.ctx;
+    const i64 m = E.mat->m_local, n = E.mat->n;
+    for (int j = 0; j < np; ++j) {
+        if (j > 0) {
+            E.P.ensure(static_cast<size_t>(std::max<i64>(1, m) * w));
+            qr_orthonormal(E, E.X.get(), w, w, E.P.get(), w);
+            std::swap(E.X, E.P);
+        }
+        E.T.ensure(static_cast<size_t>(n * w));
+        sp_mult_t(E, w, E.X.get(), w, E.T.get());
+        sp_mult(E, w, E.T.get(), w, E.X.get(), w);
+    }
+    (void)c;
+}
+
+// B[r0:r0+w, :] = (Y^T Q[:, r0:r0+w])^T stored as B^T columns; norm_b_sq +=
+static void append_coefficients(Engine& E, QBDev& st, i64 r0, i64 w, int nb_op) {
+    svt_ctx* c = E.ctx;
+    E.T.ensure(static_cast<size_t>(st.n * w));
+    sp_mult_t(E, w, st.Q.get() + r0, st.cap, E.T.get());
+    copy2d(c, E.T.get(), w, st.Bt.get() + r0, st.cap, st.n, w);
+    sumsq(c, E.T.get(), st.n, w, w, dsc(c, S_NB), nb_op);
+}
+
+// sketch.hpp:89-108
+void qb_init(Engine& E, QBDev& st, i64 t, int np, u64 seed, double frob_y_sq) {
+    svt_ctx* c = E.ctx;
+    svt_mat* A = E.mat;
+    const i64 min_dim = std::min(A->m, A->n);
+    if (t < 1 || t > min_dim) throw std::invalid_argument("qb_init: t must satisfy 1 <= t <= min(m, n)");
+    if (frob_y_sq < 0.0) frob_y_sq = frob_sq(E);
+    if (!(frob_y_sq > 0.0)) throw std::domain_error("qb_init: target matrix is all zero");
+    st.m_local = A->m_local;
+    st.n = A->n;
+    st.min_dim = min_dim;
+    st.rank = 0;
+    st.cap = 0;
+    ensure_cap(E, st, t);
+    const i64 m = A->m_local;
+    E.Om.ensure(static_cast<size_t>(A->n * t));
+    E.X.ensure(static_cast<size_t>(std::max<i64>(1, m) * t));
+    gaussian_block_dev(c, A->n, t, seed, E.Om.get(), t);
+    sp_mult(E, t, E.Om.get(), t, E.X.get(), t);
+    power_iterate(E, t, np);
+    qr_orthonormal(E, E.X.get(), t, t, st.Q.get(), st.cap);
+    append_coefficients(E, st, 0, t, 0);
+    st.norm_b_sq = read_scalar(c, S_NB);
+    st.frob_y_sq = frob_y_sq;
+    st.rank = t;
+    st.saturated = (t == min_dim);
+}
+
+// sketch.hpp:114-154
+void qb_extend(Engine& E, QBDev& st, i64 dt, int np, u64 seed) {
+    svt_ctx* c = E.ctx;
+    svt_mat* A = E.mat;
+    if (dt < 1) throw std::invalid_argument("qb_extend: dt must be >= 1");
+    const i64 width = std::min(dt, st.min_dim - st.rank);
+    if (width < 1) {
+        st.saturated = true;
+        return;
+    }
+    const i64 m = A->m_local, n = A->n, r0 = st.rank;
+    ensure_cap(E, st, r0 + width);
+    E.Om.ensure(static_cast<size_t>(n * width));
+    E.X.ensure(static_cast<size_t>(std::max<i64>(1, m) * width));
+    gaussian_block_dev(c, n, width, seed, E.Om.get(), width);
+    sp_mult(E, width, E.Om.get(), width, E.X.get(), width);
+    power_iterate(E, width, np);
+    double* Q = st.Q.get();
+    const i64 ldq = st.cap;
+    if (r0 > 0) {
+        // classical Gram-Schmidt, conditional second pass (sketch.hpp:133-136)
+        E.C.ensure(static_cast<size_t>(r0 * width));
+        gemm(c, K_GEMM, true, r0, width, m, 1.0, Q, ldq, E.X.get(), width, 0.0, E.C.get(), width);
+        allreduce(c, E.C.get(), static_cast<size_t>(r0 * width));
+        gemm(c, K_GEMM, false, m, width, r0, -1.0, Q, ldq, E.C.get(), width, 1.0, E.X.get(), width);
+        gemm(c, K_GEMM, true, r0, width, m, 1.0, Q, ldq, E.X.get(), width, 0.0, E.C.get(), width);
+        allreduce(c, E.C.get(), static_cast<size_t>(r0 * width));
+        sumsq(c, E.X.get(), m, width, width, dsc(c, S_NX), 0);
+        allreduce(c, dsc(c, S_NX), 1);
+        sumsq(c, E.C.get(), r0, width, width, dsc(c, S_NC), 0);
+        set_flag(c, dsc(c, S_NC), dsc(c, S_NX), 1e-8, 0, dfl(c, F_CGS2));
+        gemm(c, K_GEMM, false, m, width, r0, -1.0, Q, ldq, E.C.get(), width, 1.0, E.X.get(), width,
+             dfl(c, F_CGS2));
+    }
+    // QR, then conditional re-projection + QR (sketch.hpp:137-141)
+    qr_panel(E, E.X.get(), width, width, Q + r0, ldq, nullptr);
+    if (r0 > 0) reorth_if_needed(E, Q, ldq, r0, Q + r0, ldq, width);
+    // coefficient block + energy (sketch.hpp:143-150)
+    append_coefficients(E, st, r0, width, 1);
+    st.norm_b_sq = read_scalar(c, S_NB);
+    st.rank = r0 + width;
+    st.saturated = (st.rank == st.min_dim);
+}
+
+// sketch.hpp:158-162 — SVD of B through its Gram: G = B B^T = W L W^T,
+// sigma_j = ||B^T w_j|| (column norms: accurate to ~eps*sigma_1 even for the
+// small values), V = B^T W / sigma, U = Q W.  Kept mode computes only the
+// triplets with sigma > tau (the ones shrink keeps, solver.hpp:110-120).
+void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFactors& out) {
+    svt_ctx* c = E.ctx;
+    const i64 r = st.rank, n = st.n, m = st.m_local;
+    out.m_local = m;
+    out.n = n;
+    out.k = 0;
+    out.sigma.clear();
+    if (r == 0) return;
+    E.G.ensure(static_cast<size_t>(r * r));
+    E.W.ensure(static_cast<size_t>(r * r));
+    E.lam.ensure(static_cast<size_t>(r));
+    gemm(c, K_FINAL, true, r, r, n, 1.0, st.Bt.get(), st.cap, st.Bt.get(), st.cap, 0.0, E.G.get(), r);
+    sym_eig(c, E.G.get(), r, E.W.get(), E.lam.get());
+    std::vector<double> lam(static_cast<size_t>(r));
+    SVT_CUDA(cudaMemcpyAsync(lam.data(), E.lam.get(), sizeof(double) * r, cudaMemcpyDeviceToHost, c->stream));
+    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    i64 kc = r;
+    if (mode == FinalizeMode::Kept) {
+        i64 cnt = 0;
+        const double lim = tau * (1.0 - 1e-7);
+        while (cnt < r && std::sqrt(std::max(lam[static_cast<size_t>(cnt)], 0.0)) > lim) ++cnt;
+        kc = std::min(r, cnt + 1);
+    }
+    E.Vraw.ensure(static_cast<size_t>(n * kc));
+    gemm(c, K_FINAL, false, n, kc, r, 1.0, st.Bt.get(), st.cap, E.W.get(), r, 0.0, E.Vraw.get(), kc);
+    E.lam.ensure(static_cast<size_t>(std::max(r, kc)));
+    col_sumsq(c, E.Vraw.get(), n, kc, kc, E.lam.get());
+    std::vector<double> s2(static_cast<size_t>(kc));
+    SVT_CUDA(cudaMemcpyAsync(s2.data(), E.lam.get(), sizeof(double) * kc, cudaMemcpyDeviceToHost, c->stream));
+    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    std::vector<double> sig(static_cast<size_t>(kc));
+    for (i64 j = 0; j < kc; ++j) sig[static_cast<size_t>(j)] = std::sqrt(s2[static_cast<size_t>(j)]);
+    std::vector<int> perm(static_cast<size_t>(kc));
+    std::iota(perm.begin(), perm.end(), 0);
+    std::stable_sort(perm.begin(), perm.end(),
+                     [&](int a, int b) { return sig[static_cast<size_t>(a)] > sig[static_cast<size_t>(b)]; });
+    i64 k = kc;
+    if (mode == FinalizeMode::Kept) {
+        k = 0;
+        while (k < kc && sig[static_cast<size_t>(perm[static_cast<size_t>(k)])] > tau) ++k;
+    }
+    out.k = k;
+    if (k == 0) return;
+    out.sigma.resize(static_cast<size_t>(k));
+    std::vector<double> inv(static_cast<size_t>(k));
+    for (i64 j = 0; j < k; ++j) {
+        const double s = sig[static_cast<size_t>(perm[static_cast<size_t>(j)])];
+        out.sigma[static_cast<size_t>(j)] = s;
+        inv[static_cast<size_t>(j)] = (s > 0.0) ? 1.0 / s : 0.0;
+    }
+    E.perm.ensure(static_cast<size_t>(k));
+    out.d_sigma.ensure(static_cast<size_t>(2 * k));
+    SVT_CUDA(cudaMemcpyAsync(E.perm.get(), perm.data(), sizeof(int) * k, cudaMemcpyHostToDevice, c->stream));
+    SVT_CUDA(cudaMemcpyAsync(out.d_sigma.get(), out.sigma.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
+                             c->stream));
+    SVT_CUDA(cudaMemcpyAsync(out.d_sigma.get() + k, inv.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
+                             c->stream));
+    // V = (B^T W)[:, perm] / sigma
+    out.V.ensure(static_cast<size_t>(n * k));
+    permute_cols(c, E.Vraw.get(), n, kc, E.perm.get(), k, out.V.get(), k);
+    scale_cols(c, out.V.get(), n, k, k, out.d_sigma.get() + k);
+    // U = Q W[:, perm]
+    E.Wk.ensure(static_cast<size_t>(r * k));
+    permute_cols(c, E.W.get(), r, r, E.perm.get(), k, E.Wk.get(), k);
+    out.U.ensure(static_cast<size_t>(std::max<i64>(1, m) * k));
+    gemm(c, K_FINAL, false, m, k, r, 1.0, st.Q.get(), st.cap, E.Wk.get(), k, 0.0, out.U.get(), k);
+    // keep the host copy of sigma in sync with the stream (the inv upload
+    // above reads a host vector that dies with this frame)
+    SVT_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+static double error_percentage(const QBDev& st) {
+    if (!(st.frob_y_sq > 0.0)) throw std::domain_error("error_percentage: target has zero Frobenius norm");
+    const double eps = (st.frob_y_sq - st.norm_b_sq) / st.frob_y_sq;
+    return std::clamp(eps, 0.0, 1.0);
+}
+
+static void check_sketch_params(const svt_sketch_params& p) {
+    if (p.t < 1 || p.dt < 1 || p.np < 0) throw std::invalid_argument("SketchParams: need t >= 1, dt >= 1, np >= 0");
+    if (!(p.eps_threshold > 0.0 && p.eps_threshold < 1.0))
+        throw std::invalid_argument("SketchParams: eps_threshold must lie in (0, 1)");
+}
+
+static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, FinalizeMode mode, double tau) {
+    SketchOut out;
+    int rounds = 0;
+    while (error_percentage(st) > p.eps_threshold) {
+        if (st.saturated) {
+            finalize(E, st, mode, tau, out.f);
+            out.rank = st.rank;
+            out.saturated = true;
+            out.rounds = rounds;
+            return out;
+        }
+        ++rounds;
+        qb_extend(E, st, p.dt, p.np, derive_seed_u(p.seed, static_cast<u64>(rounds)));
+    }
+    finalize(E, st, mode, tau, out.f);
+    out.rank = st.rank;
+    out.saturated = false;
+    out.rounds = rounds;
+    return out;
+}
+
+// sketch.hpp:188-201
+SketchOut r3svd(Engine& E, const svt_sketch_params& p, FinalizeMode mode, double tau, double frob_y_sq) {
+    check_sketch_params(p);
+    QBDev st;
+    qb_init(E, st, p.t, p.np, derive_seed_u(p.seed, 0), frob_y_sq);
+    return run_loop(E, st, p, mode, tau);
+}
+
+// sketch.hpp:207-250
+SketchOut r4svd(Engine& E, const double* U_prev, i64 ldu, i64 s, const svt_sketch_params& p, FinalizeMode mode,
+                double tau, double frob_y_sq) {
+    check_sketch_params(p);
+    if (s == 0) {
+        svt_sketch_params fresh = p;
+        fresh.t = p.dt;
+        return r3svd(E, fresh, mode, tau, frob_y_sq);
+    }
+    svt_ctx* c = E.ctx;
+    svt_mat* A = E.mat;
+    const i64 min_dim = std::min(A->m, A->n);
+    if (s > min_dim) throw std::invalid_argument("r4svd: recycled basis wider than min(m, n)");
+    if (frob_y_sq < 0.0) frob_y_sq = frob_sq(E);
+    if (!(frob_y_sq > 0.0)) throw std::domain_error("r4svd: target matrix is all zero");
+    const i64 m = A->m_local;
+    QBDev st;
+    st.m_local = m;
+    st.n = A->n;
+    st.min_dim = min_dim;
+    ensure_cap(E, st, s);
+    copy2d(c, U_prev, ldu, st.Q.get(), st.cap, m, s);
+    // drift test max|U^T U - I| > 1e-8 -> qr_orthonormal (sketch.hpp:229-233)
+    E.D.ensure(static_cast<size_t>(s * s));
+    gemm(c, K_GEMM, true, s, s, m, 1.0, st.Q.get(), st.cap, st.Q.get(), st.cap, 0.0, E.D.get(), s);
+    allreduce(c, E.D.get(), static_cast<size_t>(s * s));
+    maxabs(c, E.D.get(), s, s, s, 1.0, dsc(c, S_MAXD));
+    set_flag(c, dsc(c, S_MAXD), nullptr, 1e-8, 1, dfl(c, F_DRIFT));
+    if (s <= 64) {
+        E.X2.ensure(static_cast<size_t>(std::max<i64>(1, m) * s));
+        copy2d(c, U_prev, ldu, E.X2.get(), s, m, s, dfl(c, F_DRIFT));
+        qr_panel(E, E.X2.get(), s, s, st.Q.get(), st.cap, dfl(c, F_DRIFT));
+    } else if (read_flag(c, F_DRIFT)) {
+        E.X2.ensure(static_cast<size_t>(std::max<i64>(1, m) * s));
+        copy2d(c, U_prev, ldu, E.X2.get(), s, m, s);
+        qr_orthonormal(E, E.X2.get(), s, s, st.Q.get(), st.cap);
+    }
+    append_coefficients(E, st, 0, s, 0);
+    st.norm_b_sq = read_scalar(c, S_NB);
+    st.frob_y_sq = frob_y_sq;
+    st.rank = s;
+    st.saturated = (s == min_dim);
+    return run_loop(E, st, p, mode, tau);
+}
+
+// sketch.hpp:165-182
+DevFactors rsvd(Engine& E, i64 k, const svt_sketch_params& p) {
+    svt_mat* A = E.mat;
+    const i64 min_dim = std::min(A->m, A->n);
+    if (k < 1) throw std::invalid_argument("rsvd: k must be >= 1");
+    if (p.p < 0 || k + p.p > min_dim) throw std::invalid_argument("rsvd: k + p must not exceed min(m, n)");
+    QBDev st;
+    // same kernels as qb_init (sketch.hpp:173-176), no zero-norm check
+    const i64 t = k + p.p;
+    st.m_local = A->m_local;
+    st.n = A->n;
+    st.min_dim = min_dim;
+    ensure_cap(E, st, t);
+    const i64 m = A->m_local;
+    E.Om.ensure(static_cast<size_t>(A->n * t));
+    E.X.ensure(static_cast<size_t>(std::max<i64>(1, m) * t));
+    gaussian_block_dev(E.ctx, A->n, t, derive_seed_u(p.seed, 0), E.Om.get(), t);
+    sp_mult(E, t, E.Om.get(), t, E.X.get(), t);
+    power_iterate(E, t, p.np);
+    qr_orthonormal(E, E.X.get(), t, t, st.Q.get(), st.cap);
+    append_coefficients(E, st, 0, t, 0);
+    st.rank = t;
+    DevFactors f;
+    finalize(E, st, FinalizeMode::Full, 0.0, f);
+    // keep the leading k triplets
+    if (f.k > k) {
+        DevFactors g;
+        g.m_local = f.m_local;
+        g.n = f.n;
+        g.k = k;
+        g.sigma.assign(f.sigma.begin(), f.sigma.begin() + k);
+        g.U.ensure(static_cast<size_t>(std::max<i64>(1, f.m_local) * k));
+        g.V.ensure(static_cast<size_t>(f.n * k));
+        g.d_sigma.ensure(static_cast<size_t>(2 * k));
+        copy2d(E.ctx, f.U.get(), f.k, g.U.get(), k, f.m_local, k);
+        copy2d(E.ctx, f.V.get(), f.k, g.V.get(), k, f.n, k);
+        SVT_CUDA(cudaMemcpyAsync(g.d_sigma.get(), f.d_sigma.get(), sizeof(double) * k, cudaMemcpyDeviceToDevice,
+                                 E.ctx->stream));
+        SVT_CUDA(cudaStreamSynchronize(E.ctx->stream));
+        return g;
+    }
+    return f;
+}
+
+// Full SVD of the densified iterate (solver.hpp:271-274): Q = I (m x m), B = Y.
+DevFactors full_svd(Engine& E) {
+    svt_ctx* c = E.ctx;
+    svt_mat* A = E.mat;
+    if (c->comm.world != 1) throw std::invalid_argument("full-svd backend is single-GPU only");
+    QBDev st;
+    st.m_local = A->m;
+    st.n = A->n;
+    st.min_dim = std::min(A->m, A->n);
+    st.cap = A->m;
+    st.rank = A->m;
+    st.Q.ensure(static_cast<size_t>(A->m * A->m));
+    fill(c, st.Q.get(), A->m * A->m, 0.0);
+    std::vector<double> eye(static_cast<size_t>(A->m * A->m), 0.0);
+    for (i64 i = 0; i < A->m; ++i) eye[static_cast<size_t>(i * A->m + i)] = 1.0;
+    SVT_CUDA(cudaMemcpyAsync(st.Q.get(), eye.data(), sizeof(double) * eye.size(), cudaMemcpyHostToDevice, c->stream));
+    DevBuf<double> dense(static_cast<size_t>(A->m * A->n));
+    densify_dev(c, A->m, A->n, A->rowptr.get(), A->col.get(), E.Y.csr, dense.get());
+    st.Bt.ensure(static_cast<size_t>(A->n * A->m));
+    transpose(c, dense.get(), A->m, A->n, A->n, st.Bt.get());
+    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    DevFactors f;
+    finalize(E, st, FinalizeMode::Full, 0.0, f);
+    return f;
+}
+
+}  // namespace svtb

@@ -1,0 +1,134 @@
+// The B200 engine behind the C ABI: device sample sets, the QB state, the
+// R3SVD / R4SVD rank-revealing loops (host control, device data) and the SVT
+// Bregman iteration (solver.hpp:215-328).
+#pragma once
+
+#include <limits>
+#include <memory>
+#include <vector>
+
+#include "../../include/svt_b200.h"
+#include "common.hpp"
+
+// Device SampledMatrix (sampled.hpp:25-110): this rank's row block as CSR
+// (int64 rowptr, int32 col, fp64 val) plus a CSC view whose value array
+// mirrors the CSR values through csr2csc.
+struct svt_mat {
+    svt_ctx* ctx = nullptr;
+    svtb::i64 m = 0, n = 0, row_begin = 0, row_end = 0, m_local = 0, nnz_local = 0, nnz_global = 0;
+    svtb::DevBuf<svtb::i64> rowptr;
+    svtb::DevBuf<int> col;
+    svtb::DevBuf<double> val;
+    svtb::DevBuf<svtb::i64> colptr;
+    svtb::DevBuf<int> cscrow;
+    svtb::DevBuf<double> val_csc;
+    svtb::DevBuf<int> csr2csc;
+};
+
+namespace svtb {
+
+// A value array on a matrix's pattern (CSR order + CSC mirror).
+struct Vals {
+    double* csr;
+    double* csc;
+};
+
+// Device factors U (m_local x k), sigma (k), V (n x k), row-major.
+struct DevFactors {
+    i64 m_local = 0, n = 0, k = 0;
+    DevBuf<double> U, V;
+    std::vector<double> sigma;
+    DevBuf<double> d_sigma;
+};
+
+// QBState (sketch.hpp:32-39) with capacity-preallocated Q (m_local x cap) and
+// B^T (n x cap), both row-major with ld = cap; appending a block is a
+// pointer offset (no conservativeResize copy, sketch.hpp:145-152).
+struct QBDev {
+    i64 m_local = 0, n = 0, min_dim = 0, cap = 0, rank = 0;
+    DevBuf<double> Q, Bt;
+    double norm_b_sq = 0.0;
+    double frob_y_sq = 0.0;
+    bool saturated = false;
+};
+
+enum class FinalizeMode { Full, Kept };
+
+struct SketchOut {
+    DevFactors f;
+    i64 rank = 0;
+    bool saturated = false;
+    int rounds = 0;
+};
+
+// Per-context reusable workspaces of the sketch engines.
+struct Engine {
+    svt_ctx* ctx;
+    svt_mat* mat;  // pattern of the target
+    Vals Y;
+    DevBuf<double> Om, X, X2, P, T, C, D, G, Rinv, hh, tmp, W, lam, Vraw, Wk;
+    DevBuf<int> perm;
+    Engine(svt_ctx* c, svt_mat* m, Vals y) : ctx(c), mat(m), Y(y) {}
+};
+
+// primitives
+double frob_sq(Engine& E);  // ||Y||_F^2 (all ranks)
+void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo);          // Y X (local rows)
+void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out /* n x w, ld w */);  // Y^T X (allreduced)
+void qr_orthonormal(Engine& E, double* X, i64 ldx, i64 w, double* Qout, i64 ldq);            // dense.hpp:103
+double spectral_norm_est(Engine& E, int iters, u64 seed);                                   // sampled.hpp:188
+
+// sketch.hpp
+void qb_init(Engine& E, QBDev& st, i64 t, int np, u64 seed, double frob_y_sq = -1.0);
+void qb_extend(Engine& E, QBDev& st, i64 dt, int np, u64 seed);
+void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFactors& out);
+SketchOut r3svd(Engine& E, const svt_sketch_params& p, FinalizeMode mode, double tau, double frob_y_sq = -1.0);
+SketchOut r4svd(Engine& E, const double* U_prev, i64 ldu, i64 s, const svt_sketch_params& p, FinalizeMode mode,
+                double tau, double frob_y_sq = -1.0);
+DevFactors rsvd(Engine& E, i64 k, const svt_sketch_params& p);
+DevFactors full_svd(Engine& E);
+
+u64 derive_seed_u(u64 seed, u64 stream);
+
+}  // namespace svtb
+
+struct svt_factors {
+    svtb::DevFactors f;
+    svtb::i64 rank = 0;
+    int saturated = 0;
+    int rounds = 0;
+};
+
+struct svt_result {
+    std::vector<svt_record> trace;
+    svtb::i64 m_local = 0, n = 0, k = 0;
+    std::vector<double> U, sigma, V;  // column-major host copies
+    int converged = 0;
+};
+
+struct svt_solver {
+    svt_ctx* ctx = nullptr;
+    svt_mat* A = nullptr;
+    svt_mat* test = nullptr;
+    svt_config cfg{};
+    svt_stop stop{};
+    svt_backend backend{};
+    svtb::DevBuf<double> Ycsr, Ycsc;
+    svtb::DevFactors X;          // current shrunk factors (U, sigma - tau, V)
+    svtb::DevFactors best;       // best-so-far
+    svtb::DevBuf<double> U_prev;  // recycled basis (m_local x s)
+    svtb::i64 s = 0;
+    svtb::DevBuf<double> Vs;  // V diag(sigma - tau)
+    double eps_threshold = 0.0;
+    double eps_min = std::numeric_limits<double>::infinity();
+    double best_metric = std::numeric_limits<double>::infinity();
+    double frob_a = 0.0;
+    double frob_y_sq = -1.0;
+    double t_start_ms = 0.0;
+    int iter = 0;
+    bool done = false;
+    bool converged = false;
+    bool result_is_current = false;
+    std::vector<svt_record> trace;
+    std::unique_ptr<svtb::Engine> engine;
+};

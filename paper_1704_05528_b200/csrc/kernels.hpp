@@ -1,0 +1,92 @@
+// Host-side launchers of the sm_100a kernels (rng.cu, sparse.cu, dense.cu).
+// All run on ctx->stream; none synchronizes.  Dense "panels" are ROW-MAJOR
+// (element (i, j) at p[i * ld + j]) so that a sparse row gather reads one
+// contiguous w-wide row; the C ABI converts to/from the reference's
+// column-major Eigen layout at the boundary.
+#pragma once
+
+#include "common.hpp"
+
+namespace svtb {
+
+// ---- RNG (dense.hpp:52-98) ---------------------------------------------
+// out (rows x cols, row-major, leading dim ld) <- the column-major fill of one
+// fresh std::mt19937_64(seed) Box-Muller stream: out[i*ld + j] = z[i + j*rows].
+void gaussian_block_dev(svt_ctx* ctx, i64 rows, i64 cols, u64 seed, double* out, i64 ld);
+
+// ---- sparse (sampled.hpp) ---------------------------------------------------
+// out[i, 0:w] = sum_{k in ptr[i]..ptr[i+1]} val[k] * X[idx[k], 0:w], i < nrows.
+// CSR (Y*X, sampled.hpp:113) and CSC (Y^T*X, sampled.hpp:130) use the same
+// kernel with the respective arrays.
+// nnz and x_rows only feed the algorithmic-bytes accounting (SURVEY §8d:
+// 12 B per entry + 8 B per row pointer + panel in + panel out).
+void spmm(svt_ctx* ctx, int cls, i64 nrows, const i64* ptr, const int* idx, const double* val, i64 nnz, i64 x_rows,
+          i64 w, const double* X, i64 ldx, double* out, i64 ldo);
+
+// Fused SDDMM + Bregman update + reductions (sampled.hpp:148-176,
+// solver.hpp:143-168, 321-323).  For each stored (i, j):
+//   p = U[i,:] . Vs[j,:]   (Vs = V diag(sigma))
+//   d = A - p;  y_old = Y;
+//   mode 1: Y = y_old + delta * d (and the Ycsc mirror)   [Bregman update]
+//   mode 2: Y = p                                          [project_low_rank]
+//   mode 0: no write                                       [held-out metrics]
+// sums[0..3] (device) = sum|d|, sum d^2, sum (A - y_old)^2, sum Y_out^2.
+void sddmm_update(svt_ctx* ctx, i64 m_local, const i64* rowptr, const int* col, const double* A, double* Y,
+                  double* Ycsc, const int* csr2csc, i64 nnz, i64 n, const double* U, i64 ldu, const double* Vs,
+                  i64 ldv, i64 k, double delta, int mode, double* d_sums4);
+
+// vals_out = alpha * vals_in (and the CSC mirror through csr2csc when given)
+void scale_values(svt_ctx* ctx, i64 nnz, const double* in, double alpha, double* out, const int* csr2csc,
+                  double* out_csc);
+// out[k] = a[k] + alpha * b[k]
+void axpy_values(svt_ctx* ctx, i64 nnz, const double* a, double alpha, const double* b, double* out);
+// dense (m_local x n, row-major) <- scatter of CSR values (FullSvd backend)
+void densify_dev(svt_ctx* ctx, i64 m_local, i64 n, const i64* rowptr, const int* col, const double* val,
+                 double* out);
+
+// ---- dense ------------------------------------------------------------------
+// C (M x N) = alpha * op(A) * B + beta * C; op(A) = A^T when transA (A stored
+// K x M row-major), else A (M x K row-major).  B is K x N row-major.  Large K
+// with a small output is split across CTAs with a deterministic fixed-order
+// reduction.  pred (device int, may be null): skip entirely when *pred == 0.
+void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+          const double* B, i64 ldb, double beta, double* C, i64 ldc, const int* pred = nullptr);
+
+// d_out[0] (op) sum of squares of X (rows x cols, ld).  op: 0 store, 1 add.
+void sumsq(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double* d_out, int op,
+           const int* pred = nullptr);
+// d_out[0] = max |X - I*diag_shift| over the rows x cols block (diag_shift 0 or 1)
+void maxabs(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double diag_shift, double* d_out);
+// flag[0] = (sqrt(a[0]) > coef * sqrt(b[0]))  (sumsq inputs)  when mode 0
+// flag[0] = (a[0] > coef)                                    when mode 1
+void set_flag(svt_ctx* ctx, const double* a, const double* b, double coef, int mode, int* flag);
+
+// Single-CTA Cholesky of the w x w Gram G (w <= 64): Rinv = L^{-T} (upper,
+// row-major, w x w).  status[0] = 1 when a pivot is not safely positive
+// (triggers the Householder fallback).  Skipped when *pred == 0.
+void chol_rinv(svt_ctx* ctx, const double* G, i64 w, double* Rinv, int* status, const int* pred);
+// Householder QR fallback (Eigen convention, all columns kept), single CTA,
+// w <= 64: Q (m x w, ldq) from X (m x w, ldx).  Runs only when
+// (pred == null || *pred) && (status == null || *status).
+void householder_qr(svt_ctx* ctx, const double* X, i64 m, i64 w, i64 ldx, double* Q, i64 ldq, double* work,
+                    const int* pred, const int* status);
+
+// Symmetric eigen-decomposition of the r x r Gram (row-major, overwritten):
+// W (r x r row-major, column j = eigenvector j), lambda descending.
+void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda);
+
+// column norms: out[j] = ||X[:, j]||^2 for j < cols
+void col_sumsq(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double* out);
+// X[:, j] *= s[j]  (s on device)
+void scale_cols(svt_ctx* ctx, double* X, i64 rows, i64 cols, i64 ld, const double* s);
+// dst (rows x cols, ldd) <- src (rows x cols, lds), optionally predicated
+void copy2d(svt_ctx* ctx, const double* src, i64 lds, double* dst, i64 ldd, i64 rows, i64 cols,
+            const int* pred = nullptr);
+void fill(svt_ctx* ctx, double* p, i64 n, double v);
+// out (cols x rows) = in^T ; in (rows x cols, ldi) ; out ld = rows
+void transpose(svt_ctx* ctx, const double* in, i64 rows, i64 cols, i64 ldi, double* out);
+// W2[:, j] = W[:, perm[j]] for j < kcols (perm on device, int)
+void permute_cols(svt_ctx* ctx, const double* W, i64 rows, i64 ldw, const int* perm, i64 kcols, double* W2,
+                  i64 ldw2);
+
+}  // namespace svtb

@@ -1,0 +1,154 @@
+// Device Gaussian sketch generator: a bit-exact std::mt19937_64 integer stream
+// (the C++ standard fixes every output) followed by the reference's explicit
+// Box-Muller transform, dense.hpp:52-98.
+//
+// Stage 1 (mt_twist_kernel): one warp owns the 312-word state in shared
+// memory and runs the twist as two data-parallel halves (words 0..155 read
+// only old words; words 156..311 read the new words 0..155), then tempers and
+// streams the raw 64-bit draws to HBM.  The state persists in global memory
+// between chunks, so arbitrarily long streams (qb_init at t0 = 5000 needs
+// 5e8 draws) are produced in bounded scratch.
+// Stage 2 (box_muller_kernel): grid-wide; pair p consumes draws 2p (u1 = 1-u)
+// and 2p+1 (u2), emits r*cos (normal 2p) and r*sin (normal 2p+1, the
+// reference's "spare"), scattered to the column-major fill position of the
+// row-major output panel.  log/sqrt/sin/cos are the CUDA double-precision
+// functions (<= 1-2 ulp from glibc; the integer stream is identical).
+#include "common.hpp"
+#include "kernels.hpp"
+
+namespace svtb {
+
+namespace {
+
+constexpr int MT_N = 312;
+constexpr int MT_M = 156;
+constexpr unsigned long long MT_A = 0xB5026F5AA96619E9ULL;
+constexpr unsigned long long MT_UM = 0xFFFFFFFF80000000ULL;
+constexpr unsigned long long MT_LM = 0x7FFFFFFFULL;
+
+__device__ __forceinline__ unsigned long long temper(unsigned long long y) {
+    y ^= (y >> 29) & 0x5555555555555555ULL;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+    y ^= (y >> 43);
+    return y;
+}
+
+__device__ __forceinline__ unsigned long long twist_word(unsigned long long cur, unsigned long long nxt,
+                                                         unsigned long long far) {
+    const unsigned long long x = (cur & MT_UM) | (nxt & MT_LM);
+    unsigned long long xa = x >> 1;
+    if (x & 1ULL) xa ^= MT_A;
+    return far ^ xa;
+}
+
+// One warp.  init != 0: seed the state (std::mt19937_64 seeding recurrence,
+// f = 6364136223846793005).  Generates ntwists * 312 draws into out.
+__global__ void __launch_bounds__(32) mt_twist_kernel(unsigned long long seed, int init,
+                                                      unsigned long long* state, long long ntwists,
+                                                      unsigned long long* out) {
+    __shared__ unsigned long long mt[MT_N];
+    const int lane = threadIdx.x;
+    if (init) {
+        if (lane == 0) {
+            unsigned long long x = seed;
+            mt[0] = x;
+            for (int i = 1; i < MT_N; ++i) {
+                x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<unsigned long long>(i);
+                mt[i] = x;
+            }
+        }
+    } else {
+        for (int i = lane; i < MT_N; i += 32) mt[i] = state[i];
+    }
+    __syncwarp();
+    for (long long t = 0; t < ntwists; ++t) {
+        // phase 1: words 0..155 (read all inputs, then write)
+        unsigned long long v[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int i = lane + 32 * q;
+            if (i < MT_M) v[q] = twist_word(mt[i], mt[i + 1], mt[i + MT_M]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int i = lane + 32 * q;
+            if (i < MT_M) mt[i] = v[q];
+        }
+        __syncwarp();
+        // phase 2: words 156..311 (word 311 reads the new word 0)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int i = MT_M + lane + 32 * q;
+            if (i < MT_N) v[q] = twist_word(mt[i], mt[(i + 1) % MT_N], mt[i - MT_M]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int i = MT_M + lane + 32 * q;
+            if (i < MT_N) mt[i] = v[q];
+        }
+        __syncwarp();
+        unsigned long long* o = out + t * MT_N;
+#pragma unroll
+        for (int q = 0; q < 10; ++q) {
+            const int i = lane + 32 * q;
+            if (i < MT_N) o[i] = temper(mt[i]);
+        }
+    }
+    __syncwarp();
+    for (int i = lane; i < MT_N; i += 32) state[i] = mt[i];
+}
+
+// pairs [0, npairs) of this chunk; global normal index q = 2*(pair0 + p) + {0,1}
+__global__ void box_muller_kernel(const unsigned long long* __restrict__ draws, long long npairs, long long pair0,
+                                  long long rows, long long total, double* __restrict__ out, long long ld) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p >= npairs) return;
+    const unsigned long long a = draws[2 * p];
+    const unsigned long long b = draws[2 * p + 1];
+    const double u1 = 1.0 - static_cast<double>(a >> 11) * 0x1.0p-53;
+    const double u2 = static_cast<double>(b >> 11) * 0x1.0p-53;
+    const double radius = sqrt(-2.0 * log(u1));
+    const double angle = 2.0 * 3.14159265358979323846 * u2;
+    const long long q0 = 2 * (pair0 + p);
+    const double z0 = radius * cos(angle);
+    const double z1 = radius * sin(angle);
+    if (q0 < total) out[(q0 % rows) * ld + q0 / rows] = z0;
+    if (q0 + 1 < total) out[((q0 + 1) % rows) * ld + (q0 + 1) / rows] = z1;
+}
+
+}  // namespace
+
+void gaussian_block_dev(svt_ctx* ctx, i64 rows, i64 cols, u64 seed, double* out, i64 ld) {
+    if (rows < 1 || cols < 1) throw std::invalid_argument("gaussian_block: dimensions must be >= 1");
+    const i64 total = rows * cols;
+    const i64 pairs_needed = (total + 1) / 2;
+    const i64 twists_needed = (2 * pairs_needed + MT_N - 1) / MT_N;
+    const i64 max_twists_per_chunk = 16384;  // 5.1M draws, 40 MB scratch
+    const i64 chunk_twists = std::min<i64>(twists_needed, max_twists_per_chunk);
+    ctx->ws_rng.ensure(static_cast<size_t>(chunk_twists * MT_N));
+    ctx->ws_mt.ensure(MT_N);
+    i64 done_twists = 0;
+    bool first = true;
+    while (done_twists < twists_needed) {
+        const i64 nt = std::min<i64>(chunk_twists, twists_needed - done_twists);
+        {
+            LaunchScope ls(ctx, K_RNG, nt * MT_N * 8.0, 0.0);
+            mt_twist_kernel<<<1, 32, 0, ctx->stream>>>(seed, first ? 1 : 0, ctx->ws_mt.get(), nt, ctx->ws_rng.get());
+        }
+        first = false;
+        const i64 pair0 = done_twists * MT_N / 2;
+        const i64 npairs = std::min<i64>(nt * MT_N / 2, pairs_needed - pair0);
+        if (npairs > 0) {
+            LaunchScope ls(ctx, K_RNG, npairs * 2 * 8.0 + npairs * 2 * 8.0, 0.0);
+            const int bs = 256;
+            box_muller_kernel<<<static_cast<unsigned>((npairs + bs - 1) / bs), bs, 0, ctx->stream>>>(
+                ctx->ws_rng.get(), npairs, pair0, rows, total, out, ld);
+        }
+        done_twists += nt;
+    }
+}
+
+}  // namespace svtb

@@ -1,0 +1,141 @@
+// Context runtime: launch accounting / CUDA-event instrumentation and the
+// NCCL communicator (resolved with dlopen so single-GPU use never needs it).
+#include <dlfcn.h>
+
+#include <cstring>
+
+#include "common.hpp"
+
+namespace svtb {
+
+LaunchScope::LaunchScope(svt_ctx* c, int k, double bytes, double flops) : ctx(c), cls(k) {
+    ctx->launch_count++;
+    KStats& s = ctx->stats[k];
+    s.launches++;
+    s.bytes += bytes;
+    s.flops += flops;
+    if (ctx->profiling) {
+        if (ctx->event_pool.size() < 2) {
+            for (int i = 0; i < 64; ++i) {
+                cudaEvent_t e;
+                SVT_CUDA(cudaEventCreate(&e));
+                ctx->event_pool.push_back(e);
+            }
+        }
+        a = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+        b = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+        SVT_CUDA(cudaEventRecord(a, ctx->stream));
+    }
+}
+
+LaunchScope::~LaunchScope() noexcept(false) {
+    cudaError_t e = cudaGetLastError();
+    if (a != nullptr) {
+        cudaEventRecord(b, ctx->stream);
+        ctx->pending.push_back({a, b, cls});
+        if (ctx->pending.size() > 4096) flush_stats(ctx);
+    }
+    if (e != cudaSuccess && std::uncaught_exceptions() == 0)
+        throw cuda_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
+}
+
+void flush_stats(svt_ctx* ctx) {
+    if (ctx->pending.empty()) return;
+    SVT_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (auto& p : ctx->pending) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) ctx->stats[p.cls].total_ms += ms;
+        ctx->event_pool.push_back(p.a);
+        ctx->event_pool.push_back(p.b);
+    }
+    ctx->pending.clear();
+}
+
+// ---------------------------------------------------------------------------
+// NCCL through dlopen
+// ---------------------------------------------------------------------------
+namespace {
+
+typedef int ncclResult_t_;
+typedef void* ncclComm_t_;
+struct NcclApi {
+    void* h = nullptr;
+    ncclResult_t_ (*GetUniqueId)(void*) = nullptr;
+    ncclResult_t_ (*CommInitRank)(ncclComm_t_*, int, /*ncclUniqueId by value*/ ...) = nullptr;
+    ncclResult_t_ (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t_, cudaStream_t) = nullptr;
+    ncclResult_t_ (*CommDestroy)(ncclComm_t_) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t_) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    if (api.h == nullptr) {
+        const char* names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char* n : names) {
+            api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+            if (api.h) break;
+        }
+        if (api.h == nullptr) throw nccl_error("libnccl.so.2 not loadable (multi-GPU needs NCCL)");
+        api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(dlsym(api.h, "ncclGetUniqueId"));
+        api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(dlsym(api.h, "ncclAllReduce"));
+        api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(api.h, "ncclCommDestroy"));
+        api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(api.h, "ncclGetErrorString"));
+        if (!api.GetUniqueId || !api.AllReduce || !api.CommDestroy)
+            throw nccl_error("libnccl.so.2 is missing required symbols");
+    }
+    return api;
+}
+
+struct UniqueId {
+    char internal[128];
+};
+
+constexpr int kNcclFloat64 = 8;  // ncclDouble
+constexpr int kNcclInt32 = 2;    // ncclInt32
+constexpr int kNcclSum = 0;
+
+void check(ncclResult_t_ r, const char* what) {
+    if (r != 0) {
+        const char* msg = nccl().GetErrorString ? nccl().GetErrorString(r) : "?";
+        throw nccl_error(std::string(what) + ": " + msg);
+    }
+}
+
+}  // namespace
+
+void nccl_unique_id(void* out128) { check(nccl().GetUniqueId(out128), "ncclGetUniqueId"); }
+
+void nccl_init(Comm& c, int rank, int world, const void* id128) {
+    c.rank = rank;
+    c.world = world;
+    if (world <= 1) return;
+    auto fn = reinterpret_cast<ncclResult_t_ (*)(ncclComm_t_*, int, UniqueId, int)>(
+        dlsym(nccl().h, "ncclCommInitRank"));
+    if (!fn) throw nccl_error("ncclCommInitRank missing");
+    UniqueId id;
+    std::memcpy(id.internal, id128, 128);
+    ncclComm_t_ comm = nullptr;
+    check(fn(&comm, world, id, rank), "ncclCommInitRank");
+    c.handle = comm;
+}
+
+void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t s) {
+    if (world <= 1 || count == 0) return;
+    check(svtb::nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, handle, s), "ncclAllReduce");
+}
+
+void Comm::allreduce_sum_i32(int* buf, size_t count, cudaStream_t s) {
+    if (world <= 1 || count == 0) return;
+    check(svtb::nccl().AllReduce(buf, buf, count, kNcclInt32, kNcclSum, handle, s), "ncclAllReduce");
+}
+
+void Comm::destroy() {
+    if (handle != nullptr) {
+        svtb::nccl().CommDestroy(handle);
+        handle = nullptr;
+    }
+}
+
+}  // namespace svtb

@@ -1,0 +1,273 @@
+// Sparse kernels on the sample set Lambda (sampled.hpp).
+//
+// Storage (per rank, its row block): CSR rowptr int64 / col int32 / val fp64,
+// plus a CSC view (colptr int64 / local row int32) whose value array is a
+// mirror of the CSR values kept in sync through csr2csc.  Y*X runs over CSR
+// and Y^T*X over CSC with the SAME gather kernel, so both are deterministic
+// (no atomics) — the reference's single-threaded results are reproducible
+// run-to-run (SPEC: bit-reproducible single-thread runs).
+//
+// Narrow panels (w <= 16, the dt = 10 rank-revealing rounds): one warp per
+// output row, one stored entry per lane, w register accumulators, warp-shuffle
+// tree reduction.  The w-wide dense row of an entry is one contiguous 8w-byte
+// gather (row-major panel), read through the read-only path; the panel is
+// L2-resident (n x 10 doubles = 8 MB at n = 1e5).
+// Wide panels (qb_init at t0 up to 5000): one warp per (row, 128-column
+// chunk); entries are broadcast 32 at a time by shuffle, lanes stride the
+// contiguous panel row (1 KB coalesced per entry).
+#include "common.hpp"
+#include "kernels.hpp"
+
+namespace svtb {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <int W>
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) spmm_narrow_kernel(
+    long long nrows, const long long* __restrict__ ptr, const int* __restrict__ idx, const double* __restrict__ val,
+    const double* __restrict__ X, long long ldx, double* __restrict__ out, long long ldo) {
+    const int lane = threadIdx.x & 31;
+    const long long row = static_cast<long long>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (row >= nrows) return;
+    double acc[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) acc[j] = 0.0;
+    const long long beg = ptr[row], end = ptr[row + 1];
+    for (long long k = beg + lane; k < end; k += 32) {
+        const int c = __ldg(idx + k);
+        const double v = __ldg(val + k);
+        const double* xr = X + static_cast<long long>(c) * ldx;
+#pragma unroll
+        for (int j = 0; j < W; ++j) acc[j] = fma(v, __ldg(xr + j), acc[j]);
+    }
+    double mine = 0.0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        const double s = warp_sum(acc[j]);
+        if (lane == j) mine = s;
+    }
+    if (lane < W) out[row * ldo + lane] = mine;
+}
+
+// wide: block = 4 warps, each warp one row, 128 columns (4 per lane) at
+// column chunk blockIdx.y
+__global__ void __launch_bounds__(128) spmm_wide_kernel(long long nrows, const long long* __restrict__ ptr,
+                                                        const int* __restrict__ idx,
+                                                        const double* __restrict__ val,
+                                                        const double* __restrict__ X, long long ldx, long long w,
+                                                        double* __restrict__ out, long long ldo) {
+    const int lane = threadIdx.x & 31;
+    const long long row = static_cast<long long>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+    if (row >= nrows) return;
+    const long long c0 = static_cast<long long>(blockIdx.y) * 128;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const long long beg = ptr[row], end = ptr[row + 1];
+    for (long long k0 = beg; k0 < end; k0 += 32) {
+        const long long k = k0 + lane;
+        int cl = 0;
+        double vl = 0.0;
+        if (k < end) {
+            cl = __ldg(idx + k);
+            vl = __ldg(val + k);
+        }
+        const int cnt = static_cast<int>(min(32LL, end - k0));
+        for (int e = 0; e < cnt; ++e) {
+            const int c = __shfl_sync(0xffffffffu, cl, e);
+            const double v = __shfl_sync(0xffffffffu, vl, e);
+            const double* xr = X + static_cast<long long>(c) * ldx + c0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const long long j = lane + 32 * q;
+                if (c0 + j < w) acc[q] = fma(v, __ldg(xr + j), acc[q]);
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const long long j = c0 + lane + 32 * q;
+        if (j < w) out[row * ldo + j] = acc[q];
+    }
+}
+
+template <int W>
+void launch_narrow(svt_ctx* ctx, i64 nrows, const i64* ptr, const int* idx, const double* val, const double* X,
+                   i64 ldx, double* out, i64 ldo) {
+    const unsigned blocks = static_cast<unsigned>((nrows + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    spmm_narrow_kernel<W><<<blocks, 32 * kWarpsPerBlock, 0, ctx->stream>>>(
+        nrows, reinterpret_cast<const long long*>(ptr), idx, val, X, ldx, out, ldo);
+}
+
+// ---- fused SDDMM + Bregman update + reductions ------------------------------
+constexpr int kSddmmWarps = 8;
+
+__global__ void __launch_bounds__(32 * kSddmmWarps) sddmm_update_kernel(
+    long long m_local, const long long* __restrict__ rowptr, const int* __restrict__ col,
+    const double* __restrict__ A, double* __restrict__ Y, double* __restrict__ Ycsc,
+    const int* __restrict__ csr2csc, const double* __restrict__ U, long long ldu, const double* __restrict__ Vs,
+    long long ldv, long long k, double delta, int mode, double* __restrict__ partials) {
+    __shared__ double red[kSddmmWarps][4];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    double s_abs = 0.0, s_sq = 0.0, s_res = 0.0, s_y = 0.0;
+    // grid-stride over rows, one warp per row
+    for (long long row = static_cast<long long>(blockIdx.x) * kSddmmWarps + warp; row < m_local;
+         row += static_cast<long long>(gridDim.x) * kSddmmWarps) {
+        const long long beg = rowptr[row], end = rowptr[row + 1];
+        const double* ur = U + row * ldu;
+        for (long long e = beg + lane; e < end; e += 32) {
+            const int c = __ldg(col + e);
+            const double* vr = Vs + static_cast<long long>(c) * ldv;
+            double p = 0.0;
+            for (long long j = 0; j < k; ++j) p = fma(__ldg(ur + j), __ldg(vr + j), p);
+            const double a = __ldg(A + e);
+            const double y_old = Y[e];
+            const double d = a - p;
+            s_abs += fabs(d);
+            s_sq = fma(d, d, s_sq);
+            const double r = a - y_old;
+            s_res = fma(r, r, s_res);
+            if (mode == 1) {
+                const double y_new = fma(delta, d, y_old);
+                Y[e] = y_new;
+                Ycsc[csr2csc[e]] = y_new;
+                s_y = fma(y_new, y_new, s_y);
+            } else if (mode == 2) {
+                Y[e] = p;
+                s_y = fma(p, p, s_y);
+            } else {
+                s_y = fma(y_old, y_old, s_y);
+            }
+        }
+    }
+    s_abs = warp_sum(s_abs);
+    s_sq = warp_sum(s_sq);
+    s_res = warp_sum(s_res);
+    s_y = warp_sum(s_y);
+    if (lane == 0) {
+        red[warp][0] = s_abs;
+        red[warp][1] = s_sq;
+        red[warp][2] = s_res;
+        red[warp][3] = s_y;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double t = 0.0;
+        for (int w = 0; w < kSddmmWarps; ++w) t += red[w][threadIdx.x];
+        partials[blockIdx.x * 4 + threadIdx.x] = t;
+    }
+}
+
+__global__ void reduce4_kernel(const double* __restrict__ partials, int nblocks, double* __restrict__ out) {
+    // one warp per component, fixed order
+    const int comp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    double t = 0.0;
+    for (int b = lane; b < nblocks; b += 32) t += partials[b * 4 + comp];
+    t = warp_sum(t);
+    if (lane == 0) out[comp] = t;
+}
+
+__global__ void scale_values_kernel(long long nnz, const double* __restrict__ in, double alpha,
+                                    double* __restrict__ out, const int* __restrict__ csr2csc,
+                                    double* __restrict__ out_csc) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= nnz) return;
+    const double v = in[e] * alpha;
+    out[e] = v;
+    if (out_csc) out_csc[csr2csc[e]] = v;
+}
+
+__global__ void axpy_values_kernel(long long nnz, const double* __restrict__ a, double alpha,
+                                   const double* __restrict__ b, double* __restrict__ out) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= nnz) return;
+    out[e] = a[e] + alpha * b[e];
+}
+
+__global__ void densify_kernel(long long m_local, long long n, const long long* __restrict__ rowptr,
+                               const int* __restrict__ col, const double* __restrict__ val,
+                               double* __restrict__ out) {
+    const long long row = blockIdx.x;
+    if (row >= m_local) return;
+    for (long long e = rowptr[row] + threadIdx.x; e < rowptr[row + 1]; e += blockDim.x)
+        out[row * n + col[e]] = val[e];
+}
+
+}  // namespace
+
+void spmm(svt_ctx* ctx, int cls, i64 nrows, const i64* ptr, const int* idx, const double* val, i64 nnz, i64 x_rows,
+          i64 w, const double* X, i64 ldx, double* out, i64 ldo) {
+    if (nrows <= 0 || w <= 0) return;
+    // algorithmic bytes: 12 B per stored entry (int32 index +
+    // fp64 value) + 8 B per row pointer + the dense panel read once + the
+    // output panel written once; 2 flops per entry per column.
+    LaunchScope ls(ctx, cls, 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * w * (x_rows + nrows), 2.0 * nnz * w);
+    if (w <= 16) {
+        switch (w) {
+#define SVT_CASE(W)                                                          \
+    case W:                                                                  \
+        launch_narrow<W>(ctx, nrows, ptr, idx, val, X, ldx, out, ldo);       \
+        break;
+            SVT_CASE(1) SVT_CASE(2) SVT_CASE(3) SVT_CASE(4) SVT_CASE(5) SVT_CASE(6) SVT_CASE(7) SVT_CASE(8)
+            SVT_CASE(9) SVT_CASE(10) SVT_CASE(11) SVT_CASE(12) SVT_CASE(13) SVT_CASE(14) SVT_CASE(15) SVT_CASE(16)
+#undef SVT_CASE
+            default:
+                break;
+        }
+    } else {
+        dim3 grid(static_cast<unsigned>((nrows + 3) / 4), static_cast<unsigned>((w + 127) / 128));
+        spmm_wide_kernel<<<grid, 128, 0, ctx->stream>>>(nrows, reinterpret_cast<const long long*>(ptr), idx, val, X,
+                                                        ldx, w, out, ldo);
+    }
+}
+
+void sddmm_update(svt_ctx* ctx, i64 m_local, const i64* rowptr, const int* col, const double* A, double* Y,
+                  double* Ycsc, const int* csr2csc, i64 nnz, i64 n, const double* U, i64 ldu, const double* Vs,
+                  i64 ldv, i64 k, double delta, int mode, double* d_sums4) {
+    const int blocks = std::max(1, std::min<int>(ctx->num_sms * 8, static_cast<int>((m_local + kSddmmWarps - 1) / kSddmmWarps)));
+    ctx->ws_partial2.ensure(static_cast<size_t>(blocks) * 4);
+    {
+        // col 4 + A 8 + Y in 8 + Y out 8 (+ CSC mirror 4 + 8) per
+        // entry, row pointers, and the k-wide factor rows read once.
+        const double per = (mode == 1) ? 40.0 : (mode == 2 ? 20.0 : 20.0);
+        LaunchScope ls(ctx, K_SDDMM, per * nnz + 8.0 * (m_local + 1) + 8.0 * k * (m_local + n), 2.0 * nnz * k);
+        sddmm_update_kernel<<<blocks, 32 * kSddmmWarps, 0, ctx->stream>>>(
+            m_local, reinterpret_cast<const long long*>(rowptr), col, A, Y, Ycsc, csr2csc, U, ldu, Vs, ldv, k,
+            delta, mode, ctx->ws_partial2.get());
+    }
+    LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
+    reduce4_kernel<<<1, 128, 0, ctx->stream>>>(ctx->ws_partial2.get(), blocks, d_sums4);
+}
+
+void scale_values(svt_ctx* ctx, i64 nnz, const double* in, double alpha, double* out, const int* csr2csc,
+                  double* out_csc) {
+    if (nnz <= 0) return;
+    LaunchScope ls(ctx, K_OTHER, nnz * 24.0, 0.0);
+    scale_values_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, ctx->stream>>>(nnz, in, alpha, out,
+                                                                                       csr2csc, out_csc);
+}
+
+void axpy_values(svt_ctx* ctx, i64 nnz, const double* a, double alpha, const double* b, double* out) {
+    if (nnz <= 0) return;
+    LaunchScope ls(ctx, K_OTHER, nnz * 24.0, 0.0);
+    axpy_values_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, ctx->stream>>>(nnz, a, alpha, b, out);
+}
+
+void densify_dev(svt_ctx* ctx, i64 m_local, i64 n, const i64* rowptr, const int* col, const double* val,
+                 double* out) {
+    SVT_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * static_cast<size_t>(m_local * n), ctx->stream));
+    if (m_local <= 0) return;
+    LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
+    densify_kernel<<<static_cast<unsigned>(m_local), 128, 0, ctx->stream>>>(
+        m_local, n, reinterpret_cast<const long long*>(rowptr), col, val, out);
+}
+
+}  // namespace svtb

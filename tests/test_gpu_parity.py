@@ -1,0 +1,388 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs, plus the reference's own property tests run on the GPU.
+
+Tolerances (BASELINE north star): revealed rank / extension rounds /
+iteration counts exact; singular values within 1e-8 relative (kept values
+relative to themselves, the rest relative to sigma_1); products / completed
+matrices within 1e-8 relative; sparse kernels within 1e-12 relative
+(different but exact-arithmetic-equivalent summation order)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1704_05528_b200 import Backend, DomainError, InvalidArgument, SketchParams, StopRule
+from paper_1704_05528_b200 import api as G
+from tests.refutil import dense_of, product, random_sampled, random_triplets
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_mat(S: O.Csr):
+    return G.SampledMatrix.from_csr(S.m, S.n, S.rowptr, S.col, S.val)
+
+
+def params(t, dt, np_, eps, seed):
+    return SketchParams(t=t, dt=dt, np=np_, eps_threshold=eps, seed=seed)
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+# ---- dense.hpp ----------------------------------------------------------------
+@pytest.mark.parametrize("shape_seed", [(3, 2, 7), (1000, 1, 1), (313, 2, 6), (157, 3, 8), (5000, 10, 99),
+                                        (20001, 7, 12345)])
+def test_gaussian_block_matches_oracle(shape_seed):
+    r, c, s = shape_seed
+    g = G.gaussian_block(r, c, s)
+    o = O.gaussian_block(r, c, s)
+    # identical mt19937_64 integers; log/sin/cos may differ by an ulp or two
+    np.testing.assert_allclose(g, o, rtol=1e-13, atol=1e-15)
+
+
+def test_gaussian_block_golden():
+    import os
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "gaussian_block.npz"))
+    for key in gold.files:
+        r, c, s = (int(x) for x in key.split("_")[1:])
+        np.testing.assert_allclose(G.gaussian_block(r, c, s), gold[key], rtol=1e-13, atol=1e-15)
+
+
+def test_gaussian_block_rejects_zero():
+    with pytest.raises(InvalidArgument):
+        G.gaussian_block(0, 3, 1)
+
+
+@pytest.mark.parametrize("shape", [(50, 10), (6, 3), (1000, 64), (2000, 100), (300, 16)])
+def test_qr_orthonormal(shape):
+    X = O.gaussian_block(*shape, 11)
+    Q = G.qr_orthonormal(X)
+    k = shape[1]
+    assert np.abs(Q.T @ Q - np.eye(k)).max() <= 1e-12
+    assert np.linalg.norm(Q @ (Q.T @ X) - X) <= 1e-10 * np.linalg.norm(X)
+
+
+def test_qr_rank_deficient_keeps_columns():  # test_dense.cpp:55-62 on the GPU
+    X = O.gaussian_block(6, 3, 3)
+    X[:, 2] = X[:, 0] + X[:, 1]
+    Q = G.qr_orthonormal(X)
+    assert Q.shape == (6, 3)
+    assert np.abs(Q.T @ Q - np.eye(3)).max() <= 1e-10
+    assert np.linalg.norm(Q @ (Q.T @ X) - X) <= 1e-9 * np.linalg.norm(X)
+    Z = G.qr_orthonormal(np.zeros((8, 3)))
+    assert np.abs(Z.T @ Z - np.eye(3)).max() <= 1e-12
+
+
+def test_qr_rejects_wide():
+    with pytest.raises(InvalidArgument):
+        G.qr_orthonormal(np.zeros((2, 4)))
+
+
+@pytest.mark.parametrize("shape", [(10, 40), (15, 9), (2, 2), (48, 60), (64, 200), (300, 500)])
+def test_small_svd_matches(shape):
+    B = O.gaussian_block(*shape, 5)
+    U, s, V = G.small_svd(B)
+    ref = np.linalg.svd(B, compute_uv=False)
+    np.testing.assert_allclose(s, ref, rtol=1e-10, atol=1e-12 * ref[0])
+    assert np.linalg.norm(product(U, s, V) - B) <= 1e-10 * np.linalg.norm(B)
+    k = min(shape)
+    assert np.abs(U.T @ U - np.eye(k)).max() <= 1e-10
+
+
+def test_small_svd_zero_block():
+    U, s, V = G.small_svd(np.zeros((2, 4)))
+    assert s.size == 2 and s.max() == 0.0
+
+
+# ---- sampled.hpp --------------------------------------------------------------
+@pytest.mark.parametrize("w", [1, 5, 10, 16, 17, 50, 300])
+def test_sp_mult_and_t_match_oracle(w):
+    S = random_sampled(300, 220, 0.1, 42)
+    Sg = gpu_mat(S)
+    X = O.gaussian_block(220, w, 43)
+    Y = O.gaussian_block(300, w, 44)
+    assert rel(G.sp_mult(Sg, X), O.sp_mult(S, X)) <= 1e-12
+    assert rel(G.sp_mult_t(Sg, Y), O.sp_mult_t(S, Y)) <= 1e-12
+
+
+def test_sp_mult_single_entry_exact():
+    S = O.sampled(2, 2, [0], [1], [5.0])
+    Sg = gpu_mat(S)
+    np.testing.assert_array_equal(G.sp_mult(Sg, np.eye(2)), [[0, 5], [0, 0]])
+    np.testing.assert_array_equal(G.sp_mult_t(Sg, np.eye(2)), [[0, 0], [5, 0]])
+
+
+def test_sp_mult_empty_rows_and_columns():
+    # rows 1, 3 and columns 0, 4 are empty
+    S = O.sampled(5, 6, [0, 0, 2, 4, 4], [1, 5, 2, 3, 1], [1.0, -2.0, 3.0, 4.0, 0.5])
+    Sg = gpu_mat(S)
+    X = O.gaussian_block(6, 4, 1)
+    Y = O.gaussian_block(5, 4, 2)
+    np.testing.assert_allclose(G.sp_mult(Sg, X), dense_of(S) @ X, rtol=1e-14, atol=1e-14)
+    np.testing.assert_allclose(G.sp_mult_t(Sg, Y), dense_of(S).T @ Y, rtol=1e-14, atol=1e-14)
+
+
+def test_project_low_rank_matches():
+    U = O.qr_orthonormal(O.gaussian_block(40, 3, 31))
+    V = O.qr_orthonormal(O.gaussian_block(30, 3, 32))
+    s = np.array([5.0, 2.0, 0.5])
+    pat = random_sampled(40, 30, 0.17, 33)
+    got = G.project_low_rank(gpu_mat(pat), U, s, V)
+    np.testing.assert_allclose(got, O.project_low_rank(pat, U, s, V), rtol=0, atol=1e-12)
+    assert (G.project_low_rank(gpu_mat(pat), U, np.zeros(3), V) == 0.0).all()
+
+
+def test_norms_spectral_kickstart():
+    S = random_sampled(60, 45, 0.2, 9)
+    Sg = gpu_mat(S)
+    assert abs(G.sp_frob_norm_sq(Sg) - O.sp_frob_norm_sq(S)) <= 1e-13 * O.sp_frob_norm_sq(S)
+    assert abs(G.spectral_norm_est(Sg, 20, 5) - O.spectral_norm_est(S, 20, 5)) <= 1e-12 * O.spectral_norm_est(S, 20, 5)
+    np.testing.assert_allclose(G.kickstart(Sg, 7.0, 1.3, 4), O.kickstart(S, 7.0, 1.3, 4).val, rtol=1e-14)
+    S1 = O.sampled(3, 3, [0], [0], [3.0])
+    assert abs(G.kickstart(gpu_mat(S1), 10.0, 1.0, 5)[0] - 12.0) <= 12e-9  # test_solver.cpp:57-66
+
+
+# ---- sketch.hpp ---------------------------------------------------------------
+def check_sketch(g, o, sigma_tol=1e-8):
+    assert g.rank == o.rank and g.extension_rounds == o.extension_rounds and g.saturated == o.saturated
+    s1 = o.sigma[0] if o.sigma.size else 1.0
+    np.testing.assert_allclose(g.sigma, o.sigma, rtol=sigma_tol, atol=sigma_tol * s1)
+    Pg, Po = product(g.U, g.sigma, g.V), product(o.U, o.sigma, o.V)
+    assert rel(Pg, Po) <= sigma_tol
+
+
+@pytest.mark.parametrize("case", [
+    (random_sampled, (60, 45, 0.3, 30), (4, 6, 1, 0.2, 31)),
+    (random_sampled, (120, 100, 0.25, 3), (5, 10, 1, 0.05, 8)),
+    (random_sampled, (200, 150, 0.1, 4), (10, 10, 1, 0.3, 9)),
+    (random_sampled, (80, 90, 0.5, 5), (3, 7, 2, 0.1, 10)),
+    (random_sampled, (100, 100, 0.3, 6), (70, 10, 1, 0.01, 11)),
+])
+def test_r3svd_matches_oracle(case):
+    gen, a, p = case
+    S = gen(*a)
+    g = G.r3svd(gpu_mat(S), params(*p))
+    o = O.r3svd(S, params(*p))
+    check_sketch(g, o)
+
+
+def test_r3svd_reveals_rank5():  # test_sketch.cpp:185-193
+    A = O.make_low_rank(60, 50, 5, 43)
+    S = O.to_sampled(A)
+    g = G.r3svd(gpu_mat(S), params(2, 2, 1, 1e-6, 44))
+    o = O.r3svd(S, params(2, 2, 1, 1e-6, 44))
+    assert not g.saturated and g.rank == o.rank and g.rank in (6, 8)
+    assert np.sum((product(g.U, g.sigma, g.V) - A) ** 2) / np.sum(A ** 2) <= 1e-6
+
+
+def test_r3svd_trivial_threshold():  # :195-200
+    res = G.r3svd(gpu_mat(random_sampled(30, 30, 0.4, 45)), params(3, 5, 1, 0.999, 46))
+    assert res.rank == 3 and res.extension_rounds == 0
+
+
+def test_r3svd_flat_spectrum_saturation():  # :202-228
+    Y = O.sampled(30, 30, np.arange(30), np.arange(30), np.ones(30))
+    Yg = gpu_mat(Y)
+    D = dense_of(Y)
+    saw = False
+    for seed in range(1, 11):
+        res = G.r3svd(Yg, params(4, 7, 1, 1e-16, seed))
+        saw |= res.saturated
+        assert res.rank == 30
+        assert np.linalg.norm(product(res.U, res.sigma, res.V) - D) <= 1e-9 * np.linalg.norm(D)
+    assert saw
+
+
+def test_r3svd_domain_error_on_zero():
+    Y = O.sampled(4, 4, [0, 1], [0, 1], [0.0, 0.0])
+    with pytest.raises(DomainError):
+        G.r3svd(gpu_mat(Y), params(1, 1, 1, 0.5, 1))
+
+
+def test_r3svd_rejects_params():
+    Yg = gpu_mat(random_sampled(10, 8, 0.5, 16))
+    with pytest.raises(InvalidArgument):
+        G.r3svd(Yg, params(0, 1, 1, 0.5, 1))
+    with pytest.raises(InvalidArgument):
+        G.r3svd(Yg, params(9, 1, 1, 0.5, 1))
+    with pytest.raises(InvalidArgument):
+        G.r3svd(Yg, params(2, 1, 1, 1.5, 1))
+
+
+def test_r4svd_exact_basis():  # :230-239
+    A = O.make_low_rank(50, 40, 4, 47)
+    U = np.linalg.svd(A, full_matrices=False)[0][:, :4]
+    res = G.r4svd(gpu_mat(O.to_sampled(A)), U, params(3, 3, 1, 1e-3, 48))
+    assert res.extension_rounds == 0 and res.rank == 4
+    assert np.linalg.norm(product(res.U, res.sigma, res.V) - A) <= 1e-8 * np.linalg.norm(A)
+
+
+def test_r4svd_useless_basis():  # :241-257
+    W = O.qr_orthonormal(O.gaussian_block(40, 10, 49))
+    s = np.array([8, 5, 3, 2, 1.0])
+    Vf = O.qr_orthonormal(O.gaussian_block(32, 5, 50))
+    A = (W[:, :5] * s) @ Vf.T
+    S = O.to_sampled(A)
+    g = G.r4svd(gpu_mat(S), W[:, 7:], params(3, 3, 1, 1e-6, 49))
+    o = O.r4svd(S, W[:, 7:], params(3, 3, 1, 1e-6, 49))
+    assert not g.saturated and g.rank == o.rank and g.rank > 3
+    assert np.sum((product(g.U, g.sigma, g.V) - A) ** 2) / np.sum(A ** 2) <= 1e-6
+
+
+def test_r4svd_empty_equals_r3svd():  # :279-290 (bit-for-bit on the device)
+    Yg = gpu_mat(random_sampled(40, 32, 0.4, 53))
+    a = G.r4svd(Yg, np.zeros((40, 0)), params(7, 5, 1, 0.01, 54))
+    b = G.r3svd(Yg, params(5, 5, 1, 0.01, 54))
+    assert a.rank == b.rank
+    assert np.array_equal(a.U, b.U) and np.array_equal(a.sigma, b.sigma) and np.array_equal(a.V, b.V)
+
+
+def test_r4svd_drift():  # :292-303
+    A = O.make_geometric(30, 25, 25, 0.6, 55)
+    U = O.qr_orthonormal(O.gaussian_block(30, 5, 56))
+    U[:, 0] += 1e-4 * U[:, 1]
+    S = O.to_sampled(A)
+    g = G.r4svd(gpu_mat(S), U, params(3, 3, 1, 0.02, 57))
+    o = O.r4svd(S, U, params(3, 3, 1, 0.02, 57))
+    assert not g.saturated and g.rank == o.rank
+    assert np.abs(g.U.T @ g.U - np.eye(g.U.shape[1])).max() <= 1e-8
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_r4svd_recycled_matches_oracle(seed):
+    S = random_sampled(150, 120, 0.3, 100 + seed)
+    prev = O.r3svd(S, params(5, 10, 1, 0.3, seed))
+    Uprev = prev.U[:, :6]
+    g = G.r4svd(gpu_mat(S), Uprev, params(5, 10, 1, 0.1, seed + 7))
+    o = O.r4svd(S, Uprev, params(5, 10, 1, 0.1, seed + 7))
+    check_sketch(g, o)
+
+
+def test_rsvd_matches_oracle():
+    A = O.make_geometric(100, 80, 80, 0.5, 39)
+    S = O.to_sampled(A)
+    p = params(1, 1, 2, 0.5, 40)
+    p.p = 5
+    g = G.rsvd(gpu_mat(S), 10, p)
+    o = O.rsvd(S, 10, p)
+    np.testing.assert_allclose(g.sigma, o.sigma, rtol=1e-8)
+    with pytest.raises(InvalidArgument):
+        G.rsvd(gpu_mat(random_sampled(10, 8, 0.5, 41)), 4, p)
+
+
+# ---- solver.hpp ---------------------------------------------------------------
+def check_runs(g, o, tol=1e-8, check_factors=True):
+    assert len(g.trace) == len(o.trace) and g.converged == o.converged
+    for a, b in zip(g.trace, o.trace):
+        assert a["rank"] == b["rank"] and a["kept"] == b["kept"] and a["extension_rounds"] == b["extension_rounds"]
+        assert a["eps_threshold"] == b["eps_threshold"]
+        for key in ("residual", "train_mae", "rel_residual_x"):
+            assert abs(a[key] - b[key]) <= tol * max(abs(b[key]), 1e-12), (key, a[key], b[key])
+    if check_factors:
+        assert g.sigma.size == o.sigma.size
+        if o.sigma.size:
+            np.testing.assert_allclose(g.sigma, o.sigma, rtol=tol)
+            assert rel(product(g.U, g.sigma, g.V), product(o.U, o.sigma, o.V)) <= tol
+
+
+def test_svt_run_matches_oracle_small():
+    A = O.make_low_rank(60, 50, 4, 23)
+    S = O.sample_dense(A, 0.5, 24)
+    cfg = O.default_config(S)
+    cfg.maxit = 40
+    cfg.seed = 25
+    g = G.svt_run(gpu_mat(S), cfg, StopRule.none())
+    o = O.svt_run(S, cfg, StopRule.none())
+    check_runs(g, o)
+
+
+def test_svt_run_cooling_replay_on_gpu():  # test_solver.cpp:157-182
+    A = O.make_low_rank(60, 50, 4, 23)
+    S = O.sample_dense(A, 0.5, 24)
+    cfg = O.default_config(S)
+    cfg.maxit = 60
+    cfg.seed = 25
+    r = G.svt_run(gpu_mat(S), cfg, StopRule.none())
+    eps_min, expected = np.inf, cfg.eps_threshold0
+    for rec in r.trace:
+        if rec["residual"] < eps_min:
+            eps_min = rec["residual"]
+        else:
+            expected *= cfg.beta
+        assert rec["eps_threshold"] == expected
+
+
+def test_svt_recovers_low_rank_40pct():  # test_solver.cpp:145-155
+    A = O.make_low_rank(200, 200, 10, 20)
+    S = O.sample_dense(A, 0.4, 21)
+    cfg = O.default_config(S)
+    cfg.maxit = 300
+    cfg.seed = 22
+    g = G.svt_run(gpu_mat(S), cfg, StopRule.train_mae(1e-3))
+    o = O.svt_run(S, cfg, StopRule.train_mae(1e-3))
+    assert g.converged and o.converged
+    assert abs(len(g.trace) - len(o.trace)) <= 1
+    assert np.linalg.norm(product(g.U, g.sigma, g.V) - A) / np.linalg.norm(A) <= 1e-2
+
+
+def test_svt_maxit_best_iterate_and_observer():
+    A = O.make_low_rank(40, 40, 3, 26)
+    S = O.sample_dense(A, 0.5, 27)
+    cfg = O.default_config(S)
+    cfg.maxit = 5
+    cfg.seed = 28
+    g = G.svt_run(gpu_mat(S), cfg, StopRule.train_mae(1e-12))
+    o = O.svt_run(S, cfg, StopRule.train_mae(1e-12))
+    check_runs(g, o)
+    assert not g.converged
+    seen = [0]
+
+    def obs(rec, U, s, V):
+        seen[0] += 1
+        return seen[0] < 3
+
+    cfg.maxit = 50
+    r = G.svt_run(gpu_mat(S), cfg, StopRule.none(), observer=obs)
+    assert len(r.trace) == 3 and r.converged
+
+
+def test_svt_rank0_and_backends():
+    A = O.make_low_rank(30, 30, 2, 29)
+    S = O.sample_dense(A, 0.6, 30)
+    cfg = O.default_config(S)
+    cfg.tau = 40.0 * cfg.tau
+    cfg.maxit = 8
+    cfg.seed = 31
+    g = G.svt_run(gpu_mat(S), cfg, StopRule.none())
+    o = O.svt_run(S, cfg, StopRule.none())
+    check_runs(g, o)
+    cfg = O.default_config(S)
+    cfg.maxit = 15
+    cfg.seed = 3
+    for be in (Backend.r3svd(), Backend.rsvd_fixed(4), Backend.full_svd()):
+        g = G.svt_run_backend(gpu_mat(S), cfg, StopRule.none(), be)
+        o = O.svt_run_backend(S, cfg, StopRule.none(), be)
+        check_runs(g, o, tol=1e-7)
+
+
+def test_svt_validates():
+    Sg = gpu_mat(O.sampled(2, 2, [0], [0], [1.0]))
+    from paper_1704_05528_b200 import SvtConfig
+    with pytest.raises(InvalidArgument):
+        G.svt_run(Sg, SvtConfig(), StopRule.none())
+
+
+def test_held_out_metrics_match_oracle():
+    rng_r, rng_c, vals = random_triplets(80, 70, 0.4, 77)
+    k = len(vals)
+    train = O.sampled(80, 70, rng_r[: int(0.9 * k)], rng_c[: int(0.9 * k)], vals[: int(0.9 * k)])
+    test = O.sampled(80, 70, rng_r[int(0.9 * k):], rng_c[int(0.9 * k):], vals[int(0.9 * k):])
+    cfg = O.default_config(train)
+    cfg.maxit = 10
+    cfg.seed = 5
+    g = G.svt_run(gpu_mat(train), cfg, StopRule.none(), test=gpu_mat(test))
+    o = O.svt_run(train, cfg, StopRule.none(), test=test)
+    check_runs(g, o)
+    for a, b in zip(g.trace, o.trace):
+        assert abs(a["test_rmse"] - b["test_rmse"]) <= 1e-8 * b["test_rmse"]
+        assert abs(a["test_mae"] - b["test_mae"]) <= 1e-8 * b["test_mae"]
