@@ -557,7 +557,12 @@ def config_params(config: int, A_nnz: int, m: int, n: int, frob_a: float):
         cfg.tau, cfg.delta = 5.0 * np.sqrt(m * n), 1.2 / p
         cfg.rel_residual_stop = 1e-4
     elif config in (3, 4):
-        cfg.tau, cfg.delta = frob_a, np.sqrt(m * n / A_nnz)
+        # tau = ||P A||_F (reference default); delta = 1.9: the reference
+        # default sqrt(mn/ns) (= 5.0 / 9.1 here) diverges on the power-law /
+        # Zipf sampling of these generators, and SVT's convergence theorem
+        # needs 0 < delta < 2 (Cai, Candes & Shen, Thm 4.1).  BASELINE leaves
+        # both unspecified.
+        cfg.tau, cfg.delta = frob_a, 1.9
     elif config == 5:
         cfg.tau, cfg.delta = 5.0 * n, 1.2 / p
         cfg.maxit = 30
