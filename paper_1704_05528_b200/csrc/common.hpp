@@ -106,6 +106,22 @@ struct Comm {
     void destroy();
 };
 void nccl_unique_id(void* out128);
+
+// Load-balanced row segmentation of a CSR / CSC view (host.cpp builds it at
+// upload): every row is one or more segments of <= kSegLen entries.
+constexpr long long kSegLen = 2048;
+struct SegPlanView {
+    long long nseg = 0;
+    const int* seg_row = nullptr;
+    const long long* seg_beg = nullptr;
+    const long long* seg_end = nullptr;
+    const int* seg_slot = nullptr;  // -1: writes its row directly; else partial slot
+    long long nlong = 0;            // rows split over several segments
+    long long nslots = 0;
+    const int* long_row = nullptr;
+    const int* long_first = nullptr;
+    const int* long_count = nullptr;
+};
 void nccl_init(Comm& c, int rank, int world, const void* id128);
 
 }  // namespace svtb
@@ -134,6 +150,7 @@ struct svt_ctx {
     int* h_flags = nullptr;       // pinned, 64 ints
     svtb::DevBuf<double> ws_partial;   // split-K / reduction partials
     svtb::DevBuf<double> ws_partial2;  // second partial buffer (reductions)
+    svtb::DevBuf<double> ws_spmm;      // long-row partials of the segmented SpMM
     svtb::DevBuf<unsigned long long> ws_rng;  // raw mt19937_64 draws
     svtb::DevBuf<unsigned long long> ws_mt;   // persistent mt state (312 words + index)
     svtb::DevBuf<double> ws_eig;              // Jacobi eigensolver workspace

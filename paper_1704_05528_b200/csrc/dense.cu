@@ -667,6 +667,21 @@ __global__ void permute_cols_kernel(const double* __restrict__ W, long long rows
     W2[i * ldw2 + j] = W[i * ldw + perm[j]];
 }
 
+__global__ void set_identity_cols_kernel(double* Z, long long rows, long long ld, long long s) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= rows * s) return;
+    const long long i = e / s, j = e % s;
+    Z[i * ld + j] = (i == j) ? 1.0 : 0.0;
+}
+
+__global__ void sub_scaled_cols_kernel(double* Y, const double* __restrict__ X, long long rows, long long cols,
+                                       long long ld, const double* __restrict__ theta) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= rows * cols) return;
+    const long long i = e / cols, j = e % cols;
+    Y[i * ld + j] -= X[i * ld + j] * theta[j];
+}
+
 inline unsigned nblk(i64 n, int bs = 256) { return static_cast<unsigned>(std::max<i64>(1, (n + bs - 1) / bs)); }
 
 }  // namespace
@@ -801,6 +816,18 @@ void copy2d(svt_ctx* ctx, const double* src, i64 lds, double* dst, i64 ldd, i64 
     if (rows * cols <= 0) return;
     LaunchScope ls(ctx, K_OTHER, 16.0 * rows * cols, 0.0);
     copy2d_kernel<<<nblk(rows * cols), 256, 0, ctx->stream>>>(src, lds, dst, ldd, rows, cols, pred);
+}
+
+void set_identity_cols(svt_ctx* ctx, double* Z, i64 rows, i64 ld, i64 s) {
+    if (rows * s <= 0) return;
+    LaunchScope ls(ctx, K_OTHER, 8.0 * rows * s, 0.0);
+    set_identity_cols_kernel<<<nblk(rows * s), 256, 0, ctx->stream>>>(Z, rows, ld, s);
+}
+
+void sub_scaled_cols(svt_ctx* ctx, double* Y, const double* X, i64 rows, i64 cols, i64 ld, const double* theta) {
+    if (rows * cols <= 0) return;
+    LaunchScope ls(ctx, K_OTHER, 24.0 * rows * cols, 2.0 * rows * cols);
+    sub_scaled_cols_kernel<<<nblk(rows * cols), 256, 0, ctx->stream>>>(Y, X, rows, cols, ld, theta);
 }
 
 void fill(svt_ctx* ctx, double* p, i64 n, double v) {

@@ -73,9 +73,12 @@ void ensure_cap(Engine& E, QBDev& st, i64 need) {
 }
 
 // One CholQR2 panel (w <= 64) with the Householder fallback.  X is preserved.
-void qr_panel(Engine& E, const double* X, i64 ldx, i64 w, double* Qout, i64 ldq, const int* pred) {
+// m rows; dist: the rows are this rank's block of a row-sharded panel (Gram
+// blocks are all-reduced) — false for replicated panels (finalize space).
+void qr_panel(Engine& E, i64 m, bool dist, const double* X, i64 ldx, i64 w, double* Qout, i64 ldq,
+              const int* pred) {
     svt_ctx* c = E.ctx;
-    const i64 m = E.mat->m_local;
+    dist = dist && c->comm.world > 1;
     E.G.ensure(static_cast<size_t>(w * w));
     E.Rinv.ensure(static_cast<size_t>(w * w));
     E.tmp.ensure(static_cast<size_t>(std::max<i64>(1, m) * w));
@@ -83,15 +86,15 @@ void qr_panel(Engine& E, const double* X, i64 ldx, i64 w, double* Qout, i64 ldq,
     zero_flag(c, F_QRSTAT);
     // pass 1: R1 = chol(X^T X), Q1 = X R1^{-1}
     gemm(c, K_QR, true, w, w, m, 1.0, X, ldx, X, ldx, 0.0, E.G.get(), w, pred);
-    allreduce(c, E.G.get(), static_cast<size_t>(w * w));
+    if (dist) allreduce(c, E.G.get(), static_cast<size_t>(w * w));
     chol_rinv(c, E.G.get(), w, E.Rinv.get(), status, pred);
     gemm(c, K_QR, false, m, w, w, 1.0, X, ldx, E.Rinv.get(), w, 0.0, E.tmp.get(), w, pred);
     // pass 2
     gemm(c, K_QR, true, w, w, m, 1.0, E.tmp.get(), w, E.tmp.get(), w, 0.0, E.G.get(), w, pred);
-    allreduce(c, E.G.get(), static_cast<size_t>(w * w));
+    if (dist) allreduce(c, E.G.get(), static_cast<size_t>(w * w));
     chol_rinv(c, E.G.get(), w, E.Rinv.get(), status, pred);
     gemm(c, K_QR, false, m, w, w, 1.0, E.tmp.get(), w, E.Rinv.get(), w, 0.0, Qout, ldq, pred);
-    if (c->comm.world == 1) {
+    if (!dist) {
         E.hh.ensure(static_cast<size_t>(std::max<i64>(1, m) * w));
         householder_qr(c, X, m, w, ldx, Qout, ldq, E.hh.get(), pred, status);
         return;
@@ -110,19 +113,18 @@ void qr_panel(Engine& E, const double* X, i64 ldx, i64 w, double* Qout, i64 ldq,
 
 // Project Q[:, 0:r0] out of the panel P (m x w, ld) and re-orthonormalize
 // it, predicated on flag `f` computed from max|Q^T P| > 1e-8 (sketch.hpp:138).
-void reorth_if_needed(Engine& E, const double* Q, i64 ldq, i64 r0, double* P, i64 ldp, i64 w) {
+void reorth_if_needed(Engine& E, i64 m, bool dist, const double* Q, i64 ldq, i64 r0, double* P, i64 ldp, i64 w) {
     svt_ctx* c = E.ctx;
-    const i64 m = E.mat->m_local;
     E.D.ensure(static_cast<size_t>(r0 * w));
     gemm(c, K_GEMM, true, r0, w, m, 1.0, Q, ldq, P, ldp, 0.0, E.D.get(), w);
-    allreduce(c, E.D.get(), static_cast<size_t>(r0 * w));
+    if (dist) allreduce(c, E.D.get(), static_cast<size_t>(r0 * w));
     maxabs(c, E.D.get(), r0, w, w, 0.0, dsc(c, S_MAXD));
     set_flag(c, dsc(c, S_MAXD), nullptr, 1e-8, 1, dfl(c, F_REORTH));
     const int* f = dfl(c, F_REORTH);
     E.X2.ensure(static_cast<size_t>(std::max<i64>(1, m) * w));
     copy2d(c, P, ldp, E.X2.get(), w, m, w, f);
     gemm(c, K_GEMM, false, m, w, r0, -1.0, Q, ldq, E.D.get(), w, 1.0, E.X2.get(), w, f);
-    qr_panel(E, E.X2.get(), w, w, P, ldp, f);
+    qr_panel(E, m, dist, E.X2.get(), w, w, P, ldp, f);
 }
 
 }  // namespace
@@ -138,13 +140,12 @@ double frob_sq(Engine& E) {
 
 void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo) {
     svt_mat* A = E.mat;
-    spmm(E.ctx, K_SPMM, A->m_local, A->rowptr.get(), A->col.get(), E.Y.csr, A->nnz_local, A->n, w, X, ldx, out, ldo);
+    spmm(E.ctx, K_SPMM, A->plan_csr.v, A->m_local, A->col.get(), E.Y.csr, A->nnz_local, A->n, w, X, ldx, out, ldo);
 }
 
 void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out) {
     svt_mat* A = E.mat;
-    spmm(E.ctx, K_SPMMT, A->n, A->colptr.get(), A->cscrow.get(), E.Y.csc, A->nnz_local, A->m_local, w, X, ldx, out,
-         w);
+    spmm(E.ctx, K_SPMMT, A->plan_csc.v, A->n, A->cscrow.get(), E.Y.csc, A->nnz_local, A->m_local, w, X, ldx, out, w);
     allreduce(E.ctx, out, static_cast<size_t>(A->n * w));
 }
 
@@ -152,8 +153,12 @@ void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out) {
 // CGS2 + CholQR2 over 64-column blocks (the column-ordered QR, same nested
 // spans).  X is clobbered.
 void qr_orthonormal(Engine& E, double* X, i64 ldx, i64 w, double* Qout, i64 ldq) {
+    qr_orthonormal(E, E.mat->m_local, true, X, ldx, w, Qout, ldq);
+}
+
+void qr_orthonormal(Engine& E, i64 m, bool dist, double* X, i64 ldx, i64 w, double* Qout, i64 ldq) {
     svt_ctx* c = E.ctx;
-    const i64 m = E.mat->m_local;
+    dist = dist && c->comm.world > 1;
     constexpr i64 B = 64;
     for (i64 b0 = 0; b0 < w; b0 += B) {
         const i64 wb = std::min(B, w - b0);
@@ -162,12 +167,12 @@ void qr_orthonormal(Engine& E, double* X, i64 ldx, i64 w, double* Qout, i64 ldq)
             E.C.ensure(static_cast<size_t>(b0 * wb));
             for (int pass = 0; pass < 2; ++pass) {
                 gemm(c, K_QR, true, b0, wb, m, 1.0, Qout, ldq, Xb, ldx, 0.0, E.C.get(), wb);
-                allreduce(c, E.C.get(), static_cast<size_t>(b0 * wb));
+                if (dist) allreduce(c, E.C.get(), static_cast<size_t>(b0 * wb));
                 gemm(c, K_QR, false, m, wb, b0, -1.0, Qout, ldq, E.C.get(), wb, 1.0, Xb, ldx);
             }
         }
-        qr_panel(E, Xb, ldx, wb, Qout + b0, ldq, nullptr);
-        if (b0 > 0) reorth_if_needed(E, Qout, ldq, b0, Qout + b0, ldq, wb);
+        qr_panel(E, m, dist, Xb, ldx, wb, Qout + b0, ldq, nullptr);
+        if (b0 > 0) reorth_if_needed(E, m, dist, Qout, ldq, b0, Qout + b0, ldq, wb);
     }
 }
 
@@ -288,8 +293,8 @@ void qb_extend(Engine& E, QBDev& st, i64 dt, int np, u64 seed) {
              dfl(c, F_CGS2));
     }
     // QR, then conditional re-projection + QR (sketch.hpp:137-141)
-    qr_panel(E, E.X.get(), width, width, Q + r0, ldq, nullptr);
-    if (r0 > 0) reorth_if_needed(E, Q, ldq, r0, Q + r0, ldq, width);
+    qr_panel(E, m, true, E.X.get(), width, width, Q + r0, ldq, nullptr);
+    if (r0 > 0) reorth_if_needed(E, m, true, Q, ldq, r0, Q + r0, ldq, width);
     // coefficient block + energy (sketch.hpp:143-150)
     append_coefficients(E, st, r0, width, 1);
     st.norm_b_sq = read_scalar(c, S_NB);
@@ -372,6 +377,127 @@ void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFact
     SVT_CUDA(cudaStreamSynchronize(c->stream));
 }
 
+// Kept-mode finalize for larger bases: only the triplets with sigma > tau
+// are needed (shrink, solver.hpp:110-120), so instead of a dense r x r
+// eigendecomposition run a Rayleigh-Ritz subspace iteration on G = B B^T
+// through B^T-products (never forming G).  R4SVD's basis starts with the
+// previous iterate's kept left singular vectors (sketch.hpp:228-234), so in Q
+// coordinates the new top singular subspace is close to e_1..e_s: the block
+// is warm-started there and converges in a few sweeps.  The block grows
+// until its smallest Ritz value falls below tau^2, and iterates until every
+// Ritz pair at or above the threshold has residual <= 1e-12 * theta_1.
+static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u64 seed, DevFactors& out) {
+    svt_ctx* c = E.ctx;
+    const i64 r = st.rank, n = st.n, m = st.m_local;
+    out.m_local = m;
+    out.n = n;
+    out.k = 0;
+    out.sigma.clear();
+    if (r <= 48) {
+        finalize(E, st, FinalizeMode::Kept, tau, out);
+        return;
+    }
+    const double tau2 = tau * tau;
+    i64 b = std::min<i64>(r, std::max<i64>(s_warm + 16, 24));
+    const i64 sw = std::min(s_warm, b);
+    DevBuf<double> Z(static_cast<size_t>(r * b)), Zq(static_cast<size_t>(r * b)), Zt(static_cast<size_t>(r * b));
+    DevBuf<double> Wn(static_cast<size_t>(n * b)), H(static_cast<size_t>(b * b)), Yh(static_cast<size_t>(b * b));
+    DevBuf<double> th(static_cast<size_t>(b)), ZY(static_cast<size_t>(r * b)), Xr(static_cast<size_t>(r * b));
+    DevBuf<double> res2(static_cast<size_t>(b));
+    fill(c, Z.get(), r * b, 0.0);
+    set_identity_cols(c, Z.get(), r, b, sw);
+    if (b > sw) gaussian_block_dev(c, r, b - sw, derive_seed_u(seed, 0x5EEDF1A1ULL), Z.get() + sw, b);
+    std::vector<double> th_h, res_h;
+    i64 kk = 0;
+    const int maxit = 100;
+    for (int it = 0; it < maxit; ++it) {
+        copy2d(c, Z.get(), b, Zt.get(), b, r, b);
+        qr_orthonormal(E, r, false, Zt.get(), b, b, Zq.get(), b);
+        gemm(c, K_FINAL, false, n, b, r, 1.0, st.Bt.get(), st.cap, Zq.get(), b, 0.0, Wn.get(), b);
+        gemm(c, K_FINAL, true, r, b, n, 1.0, st.Bt.get(), st.cap, Wn.get(), b, 0.0, Z.get(), b);
+        gemm(c, K_FINAL, true, b, b, r, 1.0, Zq.get(), b, Z.get(), b, 0.0, H.get(), b);
+        sym_eig(c, H.get(), b, Yh.get(), th.get());
+        gemm(c, K_FINAL, false, r, b, b, 1.0, Z.get(), b, Yh.get(), b, 0.0, ZY.get(), b);
+        gemm(c, K_FINAL, false, r, b, b, 1.0, Zq.get(), b, Yh.get(), b, 0.0, Xr.get(), b);
+        sub_scaled_cols(c, ZY.get(), Xr.get(), r, b, b, th.get());
+        col_sumsq(c, ZY.get(), r, b, b, res2.get());
+        th_h.resize(static_cast<size_t>(b));
+        res_h.resize(static_cast<size_t>(b));
+        SVT_CUDA(cudaMemcpyAsync(th_h.data(), th.get(), sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream));
+        SVT_CUDA(cudaMemcpyAsync(res_h.data(), res2.get(), sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream));
+        SVT_CUDA(cudaStreamSynchronize(c->stream));
+        kk = 0;
+        while (kk < b && th_h[static_cast<size_t>(kk)] > tau2 * (1.0 - 1e-6)) ++kk;
+        if (kk == b && b < r) {
+            // the block does not reach below the threshold: widen it
+            const i64 b2 = std::min<i64>(r, 2 * b);
+            DevBuf<double> Z2(static_cast<size_t>(r * b2));
+            copy2d(c, Zq.get(), b, Z2.get(), b2, r, b);
+            gaussian_block_dev(c, r, b2 - b, derive_seed_u(seed, 0x5EEDF1A2ULL + static_cast<u64>(it)), Z2.get() + b,
+                               b2);
+            b = b2;
+            Z = std::move(Z2);
+            Zq.alloc(static_cast<size_t>(r * b));
+            Zt.alloc(static_cast<size_t>(r * b));
+            Wn.alloc(static_cast<size_t>(n * b));
+            H.alloc(static_cast<size_t>(b * b));
+            Yh.alloc(static_cast<size_t>(b * b));
+            th.alloc(static_cast<size_t>(b));
+            ZY.alloc(static_cast<size_t>(r * b));
+            Xr.alloc(static_cast<size_t>(r * b));
+            res2.alloc(static_cast<size_t>(b));
+            continue;
+        }
+        const double tol = 1e-12 * std::max(th_h[0], 0.0);
+        bool conv = true;
+        const i64 check = std::min(b, kk + 1);
+        for (i64 i = 0; i < check; ++i)
+            if (!(std::sqrt(std::max(res_h[static_cast<size_t>(i)], 0.0)) <= tol)) conv = false;
+        if (conv || b == r) break;
+    }
+    c->stats[K_FINAL].flops += 0.0;
+    const i64 kc = std::min(b, kk + 1);
+    // V_raw = B^T (Zq Yh) = Wn Yh; sigma = column norms (Rayleigh quotients)
+    E.Vraw.ensure(static_cast<size_t>(n * kc));
+    gemm(c, K_FINAL, false, n, kc, b, 1.0, Wn.get(), b, Yh.get(), b, 0.0, E.Vraw.get(), kc);
+    E.lam.ensure(static_cast<size_t>(kc));
+    col_sumsq(c, E.Vraw.get(), n, kc, kc, E.lam.get());
+    std::vector<double> s2(static_cast<size_t>(kc));
+    SVT_CUDA(cudaMemcpyAsync(s2.data(), E.lam.get(), sizeof(double) * kc, cudaMemcpyDeviceToHost, c->stream));
+    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    std::vector<double> sig(static_cast<size_t>(kc));
+    for (i64 j = 0; j < kc; ++j) sig[static_cast<size_t>(j)] = std::sqrt(s2[static_cast<size_t>(j)]);
+    std::vector<int> perm(static_cast<size_t>(kc));
+    std::iota(perm.begin(), perm.end(), 0);
+    std::stable_sort(perm.begin(), perm.end(),
+                     [&](int a, int bb) { return sig[static_cast<size_t>(a)] > sig[static_cast<size_t>(bb)]; });
+    i64 k = 0;
+    while (k < kc && sig[static_cast<size_t>(perm[static_cast<size_t>(k)])] > tau) ++k;
+    out.k = k;
+    if (k == 0) return;
+    out.sigma.resize(static_cast<size_t>(k));
+    std::vector<double> inv(static_cast<size_t>(k));
+    for (i64 j = 0; j < k; ++j) {
+        out.sigma[static_cast<size_t>(j)] = sig[static_cast<size_t>(perm[static_cast<size_t>(j)])];
+        inv[static_cast<size_t>(j)] = 1.0 / out.sigma[static_cast<size_t>(j)];
+    }
+    E.perm.ensure(static_cast<size_t>(k));
+    out.d_sigma.ensure(static_cast<size_t>(2 * k));
+    SVT_CUDA(cudaMemcpyAsync(E.perm.get(), perm.data(), sizeof(int) * k, cudaMemcpyHostToDevice, c->stream));
+    SVT_CUDA(cudaMemcpyAsync(out.d_sigma.get(), out.sigma.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
+                             c->stream));
+    SVT_CUDA(cudaMemcpyAsync(out.d_sigma.get() + k, inv.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
+                             c->stream));
+    out.V.ensure(static_cast<size_t>(n * k));
+    permute_cols(c, E.Vraw.get(), n, kc, E.perm.get(), k, out.V.get(), k);
+    scale_cols(c, out.V.get(), n, k, k, out.d_sigma.get() + k);
+    E.Wk.ensure(static_cast<size_t>(r * k));
+    permute_cols(c, Xr.get(), r, b, E.perm.get(), k, E.Wk.get(), k);
+    out.U.ensure(static_cast<size_t>(std::max<i64>(1, m) * k));
+    gemm(c, K_FINAL, false, m, k, r, 1.0, st.Q.get(), st.cap, E.Wk.get(), k, 0.0, out.U.get(), k);
+    SVT_CUDA(cudaStreamSynchronize(c->stream));
+}
+
 static double error_percentage(const QBDev& st) {
     if (!(st.frob_y_sq > 0.0)) throw std::domain_error("error_percentage: target has zero Frobenius norm");
     const double eps = (st.frob_y_sq - st.norm_b_sq) / st.frob_y_sq;
@@ -384,12 +510,21 @@ static void check_sketch_params(const svt_sketch_params& p) {
         throw std::invalid_argument("SketchParams: eps_threshold must lie in (0, 1)");
 }
 
-static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, FinalizeMode mode, double tau) {
+static void finalize_mode(Engine& E, const QBDev& st, FinalizeMode mode, double tau, i64 s_warm, u64 seed,
+                          DevFactors& out) {
+    if (mode == FinalizeMode::Kept)
+        finalize_kept(E, st, tau, s_warm, seed, out);
+    else
+        finalize(E, st, mode, tau, out);
+}
+
+static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, FinalizeMode mode, double tau,
+                          i64 s_warm) {
     SketchOut out;
     int rounds = 0;
     while (error_percentage(st) > p.eps_threshold) {
         if (st.saturated) {
-            finalize(E, st, mode, tau, out.f);
+            finalize_mode(E, st, mode, tau, s_warm, p.seed, out.f);
             out.rank = st.rank;
             out.saturated = true;
             out.rounds = rounds;
@@ -398,7 +533,7 @@ static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, Fina
         ++rounds;
         qb_extend(E, st, p.dt, p.np, derive_seed_u(p.seed, static_cast<u64>(rounds)));
     }
-    finalize(E, st, mode, tau, out.f);
+    finalize_mode(E, st, mode, tau, s_warm, p.seed, out.f);
     out.rank = st.rank;
     out.saturated = false;
     out.rounds = rounds;
@@ -410,7 +545,7 @@ SketchOut r3svd(Engine& E, const svt_sketch_params& p, FinalizeMode mode, double
     check_sketch_params(p);
     QBDev st;
     qb_init(E, st, p.t, p.np, derive_seed_u(p.seed, 0), frob_y_sq);
-    return run_loop(E, st, p, mode, tau);
+    return run_loop(E, st, p, mode, tau, 0);
 }
 
 // sketch.hpp:207-250
@@ -444,7 +579,7 @@ SketchOut r4svd(Engine& E, const double* U_prev, i64 ldu, i64 s, const svt_sketc
     if (s <= 64) {
         E.X2.ensure(static_cast<size_t>(std::max<i64>(1, m) * s));
         copy2d(c, U_prev, ldu, E.X2.get(), s, m, s, dfl(c, F_DRIFT));
-        qr_panel(E, E.X2.get(), s, s, st.Q.get(), st.cap, dfl(c, F_DRIFT));
+        qr_panel(E, m, true, E.X2.get(), s, s, st.Q.get(), st.cap, dfl(c, F_DRIFT));
     } else if (read_flag(c, F_DRIFT)) {
         E.X2.ensure(static_cast<size_t>(std::max<i64>(1, m) * s));
         copy2d(c, U_prev, ldu, E.X2.get(), s, m, s);
@@ -455,7 +590,7 @@ SketchOut r4svd(Engine& E, const double* U_prev, i64 ldu, i64 s, const svt_sketc
     st.frob_y_sq = frob_y_sq;
     st.rank = s;
     st.saturated = (s == min_dim);
-    return run_loop(E, st, p, mode, tau);
+    return run_loop(E, st, p, mode, tau, s);
 }
 
 // sketch.hpp:165-182

@@ -10,10 +10,18 @@
 #include "../../include/svt_b200.h"
 #include "common.hpp"
 
+// Segment plan storage behind svtb::SegPlanView.
+struct SegPlan {
+    svtb::DevBuf<int> seg_row, seg_slot, long_row, long_first, long_count;
+    svtb::DevBuf<long long> seg_beg, seg_end;
+    svtb::SegPlanView v;
+};
+
 // Device SampledMatrix (sampled.hpp:25-110): this rank's row block as CSR
 // (int64 rowptr, int32 col, fp64 val) plus a CSC view whose value array
 // mirrors the CSR values through csr2csc.
 struct svt_mat {
+    SegPlan plan_csr, plan_csc;
     svt_ctx* ctx = nullptr;
     svtb::i64 m = 0, n = 0, row_begin = 0, row_end = 0, m_local = 0, nnz_local = 0, nnz_global = 0;
     svtb::DevBuf<svtb::i64> rowptr;
@@ -76,6 +84,7 @@ double frob_sq(Engine& E);  // ||Y||_F^2 (all ranks)
 void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo);          // Y X (local rows)
 void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out /* n x w, ld w */);  // Y^T X (allreduced)
 void qr_orthonormal(Engine& E, double* X, i64 ldx, i64 w, double* Qout, i64 ldq);            // dense.hpp:103
+void qr_orthonormal(Engine& E, i64 rows, bool dist, double* X, i64 ldx, i64 w, double* Qout, i64 ldq);
 double spectral_norm_est(Engine& E, int iters, u64 seed);                                   // sampled.hpp:188
 
 // sketch.hpp

@@ -62,6 +62,62 @@ void partition_rows(i64 m, const i64* rowptr, int world, i64* bounds) {
     bounds[world] = m;
 }
 
+// Row segmentation for the load-balanced SpMM (sparse.cu): rows longer than
+// kSegLen entries are cut into kSegLen chunks that write partial rows.
+void build_plan(const std::vector<i64>& ptr, i64 nrows, cudaStream_t s, SegPlan& P) {
+    std::vector<int> row, slot, lrow, lfirst, lcount;
+    std::vector<long long> beg, end;
+    int nslots = 0;
+    for (i64 r = 0; r < nrows; ++r) {
+        const i64 b = ptr[static_cast<size_t>(r)], e = ptr[static_cast<size_t>(r + 1)];
+        const i64 len = e - b;
+        if (len <= kSegLen) {
+            row.push_back(static_cast<int>(r));
+            beg.push_back(b);
+            end.push_back(e);
+            slot.push_back(-1);
+            continue;
+        }
+        const i64 nseg = (len + kSegLen - 1) / kSegLen;
+        lrow.push_back(static_cast<int>(r));
+        lfirst.push_back(nslots);
+        lcount.push_back(static_cast<int>(nseg));
+        for (i64 q = 0; q < nseg; ++q) {
+            row.push_back(static_cast<int>(r));
+            beg.push_back(b + q * kSegLen);
+            end.push_back(std::min<long long>(e, b + (q + 1) * kSegLen));
+            slot.push_back(nslots++);
+        }
+    }
+    auto up_i = [&](DevBuf<int>& d, const std::vector<int>& h) {
+        d.alloc(std::max<size_t>(1, h.size()));
+        if (!h.empty()) SVT_CUDA(cudaMemcpyAsync(d.get(), h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, s));
+    };
+    auto up_l = [&](DevBuf<long long>& d, const std::vector<long long>& h) {
+        d.alloc(std::max<size_t>(1, h.size()));
+        if (!h.empty())
+            SVT_CUDA(cudaMemcpyAsync(d.get(), h.data(), sizeof(long long) * h.size(), cudaMemcpyHostToDevice, s));
+    };
+    up_i(P.seg_row, row);
+    up_i(P.seg_slot, slot);
+    up_l(P.seg_beg, beg);
+    up_l(P.seg_end, end);
+    up_i(P.long_row, lrow);
+    up_i(P.long_first, lfirst);
+    up_i(P.long_count, lcount);
+    SVT_CUDA(cudaStreamSynchronize(s));  // host vectors die here
+    P.v.nseg = static_cast<long long>(row.size());
+    P.v.seg_row = P.seg_row.get();
+    P.v.seg_beg = P.seg_beg.get();
+    P.v.seg_end = P.seg_end.get();
+    P.v.seg_slot = P.seg_slot.get();
+    P.v.nlong = static_cast<long long>(lrow.size());
+    P.v.nslots = nslots;
+    P.v.long_row = P.long_row.get();
+    P.v.long_first = P.long_first.get();
+    P.v.long_count = P.long_count.get();
+}
+
 }  // namespace svtb
 
 using svtb::i64;
@@ -129,6 +185,8 @@ svt_mat* svtb_matrix_upload(svt_ctx* ctx, i64 m, i64 n, i64 row_begin, i64 row_e
             SVT_CUDA(cudaMemcpyAsync(M->val_csc.get(), vcsc.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
             SVT_CUDA(cudaMemcpyAsync(M->csr2csc.get(), c2c.data(), sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
         }
+        svtb::build_plan(rp, ml, s, M->plan_csr);
+        svtb::build_plan(cp, n, s, M->plan_csc);
         // global nnz (all ranks)
         double g = static_cast<double>(nnz);
         SVT_CUDA(cudaMemcpyAsync(ctx->d_scalars + 63, &g, sizeof(double), cudaMemcpyHostToDevice, s));

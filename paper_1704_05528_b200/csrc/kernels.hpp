@@ -20,8 +20,8 @@ void gaussian_block_dev(svt_ctx* ctx, i64 rows, i64 cols, u64 seed, double* out,
 // kernel with the respective arrays.
 // nnz and x_rows only feed the algorithmic-bytes accounting (SURVEY §8d:
 // 12 B per entry + 8 B per row pointer + panel in + panel out).
-void spmm(svt_ctx* ctx, int cls, i64 nrows, const i64* ptr, const int* idx, const double* val, i64 nnz, i64 x_rows,
-          i64 w, const double* X, i64 ldx, double* out, i64 ldo);
+void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* idx, const double* val, i64 nnz,
+          i64 x_rows, i64 w, const double* X, i64 ldx, double* out, i64 ldo);
 
 // Fused SDDMM + Bregman update + reductions (sampled.hpp:148-176,
 // solver.hpp:143-168, 321-323).  For each stored (i, j):
@@ -83,6 +83,10 @@ void scale_cols(svt_ctx* ctx, double* X, i64 rows, i64 cols, i64 ld, const doubl
 void copy2d(svt_ctx* ctx, const double* src, i64 lds, double* dst, i64 ldd, i64 rows, i64 cols,
             const int* pred = nullptr);
 void fill(svt_ctx* ctx, double* p, i64 n, double v);
+// Z[:, 0:s] <- the first s columns of the identity (rows x s, ld)
+void set_identity_cols(svt_ctx* ctx, double* Z, i64 rows, i64 ld, i64 s);
+// Y[:, j] -= theta[j] * X[:, j]  (rows x cols, same ld)
+void sub_scaled_cols(svt_ctx* ctx, double* Y, const double* X, i64 rows, i64 cols, i64 ld, const double* theta);
 // out (cols x rows) = in^T ; in (rows x cols, ldi) ; out ld = rows
 void transpose(svt_ctx* ctx, const double* in, i64 rows, i64 cols, i64 ldi, double* out);
 // W2[:, j] = W[:, perm[j]] for j < kcols (perm on device, int)

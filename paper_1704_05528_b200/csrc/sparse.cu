@@ -30,17 +30,22 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// One warp per SEGMENT of at most kSegLen stored entries (host.cpp builds
+// the plan): short rows are one segment and write their output row
+// directly; long rows (power-law users, Zipf-popular items) are split across
+// warps that write partial rows, summed afterwards in segment order
+// (deterministic).
 template <int W>
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) spmm_narrow_kernel(
-    long long nrows, const long long* __restrict__ ptr, const int* __restrict__ idx, const double* __restrict__ val,
-    const double* __restrict__ X, long long ldx, double* __restrict__ out, long long ldo) {
+    SegPlanView plan, const int* __restrict__ idx, const double* __restrict__ val, const double* __restrict__ X,
+    long long ldx, double* __restrict__ out, long long ldo, double* __restrict__ partial) {
     const int lane = threadIdx.x & 31;
-    const long long row = static_cast<long long>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
-    if (row >= nrows) return;
+    const long long sg = static_cast<long long>(blockIdx.x) * kWarpsPerBlock + (threadIdx.x >> 5);
+    if (sg >= plan.nseg) return;
     double acc[W];
 #pragma unroll
     for (int j = 0; j < W; ++j) acc[j] = 0.0;
-    const long long beg = ptr[row], end = ptr[row + 1];
+    const long long beg = plan.seg_beg[sg], end = plan.seg_end[sg];
     for (long long k = beg + lane; k < end; k += 32) {
         const int c = __ldg(idx + k);
         const double v = __ldg(val + k);
@@ -54,22 +59,28 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) spmm_narrow_kernel(
         const double s = warp_sum(acc[j]);
         if (lane == j) mine = s;
     }
-    if (lane < W) out[row * ldo + lane] = mine;
+    if (lane < W) {
+        const int slot = plan.seg_slot[sg];
+        if (slot < 0)
+            out[static_cast<long long>(plan.seg_row[sg]) * ldo + lane] = mine;
+        else
+            partial[static_cast<long long>(slot) * W + lane] = mine;
+    }
 }
 
-// wide: block = 4 warps, each warp one row, 128 columns (4 per lane) at
+// wide: block = 4 warps, each warp one segment, 128 columns (4 per lane) at
 // column chunk blockIdx.y
-__global__ void __launch_bounds__(128) spmm_wide_kernel(long long nrows, const long long* __restrict__ ptr,
-                                                        const int* __restrict__ idx,
+__global__ void __launch_bounds__(128) spmm_wide_kernel(SegPlanView plan, const int* __restrict__ idx,
                                                         const double* __restrict__ val,
                                                         const double* __restrict__ X, long long ldx, long long w,
-                                                        double* __restrict__ out, long long ldo) {
+                                                        double* __restrict__ out, long long ldo,
+                                                        double* __restrict__ partial) {
     const int lane = threadIdx.x & 31;
-    const long long row = static_cast<long long>(blockIdx.x) * 4 + (threadIdx.x >> 5);
-    if (row >= nrows) return;
+    const long long sg = static_cast<long long>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+    if (sg >= plan.nseg) return;
     const long long c0 = static_cast<long long>(blockIdx.y) * 128;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    const long long beg = ptr[row], end = ptr[row + 1];
+    const long long beg = plan.seg_beg[sg], end = plan.seg_end[sg];
     for (long long k0 = beg; k0 < end; k0 += 32) {
         const long long k = k0 + lane;
         int cl = 0;
@@ -90,19 +101,36 @@ __global__ void __launch_bounds__(128) spmm_wide_kernel(long long nrows, const l
             }
         }
     }
+    const int slot = plan.seg_slot[sg];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const long long j = c0 + lane + 32 * q;
-        if (j < w) out[row * ldo + j] = acc[q];
+        if (j >= w) continue;
+        if (slot < 0)
+            out[static_cast<long long>(plan.seg_row[sg]) * ldo + j] = acc[q];
+        else
+            partial[static_cast<long long>(slot) * w + j] = acc[q];
     }
 }
 
+// out[row, j] = sum of the row's partial slots, in segment order
+__global__ void seg_reduce_kernel(SegPlanView plan, long long w, const double* __restrict__ partial,
+                                  double* __restrict__ out, long long ldo) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= plan.nlong * w) return;
+    const long long l = e / w, j = e % w;
+    const int first = plan.long_first[l], cnt = plan.long_count[l];
+    double s = 0.0;
+    for (int t = 0; t < cnt; ++t) s += partial[static_cast<long long>(first + t) * w + j];
+    out[static_cast<long long>(plan.long_row[l]) * ldo + j] = s;
+}
+
 template <int W>
-void launch_narrow(svt_ctx* ctx, i64 nrows, const i64* ptr, const int* idx, const double* val, const double* X,
-                   i64 ldx, double* out, i64 ldo) {
-    const unsigned blocks = static_cast<unsigned>((nrows + kWarpsPerBlock - 1) / kWarpsPerBlock);
-    spmm_narrow_kernel<W><<<blocks, 32 * kWarpsPerBlock, 0, ctx->stream>>>(
-        nrows, reinterpret_cast<const long long*>(ptr), idx, val, X, ldx, out, ldo);
+void launch_narrow(svt_ctx* ctx, const SegPlanView& plan, const int* idx, const double* val, const double* X,
+                   i64 ldx, double* out, i64 ldo, double* partial) {
+    const unsigned blocks = static_cast<unsigned>((plan.nseg + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    spmm_narrow_kernel<W><<<blocks, 32 * kWarpsPerBlock, 0, ctx->stream>>>(plan, idx, val, X, ldx, out, ldo,
+                                                                         partial);
 }
 
 // ---- fused SDDMM + Bregman update + reductions ------------------------------
@@ -203,18 +231,23 @@ __global__ void densify_kernel(long long m_local, long long n, const long long* 
 
 }  // namespace
 
-void spmm(svt_ctx* ctx, int cls, i64 nrows, const i64* ptr, const int* idx, const double* val, i64 nnz, i64 x_rows,
-          i64 w, const double* X, i64 ldx, double* out, i64 ldo) {
+void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* idx, const double* val, i64 nnz,
+          i64 x_rows, i64 w, const double* X, i64 ldx, double* out, i64 ldo) {
     if (nrows <= 0 || w <= 0) return;
     // algorithmic bytes: 12 B per stored entry (int32 index +
     // fp64 value) + 8 B per row pointer + the dense panel read once + the
     // output panel written once; 2 flops per entry per column.
     LaunchScope ls(ctx, cls, 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * w * (x_rows + nrows), 2.0 * nnz * w);
+    double* partial = nullptr;
+    if (plan.nlong > 0) {
+        ctx->ws_spmm.ensure(static_cast<size_t>(plan.nslots * w));
+        partial = ctx->ws_spmm.get();
+    }
     if (w <= 16) {
         switch (w) {
-#define SVT_CASE(W)                                                          \
-    case W:                                                                  \
-        launch_narrow<W>(ctx, nrows, ptr, idx, val, X, ldx, out, ldo);       \
+#define SVT_CASE(W)                                                             \
+    case W:                                                                     \
+        launch_narrow<W>(ctx, plan, idx, val, X, ldx, out, ldo, partial);       \
         break;
             SVT_CASE(1) SVT_CASE(2) SVT_CASE(3) SVT_CASE(4) SVT_CASE(5) SVT_CASE(6) SVT_CASE(7) SVT_CASE(8)
             SVT_CASE(9) SVT_CASE(10) SVT_CASE(11) SVT_CASE(12) SVT_CASE(13) SVT_CASE(14) SVT_CASE(15) SVT_CASE(16)
@@ -223,9 +256,13 @@ void spmm(svt_ctx* ctx, int cls, i64 nrows, const i64* ptr, const int* idx, cons
                 break;
         }
     } else {
-        dim3 grid(static_cast<unsigned>((nrows + 3) / 4), static_cast<unsigned>((w + 127) / 128));
-        spmm_wide_kernel<<<grid, 128, 0, ctx->stream>>>(nrows, reinterpret_cast<const long long*>(ptr), idx, val, X,
-                                                        ldx, w, out, ldo);
+        dim3 grid(static_cast<unsigned>((plan.nseg + 3) / 4), static_cast<unsigned>((w + 127) / 128));
+        spmm_wide_kernel<<<grid, 128, 0, ctx->stream>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+    }
+    if (plan.nlong > 0) {
+        const i64 tot = plan.nlong * w;
+        seg_reduce_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(plan, w, partial, out,
+                                                                                          ldo);
     }
 }
 
