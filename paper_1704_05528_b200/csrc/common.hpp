@@ -151,6 +151,7 @@ struct svt_ctx {
     svtb::DevBuf<double> ws_partial;   // split-K / reduction partials
     svtb::DevBuf<double> ws_partial2;  // second partial buffer (reductions)
     svtb::DevBuf<double> ws_spmm;      // long-row partials of the segmented SpMM
+    svtb::DevBuf<unsigned> ws_counters;  // last-CTA-reduces counters (self-resetting)
     svtb::DevBuf<unsigned long long> ws_rng;  // raw mt19937_64 draws
     svtb::DevBuf<unsigned long long> ws_mt;   // persistent mt state (312 words + index)
     svtb::DevBuf<double> ws_eig;              // Jacobi eigensolver workspace

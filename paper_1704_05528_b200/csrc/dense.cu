@@ -166,6 +166,297 @@ void gemm_launch(svt_ctx* ctx, bool transA, i64 M, i64 N, i64 K, double alpha, c
 }
 
 // ---------------------------------------------------------------------------
+// Skinny GEMMs of the rank-revealing rounds (N = dt <= 16 output columns).
+// These stream the basis Q once per pass at HBM rate; the tile GEMM above
+// serves the wide cases.
+// ---------------------------------------------------------------------------
+
+// C (M x N) = alpha * A^T B + beta * C;  A: K x M row-major (Q), B: K x N (X).
+// One thread per column of A (coalesced row segments of Q), 32 rows of B
+// staged in shared memory and broadcast, K split across blockIdx.y; the last
+// CTA of each column tile reduces the split partials in fixed order
+// (deterministic, no separate reduction launch).
+constexpr int kTnThreads = 256;
+constexpr int kTnRows = 32;
+
+template <int N>
+__global__ void __launch_bounds__(kTnThreads) skinny_tn_kernel(
+    long long M, long long K, const double* __restrict__ A, long long lda, const double* __restrict__ B,
+    long long ldb, double alpha, double beta, double* __restrict__ C, long long ldc, long long rows_per_split,
+    double* __restrict__ partial, unsigned* __restrict__ counters, const int* __restrict__ pred) {
+    if (pred != nullptr && *pred == 0) return;
+    __shared__ double Bs[kTnRows][N];
+    __shared__ bool last;
+    const long long c = blockIdx.x * static_cast<long long>(kTnThreads) + threadIdx.x;
+    const long long k0 = blockIdx.y * rows_per_split;
+    const long long k1 = min(K, k0 + rows_per_split);
+    double acc[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) acc[j] = 0.0;
+    for (long long kb = k0; kb < k1; kb += kTnRows) {
+        const int nr = static_cast<int>(min(static_cast<long long>(kTnRows), k1 - kb));
+        __syncthreads();
+        for (int e = threadIdx.x; e < kTnRows * N; e += kTnThreads) {
+            const int rr = e / N, jj = e % N;
+            Bs[rr][jj] = (rr < nr) ? __ldg(B + (kb + rr) * ldb + jj) : 0.0;
+        }
+        __syncthreads();
+        if (c < M) {
+            const double* ap = A + kb * lda + c;
+            if (nr == kTnRows) {
+#pragma unroll 8
+                for (int rr = 0; rr < kTnRows; ++rr) {
+                    const double a = __ldg(ap + rr * lda);
+#pragma unroll
+                    for (int j = 0; j < N; ++j) acc[j] = fma(a, Bs[rr][j], acc[j]);
+                }
+            } else {
+                for (int rr = 0; rr < nr; ++rr) {
+                    const double a = __ldg(ap + rr * lda);
+#pragma unroll
+                    for (int j = 0; j < N; ++j) acc[j] = fma(a, Bs[rr][j], acc[j]);
+                }
+            }
+        }
+    }
+    if (gridDim.y == 1) {
+        if (c < M)
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const double o = (beta != 0.0) ? beta * C[c * ldc + j] : 0.0;
+                C[c * ldc + j] = fma(alpha, acc[j], o);
+            }
+        return;
+    }
+    if (c < M)
+#pragma unroll
+        for (int j = 0; j < N; ++j) partial[(blockIdx.y * M + c) * N + j] = acc[j];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(counters + blockIdx.x, 1u) == gridDim.y - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (c < M)
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            double s = 0.0;
+            for (unsigned z = 0; z < gridDim.y; ++z) s += __ldcg(partial + (z * M + c) * N + j);
+            const double o = (beta != 0.0) ? beta * C[c * ldc + j] : 0.0;
+            C[c * ldc + j] = fma(alpha, s, o);
+        }
+    if (threadIdx.x == 0) counters[blockIdx.x] = 0u;
+}
+
+// C (M x N) = alpha * A B + beta * C;  A: M x K row-major (Q), B: K x N.
+// One warp per kNnRows rows, lanes stride K (coalesced row segments of A),
+// B staged transposed in shared memory (conflict-free per lane); per-row
+// warp-shuffle reduction at the end.
+constexpr int kNnWarps = 8, kNnRows = 4, kNnChunk = 256;
+
+template <int N>
+__global__ void __launch_bounds__(32 * kNnWarps) skinny_nn_kernel(long long M, long long K, double alpha,
+                                                                  const double* __restrict__ A, long long lda,
+                                                                  const double* __restrict__ B, long long ldb,
+                                                                  double beta, double* __restrict__ C, long long ldc,
+                                                                  const int* __restrict__ pred) {
+    if (pred != nullptr && *pred == 0) return;
+    __shared__ double Bs[N][kNnChunk];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long r0 = (static_cast<long long>(blockIdx.x) * kNnWarps + warp) * kNnRows;
+    double acc[kNnRows][N];
+#pragma unroll
+    for (int r = 0; r < kNnRows; ++r)
+#pragma unroll
+        for (int j = 0; j < N; ++j) acc[r][j] = 0.0;
+    const double* ar[kNnRows];
+    bool ok[kNnRows];
+#pragma unroll
+    for (int r = 0; r < kNnRows; ++r) {
+        ok[r] = (r0 + r) < M;
+        ar[r] = A + (ok[r] ? (r0 + r) : 0) * lda;
+    }
+    for (long long kb = 0; kb < K; kb += kNnChunk) {
+        const int nk = static_cast<int>(min(static_cast<long long>(kNnChunk), K - kb));
+        __syncthreads();
+        for (int e = threadIdx.x; e < kNnChunk * N; e += 32 * kNnWarps) {
+            const int kk = e / N, jj = e % N;
+            Bs[jj][kk] = (kk < nk) ? __ldg(B + (kb + kk) * ldb + jj) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int kk = lane; kk < nk; kk += 32) {
+            double b[N];
+#pragma unroll
+            for (int j = 0; j < N; ++j) b[j] = Bs[j][kk];
+#pragma unroll
+            for (int r = 0; r < kNnRows; ++r) {
+                const double a = ok[r] ? __ldg(ar[r] + kb + kk) : 0.0;
+#pragma unroll
+                for (int j = 0; j < N; ++j) acc[r][j] = fma(a, b[j], acc[r][j]);
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kNnRows; ++r) {
+        double mine = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double s = warp_sum(acc[r][j]);
+            if (lane == j) mine = s;
+        }
+        if (ok[r] && lane < N) {
+            double* cp = C + (r0 + r) * ldc + lane;
+            const double o = (beta != 0.0) ? beta * (*cp) : 0.0;
+            *cp = fma(alpha, mine, o);
+        }
+    }
+}
+
+// Gram-type C = A^T B with M, N <= 16 and long K (a narrow panel's Gram
+// matrix): warps stride rows, lanes own (a, b) products; the last CTA
+// reduces the per-CTA partials in fixed order and, for a Cholesky QR pass,
+// factors the Gram right there (Rinv = L^{-T}, status = 1 on a bad pivot).
+constexpr int kTinyThreads = 256;
+constexpr int kTinyMaxW = 16;
+
+__global__ void __launch_bounds__(kTinyThreads) tiny_tn_kernel(long long K, int M, int N,
+                                                               const double* __restrict__ A, long long lda,
+                                                               const double* __restrict__ B, long long ldb,
+                                                               double* __restrict__ C, double* __restrict__ partial,
+                                                               unsigned* __restrict__ counter, int do_chol,
+                                                               double* __restrict__ Rinv, int* __restrict__ status,
+                                                               const int* __restrict__ pred) {
+    if (pred != nullptr && *pred == 0) return;
+    __shared__ double red[kTinyThreads / 32][kTinyMaxW * kTinyMaxW];
+    __shared__ double L[kTinyMaxW][kTinyMaxW + 1];
+    __shared__ double dorig[kTinyMaxW];
+    __shared__ bool last;
+    __shared__ int fail;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int P = M * N;
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    const long long gw = blockIdx.x * static_cast<long long>(kTinyThreads / 32) + warp;
+    const long long nw = static_cast<long long>(gridDim.x) * (kTinyThreads / 32);
+    for (long long i = gw; i < K; i += nw) {
+        const double* ai = A + i * lda;
+        const double* bi = B + i * ldb;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int p = lane + 32 * q;
+            if (p < P) acc[q] = fma(__ldg(ai + p / N), __ldg(bi + p % N), acc[q]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int p = lane + 32 * q;
+        if (p < P) red[warp][p] = acc[q];
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < P; p += kTinyThreads) {
+        double s = 0.0;
+        for (int w = 0; w < kTinyThreads / 32; ++w) s += red[w][p];
+        partial[blockIdx.x * static_cast<long long>(kTinyMaxW * kTinyMaxW) + p] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int p = threadIdx.x; p < P; p += kTinyThreads) {
+        double s = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(partial + b * static_cast<long long>(kTinyMaxW * kTinyMaxW) + p);
+        C[p] = s;
+        L[p / N][p % N] = s;
+    }
+    if (threadIdx.x == 0) {
+        *counter = 0u;
+        fail = 0;
+    }
+    __syncthreads();
+    if (!do_chol) return;
+    const int w = M;
+    if (threadIdx.x < w) dorig[threadIdx.x] = L[threadIdx.x][threadIdx.x];
+    __syncthreads();
+    for (int j = 0; j < w; ++j) {
+        const double d = L[j][j];
+        const bool bad = !(dorig[j] > 0.0) || !(d > 1e-13 * dorig[j]) || !(d < CUDART_INF);
+        const double ljj = sqrt(bad ? 1.0 : d);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (bad) fail = 1;
+            L[j][j] = ljj;
+        }
+        for (int i = j + 1 + threadIdx.x; i < w; i += kTinyThreads) L[i][j] /= ljj;
+        __syncthreads();
+        const int rem = w - j - 1;
+        for (int e = threadIdx.x; e < rem * rem; e += kTinyThreads) {
+            const int i = j + 1 + e / rem, k = j + 1 + e % rem;
+            if (k <= i) L[i][k] -= L[i][j] * L[k][j];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < w) {
+        const int c = threadIdx.x;
+        double x[kTinyMaxW];
+        for (int r = 0; r < w; ++r) x[r] = 0.0;
+        x[c] = 1.0 / L[c][c];
+        for (int r = c - 1; r >= 0; --r) {
+            double s = 0.0;
+            for (int t = r + 1; t <= c; ++t) s += L[t][r] * x[t];
+            x[r] = -s / L[r][r];
+        }
+        for (int r = 0; r < w; ++r) Rinv[r * w + c] = x[r];
+    }
+    if (threadIdx.x == 0 && fail) status[0] = 1;
+}
+
+unsigned* counters(svt_ctx* ctx) {
+    if (ctx->ws_counters.n < 8192) {
+        ctx->ws_counters.alloc(8192);
+        SVT_CUDA(cudaMemsetAsync(ctx->ws_counters.get(), 0, 8192 * sizeof(unsigned), ctx->stream));
+    }
+    return ctx->ws_counters.get();
+}
+
+template <int N>
+void skinny_tn_launch(svt_ctx* ctx, i64 M, i64 K, double alpha, const double* A, i64 lda, const double* B, i64 ldb,
+                      double beta, double* C, i64 ldc, const int* pred) {
+    const i64 tiles = (M + kTnThreads - 1) / kTnThreads;
+    if (tiles > 8000) throw std::invalid_argument("skinny_tn: too many column tiles");
+    i64 splits = std::max<i64>(1, std::min<i64>((4LL * ctx->num_sms + tiles - 1) / tiles, (K + 255) / 256));
+    while (splits > 1 && splits * M * N > (32LL << 20)) splits /= 2;
+    i64 rps = (K + splits - 1) / splits;
+    rps = ((rps + kTnRows - 1) / kTnRows) * kTnRows;
+    splits = std::max<i64>(1, (K + rps - 1) / rps);
+    unsigned* cnt = counters(ctx);
+    if (splits > 1) ctx->ws_partial.ensure(static_cast<size_t>(splits * M * N));
+    dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(splits));
+    skinny_tn_kernel<N><<<grid, kTnThreads, 0, ctx->stream>>>(M, K, A, lda, B, ldb, alpha, beta, C, ldc, rps,
+                                                              ctx->ws_partial.get(), cnt, pred);
+}
+
+template <int N>
+void skinny_nn_launch(svt_ctx* ctx, i64 M, i64 K, double alpha, const double* A, i64 lda, const double* B, i64 ldb,
+                      double beta, double* C, i64 ldc, const int* pred) {
+    const i64 rows_per_block = static_cast<i64>(kNnWarps) * kNnRows;
+    const unsigned blocks = static_cast<unsigned>((M + rows_per_block - 1) / rows_per_block);
+    skinny_nn_kernel<N><<<blocks, 32 * kNnWarps, 0, ctx->stream>>>(M, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
+}
+
+void tiny_tn_launch(svt_ctx* ctx, i64 K, int M, int N, const double* A, i64 lda, const double* B, i64 ldb, double* C,
+                    bool do_chol, double* Rinv, int* status, const int* pred) {
+    const i64 blocks = std::max<i64>(1, std::min<i64>(2LL * ctx->num_sms, (K + 127) / 128));
+    unsigned* cnt = counters(ctx) + 8191;
+    ctx->ws_partial2.ensure(static_cast<size_t>(blocks * kTinyMaxW * kTinyMaxW));
+    tiny_tn_kernel<<<static_cast<unsigned>(blocks), kTinyThreads, 0, ctx->stream>>>(
+        K, M, N, A, lda, B, ldb, C, ctx->ws_partial2.get(), cnt, do_chol ? 1 : 0, Rinv, status, pred);
+}
+
+// ---------------------------------------------------------------------------
 // reductions
 // ---------------------------------------------------------------------------
 constexpr int kRedBlocks = 256;
@@ -695,10 +986,35 @@ void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha,
         scale2d_kernel<<<nblk(M * N), 256, 0, ctx->stream>>>(C, M, N, ldc, beta, pred);
         return;
     }
-    if (N <= 16)
-        gemm_launch<128, 16, 16, 4, 4>(ctx, transA, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
-    else
-        gemm_launch<64, 64, 16, 4, 4>(ctx, transA, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
+    if (N <= 16) {
+        if (transA && M <= kTinyMaxW && alpha == 1.0 && beta == 0.0 && ldc == N) {
+            tiny_tn_launch(ctx, K, static_cast<int>(M), static_cast<int>(N), A, lda, B, ldb, C, false, nullptr,
+                           nullptr, pred);
+            return;
+        }
+        switch (N) {
+#define SVT_CASE(NN)                                                                            \
+    case NN:                                                                                    \
+        if (transA)                                                                             \
+            skinny_tn_launch<NN>(ctx, M, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);         \
+        else                                                                                    \
+            skinny_nn_launch<NN>(ctx, M, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);         \
+        return;
+            SVT_CASE(1) SVT_CASE(2) SVT_CASE(3) SVT_CASE(4) SVT_CASE(5) SVT_CASE(6) SVT_CASE(7) SVT_CASE(8)
+            SVT_CASE(9) SVT_CASE(10) SVT_CASE(11) SVT_CASE(12) SVT_CASE(13) SVT_CASE(14) SVT_CASE(15) SVT_CASE(16)
+#undef SVT_CASE
+            default:
+                break;
+        }
+    }
+    gemm_launch<64, 64, 16, 4, 4>(ctx, transA, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
+}
+
+void gram_chol(svt_ctx* ctx, const double* X, i64 ldx, i64 m, i64 w, double* G, double* Rinv, int* status,
+               const int* pred) {
+    if (w > kTinyMaxW) throw std::invalid_argument("gram_chol: panel wider than 16");
+    LaunchScope ls(ctx, K_QR, 8.0 * m * w, 1.0 * m * w * w);
+    tiny_tn_launch(ctx, m, static_cast<int>(w), static_cast<int>(w), X, ldx, X, ldx, G, true, Rinv, status, pred);
 }
 
 void sumsq(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double* d_out, int op, const int* pred) {

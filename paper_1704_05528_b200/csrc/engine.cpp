@@ -84,6 +84,17 @@ void qr_panel(Engine& E, i64 m, bool dist, const double* X, i64 ldx, i64 w, doub
     E.tmp.ensure(static_cast<size_t>(std::max<i64>(1, m) * w));
     int* status = dfl(c, F_QRSTAT);
     zero_flag(c, F_QRSTAT);
+    if (!dist && w <= 16) {
+        // fused: Gram + Cholesky + Rinv in one launch, then the triangular
+        // apply; twice (CholQR2), then the predicated Householder fallback
+        gram_chol(c, X, ldx, m, w, E.G.get(), E.Rinv.get(), status, pred);
+        gemm(c, K_QR, false, m, w, w, 1.0, X, ldx, E.Rinv.get(), w, 0.0, E.tmp.get(), w, pred);
+        gram_chol(c, E.tmp.get(), w, m, w, E.G.get(), E.Rinv.get(), status, pred);
+        gemm(c, K_QR, false, m, w, w, 1.0, E.tmp.get(), w, E.Rinv.get(), w, 0.0, Qout, ldq, pred);
+        E.hh.ensure(static_cast<size_t>(std::max<i64>(1, m) * w));
+        householder_qr(c, X, m, w, ldx, Qout, ldq, E.hh.get(), pred, status);
+        return;
+    }
     // pass 1: R1 = chol(X^T X), Q1 = X R1^{-1}
     gemm(c, K_QR, true, w, w, m, 1.0, X, ldx, X, ldx, 0.0, E.G.get(), w, pred);
     if (dist) allreduce(c, E.G.get(), static_cast<size_t>(w * w));

@@ -52,6 +52,12 @@ void densify_dev(svt_ctx* ctx, i64 m_local, i64 n, const i64* rowptr, const int*
 void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
           const double* B, i64 ldb, double beta, double* C, i64 ldc, const int* pred = nullptr);
 
+// Fused Cholesky-QR pass head for a narrow panel (w <= 16, single rank):
+// G = X^T X reduced on the device, then Cholesky and Rinv = L^{-T} in the
+// same launch; status[0] = 1 on an unsafe pivot.
+void gram_chol(svt_ctx* ctx, const double* X, i64 ldx, i64 m, i64 w, double* G, double* Rinv, int* status,
+               const int* pred);
+
 // d_out[0] (op) sum of squares of X (rows x cols, ld).  op: 0 store, 1 add.
 void sumsq(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double* d_out, int op,
            const int* pred = nullptr);
