@@ -109,7 +109,7 @@ void nccl_unique_id(void* out128);
 
 // Load-balanced row segmentation of a CSR / CSC view (host.cpp builds it at
 // upload): every row is one or more segments of <= kSegLen entries.
-constexpr long long kSegLen = 2048;
+constexpr long long kSegLen = 512;
 struct SegPlanView {
     long long nseg = 0;
     const int* seg_row = nullptr;

@@ -172,79 +172,95 @@ void gemm_launch(svt_ctx* ctx, bool transA, i64 M, i64 N, i64 K, double alpha, c
 // ---------------------------------------------------------------------------
 
 // C (M x N) = alpha * A^T B + beta * C;  A: K x M row-major (Q), B: K x N (X).
-// One thread per column of A (coalesced row segments of Q), 32 rows of B
-// staged in shared memory and broadcast, K split across blockIdx.y; the last
-// CTA of each column tile reduces the split partials in fixed order
-// (deterministic, no separate reduction launch).
-constexpr int kTnThreads = 256;
+// A CTA owns 32 columns of A (lane = column: one 256-byte row segment per
+// load) and a slab of rows split over its 8 warps; each warp stages 32 rows
+// of B in its own shared-memory slice (__syncwarp only) and keeps kTnUnroll
+// independent loads of A in flight.  The 8 warp partials are folded in
+// shared memory; CTAs along the row split write partials and the last CTA
+// of each column group reduces them in fixed order (deterministic, no extra
+// launch).
+constexpr int kTnWarps = 8;
 constexpr int kTnRows = 32;
+constexpr int kTnUnroll = 16;
 
 template <int N>
-__global__ void __launch_bounds__(kTnThreads) skinny_tn_kernel(
+__global__ void __launch_bounds__(32 * kTnWarps) skinny_tn_kernel(
     long long M, long long K, const double* __restrict__ A, long long lda, const double* __restrict__ B,
-    long long ldb, double alpha, double beta, double* __restrict__ C, long long ldc, long long rows_per_split,
+    long long ldb, double alpha, double beta, double* __restrict__ C, long long ldc, long long rows_per_cta,
     double* __restrict__ partial, unsigned* __restrict__ counters, const int* __restrict__ pred) {
     if (pred != nullptr && *pred == 0) return;
-    __shared__ double Bs[kTnRows][N];
+    // one buffer per warp: staged B rows during the stream, then the
+    // warp's per-column partials (stride N + 1) for the CTA fold
+    __shared__ double sm[kTnWarps][32 * (N + 1)];
     __shared__ bool last;
-    const long long c = blockIdx.x * static_cast<long long>(kTnThreads) + threadIdx.x;
-    const long long k0 = blockIdx.y * rows_per_split;
-    const long long k1 = min(K, k0 + rows_per_split);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* Bs = sm[warp];
+    const long long c = blockIdx.x * 32LL + lane;
+    const bool cok = c < M;
+    const long long cta_k0 = blockIdx.y * rows_per_cta;
+    const long long cta_k1 = min(K, cta_k0 + rows_per_cta);
+    const long long per_warp = (rows_per_cta + kTnWarps - 1) / kTnWarps;
+    const long long k0 = min(cta_k1, cta_k0 + warp * per_warp);
+    const long long k1 = min(cta_k1, k0 + per_warp);
     double acc[N];
 #pragma unroll
     for (int j = 0; j < N; ++j) acc[j] = 0.0;
+    const double* ac = A + (cok ? c : 0);
     for (long long kb = k0; kb < k1; kb += kTnRows) {
         const int nr = static_cast<int>(min(static_cast<long long>(kTnRows), k1 - kb));
-        __syncthreads();
-        for (int e = threadIdx.x; e < kTnRows * N; e += kTnThreads) {
-            const int rr = e / N, jj = e % N;
-            Bs[rr][jj] = (rr < nr) ? __ldg(B + (kb + rr) * ldb + jj) : 0.0;
+        __syncwarp();
+        for (int e = lane; e < kTnRows * N; e += 32) {
+            const int rr = e / N, jj = e - (e / N) * N;
+            Bs[rr * N + jj] = (rr < nr) ? __ldg(B + (kb + rr) * ldb + jj) : 0.0;
         }
-        __syncthreads();
-        if (c < M) {
-            const double* ap = A + kb * lda + c;
-            if (nr == kTnRows) {
-#pragma unroll 8
-                for (int rr = 0; rr < kTnRows; ++rr) {
-                    const double a = __ldg(ap + rr * lda);
+        __syncwarp();
+        const double* ap = ac + kb * lda;
 #pragma unroll
-                    for (int j = 0; j < N; ++j) acc[j] = fma(a, Bs[rr][j], acc[j]);
-                }
-            } else {
-                for (int rr = 0; rr < nr; ++rr) {
-                    const double a = __ldg(ap + rr * lda);
+        for (int r0 = 0; r0 < kTnRows; r0 += kTnUnroll) {
+            double a[kTnUnroll];
 #pragma unroll
-                    for (int j = 0; j < N; ++j) acc[j] = fma(a, Bs[rr][j], acc[j]);
-                }
-            }
+            for (int u = 0; u < kTnUnroll; ++u) a[u] = (cok && r0 + u < nr) ? __ldg(ap + (r0 + u) * lda) : 0.0;
+#pragma unroll
+            for (int u = 0; u < kTnUnroll; ++u)
+#pragma unroll
+                for (int j = 0; j < N; ++j) acc[j] = fma(a[u], Bs[(r0 + u) * N + j], acc[j]);
         }
     }
-    if (gridDim.y == 1) {
-        if (c < M)
+    __syncwarp();
 #pragma unroll
-            for (int j = 0; j < N; ++j) {
-                const double o = (beta != 0.0) ? beta * C[c * ldc + j] : 0.0;
-                C[c * ldc + j] = fma(alpha, acc[j], o);
-            }
-        return;
+    for (int j = 0; j < N; ++j) Bs[lane * (N + 1) + j] = acc[j];
+    __syncthreads();
+    // fold the 8 warps: thread t -> (column lane t % 32, output j range)
+    for (int e = threadIdx.x; e < 32 * N; e += 32 * kTnWarps) {
+        const int cl = e / N, j = e - (e / N) * N;
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < kTnWarps; ++w) s += sm[w][cl * (N + 1) + j];
+        const long long cc = blockIdx.x * 32LL + cl;
+        if (cc >= M) continue;
+        if (gridDim.y == 1) {
+            const double o = (beta != 0.0) ? beta * C[cc * ldc + j] : 0.0;
+            C[cc * ldc + j] = fma(alpha, s, o);
+        } else {
+            partial[(blockIdx.y * M + cc) * N + j] = s;
+        }
     }
-    if (c < M)
-#pragma unroll
-        for (int j = 0; j < N; ++j) partial[(blockIdx.y * M + c) * N + j] = acc[j];
+    if (gridDim.y == 1) return;
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) last = (atomicAdd(counters + blockIdx.x, 1u) == gridDim.y - 1);
     __syncthreads();
     if (!last) return;
     __threadfence();
-    if (c < M)
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-            double s = 0.0;
-            for (unsigned z = 0; z < gridDim.y; ++z) s += __ldcg(partial + (z * M + c) * N + j);
-            const double o = (beta != 0.0) ? beta * C[c * ldc + j] : 0.0;
-            C[c * ldc + j] = fma(alpha, s, o);
-        }
+    for (int e = threadIdx.x; e < 32 * N; e += 32 * kTnWarps) {
+        const int cl = e / N, j = e - (e / N) * N;
+        const long long cc = blockIdx.x * 32LL + cl;
+        if (cc >= M) continue;
+        double s = 0.0;
+        for (unsigned z = 0; z < gridDim.y; ++z) s += __ldcg(partial + (z * M + cc) * N + j);
+        const double o = (beta != 0.0) ? beta * C[cc * ldc + j] : 0.0;
+        C[cc * ldc + j] = fma(alpha, s, o);
+    }
     if (threadIdx.x == 0) counters[blockIdx.x] = 0u;
 }
 
@@ -425,18 +441,21 @@ unsigned* counters(svt_ctx* ctx) {
 template <int N>
 void skinny_tn_launch(svt_ctx* ctx, i64 M, i64 K, double alpha, const double* A, i64 lda, const double* B, i64 ldb,
                       double beta, double* C, i64 ldc, const int* pred) {
-    const i64 tiles = (M + kTnThreads - 1) / kTnThreads;
-    if (tiles > 8000) throw std::invalid_argument("skinny_tn: too many column tiles");
-    i64 splits = std::max<i64>(1, std::min<i64>((4LL * ctx->num_sms + tiles - 1) / tiles, (K + 255) / 256));
+    const i64 groups = (M + 31) / 32;
+    if (groups > 8000) throw std::invalid_argument("skinny_tn: too many column groups");
+    // aim for ~6 CTAs per SM overall; at least 32 rows per warp
+    i64 splits = std::max<i64>(1, (6LL * ctx->num_sms + groups - 1) / groups);
+    splits = std::min<i64>(splits, std::max<i64>(1, K / (kTnWarps * 32)));
+    splits = std::min<i64>(splits, 4096);
     while (splits > 1 && splits * M * N > (32LL << 20)) splits /= 2;
-    i64 rps = (K + splits - 1) / splits;
-    rps = ((rps + kTnRows - 1) / kTnRows) * kTnRows;
-    splits = std::max<i64>(1, (K + rps - 1) / rps);
+    i64 rpc = (K + splits - 1) / splits;
+    rpc = ((rpc + kTnWarps * kTnRows - 1) / (kTnWarps * kTnRows)) * (kTnWarps * kTnRows);
+    splits = std::max<i64>(1, (K + rpc - 1) / rpc);
     unsigned* cnt = counters(ctx);
     if (splits > 1) ctx->ws_partial.ensure(static_cast<size_t>(splits * M * N));
-    dim3 grid(static_cast<unsigned>(tiles), static_cast<unsigned>(splits));
-    skinny_tn_kernel<N><<<grid, kTnThreads, 0, ctx->stream>>>(M, K, A, lda, B, ldb, alpha, beta, C, ldc, rps,
-                                                              ctx->ws_partial.get(), cnt, pred);
+    dim3 grid(static_cast<unsigned>(groups), static_cast<unsigned>(splits));
+    skinny_tn_kernel<N><<<grid, 32 * kTnWarps, 0, ctx->stream>>>(M, K, A, lda, B, ldb, alpha, beta, C, ldc, rpc,
+                                                                 ctx->ws_partial.get(), cnt, pred);
 }
 
 template <int N>

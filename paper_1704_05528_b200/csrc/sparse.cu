@@ -54,25 +54,37 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) spmm_narrow_kernel(
     if (sg >= plan.nseg) return;
     double acc = 0.0;
     const long long beg = plan.seg_beg[sg], end = plan.seg_end[sg];
+    constexpr int STEPS = (32 + G - 1) / G;
+    // software pipeline: the next 32 indices / values are in flight while
+    // the current chunk's gathers issue (all STEPS gathers independent)
+    int cl_n = 0;
+    double vl_n = 0.0;
+    if (beg + lane < end) {
+        cl_n = __ldg(idx + beg + lane);
+        vl_n = __ldg(val + beg + lane);
+    }
     for (long long base = beg; base < end; base += 32) {
-        const long long k = base + lane;
-        int cl = 0;
-        double vl = 0.0;
-        if (k < end) {
-            cl = __ldg(idx + k);
-            vl = __ldg(val + k);
+        const int cl = cl_n;
+        const double vl = vl_n;
+        const long long kn = base + 32 + lane;
+        cl_n = 0;
+        vl_n = 0.0;
+        if (kn < end) {
+            cl_n = __ldg(idx + kn);
+            vl_n = __ldg(val + kn);
         }
-        const int cnt = static_cast<int>(min(32LL, end - base));
-#pragma unroll 4
-        for (int e0 = 0; e0 < 32; e0 += G) {
-            if (e0 >= cnt) break;
-            const int e = e0 + g;
+        double xs[STEPS], vs[STEPS];
+#pragma unroll
+        for (int s = 0; s < STEPS; ++s) {
+            const int e = s * G + g;
             const int src = e < 32 ? e : 31;
             const int c = __shfl_sync(0xffffffffu, cl, src);
-            double v = __shfl_sync(0xffffffffu, vl, src);
-            if (e >= 32) v = 0.0;
-            if (active) acc = fma(v, __ldg(X + static_cast<long long>(c) * ldx + j), acc);
+            const double v = __shfl_sync(0xffffffffu, vl, src);
+            vs[s] = (e < 32) ? v : 0.0;  // lanes past the row end carry v = 0
+            xs[s] = active ? __ldg(X + static_cast<long long>(c) * ldx + j) : 0.0;
         }
+#pragma unroll
+        for (int s = 0; s < STEPS; ++s) acc = fma(vs[s], xs[s], acc);
     }
     // fold the G groups onto lanes 0..W-1 (fixed order)
     double tot = acc;
