@@ -356,7 +356,27 @@ __global__ void __launch_bounds__(kTinyThreads) tiny_tn_kernel(long long K, int 
     for (int q = 0; q < 8; ++q) acc[q] = 0.0;
     const long long gw = blockIdx.x * static_cast<long long>(kTinyThreads / 32) + warp;
     const long long nw = static_cast<long long>(gridDim.x) * (kTinyThreads / 32);
-    for (long long i = gw; i < K; i += nw) {
+    // rows gw, gw + nw, ...: four rows' loads issued before their FMAs
+    long long i = gw;
+    for (; i + 3 * nw < K; i += 4 * nw) {
+        double a[4][8], b[4][8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double* ai = A + (i + u * nw) * lda;
+            const double* bi = B + (i + u * nw) * ldb;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int p = lane + 32 * q;
+                a[u][q] = (p < P) ? __ldg(ai + p / N) : 0.0;
+                b[u][q] = (p < P) ? __ldg(bi + p % N) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[q] = fma(a[u][q], b[u][q], acc[q]);
+    }
+    for (; i < K; i += nw) {
         const double* ai = A + i * lda;
         const double* bi = B + i * ldb;
 #pragma unroll
@@ -382,9 +402,20 @@ __global__ void __launch_bounds__(kTinyThreads) tiny_tn_kernel(long long K, int 
     __syncthreads();
     if (!last) return;
     __threadfence();
+    // fixed-order reduction over the CTA partials: 8 independent loads in
+    // flight per thread, combined in block order
     for (int p = threadIdx.x; p < P; p += kTinyThreads) {
         double s = 0.0;
-        for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(partial + b * static_cast<long long>(kTinyMaxW * kTinyMaxW) + p);
+        unsigned b = 0;
+        const long long stride = static_cast<long long>(kTinyMaxW * kTinyMaxW);
+        for (; b + 8 <= gridDim.x; b += 8) {
+            double t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t[u] = __ldcg(partial + (b + u) * stride + p);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += t[u];
+        }
+        for (; b < gridDim.x; ++b) s += __ldcg(partial + b * stride + p);
         C[p] = s;
         L[p / N][p % N] = s;
     }
@@ -468,7 +499,7 @@ void skinny_nn_launch(svt_ctx* ctx, i64 M, i64 K, double alpha, const double* A,
 
 void tiny_tn_launch(svt_ctx* ctx, i64 K, int M, int N, const double* A, i64 lda, const double* B, i64 ldb, double* C,
                     bool do_chol, double* Rinv, int* status, const int* pred) {
-    const i64 blocks = std::max<i64>(1, std::min<i64>(2LL * ctx->num_sms, (K + 127) / 128));
+    const i64 blocks = std::max<i64>(1, std::min<i64>(ctx->num_sms, (K + 255) / 256));
     unsigned* cnt = counters(ctx) + 8191;
     ctx->ws_partial2.ensure(static_cast<size_t>(blocks * kTinyMaxW * kTinyMaxW));
     tiny_tn_kernel<<<static_cast<unsigned>(blocks), kTinyThreads, 0, ctx->stream>>>(

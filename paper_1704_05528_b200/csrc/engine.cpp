@@ -270,7 +270,7 @@ void qb_init(Engine& E, QBDev& st, i64 t, int np, u64 seed, double frob_y_sq) {
 }
 
 // sketch.hpp:114-154
-void qb_extend(Engine& E, QBDev& st, i64 dt, int np, u64 seed) {
+void qb_extend(Engine& E, QBDev& st, i64 dt, int np, u64 seed, const double* omega) {
     svt_ctx* c = E.ctx;
     svt_mat* A = E.mat;
     if (dt < 1) throw std::invalid_argument("qb_extend: dt must be >= 1");
@@ -281,10 +281,13 @@ void qb_extend(Engine& E, QBDev& st, i64 dt, int np, u64 seed) {
     }
     const i64 m = A->m_local, n = A->n, r0 = st.rank;
     ensure_cap(E, st, r0 + width);
-    E.Om.ensure(static_cast<size_t>(n * width));
     E.X.ensure(static_cast<size_t>(std::max<i64>(1, m) * width));
-    gaussian_block_dev(c, n, width, seed, E.Om.get(), width);
-    sp_mult(E, width, E.Om.get(), width, E.X.get(), width);
+    if (omega == nullptr || width != dt) {
+        E.Om.ensure(static_cast<size_t>(n * width));
+        gaussian_block_dev(c, n, width, seed, E.Om.get(), width);
+        omega = E.Om.get();
+    }
+    sp_mult(E, width, omega, width, E.X.get(), width);
     power_iterate(E, width, np);
     double* Q = st.Q.get();
     const i64 ldq = st.cap;
@@ -533,6 +536,11 @@ static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, Fina
                           i64 s_warm) {
     SketchOut out;
     int rounds = 0;
+    // Omega bank: the Gaussian blocks of the next rounds depend only on
+    // (seed, round) (sketch.hpp:246-247), so they are generated kMaxOmegaBatch
+    // at a time by independent mt19937_64 warps in two launches.
+    int bank_first = 1, bank_count = 0;
+    const i64 n = E.mat->n;
     while (error_percentage(st) > p.eps_threshold) {
         if (st.saturated) {
             finalize_mode(E, st, mode, tau, s_warm, p.seed, out.f);
@@ -542,7 +550,21 @@ static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, Fina
             return out;
         }
         ++rounds;
-        qb_extend(E, st, p.dt, p.np, derive_seed_u(p.seed, static_cast<u64>(rounds)));
+        const double* omega = nullptr;
+        if (st.min_dim - st.rank >= p.dt) {
+            if (rounds >= bank_first + bank_count) {
+                const i64 left = (st.min_dim - st.rank) / p.dt;
+                const int K = static_cast<int>(std::max<i64>(1, std::min<i64>(kMaxOmegaBatch, left)));
+                u64 seeds[kMaxOmegaBatch];
+                for (int k = 0; k < K; ++k) seeds[k] = derive_seed_u(p.seed, static_cast<u64>(rounds + k));
+                E.OmBank.ensure(static_cast<size_t>(K * n * p.dt));
+                gaussian_blocks_dev(E.ctx, n, p.dt, seeds, K, E.OmBank.get(), n * p.dt, p.dt);
+                bank_first = rounds;
+                bank_count = K;
+            }
+            omega = E.OmBank.get() + static_cast<i64>(rounds - bank_first) * n * p.dt;
+        }
+        qb_extend(E, st, p.dt, p.np, derive_seed_u(p.seed, static_cast<u64>(rounds)), omega);
     }
     finalize_mode(E, st, mode, tau, s_warm, p.seed, out.f);
     out.rank = st.rank;

@@ -74,7 +74,7 @@ struct Engine {
     svt_ctx* ctx;
     svt_mat* mat;  // pattern of the target
     Vals Y;
-    DevBuf<double> Om, X, X2, P, T, C, D, G, Rinv, hh, tmp, W, lam, Vraw, Wk;
+    DevBuf<double> Om, OmBank, X, X2, P, T, C, D, G, Rinv, hh, tmp, W, lam, Vraw, Wk;
     DevBuf<int> perm;
     Engine(svt_ctx* c, svt_mat* m, Vals y) : ctx(c), mat(m), Y(y) {}
 };
@@ -89,7 +89,7 @@ double spectral_norm_est(Engine& E, int iters, u64 seed);                       
 
 // sketch.hpp
 void qb_init(Engine& E, QBDev& st, i64 t, int np, u64 seed, double frob_y_sq = -1.0);
-void qb_extend(Engine& E, QBDev& st, i64 dt, int np, u64 seed);
+void qb_extend(Engine& E, QBDev& st, i64 dt, int np, u64 seed, const double* omega = nullptr);
 void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFactors& out);
 SketchOut r3svd(Engine& E, const svt_sketch_params& p, FinalizeMode mode, double tau, double frob_y_sq = -1.0);
 SketchOut r4svd(Engine& E, const double* U_prev, i64 ldu, i64 s, const svt_sketch_params& p, FinalizeMode mode,

@@ -13,6 +13,11 @@ namespace svtb {
 // out (rows x cols, row-major, leading dim ld) <- the column-major fill of one
 // fresh std::mt19937_64(seed) Box-Muller stream: out[i*ld + j] = z[i + j*rows].
 void gaussian_block_dev(svt_ctx* ctx, i64 rows, i64 cols, u64 seed, double* out, i64 ld);
+// K <= kMaxOmegaBatch independent blocks in two launches (one warp per
+// stream): block k from std::mt19937_64(seeds[k]) into out + k * out_stride.
+constexpr int kMaxOmegaBatch = 32;
+void gaussian_blocks_dev(svt_ctx* ctx, i64 rows, i64 cols, const u64* seeds, int K, double* out, i64 out_stride,
+                         i64 ld);
 
 // ---- sparse (sampled.hpp) ---------------------------------------------------
 // out[i, 0:w] = sum_{k in ptr[i]..ptr[i+1]} val[k] * X[idx[k], 0:w], i < nrows.

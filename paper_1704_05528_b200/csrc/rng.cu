@@ -119,7 +119,104 @@ __global__ void box_muller_kernel(const unsigned long long* __restrict__ draws, 
     if (q0 + 1 < total) out[((q0 + 1) % rows) * ld + (q0 + 1) / rows] = z1;
 }
 
+// K independent streams at once: block k seeds std::mt19937_64 with
+// seeds[k] and writes ntwists * 312 draws to out + k * stride.
+struct SeedPack {
+    unsigned long long s[kMaxOmegaBatch];
+};
+
+__global__ void __launch_bounds__(32) mt_twist_multi_kernel(SeedPack seeds, long long ntwists,
+                                                            unsigned long long* __restrict__ out, long long stride) {
+    __shared__ unsigned long long mt[MT_N];
+    const int lane = threadIdx.x;
+    unsigned long long* o0 = out + blockIdx.x * stride;
+    if (lane == 0) {
+        unsigned long long x = seeds.s[blockIdx.x];
+        mt[0] = x;
+        for (int i = 1; i < MT_N; ++i) {
+            x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<unsigned long long>(i);
+            mt[i] = x;
+        }
+    }
+    __syncwarp();
+    for (long long t = 0; t < ntwists; ++t) {
+        unsigned long long v[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int i = lane + 32 * q;
+            if (i < MT_M) v[q] = twist_word(mt[i], mt[i + 1], mt[i + MT_M]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int i = lane + 32 * q;
+            if (i < MT_M) mt[i] = v[q];
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int i = MT_M + lane + 32 * q;
+            if (i < MT_N) v[q] = twist_word(mt[i], mt[(i + 1) % MT_N], mt[i - MT_M]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            const int i = MT_M + lane + 32 * q;
+            if (i < MT_N) mt[i] = v[q];
+        }
+        __syncwarp();
+        unsigned long long* o = o0 + t * MT_N;
+#pragma unroll
+        for (int q = 0; q < 10; ++q) {
+            const int i = lane + 32 * q;
+            if (i < MT_N) o[i] = temper(mt[i]);
+        }
+    }
+}
+
+__global__ void box_muller_multi_kernel(const unsigned long long* __restrict__ draws, long long draw_stride,
+                                        long long npairs, long long rows, long long total,
+                                        double* __restrict__ out, long long out_stride, long long ld) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p >= npairs) return;
+    const unsigned long long* d = draws + blockIdx.y * draw_stride;
+    double* o = out + blockIdx.y * out_stride;
+    const unsigned long long a = d[2 * p];
+    const unsigned long long b = d[2 * p + 1];
+    const double u1 = 1.0 - static_cast<double>(a >> 11) * 0x1.0p-53;
+    const double u2 = static_cast<double>(b >> 11) * 0x1.0p-53;
+    const double radius = sqrt(-2.0 * log(u1));
+    const double angle = 2.0 * 3.14159265358979323846 * u2;
+    const long long q0 = 2 * p;
+    const double z0 = radius * cos(angle);
+    const double z1 = radius * sin(angle);
+    if (q0 < total) o[(q0 % rows) * ld + q0 / rows] = z0;
+    if (q0 + 1 < total) o[((q0 + 1) % rows) * ld + (q0 + 1) / rows] = z1;
+}
+
 }  // namespace
+
+void gaussian_blocks_dev(svt_ctx* ctx, i64 rows, i64 cols, const u64* seeds, int K, double* out, i64 out_stride,
+                         i64 ld) {
+    if (rows < 1 || cols < 1) throw std::invalid_argument("gaussian_block: dimensions must be >= 1");
+    if (K < 1) return;
+    if (K > kMaxOmegaBatch) throw std::invalid_argument("gaussian_blocks_dev: too many streams");
+    const i64 total = rows * cols;
+    const i64 pairs = (total + 1) / 2;
+    const i64 twists = (2 * pairs + MT_N - 1) / MT_N;
+    const i64 draw_stride = twists * MT_N;
+    ctx->ws_rng.ensure(static_cast<size_t>(draw_stride * K));
+    SeedPack pack{};
+    for (int k = 0; k < K; ++k) pack.s[k] = seeds[k];
+    {
+        LaunchScope ls(ctx, K_RNG, 8.0 * draw_stride * K, 0.0);
+        mt_twist_multi_kernel<<<K, 32, 0, ctx->stream>>>(pack, twists, ctx->ws_rng.get(), draw_stride);
+    }
+    LaunchScope ls(ctx, K_RNG, 32.0 * pairs * K, 0.0);
+    dim3 grid(static_cast<unsigned>((pairs + 255) / 256), static_cast<unsigned>(K));
+    box_muller_multi_kernel<<<grid, 256, 0, ctx->stream>>>(ctx->ws_rng.get(), draw_stride, pairs, rows, total, out,
+                                                           out_stride, ld);
+}
 
 void gaussian_block_dev(svt_ctx* ctx, i64 rows, i64 cols, u64 seed, double* out, i64 ld) {
     if (rows < 1 || cols < 1) throw std::invalid_argument("gaussian_block: dimensions must be >= 1");

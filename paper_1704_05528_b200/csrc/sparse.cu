@@ -43,7 +43,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // L1/L2 request count per entry drops ~W-fold.  Indices and values are read
 // 32 at a time, coalesced, and broadcast by shuffle.
 template <int W>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock) spmm_narrow_kernel(
+__global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) spmm_narrow_kernel(
     SegPlanView plan, const int* __restrict__ idx, const double* __restrict__ val, const double* __restrict__ X,
     long long ldx, double* __restrict__ out, long long ldo, double* __restrict__ partial) {
     constexpr int G = 32 / W;
@@ -149,15 +149,21 @@ __global__ void __launch_bounds__(128) spmm_wide_kernel(SegPlanView plan, const 
 }
 
 // out[row, j] = sum of the row's partial slots, in segment order
+// one warp per long row: lanes stride the row's slots (independent loads),
+// then a fixed-order shuffle tree per output column
 __global__ void seg_reduce_kernel(SegPlanView plan, long long w, const double* __restrict__ partial,
                                   double* __restrict__ out, long long ldo) {
-    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (e >= plan.nlong * w) return;
-    const long long l = e / w, j = e % w;
+    const int lane = threadIdx.x & 31;
+    const long long l = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+    if (l >= plan.nlong) return;
     const int first = plan.long_first[l], cnt = plan.long_count[l];
-    double s = 0.0;
-    for (int t = 0; t < cnt; ++t) s += partial[static_cast<long long>(first + t) * w + j];
-    out[static_cast<long long>(plan.long_row[l]) * ldo + j] = s;
+    const long long row = plan.long_row[l];
+    for (long long j = 0; j < w; ++j) {
+        double s = 0.0;
+        for (int t = lane; t < cnt; t += 32) s += partial[static_cast<long long>(first + t) * w + j];
+        s = warp_sum(s);
+        if (lane == 0) out[row * ldo + j] = s;
+    }
 }
 
 template <int W>
@@ -295,8 +301,8 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
         spmm_wide_kernel<<<grid, 128, 0, ctx->stream>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
     }
     if (plan.nlong > 0) {
-        const i64 tot = plan.nlong * w;
-        seg_reduce_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(plan, w, partial, out,
+        const i64 thr = plan.nlong * 32;
+        seg_reduce_kernel<<<static_cast<unsigned>((thr + 255) / 256), 256, 0, ctx->stream>>>(plan, w, partial, out,
                                                                                           ldo);
     }
 }
