@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(32 * kNnWarps) skinny_nn_kernel(long long M, l
 constexpr int kTinyThreads = 256;
 constexpr int kTinyMaxW = 16;
 
+template <int QN>
 __global__ void __launch_bounds__(kTinyThreads) tiny_tn_kernel(long long K, int M, int N,
                                                                const double* __restrict__ A, long long lda,
                                                                const double* __restrict__ B, long long ldb,
@@ -344,6 +345,7 @@ __global__ void __launch_bounds__(kTinyThreads) tiny_tn_kernel(long long K, int 
                                                                double* __restrict__ Rinv, int* __restrict__ status,
                                                                const int* __restrict__ pred) {
     if (pred != nullptr && *pred == 0) return;
+    constexpr int RU = (QN <= 4) ? 8 : 4;  // rows whose loads are in flight together
     __shared__ double red[kTinyThreads / 32][kTinyMaxW * kTinyMaxW];
     __shared__ double L[kTinyMaxW][kTinyMaxW + 1];
     __shared__ double dorig[kTinyMaxW];
@@ -351,42 +353,41 @@ __global__ void __launch_bounds__(kTinyThreads) tiny_tn_kernel(long long K, int 
     __shared__ int fail;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int P = M * N;
-    double acc[8];
+    double acc[QN];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    for (int q = 0; q < QN; ++q) acc[q] = 0.0;
     const long long gw = blockIdx.x * static_cast<long long>(kTinyThreads / 32) + warp;
     const long long nw = static_cast<long long>(gridDim.x) * (kTinyThreads / 32);
-    // rows gw, gw + nw, ...: four rows' loads issued before their FMAs
     long long i = gw;
-    for (; i + 3 * nw < K; i += 4 * nw) {
-        double a[4][8], b[4][8];
+    for (; i + (RU - 1) * nw < K; i += RU * nw) {
+        double a[RU][QN], b[RU][QN];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < RU; ++u) {
             const double* ai = A + (i + u * nw) * lda;
             const double* bi = B + (i + u * nw) * ldb;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < QN; ++q) {
                 const int p = lane + 32 * q;
                 a[u][q] = (p < P) ? __ldg(ai + p / N) : 0.0;
                 b[u][q] = (p < P) ? __ldg(bi + p % N) : 0.0;
             }
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < RU; ++u)
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc[q] = fma(a[u][q], b[u][q], acc[q]);
+            for (int q = 0; q < QN; ++q) acc[q] = fma(a[u][q], b[u][q], acc[q]);
     }
     for (; i < K; i += nw) {
         const double* ai = A + i * lda;
         const double* bi = B + i * ldb;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < QN; ++q) {
             const int p = lane + 32 * q;
             if (p < P) acc[q] = fma(__ldg(ai + p / N), __ldg(bi + p % N), acc[q]);
         }
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < QN; ++q) {
         const int p = lane + 32 * q;
         if (p < P) red[warp][p] = acc[q];
     }
@@ -499,11 +500,23 @@ void skinny_nn_launch(svt_ctx* ctx, i64 M, i64 K, double alpha, const double* A,
 
 void tiny_tn_launch(svt_ctx* ctx, i64 K, int M, int N, const double* A, i64 lda, const double* B, i64 ldb, double* C,
                     bool do_chol, double* Rinv, int* status, const int* pred) {
-    const i64 blocks = std::max<i64>(1, std::min<i64>(ctx->num_sms, (K + 255) / 256));
+    // few CTAs with deep per-warp row unrolling: the fixed-order partial
+    // reduction in the last CTA stays short
+    const i64 blocks = std::max<i64>(1, std::min<i64>(64, (K + 1023) / 1024));
     unsigned* cnt = counters(ctx) + 8191;
     ctx->ws_partial2.ensure(static_cast<size_t>(blocks * kTinyMaxW * kTinyMaxW));
-    tiny_tn_kernel<<<static_cast<unsigned>(blocks), kTinyThreads, 0, ctx->stream>>>(
-        K, M, N, A, lda, B, ldb, C, ctx->ws_partial2.get(), cnt, do_chol ? 1 : 0, Rinv, status, pred);
+    const int P = M * N;
+    const unsigned nb = static_cast<unsigned>(blocks);
+    double* part = ctx->ws_partial2.get();
+    const int dc = do_chol ? 1 : 0;
+    if (P <= 32)
+        tiny_tn_kernel<1><<<nb, kTinyThreads, 0, ctx->stream>>>(K, M, N, A, lda, B, ldb, C, part, cnt, dc, Rinv, status, pred);
+    else if (P <= 64)
+        tiny_tn_kernel<2><<<nb, kTinyThreads, 0, ctx->stream>>>(K, M, N, A, lda, B, ldb, C, part, cnt, dc, Rinv, status, pred);
+    else if (P <= 128)
+        tiny_tn_kernel<4><<<nb, kTinyThreads, 0, ctx->stream>>>(K, M, N, A, lda, B, ldb, C, part, cnt, dc, Rinv, status, pred);
+    else
+        tiny_tn_kernel<8><<<nb, kTinyThreads, 0, ctx->stream>>>(K, M, N, A, lda, B, ldb, C, part, cnt, dc, Rinv, status, pred);
 }
 
 // ---------------------------------------------------------------------------

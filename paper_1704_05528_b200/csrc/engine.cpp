@@ -72,6 +72,23 @@ void ensure_cap(Engine& E, QBDev& st, i64 need) {
     st.cap = cap;
 }
 
+// Empty the QB state for a new sketch of A, keeping its buffers (capacity)
+// when the frame matches.
+void reset_qb(QBDev& st, const svt_mat* A) {
+    if (st.m_local != A->m_local || st.n != A->n) {
+        st.Q.release();
+        st.Bt.release();
+        st.cap = 0;
+    }
+    st.m_local = A->m_local;
+    st.n = A->n;
+    st.min_dim = std::min(A->m, A->n);
+    st.rank = 0;
+    st.norm_b_sq = 0.0;
+    st.frob_y_sq = 0.0;
+    st.saturated = false;
+}
+
 // One CholQR2 panel (w <= 64) with the Householder fallback.  X is preserved.
 // m rows; dist: the rows are this rank's block of a row-sharded panel (Gram
 // blocks are all-reduced) — false for replicated panels (finalize space).
@@ -249,11 +266,7 @@ void qb_init(Engine& E, QBDev& st, i64 t, int np, u64 seed, double frob_y_sq) {
     if (t < 1 || t > min_dim) throw std::invalid_argument("qb_init: t must satisfy 1 <= t <= min(m, n)");
     if (frob_y_sq < 0.0) frob_y_sq = frob_sq(E);
     if (!(frob_y_sq > 0.0)) throw std::domain_error("qb_init: target matrix is all zero");
-    st.m_local = A->m_local;
-    st.n = A->n;
-    st.min_dim = min_dim;
-    st.rank = 0;
-    st.cap = 0;
+    reset_qb(st, A);
     ensure_cap(E, st, t);
     const i64 m = A->m_local;
     E.Om.ensure(static_cast<size_t>(A->n * t));
@@ -414,10 +427,22 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
     const double tau2 = tau * tau;
     i64 b = std::min<i64>(r, std::max<i64>(s_warm + 16, 24));
     const i64 sw = std::min(s_warm, b);
-    DevBuf<double> Z(static_cast<size_t>(r * b)), Zq(static_cast<size_t>(r * b)), Zt(static_cast<size_t>(r * b));
-    DevBuf<double> Wn(static_cast<size_t>(n * b)), H(static_cast<size_t>(b * b)), Yh(static_cast<size_t>(b * b));
-    DevBuf<double> th(static_cast<size_t>(b)), ZY(static_cast<size_t>(r * b)), Xr(static_cast<size_t>(r * b));
-    DevBuf<double> res2(static_cast<size_t>(b));
+    // engine-owned workspaces (grow-only; no per-iteration cudaMalloc/free)
+    DevBuf<double>&Z = E.fkZ, &Zq = E.fkZq, &Zt = E.fkZt, &Wn = E.fkWn, &H = E.fkH, &Yh = E.fkYh, &th = E.fkth,
+    &ZY = E.fkZY, &Xr = E.fkXr, &res2 = E.fkres;
+    auto grow = [&](i64 bb) {
+        Z.ensure(static_cast<size_t>(r * bb));
+        Zq.ensure(static_cast<size_t>(r * bb));
+        Zt.ensure(static_cast<size_t>(r * bb));
+        Wn.ensure(static_cast<size_t>(n * bb));
+        H.ensure(static_cast<size_t>(bb * bb));
+        Yh.ensure(static_cast<size_t>(bb * bb));
+        th.ensure(static_cast<size_t>(bb));
+        ZY.ensure(static_cast<size_t>(r * bb));
+        Xr.ensure(static_cast<size_t>(r * bb));
+        res2.ensure(static_cast<size_t>(bb));
+    };
+    grow(b);
     fill(c, Z.get(), r * b, 0.0);
     set_identity_cols(c, Z.get(), r, b, sw);
     if (b > sw) gaussian_block_dev(c, r, b - sw, derive_seed_u(seed, 0x5EEDF1A1ULL), Z.get() + sw, b);
@@ -445,21 +470,13 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
         if (kk == b && b < r) {
             // the block does not reach below the threshold: widen it
             const i64 b2 = std::min<i64>(r, 2 * b);
-            DevBuf<double> Z2(static_cast<size_t>(r * b2));
-            copy2d(c, Zq.get(), b, Z2.get(), b2, r, b);
-            gaussian_block_dev(c, r, b2 - b, derive_seed_u(seed, 0x5EEDF1A2ULL + static_cast<u64>(it)), Z2.get() + b,
+            Zt.ensure(static_cast<size_t>(r * b2));
+            copy2d(c, Zq.get(), b, Zt.get(), b2, r, b);
+            gaussian_block_dev(c, r, b2 - b, derive_seed_u(seed, 0x5EEDF1A2ULL + static_cast<u64>(it)), Zt.get() + b,
                                b2);
             b = b2;
-            Z = std::move(Z2);
-            Zq.alloc(static_cast<size_t>(r * b));
-            Zt.alloc(static_cast<size_t>(r * b));
-            Wn.alloc(static_cast<size_t>(n * b));
-            H.alloc(static_cast<size_t>(b * b));
-            Yh.alloc(static_cast<size_t>(b * b));
-            th.alloc(static_cast<size_t>(b));
-            ZY.alloc(static_cast<size_t>(r * b));
-            Xr.alloc(static_cast<size_t>(r * b));
-            res2.alloc(static_cast<size_t>(b));
+            std::swap(Z, Zt);
+            grow(b);
             continue;
         }
         const double tol = 1e-12 * std::max(th_h[0], 0.0);
@@ -576,7 +593,7 @@ static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, Fina
 // sketch.hpp:188-201
 SketchOut r3svd(Engine& E, const svt_sketch_params& p, FinalizeMode mode, double tau, double frob_y_sq) {
     check_sketch_params(p);
-    QBDev st;
+    QBDev& st = E.qb;
     qb_init(E, st, p.t, p.np, derive_seed_u(p.seed, 0), frob_y_sq);
     return run_loop(E, st, p, mode, tau, 0);
 }
@@ -597,7 +614,8 @@ SketchOut r4svd(Engine& E, const double* U_prev, i64 ldu, i64 s, const svt_sketc
     if (frob_y_sq < 0.0) frob_y_sq = frob_sq(E);
     if (!(frob_y_sq > 0.0)) throw std::domain_error("r4svd: target matrix is all zero");
     const i64 m = A->m_local;
-    QBDev st;
+    QBDev& st = E.qb;
+    reset_qb(st, A);
     st.m_local = m;
     st.n = A->n;
     st.min_dim = min_dim;

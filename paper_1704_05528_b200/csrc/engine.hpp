@@ -75,7 +75,9 @@ struct Engine {
     svt_mat* mat;  // pattern of the target
     Vals Y;
     DevBuf<double> Om, OmBank, X, X2, P, T, C, D, G, Rinv, hh, tmp, W, lam, Vraw, Wk;
+    DevBuf<double> fkZ, fkZq, fkZt, fkWn, fkH, fkYh, fkth, fkZY, fkXr, fkres;  // finalize_kept
     DevBuf<int> perm;
+    QBDev qb;  // persistent QB storage: capacity survives across SVT iterations
     Engine(svt_ctx* c, svt_mat* m, Vals y) : ctx(c), mat(m), Y(y) {}
 };
 
