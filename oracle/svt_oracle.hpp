@@ -332,6 +332,28 @@ inline void one_sided_jacobi(Mat& A, Mat& V, std::vector<double>& sigma) {
 // by a one-sided Jacobi SVD (high relative accuracy; tests pin tolerance).
 inline LowRankFactors small_svd(const Mat& B) {
     LowRankFactors f;
+    // Strongly rectangular blocks (the r x n coefficient block of a sketch):
+    // QR-precondition so Jacobi rotates r-length columns instead of n-length
+    // ones.  B^T = Qb R  =>  B = R^T Qb^T,  svd(R^T) = Ur S Vr^T,  B = Ur S (Qb Vr)^T.
+    if (B.cols > 2 * B.rows && B.rows >= 16) {
+        const Mat Bt = transpose(B);          // n x r
+        const Mat Qb = qr_orthonormal(Bt);    // n x r
+        const Mat Rt = mul_tn(Bt, Qb);        // (Qb^T Bt)^T = R^T, r x r
+        LowRankFactors g = small_svd(Rt);
+        f.U = std::move(g.U);
+        f.sigma = std::move(g.sigma);
+        f.V = mul_nn(Qb, g.V);
+        return f;
+    }
+    if (B.rows > 2 * B.cols && B.cols >= 16) {
+        const Mat Qb = qr_orthonormal(B);     // m x c
+        const Mat R = mul_tn(Qb, B);          // c x c
+        LowRankFactors g = small_svd(R);
+        f.U = mul_nn(Qb, g.U);
+        f.sigma = std::move(g.sigma);
+        f.V = std::move(g.V);
+        return f;
+    }
     if (B.rows >= B.cols) {
         Mat A = B;
         Mat V;

@@ -462,6 +462,154 @@ __global__ void __launch_bounds__(kTinyThreads) tiny_tn_kernel(long long K, int 
     if (threadIdx.x == 0 && fail) status[0] = 1;
 }
 
+// Cholesky of the w x w Gram in shared memory L and Rinv = L^{-T}; all
+// threads of the block participate.  fail is block-shared.
+__device__ void block_chol_rinv(double (*L)[kTinyMaxW + 1], int w, double* dorig, int* fail, double* Rinv,
+                                int* status) {
+    if (threadIdx.x == 0) *fail = 0;
+    if (threadIdx.x < w) dorig[threadIdx.x] = L[threadIdx.x][threadIdx.x];
+    __syncthreads();
+    for (int j = 0; j < w; ++j) {
+        const double d = L[j][j];
+        const bool bad = !(dorig[j] > 0.0) || !(d > 1e-13 * dorig[j]) || !(d < CUDART_INF);
+        const double ljj = sqrt(bad ? 1.0 : d);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (bad) *fail = 1;
+            L[j][j] = ljj;
+        }
+        for (int i = j + 1 + threadIdx.x; i < w; i += blockDim.x) L[i][j] /= ljj;
+        __syncthreads();
+        const int rem = w - j - 1;
+        for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
+            const int i = j + 1 + e / rem, k = j + 1 + e % rem;
+            if (k <= i) L[i][k] -= L[i][j] * L[k][j];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < w) {
+        const int c = threadIdx.x;
+        double x[kTinyMaxW];
+        for (int r = 0; r < w; ++r) x[r] = 0.0;
+        x[c] = 1.0 / L[c][c];
+        for (int r = c - 1; r >= 0; --r) {
+            double s = 0.0;
+            for (int t = r + 1; t <= c; ++t) s += L[t][r] * x[t];
+            x[r] = -s / L[r][r];
+        }
+        for (int r = 0; r < w; ++r) Rinv[r * w + c] = x[r];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && *fail) status[0] = 1;
+}
+
+// Symmetric Gram G = X^T X of a narrow panel (W <= 12): one thread per row
+// (one contiguous 8W-byte load), the W(W+1)/2 products in registers, warp
+// shuffle + shared-memory fold per CTA, last CTA reduces the CTA partials in
+// fixed order and optionally runs the Cholesky (CholQR pass head).
+constexpr int kGramThreads = 256;
+
+template <int W>
+__global__ void __launch_bounds__(kGramThreads) gram_sym_kernel(long long K, const double* __restrict__ X,
+                                                                long long ldx, double* __restrict__ G,
+                                                                double* __restrict__ partial,
+                                                                unsigned* __restrict__ counter, int do_chol,
+                                                                double* __restrict__ Rinv, int* __restrict__ status,
+                                                                const int* __restrict__ pred) {
+    if (pred != nullptr && *pred == 0) return;
+    constexpr int P = W * (W + 1) / 2;
+    __shared__ double red[kGramThreads / 32][P];
+    __shared__ double L[kTinyMaxW][kTinyMaxW + 1];
+    __shared__ double dorig[kTinyMaxW];
+    __shared__ bool last;
+    __shared__ int fail;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double acc[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) acc[p] = 0.0;
+    const long long stride = static_cast<long long>(gridDim.x) * kGramThreads;
+    for (long long i = blockIdx.x * static_cast<long long>(kGramThreads) + threadIdx.x; i < K; i += stride) {
+        double x[W];
+#pragma unroll
+        for (int a = 0; a < W; ++a) x[a] = __ldg(X + i * ldx + a);
+        int p = 0;
+#pragma unroll
+        for (int a = 0; a < W; ++a)
+#pragma unroll
+            for (int b = 0; b <= a; ++b) {
+                acc[p] = fma(x[a], x[b], acc[p]);
+                ++p;
+            }
+    }
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const double s = warp_sum(acc[p]);
+        if (lane == 0) red[warp][p] = s;
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < P; p += kGramThreads) {
+        double s = 0.0;
+        for (int w = 0; w < kGramThreads / 32; ++w) s += red[w][p];
+        partial[blockIdx.x * static_cast<long long>(P) + p] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int p = threadIdx.x; p < P; p += kGramThreads) {
+        double s = 0.0;
+        unsigned b = 0;
+        for (; b + 8 <= gridDim.x; b += 8) {
+            double t[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) t[u] = __ldcg(partial + (b + u) * static_cast<long long>(P) + p);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s += t[u];
+        }
+        for (; b < gridDim.x; ++b) s += __ldcg(partial + b * static_cast<long long>(P) + p);
+        // p -> (a, b) with b <= a
+        int a = 0;
+        while ((a + 1) * (a + 2) / 2 <= p) ++a;
+        const int bb = p - a * (a + 1) / 2;
+        G[a * W + bb] = s;
+        G[bb * W + a] = s;
+        L[a][bb] = s;
+        L[bb][a] = s;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+    __syncthreads();
+    if (do_chol) block_chol_rinv(L, W, dorig, &fail, Rinv, status);
+}
+
+// C (M x N) = alpha * A B + beta * C for a short inner dimension (K <= 16):
+// one thread per row of A (contiguous 8K-byte row), B broadcast from shared.
+template <int KK>
+__global__ void __launch_bounds__(256) smallk_nn_kernel(long long M, int N, double alpha,
+                                                        const double* __restrict__ A, long long lda,
+                                                        const double* __restrict__ B, long long ldb, double beta,
+                                                        double* __restrict__ C, long long ldc,
+                                                        const int* __restrict__ pred) {
+    if (pred != nullptr && *pred == 0) return;
+    __shared__ double Bs[KK * 16];
+    for (int e = threadIdx.x; e < KK * N; e += blockDim.x) Bs[e] = B[(e / N) * ldb + e % N];
+    __syncthreads();
+    const long long row = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (row >= M) return;
+    double a[KK];
+#pragma unroll
+    for (int k = 0; k < KK; ++k) a[k] = __ldg(A + row * lda + k);
+    for (int j = 0; j < N; ++j) {
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < KK; ++k) s = fma(a[k], Bs[k * N + j], s);
+        double* cp = C + row * ldc + j;
+        const double o = (beta != 0.0) ? beta * (*cp) : 0.0;
+        *cp = fma(alpha, s, o);
+    }
+}
+
 unsigned* counters(svt_ctx* ctx) {
     if (ctx->ws_counters.n < 8192) {
         ctx->ws_counters.alloc(8192);
@@ -496,6 +644,44 @@ void skinny_nn_launch(svt_ctx* ctx, i64 M, i64 K, double alpha, const double* A,
     const i64 rows_per_block = static_cast<i64>(kNnWarps) * kNnRows;
     const unsigned blocks = static_cast<unsigned>((M + rows_per_block - 1) / rows_per_block);
     skinny_nn_kernel<N><<<blocks, 32 * kNnWarps, 0, ctx->stream>>>(M, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
+}
+
+void gram_sym_launch(svt_ctx* ctx, i64 K, int w, const double* X, i64 ldx, double* G, bool do_chol, double* Rinv,
+                     int* status, const int* pred) {
+    const i64 blocks = std::max<i64>(1, std::min<i64>(ctx->num_sms, (K + kGramThreads - 1) / kGramThreads));
+    unsigned* cnt = counters(ctx) + 8190;
+    ctx->ws_partial2.ensure(static_cast<size_t>(blocks * w * (w + 1) / 2));
+    const unsigned nb = static_cast<unsigned>(blocks);
+    double* part = ctx->ws_partial2.get();
+    const int dc = do_chol ? 1 : 0;
+    switch (w) {
+#define SVT_CASE(WW)                                                                                          \
+    case WW:                                                                                                  \
+        gram_sym_kernel<WW><<<nb, kGramThreads, 0, ctx->stream>>>(K, X, ldx, G, part, cnt, dc, Rinv, status, pred); \
+        break;
+        SVT_CASE(1) SVT_CASE(2) SVT_CASE(3) SVT_CASE(4) SVT_CASE(5) SVT_CASE(6) SVT_CASE(7) SVT_CASE(8)
+        SVT_CASE(9) SVT_CASE(10) SVT_CASE(11) SVT_CASE(12)
+#undef SVT_CASE
+        default:
+            throw std::invalid_argument("gram_sym: w > 12");
+    }
+}
+
+void smallk_nn_launch(svt_ctx* ctx, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
+                      i64 ldb, double beta, double* C, i64 ldc, const int* pred) {
+    const unsigned blocks = static_cast<unsigned>((M + 255) / 256);
+    const int n = static_cast<int>(N);
+    switch (K) {
+#define SVT_CASE(KK)                                                                                              \
+    case KK:                                                                                                      \
+        smallk_nn_kernel<KK><<<blocks, 256, 0, ctx->stream>>>(M, n, alpha, A, lda, B, ldb, beta, C, ldc, pred); \
+        break;
+        SVT_CASE(1) SVT_CASE(2) SVT_CASE(3) SVT_CASE(4) SVT_CASE(5) SVT_CASE(6) SVT_CASE(7) SVT_CASE(8)
+        SVT_CASE(9) SVT_CASE(10) SVT_CASE(11) SVT_CASE(12) SVT_CASE(13) SVT_CASE(14) SVT_CASE(15) SVT_CASE(16)
+#undef SVT_CASE
+        default:
+            throw std::invalid_argument("smallk_nn: K > 16");
+    }
 }
 
 void tiny_tn_launch(svt_ctx* ctx, i64 K, int M, int N, const double* A, i64 lda, const double* B, i64 ldb, double* C,
@@ -1050,6 +1236,14 @@ void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha,
         return;
     }
     if (N <= 16) {
+        if (transA && A == B && lda == ldb && M == N && M <= 12 && alpha == 1.0 && beta == 0.0 && ldc == N) {
+            gram_sym_launch(ctx, K, static_cast<int>(M), A, lda, C, false, nullptr, nullptr, pred);
+            return;
+        }
+        if (!transA && K <= 16) {
+            smallk_nn_launch(ctx, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
+            return;
+        }
         if (transA && M <= kTinyMaxW && alpha == 1.0 && beta == 0.0 && ldc == N) {
             tiny_tn_launch(ctx, K, static_cast<int>(M), static_cast<int>(N), A, lda, B, ldb, C, false, nullptr,
                            nullptr, pred);
@@ -1077,7 +1271,10 @@ void gram_chol(svt_ctx* ctx, const double* X, i64 ldx, i64 m, i64 w, double* G, 
                const int* pred) {
     if (w > kTinyMaxW) throw std::invalid_argument("gram_chol: panel wider than 16");
     LaunchScope ls(ctx, K_QR, 8.0 * m * w, 1.0 * m * w * w);
-    tiny_tn_launch(ctx, m, static_cast<int>(w), static_cast<int>(w), X, ldx, X, ldx, G, true, Rinv, status, pred);
+    if (w <= 12)
+        gram_sym_launch(ctx, m, static_cast<int>(w), X, ldx, G, true, Rinv, status, pred);
+    else
+        tiny_tn_launch(ctx, m, static_cast<int>(w), static_cast<int>(w), X, ldx, X, ldx, G, true, Rinv, status, pred);
 }
 
 void sumsq(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double* d_out, int op, const int* pred) {

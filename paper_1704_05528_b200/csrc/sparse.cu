@@ -43,7 +43,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // L1/L2 request count per entry drops ~W-fold.  Indices and values are read
 // 32 at a time, coalesced, and broadcast by shuffle.
 template <int W>
-__global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) spmm_narrow_kernel(
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) spmm_narrow_kernel(
     SegPlanView plan, const int* __restrict__ idx, const double* __restrict__ val, const double* __restrict__ X,
     long long ldx, double* __restrict__ out, long long ldo, double* __restrict__ partial) {
     constexpr int G = 32 / W;
@@ -73,18 +73,16 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock, 4) spmm_narrow_kernel(
             cl_n = __ldg(idx + kn);
             vl_n = __ldg(val + kn);
         }
-        double xs[STEPS], vs[STEPS];
 #pragma unroll
         for (int s = 0; s < STEPS; ++s) {
             const int e = s * G + g;
             const int src = e < 32 ? e : 31;
             const int c = __shfl_sync(0xffffffffu, cl, src);
-            const double v = __shfl_sync(0xffffffffu, vl, src);
-            vs[s] = (e < 32) ? v : 0.0;  // lanes past the row end carry v = 0
-            xs[s] = active ? __ldg(X + static_cast<long long>(c) * ldx + j) : 0.0;
+            double v = __shfl_sync(0xffffffffu, vl, src);
+            if (e >= 32) v = 0.0;  // lanes past the row end already carry v = 0
+            const double x = active ? __ldg(X + static_cast<long long>(c) * ldx + j) : 0.0;
+            acc = fma(v, x, acc);
         }
-#pragma unroll
-        for (int s = 0; s < STEPS; ++s) acc = fma(vs[s], xs[s], acc);
     }
     // fold the G groups onto lanes 0..W-1 (fixed order)
     double tot = acc;
