@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-budget", type=float, default=25.0, help="seconds of oracle CPU work for cpu_baseline")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle CPU work for cpu_baseline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -157,7 +157,7 @@ def run_reference(args, rank, world):
     cfg, stop = G.config_params(args.config, int(rp[-1]), m, n, frob(va))
     cfg.maxit = args.warmup + args.steps
     stamps = [time.perf_counter()]
-    budget = max(60.0, args.cpu_budget * 4)
+    budget = max(90.0, args.cpu_budget * 4)
 
     def obs(rec, U, s, V):
         stamps.append(time.perf_counter())
