@@ -130,6 +130,9 @@ int svt_ctx_reset_stats(svt_ctx* ctx);
 int svt_ctx_kernel_stats(svt_ctx* ctx, int cls, int64_t* launches, double* total_ms, double* bytes,
                          double* flops);
 int64_t svt_ctx_launch_count(svt_ctx* ctx);
+/* 1 (default): speculative multi-round batches in the rank-revealing loop
+ * (same rounds / ranks; exact-arithmetic equivalent); 0: one round at a time. */
+int svt_ctx_set_batching(svt_ctx* ctx, int on);
 
 /* ---- host-side sample-set construction (SampledMatrix ctor, sampled.hpp:27-62) */
 /* Validates and sorts triplets into CSR; throws-equivalent SVT_EINVAL on

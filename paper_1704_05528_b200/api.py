@@ -113,6 +113,10 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().svt_ctx_launch_count(self.h))
 
+    def set_batching(self, on: bool):
+        """Speculative multi-round batches (default on; same rounds/ranks)."""
+        _check(lib().svt_ctx_set_batching(self.h, C.c_int(1 if on else 0)))
+
     def close(self):
         if getattr(self, "h", None):
             lib().svt_ctx_destroy(self.h)

@@ -203,6 +203,13 @@ int svt_ctx_kernel_stats(svt_ctx* ctx, int cls, int64_t* launches, double* total
 
 int64_t svt_ctx_launch_count(svt_ctx* ctx) { return ctx ? ctx->launch_count : -1; }
 
+int svt_ctx_set_batching(svt_ctx* ctx, int on) {
+    return guard([&] {
+        need(ctx, "svt_ctx_set_batching");
+        ctx->batching = on ? 1 : 0;
+    });
+}
+
 int svt_sampled_build(int64_t m, int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols, const double* vals,
                       int64_t* rowptr_out, int64_t* col_out, double* val_out) {
     return guard([&] {

@@ -135,6 +135,7 @@ struct svt_ctx {
     void* cusolver = nullptr;  // cusolverDnHandle_t
     // instrumentation
     bool profiling = false;
+    int batching = 1;  // speculative multi-round batches in the rank-revealing loop
     svtb::i64 launch_count = 0;
     svtb::KStats stats[svtb::K_NCLASS];
     struct Pending {

@@ -780,23 +780,27 @@ __global__ void set_flag_kernel(const double* a, const double* b, double coef, i
 // ---------------------------------------------------------------------------
 // CholQR: Cholesky + explicit inverse of R = L^T, one CTA, w <= 64
 // ---------------------------------------------------------------------------
-constexpr int kCholMax = 64;
+constexpr int kCholMax = 128;  // widest Cholesky panel (a batch of rounds)
+constexpr int kHhMax = 64;     // widest Householder fallback panel
 
+// L lives in dynamic shared memory, row stride w + 1 (w <= 128: 132 KB).
 __global__ void __launch_bounds__(256) chol_rinv_kernel(const double* __restrict__ G, int w,
                                                         double* __restrict__ Rinv, int* __restrict__ status,
                                                         const int* __restrict__ pred) {
     if (pred != nullptr && *pred == 0) return;
-    __shared__ double L[kCholMax][kCholMax + 1];
-    __shared__ double dorig[kCholMax];
+    extern __shared__ double dyn[];
+    double* L = dyn;               // w x (w + 1)
+    double* dorig = dyn + w * (w + 1);
     __shared__ int fail;
+    const int ld = w + 1;
     const int tid = threadIdx.x;
     if (tid == 0) fail = 0;
-    for (int e = tid; e < w * w; e += blockDim.x) L[e / w][e % w] = G[e];
+    for (int e = tid; e < w * w; e += blockDim.x) L[(e / w) * ld + e % w] = G[e];
     __syncthreads();
-    if (tid < w) dorig[tid] = L[tid][tid];
+    if (tid < w) dorig[tid] = L[tid * ld + tid];
     __syncthreads();
     for (int j = 0; j < w; ++j) {
-        const double d = L[j][j];
+        const double d = L[j * ld + j];
         // a pivot that lost more than ~13 digits (kappa(X) beyond ~3e6 in
         // that direction) or a zero / non-finite column routes the panel to
         // the Householder fallback, which keeps all columns like
@@ -806,14 +810,14 @@ __global__ void __launch_bounds__(256) chol_rinv_kernel(const double* __restrict
         __syncthreads();
         if (tid == 0) {
             if (bad) fail = 1;
-            L[j][j] = ljj;
+            L[j * ld + j] = ljj;
         }
-        for (int i = j + 1 + tid; i < w; i += blockDim.x) L[i][j] /= ljj;
+        for (int i = j + 1 + tid; i < w; i += blockDim.x) L[i * ld + j] /= ljj;
         __syncthreads();
         const int rem = w - j - 1;
         for (int e = tid; e < rem * rem; e += blockDim.x) {
             const int i = j + 1 + e / rem, k = j + 1 + e % rem;
-            if (k <= i) L[i][k] -= L[i][j] * L[k][j];
+            if (k <= i) L[i * ld + k] -= L[i * ld + j] * L[k * ld + j];
         }
         __syncthreads();
     }
@@ -821,11 +825,11 @@ __global__ void __launch_bounds__(256) chol_rinv_kernel(const double* __restrict
     for (int c = tid; c < w; c += blockDim.x) {
         double x[kCholMax];
         for (int r = 0; r < w; ++r) x[r] = 0.0;
-        x[c] = 1.0 / L[c][c];
+        x[c] = 1.0 / L[c * ld + c];
         for (int r = c - 1; r >= 0; --r) {
             double s = 0.0;
-            for (int t = r + 1; t <= c; ++t) s += L[t][r] * x[t];
-            x[r] = -s / L[r][r];
+            for (int t = r + 1; t <= c; ++t) s += L[t * ld + r] * x[t];
+            x[r] = -s / L[r * ld + r];
         }
         for (int r = 0; r < w; ++r) Rinv[r * w + c] = x[r];
     }
@@ -856,7 +860,7 @@ __global__ void __launch_bounds__(kHhThreads) householder_kernel(const double* _
     if (pred != nullptr && *pred == 0) return;
     if (status != nullptr && *status == 0) return;
     __shared__ double red[32];
-    __shared__ double tau[kCholMax];
+    __shared__ double tau[kHhMax];
     const int tid = threadIdx.x;
     for (long long e = tid; e < m * w; e += blockDim.x) Wk[e] = X[(e / w) * ldx + e % w];
     __syncthreads();
@@ -1306,14 +1310,21 @@ void set_flag(svt_ctx* ctx, const double* a, const double* b, double coef, int m
 }
 
 void chol_rinv(svt_ctx* ctx, const double* G, i64 w, double* Rinv, int* status, const int* pred) {
-    if (w > kCholMax) throw std::invalid_argument("chol_rinv: panel wider than 64");
+    if (w > kCholMax) throw std::invalid_argument("chol_rinv: panel wider than 128");
+    const size_t smem = sizeof(double) * static_cast<size_t>(w * (w + 1) + w);
+    static bool attr_set = false;
+    if (!attr_set) {
+        SVT_CUDA(cudaFuncSetAttribute(chol_rinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(sizeof(double) * (kCholMax * (kCholMax + 1) + kCholMax))));
+        attr_set = true;
+    }
     LaunchScope ls(ctx, K_QR, 16.0 * w * w, w * w * w / 3.0);
-    chol_rinv_kernel<<<1, 256, 0, ctx->stream>>>(G, static_cast<int>(w), Rinv, status, pred);
+    chol_rinv_kernel<<<1, 256, smem, ctx->stream>>>(G, static_cast<int>(w), Rinv, status, pred);
 }
 
 void householder_qr(svt_ctx* ctx, const double* X, i64 m, i64 w, i64 ldx, double* Q, i64 ldq, double* work,
                     const int* pred, const int* status) {
-    if (w > kCholMax) throw std::invalid_argument("householder_qr: panel wider than 64");
+    if (w > kHhMax) throw std::invalid_argument("householder_qr: panel wider than 64");
     LaunchScope ls(ctx, K_QR, 0.0, 4.0 * m * w * w);
     householder_kernel<<<1, kHhThreads, 0, ctx->stream>>>(X, m, static_cast<int>(w), ldx, Q, ldq, work, pred,
                                                           status);

@@ -323,8 +323,10 @@ void qb_extend(Engine& E, QBDev& st, i64 dt, int np, u64 seed, const double* ome
     qr_panel(E, m, true, E.X.get(), width, width, Q + r0, ldq, nullptr);
     if (r0 > 0) reorth_if_needed(E, m, true, Q, ldq, r0, Q + r0, ldq, width);
     // coefficient block + energy (sketch.hpp:143-150)
-    append_coefficients(E, st, r0, width, 1);
-    st.norm_b_sq = read_scalar(c, S_NB);
+    // norm_b_sq += ||B'||_F^2 (sketch.hpp:150), accumulated on the host so
+    // batched and single rounds share one running sum
+    append_coefficients(E, st, r0, width, 0);
+    st.norm_b_sq += read_scalar(c, S_NB);
     st.rank = r0 + width;
     st.saturated = (st.rank == st.min_dim);
 }
@@ -549,6 +551,99 @@ static void finalize_mode(Engine& E, const QBDev& st, FinalizeMode mode, double 
         finalize(E, st, mode, tau, out);
 }
 
+// Speculative batch of K extension rounds.  Round j's sketch
+// Y Y^T Y Omega_j does not depend on the basis, so rounds round0..round0+K-1
+// are sketched together as one W = K*dt wide panel; the panel is projected
+// against Q with classical Gram-Schmidt (second pass when any block needs
+// it, the reference's test of sketch.hpp:134 per block) and factored by one
+// Cholesky QR of the whole panel — R is upper triangular, so the first j
+// blocks of the result span exactly what j sequential rounds would have
+// added (same nested spans as qb_extend's block-by-block QR).  The energy of
+// each block's coefficient rows then replays the reference's
+// `while error_percentage > eps` test round by round; the blocks after the
+// stopping round are discarded.  Returns the number of rounds accepted, or
+// -1 when the panel is numerically rank deficient (the caller re-runs the
+// rounds one by one with the exact fallback semantics).
+static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int round0, int K) {
+    svt_ctx* c = E.ctx;
+    svt_mat* A = E.mat;
+    const i64 w = p.dt, W = K * w, m = A->m_local, n = A->n, r0 = st.rank;
+    ensure_cap(E, st, r0 + W);
+    u64 seeds[kMaxOmegaBatch];
+    for (int k = 0; k < K; ++k) seeds[k] = derive_seed_u(p.seed, static_cast<u64>(round0 + k));
+    E.OmW.ensure(static_cast<size_t>(n * W));
+    E.XW.ensure(static_cast<size_t>(std::max<i64>(1, m) * W));
+    E.TW.ensure(static_cast<size_t>(n * W));
+    gaussian_blocks_dev(c, n, w, seeds, K, E.OmW.get(), w, W);
+    sp_mult(E, W, E.OmW.get(), W, E.XW.get(), W);
+    for (int j = 0; j < p.np; ++j) {  // np == 1 here (np >= 2 rounds run one by one)
+        sp_mult_t(E, W, E.XW.get(), W, E.TW.get());
+        sp_mult(E, W, E.TW.get(), W, E.XW.get(), W);
+    }
+    double* Q = st.Q.get();
+    const i64 ldq = st.cap;
+    if (r0 > 0) {
+        E.CW.ensure(static_cast<size_t>(r0 * W));
+        gemm(c, K_GEMM, true, r0, W, m, 1.0, Q, ldq, E.XW.get(), W, 0.0, E.CW.get(), W);
+        allreduce(c, E.CW.get(), static_cast<size_t>(r0 * W));
+        gemm(c, K_GEMM, false, m, W, r0, -1.0, Q, ldq, E.CW.get(), W, 1.0, E.XW.get(), W);
+        gemm(c, K_GEMM, true, r0, W, m, 1.0, Q, ldq, E.XW.get(), W, 0.0, E.CW.get(), W);
+        allreduce(c, E.CW.get(), static_cast<size_t>(r0 * W));
+        // per block: ||Q^T X_k|| > 1e-8 ||X_k||  (sketch.hpp:134)
+        E.eW.ensure(static_cast<size_t>(2 * W));
+        col_sumsq(c, E.XW.get(), m, W, W, E.eW.get());
+        allreduce(c, E.eW.get(), static_cast<size_t>(W));
+        col_sumsq(c, E.CW.get(), r0, W, W, E.eW.get() + W);
+        std::vector<double> cs(static_cast<size_t>(2 * W));
+        SVT_CUDA(cudaMemcpyAsync(cs.data(), E.eW.get(), sizeof(double) * 2 * W, cudaMemcpyDeviceToHost, c->stream));
+        SVT_CUDA(cudaStreamSynchronize(c->stream));
+        bool second = false;
+        for (int k = 0; k < K && !second; ++k) {
+            double nx = 0.0, nc = 0.0;
+            for (i64 q = 0; q < w; ++q) {
+                nx += cs[static_cast<size_t>(k * w + q)];
+                nc += cs[static_cast<size_t>(W + k * w + q)];
+            }
+            second = std::sqrt(nc) > 1e-8 * std::sqrt(nx);
+        }
+        if (second) gemm(c, K_GEMM, false, m, W, r0, -1.0, Q, ldq, E.CW.get(), W, 1.0, E.XW.get(), W);
+    }
+    // one Cholesky QR (twice) of the whole panel: nested spans per block
+    E.GW.ensure(static_cast<size_t>(W * W));
+    E.RW.ensure(static_cast<size_t>(W * W));
+    E.X2.ensure(static_cast<size_t>(std::max<i64>(1, m) * W));
+    zero_flag(c, F_QRSTAT);
+    int* status = dfl(c, F_QRSTAT);
+    gemm(c, K_QR, true, W, W, m, 1.0, E.XW.get(), W, E.XW.get(), W, 0.0, E.GW.get(), W);
+    allreduce(c, E.GW.get(), static_cast<size_t>(W * W));
+    chol_rinv(c, E.GW.get(), W, E.RW.get(), status, nullptr);
+    gemm(c, K_QR, false, m, W, W, 1.0, E.XW.get(), W, E.RW.get(), W, 0.0, E.X2.get(), W);
+    gemm(c, K_QR, true, W, W, m, 1.0, E.X2.get(), W, E.X2.get(), W, 0.0, E.GW.get(), W);
+    allreduce(c, E.GW.get(), static_cast<size_t>(W * W));
+    chol_rinv(c, E.GW.get(), W, E.RW.get(), status, nullptr);
+    gemm(c, K_QR, false, m, W, W, 1.0, E.X2.get(), W, E.RW.get(), W, 0.0, Q + r0, ldq);
+    if (read_flag(c, F_QRSTAT) != 0) return -1;
+    // coefficient rows of the whole batch and their per-block energies
+    sp_mult_t(E, W, Q + r0, ldq, E.TW.get());
+    copy2d(c, E.TW.get(), W, st.Bt.get() + r0, ldq, n, W);
+    col_sumsq(c, E.TW.get(), n, W, W, E.eW.get());
+    std::vector<double> e(static_cast<size_t>(W));
+    SVT_CUDA(cudaMemcpyAsync(e.data(), E.eW.get(), sizeof(double) * W, cudaMemcpyDeviceToHost, c->stream));
+    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    // replay the reference's loop test round by round
+    int accepted = 0;
+    for (int k = 0; k < K; ++k) {
+        if (k > 0 && !(error_percentage(st) > p.eps_threshold)) break;
+        double ek = 0.0;
+        for (i64 q = 0; q < w; ++q) ek += e[static_cast<size_t>(k * w + q)];
+        st.norm_b_sq += ek;
+        st.rank += w;
+        ++accepted;
+    }
+    st.saturated = (st.rank == st.min_dim);
+    return accepted;
+}
+
 static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, FinalizeMode mode, double tau,
                           i64 s_warm) {
     SketchOut out;
@@ -565,6 +660,22 @@ static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, Fina
             out.saturated = true;
             out.rounds = rounds;
             return out;
+        }
+        // speculative batch: size from the previous sketch's round count
+        // (ramp 2, 4, 8, ... without history), bounded by the remaining
+        // dimensions and the 128-column Cholesky panel
+        if (E.batching && p.np <= 1) {
+            const i64 room = (st.min_dim - st.rank) / p.dt;
+            const int kmax = static_cast<int>(std::min<i64>(std::min<i64>(kMaxOmegaBatch, 128 / p.dt), room));
+            const int est = (E.last_rounds > 0) ? (E.last_rounds - rounds + 1) : std::max(2, 2 * rounds);
+            const int K = std::min(kmax, est);
+            if (K >= 2) {
+                const int acc = qb_extend_batch(E, st, p, rounds + 1, K);
+                if (acc > 0) {
+                    rounds += acc;
+                    continue;
+                }
+            }
         }
         ++rounds;
         const double* omega = nullptr;
@@ -583,6 +694,7 @@ static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, Fina
         }
         qb_extend(E, st, p.dt, p.np, derive_seed_u(p.seed, static_cast<u64>(rounds)), omega);
     }
+    E.last_rounds = rounds;
     finalize_mode(E, st, mode, tau, s_warm, p.seed, out.f);
     out.rank = st.rank;
     out.saturated = false;

@@ -76,9 +76,12 @@ struct Engine {
     Vals Y;
     DevBuf<double> Om, OmBank, X, X2, P, T, C, D, G, Rinv, hh, tmp, W, lam, Vraw, Wk;
     DevBuf<double> fkZ, fkZq, fkZt, fkWn, fkH, fkYh, fkth, fkZY, fkXr, fkres;  // finalize_kept
+    DevBuf<double> OmW, XW, TW, CW, GW, RW, eW;  // speculative round batches
     DevBuf<int> perm;
     QBDev qb;  // persistent QB storage: capacity survives across SVT iterations
-    Engine(svt_ctx* c, svt_mat* m, Vals y) : ctx(c), mat(m), Y(y) {}
+    bool batching = true;  // speculative multi-round batches (exact-arithmetic equivalent)
+    int last_rounds = -1;  // rounds of the previous sketch (batch-size predictor)
+    Engine(svt_ctx* c, svt_mat* m, Vals y) : ctx(c), mat(m), Y(y), batching(c->batching != 0) {}
 };
 
 // primitives

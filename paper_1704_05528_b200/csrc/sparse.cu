@@ -123,15 +123,27 @@ __global__ void __launch_bounds__(128) spmm_wide_kernel(SegPlanView plan, const 
             vl = __ldg(val + k);
         }
         const int cnt = static_cast<int>(min(32LL, end - k0));
-        for (int e = 0; e < cnt; ++e) {
-            const int c = __shfl_sync(0xffffffffu, cl, e);
-            const double v = __shfl_sync(0xffffffffu, vl, e);
-            const double* xr = X + static_cast<long long>(c) * ldx + c0;
+        // four entries' gathers in flight per step (entries past cnt carry
+        // v = 0 from the masked index/value load)
+        for (int e = 0; e < cnt; e += 4) {
+            double xv[4][4], vv[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const long long j = lane + 32 * q;
-                if (c0 + j < w) acc[q] = fma(v, __ldg(xr + j), acc[q]);
+            for (int u = 0; u < 4; ++u) {
+                const int src = (e + u) & 31;
+                const int c = __shfl_sync(0xffffffffu, cl, src);
+                vv[u] = __shfl_sync(0xffffffffu, vl, src);
+                if (e + u >= cnt) vv[u] = 0.0;
+                const double* xr = X + static_cast<long long>(c) * ldx + c0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const long long j = lane + 32 * q;
+                    xv[u][q] = (c0 + j < w) ? __ldg(xr + j) : 0.0;
+                }
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = fma(vv[u], xv[u][q], acc[q]);
         }
     }
     const int slot = plan.seg_slot[sg];

@@ -390,3 +390,34 @@ def test_held_out_metrics_match_oracle():
     for a, b in zip(g.trace, o.trace):
         assert abs(a["test_rmse"] - b["test_rmse"]) <= 1e-8 * b["test_rmse"]
         assert abs(a["test_mae"] - b["test_mae"]) <= 1e-8 * b["test_mae"]
+
+
+# ---- speculative round batches -----------------------------------------------
+@pytest.mark.parametrize("seed", [3, 4])
+def test_batched_rounds_equal_sequential_and_oracle(seed):
+    S = random_sampled(400, 300, 0.2, 200 + seed)
+    ctx = G.default_context()
+    p = params(10, 10, 1, 0.02, seed)
+    ctx.set_batching(False)
+    try:
+        seq = G.r3svd(gpu_mat(S), p)
+    finally:
+        ctx.set_batching(True)
+    bat = G.r3svd(gpu_mat(S), p)
+    o = O.r3svd(S, p)
+    assert o.extension_rounds > 8
+    check_sketch(seq, o)
+    check_sketch(bat, o)
+
+
+def test_batched_svt_matches_oracle_many_rounds():
+    A = O.make_low_rank(300, 260, 8, 61)
+    S = O.sample_dense(A, 0.3, 62)
+    cfg = O.default_config(S)
+    cfg.maxit = 12
+    cfg.seed = 63
+    cfg.eps_threshold0 = 0.05
+    g = G.svt_run(gpu_mat(S), cfg, StopRule.none())
+    o = O.svt_run(S, cfg, StopRule.none())
+    assert max(r["extension_rounds"] for r in o.trace) >= 10
+    check_runs(g, o)
