@@ -564,7 +564,8 @@ static void finalize_mode(Engine& E, const QBDev& st, FinalizeMode mode, double 
 // stopping round are discarded.  Returns the number of rounds accepted, or
 // -1 when the panel is numerically rank deficient (the caller re-runs the
 // rounds one by one with the exact fallback semantics).
-static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int round0, int K) {
+static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int round0, int K,
+                           double* last_gain) {
     svt_ctx* c = E.ctx;
     svt_mat* A = E.mat;
     const i64 w = p.dt, W = K * w, m = A->m_local, n = A->n, r0 = st.rank;
@@ -637,6 +638,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         double ek = 0.0;
         for (i64 q = 0; q < w; ++q) ek += e[static_cast<size_t>(k * w + q)];
         st.norm_b_sq += ek;
+        *last_gain = ek / st.frob_y_sq;
         st.rank += w;
         ++accepted;
     }
@@ -652,6 +654,7 @@ static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, Fina
     // (seed, round) (sketch.hpp:246-247), so they are generated kMaxOmegaBatch
     // at a time by independent mt19937_64 warps in two launches.
     int bank_first = 1, bank_count = 0;
+    double last_gain = -1.0;  // energy fraction added by the latest round
     const i64 n = E.mat->n;
     while (error_percentage(st) > p.eps_threshold) {
         if (st.saturated) {
@@ -667,12 +670,23 @@ static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, Fina
         if (E.batching && p.np <= 1) {
             const i64 room = (st.min_dim - st.rank) / p.dt;
             const int kmax = static_cast<int>(std::min<i64>(std::min<i64>(kMaxOmegaBatch, 128 / p.dt), room));
-            const int est = (E.last_rounds > 0) ? (E.last_rounds - rounds + 1) : std::max(2, 2 * rounds);
+            // rounds still needed: the previous sketch's count (round counts
+            // grow slowly while the threshold cools) and a linear
+            // extrapolation of the last round's energy gain (gains shrink
+            // round by round, so this underestimates: no wasted work)
+            int est = (E.last_rounds > 0) ? (E.last_rounds - rounds + 1) : std::max(2, 2 * rounds);
+            const double ep = error_percentage(st);
+            if (last_gain > 0.0) {
+                const double need = (ep - p.eps_threshold) / last_gain;
+                est = std::max(est, static_cast<int>(std::min(1e6, std::ceil(need))) + 1);
+            }
             const int K = std::min(kmax, est);
             if (K >= 2) {
-                const int acc = qb_extend_batch(E, st, p, rounds + 1, K);
+                const double nb0 = st.norm_b_sq;
+                const int acc = qb_extend_batch(E, st, p, rounds + 1, K, &last_gain);
                 if (acc > 0) {
                     rounds += acc;
+                    (void)nb0;
                     continue;
                 }
             }
@@ -692,7 +706,9 @@ static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, Fina
             }
             omega = E.OmBank.get() + static_cast<i64>(rounds - bank_first) * n * p.dt;
         }
+        const double nb_before = st.norm_b_sq;
         qb_extend(E, st, p.dt, p.np, derive_seed_u(p.seed, static_cast<u64>(rounds)), omega);
+        last_gain = (st.norm_b_sq - nb_before) / st.frob_y_sq;
     }
     E.last_rounds = rounds;
     finalize_mode(E, st, mode, tau, s_warm, p.seed, out.f);
