@@ -132,6 +132,174 @@ __global__ void scale2d_kernel(double* C, long long M, long long N, long long ld
     C[i * ldc + j] = (beta != 0.0) ? beta * C[i * ldc + j] : 0.0;
 }
 
+// ---------------------------------------------------------------------------
+// FP64 tensor-core GEMM: mma.sync.aligned.m8n8k4.f64 (SASS DMMA).  tcgen05
+// has no f64 kind on sm_100a, so DMMA is the FP64 tensor path.  CTA tile
+// 64 x BN, 8 warps as 2 (M) x 4 (N), warp tile 32 x BN/4 = 4 x (BN/32)
+// m8n8 accumulators; BK = 16 staged in shared memory with a register
+// prefetch of the next stage (double buffer).  Fragment layouts (PTX ISA,
+// m8n8k4 .f64): A[g][t], B[t][g], C[g][2t..2t+1] with g = lane / 4,
+// t = lane % 4.  Shared rows are padded to a stride of 4 mod 16 doubles so
+// the 4 k-rows x 8 m-columns of a fragment load hit distinct bank pairs.
+// ---------------------------------------------------------------------------
+constexpr int kDmmaBM = 64;
+constexpr int kDmmaBK = 16;
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int BN, bool TA>
+__global__ void __launch_bounds__(256) dmma_gemm_kernel(long long M, long long N, long long K, double alpha,
+                                                        const double* __restrict__ A, long long lda,
+                                                        const double* __restrict__ B, long long ldb, double beta,
+                                                        double* __restrict__ C, long long ldc, long long kchunk,
+                                                        double* __restrict__ partial, const int* __restrict__ pred) {
+    if (pred != nullptr && *pred == 0) return;
+    constexpr int BM = kDmmaBM, BK = (BN == 128) ? 8 : kDmmaBK;  // 128-wide tiles stage 8 k-rows (smem)
+    constexpr int SA = BM + 4;          // padded strides (== 4 mod 16 doubles)
+    constexpr int SB = BN + ((BN % 16 == 4) ? 0 : (4 + 16 - (BN % 16)) % 16);
+    constexpr int NT = BN / 32;         // n8 tiles per warp
+    constexpr int A_PER = BK * BM / 256;
+    constexpr int B_PER = BK * BN / 256;
+    __shared__ double As[2][BK][SA];
+    __shared__ double Bs[2][BK][SB];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = (warp >> 2) * 32;          // warp's m offset in the tile
+    const int wn = (warp & 3) * (BN / 4);     // warp's n offset
+    const long long i0 = static_cast<long long>(blockIdx.x) * BM;
+    const long long j0 = static_cast<long long>(blockIdx.y) * BN;
+    const long long kbeg = static_cast<long long>(blockIdx.z) * kchunk;
+    const long long kend = min(K, kbeg + kchunk);
+    double acc[4][NT][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    double ra[A_PER], rb[B_PER];
+    auto load = [&](long long k0) {
+#pragma unroll
+        for (int q = 0; q < A_PER; ++q) {
+            const int e = tid + q * 256;
+            int kk, ii;
+            if (TA) {
+                kk = e / BM;
+                ii = e % BM;
+            } else {
+                ii = e / BK;
+                kk = e % BK;
+            }
+            const long long k = k0 + kk, i = i0 + ii;
+            ra[q] = (k < kend && i < M) ? __ldg(TA ? (A + k * lda + i) : (A + i * lda + k)) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < B_PER; ++q) {
+            const int e = tid + q * 256;
+            const int kk = e / BN, jj = e % BN;
+            const long long k = k0 + kk, j = j0 + jj;
+            rb[q] = (k < kend && j < N) ? __ldg(B + k * ldb + j) : 0.0;
+        }
+    };
+    auto store = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < A_PER; ++q) {
+            const int e = tid + q * 256;
+            int kk, ii;
+            if (TA) {
+                kk = e / BM;
+                ii = e % BM;
+            } else {
+                ii = e / BK;
+                kk = e % BK;
+            }
+            As[buf][kk][ii] = ra[q];
+        }
+#pragma unroll
+        for (int q = 0; q < B_PER; ++q) {
+            const int e = tid + q * 256;
+            Bs[buf][e / BN][e % BN] = rb[q];
+        }
+    };
+    int buf = 0;
+    if (kbeg < kend) {
+        load(kbeg);
+        store(0);
+    }
+    __syncthreads();
+    for (long long k0 = kbeg; k0 < kend; k0 += BK) {
+        const bool more = k0 + BK < kend;
+        if (more) load(k0 + BK);
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[4], bf[NT];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) af[a] = As[buf][kk + t][wm + a * 8 + g];
+#pragma unroll
+            for (int b = 0; b < NT; ++b) bf[b] = Bs[buf][kk + t][wn + b * 8 + g];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < NT; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
+        if (more) store(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
+    }
+    // epilogue: C fragment (g, 2t) and (g, 2t + 1) of each 8x8 tile
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const long long i = i0 + wm + a * 8 + g;
+        if (i >= M) continue;
+#pragma unroll
+        for (int b = 0; b < NT; ++b) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const long long j = j0 + wn + b * 8 + 2 * t + h;
+                if (j >= N) continue;
+                if (gridDim.z == 1) {
+                    const double o = (beta != 0.0) ? beta * C[i * ldc + j] : 0.0;
+                    C[i * ldc + j] = fma(alpha, acc[a][b][h], o);
+                } else {
+                    partial[(static_cast<long long>(blockIdx.z) * M + i) * N + j] = acc[a][b][h];
+                }
+            }
+        }
+    }
+}
+
+template <int BN>
+void dmma_launch(svt_ctx* ctx, bool transA, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+                 const double* B, i64 ldb, double beta, double* C, i64 ldc, const int* pred) {
+    const i64 mt = (M + kDmmaBM - 1) / kDmmaBM, nt = (N + BN - 1) / BN;
+    const i64 tiles = mt * nt;
+    i64 splits = 1;
+    const i64 target = 2LL * ctx->num_sms;
+    if (tiles < target && K > 32 * kDmmaBK) {
+        splits = std::min<i64>((target + tiles - 1) / tiles, (K + 32 * kDmmaBK - 1) / (32 * kDmmaBK));
+        splits = std::min<i64>(splits, 512);
+        while (splits > 1 && splits * M * N > (32LL << 20)) splits /= 2;
+    }
+    i64 kchunk = (K + splits - 1) / splits;
+    kchunk = ((kchunk + kDmmaBK - 1) / kDmmaBK) * kDmmaBK;  // multiple of both 16 and 8
+    splits = std::max<i64>(1, (K + kchunk - 1) / kchunk);
+    if (splits > 1) ctx->ws_partial.ensure(static_cast<size_t>(splits * M * N));
+    dim3 grid(static_cast<unsigned>(mt), static_cast<unsigned>(nt), static_cast<unsigned>(splits));
+    if (transA)
+        dmma_gemm_kernel<BN, true><<<grid, 256, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
+                                                                  kchunk, ctx->ws_partial.get(), pred);
+    else
+        dmma_gemm_kernel<BN, false><<<grid, 256, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
+                                                                   kchunk, ctx->ws_partial.get(), pred);
+    if (splits > 1) {
+        const i64 tot = M * N;
+        gemm_reduce_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(
+            M, N, static_cast<int>(splits), ctx->ws_partial.get(), alpha, beta, C, ldc, pred);
+    }
+}
+
 template <int BM, int BN, int BK, int TM, int TN>
 void gemm_launch(svt_ctx* ctx, bool transA, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
                  const double* B, i64 ldb, double beta, double* C, i64 ldc, const int* pred) {
@@ -1268,7 +1436,13 @@ void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha,
                 break;
         }
     }
-    gemm_launch<64, 64, 16, 4, 4>(ctx, transA, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
+    // FP64 tensor cores (DMMA) for everything wider than the skinny paths
+    if (N <= 32)
+        dmma_launch<32>(ctx, transA, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
+    else if (N <= 64)
+        dmma_launch<64>(ctx, transA, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
+    else
+        dmma_launch<128>(ctx, transA, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
 }
 
 void gram_chol(svt_ctx* ctx, const double* X, i64 ldx, i64 m, i64 w, double* G, double* Rinv, int* status,
