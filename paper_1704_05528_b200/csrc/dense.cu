@@ -952,7 +952,7 @@ constexpr int kCholMax = 128;  // widest Cholesky panel (a batch of rounds)
 constexpr int kHhMax = 64;     // widest Householder fallback panel
 
 // L lives in dynamic shared memory, row stride w + 1 (w <= 128: 132 KB).
-__global__ void __launch_bounds__(256) chol_rinv_kernel(const double* __restrict__ G, int w,
+__global__ void __launch_bounds__(1024) chol_rinv_kernel(const double* __restrict__ G, int w,
                                                         double* __restrict__ Rinv, int* __restrict__ status,
                                                         const int* __restrict__ pred) {
     if (pred != nullptr && *pred == 0) return;
@@ -989,17 +989,25 @@ __global__ void __launch_bounds__(256) chol_rinv_kernel(const double* __restrict
         }
         __syncthreads();
     }
-    // Rinv = L^{-T}: column c by back substitution on L^T x = e_c
-    for (int c = tid; c < w; c += blockDim.x) {
-        double x[kCholMax];
-        for (int r = 0; r < w; ++r) x[r] = 0.0;
-        x[c] = 1.0 / L[c * ld + c];
-        for (int r = c - 1; r >= 0; --r) {
+    // in-place inverse of the lower factor (LAPACK trti2 order): for j from
+    // the last column down, column j of L^{-1} = -L^{-1}_{trailing} L[:, j] / L_jj
+    double* tv = dorig;  // reuse as the column temporary (dorig is dead now)
+    for (int j = w - 1; j >= 0; --j) {
+        const double ajj = 1.0 / L[j * ld + j];
+        for (int i = j + 1 + tid; i < w; i += blockDim.x) {
             double s = 0.0;
-            for (int t = r + 1; t <= c; ++t) s += L[t * ld + r] * x[t];
-            x[r] = -s / L[r * ld + r];
+            for (int k = j + 1; k <= i; ++k) s = fma(L[i * ld + k], L[k * ld + j], s);
+            tv[i] = s;
         }
-        for (int r = 0; r < w; ++r) Rinv[r * w + c] = x[r];
+        __syncthreads();
+        for (int i = j + 1 + tid; i < w; i += blockDim.x) L[i * ld + j] = -ajj * tv[i];
+        if (tid == 0) L[j * ld + j] = ajj;
+        __syncthreads();
+    }
+    // Rinv = L^{-T} (upper), row-major
+    for (int e = tid; e < w * w; e += blockDim.x) {
+        const int r = e / w, c = e % w;
+        Rinv[e] = (r <= c) ? L[c * ld + r] : 0.0;
     }
     if (tid == 0 && fail) status[0] = 1;
 }
@@ -1493,7 +1501,7 @@ void chol_rinv(svt_ctx* ctx, const double* G, i64 w, double* Rinv, int* status, 
         attr_set = true;
     }
     LaunchScope ls(ctx, K_QR, 16.0 * w * w, w * w * w / 3.0);
-    chol_rinv_kernel<<<1, 256, smem, ctx->stream>>>(G, static_cast<int>(w), Rinv, status, pred);
+    chol_rinv_kernel<<<1, 1024, smem, ctx->stream>>>(G, static_cast<int>(w), Rinv, status, pred);
 }
 
 void householder_qr(svt_ctx* ctx, const double* X, i64 m, i64 w, i64 ldx, double* Q, i64 ldq, double* work,
