@@ -164,7 +164,11 @@ __global__ void __launch_bounds__(256) dmma_gemm_kernel(long long M, long long N
     constexpr int NT = BN / 32;         // n8 tiles per warp
     constexpr int A_PER = BK * BM / 256;
     constexpr int B_PER = BK * BN / 256;
-    __shared__ double As[2][BK][SA];
+    // A tile: k-major [BK][SA] when A^T is streamed (rows of A are k), and
+    // row-major [BM][BK + 4] otherwise so the coalesced global rows store
+    // without bank conflicts (stride 4 mod 16 doubles for the fragments)
+    constexpr int SAR = BK + 4;
+    __shared__ double As[2][TA ? BK * SA : BM * SAR];
     __shared__ double Bs[2][BK][SB];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -215,7 +219,10 @@ __global__ void __launch_bounds__(256) dmma_gemm_kernel(long long M, long long N
                 ii = e / BK;
                 kk = e % BK;
             }
-            As[buf][kk][ii] = ra[q];
+            if (TA)
+                As[buf][kk * SA + ii] = ra[q];
+            else
+                As[buf][ii * SAR + kk] = ra[q];
         }
 #pragma unroll
         for (int q = 0; q < B_PER; ++q) {
@@ -236,7 +243,8 @@ __global__ void __launch_bounds__(256) dmma_gemm_kernel(long long M, long long N
         for (int kk = 0; kk < BK; kk += 4) {
             double af[4], bf[NT];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) af[a] = As[buf][kk + t][wm + a * 8 + g];
+            for (int a = 0; a < 4; ++a)
+                af[a] = TA ? As[buf][(kk + t) * SA + wm + a * 8 + g] : As[buf][(wm + a * 8 + g) * SAR + kk + t];
 #pragma unroll
             for (int b = 0; b < NT; ++b) bf[b] = Bs[buf][kk + t][wn + b * 8 + g];
 #pragma unroll

@@ -54,21 +54,22 @@ inline u64 splitmix64(u64 x) {
 // grow Q / B^T capacity geometrically, preserving the first `rank` columns
 void ensure_cap(Engine& E, QBDev& st, i64 need) {
     if (need <= st.cap) return;
-    i64 cap = std::max<i64>(need, std::max<i64>(32, st.cap * 2));
-    cap = std::min<i64>(std::max(cap, need), std::max(st.min_dim, need));
+    // grow by 1.5x (small bases double): the basis reaches tens of thousands
+    // of columns at config 5, where a doubling would overshoot HBM
+    const i64 grown = (st.cap < 4096) ? st.cap * 2 : st.cap + st.cap / 2;
+    i64 cap = std::max<i64>(need + 128, std::max<i64>(64, grown));
+    cap = std::min<i64>(cap, std::max(st.min_dim, need));
     cap = (cap + 7) & ~7LL;
-    DevBuf<double> Q2(static_cast<size_t>(std::max<i64>(1, st.m_local) * cap));
-    DevBuf<double> B2(static_cast<size_t>(st.n * cap));
-    if (st.rank > 0) {
-        if (st.m_local > 0)
-            SVT_CUDA(cudaMemcpy2DAsync(Q2.get(), cap * sizeof(double), st.Q.get(), st.cap * sizeof(double),
-                                       st.rank * sizeof(double), st.m_local, cudaMemcpyDeviceToDevice,
-                                       E.ctx->stream));
-        SVT_CUDA(cudaMemcpy2DAsync(B2.get(), cap * sizeof(double), st.Bt.get(), st.cap * sizeof(double),
-                                   st.rank * sizeof(double), st.n, cudaMemcpyDeviceToDevice, E.ctx->stream));
-    }
-    st.Q = std::move(Q2);
-    st.Bt = std::move(B2);
+    // one buffer at a time, so the transient peak is old Q + new Q + old B^T
+    auto regrow = [&](DevBuf<double>& buf, i64 rows) {
+        DevBuf<double> nb(static_cast<size_t>(std::max<i64>(1, rows) * cap));
+        if (st.rank > 0 && rows > 0)
+            SVT_CUDA(cudaMemcpy2DAsync(nb.get(), cap * sizeof(double), buf.get(), st.cap * sizeof(double),
+                                       st.rank * sizeof(double), rows, cudaMemcpyDeviceToDevice, E.ctx->stream));
+        buf = std::move(nb);  // frees the old buffer (cudaFree orders after the copy)
+    };
+    regrow(st.Q, st.m_local);
+    regrow(st.Bt, st.n);
     st.cap = cap;
 }
 
