@@ -1595,6 +1595,23 @@ void copy2d(svt_ctx* ctx, const double* src, i64 lds, double* dst, i64 ldd, i64 
     copy2d_kernel<<<nblk(rows * cols), 256, 0, ctx->stream>>>(src, lds, dst, ldd, rows, cols, pred);
 }
 
+__global__ void cheb_combine_kernel(double* out, const double* __restrict__ GY, const double* __restrict__ Y,
+                                    const double* Xp, long long count, double c, double alpha, double beta) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= count) return;
+    double v = alpha * (GY[e] - c * Y[e]);
+    if (Xp != nullptr) v -= beta * Xp[e];
+    out[e] = v;
+}
+
+void cheb_combine(svt_ctx* ctx, double* out, const double* GY, const double* Y, const double* Xp, i64 count,
+                  double c, double alpha, double beta) {
+    if (count <= 0) return;
+    LaunchScope ls(ctx, K_FINAL, 32.0 * count, 4.0 * count);
+    cheb_combine_kernel<<<nblk(count), 256, 0, ctx->stream>>>(out, GY, Y, beta != 0.0 ? Xp : nullptr, count, c,
+                                                              alpha, beta);
+}
+
 void set_identity_cols(svt_ctx* ctx, double* Z, i64 rows, i64 ld, i64 s) {
     if (rows * s <= 0) return;
     LaunchScope ls(ctx, K_OTHER, 8.0 * rows * s, 0.0);

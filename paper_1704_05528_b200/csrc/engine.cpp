@@ -459,10 +459,11 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
         gemm(c, K_FINAL, true, r, b, n, 1.0, st.Bt.get(), st.cap, Wn.get(), b, 0.0, Z.get(), b);
         gemm(c, K_FINAL, true, b, b, r, 1.0, Zq.get(), b, Z.get(), b, 0.0, H.get(), b);
         sym_eig(c, H.get(), b, Yh.get(), th.get());
-        gemm(c, K_FINAL, false, r, b, b, 1.0, Z.get(), b, Yh.get(), b, 0.0, ZY.get(), b);
-        gemm(c, K_FINAL, false, r, b, b, 1.0, Zq.get(), b, Yh.get(), b, 0.0, Xr.get(), b);
-        sub_scaled_cols(c, ZY.get(), Xr.get(), r, b, b, th.get());
-        col_sumsq(c, ZY.get(), r, b, b, res2.get());
+        gemm(c, K_FINAL, false, r, b, b, 1.0, Z.get(), b, Yh.get(), b, 0.0, ZY.get(), b);   // G X
+        gemm(c, K_FINAL, false, r, b, b, 1.0, Zq.get(), b, Yh.get(), b, 0.0, Xr.get(), b);  // X (Ritz)
+        copy2d(c, ZY.get(), b, Zt.get(), b, r, b);
+        sub_scaled_cols(c, Zt.get(), Xr.get(), r, b, b, th.get());
+        col_sumsq(c, Zt.get(), r, b, b, res2.get());
         th_h.resize(static_cast<size_t>(b));
         res_h.resize(static_cast<size_t>(b));
         SVT_CUDA(cudaMemcpyAsync(th_h.data(), th.get(), sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream));
@@ -487,7 +488,33 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
         const i64 check = std::min(b, kk + 1);
         for (i64 i = 0; i < check; ++i)
             if (!(std::sqrt(std::max(res_h[static_cast<size_t>(i)], 0.0)) <= tol)) conv = false;
-        if (conv || b == r) break;
+        if (conv || b == r || it == maxit - 1) break;
+        // Chebyshev filter (Zhou & Saad's scaled recurrence) on the Ritz
+        // block: damps the unwanted interval [0, tau^2] of G = B B^T and
+        // amplifies the eigenvalues above it; the first product G X is the
+        // Rayleigh-Ritz step's Z Yh.  Z <- p_d(G) X for the next sweep.
+        const double lmax = th_h[0];
+        if (kk > 0 && lmax > tau2 * (1.0 + 1e-12)) {
+            const int degree = 8;
+            const double e = 0.5 * tau2, cc = 0.5 * tau2;
+            const double sigma1 = e / (lmax - cc);
+            double sigma = sigma1;
+            double* Xp = Xr.get();  // p_{j-1}
+            double* Yc = Z.get();   // p_j
+            double* GY = ZY.get();  // G p_j (starts as G X)
+            cheb_combine(c, Yc, GY, Xp, nullptr, r * b, cc, sigma1 / e, 0.0);  // p_1
+            for (int j = 2; j <= degree; ++j) {
+                gemm(c, K_FINAL, false, n, b, r, 1.0, st.Bt.get(), st.cap, Yc, b, 0.0, Wn.get(), b);
+                gemm(c, K_FINAL, true, r, b, n, 1.0, st.Bt.get(), st.cap, Wn.get(), b, 0.0, GY, b);
+                const double sn = 1.0 / (2.0 / sigma1 - sigma);
+                cheb_combine(c, Xp, GY, Yc, Xp, r * b, cc, 2.0 * sn / e, sigma * sn);  // p_{j} -> Xp
+                std::swap(Xp, Yc);
+                sigma = sn;
+            }
+            if (Yc != Z.get()) copy2d(c, Yc, b, Z.get(), b, r, b);
+        } else {
+            copy2d(c, ZY.get(), b, Z.get(), b, r, b);  // plain subspace step
+        }
     }
     c->stats[K_FINAL].flops += 0.0;
     const i64 kc = std::min(b, kk + 1);

@@ -96,6 +96,10 @@ void copy2d(svt_ctx* ctx, const double* src, i64 lds, double* dst, i64 ldd, i64 
 void fill(svt_ctx* ctx, double* p, i64 n, double v);
 // Z[:, 0:s] <- the first s columns of the identity (rows x s, ld)
 void set_identity_cols(svt_ctx* ctx, double* Z, i64 rows, i64 ld, i64 s);
+// out[i] = alpha * (GY[i] - c * Y[i]) - beta * Xp[i]  (Chebyshev filter step;
+// Xp may be null when beta == 0; out may alias Xp)
+void cheb_combine(svt_ctx* ctx, double* out, const double* GY, const double* Y, const double* Xp, i64 count,
+                  double c, double alpha, double beta);
 // Y[:, j] -= theta[j] * X[:, j]  (rows x cols, same ld)
 void sub_scaled_cols(svt_ctx* ctx, double* Y, const double* X, i64 rows, i64 cols, i64 ld, const double* theta);
 // out (cols x rows) = in^T ; in (rows x cols, ldi) ; out ld = rows
