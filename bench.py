@@ -22,6 +22,11 @@ import time
 
 import numpy as np
 
+# load every kernel of libsvt_b200 at context creation: with lazy module
+# loading the first launch of a template variant (e.g. a wider DMMA tile once
+# the basis grows) lands inside the timed region
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 

@@ -2,6 +2,8 @@
 // the per-context stream / communicator / instrumentation state.
 #pragma once
 
+#include <algorithm>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -73,9 +75,11 @@ struct DevBuf {
         SVT_CUDA(cudaMalloc(&p, count * sizeof(T)));
         n = count;
     }
-    // grow-only; contents are not preserved
+    // grow-only, with 1.5x slack once allocated (workspaces sized by the
+    // basis rank grow a little every SVT iteration, and cudaFree stalls the
+    // device); contents are not preserved
     void ensure(size_t count) {
-        if (count > n) alloc(count);
+        if (count > n) alloc(n ? std::max(count, n + n / 2) : count);
     }
     void release() {
         if (p) cudaFree(p);

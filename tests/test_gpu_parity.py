@@ -421,3 +421,21 @@ def test_batched_svt_matches_oracle_many_rounds():
     o = O.svt_run(S, cfg, StopRule.none())
     assert max(r["extension_rounds"] for r in o.trace) >= 10
     check_runs(g, o)
+
+
+# ---- kept-mode finalize on a wide basis (Rayleigh-Ritz path, rank > 48) --------
+@pytest.mark.parametrize("seed", [71, 72])
+def test_svt_kept_finalize_wide_basis(seed):
+    rng = np.random.default_rng(seed)
+    A = O.make_low_rank(500, 400, 12, seed) + 0.3 * rng.standard_normal((500, 400))
+    S = O.sample_dense(A, 0.3, seed + 1)
+    cfg = O.default_config(S)
+    cfg.t0 = 80
+    cfg.dt = 16
+    cfg.maxit = 6
+    cfg.seed = seed + 2
+    g = G.svt_run(gpu_mat(S), cfg, StopRule.none())
+    o = O.svt_run(S, cfg, StopRule.none())
+    assert all(r["rank"] > 48 for r in o.trace)
+    assert o.trace[0]["kept"] > 0 and max(r["kept"] for r in o.trace) >= 8
+    check_runs(g, o)
