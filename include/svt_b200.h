@@ -130,6 +130,9 @@ int svt_ctx_reset_stats(svt_ctx* ctx);
 int svt_ctx_kernel_stats(svt_ctx* ctx, int cls, int64_t* launches, double* total_ms, double* bytes,
                          double* flops);
 int64_t svt_ctx_launch_count(svt_ctx* ctx);
+/* host-side accounting: stream synchronizations the library issued and the
+ * host time spent blocked in them (timed only while profiling is on) */
+int svt_ctx_host_stats(svt_ctx* ctx, int64_t* syncs, double* sync_ms);
 /* 1 (default): speculative multi-round batches in the rank-revealing loop
  * (same rounds / ranks; exact-arithmetic equivalent); 0: one round at a time. */
 int svt_ctx_set_batching(svt_ctx* ctx, int on);
@@ -166,6 +169,15 @@ int svt_sp_axpy(svt_mat* Y, double alpha, const double* d_vals, double* out_vals
 int svt_sp_frob_norm_sq(svt_mat* S, double* out);                                 /* sampled.hpp:178 */
 int svt_spectral_norm_est(svt_mat* S, int iters, uint64_t seed, double* out);     /* sampled.hpp:188 */
 int svt_kickstart(svt_mat* A, double tau, double delta, uint64_t seed, double* out_vals); /* solver.hpp:125 */
+
+/* Device-pointer FP64 contraction on the context stream, row-major:
+ * C (M x N) = alpha * op(A) * B + beta * C, op(A) = A^T (A stored K x M) when
+ * transA, else A (M x K).  The kernel family behind every dense product of
+ * the sketch (block Gram-Schmidt Q^T X / X - Q C, CholQR Grams, B = Q^T Y
+ * updates; sketch.hpp:133-141, dense.hpp:103-110); exposed for tuning and
+ * its own parity tests.  Asynchronous. */
+int svt_dev_gemm(svt_ctx* ctx, int transA, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                 int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
 
 /* ---- sketch engines (sketch.hpp) -------------------------------------- */
 int svt_rsvd(svt_mat* Y, int64_t k, const svt_sketch_params* p, svt_factors** out);  /* sketch.hpp:165 */

@@ -20,7 +20,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._abi import (OBSERVER_FN, Backend, IterationRecord, SketchParams, StopRule, SvtConfig, raise_for)
+from ._abi import (OBSERVER_FN, Backend, InvalidArgument, IterationRecord, SketchParams, StopRule, SvtConfig,
+                   raise_for)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libsvt_b200.so")
@@ -113,6 +114,12 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().svt_ctx_launch_count(self.h))
 
+    def host_stats(self):
+        """(stream synchronizations issued, host ms blocked in them)."""
+        n, ms = C.c_int64(), C.c_double()
+        _check(lib().svt_ctx_host_stats(self.h, C.byref(n), C.byref(ms)))
+        return dict(syncs=n.value, sync_ms=ms.value)
+
     def set_batching(self, on: bool):
         """Speculative multi-round batches (default on; same rounds/ranks)."""
         _check(lib().svt_ctx_set_batching(self.h, C.c_int(1 if on else 0)))
@@ -137,6 +144,28 @@ def default_context() -> Context:
     if _default_ctx is None:
         _default_ctx = Context(0)
     return _default_ctx
+
+
+def dev_gemm(a, b, c, trans_a=False, alpha=1.0, beta=0.0, ctx: Context | None = None):
+    """C = alpha * op(A) @ B + beta * C on the device (svt_dev_gemm) for
+    row-major contiguous float64 CUDA tensors; op(A) = A.T when trans_a.
+    Synchronizes torch's stream and the library stream on both sides."""
+    import torch
+    ctx = ctx or default_context()
+    for t in (a, b, c):
+        if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+            raise InvalidArgument("dev_gemm: contiguous float64 CUDA tensors required")
+    K, M = (a.shape[0], a.shape[1]) if trans_a else (a.shape[1], a.shape[0])
+    N = b.shape[1]
+    if b.shape[0] != K or tuple(c.shape) != (M, N):
+        raise InvalidArgument("dev_gemm: shape mismatch")
+    torch.cuda.synchronize()
+    _check(lib().svt_dev_gemm(ctx.h, C.c_int(1 if trans_a else 0), C.c_int64(M), C.c_int64(N), C.c_int64(K),
+                              C.c_double(alpha), C.c_void_p(a.data_ptr()), C.c_int64(a.shape[1]),
+                              C.c_void_p(b.data_ptr()), C.c_int64(N), C.c_double(beta),
+                              C.c_void_p(c.data_ptr()), C.c_int64(N)))
+    ctx.sync()
+    return c
 
 
 # ---------------------------------------------------------------------------

@@ -71,7 +71,7 @@ DevBuf<double> upload_cm(svt_ctx* c, const double* h, i64 rows, i64 cols) {
     for (i64 i = 0; i < rows; ++i)
         for (i64 j = 0; j < cols; ++j) rm[static_cast<size_t>(i * cols + j)] = h[i + j * rows];
     SVT_CUDA(cudaMemcpyAsync(d.get(), rm.data(), sizeof(double) * rm.size(), cudaMemcpyHostToDevice, c->stream));
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
     return d;
 }
 
@@ -79,7 +79,7 @@ void download_cm(svt_ctx* c, const double* d, i64 rows, i64 cols, i64 ld, double
     if (rows * cols == 0) return;
     std::vector<double> rm(static_cast<size_t>(rows * ld));
     SVT_CUDA(cudaMemcpyAsync(rm.data(), d, sizeof(double) * rows * ld, cudaMemcpyDeviceToHost, c->stream));
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
     for (i64 i = 0; i < rows; ++i)
         for (i64 j = 0; j < cols; ++j) h[i + j * rows] = rm[static_cast<size_t>(i * ld + j)];
 }
@@ -114,7 +114,7 @@ int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, sv
         SVT_CUDA(cudaMemsetAsync(c->d_scalars, 0, 64 * sizeof(double), c->stream));
         SVT_CUDA(cudaMemsetAsync(c->d_flags, 0, 64 * sizeof(int), c->stream));
         nccl_init(c->comm, rank, world, nccl_id);
-        SVT_CUDA(cudaStreamSynchronize(c->stream));
+        sync_stream(c.get());
         *out = c.release();
     });
 }
@@ -157,7 +157,7 @@ int svt_ctx_destroy(svt_ctx* ctx) {
 int svt_ctx_sync(svt_ctx* ctx) {
     return guard([&] {
         need(ctx, "svt_ctx_sync");
-        SVT_CUDA(cudaStreamSynchronize(ctx->stream));
+        sync_stream(ctx);
     });
 }
 
@@ -176,6 +176,7 @@ int svt_ctx_set_profiling(svt_ctx* ctx, int on) {
         need(ctx, "svt_ctx_set_profiling");
         flush_stats(ctx);
         ctx->profiling = on != 0;
+        ctx->gap_debug = ctx->profiling && std::getenv("SVTB_DEBUG_GAPS") != nullptr;
     });
 }
 
@@ -185,6 +186,8 @@ int svt_ctx_reset_stats(svt_ctx* ctx) {
         flush_stats(ctx);
         for (auto& s : ctx->stats) s = KStats{};
         ctx->launch_count = 0;
+        ctx->host_syncs = 0;
+        ctx->host_sync_ms = 0.0;
     });
 }
 
@@ -202,6 +205,15 @@ int svt_ctx_kernel_stats(svt_ctx* ctx, int cls, int64_t* launches, double* total
 }
 
 int64_t svt_ctx_launch_count(svt_ctx* ctx) { return ctx ? ctx->launch_count : -1; }
+
+int svt_ctx_host_stats(svt_ctx* ctx, int64_t* syncs, double* sync_ms) {
+    return guard([&] {
+        need(ctx, "svt_ctx_host_stats");
+        if (ctx->gap_debug) print_gap_stats(ctx);
+        if (syncs) *syncs = ctx->host_syncs;
+        if (sync_ms) *sync_ms = ctx->host_sync_ms;
+    });
+}
 
 int svt_ctx_set_batching(svt_ctx* ctx, int on) {
     return guard([&] {
@@ -267,7 +279,7 @@ int svt_matrix_set_values(svt_mat* M, const double* vals) {
         svt_ctx* c = M->ctx;
         SVT_CUDA(cudaMemcpyAsync(M->val.get(), vals, sizeof(double) * M->nnz_local, cudaMemcpyHostToDevice, c->stream));
         scale_values(c, M->nnz_local, M->val.get(), 1.0, M->val.get(), M->csr2csc.get(), M->val_csc.get());
-        SVT_CUDA(cudaStreamSynchronize(c->stream));
+        sync_stream(c);
     });
 }
 
@@ -278,7 +290,7 @@ int svt_matrix_get_values(svt_mat* M, double* vals) {
         need(vals, "svt_matrix_get_values");
         svt_ctx* c = M->ctx;
         SVT_CUDA(cudaMemcpyAsync(vals, M->val.get(), sizeof(double) * M->nnz_local, cudaMemcpyDeviceToHost, c->stream));
-        SVT_CUDA(cudaStreamSynchronize(c->stream));
+        sync_stream(c);
     });
 }
 
@@ -368,6 +380,17 @@ int svt_small_svd(svt_ctx* ctx, int64_t rows, int64_t cols, const double* B, dou
     });
 }
 
+int svt_dev_gemm(svt_ctx* ctx, int transA, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                 int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+    return guard([&] {
+        need(ctx, "svt_dev_gemm");
+        if (M < 0 || N < 0 || K < 0) throw std::invalid_argument("dev_gemm: negative dimension");
+        if (!A || !B || !C) throw std::invalid_argument("dev_gemm: null operand");
+        if (ldb < N || ldc < N || lda < (transA ? M : K)) throw std::invalid_argument("dev_gemm: leading dimension");
+        gemm(ctx, K_GEMM, transA != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    });
+}
+
 int svt_sp_mult(svt_mat* S, int64_t w, const double* X, double* out) {
     return guard([&] {
         need(S, "svt_sp_mult");
@@ -411,7 +434,7 @@ int svt_project_low_rank(svt_mat* P, int64_t k, const double* U, const double* s
         sddmm_update(c, P->m_local, P->rowptr.get(), P->col.get(), P->val.get(), out.get(), nullptr, nullptr,
                      P->nnz_local, P->n, dU.get(), k, dV.get(), k, k, 0.0, 2, c->d_scalars + 40);
         SVT_CUDA(cudaMemcpyAsync(out_vals, out.get(), sizeof(double) * P->nnz_local, cudaMemcpyDeviceToHost, c->stream));
-        SVT_CUDA(cudaStreamSynchronize(c->stream));
+        sync_stream(c);
     });
 }
 
@@ -425,7 +448,7 @@ int svt_sp_axpy(svt_mat* Y, double alpha, const double* d_vals, double* out_vals
         SVT_CUDA(cudaMemcpyAsync(d.get(), d_vals, sizeof(double) * nnz, cudaMemcpyHostToDevice, c->stream));
         axpy_values(c, nnz, Y->val.get(), alpha, d.get(), o.get());
         SVT_CUDA(cudaMemcpyAsync(out_vals, o.get(), sizeof(double) * nnz, cudaMemcpyDeviceToHost, c->stream));
-        SVT_CUDA(cudaStreamSynchronize(c->stream));
+        sync_stream(c);
     });
 }
 
@@ -457,7 +480,7 @@ int svt_kickstart(svt_mat* A, double tau, double delta, uint64_t seed, double* o
         if (A->nnz_local > 0)
             SVT_CUDA(cudaMemcpyAsync(out_vals, y.get(), sizeof(double) * A->nnz_local, cudaMemcpyDeviceToHost,
                                      c->stream));
-        SVT_CUDA(cudaStreamSynchronize(c->stream));
+        sync_stream(c);
     });
 }
 
@@ -515,7 +538,7 @@ int svt_r4svd(svt_mat* Y, int64_t s, const double* U_prev, int64_t ldu, const sv
                 for (i64 j = 0; j < s; ++j) rm[static_cast<size_t>(i * s + j)] = U_prev[i + j * ldu];
             SVT_CUDA(cudaMemcpyAsync(dU.get(), rm.data(), sizeof(double) * rm.size(), cudaMemcpyHostToDevice,
                                      c->stream));
-            SVT_CUDA(cudaStreamSynchronize(c->stream));
+            sync_stream(c);
         }
         SketchOut so = r4svd(E, dU.get(), s, s, *p, FinalizeMode::Full, 0.0);
         wrap_factors(out, std::move(so.f), so.rank, so.saturated, so.rounds);

@@ -6,7 +6,10 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdlib>
+#include <map>
 #include <cstdio>
 #include <memory>
 #include <stdexcept>
@@ -45,6 +48,17 @@ struct oom_error : std::runtime_error {
 
 #define SVT_CHECK_LAUNCH() SVT_CUDA(cudaGetLastError())
 
+// Process-wide device allocation counters (host time in cudaMalloc/cudaFree).
+struct AllocStats {
+    long long count = 0, frees = 0;
+    double bytes = 0.0, ms = 0.0;
+    bool verbose = std::getenv("SVTB_DEBUG_ALLOC") != nullptr;
+};
+inline AllocStats& alloc_stats() {
+    static AllocStats s;
+    return s;
+}
+
 // RAII device allocation.
 template <typename T>
 struct DevBuf {
@@ -72,7 +86,14 @@ struct DevBuf {
     void alloc(size_t count) {
         release();
         if (count == 0) return;
+        const auto t0 = std::chrono::steady_clock::now();
         SVT_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        alloc_stats().count++;
+        alloc_stats().bytes += static_cast<double>(count * sizeof(T));
+        alloc_stats().ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (alloc_stats().verbose)
+            std::fprintf(stderr, "[alloc] #%lld %.3f MB (%zu x %zu B)\n", alloc_stats().count,
+                         count * sizeof(T) / 1e6, count, sizeof(T));
         n = count;
     }
     // grow-only, with 1.5x slack once allocated (workspaces sized by the
@@ -82,7 +103,12 @@ struct DevBuf {
         if (count > n) alloc(n ? std::max(count, n + n / 2) : count);
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            const auto t0 = std::chrono::steady_clock::now();
+            cudaFree(p);
+            alloc_stats().frees++;
+            alloc_stats().ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        }
         p = nullptr;
         n = 0;
     }
@@ -142,6 +168,15 @@ struct svt_ctx {
     int batching = 1;  // speculative multi-round batches in the rank-revealing loop
     svtb::i64 launch_count = 0;
     svtb::KStats stats[svtb::K_NCLASS];
+    svtb::i64 host_syncs = 0;     // stream synchronizations issued by the library
+    double host_sync_ms = 0.0;    // host time spent blocked in them (profiling only)
+    // debug (SVTB_DEBUG_GAPS): host latency from a sync's return to the next
+    // launch, per sync site -- the device idles for that long
+    bool gap_debug = false;
+    bool gap_open = false;
+    int gap_site = 0;
+    std::chrono::steady_clock::time_point gap_t0;
+    std::map<int, std::pair<long long, double>> gap_stats;
     struct Pending {
         cudaEvent_t a, b;
         int cls;
@@ -174,6 +209,10 @@ struct LaunchScope {
     LaunchScope(svt_ctx* c, int k, double bytes, double flops);
     ~LaunchScope() noexcept(false);
 };
+// Blocking wait for the context stream (counted; timed when profiling).
+void print_gap_stats(svt_ctx* c);
+void sync_stream(svt_ctx* c, int site = __builtin_LINE(), const char* file = __builtin_FILE());
+
 void flush_stats(svt_ctx* ctx);  // resolve pending event pairs (syncs)
 
 }  // namespace svtb

@@ -278,24 +278,208 @@ __global__ void __launch_bounds__(256) dmma_gemm_kernel(long long M, long long N
     }
 }
 
+// ---------------------------------------------------------------------------
+// Same DMMA tile, fed by a 3-stage cp.async (LDGSTS) pipeline with BK = 16:
+// global -> shared copies bypass the registers (no staging registers, so the
+// 64 accumulator registers fit two CTAs per SM) and two stages are in flight
+// while the warps run 64 DMMA per stage.  Requires 16-byte aligned operands
+// with even leading dimensions (checked by the launcher; the register-staged
+// kernel above handles the rest).  Out-of-range elements are zero-filled by
+// the copy's src-size operand.
+// ---------------------------------------------------------------------------
+constexpr int kCpStages = 3;
+constexpr int kCpBK = 16;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int bytes) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int BN, bool TA>
+struct CpTile {
+    static constexpr int BM = kDmmaBM, BK = kCpBK;
+    static constexpr int SA = BM + 4;   // TA: [BK][SA]
+    static constexpr int SAR = BK + 4;  // !TA: [BM][SAR]
+    static constexpr int SB = BN + 4;   // [BK][SB]; BN + 4 == 4 mod 16 for BN in {32, 64, 128}
+    static constexpr int A_ELEMS = TA ? BK * SA : BM * SAR;
+    static constexpr int B_ELEMS = BK * SB;
+    static constexpr size_t SMEM = sizeof(double) * kCpStages * (A_ELEMS + B_ELEMS);
+};
+
+template <int BN, bool TA>
+__global__ void __launch_bounds__(256, 2) dmma_cp_kernel(long long M, long long N, long long K, double alpha,
+                                                         const double* __restrict__ A, long long lda,
+                                                         const double* __restrict__ B, long long ldb, double beta,
+                                                         double* __restrict__ C, long long ldc, long long kchunk,
+                                                         double* __restrict__ partial, const int* __restrict__ pred) {
+    if (pred != nullptr && *pred == 0) return;
+    using T = CpTile<BN, TA>;
+    constexpr int BM = T::BM, BK = T::BK, SA = T::SA, SAR = T::SAR, SB = T::SB;
+    constexpr int NT = BN / 32;
+    constexpr int A_CH = BM * BK / 2 / 256;  // 16-byte chunks per thread
+    constexpr int B_CH = BK * BN / 2 / 256;
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;
+    double* Bs = smem + kCpStages * T::A_ELEMS;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = (warp >> 2) * 32;
+    const int wn = (warp & 3) * (BN / 4);
+    const long long i0 = static_cast<long long>(blockIdx.x) * BM;
+    const long long j0 = static_cast<long long>(blockIdx.y) * BN;
+    const long long kbeg = static_cast<long long>(blockIdx.z) * kchunk;
+    const long long kend = min(K, kbeg + kchunk);
+    const long long nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+    auto issue = [&](int stage, long long k0) {
+        double* as = As + stage * T::A_ELEMS;
+        double* bs = Bs + stage * T::B_ELEMS;
+#pragma unroll
+        for (int q = 0; q < A_CH; ++q) {
+            const int c = tid + q * 256;
+            if (TA) {
+                const int kk = c / (BM / 2), ii = (c % (BM / 2)) * 2;
+                const long long k = k0 + kk, i = i0 + ii;
+                const int v = (k < kend) ? static_cast<int>(max(0LL, min(2LL, M - i))) : 0;
+                cp_async16(as + kk * SA + ii, v ? A + k * lda + i : A, 8 * v);
+            } else {
+                const int ii = c / (BK / 2), kk = (c % (BK / 2)) * 2;
+                const long long k = k0 + kk, i = i0 + ii;
+                const int v = (i < M) ? static_cast<int>(max(0LL, min(2LL, kend - k))) : 0;
+                cp_async16(as + ii * SAR + kk, v ? A + i * lda + k : A, 8 * v);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < B_CH; ++q) {
+            const int c = tid + q * 256;
+            const int kk = c / (BN / 2), jj = (c % (BN / 2)) * 2;
+            const long long k = k0 + kk, j = j0 + jj;
+            const int v = (k < kend) ? static_cast<int>(max(0LL, min(2LL, N - j))) : 0;
+            cp_async16(bs + kk * SB + jj, v ? B + k * ldb + j : B, 8 * v);
+        }
+    };
+    double acc[4][NT][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll
+    for (int st = 0; st < kCpStages - 1; ++st) {
+        if (st < nk) issue(st, kbeg + st * BK);
+        cp_async_commit();
+    }
+    for (long long it = 0; it < nk; ++it) {
+        cp_async_wait<kCpStages - 2>();
+        __syncthreads();
+        const long long nx = it + kCpStages - 1;
+        if (nx < nk) issue(static_cast<int>(nx % kCpStages), kbeg + nx * BK);
+        cp_async_commit();
+        const int stg = static_cast<int>(it % kCpStages);
+        const double* as = As + stg * T::A_ELEMS;
+        const double* bs = Bs + stg * T::B_ELEMS;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double af[4], bf[NT];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+                af[a] = TA ? as[(kk + t) * SA + wm + a * 8 + g] : as[(wm + a * 8 + g) * SAR + kk + t];
+#pragma unroll
+            for (int b = 0; b < NT; ++b) bf[b] = bs[(kk + t) * SB + wn + b * 8 + g];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < NT; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const long long i = i0 + wm + a * 8 + g;
+        if (i >= M) continue;
+#pragma unroll
+        for (int b = 0; b < NT; ++b) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const long long j = j0 + wn + b * 8 + 2 * t + h;
+                if (j >= N) continue;
+                if (gridDim.z == 1) {
+                    const double o = (beta != 0.0) ? beta * C[i * ldc + j] : 0.0;
+                    C[i * ldc + j] = fma(alpha, acc[a][b][h], o);
+                } else {
+                    partial[(static_cast<long long>(blockIdx.z) * M + i) * N + j] = acc[a][b][h];
+                }
+            }
+        }
+    }
+}
+
 template <int BN>
 void dmma_launch(svt_ctx* ctx, bool transA, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
                  const double* B, i64 ldb, double beta, double* C, i64 ldc, const int* pred) {
     const i64 mt = (M + kDmmaBM - 1) / kDmmaBM, nt = (N + BN - 1) / BN;
     const i64 tiles = mt * nt;
+    // the cp.async pipeline needs 16-byte aligned rows
+    const bool cp = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
+                    (reinterpret_cast<uintptr_t>(B) % 16 == 0) && !std::getenv("SVTB_NO_CPASYNC");
+    // resident CTAs per wave (occupancy of this instantiation, cached)
+    static int per_sm[4] = {0, 0, 0, 0};
+    int& ps = per_sm[(transA ? 1 : 0) + (cp ? 2 : 0)];
+    if (ps == 0) {
+        if (cp) {
+            SVT_CUDA(cudaFuncSetAttribute(dmma_cp_kernel<BN, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(CpTile<BN, true>::SMEM)));
+            SVT_CUDA(cudaFuncSetAttribute(dmma_cp_kernel<BN, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(CpTile<BN, false>::SMEM)));
+            if (transA)
+                SVT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, dmma_cp_kernel<BN, true>, 256,
+                                                                       CpTile<BN, true>::SMEM));
+            else
+                SVT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, dmma_cp_kernel<BN, false>, 256,
+                                                                       CpTile<BN, false>::SMEM));
+        } else if (transA) {
+            SVT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, dmma_gemm_kernel<BN, true>, 256, 0));
+        } else {
+            SVT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, dmma_gemm_kernel<BN, false>, 256, 0));
+        }
+        ps = std::max(1, ps);
+    }
+    const i64 cap = static_cast<i64>(ps) * ctx->num_sms;
+    // split-K: minimise waves x k-steps per CTA (+ the partial-sum traffic of
+    // the fixed-order reduction), so a grid never ends in a nearly empty wave
     i64 splits = 1;
-    const i64 target = 2LL * ctx->num_sms;
-    if (tiles < target && K > 32 * kDmmaBK) {
-        splits = std::min<i64>((target + tiles - 1) / tiles, (K + 32 * kDmmaBK - 1) / (32 * kDmmaBK));
-        splits = std::min<i64>(splits, 512);
-        while (splits > 1 && splits * M * N > (32LL << 20)) splits /= 2;
+    if (K > 32 * kDmmaBK) {
+        const i64 kmax = std::min<i64>(512, (K + 32 * kDmmaBK - 1) / (32 * kDmmaBK));
+        double best = 1e300;
+        for (i64 sp = 1; sp <= kmax; ++sp) {
+            if (sp > 1 && sp * M * N > (32LL << 20)) break;
+            const i64 waves = (tiles * sp + cap - 1) / cap;
+            const double ksteps = std::ceil(static_cast<double>(K) / (sp * kDmmaBK));
+            // a k-step of one CTA streams (BM + BN) x BK doubles; the reduce
+            // reads sp partial tiles once
+            const double cost = waves * ksteps * (kDmmaBM + BN) * kDmmaBK +
+                                (sp > 1 ? static_cast<double>(sp) * M * N / cap * 4.0 : 0.0);
+            if (cost < best * 0.999) {
+                best = cost;
+                splits = sp;
+            }
+        }
     }
     i64 kchunk = (K + splits - 1) / splits;
     kchunk = ((kchunk + kDmmaBK - 1) / kDmmaBK) * kDmmaBK;  // multiple of both 16 and 8
     splits = std::max<i64>(1, (K + kchunk - 1) / kchunk);
     if (splits > 1) ctx->ws_partial.ensure(static_cast<size_t>(splits * M * N));
     dim3 grid(static_cast<unsigned>(mt), static_cast<unsigned>(nt), static_cast<unsigned>(splits));
-    if (transA)
+    if (cp && transA)
+        dmma_cp_kernel<BN, true><<<grid, 256, CpTile<BN, true>::SMEM, ctx->stream>>>(
+            M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, ctx->ws_partial.get(), pred);
+    else if (cp)
+        dmma_cp_kernel<BN, false><<<grid, 256, CpTile<BN, false>::SMEM, ctx->stream>>>(
+            M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, ctx->ws_partial.get(), pred);
+    else if (transA)
         dmma_gemm_kernel<BN, true><<<grid, 256, 0, ctx->stream>>>(M, N, K, alpha, A, lda, B, ldb, beta, C, ldc,
                                                                   kchunk, ctx->ws_partial.get(), pred);
     else
@@ -960,6 +1144,11 @@ constexpr int kCholMax = 128;  // widest Cholesky panel (a batch of rounds)
 constexpr int kHhMax = 64;     // widest Householder fallback panel
 
 // L lives in dynamic shared memory, row stride w + 1 (w <= 128: 132 KB).
+// Right-looking Cholesky with the pivot division folded into the trailing
+// update (A_ik -= A_ij A_kj / A_jj), so each column step needs one barrier;
+// the columns are scaled by 1/sqrt(pivot) in one pass at the end.  The
+// triangular inverse runs column by column (LAPACK trti2 order) with eight
+// threads per row splitting each dot product (shuffle-reduced).
 __global__ void __launch_bounds__(1024) chol_rinv_kernel(const double* __restrict__ G, int w,
                                                         double* __restrict__ Rinv, int* __restrict__ status,
                                                         const int* __restrict__ pred) {
@@ -967,9 +1156,11 @@ __global__ void __launch_bounds__(1024) chol_rinv_kernel(const double* __restric
     extern __shared__ double dyn[];
     double* L = dyn;               // w x (w + 1)
     double* dorig = dyn + w * (w + 1);
+    __shared__ double piv[kCholMax];
     __shared__ int fail;
     const int ld = w + 1;
     const int tid = threadIdx.x;
+    const int tx = tid & 31, ty = tid >> 5;
     if (tid == 0) fail = 0;
     for (int e = tid; e < w * w; e += blockDim.x) L[(e / w) * ld + e % w] = G[e];
     __syncthreads();
@@ -982,33 +1173,44 @@ __global__ void __launch_bounds__(1024) chol_rinv_kernel(const double* __restric
         // the Householder fallback, which keeps all columns like
         // qr_orthonormal (dense.hpp:100-102)
         const bool bad = !(dorig[j] > 0.0) || !(d > 1e-13 * dorig[j]) || !(d < CUDART_INF);
-        const double ljj = sqrt(bad ? 1.0 : d);
-        __syncthreads();
+        const double dd = bad ? 1.0 : d;
+        const double inv = 1.0 / dd;
         if (tid == 0) {
             if (bad) fail = 1;
-            L[j * ld + j] = ljj;
+            piv[j] = dd;
         }
-        for (int i = j + 1 + tid; i < w; i += blockDim.x) L[i * ld + j] /= ljj;
-        __syncthreads();
-        const int rem = w - j - 1;
-        for (int e = tid; e < rem * rem; e += blockDim.x) {
-            const int i = j + 1 + e / rem, k = j + 1 + e % rem;
-            if (k <= i) L[i * ld + k] -= L[i * ld + j] * L[k * ld + j];
+        // trailing update of the lower triangle, rows i > j, columns j < k <= i
+        for (int i = j + 1 + ty; i < w; i += 32) {
+            const double lij = L[i * ld + j] * inv;
+            for (int k = j + 1 + tx; k <= i; k += 32) L[i * ld + k] -= lij * L[k * ld + j];
         }
         __syncthreads();
     }
-    // in-place inverse of the lower factor (LAPACK trti2 order): for j from
-    // the last column down, column j of L^{-1} = -L^{-1}_{trailing} L[:, j] / L_jj
+    // scale: L_ij = A_ij / sqrt(d_j) (i > j), L_jj = sqrt(d_j)
+    for (int e = tid; e < w * w; e += blockDim.x) {
+        const int i = e / w, j = e % w;
+        if (j < i)
+            L[i * ld + j] *= rsqrt(piv[j]);
+        else if (j == i)
+            L[i * ld + i] = sqrt(piv[i]);
+    }
+    __syncthreads();
+    // in-place inverse of the lower factor: for j from the last column down,
+    // column j of L^{-1} = -L^{-1}_{trailing} L[:, j] / L_jj
     double* tv = dorig;  // reuse as the column temporary (dorig is dead now)
+    const int sub = tid & 7, row0 = tid >> 3;  // 8 threads per row, 128 rows
     for (int j = w - 1; j >= 0; --j) {
-        const double ajj = 1.0 / L[j * ld + j];
-        for (int i = j + 1 + tid; i < w; i += blockDim.x) {
-            double s = 0.0;
-            for (int k = j + 1; k <= i; ++k) s = fma(L[i * ld + k], L[k * ld + j], s);
-            tv[i] = s;
-        }
+        const int i = j + 1 + row0;
+        double s = 0.0;
+        if (i < w)
+            for (int k = j + 1 + sub; k <= i; k += 8) s = fma(L[i * ld + k], L[k * ld + j], s);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        if (i < w && sub == 0) tv[i] = s;
         __syncthreads();
-        for (int i = j + 1 + tid; i < w; i += blockDim.x) L[i * ld + j] = -ajj * tv[i];
+        const double ajj = 1.0 / L[j * ld + j];
+        for (int r = j + 1 + tid; r < w; r += blockDim.x) L[r * ld + j] = -ajj * tv[r];
         if (tid == 0) L[j * ld + j] = ajj;
         __syncthreads();
     }
@@ -1554,7 +1756,7 @@ void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
     // sort descending on the host (r values), gather the eigenvectors
     std::vector<double> lh(static_cast<size_t>(rp));
     SVT_CUDA(cudaMemcpyAsync(lh.data(), lam_u, sizeof(double) * rp, cudaMemcpyDeviceToHost, ctx->stream));
-    SVT_CUDA(cudaStreamSynchronize(ctx->stream));
+    sync_stream(ctx);
     std::vector<int> perm(static_cast<size_t>(r));
     for (i64 j = 0; j < r; ++j) perm[static_cast<size_t>(j)] = static_cast<int>(j);
     // the padded zero column (if any) is index r and is excluded
@@ -1568,7 +1770,7 @@ void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
         LaunchScope ls(ctx, K_FINAL, 16.0 * r * r, 0.0);
         gather_eigvecs_kernel<<<nblk(r * r), 256, 0, ctx->stream>>>(V, rp, dperm.get(), r, W);
     }
-    SVT_CUDA(cudaStreamSynchronize(ctx->stream));
+    sync_stream(ctx);
 }
 
 void col_sumsq(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double* out) {

@@ -33,13 +33,13 @@ int* dfl(svt_ctx* c, int i) { return c->d_flags + i; }
 
 double read_scalar(svt_ctx* c, int i) {
     SVT_CUDA(cudaMemcpyAsync(c->h_scalars + i, c->d_scalars + i, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
     return c->h_scalars[i];
 }
 
 int read_flag(svt_ctx* c, int i) {
     SVT_CUDA(cudaMemcpyAsync(c->h_flags + i, c->d_flags + i, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
     return c->h_flags[i];
 }
 
@@ -79,13 +79,13 @@ void ensure_cap(Engine& E, QBDev& st, i64 need) {
     const bool dbg = std::getenv("SVTB_DEBUG_CAP") != nullptr;
     std::chrono::steady_clock::time_point t0;
     if (dbg) {
-        SVT_CUDA(cudaStreamSynchronize(E.ctx->stream));
+        sync_stream(E.ctx);
         t0 = std::chrono::steady_clock::now();
     }
     regrow(st.Q, st.m_local);
     regrow(st.Bt, st.n);
     if (dbg) {
-        SVT_CUDA(cudaStreamSynchronize(E.ctx->stream));
+        sync_stream(E.ctx);
         const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         std::fprintf(stderr, "[ensure_cap] %lld -> %lld cols (rank %lld): %.1f ms\n", static_cast<long long>(st.cap),
                      static_cast<long long>(cap), static_cast<long long>(st.rank), ms);
@@ -371,7 +371,7 @@ void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFact
     sym_eig(c, E.G.get(), r, E.W.get(), E.lam.get());
     std::vector<double> lam(static_cast<size_t>(r));
     SVT_CUDA(cudaMemcpyAsync(lam.data(), E.lam.get(), sizeof(double) * r, cudaMemcpyDeviceToHost, c->stream));
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
     i64 kc = r;
     if (mode == FinalizeMode::Kept) {
         i64 cnt = 0;
@@ -385,7 +385,7 @@ void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFact
     col_sumsq(c, E.Vraw.get(), n, kc, kc, E.lam.get());
     std::vector<double> s2(static_cast<size_t>(kc));
     SVT_CUDA(cudaMemcpyAsync(s2.data(), E.lam.get(), sizeof(double) * kc, cudaMemcpyDeviceToHost, c->stream));
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
     std::vector<double> sig(static_cast<size_t>(kc));
     for (i64 j = 0; j < kc; ++j) sig[static_cast<size_t>(j)] = std::sqrt(s2[static_cast<size_t>(j)]);
     std::vector<int> perm(static_cast<size_t>(kc));
@@ -424,7 +424,7 @@ void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFact
     gemm(c, K_FINAL, false, m, k, r, 1.0, st.Q.get(), st.cap, E.Wk.get(), k, 0.0, out.U.get(), k);
     // keep the host copy of sigma in sync with the stream (the inv upload
     // above reads a host vector that dies with this frame)
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
 }
 
 // Kept-mode finalize for larger bases: only the triplets with sigma > tau
@@ -490,7 +490,7 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
         res_h.resize(static_cast<size_t>(b));
         SVT_CUDA(cudaMemcpyAsync(th_h.data(), th.get(), sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream));
         SVT_CUDA(cudaMemcpyAsync(res_h.data(), res2.get(), sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream));
-        SVT_CUDA(cudaStreamSynchronize(c->stream));
+        sync_stream(c);
         kk = 0;
         while (kk < b && th_h[static_cast<size_t>(kk)] > tau2 * (1.0 - 1e-6)) ++kk;
         if (kk == b && b < r) {
@@ -566,7 +566,7 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
             }
             SVT_CUDA(cudaMemcpyAsync(res2.get(), sc.data(), sizeof(double) * b, cudaMemcpyHostToDevice, c->stream));
             scale_cols(c, Z.get(), r, b, b, res2.get());
-            SVT_CUDA(cudaStreamSynchronize(c->stream));  // sc dies with this scope
+            sync_stream(c);  // sc dies with this scope
         } else {
             copy2d(c, ZY.get(), b, Z.get(), b, r, b);  // plain subspace step
         }
@@ -583,7 +583,7 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
     col_sumsq(c, E.Vraw.get(), n, kc, kc, E.lam.get());
     std::vector<double> s2(static_cast<size_t>(kc));
     SVT_CUDA(cudaMemcpyAsync(s2.data(), E.lam.get(), sizeof(double) * kc, cudaMemcpyDeviceToHost, c->stream));
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
     std::vector<double> sig(static_cast<size_t>(kc));
     for (i64 j = 0; j < kc; ++j) sig[static_cast<size_t>(j)] = std::sqrt(s2[static_cast<size_t>(j)]);
     std::vector<int> perm(static_cast<size_t>(kc));
@@ -614,7 +614,7 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
     permute_cols(c, Xr.get(), r, b, E.perm.get(), k, E.Wk.get(), k);
     out.U.ensure(static_cast<size_t>(std::max<i64>(1, m) * k));
     gemm(c, K_FINAL, false, m, k, r, 1.0, st.Q.get(), st.cap, E.Wk.get(), k, 0.0, out.U.get(), k);
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
 }
 
 static double error_percentage(const QBDev& st) {
@@ -683,7 +683,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         col_sumsq(c, E.CW.get(), r0, W, W, E.eW.get() + W);
         std::vector<double> cs(static_cast<size_t>(2 * W));
         SVT_CUDA(cudaMemcpyAsync(cs.data(), E.eW.get(), sizeof(double) * 2 * W, cudaMemcpyDeviceToHost, c->stream));
-        SVT_CUDA(cudaStreamSynchronize(c->stream));
+        sync_stream(c);
         bool second = false;
         for (int k = 0; k < K && !second; ++k) {
             double nx = 0.0, nc = 0.0;
@@ -716,7 +716,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
     col_sumsq(c, E.TW.get(), n, W, W, E.eW.get());
     std::vector<double> e(static_cast<size_t>(W));
     SVT_CUDA(cudaMemcpyAsync(e.data(), E.eW.get(), sizeof(double) * W, cudaMemcpyDeviceToHost, c->stream));
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
     // replay the reference's loop test round by round
     int accepted = 0;
     for (int k = 0; k < K; ++k) {
@@ -896,7 +896,7 @@ DevFactors rsvd(Engine& E, i64 k, const svt_sketch_params& p) {
         copy2d(E.ctx, f.V.get(), f.k, g.V.get(), k, f.n, k);
         SVT_CUDA(cudaMemcpyAsync(g.d_sigma.get(), f.d_sigma.get(), sizeof(double) * k, cudaMemcpyDeviceToDevice,
                                  E.ctx->stream));
-        SVT_CUDA(cudaStreamSynchronize(E.ctx->stream));
+        sync_stream(E.ctx);
         return g;
     }
     return f;
@@ -922,7 +922,7 @@ DevFactors full_svd(Engine& E) {
     densify_dev(c, A->m, A->n, A->rowptr.get(), A->col.get(), E.Y.csr, dense.get());
     st.Bt.ensure(static_cast<size_t>(A->n * A->m));
     transpose(c, dense.get(), A->m, A->n, A->n, st.Bt.get());
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
     DevFactors f;
     finalize(E, st, FinalizeMode::Full, 0.0, f);
     return f;

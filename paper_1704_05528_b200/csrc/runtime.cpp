@@ -2,6 +2,8 @@
 // NCCL communicator (resolved with dlopen so single-GPU use never needs it).
 #include <dlfcn.h>
 
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 
 #include "common.hpp"
@@ -10,6 +12,12 @@ namespace svtb {
 
 LaunchScope::LaunchScope(svt_ctx* c, int k, double bytes, double flops) : ctx(c), cls(k) {
     ctx->launch_count++;
+    if (ctx->gap_open) {
+        auto& g = ctx->gap_stats[ctx->gap_site];
+        g.first++;
+        g.second += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ctx->gap_t0).count();
+        ctx->gap_open = false;
+    }
     KStats& s = ctx->stats[k];
     s.launches++;
     s.bytes += bytes;
@@ -39,6 +47,32 @@ LaunchScope::~LaunchScope() noexcept(false) {
     }
     if (e != cudaSuccess && std::uncaught_exceptions() == 0)
         throw cuda_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
+}
+
+void sync_stream(svt_ctx* c, int site, const char* file) {
+    c->host_syncs++;
+    if (!c->profiling) {
+        SVT_CUDA(cudaStreamSynchronize(c->stream));
+        return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    const auto t1 = std::chrono::steady_clock::now();
+    c->host_sync_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+    if (c->gap_debug) {
+        c->gap_open = true;
+        c->gap_site = site + (file && std::strstr(file, "engine") ? 100000 : file && std::strstr(file, "solver") ? 200000 : 300000);
+        c->gap_t0 = t1;
+    }
+}
+
+void print_gap_stats(svt_ctx* c) {
+    std::fprintf(stderr, "[alloc] %lld mallocs, %lld frees, %.1f MB, %.3f ms\n", alloc_stats().count,
+                 alloc_stats().frees, alloc_stats().bytes / 1e6, alloc_stats().ms);
+    for (auto& kv : c->gap_stats)
+        std::fprintf(stderr, "[gaps] site %d: %lld gaps, %.3f ms total, %.1f us mean\n", kv.first, kv.second.first,
+                     kv.second.second, 1000.0 * kv.second.second / std::max(1LL, kv.second.first));
+    c->gap_stats.clear();
 }
 
 void flush_stats(svt_ctx* ctx) {

@@ -72,7 +72,7 @@ void to_host_cm(svt_ctx* c, const double* d, i64 rows, i64 k, std::vector<double
     if (rows * k == 0) return;
     std::vector<double> tmp(static_cast<size_t>(rows * k));
     SVT_CUDA(cudaMemcpyAsync(tmp.data(), d, sizeof(double) * rows * k, cudaMemcpyDeviceToHost, c->stream));
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
     for (i64 i = 0; i < rows; ++i)
         for (i64 j = 0; j < k; ++j) out[static_cast<size_t>(i + j * rows)] = tmp[static_cast<size_t>(i * k + j)];
 }
@@ -113,7 +113,7 @@ svt_solver* solver_create(svt_mat* A, const svt_config& cfg, svt_stop stop, svt_
     c->comm.allreduce_sum(c->d_scalars + S_FA, 1, c->stream);
     SVT_CUDA(cudaMemcpyAsync(c->h_scalars + S_FA, c->d_scalars + S_FA, sizeof(double), cudaMemcpyDeviceToHost,
                              c->stream));
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
     S->frob_a = std::sqrt(c->h_scalars[S_FA]);
     S->eps_threshold = cfg.eps_threshold0;
     S->X.m_local = S->best.m_local = A->m_local;
@@ -203,7 +203,7 @@ void solver_step(svt_solver* S, svt_observer_fn obs, void* user, svt_record* rec
     }
     SVT_CUDA(cudaMemcpyAsync(c->h_scalars + S_SUMS, c->d_scalars + S_SUMS, sizeof(double) * 8,
                              cudaMemcpyDeviceToHost, c->stream));
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    sync_stream(c);
     const double* sums = c->h_scalars + S_SUMS;
     const double* tsums = c->h_scalars + S_TSUMS;
 

@@ -158,9 +158,9 @@ __global__ void __launch_bounds__(128) spmm_wide_kernel(SegPlanView plan, const 
     }
 }
 
-// out[row, j] = sum of the row's partial slots, in segment order
-// one warp per long row: lanes stride the row's slots (independent loads),
-// then a fixed-order shuffle tree per output column
+// out[row, j] = sum of the row's partial slots in a fixed (deterministic)
+// order.  Narrow panels: one warp per long row, lanes over the slots, a
+// shuffle tree per column.
 __global__ void seg_reduce_kernel(SegPlanView plan, long long w, const double* __restrict__ partial,
                                   double* __restrict__ out, long long ldo) {
     const int lane = threadIdx.x & 31;
@@ -168,11 +168,41 @@ __global__ void seg_reduce_kernel(SegPlanView plan, long long w, const double* _
     if (l >= plan.nlong) return;
     const int first = plan.long_first[l], cnt = plan.long_count[l];
     const long long row = plan.long_row[l];
+    const double* base = partial + static_cast<long long>(first) * w;
     for (long long j = 0; j < w; ++j) {
         double s = 0.0;
-        for (int t = lane; t < cnt; t += 32) s += partial[static_cast<long long>(first + t) * w + j];
+        for (int t = lane; t < cnt; t += 32) s += base[static_cast<long long>(t) * w + j];
         s = warp_sum(s);
         if (lane == 0) out[row * ldo + j] = s;
+    }
+}
+
+// Wide panels: one CTA of 8 warps per long row (Zipf-popular items have
+// hundreds of slots); warp q sums slots q, q + 8, ... with lanes over the
+// columns (coalesced slot rows), then the 8 warp sums are added in warp
+// order.
+constexpr int kSegRedWarps = 8;
+__global__ void __launch_bounds__(32 * kSegRedWarps) seg_reduce_wide_kernel(SegPlanView plan, long long w,
+                                                                        const double* __restrict__ partial,
+                                                                        double* __restrict__ out, long long ldo) {
+    extern __shared__ double red[];  // [kSegRedWarps][w]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long l = blockIdx.x;
+    const int first = plan.long_first[l], cnt = plan.long_count[l];
+    const long long row = plan.long_row[l];
+    const double* base = partial + static_cast<long long>(first) * w;
+    for (long long j = lane; j < w; j += 32) {
+        double s = 0.0;
+#pragma unroll 4
+        for (int t = warp; t < cnt; t += kSegRedWarps) s += base[static_cast<long long>(t) * w + j];
+        red[warp * w + j] = s;
+    }
+    __syncthreads();
+    for (long long j = threadIdx.x; j < w; j += blockDim.x) {
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < kSegRedWarps; ++q) s += red[q * w + j];
+        out[row * ldo + j] = s;
     }
 }
 
@@ -311,9 +341,23 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
         spmm_wide_kernel<<<grid, 128, 0, ctx->stream>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
     }
     if (plan.nlong > 0) {
-        const i64 thr = plan.nlong * 32;
-        seg_reduce_kernel<<<static_cast<unsigned>((thr + 255) / 256), 256, 0, ctx->stream>>>(plan, w, partial, out,
-                                                                                          ldo);
+        if (w >= 8 && w <= 512) {
+            const size_t smem = sizeof(double) * kSegRedWarps * static_cast<size_t>(w);
+            if (smem > 48 * 1024) {
+                static bool attr = false;
+                if (!attr) {
+                    SVT_CUDA(cudaFuncSetAttribute(seg_reduce_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  static_cast<int>(sizeof(double) * kSegRedWarps * 512)));
+                    attr = true;
+                }
+            }
+            seg_reduce_wide_kernel<<<static_cast<unsigned>(plan.nlong), 32 * kSegRedWarps, smem, ctx->stream>>>(
+                plan, w, partial, out, ldo);
+        } else {
+            const i64 thr = plan.nlong * 32;
+            seg_reduce_kernel<<<static_cast<unsigned>((thr + 255) / 256), 256, 0, ctx->stream>>>(plan, w, partial,
+                                                                                              out, ldo);
+        }
     }
 }
 

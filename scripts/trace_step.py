@@ -1,0 +1,63 @@
+"""Trace a few SVT iterations with torch.profiler (CUPTI): kernel activity of
+libsvt_b200 plus the CUDA runtime calls of the host thread, then report the
+device-idle gaps and the host calls that overlap them.  Development tool."""
+import argparse
+import json
+import os
+import sys
+
+import torch
+from torch.profiler import ProfilerActivity, profile
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1704_05528_b200 import api as G  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+from explore import load  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=4)
+ap.add_argument("--warm", type=int, default=5)
+ap.add_argument("--iters", type=int, default=2)
+ap.add_argument("--out", default="gpurun_out/trace.json")
+args = ap.parse_args()
+
+ctx = G.default_context()
+A, test, cfg, stop, _ = load(args.config, 1)
+S = G.Solver(A, cfg, stop, test=test)
+for _ in range(args.warm):
+    S.step()
+ctx.sync()
+with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
+    for _ in range(args.iters):
+        S.step()
+    ctx.sync()
+prof.export_chrome_trace(args.out)
+ev = json.load(open(args.out))["traceEvents"]
+kern = sorted([(e["ts"], e["ts"] + e.get("dur", 0), e["name"]) for e in ev
+               if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset")], key=lambda x: x[0])
+rt = sorted([(e["ts"], e["ts"] + e.get("dur", 0), e["name"]) for e in ev if e.get("cat") == "cuda_runtime"],
+            key=lambda x: x[0])
+busy = sum(b - a for a, b, _ in kern)
+span = kern[-1][1] - kern[0][0]
+print(f"kernels {len(kern)}  device busy {busy/1e3:.1f} ms of span {span/1e3:.1f} ms  runtime calls {len(rt)}")
+gaps = []
+for (a0, a1, an), (b0, b1, bn) in zip(kern, kern[1:]):
+    if b0 - a1 > 200:
+        gaps.append((b0 - a1, a1, b0, an, bn))
+gaps.sort(reverse=True)
+tot = sum(g[0] for g in gaps)
+print(f"idle gaps > 200 us: {len(gaps)}, total {tot/1e3:.1f} ms")
+from collections import Counter
+for g, a1, b0, an, bn in gaps[:25]:
+    calls = Counter()
+    for r0, r1, rn in rt:
+        ov = min(r1, b0) - max(r0, a1)
+        if ov > 0:
+            calls[rn] += ov
+    top = ", ".join(f"{k} {v/1e3:.2f}ms" for k, v in calls.most_common(4))
+    print(f"  gap {g/1e3:8.2f} ms after {an[:40]:40s} before {bn[:40]:40s} | host: {top}")
+# host-side totals per runtime call
+tot_rt = Counter()
+for r0, r1, rn in rt:
+    tot_rt[rn] += r1 - r0
+print("runtime call totals:", ", ".join(f"{k} {v/1e3:.1f}ms" for k, v in tot_rt.most_common(10)))

@@ -439,3 +439,22 @@ def test_svt_kept_finalize_wide_basis(seed):
     assert all(r["rank"] > 48 for r in o.trace)
     assert o.trace[0]["kept"] > 0 and max(r["kept"] for r in o.trace) >= 8
     check_runs(g, o)
+
+
+# ---- the FP64 contraction kernels (DMMA tiles, split-K, skinny paths) -------
+@pytest.mark.parametrize("shape", [(1300, 120, 69878, True), (69878, 120, 1300, False), (120, 120, 69878, True),
+                                   (69878, 120, 120, False), (37, 5, 1000, True), (1000, 7, 13, False),
+                                   (2000, 64, 3000, True), (513, 33, 77, False), (12, 12, 5000, True)])
+def test_dev_gemm_matches_fp64_reference(shape):
+    import torch
+    M, N, K, ta = shape
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
+    a = torch.randn((K, M) if ta else (M, K), dtype=torch.float64, device="cuda", generator=g)
+    b = torch.randn((K, N), dtype=torch.float64, device="cuda", generator=g)
+    c0 = torch.randn((M, N), dtype=torch.float64, device="cuda", generator=g)
+    c = c0.clone()
+    G.dev_gemm(a, b, c, trans_a=ta, alpha=-0.5, beta=0.75)
+    ref = -0.5 * ((a.T if ta else a) @ b) + 0.75 * c0
+    scale = (a.abs().T if ta else a.abs()) @ b.abs()
+    err = ((c - ref).abs() / (0.5 * scale + 0.75 * c0.abs() + 1e-300)).max().item()
+    assert err <= 1e-13 * max(1.0, np.sqrt(K) / 10), err
