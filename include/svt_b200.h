@@ -179,6 +179,13 @@ int svt_kickstart(svt_mat* A, double tau, double delta, uint64_t seed, double* o
 int svt_dev_gemm(svt_ctx* ctx, int transA, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                  int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
 
+/* Device-pointer sparse products on the context stream (row-major panels):
+ * out (m_local x w) = S * X (X: n x w) or, transpose != 0, out (n x w) = S^T * X
+ * (X: m_local x w, out packed, all-reduced across ranks) -- sampled.hpp:113 /
+ * :130 without the host copies.  Asynchronous. */
+int svt_dev_sp_mult(svt_mat* S, int transpose, int64_t w, const double* X, int64_t ldx, double* out,
+                    int64_t ldo);
+
 /* ---- sketch engines (sketch.hpp) -------------------------------------- */
 int svt_rsvd(svt_mat* Y, int64_t k, const svt_sketch_params* p, svt_factors** out);  /* sketch.hpp:165 */
 int svt_r3svd(svt_mat* Y, const svt_sketch_params* p, svt_factors** out);            /* sketch.hpp:188 */

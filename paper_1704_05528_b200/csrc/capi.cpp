@@ -405,6 +405,22 @@ int svt_sp_mult(svt_mat* S, int64_t w, const double* X, double* out) {
     });
 }
 
+int svt_dev_sp_mult(svt_mat* S, int transpose, int64_t w, const double* X, int64_t ldx, double* out, int64_t ldo) {
+    return guard([&] {
+        need(S, "svt_dev_sp_mult");
+        if (w < 0 || ldx < w || ldo < w) throw std::invalid_argument("dev_sp_mult: bad width / leading dimension");
+        if (w == 0) return;
+        if (!X || !out) throw std::invalid_argument("dev_sp_mult: null panel");
+        Engine E = engine_for(S);
+        if (transpose) {
+            if (ldo != w) throw std::invalid_argument("dev_sp_mult: transposed output must be packed (ldo == w)");
+            sp_mult_t(E, w, X, ldx, out);
+        } else {
+            sp_mult(E, w, X, ldx, out, ldo);
+        }
+    });
+}
+
 int svt_sp_mult_t(svt_mat* S, int64_t w, const double* X, double* out) {
     return guard([&] {
         need(S, "svt_sp_mult_t");

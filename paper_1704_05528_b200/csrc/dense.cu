@@ -1143,75 +1143,156 @@ __global__ void set_flag_kernel(const double* a, const double* b, double coef, i
 constexpr int kCholMax = 128;  // widest Cholesky panel (a batch of rounds)
 constexpr int kHhMax = 64;     // widest Householder fallback panel
 
-// L lives in dynamic shared memory, row stride w + 1 (w <= 128: 132 KB).
-// Right-looking Cholesky with the pivot division folded into the trailing
-// update (A_ik -= A_ij A_kj / A_jj), so each column step needs one barrier;
-// the columns are scaled by 1/sqrt(pivot) in one pass at the end.  The
-// triangular inverse runs column by column (LAPACK trti2 order) with eight
-// threads per row splitting each dot product (shuffle-reduced).
-__global__ void __launch_bounds__(1024) chol_rinv_kernel(const double* __restrict__ G, int w,
+// L lives in dynamic shared memory, row stride w + 1 (w <= 128: 132 KB), plus
+// a w x 8 panel temporary.  Blocked in 8-column panels:
+//  * Cholesky (right-looking): warp 0 factors the 8-column panel in registers
+//    (lane = row, shuffles broadcast the pivots and the panel rows), then all
+//    32 warps apply the rank-8 update to the trailing lower triangle -- two
+//    barriers per panel instead of one per column;
+//  * inverse of the lower factor, block columns from the last: with
+//    L = [[D, 0], [B, E]], L^{-1} = [[D^{-1}, 0], [-E^{-1} B D^{-1}, E^{-1}]],
+//    E^{-1} already in place; T = E^{-1} B is one dot product per element
+//    (all threads), then the block is T D^{-1} and D is inverted by one warp.
+// A pivot that lost more than ~13 digits (kappa(X) beyond ~3e6 in that
+// direction) or a zero / non-finite column sets status, which routes the
+// panel to the Householder fallback (it keeps all columns like
+// qr_orthonormal, dense.hpp:100-102).
+constexpr int kCholPanel = 8;
+
+__global__ void __launch_bounds__(512) chol_rinv_kernel(const double* __restrict__ G, int w,
                                                         double* __restrict__ Rinv, int* __restrict__ status,
                                                         const int* __restrict__ pred) {
     if (pred != nullptr && *pred == 0) return;
+    constexpr int P = kCholPanel;
     extern __shared__ double dyn[];
-    double* L = dyn;               // w x (w + 1)
-    double* dorig = dyn + w * (w + 1);
-    __shared__ double piv[kCholMax];
+    double* L = dyn;                   // w x (w + 1)
+    double* dorig = dyn + w * (w + 1);  // w
+    double* T = dorig + w;              // w x P (panel temporary)
     __shared__ int fail;
     const int ld = w + 1;
-    const int tid = threadIdx.x;
-    const int tx = tid & 31, ty = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) fail = 0;
     for (int e = tid; e < w * w; e += blockDim.x) L[(e / w) * ld + e % w] = G[e];
     __syncthreads();
     if (tid < w) dorig[tid] = L[tid * ld + tid];
     __syncthreads();
-    for (int j = 0; j < w; ++j) {
-        const double d = L[j * ld + j];
-        // a pivot that lost more than ~13 digits (kappa(X) beyond ~3e6 in
-        // that direction) or a zero / non-finite column routes the panel to
-        // the Householder fallback, which keeps all columns like
-        // qr_orthonormal (dense.hpp:100-102)
-        const bool bad = !(dorig[j] > 0.0) || !(d > 1e-13 * dorig[j]) || !(d < CUDART_INF);
-        const double dd = bad ? 1.0 : d;
-        const double inv = 1.0 / dd;
-        if (tid == 0) {
-            if (bad) fail = 1;
-            piv[j] = dd;
+    // ---- Cholesky --------------------------------------------------------
+    for (int c0 = 0; c0 < w; c0 += P) {
+        const int pw = min(P, w - c0);
+        if (warp == 0) {
+            double a[4][P];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int r = c0 + lane + 32 * q;
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) a[q][jj] = (r < w && jj < pw) ? L[r * ld + c0 + jj] : 0.0;
+            }
+            bool bad_any = false;
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) {
+                if (jj < pw) {
+                    const int j = c0 + jj;
+                    const double d = __shfl_sync(0xffffffffu, a[0][jj], jj);
+                    const bool bad = !(dorig[j] > 0.0) || !(d > 1e-13 * dorig[j]) || !(d < CUDART_INF);
+                    bad_any |= bad;
+                    const double sq = sqrt(bad ? 1.0 : d);
+                    const double inv = 1.0 / sq;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int r = c0 + lane + 32 * q;
+                        if (r > j) a[q][jj] *= inv;
+                        else if (r == j) a[q][jj] = sq;
+                    }
+#pragma unroll
+                    for (int kk = jj + 1; kk < P; ++kk) {
+                        if (kk < pw) {
+                            const double lk = __shfl_sync(0xffffffffu, a[0][jj], kk);  // L[c0 + kk][j]
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const int r = c0 + lane + 32 * q;
+                                if (r >= c0 + kk) a[q][kk] -= a[q][jj] * lk;
+                            }
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int r = c0 + lane + 32 * q;
+                if (r < w)
+#pragma unroll
+                    for (int jj = 0; jj < P; ++jj)
+                        if (jj < pw && c0 + jj <= r) L[r * ld + c0 + jj] = a[q][jj];
+            }
+            if (lane == 0 && bad_any) fail = 1;
         }
-        // trailing update of the lower triangle, rows i > j, columns j < k <= i
-        for (int i = j + 1 + ty; i < w; i += 32) {
-            const double lij = L[i * ld + j] * inv;
-            for (int k = j + 1 + tx; k <= i; k += 32) L[i * ld + k] -= lij * L[k * ld + j];
+        __syncthreads();
+        // rank-pw update of the trailing lower triangle
+        const int t0 = c0 + pw;
+        for (int i = t0 + (tid >> 5); i < w; i += (blockDim.x >> 5)) {
+            double li[P];
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) li[jj] = jj < pw ? L[i * ld + c0 + jj] : 0.0;
+            for (int k = t0 + lane; k <= i; k += 32) {
+                double s = L[i * ld + k];
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) s -= li[jj] * L[k * ld + c0 + jj];
+                L[i * ld + k] = s;
+            }
         }
         __syncthreads();
     }
-    // scale: L_ij = A_ij / sqrt(d_j) (i > j), L_jj = sqrt(d_j)
-    for (int e = tid; e < w * w; e += blockDim.x) {
-        const int i = e / w, j = e % w;
-        if (j < i)
-            L[i * ld + j] *= rsqrt(piv[j]);
-        else if (j == i)
-            L[i * ld + i] = sqrt(piv[i]);
-    }
-    __syncthreads();
-    // in-place inverse of the lower factor: for j from the last column down,
-    // column j of L^{-1} = -L^{-1}_{trailing} L[:, j] / L_jj
-    double* tv = dorig;  // reuse as the column temporary (dorig is dead now)
-    const int sub = tid & 7, row0 = tid >> 3;  // 8 threads per row, 128 rows
-    for (int j = w - 1; j >= 0; --j) {
-        const int i = j + 1 + row0;
-        double s = 0.0;
-        if (i < w)
-            for (int k = j + 1 + sub; k <= i; k += 8) s = fma(L[i * ld + k], L[k * ld + j], s);
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        s += __shfl_xor_sync(0xffffffffu, s, 4);
-        if (i < w && sub == 0) tv[i] = s;
+    // ---- inverse of the lower factor, block columns from the last ---------
+    const int nblk = (w + P - 1) / P;
+    for (int bj = nblk - 1; bj >= 0; --bj) {
+        const int c0 = bj * P, pw = min(P, w - c0), t0 = c0 + pw;
+        // T[i - t0][jj] = sum_{t0 <= k <= i} Einv[i][k] * B[k][jj]  (E^{-1} in place)
+        const int nrow = w - t0;
+        for (int e = tid; e < nrow * pw; e += blockDim.x) {
+            const int i = t0 + e / pw, jj = e % pw;
+            double s0 = 0.0, s1 = 0.0;
+            int k = t0;
+            for (; k + 1 <= i; k += 2) {
+                s0 = fma(L[i * ld + k], L[k * ld + c0 + jj], s0);
+                s1 = fma(L[i * ld + k + 1], L[(k + 1) * ld + c0 + jj], s1);
+            }
+            if (k <= i) s0 = fma(L[i * ld + k], L[k * ld + c0 + jj], s0);
+            T[(i - t0) * P + jj] = s0 + s1;
+        }
+        // invert the diagonal block in place (one warp, lane jj = column jj):
+        // x_jj = 1 / D_jj, x_i = -(sum_{jj <= k < i} D_ik x_k) / D_ii
+        if (warp == 0) {
+            double x[P];
+#pragma unroll
+            for (int i = 0; i < P; ++i) x[i] = 0.0;
+            if (lane < pw) {
+#pragma unroll
+                for (int i = 0; i < P; ++i) {
+                    if (i < pw && i >= lane) {
+                        double sacc = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+                        for (int k = 0; k < P; ++k)
+                            if (k >= lane && k < i) sacc -= L[(c0 + i) * ld + c0 + k] * x[k];
+                        x[i] = sacc / L[(c0 + i) * ld + c0 + i];
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane < pw)
+#pragma unroll
+                for (int i = 0; i < P; ++i)
+                    if (i < pw && i >= lane) L[(c0 + i) * ld + c0 + lane] = x[i];
+        }
         __syncthreads();
-        const double ajj = 1.0 / L[j * ld + j];
-        for (int r = j + 1 + tid; r < w; r += blockDim.x) L[r * ld + j] = -ajj * tv[r];
-        if (tid == 0) L[j * ld + j] = ajj;
+        // block below the diagonal: -T * D^{-1}  (D^{-1} lower, in place now)
+        for (int e = tid; e < nrow * pw; e += blockDim.x) {
+            const int i = t0 + e / pw, jj = e % pw;
+            double sacc = 0.0;
+#pragma unroll
+            for (int k = 0; k < P; ++k)
+                if (k >= jj && k < pw) sacc = fma(T[(i - t0) * P + k], L[(c0 + k) * ld + c0 + jj], sacc);
+            L[i * ld + c0 + jj] = -sacc;
+        }
         __syncthreads();
     }
     // Rinv = L^{-T} (upper), row-major
@@ -1703,15 +1784,16 @@ void set_flag(svt_ctx* ctx, const double* a, const double* b, double coef, int m
 
 void chol_rinv(svt_ctx* ctx, const double* G, i64 w, double* Rinv, int* status, const int* pred) {
     if (w > kCholMax) throw std::invalid_argument("chol_rinv: panel wider than 128");
-    const size_t smem = sizeof(double) * static_cast<size_t>(w * (w + 1) + w);
+    const size_t smem = sizeof(double) * static_cast<size_t>(w * (w + 1) + w + w * kCholPanel);
     static bool attr_set = false;
     if (!attr_set) {
-        SVT_CUDA(cudaFuncSetAttribute(chol_rinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(sizeof(double) * (kCholMax * (kCholMax + 1) + kCholMax))));
+        SVT_CUDA(cudaFuncSetAttribute(
+            chol_rinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            static_cast<int>(sizeof(double) * (kCholMax * (kCholMax + 1) + kCholMax + kCholMax * kCholPanel))));
         attr_set = true;
     }
     LaunchScope ls(ctx, K_QR, 16.0 * w * w, w * w * w / 3.0);
-    chol_rinv_kernel<<<1, 1024, smem, ctx->stream>>>(G, static_cast<int>(w), Rinv, status, pred);
+    chol_rinv_kernel<<<1, 512, smem, ctx->stream>>>(G, static_cast<int>(w), Rinv, status, pred);
 }
 
 void householder_qr(svt_ctx* ctx, const double* X, i64 m, i64 w, i64 ldx, double* Q, i64 ldq, double* work,

@@ -15,6 +15,8 @@
 // Wide panels (qb_init at t0 up to 5000): one warp per (row, 128-column
 // chunk); entries are broadcast 32 at a time by shuffle, lanes stride the
 // contiguous panel row (1 KB coalesced per entry).
+#include <cstdlib>
+
 #include "common.hpp"
 #include "kernels.hpp"
 
@@ -101,8 +103,11 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) spmm_narrow_kernel(
     }
 }
 
-// wide: block = 4 warps, each warp one segment, 128 columns (4 per lane) at
-// column chunk blockIdx.y
+// wide: block = 4 warps, each warp one segment, a chunk of 32*Q columns (Q
+// per lane) at column chunk blockIdx.y; U = 16 / Q entries are gathered per
+// step so every warp keeps ~16 independent 8-byte loads per lane in flight
+// whatever the panel width (a 32-wide panel would otherwise be latency bound).
+template <int Q, int U>
 __global__ void __launch_bounds__(128) spmm_wide_kernel(SegPlanView plan, const int* __restrict__ idx,
                                                         const double* __restrict__ val,
                                                         const double* __restrict__ X, long long ldx, long long w,
@@ -111,8 +116,13 @@ __global__ void __launch_bounds__(128) spmm_wide_kernel(SegPlanView plan, const 
     const int lane = threadIdx.x & 31;
     const long long sg = static_cast<long long>(blockIdx.x) * 4 + (threadIdx.x >> 5);
     if (sg >= plan.nseg) return;
-    const long long c0 = static_cast<long long>(blockIdx.y) * 128;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const long long c0 = static_cast<long long>(blockIdx.y) * (32 * Q);
+    double acc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc[q] = 0.0;
+    bool colok[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) colok[q] = c0 + lane + 32 * q < w;
     const long long beg = plan.seg_beg[sg], end = plan.seg_end[sg];
     for (long long k0 = beg; k0 < end; k0 += 32) {
         const long long k = k0 + lane;
@@ -123,34 +133,31 @@ __global__ void __launch_bounds__(128) spmm_wide_kernel(SegPlanView plan, const 
             vl = __ldg(val + k);
         }
         const int cnt = static_cast<int>(min(32LL, end - k0));
-        // four entries' gathers in flight per step (entries past cnt carry
+        // U entries' gathers in flight per step (entries past cnt carry
         // v = 0 from the masked index/value load)
-        for (int e = 0; e < cnt; e += 4) {
-            double xv[4][4], vv[4];
+        for (int e = 0; e < cnt; e += U) {
+            double xv[U][Q], vv[U];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const int src = (e + u) & 31;
                 const int c = __shfl_sync(0xffffffffu, cl, src);
                 vv[u] = __shfl_sync(0xffffffffu, vl, src);
                 if (e + u >= cnt) vv[u] = 0.0;
-                const double* xr = X + static_cast<long long>(c) * ldx + c0;
+                const double* xr = X + static_cast<long long>(c) * ldx + c0 + lane;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const long long j = lane + 32 * q;
-                    xv[u][q] = (c0 + j < w) ? __ldg(xr + j) : 0.0;
-                }
+                for (int q = 0; q < Q; ++q) xv[u][q] = colok[q] ? __ldg(xr + 32 * q) : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < U; ++u)
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc[q] = fma(vv[u], xv[u][q], acc[q]);
+                for (int q = 0; q < Q; ++q) acc[q] = fma(vv[u], xv[u][q], acc[q]);
         }
     }
     const int slot = plan.seg_slot[sg];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < Q; ++q) {
         const long long j = c0 + lane + 32 * q;
-        if (j >= w) continue;
+        if (!colok[q]) continue;
         if (slot < 0)
             out[static_cast<long long>(plan.seg_row[sg]) * ldo + j] = acc[q];
         else
@@ -337,8 +344,19 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
                 break;
         }
     } else {
-        dim3 grid(static_cast<unsigned>((plan.nseg + 3) / 4), static_cast<unsigned>((w + 127) / 128));
-        spmm_wide_kernel<<<grid, 128, 0, ctx->stream>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+        const unsigned nb = static_cast<unsigned>((plan.nseg + 3) / 4);
+        if (w <= 32)
+            spmm_wide_kernel<1, 16><<<dim3(nb, 1), 128, 0, ctx->stream>>>(plan, idx, val, X, ldx, w, out, ldo,
+                                                                          partial);
+        else if (w <= 64)
+            spmm_wide_kernel<2, 8><<<dim3(nb, 1), 128, 0, ctx->stream>>>(plan, idx, val, X, ldx, w, out, ldo,
+                                                                         partial);
+        else if (w <= 96)
+            spmm_wide_kernel<3, 5><<<dim3(nb, 1), 128, 0, ctx->stream>>>(plan, idx, val, X, ldx, w, out, ldo,
+                                                                         partial);
+        else
+            spmm_wide_kernel<4, 4><<<dim3(nb, static_cast<unsigned>((w + 127) / 128)), 128, 0, ctx->stream>>>(
+                plan, idx, val, X, ldx, w, out, ldo, partial);
     }
     if (plan.nlong > 0) {
         if (w >= 8 && w <= 512) {
