@@ -106,6 +106,7 @@ int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, sv
         auto c = std::make_unique<svt_ctx>();
         c->device = device;
         SVT_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        SVT_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
         SVT_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
         SVT_CUDA(cudaMallocHost(&c->h_scalars, 64 * sizeof(double)));
         SVT_CUDA(cudaMallocHost(&c->h_flags, 64 * sizeof(int)));
@@ -133,6 +134,7 @@ int svt_ctx_destroy(svt_ctx* ctx) {
         if (!ctx) return;
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->stream);
+        if (ctx->side) cudaStreamSynchronize(ctx->side);
         for (auto& p : ctx->pending) {
             cudaEventDestroy(p.a);
             cudaEventDestroy(p.b);
@@ -142,6 +144,7 @@ int svt_ctx_destroy(svt_ctx* ctx) {
         ctx->ws_partial.release();
         ctx->ws_partial2.release();
         ctx->ws_rng.release();
+        ctx->ws_rng_side.release();
         ctx->ws_mt.release();
         ctx->ws_eig.release();
         ctx->ws_info.release();
@@ -150,6 +153,7 @@ int svt_ctx_destroy(svt_ctx* ctx) {
         cudaFreeHost(ctx->h_scalars);
         cudaFreeHost(ctx->h_flags);
         cudaStreamDestroy(ctx->stream);
+        if (ctx->side) cudaStreamDestroy(ctx->side);
         delete ctx;
     });
 }

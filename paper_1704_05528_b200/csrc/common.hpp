@@ -160,6 +160,7 @@ void nccl_init(Comm& c, int rank, int world, const void* id128);
 struct svt_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // side stream: Omega prefetch for the next round batch
     int num_sms = 148;
     svtb::Comm comm;
     void* cusolver = nullptr;  // cusolverDnHandle_t
@@ -180,6 +181,7 @@ struct svt_ctx {
     struct Pending {
         cudaEvent_t a, b;
         int cls;
+        bool side;
     };
     std::vector<Pending> pending;
     std::vector<cudaEvent_t> event_pool;
@@ -193,6 +195,7 @@ struct svt_ctx {
     svtb::DevBuf<double> ws_spmm;      // long-row partials of the segmented SpMM
     svtb::DevBuf<unsigned> ws_counters;  // last-CTA-reduces counters (self-resetting)
     svtb::DevBuf<unsigned long long> ws_rng;  // raw mt19937_64 draws
+    svtb::DevBuf<unsigned long long> ws_rng_side;  // raw draws of the side-stream prefetch
     svtb::DevBuf<unsigned long long> ws_mt;   // persistent mt state (312 words + index)
     svtb::DevBuf<double> ws_eig;              // Jacobi eigensolver workspace
     svtb::DevBuf<int> ws_info;
@@ -206,7 +209,8 @@ struct LaunchScope {
     svt_ctx* ctx;
     int cls;
     cudaEvent_t a = nullptr, b = nullptr;
-    LaunchScope(svt_ctx* c, int k, double bytes, double flops);
+    cudaStream_t st = nullptr;
+    LaunchScope(svt_ctx* c, int k, double bytes, double flops, cudaStream_t stream = nullptr);
     ~LaunchScope() noexcept(false);
 };
 // Blocking wait for the context stream (counted; timed when profiling).

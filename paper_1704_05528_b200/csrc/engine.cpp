@@ -657,12 +657,51 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
     const i64 w = p.dt, W = K * w, m = A->m_local, n = A->n, r0 = st.rank;
     ensure_cap(E, st, r0 + W);
     u64 seeds[kMaxOmegaBatch];
-    for (int k = 0; k < K; ++k) seeds[k] = derive_seed_u(p.seed, static_cast<u64>(round0 + k));
-    E.OmW.ensure(static_cast<size_t>(n * W));
     E.XW.ensure(static_cast<size_t>(std::max<i64>(1, m) * W));
     E.TW.ensure(static_cast<size_t>(n * W));
-    gaussian_blocks_dev(c, n, w, seeds, K, E.OmW.get(), w, W);
-    sp_mult(E, W, E.OmW.get(), W, E.XW.get(), W);
+    auto& pre = E.pre;
+    i64 ldom = W;
+    if (pre.valid && pre.seed == p.seed && pre.round0 == round0 && pre.K >= K && c->side) {
+        // this batch's Omega was generated on the side stream during the
+        // previous batch
+        SVT_CUDA(cudaStreamWaitEvent(c->stream, pre.ready, 0));
+        std::swap(E.OmW, pre.buf);
+        ldom = pre.ld;
+    } else {
+        for (int k = 0; k < K; ++k) seeds[k] = derive_seed_u(p.seed, static_cast<u64>(round0 + k));
+        E.OmW.ensure(static_cast<size_t>(n * W));
+        gaussian_blocks_dev(c, n, w, seeds, K, E.OmW.get(), w, W);
+    }
+    pre.valid = false;
+    sp_mult(E, W, E.OmW.get(), ldom, E.XW.get(), W);
+    // prefetch the next batch's Omega (rounds round0 + K ..) on the side
+    // stream; it overlaps the rest of this batch.  The buffer it writes was
+    // last read by the previous batch's first product, which precedes this
+    // point on the main stream.
+    const i64 room = (st.min_dim - (r0 + W)) / w;
+    const int Kn = static_cast<int>(std::min<i64>(std::min<i64>(kMaxOmegaBatch, 128 / w), room));
+    static const bool no_prefetch = std::getenv("SVTB_NO_PREFETCH") != nullptr;
+    if (c->side && Kn >= 2 && !no_prefetch) {
+        if (!pre.ready) {
+            SVT_CUDA(cudaEventCreateWithFlags(&pre.ready, cudaEventDisableTiming));
+            SVT_CUDA(cudaEventCreateWithFlags(&pre.consumed, cudaEventDisableTiming));
+        }
+        const i64 Wn = static_cast<i64>(Kn) * w;
+        SVT_CUDA(cudaEventRecord(pre.consumed, c->stream));
+        SVT_CUDA(cudaStreamWaitEvent(c->side, pre.consumed, 0));
+        if (pre.buf.n < static_cast<size_t>(n * Wn)) {
+            SVT_CUDA(cudaStreamSynchronize(c->side));
+            pre.buf.ensure(static_cast<size_t>(n * Wn));
+        }
+        for (int k = 0; k < Kn; ++k) seeds[k] = derive_seed_u(p.seed, static_cast<u64>(round0 + K + k));
+        gaussian_blocks_dev(c, n, w, seeds, Kn, pre.buf.get(), w, Wn, true);
+        SVT_CUDA(cudaEventRecord(pre.ready, c->side));
+        pre.valid = true;
+        pre.seed = p.seed;
+        pre.round0 = round0 + K;
+        pre.K = Kn;
+        pre.ld = Wn;
+    }
     for (int j = 0; j < p.np; ++j) {  // np == 1 here (np >= 2 rounds run one by one)
         sp_mult_t(E, W, E.XW.get(), W, E.TW.get());
         sp_mult(E, W, E.TW.get(), W, E.XW.get(), W);

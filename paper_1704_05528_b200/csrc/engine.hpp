@@ -77,11 +77,31 @@ struct Engine {
     DevBuf<double> Om, OmBank, X, X2, P, T, C, D, G, Rinv, hh, tmp, W, lam, Vraw, Wk;
     DevBuf<double> fkZ, fkZq, fkZt, fkWn, fkH, fkYh, fkth, fkZY, fkXr, fkres;  // finalize_kept
     DevBuf<double> OmW, XW, TW, CW, GW, RW, eW;  // speculative round batches
+    // Omega of the next batch, generated on ctx->side while the current
+    // batch runs (its rounds' seeds do not depend on the data)
+    struct OmegaPrefetch {
+        DevBuf<double> buf;
+        bool valid = false;
+        u64 seed = 0;
+        int round0 = 0, K = 0;
+        i64 ld = 0;
+        cudaEvent_t ready = nullptr, consumed = nullptr;
+    } pre;
     DevBuf<int> perm;
     QBDev qb;  // persistent QB storage: capacity survives across SVT iterations
     bool batching = true;  // speculative multi-round batches (exact-arithmetic equivalent)
     int last_rounds = -1;  // rounds of the previous sketch (batch-size predictor)
     Engine(svt_ctx* c, svt_mat* m, Vals y) : ctx(c), mat(m), Y(y), batching(c->batching != 0) {}
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+    Engine(Engine&&) = delete;
+    ~Engine() {
+        if (pre.ready || pre.consumed) {
+            if (ctx && ctx->side) cudaStreamSynchronize(ctx->side);
+            if (pre.ready) cudaEventDestroy(pre.ready);
+            if (pre.consumed) cudaEventDestroy(pre.consumed);
+        }
+    }
 };
 
 // primitives

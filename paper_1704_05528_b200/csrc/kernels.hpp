@@ -16,8 +16,10 @@ void gaussian_block_dev(svt_ctx* ctx, i64 rows, i64 cols, u64 seed, double* out,
 // K <= kMaxOmegaBatch independent blocks in two launches (one warp per
 // stream): block k from std::mt19937_64(seeds[k]) into out + k * out_stride.
 constexpr int kMaxOmegaBatch = 32;
+// on_side: run on ctx->side with its own scratch (the caller orders it
+// against the main stream with events).
 void gaussian_blocks_dev(svt_ctx* ctx, i64 rows, i64 cols, const u64* seeds, int K, double* out, i64 out_stride,
-                         i64 ld);
+                         i64 ld, bool on_side = false);
 
 // ---- sparse (sampled.hpp) ---------------------------------------------------
 // out[i, 0:w] = sum_{k in ptr[i]..ptr[i+1]} val[k] * X[idx[k], 0:w], i < nrows.

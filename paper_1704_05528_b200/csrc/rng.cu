@@ -197,7 +197,9 @@ __global__ void box_muller_multi_kernel(const unsigned long long* __restrict__ d
 }  // namespace
 
 void gaussian_blocks_dev(svt_ctx* ctx, i64 rows, i64 cols, const u64* seeds, int K, double* out, i64 out_stride,
-                         i64 ld) {
+                         i64 ld, bool on_side) {
+    cudaStream_t stream = on_side ? ctx->side : ctx->stream;
+    DevBuf<unsigned long long>& scratch = on_side ? ctx->ws_rng_side : ctx->ws_rng;
     if (rows < 1 || cols < 1) throw std::invalid_argument("gaussian_block: dimensions must be >= 1");
     if (K < 1) return;
     if (K > kMaxOmegaBatch) throw std::invalid_argument("gaussian_blocks_dev: too many streams");
@@ -205,16 +207,16 @@ void gaussian_blocks_dev(svt_ctx* ctx, i64 rows, i64 cols, const u64* seeds, int
     const i64 pairs = (total + 1) / 2;
     const i64 twists = (2 * pairs + MT_N - 1) / MT_N;
     const i64 draw_stride = twists * MT_N;
-    ctx->ws_rng.ensure(static_cast<size_t>(draw_stride * K));
+    scratch.ensure(static_cast<size_t>(draw_stride * K));
     SeedPack pack{};
     for (int k = 0; k < K; ++k) pack.s[k] = seeds[k];
     {
-        LaunchScope ls(ctx, K_RNG, 8.0 * draw_stride * K, 0.0);
-        mt_twist_multi_kernel<<<K, 32, 0, ctx->stream>>>(pack, twists, ctx->ws_rng.get(), draw_stride);
+        LaunchScope ls(ctx, K_RNG, 8.0 * draw_stride * K, 0.0, stream);
+        mt_twist_multi_kernel<<<K, 32, 0, stream>>>(pack, twists, scratch.get(), draw_stride);
     }
-    LaunchScope ls(ctx, K_RNG, 32.0 * pairs * K, 0.0);
+    LaunchScope ls(ctx, K_RNG, 32.0 * pairs * K, 0.0, stream);
     dim3 grid(static_cast<unsigned>((pairs + 255) / 256), static_cast<unsigned>(K));
-    box_muller_multi_kernel<<<grid, 256, 0, ctx->stream>>>(ctx->ws_rng.get(), draw_stride, pairs, rows, total, out,
+    box_muller_multi_kernel<<<grid, 256, 0, stream>>>(scratch.get(), draw_stride, pairs, rows, total, out,
                                                            out_stride, ld);
 }
 

@@ -10,7 +10,8 @@
 
 namespace svtb {
 
-LaunchScope::LaunchScope(svt_ctx* c, int k, double bytes, double flops) : ctx(c), cls(k) {
+LaunchScope::LaunchScope(svt_ctx* c, int k, double bytes, double flops, cudaStream_t stream)
+    : ctx(c), cls(k), st(stream ? stream : c->stream) {
     ctx->launch_count++;
     if (ctx->gap_open) {
         auto& g = ctx->gap_stats[ctx->gap_site];
@@ -34,15 +35,15 @@ LaunchScope::LaunchScope(svt_ctx* c, int k, double bytes, double flops) : ctx(c)
         ctx->event_pool.pop_back();
         b = ctx->event_pool.back();
         ctx->event_pool.pop_back();
-        SVT_CUDA(cudaEventRecord(a, ctx->stream));
+        SVT_CUDA(cudaEventRecord(a, st));
     }
 }
 
 LaunchScope::~LaunchScope() noexcept(false) {
     cudaError_t e = cudaGetLastError();
     if (a != nullptr) {
-        cudaEventRecord(b, ctx->stream);
-        ctx->pending.push_back({a, b, cls});
+        cudaEventRecord(b, st);
+        ctx->pending.push_back({a, b, cls, st != ctx->stream});
         if (ctx->pending.size() > 4096) flush_stats(ctx);
     }
     if (e != cudaSuccess && std::uncaught_exceptions() == 0)
@@ -78,6 +79,7 @@ void print_gap_stats(svt_ctx* c) {
 void flush_stats(svt_ctx* ctx) {
     if (ctx->pending.empty()) return;
     SVT_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->side) SVT_CUDA(cudaStreamSynchronize(ctx->side));
     for (auto& p : ctx->pending) {
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) ctx->stats[p.cls].total_ms += ms;
