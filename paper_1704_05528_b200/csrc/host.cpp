@@ -8,6 +8,7 @@
 // reference's row order).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <numeric>
 #include <string>
 
@@ -122,6 +123,50 @@ void build_plan(const std::vector<i64>& ptr, i64 nrows, cudaStream_t s, SegPlan&
 
 using svtb::i64;
 
+// Upload only the CSR arrays; validation, the CSC view, csr2csc and the
+// segment plans are built on the device (build.cu).
+static svt_mat* upload_device_build(svt_ctx* ctx, i64 m, i64 n, i64 row_begin, i64 row_end,
+                                    const std::vector<i64>& rp, const i64* col, const double* val, i64 nnz) {
+    const i64 ml = row_end - row_begin;
+    auto* M = new svt_mat();
+    try {
+        M->ctx = ctx;
+        M->m = m;
+        M->n = n;
+        M->row_begin = row_begin;
+        M->row_end = row_end;
+        M->m_local = ml;
+        M->nnz_local = nnz;
+        M->rowptr.alloc(static_cast<size_t>(ml + 1));
+        M->col.alloc(static_cast<size_t>(std::max<i64>(1, nnz)));
+        M->val.alloc(static_cast<size_t>(std::max<i64>(1, nnz)));
+        M->colptr.alloc(static_cast<size_t>(n + 1));
+        M->cscrow.alloc(static_cast<size_t>(std::max<i64>(1, nnz)));
+        M->val_csc.alloc(static_cast<size_t>(std::max<i64>(1, nnz)));
+        M->csr2csc.alloc(static_cast<size_t>(std::max<i64>(1, nnz)));
+        svtb::DevBuf<i64> col64(static_cast<size_t>(std::max<i64>(1, nnz)));
+        cudaStream_t s = ctx->stream;
+        SVT_CUDA(cudaMemcpyAsync(M->rowptr.get(), rp.data(), sizeof(i64) * (ml + 1), cudaMemcpyHostToDevice, s));
+        if (nnz > 0) {
+            SVT_CUDA(cudaMemcpyAsync(col64.get(), col, sizeof(i64) * nnz, cudaMemcpyHostToDevice, s));
+            SVT_CUDA(cudaMemcpyAsync(M->val.get(), val, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+        }
+        const int code = svtb::build_sampled_device(ctx, M, reinterpret_cast<const long long*>(col64.get()));
+        if (code & 1) throw std::invalid_argument("svt_matrix_upload: column out of range");
+        if (code & 2) throw std::invalid_argument("svt_matrix_upload: non-finite value");
+        double g = static_cast<double>(nnz);
+        SVT_CUDA(cudaMemcpyAsync(ctx->d_scalars + 63, &g, sizeof(double), cudaMemcpyHostToDevice, s));
+        ctx->comm.allreduce_sum(ctx->d_scalars + 63, 1, s);
+        SVT_CUDA(cudaMemcpyAsync(&g, ctx->d_scalars + 63, sizeof(double), cudaMemcpyDeviceToHost, s));
+        svtb::sync_stream(ctx);
+        M->nnz_global = static_cast<i64>(g + 0.5);
+    } catch (...) {
+        delete M;
+        throw;
+    }
+    return M;
+}
+
 svt_mat* svtb_matrix_upload(svt_ctx* ctx, i64 m, i64 n, i64 row_begin, i64 row_end, const i64* rowptr,
                             const i64* col, const double* val) {
     if (m < 1 || n < 1) throw std::invalid_argument("svt_matrix_upload: dimensions must be >= 1");
@@ -138,6 +183,8 @@ svt_mat* svtb_matrix_upload(svt_ctx* ctx, i64 m, i64 n, i64 row_begin, i64 row_e
         if (i > 0 && rp[static_cast<size_t>(i)] < rp[static_cast<size_t>(i - 1)])
             throw std::invalid_argument("svt_matrix_upload: rowptr not monotone");
     }
+    if (!std::getenv("SVTB_HOST_BUILD")) return upload_device_build(ctx, m, n, row_begin, row_end, rp, col + base,
+                                                                    val + base, nnz);
     std::vector<int> ci(static_cast<size_t>(nnz));
     for (i64 k = 0; k < nnz; ++k) {
         const i64 c = col[base + k];

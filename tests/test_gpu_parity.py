@@ -458,3 +458,56 @@ def test_dev_gemm_matches_fp64_reference(shape):
     scale = (a.abs().T if ta else a.abs()) @ b.abs()
     err = ((c - ref).abs() / (0.5 * scale + 0.75 * c0.abs() + 1e-300)).max().item()
     assert err <= 1e-13 * max(1.0, np.sqrt(K) / 10), err
+
+
+# ---- device-side sample-set construction (csrc/build.cu) ----------------------
+def _skewed_csr(seed):
+    """Rows and columns longer than one 512-entry segment, empty rows and
+    columns, and short rows: every branch of the segment plans."""
+    rng = np.random.default_rng(seed)
+    m, n = 1200, 2500
+    rows, cols = [], []
+    for i in range(m):
+        if i % 97 == 5:
+            deg = 1700
+        elif i % 13 == 0:
+            deg = 0
+        else:
+            deg = int(rng.integers(1, 40))
+        c = rng.choice(n - 3, size=deg, replace=False)  # the last 3 columns stay empty
+        c = np.concatenate([c, [7]]) if (i % 2 == 0 and deg and 7 not in c) else c
+        rows += [i] * len(c)
+        cols += list(c)
+    vals = rng.standard_normal(len(rows))
+    rp, co, va = G.build_csr(m, n, rows, cols, vals)
+    return m, n, rp, co, va
+
+
+@pytest.mark.parametrize("seed", [81, 82])
+def test_device_build_matches_host_build(seed, monkeypatch):
+    m, n, rp, co, va = _skewed_csr(seed)
+    assert np.bincount(co, minlength=n)[7] > 512 and np.diff(rp).max() > 512
+    dev = G.SampledMatrix.from_csr(m, n, rp, co, va)
+    monkeypatch.setenv("SVTB_HOST_BUILD", "1")
+    host = G.SampledMatrix.from_csr(m, n, rp, co, va)
+    monkeypatch.delenv("SVTB_HOST_BUILD")
+    rng = np.random.default_rng(seed)
+    for w in (1, 10, 40, 120):
+        X = rng.standard_normal((n, w))
+        Xt = rng.standard_normal((m, w))
+        assert np.array_equal(G.sp_mult(dev, X), G.sp_mult(host, X))
+        assert np.array_equal(G.sp_mult_t(dev, Xt), G.sp_mult_t(host, Xt))
+    S = O.Csr(m, n, rp, co, va)
+    np.testing.assert_allclose(G.sp_mult_t(dev, Xt), O.sp_mult_t(S, Xt), rtol=1e-12, atol=1e-12)
+    p = params(10, 10, 1, 0.2, seed)
+    a, b = G.r3svd(dev, p), G.r3svd(host, p)
+    assert a.rank == b.rank and np.array_equal(a.sigma, b.sigma)
+
+
+def test_device_build_validates():
+    with pytest.raises(InvalidArgument):
+        G.SampledMatrix.from_csr(2, 3, [0, 1, 2], [0, 3], [1.0, 2.0])
+    with pytest.raises(InvalidArgument):
+        G.SampledMatrix.from_csr(2, 3, [0, 1, 2], [0, 1], [1.0, np.nan])
+    with pytest.raises(InvalidArgument):
+        G.SampledMatrix.from_csr(2, 3, [0, 2, 1], [0, 1], [1.0, 2.0])
