@@ -111,17 +111,39 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN)) gemm_kernel(
     }
 }
 
-__global__ void gemm_reduce_kernel(long long M, long long N, int splits, const double* __restrict__ partial,
-                                   double alpha, double beta, double* __restrict__ C, long long ldc,
-                                   const int* __restrict__ pred) {
+// Split-K partial sums -> C.  A CTA owns 32 consecutive output elements;
+// warp q adds splits q, q + 8, ... (lanes = elements, coalesced), then the 8
+// warp sums are added in warp order: fixed order, deterministic.
+constexpr int kRedWarps = 8;
+__global__ void __launch_bounds__(32 * kRedWarps) gemm_reduce_kernel(long long M, long long N, int splits,
+                                                                   const double* __restrict__ partial,
+                                                                   double alpha, double beta,
+                                                                   double* __restrict__ C, long long ldc,
+                                                                   const int* __restrict__ pred) {
     if (pred != nullptr && *pred == 0) return;
-    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
-    if (e >= M * N) return;
-    const long long i = e / N, j = e % N;
-    double s = 0.0;
-    for (int z = 0; z < splits; ++z) s += partial[static_cast<long long>(z) * M * N + e];
-    const double c = (beta != 0.0) ? beta * C[i * ldc + j] : 0.0;
-    C[i * ldc + j] = fma(alpha, s, c);
+    __shared__ double red[kRedWarps][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long e = blockIdx.x * 32LL + lane;
+    const long long tot = M * N;
+    double s0 = 0.0, s1 = 0.0;
+    if (e < tot) {
+        int z = warp;
+        for (; z + kRedWarps < splits; z += 2 * kRedWarps) {
+            s0 += partial[static_cast<long long>(z) * tot + e];
+            s1 += partial[static_cast<long long>(z + kRedWarps) * tot + e];
+        }
+        if (z < splits) s0 += partial[static_cast<long long>(z) * tot + e];
+    }
+    red[warp][lane] = s0 + s1;
+    __syncthreads();
+    if (warp == 0 && e < tot) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < kRedWarps; ++q) t += red[q][lane];
+        const long long i = e / N, j = e % N;
+        const double c = (beta != 0.0) ? beta * C[i * ldc + j] : 0.0;
+        C[i * ldc + j] = fma(alpha, t, c);
+    }
 }
 
 __global__ void scale2d_kernel(double* C, long long M, long long N, long long ldc, double beta, const int* pred) {
@@ -487,7 +509,7 @@ void dmma_launch(svt_ctx* ctx, bool transA, i64 M, i64 N, i64 K, double alpha, c
                                                                    kchunk, ctx->ws_partial.get(), pred);
     if (splits > 1) {
         const i64 tot = M * N;
-        gemm_reduce_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(
+        gemm_reduce_kernel<<<static_cast<unsigned>((tot + 31) / 32), 32 * kRedWarps, 0, ctx->stream>>>(
             M, N, static_cast<int>(splits), ctx->ws_partial.get(), alpha, beta, C, ldc, pred);
     }
 }
@@ -520,7 +542,7 @@ void gemm_launch(svt_ctx* ctx, bool transA, i64 M, i64 N, i64 K, double alpha, c
             M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, ctx->ws_partial.get(), pred);
     if (splits > 1) {
         const i64 tot = M * N;
-        gemm_reduce_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(
+        gemm_reduce_kernel<<<static_cast<unsigned>((tot + 31) / 32), 32 * kRedWarps, 0, ctx->stream>>>(
             M, N, static_cast<int>(splits), ctx->ws_partial.get(), alpha, beta, C, ldc, pred);
     }
 }
@@ -1607,15 +1629,25 @@ __global__ void col_sumsq_partial_kernel(const double* __restrict__ X, long long
     const long long j = blockIdx.x * 32LL + (threadIdx.x & 31);
     const int ty = threadIdx.x >> 5;  // 8 row lanes
     __shared__ double red[8][33];
-    double s = 0.0;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
     const long long r0 = blockIdx.y * rows_per_block;
     const long long r1 = min(rows, r0 + rows_per_block);
-    if (j < cols)
-        for (long long i = r0 + ty; i < r1; i += 8) {
-            const double v = X[i * ld + j];
-            s = fma(v, v, s);
+    if (j < cols) {
+        long long i = r0 + ty;
+        for (; i + 24 < r1; i += 32) {  // four independent chains
+            const double a = X[i * ld + j], b = X[(i + 8) * ld + j];
+            const double c = X[(i + 16) * ld + j], d = X[(i + 24) * ld + j];
+            s0 = fma(a, a, s0);
+            s1 = fma(b, b, s1);
+            s2 = fma(c, c, s2);
+            s3 = fma(d, d, s3);
         }
-    red[ty][threadIdx.x & 31] = s;
+        for (; i < r1; i += 8) {
+            const double v = X[i * ld + j];
+            s0 = fma(v, v, s0);
+        }
+    }
+    red[ty][threadIdx.x & 31] = (s0 + s1) + (s2 + s3);
     __syncthreads();
     if (ty == 0 && j < cols) {
         double t = 0.0;
@@ -1857,7 +1889,10 @@ void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
 
 void col_sumsq(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double* out) {
     if (cols <= 0) return;
-    const i64 rpb = std::max<i64>(256, (rows + 63) / 64);
+    // ~4 CTAs per SM in total over the column blocks x row parts
+    const i64 xblk = (cols + 31) / 32;
+    const i64 parts_want = std::max<i64>(1, (4 * ctx->num_sms + xblk - 1) / xblk);
+    const i64 rpb = std::max<i64>(64, (rows + parts_want - 1) / parts_want);
     const i64 nparts = std::max<i64>(1, (rows + rpb - 1) / rpb);
     ctx->ws_partial2.ensure(static_cast<size_t>(nparts * cols));
     LaunchScope ls(ctx, K_OTHER, 8.0 * rows * cols, 2.0 * rows * cols);

@@ -748,6 +748,11 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
             sync_stream(c);
             for (int k = 0; k < K && !second; ++k)
                 second = std::sqrt(block_sum(W, k)) > 1e-8 * std::sqrt(block_sum(0, k));
+            if (std::getenv("SVTB_DEBUG_BATCH"))
+                for (int k = 0; k < K; ++k)
+                    std::fprintf(stderr, "[orth] r0=%lld k=%d |X1|/|X|=%.3e |QtX1|/|X1|=%.3e\n",
+                                 static_cast<long long>(r0), k, std::sqrt(block_sum(0, k) / block_sum(2 * W, k)),
+                                 std::sqrt(block_sum(W, k) / block_sum(0, k)));
         }
         if (second) gemm(c, K_GEMM, false, m, W, r0, -1.0, Q, ldq, E.CW.get(), W, 1.0, E.XW.get(), W);
         if (std::getenv("SVTB_DEBUG_BATCH"))
