@@ -96,11 +96,11 @@ struct DevBuf {
                          count * sizeof(T) / 1e6, count, sizeof(T));
         n = count;
     }
-    // grow-only, with 1.5x slack once allocated (workspaces sized by the
-    // basis rank grow a little every SVT iteration, and cudaFree stalls the
-    // device); contents are not preserved
+    // grow-only, doubling once allocated (workspaces sized by the basis rank
+    // grow a little every SVT iteration, and cudaFree stalls the device, so
+    // regrowth must stay logarithmic); contents are not preserved
     void ensure(size_t count) {
-        if (count > n) alloc(n ? std::max(count, n + n / 2) : count);
+        if (count > n) alloc(n ? std::max(count, 2 * n) : count);
     }
     void release() {
         if (p) {

@@ -164,6 +164,13 @@ __global__ void scale2d_kernel(double* C, long long M, long long N, long long ld
 // t = lane % 4.  Shared rows are padded to a stride of 4 mod 16 doubles so
 // the 4 k-rows x 8 m-columns of a fragment load hit distinct bank pairs.
 // ---------------------------------------------------------------------------
+// Split-K partial buffer: sized once for the largest split the launchers
+// allow (32M doubles), so it never regrows (a cudaFree inside an SVT step
+// would stall the device mid-iteration).
+inline void ensure_partial(svt_ctx* ctx, size_t need) {
+    if (need > ctx->ws_partial.n) ctx->ws_partial.ensure(std::max<size_t>(need, size_t(32) << 20));
+}
+
 constexpr int kDmmaBM = 64;
 constexpr int kDmmaBK = 16;
 
@@ -493,7 +500,7 @@ void dmma_launch(svt_ctx* ctx, bool transA, i64 M, i64 N, i64 K, double alpha, c
     i64 kchunk = (K + splits - 1) / splits;
     kchunk = ((kchunk + kDmmaBK - 1) / kDmmaBK) * kDmmaBK;  // multiple of both 16 and 8
     splits = std::max<i64>(1, (K + kchunk - 1) / kchunk);
-    if (splits > 1) ctx->ws_partial.ensure(static_cast<size_t>(splits * M * N));
+    if (splits > 1) ensure_partial(ctx, static_cast<size_t>(splits * M * N));
     dim3 grid(static_cast<unsigned>(mt), static_cast<unsigned>(nt), static_cast<unsigned>(splits));
     if (cp && transA)
         dmma_cp_kernel<BN, true><<<grid, 256, CpTile<BN, true>::SMEM, ctx->stream>>>(
@@ -531,7 +538,7 @@ void gemm_launch(svt_ctx* ctx, bool transA, i64 M, i64 N, i64 K, double alpha, c
     kchunk = ((kchunk + BK - 1) / BK) * BK;
     splits = (K + kchunk - 1) / kchunk;
     if (splits < 1) splits = 1;
-    if (splits > 1) ctx->ws_partial.ensure(static_cast<size_t>(splits * M * N));
+    if (splits > 1) ensure_partial(ctx, static_cast<size_t>(splits * M * N));
     dim3 grid(static_cast<unsigned>(mt), static_cast<unsigned>(nt), static_cast<unsigned>(splits));
     constexpr int NT = (BM / TM) * (BN / TN);
     if (transA)
@@ -1014,7 +1021,7 @@ void skinny_tn_launch(svt_ctx* ctx, i64 M, i64 K, double alpha, const double* A,
     rpc = ((rpc + kTnWarps * kTnRows - 1) / (kTnWarps * kTnRows)) * (kTnWarps * kTnRows);
     splits = std::max<i64>(1, (K + rpc - 1) / rpc);
     unsigned* cnt = counters(ctx);
-    if (splits > 1) ctx->ws_partial.ensure(static_cast<size_t>(splits * M * N));
+    if (splits > 1) ensure_partial(ctx, static_cast<size_t>(splits * M * N));
     dim3 grid(static_cast<unsigned>(groups), static_cast<unsigned>(splits));
     skinny_tn_kernel<N><<<grid, 32 * kTnWarps, 0, ctx->stream>>>(M, K, A, lda, B, ldb, alpha, beta, C, ldc, rpc,
                                                                  ctx->ws_partial.get(), cnt, pred);
@@ -1193,9 +1200,34 @@ __global__ void __launch_bounds__(512) chol_rinv_kernel(const double* __restrict
     __shared__ int fail;
     const int ld = w + 1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ double wmax[16];
     if (tid == 0) fail = 0;
-    for (int e = tid; e < w * w; e += blockDim.x) L[(e / w) * ld + e % w] = G[e];
+    double emax = 0.0;
+    for (int e = tid; e < w * w; e += blockDim.x) {
+        const double g = G[e];
+        L[(e / w) * ld + e % w] = g;
+        const double d = fabs(g - ((e / w == e % w) ? 1.0 : 0.0));
+        emax = (d > emax || d != d) ? d : emax;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) emax = fmax(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    if (lane == 0) wmax[warp] = emax;
     __syncthreads();
+    emax = 0.0;
+    for (int q = 0; q < static_cast<int>(blockDim.x >> 5); ++q) emax = fmax(emax, wmax[q]);
+    // Second CholQR pass: G = I + E with E at rounding level (measured
+    // max|E| ~ 1e-13 at W = 120).  Then R = I + triu(E, 1) + diag(E) / 2 +
+    // O(E^2) and R^{-1} = I - triu(E, 1) - diag(E) / 2 + O(E^2): with
+    // max|E| <= 1e-8 / w the O(E^2) term is below 1e-16, so the factor is
+    // written directly (upper triangular: the nested spans are unchanged).
+    if (emax <= 1e-8 / static_cast<double>(w)) {
+        for (int e = tid; e < w * w; e += blockDim.x) {
+            const int r = e / w, c = e % w;
+            const double g = L[r * ld + c];
+            Rinv[e] = (r < c) ? -g : (r == c ? 1.0 - 0.5 * (g - 1.0) : 0.0);
+        }
+        return;
+    }
     if (tid < w) dorig[tid] = L[tid * ld + tid];
     __syncthreads();
     // ---- Cholesky --------------------------------------------------------
@@ -1420,7 +1452,8 @@ __global__ void __launch_bounds__(kHhThreads) householder_kernel(const double* _
 constexpr int kJacMax = 48;
 
 __global__ void __launch_bounds__(1024) jacobi_eig_kernel(const double* __restrict__ G, int r,
-                                                          double* __restrict__ W, double* __restrict__ lambda) {
+                                                          double* __restrict__ W, double* __restrict__ lambda,
+                                                          int dbg) {
     __shared__ double A[kJacMax][kJacMax + 1];  // column j = A[.][j]
     __shared__ double V[kJacMax][kJacMax + 1];
     __shared__ double nrm[kJacMax];
@@ -1428,6 +1461,9 @@ __global__ void __launch_bounds__(1024) jacobi_eig_kernel(const double* __restri
     __shared__ int rotated;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rp = (r + 1) & ~1;  // even, padded with a zero column
+    // rotation threshold just above the rounding floor of the computed
+    // column dot products (~sqrt(r) eps): a tighter one only burns sweeps
+    const double jtol = 8.0 * sqrt(static_cast<double>(rp)) * 1.1102230246251565e-16;
     for (int e = tid; e < kJacMax * kJacMax; e += blockDim.x) {
         const int i = e / kJacMax, j = e % kJacMax;
         A[i][j] = (i < r && j < r) ? G[i * r + j] : 0.0;
@@ -1457,7 +1493,7 @@ __global__ void __launch_bounds__(1024) jacobi_eig_kernel(const double* __restri
                 al = warp_sum(al);
                 be = warp_sum(be);
                 ga = warp_sum(ga);
-                if (ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
+                if (ga != 0.0 && fabs(ga) > jtol * sqrt(al * be)) {
                     const double zeta = (be - al) / (2.0 * ga);
                     const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                     const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
@@ -1474,8 +1510,12 @@ __global__ void __launch_bounds__(1024) jacobi_eig_kernel(const double* __restri
             }
             __syncthreads();
         }
-        if (!rotated) break;
+        if (!rotated) {
+            if (dbg && tid == 0) printf("[jacobi] r=%d sweeps=%d\n", r, sweep + 1);
+            break;
+        }
         __syncthreads();
+        if (dbg && tid == 0 && sweep == 39) printf("[jacobi] r=%d hit the sweep cap\n", r);
     }
     // eigenvalue j = +-||A[:, j]|| with the sign of v_j^T A_j (PSD: +)
     if (tid < r) {
@@ -1541,6 +1581,7 @@ __global__ void __launch_bounds__(256) jacobi_coop_kernel(double* __restrict__ A
     unsigned* count = sync;
     unsigned* gen = sync + 1;
     unsigned* rot = sync + 2;  // rot[0], rot[1]: rotations of the current / next sweep
+    const double jtol = 8.0 * sqrt(static_cast<double>(rp)) * 1.1102230246251565e-16;
     for (int sweep = 0; sweep < max_sweeps; ++sweep) {
         if (blockIdx.x == 0 && threadIdx.x == 0) rot[(sweep + 1) & 1] = 0u;
         for (int step = 0; step < rp - 1; ++step) {
@@ -1565,7 +1606,7 @@ __global__ void __launch_bounds__(256) jacobi_coop_kernel(double* __restrict__ A
                 al = warp_sum(al);
                 be = warp_sum(be);
                 ga = warp_sum(ga);
-                if (ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
+                if (ga != 0.0 && fabs(ga) > jtol * sqrt(al * be)) {
                     const double zeta = (be - al) / (2.0 * ga);
                     const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                     const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
@@ -1840,7 +1881,8 @@ void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
     if (r <= 0) return;
     if (r <= kJacMax) {
         LaunchScope ls(ctx, K_FINAL, 16.0 * r * r, 0.0);
-        jacobi_eig_kernel<<<1, 1024, 0, ctx->stream>>>(G, static_cast<int>(r), W, lambda);
+        static const int dbg = std::getenv("SVTB_DEBUG_JACOBI") ? 1 : 0;
+        jacobi_eig_kernel<<<1, 1024, 0, ctx->stream>>>(G, static_cast<int>(r), W, lambda, dbg);
         return;
     }
     // Larger Grams: cooperative multi-CTA one-sided Jacobi.

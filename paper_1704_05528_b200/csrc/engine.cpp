@@ -771,6 +771,10 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
     gemm(c, K_QR, false, m, W, W, 1.0, E.XW.get(), W, E.RW.get(), W, 0.0, E.X2.get(), W);
     gemm(c, K_QR, true, W, W, m, 1.0, E.X2.get(), W, E.X2.get(), W, 0.0, E.GW.get(), W);
     allreduce(c, E.GW.get(), static_cast<size_t>(W * W));
+    if (std::getenv("SVTB_DEBUG_G2")) {
+        maxabs(c, E.GW.get(), W, W, W, 1.0, dsc(c, S_TMP));
+        std::fprintf(stderr, "[g2] W=%lld max|G2-I|=%.3e\n", static_cast<long long>(W), read_scalar(c, S_TMP));
+    }
     chol_rinv(c, E.GW.get(), W, E.RW.get(), status, nullptr);
     gemm(c, K_QR, false, m, W, W, 1.0, E.X2.get(), W, E.RW.get(), W, 0.0, Q + r0, ldq);
     if (read_flag(c, F_QRSTAT) != 0) {
