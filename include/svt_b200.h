@@ -150,6 +150,16 @@ int svt_partition_rows(int64_t m, const int64_t* rowptr, int world, int64_t* bou
  * is subtracted).  col is 0-based global column index. */
 int svt_matrix_upload(svt_ctx* ctx, int64_t m, int64_t n, int64_t row_begin, int64_t row_end,
                       const int64_t* rowptr, const int64_t* col, const double* val, svt_mat** out);
+/* SampledMatrix(rows, cols, values) (sampled.hpp:27-62) built on the device:
+ * unsorted triplets are uploaded, validated (range, finiteness, duplicates;
+ * SVT_EINVAL with the reference's messages), radix-sorted by (row, col), and
+ * the rows [row_begin, row_end) kept as this rank's block. */
+int svt_matrix_from_triplets(svt_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                             const int64_t* cols, const double* vals, int64_t row_begin, int64_t row_end,
+                             svt_mat** out);
+/* The rank's local CSR back on the host: rowptr (m_local + 1, rebased),
+ * col (nnz_local, global column index), val (nnz_local). */
+int svt_matrix_csr(svt_mat* mat, int64_t* rowptr, int64_t* col, double* val);
 int svt_matrix_free(svt_mat* mat);
 int svt_matrix_info(svt_mat* mat, int64_t* m, int64_t* n, int64_t* nnz_local, int64_t* row_begin,
                     int64_t* row_end);

@@ -207,7 +207,8 @@ class SampledMatrix:
                  row_block=None):
         self.ctx = ctx or default_context()
         if _csr is None:
-            _csr = build_csr(m, n, rows, cols, vals)
+            self._from_triplets(m, n, rows, cols, vals, row_block)
+            return
         rp, co, va = _csr
         self.m, self.n = int(m), int(n)
         rb, re_ = (0, self.m) if row_block is None else (int(row_block[0]), int(row_block[1]))
@@ -224,6 +225,36 @@ class SampledMatrix:
                                        _ptr(self.col if self.col.size else np.zeros(1, np.int64), P_I64),
                                        _ptr(self._val if self._val.size else np.zeros(1)), C.byref(h)))
         self.h = h
+
+    def _from_triplets(self, m, n, rows, cols, vals, row_block):
+        """sampled.hpp:27-62 on the device (svt_matrix_from_triplets): sort,
+        validation and duplicate detection run in HBM; the local CSR is read
+        back for the host-side attributes."""
+        rows = np.ascontiguousarray(rows, dtype=np.int64).ravel()
+        cols = np.ascontiguousarray(cols, dtype=np.int64).ravel()
+        vals = np.ascontiguousarray(vals, dtype=np.float64).ravel()
+        if not (rows.size == cols.size == vals.size):
+            raise InvalidArgument("SampledMatrix: rows, cols and values differ in length")
+        self.m, self.n = int(m), int(n)
+        rb, re_ = (0, self.m) if row_block is None else (int(row_block[0]), int(row_block[1]))
+        h = C.c_void_p()
+        one = np.zeros(1, np.int64)
+        _check(lib().svt_matrix_from_triplets(
+            self.ctx.h, C.c_int64(self.m), C.c_int64(self.n), C.c_int64(rows.size),
+            _ptr(rows if rows.size else one, P_I64), _ptr(cols if cols.size else one, P_I64),
+            _ptr(vals if vals.size else np.zeros(1)), C.c_int64(rb), C.c_int64(re_), C.byref(h)))
+        self.h = h
+        self.row_begin, self.row_end = rb, re_
+        mm, nn, nl, b0, b1 = (C.c_int64() for _ in range(5))
+        _check(lib().svt_matrix_info(h, C.byref(mm), C.byref(nn), C.byref(nl), C.byref(b0), C.byref(b1)))
+        nnz_l = nl.value
+        self.rowptr = np.zeros(re_ - rb + 1, np.int64)
+        self.col = np.zeros(max(nnz_l, 1), np.int64)
+        self._val = np.zeros(max(nnz_l, 1))
+        _check(lib().svt_matrix_csr(h, _ptr(self.rowptr, P_I64), _ptr(self.col, P_I64), _ptr(self._val)))
+        self.col, self._val = self.col[:nnz_l], self._val[:nnz_l]
+        self.rowptr_global = np.concatenate([np.zeros(rb, np.int64), self.rowptr,
+                                             np.full(self.m - re_, self.rowptr[-1], np.int64)])
 
     @classmethod
     def from_csr(cls, m, n, rowptr, col, val, ctx=None, row_block=None):

@@ -105,6 +105,69 @@ __global__ void plan_fill_kernel(long long rows, const long long* __restrict__ p
     }
 }
 
+// ---- SampledMatrix from triplets (sampled.hpp:27-62) -------------------
+// keys = row * n + col; the first offending input index of each error kind
+// is recorded (atomicMin) so the host can name the entry like the reference.
+__global__ void triplet_keys_kernel(long long nnz, long long m, long long n, const long long* __restrict__ rows,
+                                    const long long* __restrict__ cols, const double* __restrict__ vals,
+                                    unsigned long long* __restrict__ keys, int* __restrict__ idx,
+                                    unsigned long long* __restrict__ first_bad) {
+    const long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (k >= nnz) return;
+    const long long r = rows[k], c = cols[k];
+    const bool ok = r >= 0 && r < m && c >= 0 && c < n;
+    if (!ok) atomicMin(first_bad, static_cast<unsigned long long>(k));
+    if (!isfinite(vals[k])) atomicMin(first_bad + 1, static_cast<unsigned long long>(k));
+    keys[k] = ok ? static_cast<unsigned long long>(r) * static_cast<unsigned long long>(n) +
+                       static_cast<unsigned long long>(c)
+                 : 0ULL;
+    idx[k] = static_cast<int>(k);
+}
+
+// adjacent equal sorted keys: the later entry (in sorted order) is a duplicate
+__global__ void duplicate_kernel(long long nnz, const unsigned long long* __restrict__ keys,
+                                 const int* __restrict__ perm, unsigned long long* __restrict__ first_dup) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p < 1 || p >= nnz) return;
+    if (keys[p] == keys[p - 1]) atomicMin(first_dup, static_cast<unsigned long long>(perm[p]));
+}
+
+__device__ __forceinline__ long long lower_bound_key(const unsigned long long* keys, long long nnz,
+                                                     unsigned long long v) {
+    long long lo = 0, hi = nnz;
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (keys[mid] < v)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// local CSR of rows [rb, rb + ml): rowptr (rebased), int64 columns, values
+__global__ void triplet_rowptr_kernel(long long ml, long long rb, long long n, long long nnz,
+                                      const unsigned long long* __restrict__ keys, long long* __restrict__ rowptr) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i > ml) return;
+    const long long lo = lower_bound_key(keys, nnz, static_cast<unsigned long long>(rb) * n);
+    rowptr[i] = lower_bound_key(keys, nnz, static_cast<unsigned long long>(rb + i) * n) - lo;
+}
+
+__global__ void lower_bound_one_kernel(const unsigned long long* __restrict__ keys, long long nnz,
+                                       unsigned long long v, long long* __restrict__ out) {
+    out[0] = lower_bound_key(keys, nnz, v);
+}
+
+__global__ void triplet_fill_kernel(long long cnt, long long lo, long long n, const unsigned long long* __restrict__ keys,
+                                    const int* __restrict__ perm, const double* __restrict__ vals,
+                                    long long* __restrict__ col64, double* __restrict__ val) {
+    const long long k = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (k >= cnt) return;
+    col64[k] = static_cast<long long>(keys[lo + k] % static_cast<unsigned long long>(n));
+    val[k] = vals[perm[lo + k]];
+}
+
 inline unsigned nb(long long n, int t = 256) { return static_cast<unsigned>((n + t - 1) / t); }
 
 // exclusive scan of n ints into out (n + 1 entries; out[n] = total)
@@ -215,6 +278,85 @@ int build_sampled_device(svt_ctx* ctx, svt_mat* M, const long long* col64) {
     build_plan_device(ctx, reinterpret_cast<const long long*>(M->colptr.get()), n, M->plan_csc);
     sync_stream(ctx);  // temporaries die here
     return 0;
+}
+
+// SampledMatrix from unsorted triplets, sorted and validated on the device
+// (radix sort of row * n + col; duplicates are adjacent keys).  Fills M's
+// local CSR for rows [row_begin, row_end) and the rest of the structure.
+// Throws std::invalid_argument with the reference's messages.
+void build_from_triplets_device(svt_ctx* ctx, svt_mat* M, i64 nnz, const i64* rows, const i64* cols,
+                                const double* vals) {
+    cudaStream_t s = ctx->stream;
+    const i64 m = M->m, n = M->n, rb = M->row_begin, ml = M->m_local;
+    DevBuf<long long> drow(static_cast<size_t>(nnz)), dcol(static_cast<size_t>(nnz));
+    DevBuf<double> dval(static_cast<size_t>(nnz));
+    DevBuf<unsigned long long> keys(static_cast<size_t>(nnz)), skeys(static_cast<size_t>(nnz));
+    DevBuf<int> idx(static_cast<size_t>(nnz)), perm(static_cast<size_t>(nnz));
+    DevBuf<unsigned long long> flags(4);
+    DevBuf<unsigned char> tmp;
+    SVT_CUDA(cudaMemcpyAsync(drow.get(), rows, sizeof(i64) * nnz, cudaMemcpyHostToDevice, s));
+    SVT_CUDA(cudaMemcpyAsync(dcol.get(), cols, sizeof(i64) * nnz, cudaMemcpyHostToDevice, s));
+    SVT_CUDA(cudaMemcpyAsync(dval.get(), vals, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+    SVT_CUDA(cudaMemsetAsync(flags.get(), 0xff, sizeof(unsigned long long) * 4, s));
+    {
+        LaunchScope ls(ctx, K_OTHER, 36.0 * nnz, 0.0);
+        triplet_keys_kernel<<<nb(nnz), 256, 0, s>>>(nnz, m, n, drow.get(), dcol.get(), dval.get(), keys.get(),
+                                                    idx.get(), flags.get());
+    }
+    unsigned long long hf[4];
+    SVT_CUDA(cudaMemcpyAsync(hf, flags.get(), sizeof(hf), cudaMemcpyDeviceToHost, s));
+    sync_stream(ctx);
+    auto entry = [&](unsigned long long k) {
+        return "(" + std::to_string(rows[k]) + ", " + std::to_string(cols[k]) + ")";
+    };
+    if (hf[0] != ~0ULL) throw std::invalid_argument("SampledMatrix: entry " + entry(hf[0]) + " out of range");
+    int end_bit = 1;
+    while (end_bit < 64 && (1ULL << end_bit) < static_cast<unsigned long long>(m) * static_cast<unsigned long long>(n))
+        ++end_bit;
+    size_t bytes = 0;
+    SVT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.get(), skeys.get(), idx.get(), perm.get(),
+                                             static_cast<int>(nnz), 0, end_bit, s));
+    tmp.ensure(bytes);
+    SVT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, keys.get(), skeys.get(), idx.get(), perm.get(),
+                                             static_cast<int>(nnz), 0, end_bit, s));
+    {
+        LaunchScope ls(ctx, K_OTHER, 20.0 * nnz, 0.0);
+        duplicate_kernel<<<nb(nnz), 256, 0, s>>>(nnz, skeys.get(), perm.get(), flags.get() + 2);
+    }
+    SVT_CUDA(cudaMemcpyAsync(hf, flags.get(), sizeof(hf), cudaMemcpyDeviceToHost, s));
+    sync_stream(ctx);
+    if (hf[1] != ~0ULL) throw std::invalid_argument("SampledMatrix: non-finite value at " + entry(hf[1]));
+    if (hf[2] != ~0ULL) throw std::invalid_argument("SampledMatrix: duplicate entry " + entry(hf[2]));
+    // this rank's rows
+    {
+        LaunchScope ls(ctx, K_OTHER, 8.0 * (ml + 1), 0.0);
+        triplet_rowptr_kernel<<<nb(ml + 1), 256, 0, s>>>(ml, rb, n, nnz, skeys.get(),
+                                                         reinterpret_cast<long long*>(M->rowptr.get()));
+    }
+    // global position of the block's first entry and the block's entry count
+    long long lo_hi[2] = {0, 0};
+    DevBuf<long long> lo_dev(1);
+    lower_bound_one_kernel<<<1, 1, 0, s>>>(skeys.get(), nnz, static_cast<unsigned long long>(rb) * n, lo_dev.get());
+    SVT_CUDA(cudaMemcpyAsync(&lo_hi[0], lo_dev.get(), sizeof(long long), cudaMemcpyDeviceToHost, s));
+    SVT_CUDA(cudaMemcpyAsync(&lo_hi[1], reinterpret_cast<long long*>(M->rowptr.get()) + ml, sizeof(long long),
+                             cudaMemcpyDeviceToHost, s));
+    sync_stream(ctx);
+    const i64 lo = lo_hi[0], cnt = lo_hi[1];
+    if (cnt > 2147483647LL) throw std::invalid_argument("svt_matrix_upload: > 2^31 entries per rank");
+    M->nnz_local = cnt;
+    M->col.alloc(static_cast<size_t>(std::max<i64>(1, cnt)));
+    M->val.alloc(static_cast<size_t>(std::max<i64>(1, cnt)));
+    M->cscrow.alloc(static_cast<size_t>(std::max<i64>(1, cnt)));
+    M->val_csc.alloc(static_cast<size_t>(std::max<i64>(1, cnt)));
+    M->csr2csc.alloc(static_cast<size_t>(std::max<i64>(1, cnt)));
+    DevBuf<long long> col64(static_cast<size_t>(std::max<i64>(1, cnt)));
+    if (cnt > 0) {
+        LaunchScope ls(ctx, K_OTHER, 28.0 * cnt, 0.0);
+        triplet_fill_kernel<<<nb(cnt), 256, 0, s>>>(cnt, lo, n, skeys.get(), perm.get(), dval.get(), col64.get(),
+                                                    M->val.get());
+    }
+    const int code = build_sampled_device(ctx, M, col64.get());
+    if (code != 0) throw std::invalid_argument("SampledMatrix: invalid entry");
 }
 
 }  // namespace svtb

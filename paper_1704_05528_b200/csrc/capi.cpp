@@ -258,6 +258,59 @@ int svt_matrix_upload(svt_ctx* ctx, int64_t m, int64_t n, int64_t row_begin, int
     });
 }
 
+int svt_matrix_from_triplets(svt_ctx* ctx, int64_t m, int64_t n, int64_t nnz, const int64_t* rows,
+                             const int64_t* cols, const double* vals, int64_t row_begin, int64_t row_end,
+                             svt_mat** out) {
+    return guard([&] {
+        need(ctx, "svt_matrix_from_triplets");
+        need(out, "svt_matrix_from_triplets");
+        if (m < 1 || n < 1) throw std::invalid_argument("SampledMatrix: dimensions must be >= 1");
+        if (nnz < 1) throw std::invalid_argument("SampledMatrix: at least one entry required");
+        if (nnz > 2147483647LL) throw std::invalid_argument("SampledMatrix: more than 2^31 entries");
+        if (!rows || !cols || !vals) throw std::invalid_argument("SampledMatrix: null triplet array");
+        if (row_begin < 0 || row_end < row_begin || row_end > m)
+            throw std::invalid_argument("svt_matrix_upload: bad row block");
+        SVT_CUDA(cudaSetDevice(ctx->device));
+        auto M = std::make_unique<svt_mat>();
+        M->ctx = ctx;
+        M->m = m;
+        M->n = n;
+        M->row_begin = row_begin;
+        M->row_end = row_end;
+        M->m_local = row_end - row_begin;
+        M->rowptr.alloc(static_cast<size_t>(M->m_local + 1));
+        M->colptr.alloc(static_cast<size_t>(n + 1));
+        build_from_triplets_device(ctx, M.get(), nnz, rows, cols, vals);
+        double g = static_cast<double>(M->nnz_local);
+        SVT_CUDA(cudaMemcpyAsync(ctx->d_scalars + 63, &g, sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        ctx->comm.allreduce_sum(ctx->d_scalars + 63, 1, ctx->stream);
+        SVT_CUDA(cudaMemcpyAsync(&g, ctx->d_scalars + 63, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        sync_stream(ctx);
+        M->nnz_global = static_cast<i64>(g + 0.5);
+        *out = M.release();
+    });
+}
+
+int svt_matrix_csr(svt_mat* mat, int64_t* rowptr, int64_t* col, double* val) {
+    return guard([&] {
+        need(mat, "svt_matrix_csr");
+        svt_ctx* c = mat->ctx;
+        const i64 nnz = mat->nnz_local, ml = mat->m_local;
+        if (rowptr)
+            SVT_CUDA(cudaMemcpyAsync(rowptr, mat->rowptr.get(), sizeof(int64_t) * (ml + 1), cudaMemcpyDeviceToHost,
+                                     c->stream));
+        std::vector<int> ci;
+        if (col && nnz > 0) {
+            ci.resize(static_cast<size_t>(nnz));
+            SVT_CUDA(cudaMemcpyAsync(ci.data(), mat->col.get(), sizeof(int) * nnz, cudaMemcpyDeviceToHost, c->stream));
+        }
+        if (val && nnz > 0)
+            SVT_CUDA(cudaMemcpyAsync(val, mat->val.get(), sizeof(double) * nnz, cudaMemcpyDeviceToHost, c->stream));
+        sync_stream(c);
+        for (i64 k = 0; k < static_cast<i64>(ci.size()); ++k) col[k] = ci[static_cast<size_t>(k)];
+    });
+}
+
 int svt_matrix_free(svt_mat* mat) {
     return guard([&] { delete mat; });
 }

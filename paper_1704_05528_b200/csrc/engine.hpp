@@ -127,6 +127,8 @@ u64 derive_seed_u(u64 seed, u64 stream);
 // build.cu: device-side CSC view / csr2csc / segment plans of an uploaded CSR
 void build_plan_device(svt_ctx* ctx, const long long* ptr, i64 rows, SegPlan& P);
 int build_sampled_device(svt_ctx* ctx, svt_mat* M, const long long* col64);
+void build_from_triplets_device(svt_ctx* ctx, svt_mat* M, i64 nnz, const i64* rows, const i64* cols,
+                                const double* vals);
 
 }  // namespace svtb
 

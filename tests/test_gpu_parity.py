@@ -511,3 +511,32 @@ def test_device_build_validates():
         G.SampledMatrix.from_csr(2, 3, [0, 1, 2], [0, 1], [1.0, np.nan])
     with pytest.raises(InvalidArgument):
         G.SampledMatrix.from_csr(2, 3, [0, 2, 1], [0, 1], [1.0, 2.0])
+
+
+@pytest.mark.parametrize("seed", [91, 92])
+def test_device_triplet_build_matches_host_sort(seed):
+    rng = np.random.default_rng(seed)
+    m, n, k = 700, 900, 40000
+    flat = rng.choice(m * n, size=k, replace=False)  # unsorted, distinct
+    rows, cols = flat // n, flat % n
+    vals = rng.standard_normal(k)
+    rp, co, va = G.build_csr(m, n, rows, cols, vals)  # host restatement of sampled.hpp:27-62
+    S = G.SampledMatrix(m, n, rows, cols, vals)
+    assert np.array_equal(S.rowptr, rp) and np.array_equal(S.col, co) and np.array_equal(S.values(), va)
+    B = G.SampledMatrix(m, n, rows, cols, vals, row_block=(100, 450))
+    s0, s1 = int(rp[100]), int(rp[450])
+    assert np.array_equal(B.rowptr, rp[100:451] - rp[100]) and np.array_equal(B.col, co[s0:s1])
+    assert np.array_equal(B.values(), va[s0:s1])
+    X = rng.standard_normal((n, 7))
+    np.testing.assert_array_equal(G.sp_mult(S, X), G.sp_mult(G.SampledMatrix.from_csr(m, n, rp, co, va), X))
+
+
+def test_device_triplet_build_errors():  # sampled.hpp:27-62 messages
+    with pytest.raises(InvalidArgument, match="out of range"):
+        G.SampledMatrix(3, 3, [0, 3], [0, 1], [1.0, 2.0])
+    with pytest.raises(InvalidArgument, match="non-finite"):
+        G.SampledMatrix(3, 3, [0, 1], [0, 1], [1.0, np.inf])
+    with pytest.raises(InvalidArgument, match=r"duplicate entry \(1, 2\)"):
+        G.SampledMatrix(3, 3, [1, 0, 1], [2, 0, 2], [1.0, 2.0, 3.0])
+    with pytest.raises(InvalidArgument):
+        G.SampledMatrix(3, 3, [], [], [])
