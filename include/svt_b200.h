@@ -166,6 +166,39 @@ int svt_matrix_info(svt_mat* mat, int64_t* m, int64_t* n, int64_t* nnz_local, in
 int svt_matrix_set_values(svt_mat* mat, const double* vals);
 int svt_matrix_get_values(svt_mat* mat, double* vals);
 
+/* ---- formats (io.hpp): readers / writers either side of the path ------ */
+/* Host triplet set: 0-based (row, col, value) in an m x n frame; a ratings
+ * file also carries the original user / item ids of the dense indices. */
+typedef struct svt_triplets svt_triplets;
+int svt_read_matrix_market(const char* path, svt_triplets** out);              /* io.hpp:118-173 */
+int svt_read_ratings(const char* path, const char* separator, svt_triplets** out); /* io.hpp:383-470 */
+int svt_sample_image(int64_t width, int64_t height, const uint8_t* pixels, double fraction, uint64_t seed,
+                     svt_triplets** out);                                         /* io.hpp:329-350 */
+int svt_split_ratings(svt_triplets* ds, double train_fraction, uint64_t seed, svt_triplets** train,
+                      svt_triplets** test);                                       /* io.hpp:474-497 */
+/* a triplet set from host arrays (no validation; SampledMatrix construction validates) */
+int svt_triplets_create(int64_t m, int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                        const double* vals, svt_triplets** out);
+int svt_triplets_info(svt_triplets* t, int64_t* m, int64_t* n, int64_t* nnz);
+int svt_triplets_copy(svt_triplets* t, int64_t* rows, int64_t* cols, double* vals);
+/* ratings only: user_ids (m entries), item_ids (n entries); provenance line */
+int svt_triplets_ids(svt_triplets* t, int64_t* user_ids, int64_t* item_ids);
+const char* svt_triplets_provenance(svt_triplets* t);
+int svt_triplets_free(svt_triplets* t);
+/* device SampledMatrix of a triplet set (svt_matrix_from_triplets semantics) */
+int svt_matrix_from_triplet_set(svt_ctx* ctx, svt_triplets* t, int64_t row_begin, int64_t row_end, svt_mat** out);
+/* coordinate writer of a host CSR (1-based, %.17g: exact round trip), io.hpp:176-193 */
+int svt_write_matrix_market(const char* path, int64_t m, int64_t n, const int64_t* rowptr, const int64_t* col,
+                            const double* val);
+/* dense `array real general`, column-major; data == NULL queries the shape */
+int svt_read_matrix_market_array(const char* path, int64_t* rows, int64_t* cols, double* data); /* io.hpp:196-231 */
+int svt_write_matrix_market_array(const char* path, int64_t rows, int64_t cols, const double* data); /* :233-246 */
+/* PGM (P5 / P2, maxval 255); pixels row-major; pixels == NULL queries the shape */
+int svt_read_pgm(const char* path, int64_t* width, int64_t* height, uint8_t* pixels); /* io.hpp:272-313 */
+int svt_write_pgm(const char* path, int64_t width, int64_t height, const uint8_t* pixels); /* io.hpp:316-327 */
+/* round + clamp a column-major rows x cols reconstruction into 8-bit pixels (row-major) */
+int svt_quantize_image(int64_t rows, int64_t cols, const double* X, uint8_t* pixels); /* io.hpp:367-381 */
+
 /* ---- primitives (host in/out; dense.hpp / sampled.hpp) ---------------- */
 int svt_gaussian_block(svt_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out); /* dense.hpp:86 */
 int svt_qr_orthonormal(svt_ctx* ctx, int64_t rows, int64_t cols, const double* X, double* Q); /* dense.hpp:103 */

@@ -6,6 +6,7 @@
 #include <string>
 
 #include "engine.hpp"
+#include "io.hpp"
 #include "kernels.hpp"
 
 namespace svtb {
@@ -308,6 +309,174 @@ int svt_matrix_csr(svt_mat* mat, int64_t* rowptr, int64_t* col, double* val) {
             SVT_CUDA(cudaMemcpyAsync(val, mat->val.get(), sizeof(double) * nnz, cudaMemcpyDeviceToHost, c->stream));
         sync_stream(c);
         for (i64 k = 0; k < static_cast<i64>(ci.size()); ++k) col[k] = ci[static_cast<size_t>(k)];
+    });
+}
+
+// ---- formats ---------------------------------------------------------------
+struct svt_triplets {
+    svtb::Triplets t;
+};
+
+int svt_read_matrix_market(const char* path, svt_triplets** out) {
+    return guard([&] {
+        need(path, "svt_read_matrix_market");
+        need(out, "svt_read_matrix_market");
+        auto T = std::make_unique<svt_triplets>();
+        T->t = svtb::read_matrix_market(path);
+        *out = T.release();
+    });
+}
+
+int svt_read_ratings(const char* path, const char* separator, svt_triplets** out) {
+    return guard([&] {
+        need(path, "svt_read_ratings");
+        need(out, "svt_read_ratings");
+        auto T = std::make_unique<svt_triplets>();
+        T->t = svtb::read_ratings(path, separator ? separator : "::");
+        *out = T.release();
+    });
+}
+
+int svt_sample_image(int64_t width, int64_t height, const uint8_t* pixels, double fraction, uint64_t seed,
+                     svt_triplets** out) {
+    return guard([&] {
+        need(pixels, "svt_sample_image");
+        need(out, "svt_sample_image");
+        if (width < 1 || height < 1) throw std::invalid_argument("sample_image: bad dimensions");
+        auto T = std::make_unique<svt_triplets>();
+        T->t = svtb::sample_image(width, height, pixels, fraction, seed);
+        *out = T.release();
+    });
+}
+
+int svt_split_ratings(svt_triplets* ds, double train_fraction, uint64_t seed, svt_triplets** train,
+                      svt_triplets** test) {
+    return guard([&] {
+        need(ds, "svt_split_ratings");
+        need(train, "svt_split_ratings");
+        need(test, "svt_split_ratings");
+        auto A = std::make_unique<svt_triplets>(), B = std::make_unique<svt_triplets>();
+        svtb::split_ratings(ds->t, train_fraction, seed, A->t, B->t);
+        *train = A.release();
+        *test = B.release();
+    });
+}
+
+int svt_triplets_create(int64_t m, int64_t n, int64_t nnz, const int64_t* rows, const int64_t* cols,
+                        const double* vals, svt_triplets** out) {
+    return guard([&] {
+        need(out, "svt_triplets_create");
+        if (m < 0 || n < 0 || nnz < 0 || (nnz > 0 && (!rows || !cols || !vals)))
+            throw std::invalid_argument("svt_triplets_create: bad arguments");
+        auto T = std::make_unique<svt_triplets>();
+        T->t.m = m;
+        T->t.n = n;
+        T->t.r.assign(rows, rows + nnz);
+        T->t.c.assign(cols, cols + nnz);
+        T->t.v.assign(vals, vals + nnz);
+        *out = T.release();
+    });
+}
+
+int svt_triplets_info(svt_triplets* t, int64_t* m, int64_t* n, int64_t* nnz) {
+    return guard([&] {
+        need(t, "svt_triplets_info");
+        if (m) *m = t->t.m;
+        if (n) *n = t->t.n;
+        if (nnz) *nnz = static_cast<int64_t>(t->t.r.size());
+    });
+}
+
+int svt_triplets_copy(svt_triplets* t, int64_t* rows, int64_t* cols, double* vals) {
+    return guard([&] {
+        need(t, "svt_triplets_copy");
+        const size_t k = t->t.r.size();
+        if (rows) std::memcpy(rows, t->t.r.data(), sizeof(int64_t) * k);
+        if (cols) std::memcpy(cols, t->t.c.data(), sizeof(int64_t) * k);
+        if (vals) std::memcpy(vals, t->t.v.data(), sizeof(double) * k);
+    });
+}
+
+int svt_triplets_ids(svt_triplets* t, int64_t* user_ids, int64_t* item_ids) {
+    return guard([&] {
+        need(t, "svt_triplets_ids");
+        if (t->t.user_ids.empty()) throw std::invalid_argument("svt_triplets_ids: not a ratings set");
+        if (user_ids) std::memcpy(user_ids, t->t.user_ids.data(), sizeof(int64_t) * t->t.user_ids.size());
+        if (item_ids) std::memcpy(item_ids, t->t.item_ids.data(), sizeof(int64_t) * t->t.item_ids.size());
+    });
+}
+
+const char* svt_triplets_provenance(svt_triplets* t) { return t ? t->t.provenance.c_str() : ""; }
+
+int svt_triplets_free(svt_triplets* t) {
+    return guard([&] { delete t; });
+}
+
+int svt_matrix_from_triplet_set(svt_ctx* ctx, svt_triplets* t, int64_t row_begin, int64_t row_end, svt_mat** out) {
+    const int g = guard([&] { need(t, "svt_matrix_from_triplet_set"); });
+    if (g != SVT_OK) return g;
+    const int64_t one = 0;
+    const double zero = 0.0;
+    const bool e = t->t.r.empty();
+    return svt_matrix_from_triplets(ctx, t->t.m, t->t.n, static_cast<int64_t>(t->t.r.size()),
+                                    e ? &one : t->t.r.data(), e ? &one : t->t.c.data(), e ? &zero : t->t.v.data(),
+                                    row_begin, row_end, out);
+}
+
+int svt_write_matrix_market(const char* path, int64_t m, int64_t n, const int64_t* rowptr, const int64_t* col,
+                            const double* val) {
+    return guard([&] {
+        need(path, "svt_write_matrix_market");
+        need(rowptr, "svt_write_matrix_market");
+        if (m < 1 || n < 1) throw std::invalid_argument("write_matrix_market: bad dimensions");
+        svtb::write_matrix_market(path, m, n, rowptr, col, val);
+    });
+}
+
+int svt_read_matrix_market_array(const char* path, int64_t* rows, int64_t* cols, double* data) {
+    return guard([&] {
+        need(path, "svt_read_matrix_market_array");
+        i64 r = 0, c = 0;
+        const auto X = svtb::read_matrix_market_array(path, r, c);
+        if (rows) *rows = r;
+        if (cols) *cols = c;
+        if (data) std::memcpy(data, X.data(), sizeof(double) * X.size());
+    });
+}
+
+int svt_write_matrix_market_array(const char* path, int64_t rows, int64_t cols, const double* data) {
+    return guard([&] {
+        need(path, "svt_write_matrix_market_array");
+        if (rows < 0 || cols < 0 || (rows * cols > 0 && !data))
+            throw std::invalid_argument("write_matrix_market_array: bad arguments");
+        svtb::write_matrix_market_array(path, rows, cols, data);
+    });
+}
+
+int svt_read_pgm(const char* path, int64_t* width, int64_t* height, uint8_t* pixels) {
+    return guard([&] {
+        need(path, "svt_read_pgm");
+        i64 w = 0, h = 0;
+        const auto px = svtb::read_pgm(path, w, h);
+        if (width) *width = w;
+        if (height) *height = h;
+        if (pixels) std::memcpy(pixels, px.data(), px.size());
+    });
+}
+
+int svt_write_pgm(const char* path, int64_t width, int64_t height, const uint8_t* pixels) {
+    return guard([&] {
+        need(path, "svt_write_pgm");
+        svtb::write_pgm(path, width, height, pixels);
+    });
+}
+
+int svt_quantize_image(int64_t rows, int64_t cols, const double* X, uint8_t* pixels) {
+    return guard([&] {
+        need(X, "svt_quantize_image");
+        need(pixels, "svt_quantize_image");
+        if (rows < 0 || cols < 0) throw std::invalid_argument("quantize_image: bad dimensions");
+        svtb::quantize_image(rows, cols, X, pixels);
     });
 }
 

@@ -420,4 +420,7 @@ void synth_config_csr(int config, u64 seed, i64* m, i64* n, i64* nnz, i64* rowpt
     if (val) std::memcpy(val, g_cache.val.data(), sizeof(double) * g_cache.val.size());
 }
 
+// the partial Fisher-Yates sampler for the formats module (io.cpp)
+std::vector<u64> sample_positions_exported(u64 total, u64 ns, u64 seed) { return sample_positions(total, ns, seed); }
+
 }  // namespace svtb
