@@ -199,6 +199,10 @@ int svt_write_pgm(const char* path, int64_t width, int64_t height, const uint8_t
 /* round + clamp a column-major rows x cols reconstruction into 8-bit pixels (row-major) */
 int svt_quantize_image(int64_t rows, int64_t cols, const double* X, uint8_t* pixels); /* io.hpp:367-381 */
 
+/* trace export, schema "svt-trace v1": json = 0 -> write_trace_csv, 1 ->
+ * write_trace_json (solver.hpp:346-386) */
+int svt_write_trace(const svt_record* records, int64_t count, const char* path, int json);
+
 /* ---- primitives (host in/out; dense.hpp / sampled.hpp) ---------------- */
 int svt_gaussian_block(svt_ctx* ctx, int64_t rows, int64_t cols, uint64_t seed, double* out); /* dense.hpp:86 */
 int svt_qr_orthonormal(svt_ctx* ctx, int64_t rows, int64_t cols, const double* X, double* Q); /* dense.hpp:103 */

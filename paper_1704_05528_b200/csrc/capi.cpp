@@ -480,6 +480,14 @@ int svt_quantize_image(int64_t rows, int64_t cols, const double* X, uint8_t* pix
     });
 }
 
+int svt_write_trace(const svt_record* records, int64_t count, const char* path, int json) {
+    return guard([&] {
+        need(path, "svt_write_trace");
+        if (count < 0 || (count > 0 && !records)) throw std::invalid_argument("svt_write_trace: bad records");
+        svtb::write_trace(records, count, path, json != 0);
+    });
+}
+
 int svt_matrix_free(svt_mat* mat) {
     return guard([&] { delete mat; });
 }

@@ -5,6 +5,7 @@
 #include <vector>
 
 #include "common.hpp"
+#include "../../include/svt_b200.h"
 
 namespace svtb {
 
@@ -28,5 +29,6 @@ Triplets sample_image(i64 width, i64 height, const unsigned char* pixels, double
 void quantize_image(i64 rows, i64 cols, const double* X_colmajor, unsigned char* pixels);
 Triplets read_ratings(const std::string& path, const std::string& separator);
 void split_ratings(const Triplets& ds, double train_fraction, u64 seed, Triplets& train, Triplets& test);
+void write_trace(const svt_record* recs, i64 count, const std::string& path, bool json);
 
 }  // namespace svtb

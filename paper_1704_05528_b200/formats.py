@@ -226,3 +226,25 @@ def split_ratings(ds: RatingsDataset, train_fraction: float, seed: int, ctx: Con
                                   C.byref(b)))
     ta, tb = _Triplets(a), _Triplets(b)
     return ta.to_matrix(ctx), tb.to_matrix(ctx)
+
+
+# ---- trace export ------------------------------------------------------------------------
+def _records(trace):
+    from ._abi import IterationRecord
+    arr = (IterationRecord * max(len(trace), 1))()
+    for i, rec in enumerate(trace):
+        for name, _ in IterationRecord._fields_:
+            if name in rec:
+                setattr(arr[i], name, rec[name])
+    return arr
+
+
+def write_trace_csv(trace, path: str) -> None:
+    """write_trace_csv (solver.hpp:346-364), schema "svt-trace v1"; trace is
+    SvtResult.trace (a list of IterationRecord dicts)."""
+    _check(_L().svt_write_trace(_records(trace), C.c_int64(len(trace)), str(path).encode(), C.c_int(0)))
+
+
+def write_trace_json(trace, path: str) -> None:
+    """write_trace_json (solver.hpp:366-386)."""
+    _check(_L().svt_write_trace(_records(trace), C.c_int64(len(trace)), str(path).encode(), C.c_int(1)))

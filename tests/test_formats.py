@@ -231,3 +231,31 @@ def test_split_ratings_and_sample_image_on_device(tmp_path):
     D = S.dense()
     mask = D != 0
     assert np.array_equal(D[mask], img.pixels[mask].astype(float))
+
+
+# ---- trace export (solver.hpp:346-386) ------------------------------------------------
+def _trace():
+    return [dict(iter=1, rank=10, residual=0.1, eps_threshold=0.5, train_mae=1.0 / 3.0, sketch_ms=1.23456,
+                 total_ms=2.0),
+            dict(iter=2, rank=20, residual=2.5e-17, eps_threshold=0.475, train_mae=0.25, sketch_ms=0.0005,
+                 total_ms=1e3)]
+
+
+def test_trace_csv_schema(tmp_path):
+    p = str(tmp_path / "t.csv")
+    F.write_trace_csv(_trace(), p)
+    assert open(p).read() == ("# svt-trace v1\niter,rank,residual,eps_threshold,train_mae,sketch_ms,total_ms\n"
+                              "1,10,0.10000000000000001,0.5,0.33333333333333331,1.235,2.000\n"
+                              "2,20,2.4999999999999999e-17,0.47499999999999998,0.25,0.001,1000.000\n")
+
+
+def test_trace_json_schema(tmp_path):
+    import json
+    p = str(tmp_path / "t.json")
+    F.write_trace_json(_trace(), p)
+    text = open(p).read()
+    assert text.startswith('{\n  "schema": "svt-trace v1",\n  "rows": [\n    {"iter": 1, "rank": 10, ')
+    doc = json.loads(text)
+    assert doc["rows"][1]["residual"] == 2.5e-17 and doc["rows"][0]["sketch_ms"] == 1.235
+    F.write_trace_json([], p)
+    assert json.loads(open(p).read()) == {"schema": "svt-trace v1", "rows": []}
