@@ -1451,6 +1451,111 @@ __global__ void __launch_bounds__(kHhThreads) householder_kernel(const double* _
 // ---------------------------------------------------------------------------
 constexpr int kJacMax = 48;
 
+// Two-sided cyclic Jacobi for a symmetric r x r matrix (r <= 48), one CTA:
+// round-robin parallel ordering, the rp/2 disjoint rotations of a step are
+// computed from (a_pp, a_qq, a_pq) alone (no column dot products), then
+// applied to the rows and to the columns (and to V) in two barrier-separated
+// phases.  Eigenvalues = diag(A), eigenvectors = columns of V; sorted
+// descending (stable).
+__global__ void __launch_bounds__(512) jacobi_sym_kernel(const double* __restrict__ G, int r,
+                                                         double* __restrict__ W, double* __restrict__ lambda) {
+    __shared__ double A[kJacMax][kJacMax + 1];
+    __shared__ double V[kJacMax][kJacMax + 1];
+    __shared__ double cs[kJacMax / 2][2];
+    __shared__ int pq[kJacMax / 2][2];
+    __shared__ double dg[kJacMax];
+    __shared__ int order[kJacMax];
+    __shared__ int rotated;
+    const int tid = threadIdx.x;
+    const int rp = (r + 1) & ~1;  // even, padded with a zero row / column
+    const int np = rp / 2;
+    const double tol = 4.0 * 2.220446049250313e-16;
+    for (int e = tid; e < rp * rp; e += blockDim.x) {
+        const int i = e / rp, j = e % rp;
+        A[i][j] = (i < r && j < r) ? G[i * r + j] : 0.0;
+        V[i][j] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    for (int sweep = 0; sweep < 60; ++sweep) {
+        if (tid == 0) rotated = 0;
+        __syncthreads();
+        for (int step = 0; step < rp - 1; ++step) {
+            if (tid < np) {
+                const int a = tid, b = rp - 1 - tid;
+                int p = (a == 0) ? 0 : 1 + (a - 1 + step) % (rp - 1);
+                int q = (b == 0) ? 0 : 1 + (b - 1 + step) % (rp - 1);
+                if (p > q) {
+                    const int t = p;
+                    p = q;
+                    q = t;
+                }
+                const double app = A[p][p], aqq = A[q][q], apq = A[p][q];
+                double c = 1.0, sn = 0.0;
+                if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq))) {
+                    const double tau = (aqq - app) / (2.0 * apq);
+                    const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                    c = 1.0 / sqrt(1.0 + t * t);
+                    sn = t * c;
+                    rotated = 1;
+                }
+                pq[tid][0] = p;
+                pq[tid][1] = q;
+                cs[tid][0] = c;
+                cs[tid][1] = sn;
+            }
+            __syncthreads();
+            // rows: A <- J^T A
+            for (int e = tid; e < np * rp; e += blockDim.x) {
+                const int k = e / rp, j = e % rp;
+                const double c = cs[k][0], sn = cs[k][1];
+                if (sn == 0.0) continue;
+                const int p = pq[k][0], q = pq[k][1];
+                const double x = A[p][j], y = A[q][j];
+                A[p][j] = c * x - sn * y;
+                A[q][j] = sn * x + c * y;
+            }
+            __syncthreads();
+            // columns: A <- A J, V <- V J
+            for (int e = tid; e < np * rp; e += blockDim.x) {
+                const int k = e / rp, i = e % rp;
+                const double c = cs[k][0], sn = cs[k][1];
+                if (sn == 0.0) continue;
+                const int p = pq[k][0], q = pq[k][1];
+                const double x = A[i][p], y = A[i][q];
+                A[i][p] = c * x - sn * y;
+                A[i][q] = sn * x + c * y;
+                const double vx = V[i][p], vy = V[i][q];
+                V[i][p] = c * vx - sn * vy;
+                V[i][q] = sn * vx + c * vy;
+            }
+            __syncthreads();
+        }
+        if (!rotated) break;
+    }
+    if (tid < r) {
+        dg[tid] = A[tid][tid];
+        order[tid] = tid;
+    }
+    __syncthreads();
+    if (tid == 0) {  // stable insertion sort, descending
+        for (int i = 1; i < r; ++i) {
+            const int o = order[i];
+            int j = i - 1;
+            while (j >= 0 && dg[order[j]] < dg[o]) {
+                order[j + 1] = order[j];
+                --j;
+            }
+            order[j + 1] = o;
+        }
+    }
+    __syncthreads();
+    for (int e = tid; e < r * r; e += blockDim.x) {
+        const int i = e / r, j = e % r;
+        W[i * r + j] = V[i][order[j]];
+    }
+    if (tid < r) lambda[tid] = dg[order[tid]];
+}
+
 __global__ void __launch_bounds__(1024) jacobi_eig_kernel(const double* __restrict__ G, int r,
                                                           double* __restrict__ W, double* __restrict__ lambda,
                                                           int dbg) {
@@ -1881,8 +1986,13 @@ void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
     if (r <= 0) return;
     if (r <= kJacMax) {
         LaunchScope ls(ctx, K_FINAL, 16.0 * r * r, 0.0);
-        static const int dbg = std::getenv("SVTB_DEBUG_JACOBI") ? 1 : 0;
-        jacobi_eig_kernel<<<1, 1024, 0, ctx->stream>>>(G, static_cast<int>(r), W, lambda, dbg);
+        static const int variant = std::getenv("SVTB_JACOBI_ONESIDED") ? 1 : 0;
+        if (variant) {
+            static const int dbg = std::getenv("SVTB_DEBUG_JACOBI") ? 1 : 0;
+            jacobi_eig_kernel<<<1, 1024, 0, ctx->stream>>>(G, static_cast<int>(r), W, lambda, dbg);
+        } else {
+            jacobi_sym_kernel<<<1, 512, 0, ctx->stream>>>(G, static_cast<int>(r), W, lambda);
+        }
         return;
     }
     // Larger Grams: cooperative multi-CTA one-sided Jacobi.
