@@ -298,13 +298,25 @@ def main():
     roof.update({"kernel": dom, "arith_intensity_flop_per_byte": ai, "machine_balance": balance,
                  "launches": s["launches"], "avg_launch_us": 1000.0 * s["total_ms"] / max(1, s["launches"]),
                  "share_of_step": s["total_ms"] / max(1e-9, sum(v["total_ms"] for v in stats.values()))})
-    # the sparse passes, always reported against HBM (north star: SpMM/SDDMM GB/s vs peak)
+    # the sparse passes, always reported against HBM (north star: SpMM/SDDMM
+    # GB/s vs peak), plus the SpMMs' L2 gather rate: every stored entry reads
+    # one 8w-byte panel row (= 4 x the 2 nnz w flops), which is what bounds
+    # them (ncu: DRAM ~3 %, L2 hit ~96 %); ceiling = the LTS throughput cap
+    # of the microarchitecture guide (~6300 B/clk at 1.965 GHz)
+    l2_cap_tbs = 6300.0 * 1.965e9 / 1e12
     sparse = {}
     for k in ("spmm", "spmm_t", "sddmm_update"):
         v = stats[k]
         if v["total_ms"] > 0:
             sparse[k] = {"achieved_gbs": v["bytes"] / (v["total_ms"] * 1e-3) / 1e9,
                          "frac": v["bytes"] / (v["total_ms"] * 1e-3) / 1e9 / peak_bw}
+            if k != "sddmm_update":
+                g = 4.0 * v["flops"] / (v["total_ms"] * 1e-3) / 1e12
+                sparse[k].update({"l2_gather_tbs": g, "l2_gather_ceiling_tbs": l2_cap_tbs,
+                                  "l2_gather_frac": g / l2_cap_tbs})
+    if dom in ("spmm", "spmm_t"):
+        roof["note"] = ("L2-gather bound, not HBM: see sparse_roofline[%s].l2_gather_* (DRAM traffic per "
+                        "launch ~ the algorithmic bytes)" % dom)
     step_ms_kernels = {k: v["total_ms"] / args.steps for k, v in stats.items()}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
