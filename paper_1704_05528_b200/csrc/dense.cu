@@ -1451,83 +1451,80 @@ __global__ void __launch_bounds__(kHhThreads) householder_kernel(const double* _
 // ---------------------------------------------------------------------------
 constexpr int kJacMax = 48;
 
-// Two-sided cyclic Jacobi for a symmetric r x r matrix (r <= 48), one CTA:
-// round-robin parallel ordering, the rp/2 disjoint rotations of a step are
-// computed from (a_pp, a_qq, a_pq) alone (no column dot products), then
-// applied to the rows and to the columns (and to V) in two barrier-separated
-// phases.  Eigenvalues = diag(A), eigenvectors = columns of V; sorted
-// descending (stable).
-__global__ void __launch_bounds__(512) jacobi_sym_kernel(const double* __restrict__ G, int r,
-                                                         double* __restrict__ W, double* __restrict__ lambda) {
-    __shared__ double A[kJacMax][kJacMax + 1];
-    __shared__ double V[kJacMax][kJacMax + 1];
-    __shared__ double cs[kJacMax / 2][2];
-    __shared__ int pq[kJacMax / 2][2];
-    __shared__ double dg[kJacMax];
-    __shared__ int order[kJacMax];
+// Two-sided cyclic Jacobi for a symmetric r x r matrix (r <= RP <= 48), one
+// CTA: round-robin parallel ordering (the step's RP/2 pairs precomputed in
+// shared memory), the disjoint rotations of a step computed from
+// (a_pp, a_qq, a_pq) alone, then applied to the rows and to the columns (and
+// V) in barrier-separated phases.  RP is a compile-time bucket (16 / 32 /
+// 48), the matrix is zero-padded to it (padding never rotates), so every
+// index split is a shift or a constant multiply.  Eigenvalues = diag(A),
+// eigenvectors = columns of V, sorted descending (stable).
+template <int RP>
+__global__ void __launch_bounds__(32 * RP / 2) jacobi_sym_kernel(const double* __restrict__ G, int r,
+                                                                 double* __restrict__ W, double* __restrict__ lambda) {
+    constexpr int NP = RP / 2;
+    constexpr int NT = 32 * NP;  // one warp per pair
+    __shared__ double A[RP][RP + 1];
+    __shared__ double V[RP][RP + 1];
+    __shared__ double cs[NP][2];
+    __shared__ unsigned char sched[RP - 1][NP][2];
+    __shared__ double dg[RP];
+    __shared__ int order[RP];
     __shared__ int rotated;
-    const int tid = threadIdx.x;
-    const int rp = (r + 1) & ~1;  // even, padded with a zero row / column
-    const int np = rp / 2;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const double tol = 4.0 * 2.220446049250313e-16;
-    for (int e = tid; e < rp * rp; e += blockDim.x) {
-        const int i = e / rp, j = e % rp;
+    for (int e = tid; e < RP * RP; e += NT) {
+        const int i = e / RP, j = e % RP;
         A[i][j] = (i < r && j < r) ? G[i * r + j] : 0.0;
         V[i][j] = (i == j) ? 1.0 : 0.0;
+    }
+    for (int e = tid; e < (RP - 1) * NP; e += NT) {
+        const int step = e / NP, k = e % NP;
+        const int a = k, b = RP - 1 - k;
+        int p = (a == 0) ? 0 : 1 + (a - 1 + step) % (RP - 1);
+        int q = (b == 0) ? 0 : 1 + (b - 1 + step) % (RP - 1);
+        sched[step][k][0] = static_cast<unsigned char>(p < q ? p : q);
+        sched[step][k][1] = static_cast<unsigned char>(p < q ? q : p);
     }
     __syncthreads();
     for (int sweep = 0; sweep < 60; ++sweep) {
         if (tid == 0) rotated = 0;
         __syncthreads();
-        for (int step = 0; step < rp - 1; ++step) {
-            if (tid < np) {
-                const int a = tid, b = rp - 1 - tid;
-                int p = (a == 0) ? 0 : 1 + (a - 1 + step) % (rp - 1);
-                int q = (b == 0) ? 0 : 1 + (b - 1 + step) % (rp - 1);
-                if (p > q) {
-                    const int t = p;
-                    p = q;
-                    q = t;
-                }
+        for (int step = 0; step < RP - 1; ++step) {
+            const int p = sched[step][warp][0], q = sched[step][warp][1];
+            if (lane == 0) {
                 const double app = A[p][p], aqq = A[q][q], apq = A[p][q];
                 double c = 1.0, sn = 0.0;
                 if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq))) {
                     const double tau = (aqq - app) / (2.0 * apq);
                     const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                    c = 1.0 / sqrt(1.0 + t * t);
+                    c = rsqrt(1.0 + t * t);
                     sn = t * c;
                     rotated = 1;
                 }
-                pq[tid][0] = p;
-                pq[tid][1] = q;
-                cs[tid][0] = c;
-                cs[tid][1] = sn;
+                cs[warp][0] = c;
+                cs[warp][1] = sn;
             }
+            __syncwarp();
+            const double c = cs[warp][0], sn = cs[warp][1];
+            // rows p, q of A (this warp's pair only: disjoint from the others)
+            if (sn != 0.0)
+                for (int j = lane; j < RP; j += 32) {
+                    const double x = A[p][j], y = A[q][j];
+                    A[p][j] = c * x - sn * y;
+                    A[q][j] = sn * x + c * y;
+                }
             __syncthreads();
-            // rows: A <- J^T A
-            for (int e = tid; e < np * rp; e += blockDim.x) {
-                const int k = e / rp, j = e % rp;
-                const double c = cs[k][0], sn = cs[k][1];
-                if (sn == 0.0) continue;
-                const int p = pq[k][0], q = pq[k][1];
-                const double x = A[p][j], y = A[q][j];
-                A[p][j] = c * x - sn * y;
-                A[q][j] = sn * x + c * y;
-            }
-            __syncthreads();
-            // columns: A <- A J, V <- V J
-            for (int e = tid; e < np * rp; e += blockDim.x) {
-                const int k = e / rp, i = e % rp;
-                const double c = cs[k][0], sn = cs[k][1];
-                if (sn == 0.0) continue;
-                const int p = pq[k][0], q = pq[k][1];
-                const double x = A[i][p], y = A[i][q];
-                A[i][p] = c * x - sn * y;
-                A[i][q] = sn * x + c * y;
-                const double vx = V[i][p], vy = V[i][q];
-                V[i][p] = c * vx - sn * vy;
-                V[i][q] = sn * vx + c * vy;
-            }
+            // columns p, q of A and V
+            if (sn != 0.0)
+                for (int i = lane; i < RP; i += 32) {
+                    const double x = A[i][p], y = A[i][q];
+                    A[i][p] = c * x - sn * y;
+                    A[i][q] = sn * x + c * y;
+                    const double vx = V[i][p], vy = V[i][q];
+                    V[i][p] = c * vx - sn * vy;
+                    V[i][q] = sn * vx + c * vy;
+                }
             __syncthreads();
         }
         if (!rotated) break;
@@ -1549,7 +1546,7 @@ __global__ void __launch_bounds__(512) jacobi_sym_kernel(const double* __restric
         }
     }
     __syncthreads();
-    for (int e = tid; e < r * r; e += blockDim.x) {
+    for (int e = tid; e < r * r; e += NT) {
         const int i = e / r, j = e % r;
         W[i * r + j] = V[i][order[j]];
     }
@@ -1991,7 +1988,19 @@ void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
             static const int dbg = std::getenv("SVTB_DEBUG_JACOBI") ? 1 : 0;
             jacobi_eig_kernel<<<1, 1024, 0, ctx->stream>>>(G, static_cast<int>(r), W, lambda, dbg);
         } else {
-            jacobi_sym_kernel<<<1, 512, 0, ctx->stream>>>(G, static_cast<int>(r), W, lambda);
+            const int ri = static_cast<int>(r);
+            if (r <= 8)
+                jacobi_sym_kernel<8><<<1, 32 * 4, 0, ctx->stream>>>(G, ri, W, lambda);
+            else if (r <= 16)
+                jacobi_sym_kernel<16><<<1, 32 * 8, 0, ctx->stream>>>(G, ri, W, lambda);
+            else if (r <= 24)
+                jacobi_sym_kernel<24><<<1, 32 * 12, 0, ctx->stream>>>(G, ri, W, lambda);
+            else if (r <= 32)
+                jacobi_sym_kernel<32><<<1, 32 * 16, 0, ctx->stream>>>(G, ri, W, lambda);
+            else if (r <= 40)
+                jacobi_sym_kernel<40><<<1, 32 * 20, 0, ctx->stream>>>(G, ri, W, lambda);
+            else
+                jacobi_sym_kernel<48><<<1, 32 * 24, 0, ctx->stream>>>(G, ri, W, lambda);
         }
         return;
     }
