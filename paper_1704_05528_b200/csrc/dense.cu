@@ -451,9 +451,10 @@ void dmma_launch(svt_ctx* ctx, bool transA, i64 M, i64 N, i64 K, double alpha, c
                  const double* B, i64 ldb, double beta, double* C, i64 ldc, const int* pred) {
     const i64 mt = (M + kDmmaBM - 1) / kDmmaBM, nt = (N + BN - 1) / BN;
     const i64 tiles = mt * nt;
+    static const bool no_cpasync = std::getenv("SVTB_NO_CPASYNC") != nullptr;
     // the cp.async pipeline needs 16-byte aligned rows
     const bool cp = (lda % 2 == 0) && (ldb % 2 == 0) && (reinterpret_cast<uintptr_t>(A) % 16 == 0) &&
-                    (reinterpret_cast<uintptr_t>(B) % 16 == 0) && !std::getenv("SVTB_NO_CPASYNC");
+                    (reinterpret_cast<uintptr_t>(B) % 16 == 0) && !no_cpasync;
     // resident CTAs per wave (occupancy of this instantiation, cached)
     static int per_sm[4] = {0, 0, 0, 0};
     int& ps = per_sm[(transA ? 1 : 0) + (cp ? 2 : 0)];

@@ -43,6 +43,11 @@ int read_flag(svt_ctx* c, int i) {
     return c->h_flags[i];
 }
 
+bool debug_batch() {
+    static const bool on = std::getenv("SVTB_DEBUG_BATCH") != nullptr;
+    return on;
+}
+
 void zero_flag(svt_ctx* c, int i) { SVT_CUDA(cudaMemsetAsync(c->d_flags + i, 0, sizeof(int), c->stream)); }
 
 void allreduce(svt_ctx* c, double* p, size_t n) { c->comm.allreduce_sum(p, n, c->stream); }
@@ -748,14 +753,14 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
             sync_stream(c);
             for (int k = 0; k < K && !second; ++k)
                 second = std::sqrt(block_sum(W, k)) > 1e-8 * std::sqrt(block_sum(0, k));
-            if (std::getenv("SVTB_DEBUG_BATCH"))
+            if (debug_batch())
                 for (int k = 0; k < K; ++k)
                     std::fprintf(stderr, "[orth] r0=%lld k=%d |X1|/|X|=%.3e |QtX1|/|X1|=%.3e\n",
                                  static_cast<long long>(r0), k, std::sqrt(block_sum(0, k) / block_sum(2 * W, k)),
                                  std::sqrt(block_sum(W, k) / block_sum(0, k)));
         }
         if (second) gemm(c, K_GEMM, false, m, W, r0, -1.0, Q, ldq, E.CW.get(), W, 1.0, E.XW.get(), W);
-        if (std::getenv("SVTB_DEBUG_BATCH"))
+        if (debug_batch())
             std::fprintf(stderr, "[batch] round0=%d K=%d r0=%lld check=%d second_pass=%d\n", round0, K,
                          static_cast<long long>(r0), need_check ? 1 : 0, second ? 1 : 0);
     }
@@ -771,14 +776,15 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
     gemm(c, K_QR, false, m, W, W, 1.0, E.XW.get(), W, E.RW.get(), W, 0.0, E.X2.get(), W);
     gemm(c, K_QR, true, W, W, m, 1.0, E.X2.get(), W, E.X2.get(), W, 0.0, E.GW.get(), W);
     allreduce(c, E.GW.get(), static_cast<size_t>(W * W));
-    if (std::getenv("SVTB_DEBUG_G2")) {
+    static const bool debug_g2 = std::getenv("SVTB_DEBUG_G2") != nullptr;
+    if (debug_g2) {
         maxabs(c, E.GW.get(), W, W, W, 1.0, dsc(c, S_TMP));
         std::fprintf(stderr, "[g2] W=%lld max|G2-I|=%.3e\n", static_cast<long long>(W), read_scalar(c, S_TMP));
     }
     chol_rinv(c, E.GW.get(), W, E.RW.get(), status, nullptr);
     gemm(c, K_QR, false, m, W, W, 1.0, E.X2.get(), W, E.RW.get(), W, 0.0, Q + r0, ldq);
     if (read_flag(c, F_QRSTAT) != 0) {
-        if (std::getenv("SVTB_DEBUG_BATCH"))
+        if (debug_batch())
             std::fprintf(stderr, "[batch] round0=%d K=%d W=%lld r0=%lld: Cholesky QR failed, sequential rounds\n",
                          round0, K, static_cast<long long>(W), static_cast<long long>(r0));
         return -1;
