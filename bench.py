@@ -74,27 +74,60 @@ def frob(val):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region, in
+    process through NVML (no nvidia-smi process spawns competing with the
+    host thread); falls back to nvidia-smi when NVML is unavailable."""
 
     def __init__(self, index=0):
         self.samples, self.index, self.stop_ev = [], index, threading.Event()
         self.th = None
+        self.max_mhz = None
+
+    def _nvml(self):
+        import pynvml as N
+        N.nvmlInit()
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+        bits = {"hw_slowdown": N.nvmlClocksThrottleReasonHwSlowdown,
+                "hw_thermal_slowdown": getattr(N, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+                "sw_thermal_slowdown": getattr(N, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+                "sw_power_cap": N.nvmlClocksThrottleReasonSwPowerCap}
+
+        def sample():
+            sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+            mask = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            return sm, sorted(k for k, b in bits.items() if mask & b)
+        return sample
+
+    def _smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+        def sample():
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                 timeout=5).stdout.strip()
+            f = [x.strip() for x in out.split(",")]
+            if f[1].replace(".", "").isdigit():
+                self.max_mhz = float(f[1])
+            return float(f[0]), sorted(names[i] for i in range(4) if f[2 + i] == "Active")
+        return sample
 
     def start(self):
+        try:
+            sample = self._nvml()
+        except Exception:
+            sample = self._smi()
+
         def run():
-            q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap")
             while not self.stop_ev.is_set():
                 try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip()
-                    if out:
-                        self.samples.append([x.strip() for x in out.split(",")])
+                    self.samples.append(sample())
                 except Exception:
                     pass
-                self.stop_ev.wait(0.2)
+                self.stop_ev.wait(0.1)
 
         self.th = threading.Thread(target=run, daemon=True)
         self.th.start()
@@ -104,13 +137,11 @@ class ClockSampler:
         if self.th:
             self.th.join(timeout=10)
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].strip() == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"]}
+        sm = [s[0] for s in self.samples]
+        reasons = sorted({r for s in self.samples for r in s[1]})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples)}
 
 
 def measured_peak():

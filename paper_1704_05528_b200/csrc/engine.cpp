@@ -69,7 +69,14 @@ void ensure_cap(Engine& E, QBDev& st, i64 need) {
     SVT_CUDA(cudaMemGetInfo(&free_b, &total_b));
     const double per_col = 8.0 * static_cast<double>(std::max<i64>(1, st.m_local) + st.n);
     const bool roomy = per_col * static_cast<double>(2 * st.cap) < 0.45 * static_cast<double>(free_b);
-    const i64 grown = roomy ? st.cap * 2 : st.cap + st.cap / 4;
+    i64 grown = roomy ? st.cap * 2 : st.cap + st.cap / 4;
+    if (st.cap == 0 && E.mat != nullptr && E.mat->nnz_global >= (1LL << 20)) {
+        // first sketch of a large problem: reserve the whole basis range the
+        // panels can take in ~40 % of free HBM (all of min(m, n) for config
+        // 4: 6.9 GB), so no multi-GB regrow lands inside an SVT iteration
+        // (a fresh device maps new pages slowly)
+        grown = static_cast<i64>(0.4 * static_cast<double>(free_b) / per_col);
+    }
     i64 cap = std::max<i64>(need + 128, std::max<i64>(64, grown));
     cap = std::min<i64>(cap, std::max(st.min_dim, need));
     cap = (cap + 7) & ~7LL;
