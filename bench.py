@@ -365,6 +365,7 @@ def main():
             traffic = None
     roof["traffic"] = traffic
 
+    solver.close()  # release the timed run's basis before the e2e run allocates its own
     # e2e: the public C-ABI call with host buffers: upload + kickstart + K
     # iterations (each reads its record back) + factor download
     e2e = None
@@ -425,7 +426,6 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
-    solver.close()
     if dist:
         dist.barrier()
         dist.destroy_process_group()
