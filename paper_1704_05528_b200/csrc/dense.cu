@@ -1167,6 +1167,30 @@ __global__ void set_flag_kernel(const double* a, const double* b, double coef, i
         flag[0] = (a[0] > coef) ? 1 : 0;
 }
 
+// Per-block decisions of a round batch (K blocks of w columns), one warp:
+// mode 0: flag = some block kept less than thr2 of its squared norm
+//         (after[k] < thr2 * before[k]): the re-check product is needed;
+// mode 1: flag = gate && some block has ||Q^T X_k|| > 1e-8 ||X_k||
+//         (sketch.hpp:134): the second Gram-Schmidt pass is needed.
+__global__ void block_flags_kernel(const double* __restrict__ after, const double* __restrict__ before,
+                                   const double* __restrict__ proj, int K, int w, double thr2, int mode,
+                                   const int* __restrict__ gate, int* __restrict__ flag) {
+    const int lane = threadIdx.x;
+    int hit = 0;
+    if (mode == 0 || *gate != 0) {
+        for (int k = lane; k < K; k += 32) {
+            double a = 0.0, b = 0.0;
+            for (int q = 0; q < w; ++q) {
+                a += after[k * w + q];
+                b += (mode == 0) ? before[k * w + q] : proj[k * w + q];
+            }
+            if (mode == 0 ? !(a >= thr2 * b) : (sqrt(b) > 1e-8 * sqrt(a))) hit = 1;
+        }
+    }
+    hit = __any_sync(0xffffffffu, hit);
+    if (lane == 0) flag[0] = hit;
+}
+
 // ---------------------------------------------------------------------------
 // CholQR: Cholesky + explicit inverse of R = L^T, one CTA, w <= 64
 // ---------------------------------------------------------------------------
@@ -1951,6 +1975,12 @@ void maxabs(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double di
     LaunchScope ls(ctx, K_OTHER, 8.0 * tot, 0.0);
     maxabs_partial_kernel<<<blocks, 256, 0, ctx->stream>>>(X, rows, cols, ld, diag_shift, ctx->ws_partial2.get());
     finish_kernel<<<1, 32, 0, ctx->stream>>>(ctx->ws_partial2.get(), blocks, d_out, 2, nullptr);
+}
+
+void block_flags(svt_ctx* ctx, const double* after, const double* before, const double* proj, int K, int w,
+                 double thr2, int mode, const int* gate, int* flag) {
+    LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
+    block_flags_kernel<<<1, 32, 0, ctx->stream>>>(after, before, proj, K, w, thr2, mode, gate, flag);
 }
 
 void set_flag(svt_ctx* ctx, const double* a, const double* b, double coef, int mode, int* flag) {

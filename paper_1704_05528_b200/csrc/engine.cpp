@@ -26,7 +26,7 @@ namespace {
 
 // scalar / flag slots in ctx->d_scalars / ctx->d_flags
 enum : int { S_FROB = 0, S_NX = 1, S_NC = 2, S_MAXD = 3, S_NB = 4, S_TMP = 5, S_SPEC = 6 };
-enum : int { F_CGS2 = 0, F_REORTH = 1, F_QRSTAT = 2, F_DRIFT = 3, F_BLK = 4 };
+enum : int { F_CGS2 = 0, F_REORTH = 1, F_QRSTAT = 2, F_DRIFT = 3, F_BLK = 4, F_CHECK = 5, F_SECOND = 6 };
 
 double* dsc(svt_ctx* c, int i) { return c->d_scalars + i; }
 int* dfl(svt_ctx* c, int i) { return c->d_flags + i; }
@@ -724,7 +724,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         // block Gram-Schmidt against Q, then the reference's per-round test
         // ||Q^T X_k|| > 1e-8 ||X_k|| for a second pass (sketch.hpp:134).
         // After one pass ||Q^T X_k|| is a rounding residual, at most
-        // at most ~(m + r0) * eps * ||X_k before||; while the projection
+        // ~(m + r0) * eps * ||X_k before||; while the projection
         // keeps more than max(1e-3, 1e8 (m + r0) eps) of every block's norm
         // the test is false with that margin, so the check product Q^T X is
         // only formed when some block lost more (near-dependent rounds).
@@ -737,39 +737,21 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         col_sumsq(c, E.XW.get(), m, W, W, E.eW.get());
         allreduce(c, E.eW.get(), static_cast<size_t>(W));
         allreduce(c, E.eW.get() + 2 * W, static_cast<size_t>(W));
-        std::vector<double> cs(static_cast<size_t>(3 * W));
-        SVT_CUDA(cudaMemcpyAsync(cs.data(), E.eW.get(), sizeof(double) * 3 * W, cudaMemcpyDeviceToHost, c->stream));
-        sync_stream(c);
-        auto block_sum = [&](i64 off, int k) {
-            double t = 0.0;
-            for (i64 q = 0; q < w; ++q) t += cs[static_cast<size_t>(off + k * w + q)];
-            return t;
-        };
-        // worst-case rounding of the two products ~ (m + r0) eps ||X_k||
+        // worst-case rounding of the two products ~ (m + r0) eps ||X_k||;
+        // the decisions are taken on the device (predicated kernels), so the
+        // batch issues no host synchronization here
         const double thr = std::max(1e-3, 1.1e-8 * static_cast<double>(A->m + r0));
-        bool need_check = false;
-        for (int k = 0; k < K && !need_check; ++k)
-            need_check = !(block_sum(0, k) >= thr * thr * block_sum(2 * W, k));
-        bool second = false;
-        if (need_check) {
-            gemm(c, K_GEMM, true, r0, W, m, 1.0, Q, ldq, E.XW.get(), W, 0.0, E.CW.get(), W);
-            allreduce(c, E.CW.get(), static_cast<size_t>(r0 * W));
-            col_sumsq(c, E.CW.get(), r0, W, W, E.eW.get() + W);
-            SVT_CUDA(cudaMemcpyAsync(cs.data() + W, E.eW.get() + W, sizeof(double) * W, cudaMemcpyDeviceToHost,
-                                     c->stream));
-            sync_stream(c);
-            for (int k = 0; k < K && !second; ++k)
-                second = std::sqrt(block_sum(W, k)) > 1e-8 * std::sqrt(block_sum(0, k));
-            if (debug_batch())
-                for (int k = 0; k < K; ++k)
-                    std::fprintf(stderr, "[orth] r0=%lld k=%d |X1|/|X|=%.3e |QtX1|/|X1|=%.3e\n",
-                                 static_cast<long long>(r0), k, std::sqrt(block_sum(0, k) / block_sum(2 * W, k)),
-                                 std::sqrt(block_sum(W, k) / block_sum(0, k)));
-        }
-        if (second) gemm(c, K_GEMM, false, m, W, r0, -1.0, Q, ldq, E.CW.get(), W, 1.0, E.XW.get(), W);
+        block_flags(c, E.eW.get(), E.eW.get() + 2 * W, nullptr, K, static_cast<int>(w), thr * thr, 0, nullptr,
+                    dfl(c, F_CHECK));
+        gemm(c, K_GEMM, true, r0, W, m, 1.0, Q, ldq, E.XW.get(), W, 0.0, E.CW.get(), W, dfl(c, F_CHECK));
+        allreduce(c, E.CW.get(), static_cast<size_t>(r0 * W));
+        col_sumsq(c, E.CW.get(), r0, W, W, E.eW.get() + W);
+        block_flags(c, E.eW.get(), nullptr, E.eW.get() + W, K, static_cast<int>(w), 0.0, 1, dfl(c, F_CHECK),
+                    dfl(c, F_SECOND));
+        gemm(c, K_GEMM, false, m, W, r0, -1.0, Q, ldq, E.CW.get(), W, 1.0, E.XW.get(), W, dfl(c, F_SECOND));
         if (debug_batch())
             std::fprintf(stderr, "[batch] round0=%d K=%d r0=%lld check=%d second_pass=%d\n", round0, K,
-                         static_cast<long long>(r0), need_check ? 1 : 0, second ? 1 : 0);
+                         static_cast<long long>(r0), read_flag(c, F_CHECK), read_flag(c, F_SECOND));
     }
     // one Cholesky QR (twice) of the whole panel: nested spans per block
     E.GW.ensure(static_cast<size_t>(W * W));

@@ -74,6 +74,11 @@ void maxabs(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double di
 // flag[0] = (a[0] > coef)                                    when mode 1
 void set_flag(svt_ctx* ctx, const double* a, const double* b, double coef, int mode, int* flag);
 
+// Round-batch decisions on the device (no host synchronization): mode 0,
+// flag = any block with sum(after_k) < thr2 * sum(before_k); mode 1, flag =
+// *gate && any block with ||proj_k|| > 1e-8 ||after_k|| (sketch.hpp:134).
+void block_flags(svt_ctx* ctx, const double* after, const double* before, const double* proj, int K, int w,
+                 double thr2, int mode, const int* gate, int* flag);
 // Single-CTA Cholesky of the w x w Gram G (w <= 64): Rinv = L^{-T} (upper,
 // row-major, w x w).  status[0] = 1 when a pivot is not safely positive
 // (triggers the Householder fallback).  Skipped when *pred == 0.
