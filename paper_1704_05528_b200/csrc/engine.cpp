@@ -199,15 +199,19 @@ double frob_sq(Engine& E) {
     return read_scalar(c, S_FROB);
 }
 
-void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo) {
+void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo, cudaStream_t stream,
+             DevBuf<double>* scratch) {
     svt_mat* A = E.mat;
-    spmm(E.ctx, K_SPMM, A->plan_csr.v, A->m_local, A->col.get(), E.Y.csr, A->nnz_local, A->n, w, X, ldx, out, ldo);
+    spmm(E.ctx, K_SPMM, A->plan_csr.v, A->m_local, A->col.get(), E.Y.csr, A->nnz_local, A->n, w, X, ldx, out, ldo,
+         stream, scratch);
 }
 
-void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out) {
+void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out, cudaStream_t stream,
+               DevBuf<double>* scratch) {
     svt_mat* A = E.mat;
-    spmm(E.ctx, K_SPMMT, A->plan_csc.v, A->n, A->cscrow.get(), E.Y.csc, A->nnz_local, A->m_local, w, X, ldx, out, w);
-    allreduce(E.ctx, out, static_cast<size_t>(A->n * w));
+    spmm(E.ctx, K_SPMMT, A->plan_csc.v, A->n, A->cscrow.get(), E.Y.csc, A->nnz_local, A->m_local, w, X, ldx, out, w,
+         stream, scratch);
+    E.ctx->comm.allreduce_sum(out, static_cast<size_t>(A->n * w), stream ? stream : E.ctx->stream);
 }
 
 // dense.hpp:103-110 on a panel of any width: CholQR2 (w <= 64) or block
@@ -662,62 +666,77 @@ static void finalize_mode(Engine& E, const QBDev& st, FinalizeMode mode, double 
 // stopping round are discarded.  Returns the number of rounds accepted, or
 // -1 when the panel is numerically rank deficient (the caller re-runs the
 // rounds one by one with the exact fallback semantics).
-static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int round0, int K,
-                           double* last_gain) {
+// Sketch of a batch (Omega for rounds round0 .. round0 + K - 1, then
+// X = Y (Y^T (Y Omega))) into spec slot `slot`, on `stream` (main or side).
+static void batch_sketch(Engine& E, const svt_sketch_params& p, int round0, int K, int slot, bool side) {
     svt_ctx* c = E.ctx;
     svt_mat* A = E.mat;
-    const i64 w = p.dt, W = K * w, m = A->m_local, n = A->n, r0 = st.rank;
-    ensure_cap(E, st, r0 + W);
+    auto& sp = E.spec;
+    const i64 w = p.dt, W = static_cast<i64>(K) * w, m = A->m_local, n = A->n;
+    cudaStream_t s = side ? c->side : c->stream;
+    DevBuf<double>* part = side ? &sp.part : nullptr;
     u64 seeds[kMaxOmegaBatch];
-    E.XW.ensure(static_cast<size_t>(std::max<i64>(1, m) * W));
-    E.TW.ensure(static_cast<size_t>(n * W));
-    auto& pre = E.pre;
-    i64 ldom = W;
-    if (pre.valid && pre.seed == p.seed && pre.round0 == round0 && pre.K >= K && c->side) {
-        // this batch's Omega was generated on the side stream during the
-        // previous batch
-        SVT_CUDA(cudaStreamWaitEvent(c->stream, pre.ready, 0));
-        std::swap(E.OmW, pre.buf);
-        ldom = pre.ld;
-    } else {
-        for (int k = 0; k < K; ++k) seeds[k] = derive_seed_u(p.seed, static_cast<u64>(round0 + k));
-        E.OmW.ensure(static_cast<size_t>(n * W));
-        gaussian_blocks_dev(c, n, w, seeds, K, E.OmW.get(), w, W);
+    for (int k = 0; k < K; ++k) seeds[k] = derive_seed_u(p.seed, static_cast<u64>(round0 + k));
+    sp.om[slot].ensure(static_cast<size_t>(n * W));
+    sp.x[slot].ensure(static_cast<size_t>(std::max<i64>(1, m) * W));
+    sp.t[slot].ensure(static_cast<size_t>(n * W));
+    gaussian_blocks_dev(c, n, w, seeds, K, sp.om[slot].get(), w, W, side);
+    sp_mult(E, W, sp.om[slot].get(), W, sp.x[slot].get(), W, s, part);
+    for (int j = 0; j < p.np; ++j) {  // np <= 1 on this path
+        sp_mult_t(E, W, sp.x[slot].get(), W, sp.t[slot].get(), s, part);
+        sp_mult(E, W, sp.t[slot].get(), W, sp.x[slot].get(), W, s, part);
     }
-    pre.valid = false;
-    sp_mult(E, W, E.OmW.get(), ldom, E.XW.get(), W);
-    // prefetch the next batch's Omega (rounds round0 + K ..) on the side
-    // stream; it overlaps the rest of this batch.  The buffer it writes was
-    // last read by the previous batch's first product, which precedes this
-    // point on the main stream.
+}
+
+static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int round0, int K,
+                           double* last_gain, int K_next) {
+    svt_ctx* c = E.ctx;
+    svt_mat* A = E.mat;
+    auto& sp = E.spec;
+    const i64 w = p.dt, m = A->m_local, n = A->n, r0 = st.rank;
+    static const bool no_spec = std::getenv("SVTB_NO_SPECULATION") != nullptr;
+    const bool use_spec = sp.valid && sp.seed == p.seed && sp.round0 == round0;
+    int slot = 0;
+    if (sp.valid) {
+        // the batch sketched on the side stream during the previous batch
+        // (or a stale one from an ended sketch, drained here)
+        SVT_CUDA(cudaStreamWaitEvent(c->stream, sp.ready, 0));
+        slot = use_spec ? sp.slot : (sp.slot ^ 1);
+        if (use_spec) K = sp.K;
+    }
+    sp.valid = false;
+    const i64 W = static_cast<i64>(K) * w;
+    ensure_cap(E, st, r0 + W);
+    if (!use_spec) batch_sketch(E, p, round0, K, slot, false);
+    // speculative sketch of the next batch (rounds round0 + K ..): it only
+    // needs Omega and Y, so it runs on the side stream concurrently with this
+    // batch's Gram-Schmidt / QR; the replay below decides whether it is used
     const i64 room = (st.min_dim - (r0 + W)) / w;
-    const int Kn = static_cast<int>(std::min<i64>(std::min<i64>(kMaxOmegaBatch, 128 / w), room));
-    static const bool no_prefetch = std::getenv("SVTB_NO_PREFETCH") != nullptr;
-    if (c->side && Kn >= 2 && !no_prefetch) {
-        if (!pre.ready) {
-            SVT_CUDA(cudaEventCreateWithFlags(&pre.ready, cudaEventDisableTiming));
-            SVT_CUDA(cudaEventCreateWithFlags(&pre.consumed, cudaEventDisableTiming));
+    const int Kn = static_cast<int>(std::min<i64>(K_next, room));
+    // (single rank only: NCCL collectives of one communicator must not run
+    // concurrently on two streams)
+    if (c->side && Kn >= 2 && !no_spec && c->comm.world == 1) {
+        if (!sp.ready) {
+            SVT_CUDA(cudaEventCreateWithFlags(&sp.ready, cudaEventDisableTiming));
+            SVT_CUDA(cudaEventCreateWithFlags(&sp.freed[0], cudaEventDisableTiming));
+            SVT_CUDA(cudaEventCreateWithFlags(&sp.freed[1], cudaEventDisableTiming));
+            SVT_CUDA(cudaEventRecord(sp.freed[0], c->stream));
+            SVT_CUDA(cudaEventRecord(sp.freed[1], c->stream));
         }
-        const i64 Wn = static_cast<i64>(Kn) * w;
-        SVT_CUDA(cudaEventRecord(pre.consumed, c->stream));
-        SVT_CUDA(cudaStreamWaitEvent(c->side, pre.consumed, 0));
-        if (pre.buf.n < static_cast<size_t>(n * Wn)) {
-            SVT_CUDA(cudaStreamSynchronize(c->side));
-            pre.buf.ensure(static_cast<size_t>(n * Wn));
-        }
-        for (int k = 0; k < Kn; ++k) seeds[k] = derive_seed_u(p.seed, static_cast<u64>(round0 + K + k));
-        gaussian_blocks_dev(c, n, w, seeds, Kn, pre.buf.get(), w, Wn, true);
-        SVT_CUDA(cudaEventRecord(pre.ready, c->side));
-        pre.valid = true;
-        pre.seed = p.seed;
-        pre.round0 = round0 + K;
-        pre.K = Kn;
-        pre.ld = Wn;
+        const int ns = slot ^ 1;
+        // buffers of slot ns are free once the main stream is done with the
+        // batch that used them; regrowth (cudaFree) synchronizes the device
+        SVT_CUDA(cudaStreamWaitEvent(c->side, sp.freed[ns], 0));
+        batch_sketch(E, p, round0 + K, Kn, ns, true);
+        SVT_CUDA(cudaEventRecord(sp.ready, c->side));
+        sp.valid = true;
+        sp.seed = p.seed;
+        sp.round0 = round0 + K;
+        sp.K = Kn;
+        sp.slot = ns;
     }
-    for (int j = 0; j < p.np; ++j) {  // np == 1 here (np >= 2 rounds run one by one)
-        sp_mult_t(E, W, E.XW.get(), W, E.TW.get());
-        sp_mult(E, W, E.TW.get(), W, E.XW.get(), W);
-    }
+    double* XW = sp.x[slot].get();
+    E.TW.ensure(static_cast<size_t>(n * W));
     double* Q = st.Q.get();
     const i64 ldq = st.cap;
     if (r0 > 0) {
@@ -730,11 +749,11 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         // only formed when some block lost more (near-dependent rounds).
         E.CW.ensure(static_cast<size_t>(r0 * W));
         E.eW.ensure(static_cast<size_t>(3 * W));
-        col_sumsq(c, E.XW.get(), m, W, W, E.eW.get() + 2 * W);
-        gemm(c, K_GEMM, true, r0, W, m, 1.0, Q, ldq, E.XW.get(), W, 0.0, E.CW.get(), W);
+        col_sumsq(c, XW, m, W, W, E.eW.get() + 2 * W);
+        gemm(c, K_GEMM, true, r0, W, m, 1.0, Q, ldq, XW, W, 0.0, E.CW.get(), W);
         allreduce(c, E.CW.get(), static_cast<size_t>(r0 * W));
-        gemm(c, K_GEMM, false, m, W, r0, -1.0, Q, ldq, E.CW.get(), W, 1.0, E.XW.get(), W);
-        col_sumsq(c, E.XW.get(), m, W, W, E.eW.get());
+        gemm(c, K_GEMM, false, m, W, r0, -1.0, Q, ldq, E.CW.get(), W, 1.0, XW, W);
+        col_sumsq(c, XW, m, W, W, E.eW.get());
         allreduce(c, E.eW.get(), static_cast<size_t>(W));
         allreduce(c, E.eW.get() + 2 * W, static_cast<size_t>(W));
         // worst-case rounding of the two products ~ (m + r0) eps ||X_k||;
@@ -743,12 +762,12 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         const double thr = std::max(1e-3, 1.1e-8 * static_cast<double>(A->m + r0));
         block_flags(c, E.eW.get(), E.eW.get() + 2 * W, nullptr, K, static_cast<int>(w), thr * thr, 0, nullptr,
                     dfl(c, F_CHECK));
-        gemm(c, K_GEMM, true, r0, W, m, 1.0, Q, ldq, E.XW.get(), W, 0.0, E.CW.get(), W, dfl(c, F_CHECK));
+        gemm(c, K_GEMM, true, r0, W, m, 1.0, Q, ldq, XW, W, 0.0, E.CW.get(), W, dfl(c, F_CHECK));
         allreduce(c, E.CW.get(), static_cast<size_t>(r0 * W));
         col_sumsq(c, E.CW.get(), r0, W, W, E.eW.get() + W);
         block_flags(c, E.eW.get(), nullptr, E.eW.get() + W, K, static_cast<int>(w), 0.0, 1, dfl(c, F_CHECK),
                     dfl(c, F_SECOND));
-        gemm(c, K_GEMM, false, m, W, r0, -1.0, Q, ldq, E.CW.get(), W, 1.0, E.XW.get(), W, dfl(c, F_SECOND));
+        gemm(c, K_GEMM, false, m, W, r0, -1.0, Q, ldq, E.CW.get(), W, 1.0, XW, W, dfl(c, F_SECOND));
         if (debug_batch())
             std::fprintf(stderr, "[batch] round0=%d K=%d r0=%lld check=%d second_pass=%d\n", round0, K,
                          static_cast<long long>(r0), read_flag(c, F_CHECK), read_flag(c, F_SECOND));
@@ -759,10 +778,11 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
     E.X2.ensure(static_cast<size_t>(std::max<i64>(1, m) * W));
     zero_flag(c, F_QRSTAT);
     int* status = dfl(c, F_QRSTAT);
-    gemm(c, K_QR, true, W, W, m, 1.0, E.XW.get(), W, E.XW.get(), W, 0.0, E.GW.get(), W);
+    gemm(c, K_QR, true, W, W, m, 1.0, XW, W, XW, W, 0.0, E.GW.get(), W);
     allreduce(c, E.GW.get(), static_cast<size_t>(W * W));
     chol_rinv(c, E.GW.get(), W, E.RW.get(), status, nullptr);
-    gemm(c, K_QR, false, m, W, W, 1.0, E.XW.get(), W, E.RW.get(), W, 0.0, E.X2.get(), W);
+    gemm(c, K_QR, false, m, W, W, 1.0, XW, W, E.RW.get(), W, 0.0, E.X2.get(), W);
+    if (sp.freed[slot]) SVT_CUDA(cudaEventRecord(sp.freed[slot], c->stream));  // XW is dead from here
     gemm(c, K_QR, true, W, W, m, 1.0, E.X2.get(), W, E.X2.get(), W, 0.0, E.GW.get(), W);
     allreduce(c, E.GW.get(), static_cast<size_t>(W * W));
     static const bool debug_g2 = std::getenv("SVTB_DEBUG_G2") != nullptr;
@@ -835,12 +855,18 @@ static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, Fina
                 est = std::max(est, static_cast<int>(std::min(1e6, std::ceil(need))) + 1);
             }
             const int K = std::min(kmax, est);
-            if (K >= 2) {
-                const double nb0 = st.norm_b_sq;
-                const int acc = qb_extend_batch(E, st, p, rounds + 1, K, &last_gain);
+            // a batch already sketched on the side stream for this round
+            // is used whatever the current estimate
+            const bool spec_here = E.spec.valid && E.spec.seed == p.seed && E.spec.round0 == rounds + 1;
+            if (K >= 2 || spec_here) {
+                // size of the batch after this one if all of this one's
+                // rounds are accepted (same estimate, K rounds later)
+                const int Kb = spec_here ? E.spec.K : K;
+                const int est_next = est - Kb;
+                const int K_next = std::min<int>(static_cast<int>(std::min<i64>(kMaxOmegaBatch, 128 / p.dt)), est_next);
+                const int acc = qb_extend_batch(E, st, p, rounds + 1, K, &last_gain, K_next);
                 if (acc > 0) {
                     rounds += acc;
-                    (void)nb0;
                     continue;
                 }
             }

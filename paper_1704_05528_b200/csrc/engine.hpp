@@ -77,16 +77,18 @@ struct Engine {
     DevBuf<double> Om, OmBank, X, X2, P, T, C, D, G, Rinv, hh, tmp, W, lam, Vraw, Wk;
     DevBuf<double> fkZ, fkZq, fkZt, fkWn, fkH, fkYh, fkth, fkZY, fkXr, fkres;  // finalize_kept
     DevBuf<double> OmW, XW, TW, CW, GW, RW, eW;  // speculative round batches
-    // Omega of the next batch, generated on ctx->side while the current
-    // batch runs (its rounds' seeds do not depend on the data)
-    struct OmegaPrefetch {
-        DevBuf<double> buf;
-        bool valid = false;
+    // Speculative sketch of the next round batch (Omega + the power-iteration
+    // products, which do not depend on the basis) computed on ctx->side while
+    // the current batch's Gram-Schmidt / QR run on the main stream.  Two
+    // buffer slots alternate between the batch in flight and the next one.
+    struct SpecSketch {
+        DevBuf<double> om[2], x[2], t[2];
+        DevBuf<double> part;  // long-row partials of the side-stream SpMMs
+        bool valid = false;   // a speculative batch is in flight / ready
         u64 seed = 0;
-        int round0 = 0, K = 0;
-        i64 ld = 0;
-        cudaEvent_t ready = nullptr, consumed = nullptr;
-    } pre;
+        int round0 = 0, K = 0, slot = 0;
+        cudaEvent_t ready = nullptr, freed[2] = {nullptr, nullptr};
+    } spec;
     DevBuf<int> perm;
     QBDev qb;  // persistent QB storage: capacity survives across SVT iterations
     bool batching = true;  // speculative multi-round batches (exact-arithmetic equivalent)
@@ -96,18 +98,23 @@ struct Engine {
     Engine& operator=(const Engine&) = delete;
     Engine(Engine&&) = delete;
     ~Engine() {
-        if (pre.ready || pre.consumed) {
+        if (spec.ready) {
             if (ctx && ctx->side) cudaStreamSynchronize(ctx->side);
-            if (pre.ready) cudaEventDestroy(pre.ready);
-            if (pre.consumed) cudaEventDestroy(pre.consumed);
+            cudaEventDestroy(spec.ready);
+            cudaEventDestroy(spec.freed[0]);
+            cudaEventDestroy(spec.freed[1]);
         }
     }
 };
 
 // primitives
 double frob_sq(Engine& E);  // ||Y||_F^2 (all ranks)
-void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo);          // Y X (local rows)
-void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out /* n x w, ld w */);  // Y^T X (allreduced)
+// Y X (local rows) / Y^T X (n x w, ld w, all-reduced); stream / scratch:
+// optional launch on another stream with its own long-row partial buffer
+void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo, cudaStream_t stream = nullptr,
+             DevBuf<double>* scratch = nullptr);
+void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out, cudaStream_t stream = nullptr,
+               DevBuf<double>* scratch = nullptr);
 void qr_orthonormal(Engine& E, double* X, i64 ldx, i64 w, double* Qout, i64 ldq);            // dense.hpp:103
 void qr_orthonormal(Engine& E, i64 rows, bool dist, double* X, i64 ldx, i64 w, double* Qout, i64 ldq);
 double spectral_norm_est(Engine& E, int iters, u64 seed);                                   // sampled.hpp:188

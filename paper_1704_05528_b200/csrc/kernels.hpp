@@ -27,8 +27,11 @@ void gaussian_blocks_dev(svt_ctx* ctx, i64 rows, i64 cols, const u64* seeds, int
 // kernel with the respective arrays.
 // nnz and x_rows only feed the algorithmic-bytes accounting (SURVEY §8d:
 // 12 B per entry + 8 B per row pointer + panel in + panel out).
+// stream / scratch (optional): launch on another stream with its own
+// long-row partial buffer (a speculative batch on ctx->side).
 void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* idx, const double* val, i64 nnz,
-          i64 x_rows, i64 w, const double* X, i64 ldx, double* out, i64 ldo);
+          i64 x_rows, i64 w, const double* X, i64 ldx, double* out, i64 ldo, cudaStream_t stream = nullptr,
+          DevBuf<double>* scratch = nullptr);
 
 // Fused SDDMM + Bregman update + reductions (sampled.hpp:148-176,
 // solver.hpp:143-168, 321-323).  For each stored (i, j):

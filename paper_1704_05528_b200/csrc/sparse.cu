@@ -214,11 +214,11 @@ __global__ void __launch_bounds__(32 * kSegRedWarps) seg_reduce_wide_kernel(SegP
 }
 
 template <int W>
-void launch_narrow(svt_ctx* ctx, const SegPlanView& plan, const int* idx, const double* val, const double* X,
-                   i64 ldx, double* out, i64 ldo, double* partial) {
+void launch_narrow(svt_ctx* ctx, cudaStream_t s, const SegPlanView& plan, const int* idx, const double* val,
+                   const double* X, i64 ldx, double* out, i64 ldo, double* partial) {
+    (void)ctx;
     const unsigned blocks = static_cast<unsigned>((plan.nseg + kWarpsPerBlock - 1) / kWarpsPerBlock);
-    spmm_narrow_kernel<W><<<blocks, 32 * kWarpsPerBlock, 0, ctx->stream>>>(plan, idx, val, X, ldx, out, ldo,
-                                                                         partial);
+    spmm_narrow_kernel<W><<<blocks, 32 * kWarpsPerBlock, 0, s>>>(plan, idx, val, X, ldx, out, ldo, partial);
 }
 
 // ---- fused SDDMM + Bregman update + reductions ------------------------------
@@ -320,22 +320,25 @@ __global__ void densify_kernel(long long m_local, long long n, const long long* 
 }  // namespace
 
 void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* idx, const double* val, i64 nnz,
-          i64 x_rows, i64 w, const double* X, i64 ldx, double* out, i64 ldo) {
+          i64 x_rows, i64 w, const double* X, i64 ldx, double* out, i64 ldo, cudaStream_t stream,
+          DevBuf<double>* scratch) {
     if (nrows <= 0 || w <= 0) return;
+    cudaStream_t s = stream ? stream : ctx->stream;
+    DevBuf<double>& part = scratch ? *scratch : ctx->ws_spmm;
     // algorithmic bytes: 12 B per stored entry (int32 index +
     // fp64 value) + 8 B per row pointer + the dense panel read once + the
     // output panel written once; 2 flops per entry per column.
-    LaunchScope ls(ctx, cls, 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * w * (x_rows + nrows), 2.0 * nnz * w);
+    LaunchScope ls(ctx, cls, 12.0 * nnz + 8.0 * (nrows + 1) + 8.0 * w * (x_rows + nrows), 2.0 * nnz * w, s);
     double* partial = nullptr;
     if (plan.nlong > 0) {
-        ctx->ws_spmm.ensure(static_cast<size_t>(plan.nslots * w));
-        partial = ctx->ws_spmm.get();
+        part.ensure(static_cast<size_t>(plan.nslots * w));
+        partial = part.get();
     }
     if (w <= 16) {
         switch (w) {
 #define SVT_CASE(W)                                                             \
     case W:                                                                     \
-        launch_narrow<W>(ctx, plan, idx, val, X, ldx, out, ldo, partial);       \
+        launch_narrow<W>(ctx, s, plan, idx, val, X, ldx, out, ldo, partial);       \
         break;
             SVT_CASE(1) SVT_CASE(2) SVT_CASE(3) SVT_CASE(4) SVT_CASE(5) SVT_CASE(6) SVT_CASE(7) SVT_CASE(8)
             SVT_CASE(9) SVT_CASE(10) SVT_CASE(11) SVT_CASE(12) SVT_CASE(13) SVT_CASE(14) SVT_CASE(15) SVT_CASE(16)
@@ -346,16 +349,16 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
     } else {
         const unsigned nb = static_cast<unsigned>((plan.nseg + 3) / 4);
         if (w <= 32)
-            spmm_wide_kernel<1, 16><<<dim3(nb, 1), 128, 0, ctx->stream>>>(plan, idx, val, X, ldx, w, out, ldo,
+            spmm_wide_kernel<1, 16><<<dim3(nb, 1), 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo,
                                                                           partial);
         else if (w <= 64)
-            spmm_wide_kernel<2, 8><<<dim3(nb, 1), 128, 0, ctx->stream>>>(plan, idx, val, X, ldx, w, out, ldo,
+            spmm_wide_kernel<2, 8><<<dim3(nb, 1), 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo,
                                                                          partial);
         else if (w <= 96)
-            spmm_wide_kernel<3, 5><<<dim3(nb, 1), 128, 0, ctx->stream>>>(plan, idx, val, X, ldx, w, out, ldo,
+            spmm_wide_kernel<3, 5><<<dim3(nb, 1), 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo,
                                                                          partial);
         else
-            spmm_wide_kernel<4, 4><<<dim3(nb, static_cast<unsigned>((w + 127) / 128)), 128, 0, ctx->stream>>>(
+            spmm_wide_kernel<4, 4><<<dim3(nb, static_cast<unsigned>((w + 127) / 128)), 128, 0, s>>>(
                 plan, idx, val, X, ldx, w, out, ldo, partial);
     }
     if (plan.nlong > 0) {
@@ -369,11 +372,11 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
                     attr = true;
                 }
             }
-            seg_reduce_wide_kernel<<<static_cast<unsigned>(plan.nlong), 32 * kSegRedWarps, smem, ctx->stream>>>(
+            seg_reduce_wide_kernel<<<static_cast<unsigned>(plan.nlong), 32 * kSegRedWarps, smem, s>>>(
                 plan, w, partial, out, ldo);
         } else {
             const i64 thr = plan.nlong * 32;
-            seg_reduce_kernel<<<static_cast<unsigned>((thr + 255) / 256), 256, 0, ctx->stream>>>(plan, w, partial,
+            seg_reduce_kernel<<<static_cast<unsigned>((thr + 255) / 256), 256, 0, s>>>(plan, w, partial,
                                                                                               out, ldo);
         }
     }
