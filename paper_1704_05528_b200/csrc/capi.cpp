@@ -1,6 +1,7 @@
 // The C ABI (include/svt_b200.h).  Every entry point catches and maps the
 // engine's exceptions to the status codes that correspond to the reference's
 // exception types; messages are kept per thread for svt_last_error().
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -106,8 +107,14 @@ int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, sv
         SVT_CUDA(cudaSetDevice(device));
         auto c = std::make_unique<svt_ctx>();
         c->device = device;
-        SVT_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-        SVT_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+        // the main stream carries the critical path (Gram-Schmidt / QR of the
+        // batch in flight); the side stream's speculative sketch fills the
+        // SMs it leaves idle: give the main stream the higher priority
+        int prio_lo = 0, prio_hi = 0;
+        SVT_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        static const bool flat = std::getenv("SVTB_FLAT_PRIORITY") != nullptr;
+        SVT_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, flat ? prio_lo : prio_hi));
+        SVT_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo));
         SVT_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
         SVT_CUDA(cudaMallocHost(&c->h_scalars, 64 * sizeof(double)));
         SVT_CUDA(cudaMallocHost(&c->h_flags, 64 * sizeof(int)));
