@@ -459,7 +459,11 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
     out.n = n;
     out.k = 0;
     out.sigma.clear();
-    if (r <= 48) {
+    // small bases, or bases of which a large share is kept (the subspace
+    // iteration would span most of the space anyway, and the pairs crowd
+    // against the threshold where its residual criterion converges slowest):
+    // the dense Gram eigensolve, exact to rounding
+    if (r <= 48 || (r <= 1024 && 4 * (s_warm + 16) >= r)) {
         finalize(E, st, FinalizeMode::Kept, tau, out);
         return;
     }
@@ -647,7 +651,8 @@ static void check_sketch_params(const svt_sketch_params& p) {
 
 static void finalize_mode(Engine& E, const QBDev& st, FinalizeMode mode, double tau, i64 s_warm, u64 seed,
                           DevFactors& out) {
-    if (mode == FinalizeMode::Kept)
+    static const bool dense = std::getenv("SVTB_FINALIZE_DENSE") != nullptr;  // debug: Gram eigensolve
+    if (mode == FinalizeMode::Kept && !dense)
         finalize_kept(E, st, tau, s_warm, seed, out);
     else
         finalize(E, st, mode, tau, out);

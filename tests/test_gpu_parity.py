@@ -583,3 +583,27 @@ def test_full_size_batched_equals_sequential_and_is_deterministic(config, iters)
     np.testing.assert_allclose(rb.U.T @ rb.U, np.eye(k), atol=1e-10)
     Vn = rb.V / np.linalg.norm(rb.V, axis=0)
     np.testing.assert_allclose(Vn.T @ Vn, np.eye(k), atol=1e-10)
+
+
+# ---- BASELINE configs 1-3 at full size against the oracle ---------------------------
+@pytest.mark.parametrize("config,iters", [(1, 2), (2, 8), (3, 4)])
+def test_baseline_config_matches_oracle(config, iters):
+    """The BASELINE.json configurations the oracle can run in seconds, at
+    their full sizes: revealed rank, kept rank and extension rounds exact per
+    iteration; residual / train MAE / relative residual and held-out
+    MAE / RMSE to 1e-8; final singular values and completed matrix to 1e-8."""
+    d = G.synth_config(config, 1)
+    m, n = d["m"], d["n"]
+    rp, co, va = G.build_csr(m, n, *d["train"])
+    S = O.Csr(m, n, rp, co, va)
+    T = O.Csr(m, n, *G.build_csr(m, n, *d["test"])) if d["test"] is not None else None
+    cfg, stop = G.config_params(config, int(rp[-1]), m, n, float(np.sqrt(np.sum(va * va))))
+    cfg.maxit = iters
+    g = G.svt_run(gpu_mat(S), cfg, stop, test=gpu_mat(T) if T is not None else None)
+    o = O.svt_run(S, cfg, stop, test=T)
+    assert len(o.trace) == iters
+    check_runs(g, o)
+    if T is not None:
+        for a, b in zip(g.trace, o.trace):
+            assert abs(a["test_rmse"] - b["test_rmse"]) <= 1e-8 * b["test_rmse"]
+            assert abs(a["test_mae"] - b["test_mae"]) <= 1e-8 * b["test_mae"]
