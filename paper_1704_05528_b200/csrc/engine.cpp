@@ -651,7 +651,7 @@ static void check_sketch_params(const svt_sketch_params& p) {
 
 static void finalize_mode(Engine& E, const QBDev& st, FinalizeMode mode, double tau, i64 s_warm, u64 seed,
                           DevFactors& out) {
-    static const bool dense = std::getenv("SVTB_FINALIZE_DENSE") != nullptr;  // debug: Gram eigensolve
+    const bool dense = std::getenv("SVTB_FINALIZE_DENSE") != nullptr;  // per sketch; test / debug switch
     if (mode == FinalizeMode::Kept && !dense)
         finalize_kept(E, st, tau, s_warm, seed, out);
     else

@@ -607,3 +607,20 @@ def test_baseline_config_matches_oracle(config, iters):
         for a, b in zip(g.trace, o.trace):
             assert abs(a["test_rmse"] - b["test_rmse"]) <= 1e-8 * b["test_rmse"]
             assert abs(a["test_mae"] - b["test_mae"]) <= 1e-8 * b["test_mae"]
+
+
+@pytest.mark.parametrize("config,iters", [(4, 3)])
+def test_kept_finalize_matches_dense_finalize_full_size(config, iters, monkeypatch):
+    """Config 4 is beyond the oracle's reach; the kept-mode finalize
+    (Chebyshev-accelerated Rayleigh-Ritz on G = B B^T) is checked against the
+    dense Gram eigensolve (cooperative Jacobi on the full r x r Gram) on the
+    same iterations: identical ranks / rounds / kept ranks, residual and MAE
+    to 1e-8."""
+    _, kept, rk = _config_solver(config, iters)
+    monkeypatch.setenv("SVTB_FINALIZE_DENSE", "1")
+    _, dense, rd = _config_solver(config, iters)
+    for a, b in zip(kept, dense):
+        assert (a["rank"], a["extension_rounds"], a["kept"]) == (b["rank"], b["extension_rounds"], b["kept"])
+        for key in ("residual", "train_mae", "rel_residual_x"):
+            assert abs(a[key] - b[key]) <= 1e-8 * abs(b[key]), (key, a[key], b[key])
+    np.testing.assert_allclose(rk.sigma, rd.sigma, rtol=1e-8)
