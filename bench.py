@@ -225,7 +225,7 @@ def run_reference(args, rank, world):
     print(json.dumps({
         "metric": "SVT iters/sec (R4SVD)", "value": value, "unit": "iter/s", "n_gpus": world, "steps": len(timed),
         "warmup": min(args.warmup, len(d)), "ms_per_step": 1000.0 / value, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
         "config": {"workload": CONFIG_NAMES[args.config], "config": args.config, "m": m, "n": n,
                    "nnz": int(rp[-1]), "parallelism": "single CPU thread (reference has no threads)"},
         "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "port", "sample": sample},
@@ -406,7 +406,7 @@ def main():
         line = {
             "metric": "SVT iters/sec (R4SVD)", "value": value, "unit": "iter/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": CONFIG_NAMES[args.config], "config": args.config, "m": m, "n": n,
                        "nnz": int(rp[-1]), "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU",
                        "iterations_timed": [r["iter"] for r in recs], "revealed_rank": [r["rank"] for r in recs],
