@@ -269,6 +269,7 @@ int build_sampled_device(svt_ctx* ctx, svt_mat* M, const long long* col64) {
         csc_fill_kernel<<<nb(nnz), 256, 0, s>>>(nnz, perm.get(), rid.get(), M->val.get(), M->cscrow.get(),
                                                 M->val_csc.get(), M->csr2csc.get());
     }
+    M->csc2csr = std::move(perm);  // the stable sort's permutation is the CSC -> CSR map
     {
         LaunchScope ls(ctx, K_OTHER, 8.0 * (n + 1), 0.0);
         colptr_kernel<<<nb(n + 1), 256, 0, s>>>(nnz, n, sorted_col.get(),

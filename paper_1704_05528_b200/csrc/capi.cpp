@@ -688,7 +688,7 @@ int svt_project_low_rank(svt_mat* P, int64_t k, const double* U, const double* s
             for (i64 i = 0; i < P->n; ++i) vs[static_cast<size_t>(i + j * P->n)] = V[i + j * P->n] * sigma[j];
         DevBuf<double> dV = upload_cm(c, vs.data(), P->n, k);
         DevBuf<double> out(static_cast<size_t>(std::max<i64>(1, P->nnz_local)));
-        sddmm_update(c, P->m_local, P->rowptr.get(), P->col.get(), P->val.get(), out.get(), nullptr, nullptr,
+        sddmm_update(c, P->plan_csr.v, P->m_local, P->col.get(), P->val.get(), out.get(), nullptr, nullptr,
                      P->nnz_local, P->n, dU.get(), k, dV.get(), k, k, 0.0, 2, c->d_scalars + 40);
         SVT_CUDA(cudaMemcpyAsync(out_vals, out.get(), sizeof(double) * P->nnz_local, cudaMemcpyDeviceToHost, c->stream));
         sync_stream(c);

@@ -31,6 +31,7 @@ struct svt_mat {
     svtb::DevBuf<int> cscrow;
     svtb::DevBuf<double> val_csc;
     svtb::DevBuf<int> csr2csc;
+    svtb::DevBuf<int> csc2csr;  // inverse permutation (CSC position -> CSR entry)
 };
 
 namespace svtb {

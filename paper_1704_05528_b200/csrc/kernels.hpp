@@ -41,10 +41,12 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
 //   mode 2: Y = p                                          [project_low_rank]
 //   mode 0: no write                                       [held-out metrics]
 // sums[0..3] (device) = sum|d|, sum d^2, sum (A - y_old)^2, sum Y_out^2.
-void sddmm_update(svt_ctx* ctx, i64 m_local, const i64* rowptr, const int* col, const double* A, double* Y,
+void sddmm_update(svt_ctx* ctx, const SegPlanView& plan, i64 m_local, const int* col, const double* A, double* Y,
                   double* Ycsc, const int* csr2csc, i64 nnz, i64 n, const double* U, i64 ldu, const double* Vs,
                   i64 ldv, i64 k, double delta, int mode, double* d_sums4);
 
+// Ycsc[p] = Y[csc2csr[p]]: rebuild the CSC value mirror after an update
+void mirror_csc(svt_ctx* ctx, i64 nnz, const int* csc2csr, const double* Y, double* Ycsc);
 // vals_out = alpha * vals_in (and the CSC mirror through csr2csc when given)
 void scale_values(svt_ctx* ctx, i64 nnz, const double* in, double alpha, double* out, const int* csr2csc,
                   double* out_csc);

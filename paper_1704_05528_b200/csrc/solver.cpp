@@ -191,13 +191,17 @@ void solver_step(svt_solver* S, svt_observer_fn obs, void* user, svt_record* rec
         copy2d(c, X.V.get(), k, S->Vs.get(), k, A->n, k);
         scale_cols(c, S->Vs.get(), A->n, k, k, X.d_sigma.get());
     }
-    sddmm_update(c, A->m_local, A->rowptr.get(), A->col.get(), A->val.get(), S->Ycsr.get(), S->Ycsc.get(),
-                 A->csr2csc.get(), A->nnz_local, A->n, X.U.get(), k, S->Vs.get(), k, k, cfg.delta, 1,
-                 c->d_scalars + S_SUMS);
+    // with the inverse permutation the CSC mirror is rebuilt by a coalesced
+    // gather pass instead of a scattered write inside the update
+    const bool gather = A->csc2csr.n > 0 && A->nnz_local > 0;
+    sddmm_update(c, A->plan_csr.v, A->m_local, A->col.get(), A->val.get(), S->Ycsr.get(),
+                 gather ? nullptr : S->Ycsc.get(), A->csr2csc.get(), A->nnz_local, A->n, X.U.get(), k, S->Vs.get(),
+                 k, k, cfg.delta, 1, c->d_scalars + S_SUMS);
+    if (gather) mirror_csc(c, A->nnz_local, A->csc2csr.get(), S->Ycsr.get(), S->Ycsc.get());
     c->comm.allreduce_sum(c->d_scalars + S_SUMS, 4, c->stream);
     if (S->test != nullptr) {
         svt_mat* T = S->test;
-        sddmm_update(c, T->m_local, T->rowptr.get(), T->col.get(), T->val.get(), T->val.get(), nullptr, nullptr,
+        sddmm_update(c, T->plan_csr.v, T->m_local, T->col.get(), T->val.get(), T->val.get(), nullptr, nullptr,
                      T->nnz_local, T->n, X.U.get(), k, S->Vs.get(), k, k, 0.0, 0, c->d_scalars + S_TSUMS);
         c->comm.allreduce_sum(c->d_scalars + S_TSUMS, 4, c->stream);
     }

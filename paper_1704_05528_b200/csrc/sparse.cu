@@ -223,43 +223,195 @@ void launch_narrow(svt_ctx* ctx, cudaStream_t s, const SegPlanView& plan, const 
 
 // ---- fused SDDMM + Bregman update + reductions ------------------------------
 constexpr int kSddmmWarps = 8;
+constexpr int kSddmmU = 4;  // entries per lane group in flight
 
+// Fused SDDMM + Bregman update + reductions, one warp per row.  The warp is
+// G = 32 / KP groups of KP lanes (KP = the kept rank k rounded up to a power
+// of two, at most 32); group g takes every G-th stored entry of the row and
+// its lanes split the k-long dot product U[i,:] . Vs[j,:], so each factor row
+// is read with coalesced loads (a lane-per-entry loop would touch 32
+// different rows per load instruction).  The group's partial products are
+// reduced with shuffles; the group leader applies the update and the sums.
+template <int KP>
 __global__ void __launch_bounds__(32 * kSddmmWarps) sddmm_update_kernel(
-    long long m_local, const long long* __restrict__ rowptr, const int* __restrict__ col,
+    SegPlanView plan, const int* __restrict__ col,
     const double* __restrict__ A, double* __restrict__ Y, double* __restrict__ Ycsc,
     const int* __restrict__ csr2csc, const double* __restrict__ U, long long ldu, const double* __restrict__ Vs,
     long long ldv, long long k, double delta, int mode, double* __restrict__ partials) {
+    constexpr int G = 32 / KP;
+    __shared__ double red[kSddmmWarps][4];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int g = lane / KP, j0 = lane % KP;
+    double s_abs = 0.0, s_sq = 0.0, s_res = 0.0, s_y = 0.0;
+    // grid-stride over the SpMM's row segments (<= kSegLen entries each), so
+    // power-law rows do not leave the CTA's other warps idle at the barrier
+    for (long long sg = static_cast<long long>(blockIdx.x) * kSddmmWarps + warp; sg < plan.nseg;
+         sg += static_cast<long long>(gridDim.x) * kSddmmWarps) {
+        const long long row = plan.seg_row[sg];
+        const long long beg = plan.seg_beg[sg], end = plan.seg_end[sg];
+        const double* ur = U + row * ldu;
+        // kSddmmU entries per group per step: independent dot products in flight
+        for (long long e0 = beg; e0 < end; e0 += static_cast<long long>(G) * kSddmmU) {
+            double p[kSddmmU], av[kSddmmU], yv[kSddmmU];
+            int cc[kSddmmU];
+#pragma unroll
+            for (int u = 0; u < kSddmmU; ++u) {
+                const long long e = e0 + static_cast<long long>(u) * G + g;
+                cc[u] = (e < end) ? __ldg(col + e) : -1;
+                // the applying lane's A / Y are loaded up front, overlapping
+                // the factor-row gathers
+                const bool own = e < end && j0 == (u % KP);
+                av[u] = own ? __ldg(A + e) : 0.0;
+                yv[u] = own ? Y[e] : 0.0;
+            }
+            if (k <= KP) {
+                // one dimension per lane: unconditional, independent loads
+                // (clamped indices, zero multiplier) so the kSddmmU entries'
+                // gathers overlap instead of serializing on branches
+                const int jl = (j0 < k) ? j0 : 0;
+                const double uj = (j0 < k) ? __ldg(ur + jl) : 0.0;
+#pragma unroll
+                for (int u = 0; u < kSddmmU; ++u)
+                    p[u] = uj * __ldg(Vs + static_cast<long long>(max(cc[u], 0)) * ldv + jl);
+            } else {
+#pragma unroll
+                for (int u = 0; u < kSddmmU; ++u) {
+                    p[u] = 0.0;
+                    if (cc[u] >= 0) {
+                        const double* vr = Vs + static_cast<long long>(cc[u]) * ldv;
+                        for (long long jj = j0; jj < k; jj += KP) p[u] = fma(__ldg(ur + jj), __ldg(vr + jj), p[u]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kSddmmU; ++u)
+#pragma unroll
+                for (int o = KP / 2; o > 0; o >>= 1) p[u] += __shfl_xor_sync(0xffffffffu, p[u], o);
+            // the update of entry u is applied by lane u % KP of its group
+#pragma unroll
+            for (int u = 0; u < kSddmmU; ++u) {
+                const long long e = e0 + static_cast<long long>(u) * G + g;
+                if (e >= end || j0 != (u % KP)) continue;
+                const double a = av[u];
+                const double y_old = yv[u];
+                const double d = a - p[u];
+                s_abs += fabs(d);
+                s_sq = fma(d, d, s_sq);
+                const double r = a - y_old;
+                s_res = fma(r, r, s_res);
+                if (mode == 1) {
+                    const double y_new = fma(delta, d, y_old);
+                    Y[e] = y_new;
+                    if (Ycsc) Ycsc[csr2csc[e]] = y_new;
+                    s_y = fma(y_new, y_new, s_y);
+                } else if (mode == 2) {
+                    Y[e] = p[u];
+                    s_y = fma(p[u], p[u], s_y);
+                } else {
+                    s_y = fma(y_old, y_old, s_y);
+                }
+            }
+        }
+    }
+    s_abs = warp_sum(s_abs);
+    s_sq = warp_sum(s_sq);
+    s_res = warp_sum(s_res);
+    s_y = warp_sum(s_y);
+    if (lane == 0) {
+        red[warp][0] = s_abs;
+        red[warp][1] = s_sq;
+        red[warp][2] = s_res;
+        red[warp][3] = s_y;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double t = 0.0;
+        for (int w = 0; w < kSddmmWarps; ++w) t += red[w][threadIdx.x];
+        partials[blockIdx.x * 4 + threadIdx.x] = t;
+    }
+}
+
+// CSC value mirror from the CSR values: Ycsc[p] = Y[csc2csr[p]] (a coalesced
+// write with a gathered read, instead of a scattered 8-byte write per entry
+// inside the update kernel, which costs a DRAM read-modify-write per sector)
+__global__ void mirror_csc_kernel(long long nnz, const int* __restrict__ csc2csr, const double* __restrict__ Y,
+                                  double* __restrict__ Ycsc) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p < nnz) Ycsc[p] = Y[__ldg(csc2csr + p)];
+}
+
+// Large kept rank (16 < k <= 64): lane l holds U[i, l] and U[i, l + 32] in
+// registers for the whole segment; 32 entries are processed per step: every
+// lane forms its partial dot product for all 32 (coalesced loads of each
+// factor row across the warp), then a transposing butterfly (reduce-scatter:
+// 16 + 8 + 4 + 2 + 1 shuffles) leaves the full sum of entry e0 + l on lane l,
+// so the 32 updates run lane-parallel with coalesced A / Y accesses.
+__global__ void __launch_bounds__(32 * kSddmmWarps) sddmm_update_wide_kernel(
+    SegPlanView plan, const int* __restrict__ col, const double* __restrict__ A, double* __restrict__ Y,
+    double* __restrict__ Ycsc, const int* __restrict__ csr2csc, const double* __restrict__ U, long long ldu,
+    const double* __restrict__ Vs, long long ldv, int k, double delta, int mode, double* __restrict__ partials) {
     __shared__ double red[kSddmmWarps][4];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     double s_abs = 0.0, s_sq = 0.0, s_res = 0.0, s_y = 0.0;
-    // grid-stride over rows, one warp per row
-    for (long long row = static_cast<long long>(blockIdx.x) * kSddmmWarps + warp; row < m_local;
-         row += static_cast<long long>(gridDim.x) * kSddmmWarps) {
-        const long long beg = rowptr[row], end = rowptr[row + 1];
+    const bool lo = lane < k, hi = lane + 32 < k;
+    for (long long sg = static_cast<long long>(blockIdx.x) * kSddmmWarps + warp; sg < plan.nseg;
+         sg += static_cast<long long>(gridDim.x) * kSddmmWarps) {
+        const long long row = plan.seg_row[sg];
+        const long long beg = plan.seg_beg[sg], end = plan.seg_end[sg];
         const double* ur = U + row * ldu;
-        for (long long e = beg + lane; e < end; e += 32) {
-            const int c = __ldg(col + e);
-            const double* vr = Vs + static_cast<long long>(c) * ldv;
-            double p = 0.0;
-            for (long long j = 0; j < k; ++j) p = fma(__ldg(ur + j), __ldg(vr + j), p);
-            const double a = __ldg(A + e);
-            const double y_old = Y[e];
-            const double d = a - p;
-            s_abs += fabs(d);
-            s_sq = fma(d, d, s_sq);
-            const double r = a - y_old;
-            s_res = fma(r, r, s_res);
-            if (mode == 1) {
-                const double y_new = fma(delta, d, y_old);
-                Y[e] = y_new;
-                Ycsc[csr2csc[e]] = y_new;
-                s_y = fma(y_new, y_new, s_y);
-            } else if (mode == 2) {
-                Y[e] = p;
-                s_y = fma(p, p, s_y);
-            } else {
-                s_y = fma(y_old, y_old, s_y);
+        const double u0 = lo ? __ldg(ur + lane) : 0.0;
+        const double u1 = hi ? __ldg(ur + lane + 32) : 0.0;
+        for (long long e0 = beg; e0 < end; e0 += 32) {
+            const long long e = e0 + lane;
+            const int cl = (e < end) ? __ldg(col + e) : -1;
+            const double a_pre = (e < end) ? __ldg(A + e) : 0.0;
+            const double y_pre = (e < end) ? Y[e] : 0.0;
+            // all 64 factor-row loads are unconditional and independent (a
+            // branch per entry would serialize them on the L2 latency): past
+            // the segment end the row index is clamped to 0 and its product
+            // discarded with the entry
+            double p[32];
+            const int lane_lo = lo ? lane : 0, lane_hi = hi ? lane + 32 : 0;
+#pragma unroll
+            for (int u = 0; u < 32; ++u) {
+                const int c = max(__shfl_sync(0xffffffffu, cl, u), 0);
+                const double* vr = Vs + static_cast<long long>(c) * ldv;
+                p[u] = fma(u1, __ldg(vr + lane_hi), u0 * __ldg(vr + lane_lo));
+            }
+            // reduce-scatter: after the level of width o, lane l keeps the o
+            // sums of the entries whose index agrees with l on bits >= o
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const bool up = (lane & o) != 0;
+#pragma unroll
+                for (int i = 0; i < o; ++i) {
+                    const double send = up ? p[i] : p[i + o];
+                    const double keep = up ? p[i + o] : p[i];
+                    p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+            if (e < end) {
+                const double pe = p[0];
+                const double a = a_pre;
+                const double y_old = y_pre;
+                const double d = a - pe;
+                s_abs += fabs(d);
+                s_sq = fma(d, d, s_sq);
+                const double r = a - y_old;
+                s_res = fma(r, r, s_res);
+                if (mode == 1) {
+                    const double y_new = fma(delta, d, y_old);
+                    Y[e] = y_new;
+                    if (Ycsc) Ycsc[csr2csc[e]] = y_new;
+                    s_y = fma(y_new, y_new, s_y);
+                } else if (mode == 2) {
+                    Y[e] = pe;
+                    s_y = fma(pe, pe, s_y);
+                } else {
+                    s_y = fma(y_old, y_old, s_y);
+                }
             }
         }
     }
@@ -382,22 +534,46 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
     }
 }
 
-void sddmm_update(svt_ctx* ctx, i64 m_local, const i64* rowptr, const int* col, const double* A, double* Y,
+void sddmm_update(svt_ctx* ctx, const SegPlanView& plan, i64 m_local, const int* col, const double* A, double* Y,
                   double* Ycsc, const int* csr2csc, i64 nnz, i64 n, const double* U, i64 ldu, const double* Vs,
                   i64 ldv, i64 k, double delta, int mode, double* d_sums4) {
-    const int blocks = std::max(1, std::min<int>(ctx->num_sms * 8, static_cast<int>((m_local + kSddmmWarps - 1) / kSddmmWarps)));
+    const int blocks =
+        std::max(1, std::min<int>(ctx->num_sms * 8, static_cast<int>((plan.nseg + kSddmmWarps - 1) / kSddmmWarps)));
     ctx->ws_partial2.ensure(static_cast<size_t>(blocks) * 4);
     {
         // col 4 + A 8 + Y in 8 + Y out 8 (+ CSC mirror 4 + 8) per
         // entry, row pointers, and the k-wide factor rows read once.
-        const double per = (mode == 1) ? 40.0 : (mode == 2 ? 20.0 : 20.0);
+        const double per = (mode == 1) ? (Ycsc ? 40.0 : 28.0) : 20.0;
         LaunchScope ls(ctx, K_SDDMM, per * nnz + 8.0 * (m_local + 1) + 8.0 * k * (m_local + n), 2.0 * nnz * k);
-        sddmm_update_kernel<<<blocks, 32 * kSddmmWarps, 0, ctx->stream>>>(
-            m_local, reinterpret_cast<const long long*>(rowptr), col, A, Y, Ycsc, csr2csc, U, ldu, Vs, ldv, k,
-            delta, mode, ctx->ws_partial2.get());
+        double* part = ctx->ws_partial2.get();
+#define SVT_SDDMM(KP)                                                                                       \
+    sddmm_update_kernel<KP><<<blocks, 32 * kSddmmWarps, 0, ctx->stream>>>(plan, col, A, Y, Ycsc, csr2csc,     \
+                                                                         U, ldu, Vs, ldv, k, delta, mode, part)
+        if (k <= 1)
+            SVT_SDDMM(1);
+        else if (k <= 2)
+            SVT_SDDMM(2);
+        else if (k <= 4)
+            SVT_SDDMM(4);
+        else if (k <= 8)
+            SVT_SDDMM(8);
+        else if (k <= 16)
+            SVT_SDDMM(16);
+        else if (k <= 64)
+            sddmm_update_wide_kernel<<<blocks, 32 * kSddmmWarps, 0, ctx->stream>>>(
+                plan, col, A, Y, Ycsc, csr2csc, U, ldu, Vs, ldv, static_cast<int>(k), delta, mode, part);
+        else
+            SVT_SDDMM(32);
+#undef SVT_SDDMM
     }
     LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
     reduce4_kernel<<<1, 128, 0, ctx->stream>>>(ctx->ws_partial2.get(), blocks, d_sums4);
+}
+
+void mirror_csc(svt_ctx* ctx, i64 nnz, const int* csc2csr, const double* Y, double* Ycsc) {
+    if (nnz <= 0) return;
+    LaunchScope ls(ctx, K_SDDMM, 20.0 * nnz, 0.0);
+    mirror_csc_kernel<<<static_cast<unsigned>((nnz + 255) / 256), 256, 0, ctx->stream>>>(nnz, csc2csr, Y, Ycsc);
 }
 
 void scale_values(svt_ctx* ctx, i64 nnz, const double* in, double alpha, double* out, const int* csr2csc,
