@@ -77,7 +77,7 @@ struct Engine {
     Vals Y;
     DevBuf<double> Om, OmBank, X, X2, P, T, C, D, G, Rinv, hh, tmp, W, lam, Vraw, Wk;
     DevBuf<double> fkZ, fkZq, fkZt, fkWn, fkH, fkYh, fkth, fkZY, fkXr, fkres;  // finalize_kept
-    DevBuf<double> OmW, XW, TW, CW, GW, RW, eW;  // speculative round batches
+    DevBuf<double> TW, CW, GW, RW, eW;  // round batches (the sketch panels live in spec)
     // Speculative sketch of the next round batch (Omega + the power-iteration
     // products, which do not depend on the basis) computed on ctx->side while
     // the current batch's Gram-Schmidt / QR run on the main stream.  Two
