@@ -299,6 +299,7 @@ def main():
     recs = []
     for _ in range(args.steps):
         recs.append(solver.step())
+    ctx.join()  # the timed region also covers any speculative side-stream work still in flight
     e1.record(stream)
     e1.synchronize()
     torch.cuda.synchronize()

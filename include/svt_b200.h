@@ -121,6 +121,9 @@ int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, sv
 int svt_nccl_get_unique_id(void* out128);
 int svt_ctx_destroy(svt_ctx* ctx);
 int svt_ctx_sync(svt_ctx* ctx);
+/* make the context stream wait for all work issued on the library's side
+ * stream (speculative batches); asynchronous */
+int svt_ctx_join(svt_ctx* ctx);
 void* svt_ctx_stream(svt_ctx* ctx); /* the cudaStream_t every kernel runs on */
 int svt_ctx_rank(svt_ctx* ctx, int* rank, int* world);
 /* instrumentation: per-kernel-class CUDA-event timing (0 = off) */

@@ -100,6 +100,10 @@ class Context:
     def sync(self):
         _check(lib().svt_ctx_sync(self.h))
 
+    def join(self):
+        """Order the context stream after the side stream's work (async)."""
+        _check(lib().svt_ctx_join(self.h))
+
     def set_profiling(self, on: bool):
         _check(lib().svt_ctx_set_profiling(self.h, C.c_int(1 if on else 0)))
 

@@ -173,6 +173,18 @@ int svt_ctx_sync(svt_ctx* ctx) {
     });
 }
 
+int svt_ctx_join(svt_ctx* ctx) {
+    return guard([&] {
+        need(ctx, "svt_ctx_join");
+        if (!ctx->side) return;
+        cudaEvent_t ev;
+        SVT_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        SVT_CUDA(cudaEventRecord(ev, ctx->side));
+        SVT_CUDA(cudaStreamWaitEvent(ctx->stream, ev, 0));
+        SVT_CUDA(cudaEventDestroy(ev));
+    });
+}
+
 void* svt_ctx_stream(svt_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
 int svt_ctx_rank(svt_ctx* ctx, int* rank, int* world) {

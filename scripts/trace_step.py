@@ -14,6 +14,31 @@ from paper_1704_05528_b200 import api as G  # noqa: E402
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from explore import load  # noqa: E402
 
+
+def union(iv):
+    iv = sorted(iv)
+    out = []
+    for a, b in iv:
+        if out and a <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], b)
+        else:
+            out.append([a, b])
+    return out
+
+
+def inter_len(A, B):
+    i = j = 0
+    t = 0.0
+    while i < len(A) and j < len(B):
+        lo, hi = max(A[i][0], B[j][0]), min(A[i][1], B[j][1])
+        if hi > lo:
+            t += hi - lo
+        if A[i][1] < B[j][1]:
+            i += 1
+        else:
+            j += 1
+    return t
+
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--warm", type=int, default=5)
@@ -38,6 +63,18 @@ kern = sorted([(e["ts"], e["ts"] + e.get("dur", 0), e["name"]) for e in ev
 rt = sorted([(e["ts"], e["ts"] + e.get("dur", 0), e["name"]) for e in ev if e.get("cat") == "cuda_runtime"],
             key=lambda x: x[0])
 busy = sum(b - a for a, b, _ in kern)
+by_stream = {}
+for e in ev:
+    if e.get("cat") == "kernel":
+        by_stream.setdefault(e.get("args", {}).get("stream"), []).append((e["ts"], e["ts"] + e.get("dur", 0)))
+streams = {k: union(v) for k, v in by_stream.items()}
+for k, v in streams.items():
+    print(f"stream {k}: {len(by_stream[k])} kernels, busy {sum(b - a for a, b in v)/1e3:.1f} ms")
+ks = list(streams)
+if len(ks) >= 2:
+    print(f"overlap of streams {ks[0]} and {ks[1]}: {inter_len(streams[ks[0]], streams[ks[1]])/1e3:.1f} ms")
+allu = union([iv for v in streams.values() for iv in v])
+print(f"device busy (union): {sum(b - a for a, b in allu)/1e3:.1f} ms")
 span = kern[-1][1] - kern[0][0]
 print(f"kernels {len(kern)}  device busy {busy/1e3:.1f} ms of span {span/1e3:.1f} ms  runtime calls {len(rt)}")
 gaps = []
