@@ -1472,25 +1472,34 @@ __global__ void __launch_bounds__(kHhThreads) householder_kernel(const double* _
 }
 
 // ---------------------------------------------------------------------------
-// single-CTA one-sided Jacobi eigensolver for the small Gram (r <= 48)
+// single-CTA Jacobi eigensolver for the small symmetric matrices (r <= 112)
 // ---------------------------------------------------------------------------
-constexpr int kJacMax = 48;
 
-// Two-sided cyclic Jacobi for a symmetric r x r matrix (r <= RP <= 48), one
-// CTA: round-robin parallel ordering (the step's RP/2 pairs precomputed in
-// shared memory), the disjoint rotations of a step computed from
-// (a_pp, a_qq, a_pq) alone, then applied to the rows and to the columns (and
-// V) in barrier-separated phases.  RP is a compile-time bucket (16 / 32 /
-// 48), the matrix is zero-padded to it (padding never rotates), so every
-// index split is a shift or a constant multiply.  Eigenvalues = diag(A),
+// Two-sided cyclic Jacobi for a symmetric r x r matrix (r <= RP <= 112), one
+// CTA, A and V in (dynamic) shared memory: round-robin parallel ordering (the
+// step's RP/2 pairs precomputed), the disjoint rotations of a step computed
+// from (a_pp, a_qq, a_pq) alone, then applied to the rows and to the columns
+// (and V) in barrier-separated phases; a warp per pair (two for RP > 64).  RP
+// is a compile-time bucket, the matrix zero-padded to it (padding never
+// rotates).  A pair below the absolute floor 1e-17 * max|a_ii| is rounding
+// noise of a rank-deficient Gram and is not rotated.  Eigenvalues = diag(A),
 // eigenvectors = columns of V, sorted descending (stable).
 template <int RP>
-__global__ void __launch_bounds__(32 * RP / 2) jacobi_sym_kernel(const double* __restrict__ G, int r,
-                                                                 double* __restrict__ W, double* __restrict__ lambda) {
-    constexpr int NP = RP / 2;
-    constexpr int NT = 32 * NP;  // one warp per pair
-    __shared__ double A[RP][RP + 1];
-    __shared__ double V[RP][RP + 1];
+struct JacSym {
+    static constexpr int NP = RP / 2;
+    static constexpr int WARPS = NP < 32 ? NP : 32;
+    static constexpr int NT = 32 * WARPS;
+    static constexpr size_t SMEM = sizeof(double) * 2 * RP * (RP + 1);  // A and V
+};
+
+template <int RP>
+__global__ void __launch_bounds__(JacSym<RP>::NT) jacobi_sym_kernel(const double* __restrict__ G, int r,
+                                                                    double* __restrict__ W,
+                                                                    double* __restrict__ lambda) {
+    constexpr int NP = JacSym<RP>::NP, WARPS = JacSym<RP>::WARPS, NT = JacSym<RP>::NT;
+    extern __shared__ __align__(16) double jac_smem[];
+    double(*A)[RP + 1] = reinterpret_cast<double(*)[RP + 1]>(jac_smem);
+    double(*V)[RP + 1] = reinterpret_cast<double(*)[RP + 1]>(jac_smem + RP * (RP + 1));
     __shared__ double cs[NP][2];
     __shared__ unsigned char sched[RP - 1][NP][2];
     __shared__ double dg[RP];
@@ -1512,36 +1521,46 @@ __global__ void __launch_bounds__(32 * RP / 2) jacobi_sym_kernel(const double* _
         sched[step][k][1] = static_cast<unsigned char>(p < q ? q : p);
     }
     __syncthreads();
+    double dmax = 0.0;
+    for (int i = 0; i < r; ++i) dmax = fmax(dmax, fabs(A[i][i]));
+    const double afloor = 1e-17 * dmax;
     for (int sweep = 0; sweep < 60; ++sweep) {
         if (tid == 0) rotated = 0;
         __syncthreads();
         for (int step = 0; step < RP - 1; ++step) {
-            const int p = sched[step][warp][0], q = sched[step][warp][1];
-            if (lane == 0) {
-                const double app = A[p][p], aqq = A[q][q], apq = A[p][q];
-                double c = 1.0, sn = 0.0;
-                if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq))) {
-                    const double tau = (aqq - app) / (2.0 * apq);
-                    const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                    c = rsqrt(1.0 + t * t);
-                    sn = t * c;
-                    rotated = 1;
+            if (lane == 0)
+                for (int k = warp; k < NP; k += WARPS) {
+                    const int p = sched[step][k][0], q = sched[step][k][1];
+                    const double app = A[p][p], aqq = A[q][q], apq = A[p][q];
+                    double c = 1.0, sn = 0.0;
+                    if (apq != 0.0 && fabs(apq) > tol * sqrt(fabs(app) * fabs(aqq)) && fabs(apq) > afloor) {
+                        const double tau = (aqq - app) / (2.0 * apq);
+                        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
+                        c = rsqrt(1.0 + t * t);
+                        sn = t * c;
+                        rotated = 1;
+                    }
+                    cs[k][0] = c;
+                    cs[k][1] = sn;
                 }
-                cs[warp][0] = c;
-                cs[warp][1] = sn;
-            }
             __syncwarp();
-            const double c = cs[warp][0], sn = cs[warp][1];
-            // rows p, q of A (this warp's pair only: disjoint from the others)
-            if (sn != 0.0)
+            // rows p, q of A (this warp's pairs: disjoint from the others)
+            for (int k = warp; k < NP; k += WARPS) {
+                const double c = cs[k][0], sn = cs[k][1];
+                if (sn == 0.0) continue;
+                const int p = sched[step][k][0], q = sched[step][k][1];
                 for (int j = lane; j < RP; j += 32) {
                     const double x = A[p][j], y = A[q][j];
                     A[p][j] = c * x - sn * y;
                     A[q][j] = sn * x + c * y;
                 }
+            }
             __syncthreads();
             // columns p, q of A and V
-            if (sn != 0.0)
+            for (int k = warp; k < NP; k += WARPS) {
+                const double c = cs[k][0], sn = cs[k][1];
+                if (sn == 0.0) continue;
+                const int p = sched[step][k][0], q = sched[step][k][1];
                 for (int i = lane; i < RP; i += 32) {
                     const double x = A[i][p], y = A[i][q];
                     A[i][p] = c * x - sn * y;
@@ -1550,6 +1569,7 @@ __global__ void __launch_bounds__(32 * RP / 2) jacobi_sym_kernel(const double* _
                     V[i][p] = c * vx - sn * vy;
                     V[i][q] = sn * vx + c * vy;
                 }
+            }
             __syncthreads();
         }
         if (!rotated) break;
@@ -1578,101 +1598,6 @@ __global__ void __launch_bounds__(32 * RP / 2) jacobi_sym_kernel(const double* _
     if (tid < r) lambda[tid] = dg[order[tid]];
 }
 
-__global__ void __launch_bounds__(1024) jacobi_eig_kernel(const double* __restrict__ G, int r,
-                                                          double* __restrict__ W, double* __restrict__ lambda,
-                                                          int dbg) {
-    __shared__ double A[kJacMax][kJacMax + 1];  // column j = A[.][j]
-    __shared__ double V[kJacMax][kJacMax + 1];
-    __shared__ double nrm[kJacMax];
-    __shared__ int order[kJacMax];
-    __shared__ int rotated;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int rp = (r + 1) & ~1;  // even, padded with a zero column
-    // rotation threshold just above the rounding floor of the computed
-    // column dot products (~sqrt(r) eps): a tighter one only burns sweeps
-    const double jtol = 8.0 * sqrt(static_cast<double>(rp)) * 1.1102230246251565e-16;
-    for (int e = tid; e < kJacMax * kJacMax; e += blockDim.x) {
-        const int i = e / kJacMax, j = e % kJacMax;
-        A[i][j] = (i < r && j < r) ? G[i * r + j] : 0.0;
-        V[i][j] = (i == j) ? 1.0 : 0.0;
-    }
-    __syncthreads();
-    for (int sweep = 0; sweep < 40; ++sweep) {
-        if (tid == 0) rotated = 0;
-        __syncthreads();
-        for (int step = 0; step < rp - 1; ++step) {
-            const int k = warp;
-            if (k < rp / 2) {
-                auto player = [&](int pos) { return pos == 0 ? 0 : 1 + (pos - 1 + step) % (rp - 1); };
-                int p = player(k), q = player(rp - 1 - k);
-                if (p > q) {
-                    const int t = p;
-                    p = q;
-                    q = t;
-                }
-                double al = 0.0, be = 0.0, ga = 0.0;
-                for (int i = lane; i < rp; i += 32) {
-                    const double x = A[i][p], y = A[i][q];
-                    al = fma(x, x, al);
-                    be = fma(y, y, be);
-                    ga = fma(x, y, ga);
-                }
-                al = warp_sum(al);
-                be = warp_sum(be);
-                ga = warp_sum(ga);
-                if (ga != 0.0 && fabs(ga) > jtol * sqrt(al * be)) {
-                    const double zeta = (be - al) / (2.0 * ga);
-                    const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                    const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-                    for (int i = lane; i < rp; i += 32) {
-                        const double x = A[i][p], y = A[i][q];
-                        A[i][p] = c * x - s * y;
-                        A[i][q] = s * x + c * y;
-                        const double vx = V[i][p], vy = V[i][q];
-                        V[i][p] = c * vx - s * vy;
-                        V[i][q] = s * vx + c * vy;
-                    }
-                    if (lane == 0) rotated = 1;
-                }
-            }
-            __syncthreads();
-        }
-        if (!rotated) {
-            if (dbg && tid == 0) printf("[jacobi] r=%d sweeps=%d\n", r, sweep + 1);
-            break;
-        }
-        __syncthreads();
-        if (dbg && tid == 0 && sweep == 39) printf("[jacobi] r=%d hit the sweep cap\n", r);
-    }
-    // eigenvalue j = +-||A[:, j]|| with the sign of v_j^T A_j (PSD: +)
-    if (tid < r) {
-        double s = 0.0, d = 0.0;
-        for (int i = 0; i < r; ++i) {
-            s = fma(A[i][tid], A[i][tid], s);
-            d = fma(V[i][tid], A[i][tid], d);
-        }
-        nrm[tid] = (d < 0.0 ? -1.0 : 1.0) * sqrt(s);
-        order[tid] = tid;
-    }
-    __syncthreads();
-    if (tid == 0) {  // stable insertion sort, descending
-        for (int i = 1; i < r; ++i) {
-            const int o = order[i];
-            int j = i - 1;
-            while (j >= 0 && nrm[order[j]] < nrm[o]) {
-                order[j + 1] = order[j];
-                --j;
-            }
-            order[j + 1] = o;
-        }
-    }
-    __syncthreads();
-    for (int e = tid; e < r * r; e += blockDim.x) {
-        const int i = e / r, j = e % r;
-        W[i * r + j] = V[i][order[j]];
-    }
-    if (tid < r) lambda[tid] = nrm[order[tid]];
-}
 
 // ---------------------------------------------------------------------------
 // Cooperative one-sided Jacobi for larger Grams: columns of A (= G) and V live
@@ -1709,6 +1634,24 @@ __global__ void __launch_bounds__(256) jacobi_coop_kernel(double* __restrict__ A
     unsigned* gen = sync + 1;
     unsigned* rot = sync + 2;  // rot[0], rot[1]: rotations of the current / next sweep
     const double jtol = 8.0 * sqrt(static_cast<double>(rp)) * 1.1102230246251565e-16;
+    // absolute floor: ||A||_F is invariant under the rotations; a pair whose
+    // inner product is below (rounding x ||A||_F)^2 is left alone (columns
+    // of negligible norm -- rank-deficient Grams -- never meet the relative
+    // test and would burn every sweep)
+    __shared__ double fro2_s;
+    if (threadIdx.x == 0) fro2_s = 0.0;
+    __syncthreads();
+    {
+        double part = 0.0;
+        for (long long e = threadIdx.x; e < static_cast<long long>(rp) * rp; e += blockDim.x) {
+            const double x = __ldcg(A + e);
+            part = fma(x, x, part);
+        }
+        part = warp_sum(part);
+        if (lane == 0) atomicAdd(&fro2_s, part);
+    }
+    __syncthreads();
+    const double afloor = 1e-30 * fro2_s;
     for (int sweep = 0; sweep < max_sweeps; ++sweep) {
         if (blockIdx.x == 0 && threadIdx.x == 0) rot[(sweep + 1) & 1] = 0u;
         for (int step = 0; step < rp - 1; ++step) {
@@ -1733,7 +1676,7 @@ __global__ void __launch_bounds__(256) jacobi_coop_kernel(double* __restrict__ A
                 al = warp_sum(al);
                 be = warp_sum(be);
                 ga = warp_sum(ga);
-                if (ga != 0.0 && fabs(ga) > jtol * sqrt(al * be)) {
+                if (ga != 0.0 && fabs(ga) > jtol * sqrt(al * be) && fabs(ga) > afloor) {
                     const double zeta = (be - al) / (2.0 * ga);
                     const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
                     const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
@@ -2010,29 +1953,40 @@ void householder_qr(svt_ctx* ctx, const double* X, i64 m, i64 w, i64 ldx, double
                                                           status);
 }
 
+template <int RP>
+void jacobi_sym_launch(svt_ctx* ctx, const double* G, int r, double* W, double* lambda) {
+    constexpr size_t smem = JacSym<RP>::SMEM;
+    if (smem > 48 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            SVT_CUDA(cudaFuncSetAttribute(jacobi_sym_kernel<RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(smem)));
+            attr = true;
+        }
+    }
+    jacobi_sym_kernel<RP><<<1, JacSym<RP>::NT, smem, ctx->stream>>>(G, r, W, lambda);
+}
+
+// single-CTA two-sided Jacobi in shared memory for r <= kJacSymMax
+constexpr int kJacSymMax = 112;
+void launch_jacobi_sym(svt_ctx* ctx, const double* G, int r, double* W, double* lambda) {
+    if (r <= 8) jacobi_sym_launch<8>(ctx, G, r, W, lambda);
+    else if (r <= 16) jacobi_sym_launch<16>(ctx, G, r, W, lambda);
+    else if (r <= 24) jacobi_sym_launch<24>(ctx, G, r, W, lambda);
+    else if (r <= 32) jacobi_sym_launch<32>(ctx, G, r, W, lambda);
+    else if (r <= 40) jacobi_sym_launch<40>(ctx, G, r, W, lambda);
+    else if (r <= 48) jacobi_sym_launch<48>(ctx, G, r, W, lambda);
+    else if (r <= 64) jacobi_sym_launch<64>(ctx, G, r, W, lambda);
+    else if (r <= 80) jacobi_sym_launch<80>(ctx, G, r, W, lambda);
+    else if (r <= 96) jacobi_sym_launch<96>(ctx, G, r, W, lambda);
+    else jacobi_sym_launch<112>(ctx, G, r, W, lambda);
+}
+
 void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
     if (r <= 0) return;
-    if (r <= kJacMax) {
+    if (r <= kJacSymMax) {
         LaunchScope ls(ctx, K_FINAL, 16.0 * r * r, 0.0);
-        static const int variant = std::getenv("SVTB_JACOBI_ONESIDED") ? 1 : 0;
-        if (variant) {
-            static const int dbg = std::getenv("SVTB_DEBUG_JACOBI") ? 1 : 0;
-            jacobi_eig_kernel<<<1, 1024, 0, ctx->stream>>>(G, static_cast<int>(r), W, lambda, dbg);
-        } else {
-            const int ri = static_cast<int>(r);
-            if (r <= 8)
-                jacobi_sym_kernel<8><<<1, 32 * 4, 0, ctx->stream>>>(G, ri, W, lambda);
-            else if (r <= 16)
-                jacobi_sym_kernel<16><<<1, 32 * 8, 0, ctx->stream>>>(G, ri, W, lambda);
-            else if (r <= 24)
-                jacobi_sym_kernel<24><<<1, 32 * 12, 0, ctx->stream>>>(G, ri, W, lambda);
-            else if (r <= 32)
-                jacobi_sym_kernel<32><<<1, 32 * 16, 0, ctx->stream>>>(G, ri, W, lambda);
-            else if (r <= 40)
-                jacobi_sym_kernel<40><<<1, 32 * 20, 0, ctx->stream>>>(G, ri, W, lambda);
-            else
-                jacobi_sym_kernel<48><<<1, 32 * 24, 0, ctx->stream>>>(G, ri, W, lambda);
-        }
+        launch_jacobi_sym(ctx, G, static_cast<int>(r), W, lambda);
         return;
     }
     // Larger Grams: cooperative multi-CTA one-sided Jacobi.

@@ -459,11 +459,12 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
     out.n = n;
     out.k = 0;
     out.sigma.clear();
-    // small bases, or bases of which a large share is kept (the subspace
+    // small bases (single-CTA Jacobi up to 112), or bases of which a large
+    // share is kept (the subspace
     // iteration would span most of the space anyway, and the pairs crowd
     // against the threshold where its residual criterion converges slowest):
     // the dense Gram eigensolve, exact to rounding
-    if (r <= 48 || (r <= 1024 && 4 * (s_warm + 16) >= r)) {
+    if (r <= 112 || (r <= 1024 && 4 * (s_warm + 16) >= r)) {
         finalize(E, st, FinalizeMode::Kept, tau, out);
         return;
     }
