@@ -624,3 +624,44 @@ def test_kept_finalize_matches_dense_finalize_full_size(config, iters, monkeypat
         for key in ("residual", "train_mae", "rel_residual_x"):
             assert abs(a[key] - b[key]) <= 1e-8 * abs(b[key]), (key, a[key], b[key])
     np.testing.assert_allclose(rk.sigma, rd.sigma, rtol=1e-8)
+
+
+def test_config5_first_iteration_properties():
+    """BASELINE config 5 (1e5 x 1e5, 1e8 observed) at full size, first SVT
+    iteration (t0 = 5000 sketch + ~1,550 extension rounds to r = 20,500):
+    speculative batches reproduce the sequential rounds (same revealed rank,
+    round count and kept rank; residual and MAE to 1e-8), two runs are
+    bitwise identical, and the kept left factors are orthonormal."""
+    ctx = G.default_context()
+    d = G.synth_config(5, 1)
+    m, n = d["m"], d["n"]
+    rp, co, va = d["csr"]
+    A = G.SampledMatrix.from_csr(m, n, rp, co, va)
+    cfg, stop = G.config_params(5, int(rp[-1]), m, n, float(np.sqrt(np.sum(va * va))))
+    cfg.maxit = 1
+
+    def run(batching):
+        ctx.set_batching(batching)
+        try:
+            S = G.Solver(A, cfg, stop)
+            rec = S.step()
+            res = S.result()
+            S.close()
+        finally:
+            ctx.set_batching(True)
+        return rec, res
+
+    seq, rs = run(False)
+    bat, rb = run(True)
+    bat2, rb2 = run(True)
+    assert (seq["rank"], seq["extension_rounds"], seq["kept"]) == (bat["rank"], bat["extension_rounds"], bat["kept"])
+    assert bat["rank"] > 10000 and bat["kept"] > 0
+    for key in ("residual", "train_mae", "rel_residual_x"):
+        assert abs(seq[key] - bat[key]) <= 1e-8 * abs(seq[key])
+    assert {k: v for k, v in bat.items() if not k.endswith("_ms")} == \
+        {k: v for k, v in bat2.items() if not k.endswith("_ms")}
+    assert np.array_equal(rb.sigma, rb2.sigma)
+    np.testing.assert_allclose(rb.sigma, rs.sigma, rtol=1e-8)
+    k = rb.sigma.size
+    np.testing.assert_allclose(rb.U.T @ rb.U, np.eye(k), atol=1e-10)
+    A.close()
