@@ -701,7 +701,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
     auto& sp = E.spec;
     const i64 w = p.dt, m = A->m_local, n = A->n, r0 = st.rank;
     static const bool no_spec = std::getenv("SVTB_NO_SPECULATION") != nullptr;
-    const bool use_spec = sp.valid && sp.seed == p.seed && sp.round0 == round0;
+    const bool use_spec = sp.valid && sp.gen == E.sketch_gen && sp.seed == p.seed && sp.round0 == round0;
     int slot = 0;
     if (sp.valid) {
         // the batch sketched on the side stream during the previous batch
@@ -736,6 +736,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         batch_sketch(E, p, round0 + K, Kn, ns, true);
         SVT_CUDA(cudaEventRecord(sp.ready, c->side));
         sp.valid = true;
+        sp.gen = E.sketch_gen;
         sp.seed = p.seed;
         sp.round0 = round0 + K;
         sp.K = Kn;
@@ -830,6 +831,7 @@ static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, Fina
                           i64 s_warm) {
     SketchOut out;
     int rounds = 0;
+    ++E.sketch_gen;  // speculative batches of an earlier sketch can never be used by this one
     // Omega bank: the Gaussian blocks of the next rounds depend only on
     // (seed, round) (sketch.hpp:246-247), so they are generated kMaxOmegaBatch
     // at a time by independent mt19937_64 warps in two launches.
@@ -863,7 +865,8 @@ static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, Fina
             const int K = std::min(kmax, est);
             // a batch already sketched on the side stream for this round
             // is used whatever the current estimate
-            const bool spec_here = E.spec.valid && E.spec.seed == p.seed && E.spec.round0 == rounds + 1;
+            const bool spec_here = E.spec.valid && E.spec.gen == E.sketch_gen && E.spec.seed == p.seed &&
+                                   E.spec.round0 == rounds + 1;
             if (K >= 2 || spec_here) {
                 // size of the batch after this one if all of this one's
                 // rounds are accepted (same estimate, K rounds later)

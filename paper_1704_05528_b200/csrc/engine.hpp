@@ -87,6 +87,7 @@ struct Engine {
         DevBuf<double> part;  // long-row partials of the side-stream SpMMs
         bool valid = false;   // a speculative batch is in flight / ready
         u64 seed = 0;
+        u64 gen = 0;          // sketch generation it belongs to
         int round0 = 0, K = 0, slot = 0;
         cudaEvent_t ready = nullptr, freed[2] = {nullptr, nullptr};
     } spec;
@@ -94,6 +95,7 @@ struct Engine {
     QBDev qb;  // persistent QB storage: capacity survives across SVT iterations
     bool batching = true;  // speculative multi-round batches (exact-arithmetic equivalent)
     int last_rounds = -1;  // rounds of the previous sketch (batch-size predictor)
+    u64 sketch_gen = 0;    // incremented per sketch: a speculative batch never outlives its sketch
     Engine(svt_ctx* c, svt_mat* m, Vals y) : ctx(c), mat(m), Y(y), batching(c->batching != 0) {}
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
