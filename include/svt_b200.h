@@ -229,6 +229,13 @@ int svt_kickstart(svt_mat* A, double tau, double delta, uint64_t seed, double* o
 int svt_dev_gemm(svt_ctx* ctx, int transA, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                  int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
 
+/* Device-pointer symmetric eigensolve on the context stream: G (r x r,
+ * row-major, symmetric) = W diag(lambda) W^T, lambda descending, W row-major
+ * with the eigenvectors as columns -- the dense step of sketch.hpp:158-162
+ * (SVD of B through its Gram), exposed for its own parity tests.  G is not
+ * modified.  Synchronous. */
+int svt_dev_sym_eig(svt_ctx* ctx, const double* G, int64_t r, double* W, double* lambda);
+
 /* Device-pointer sparse products on the context stream (row-major panels):
  * out (m_local x w) = S * X (X: n x w) or, transpose != 0, out (n x w) = S^T * X
  * (X: m_local x w, out packed, all-reduced across ranks) -- sampled.hpp:113 /

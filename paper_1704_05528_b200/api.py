@@ -172,6 +172,24 @@ def dev_gemm(a, b, c, trans_a=False, alpha=1.0, beta=0.0, ctx: Context | None = 
     return c
 
 
+def dev_sym_eig(g, ctx: Context | None = None):
+    """(lambda descending, W) with g = W diag(lambda) W^T for a symmetric
+    row-major contiguous float64 CUDA tensor (svt_dev_sym_eig; the Gram
+    eigensolve of sketch.hpp:158-162)."""
+    import torch
+    ctx = ctx or default_context()
+    if not (g.is_cuda and g.dtype == torch.float64 and g.is_contiguous() and g.dim() == 2
+            and g.shape[0] == g.shape[1]):
+        raise InvalidArgument("dev_sym_eig: square contiguous float64 CUDA tensor required")
+    r = g.shape[0]
+    w = torch.empty((r, r), dtype=torch.float64, device=g.device)
+    lam = torch.empty((max(r, 1),), dtype=torch.float64, device=g.device)
+    torch.cuda.synchronize()
+    _check(lib().svt_dev_sym_eig(ctx.h, C.c_void_p(g.data_ptr()), C.c_int64(r), C.c_void_p(w.data_ptr()),
+                                 C.c_void_p(lam.data_ptr())))
+    return lam[:r], w
+
+
 # ---------------------------------------------------------------------------
 def build_csr(m, n, rows, cols, vals):
     """SampledMatrix ctor semantics (sampled.hpp:27-62) on the host: returns

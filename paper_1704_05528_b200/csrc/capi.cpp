@@ -644,6 +644,20 @@ int svt_dev_gemm(svt_ctx* ctx, int transA, int64_t M, int64_t N, int64_t K, doub
     });
 }
 
+int svt_dev_sym_eig(svt_ctx* ctx, const double* G, int64_t r, double* W, double* lambda) {
+    return guard([&] {
+        need(ctx, "svt_dev_sym_eig");
+        if (r < 0) throw std::invalid_argument("dev_sym_eig: negative order");
+        if (r == 0) return;
+        if (!G || !W || !lambda) throw std::invalid_argument("dev_sym_eig: null operand");
+        // sym_eig may overwrite its input: work on a copy
+        DevBuf<double> Gc(static_cast<size_t>(r * r));
+        SVT_CUDA(cudaMemcpyAsync(Gc.get(), G, sizeof(double) * r * r, cudaMemcpyDeviceToDevice, ctx->stream));
+        sym_eig(ctx, Gc.get(), r, W, lambda);
+        sync_stream(ctx);
+    });
+}
+
 int svt_sp_mult(svt_mat* S, int64_t w, const double* X, double* out) {
     return guard([&] {
         need(S, "svt_sp_mult");

@@ -12,6 +12,8 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "common.hpp"
@@ -1695,11 +1697,162 @@ __global__ void __launch_bounds__(256) jacobi_coop_kernel(double* __restrict__ A
             }
             grid_barrier(count, gen, gridDim.x);
         }
-        if (atomicAdd(rot + (sweep & 1), 0u) == 0u) break;
+        if (atomicAdd(rot + (sweep & 1), 0u) == 0u) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) sync[4] = sweep + 1;
+            break;
+        }
         grid_barrier(count, gen, gridDim.x);
+        if (blockIdx.x == 0 && threadIdx.x == 0) sync[4] = sweep + 1;
     }
     // eigenvalue j = sign(v_j . a_j) ||a_j||
     for (int j = gwarp; j < rp; j += nwarps) {
+        const double* aj = A + static_cast<long long>(j) * rp;
+        const double* vj = V + static_cast<long long>(j) * rp;
+        double s = 0.0, d = 0.0;
+        for (int i = lane; i < rp; i += 32) {
+            const double x = __ldcg(aj + i);
+            s = fma(x, x, s);
+            d = fma(__ldcg(vj + i), x, d);
+        }
+        s = warp_sum(s);
+        d = warp_sum(d);
+        if (lane == 0) lambda[j] = (d < 0.0 ? -1.0 : 1.0) * sqrt(s);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Blocked one-sided Jacobi (the mid-size Grams, 112 < r <= ~6000): the
+// columns of A (= G) and V are grouped into nb blocks of b columns; each step
+// of the round-robin tournament over the blocks gives every CTA one block
+// pair, which it stages in shared memory (2b columns of A and of V), sweeps
+// with all 2b(2b-1)/2 column rotations (one warp per disjoint pair, a
+// __syncthreads between the 2b-1 rounds) and writes back.  One grid barrier
+// per step instead of one per column-pair round: nb - 1 = rp/b - 1 barriers
+// a sweep rather than rp - 1, and the rotations read shared memory instead
+// of L2.  Convergence: a sweep that rotated nothing (same relative test and
+// absolute floor as jacobi_coop_kernel).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) jacobi_blk_kernel(double* __restrict__ A, double* __restrict__ V, int rp,
+                                                         int b, int max_sweeps, unsigned* __restrict__ sync,
+                                                         double* __restrict__ lambda) {
+    extern __shared__ double jb_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int nb = rp / b, npair = nb / 2, w2 = 2 * b;
+    const long long blk = static_cast<long long>(b) * rp;  // doubles per block
+    double* sA = jb_smem;                                  // 2b columns x rp
+    double* sV = jb_smem + 2 * blk;
+    unsigned* count = sync;
+    unsigned* gen = sync + 1;
+    unsigned* rot = sync + 2;
+    const double jtol = 8.0 * sqrt(static_cast<double>(rp)) * 1.1102230246251565e-16;
+    __shared__ double fro2_s;
+    __shared__ unsigned nrot_s;
+    if (threadIdx.x == 0) fro2_s = 0.0;
+    __syncthreads();
+    {
+        double part = 0.0;
+        for (long long e = threadIdx.x; e < static_cast<long long>(rp) * rp; e += blockDim.x) {
+            const double x = __ldcg(A + e);
+            part = fma(x, x, part);
+        }
+        part = warp_sum(part);
+        if (lane == 0) atomicAdd(&fro2_s, part);
+    }
+    __syncthreads();
+    // absolute test: after rotations every column carries rounding of
+    // ~eps ||G||_F, so a pair whose inner product is below
+    // 8 eps ||G||_F (||a_p|| + ||a_q||) is left alone -- the rotation would
+    // only mix rounding noise (the residual it removes is |ga| / (|l_p| +
+    // |l_q|) <= 8 eps ||G||_F, the backward error of any stable eigensolver)
+    const double afro = 8.0 * 1.1102230246251565e-16 * sqrt(fro2_s);
+    int sweep = 0;
+    for (; sweep < max_sweeps; ++sweep) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) rot[(sweep + 1) & 1] = 0u;
+        for (int step = 0; step < nb - 1; ++step) {
+            for (int k = blockIdx.x; k < npair; k += gridDim.x) {
+                const int a = k, bb = nb - 1 - k;
+                const int P = (a == 0) ? 0 : 1 + (a - 1 + step) % (nb - 1);
+                const int Q = (bb == 0) ? 0 : 1 + (bb - 1 + step) % (nb - 1);
+                const double2* gA0 = reinterpret_cast<const double2*>(A + P * blk);
+                const double2* gA1 = reinterpret_cast<const double2*>(A + Q * blk);
+                const double2* gV0 = reinterpret_cast<const double2*>(V + P * blk);
+                const double2* gV1 = reinterpret_cast<const double2*>(V + Q * blk);
+                double2* s2A = reinterpret_cast<double2*>(sA);
+                double2* s2V = reinterpret_cast<double2*>(sV);
+                const long long h = blk / 2;  // blk is even (rp is)
+                for (long long e = threadIdx.x; e < h; e += blockDim.x) {
+                    s2A[e] = __ldcg(gA0 + e);
+                    s2A[h + e] = __ldcg(gA1 + e);
+                    s2V[e] = __ldcg(gV0 + e);
+                    s2V[h + e] = __ldcg(gV1 + e);
+                }
+                if (threadIdx.x == 0) nrot_s = 0u;
+                __syncthreads();
+                for (int t = 0; t < w2 - 1; ++t) {
+                    for (int i = warp; i < b; i += nwarps) {
+                        const int x = i, y = w2 - 1 - i;
+                        int p = (x == 0) ? 0 : 1 + (x - 1 + t) % (w2 - 1);
+                        int q = (y == 0) ? 0 : 1 + (y - 1 + t) % (w2 - 1);
+                        if (p > q) {
+                            const int tmp = p;
+                            p = q;
+                            q = tmp;
+                        }
+                        double* ap = sA + static_cast<long long>(p) * rp;
+                        double* aq = sA + static_cast<long long>(q) * rp;
+                        double al = 0.0, be = 0.0, ga = 0.0;
+#pragma unroll 4
+                        for (int r = lane; r < rp; r += 32) {
+                            const double u = ap[r], v = aq[r];
+                            al = fma(u, u, al);
+                            be = fma(v, v, be);
+                            ga = fma(u, v, ga);
+                        }
+                        al = warp_sum(al);
+                        be = warp_sum(be);
+                        ga = warp_sum(ga);
+                        if (ga != 0.0 && fabs(ga) > jtol * sqrt(al * be) && fabs(ga) > afro * (sqrt(al) + sqrt(be))) {
+                            const double zeta = (be - al) / (2.0 * ga);
+                            const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                            const double c = 1.0 / sqrt(1.0 + tt * tt), sn = c * tt;
+                            double* vp = sV + static_cast<long long>(p) * rp;
+                            double* vq = sV + static_cast<long long>(q) * rp;
+#pragma unroll 4
+                            for (int r = lane; r < rp; r += 32) {
+                                const double u = ap[r], v = aq[r];
+                                ap[r] = c * u - sn * v;
+                                aq[r] = sn * u + c * v;
+                                const double vu = vp[r], vv = vq[r];
+                                vp[r] = c * vu - sn * vv;
+                                vq[r] = sn * vu + c * vv;
+                            }
+                            if (lane == 0) atomicAdd(&nrot_s, 1u);
+                        }
+                    }
+                    __syncthreads();
+                }
+                double2* oA0 = reinterpret_cast<double2*>(A + P * blk);
+                double2* oA1 = reinterpret_cast<double2*>(A + Q * blk);
+                double2* oV0 = reinterpret_cast<double2*>(V + P * blk);
+                double2* oV1 = reinterpret_cast<double2*>(V + Q * blk);
+                for (long long e = threadIdx.x; e < h; e += blockDim.x) {
+                    __stcg(oA0 + e, s2A[e]);
+                    __stcg(oA1 + e, s2A[h + e]);
+                    __stcg(oV0 + e, s2V[e]);
+                    __stcg(oV1 + e, s2V[h + e]);
+                }
+                if (threadIdx.x == 0 && nrot_s) atomicAdd(rot + (sweep & 1), nrot_s);
+                __syncthreads();
+            }
+            grid_barrier(count, gen, gridDim.x);
+        }
+        if (atomicAdd(rot + (sweep & 1), 0u) == 0u) break;
+        grid_barrier(count, gen, gridDim.x);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) sync[4] = sweep + 1;
+    // eigenvalue j = sign(v_j . a_j) ||a_j||
+    const int gwarp = blockIdx.x * nwarps + warp, gw = gridDim.x * nwarps;
+    for (int j = gwarp; j < rp; j += gw) {
         const double* aj = A + static_cast<long long>(j) * rp;
         const double* vj = V + static_cast<long long>(j) * rp;
         double s = 0.0, d = 0.0;
@@ -1989,8 +2142,14 @@ void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
         launch_jacobi_sym(ctx, G, static_cast<int>(r), W, lambda);
         return;
     }
-    // Larger Grams: cooperative multi-CTA one-sided Jacobi.
-    const i64 rp = (r + 1) & ~1LL;
+    // Larger Grams: cooperative multi-CTA one-sided Jacobi, blocked with the
+    // block pairs staged in shared memory while 2b columns of A and V fit
+    // (b chosen for >= 32 block pairs a step), else column pairs in L2.
+    constexpr i64 kJbSmem = 200 * 1024;
+    i64 bsz = std::min<i64>(16, kJbSmem / (32 * (r + 1)));
+    bsz = std::min<i64>(bsz, std::max<i64>(1, r / 64));
+    const bool blocked = bsz >= 1 && std::getenv("SVTB_JACOBI_SCALAR") == nullptr;
+    const i64 rp = blocked ? (r + 2 * bsz - 1) / (2 * bsz) * (2 * bsz) : (r + 1) & ~1LL;
     ctx->ws_eig.ensure(static_cast<size_t>(2 * rp * rp + rp));
     ctx->ws_info.ensure(8);
     double* A = ctx->ws_eig.get();
@@ -2001,14 +2160,26 @@ void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
         LaunchScope ls(ctx, K_FINAL, 16.0 * rp * rp, 0.0);
         init_jacobi_kernel<<<nblk(rp * rp), 256, 0, ctx->stream>>>(G, r, rp, A, V);
     }
-    int per_sm = 0;
-    SVT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_coop_kernel, 256, 0));
-    const int want = static_cast<int>(std::min<i64>(std::max(1, per_sm) * ctx->num_sms, (rp / 2 + 7) / 8));
-    const int grid = std::max(1, std::min(want, std::max(1, per_sm) * ctx->num_sms));
+    int per_sm = 0, grid = 1;
     int rpi = static_cast<int>(rp), sweeps = 40;
     unsigned* sync = reinterpret_cast<unsigned*>(ctx->ws_info.get());
-    void* args[] = {&A, &V, &rpi, &sweeps, &sync, &lam_u};
-    {
+    if (blocked) {
+        int bi = static_cast<int>(bsz);
+        const size_t smem = static_cast<size_t>(4 * bsz * rp) * sizeof(double);
+        SVT_CUDA(cudaFuncSetAttribute(jacobi_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        SVT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_blk_kernel, 256, smem));
+        const i64 npair = rp / bsz / 2;
+        grid = static_cast<int>(std::max<i64>(1, std::min<i64>(npair, std::max(1, per_sm) * ctx->num_sms)));
+        void* args[] = {&A, &V, &rpi, &bi, &sweeps, &sync, &lam_u};
+        LaunchScope ls(ctx, K_FINAL, 0.0, 6.0 * rp * rp * rp * 8);
+        SVT_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_blk_kernel), grid, 256, args, smem,
+                                             ctx->stream));
+    } else {
+        SVT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_coop_kernel, 256, 0));
+        const int want = static_cast<int>(std::min<i64>(std::max(1, per_sm) * ctx->num_sms, (rp / 2 + 7) / 8));
+        grid = std::max(1, std::min(want, std::max(1, per_sm) * ctx->num_sms));
+        void* args[] = {&A, &V, &rpi, &sweeps, &sync, &lam_u};
         LaunchScope ls(ctx, K_FINAL, 0.0, 6.0 * rp * rp * rp * 8);
         SVT_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(jacobi_coop_kernel), grid, 256, args, 0,
                                              ctx->stream));
@@ -2017,9 +2188,15 @@ void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
     std::vector<double> lh(static_cast<size_t>(rp));
     SVT_CUDA(cudaMemcpyAsync(lh.data(), lam_u, sizeof(double) * rp, cudaMemcpyDeviceToHost, ctx->stream));
     sync_stream(ctx);
+    if (std::getenv("SVTB_DEBUG_JACOBI")) {
+        unsigned sw = 0;
+        SVT_CUDA(cudaMemcpy(&sw, sync + 4, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "[jacobi] r=%lld rp=%lld b=%lld grid=%d sweeps=%u\n", static_cast<long long>(r),
+                     static_cast<long long>(rp), static_cast<long long>(blocked ? bsz : 0), grid, sw);
+    }
     std::vector<int> perm(static_cast<size_t>(r));
     for (i64 j = 0; j < r; ++j) perm[static_cast<size_t>(j)] = static_cast<int>(j);
-    // the padded zero column (if any) is index r and is excluded
+    // the padded zero columns (if any) are indices >= r and are excluded
     std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return lh[x] > lh[y]; });
     std::vector<double> ls_sorted(static_cast<size_t>(r));
     for (i64 j = 0; j < r; ++j) ls_sorted[static_cast<size_t>(j)] = lh[static_cast<size_t>(perm[static_cast<size_t>(j)])];

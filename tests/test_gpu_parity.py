@@ -460,6 +460,44 @@ def test_dev_gemm_matches_fp64_reference(shape):
     assert err <= 1e-13 * max(1.0, np.sqrt(K) / 10), err
 
 
+# ---- the Gram eigensolver (sketch.hpp:158-162): shared-memory two-sided Jacobi
+# (r <= 112), blocked one-sided Jacobi (block pairs staged in shared memory),
+# scalar cooperative one-sided Jacobi (SVTB_JACOBI_SCALAR) -----------------------
+def _graded_gram(r, n, decay, seed):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    qa, _ = torch.linalg.qr(torch.randn(r, r, dtype=torch.float64, device="cuda", generator=g))
+    qb, _ = torch.linalg.qr(torch.randn(n, r, dtype=torch.float64, device="cuda", generator=g))
+    s = 1e3 * torch.exp(-decay * torch.arange(r, dtype=torch.float64, device="cuda") / r)
+    if r > 20:
+        s[r // 3: r // 3 + 4] = s[r // 3]  # a cluster of four equal values
+        s[-3:] = 0.0  # rank deficient
+    B = (qa * s) @ qb.T
+    return (B @ B.T).contiguous()
+
+
+@pytest.mark.parametrize("r,decay,scalar", [(1, 1.0, False), (2, 1.0, False), (64, 6.0, False), (112, 6.0, False),
+                                            (113, 6.0, False), (130, 12.0, False), (200, 3.0, False),
+                                            (257, 6.0, False), (512, 12.0, False), (200, 6.0, True)])
+def test_dev_sym_eig_matches_fp64_reference(r, decay, scalar, monkeypatch):
+    """Tolerance: eigenvalues and residuals ||G w - l w|| within 1e-12 ||G||,
+    W orthonormal to 1e-11 (FP64 backward stability; torch.linalg.eigvalsh
+    is the reference)."""
+    import torch
+    if scalar:
+        monkeypatch.setenv("SVTB_JACOBI_SCALAR", "1")
+    A = _graded_gram(r, max(r, 300), decay, 1000 + r)
+    A0 = A.clone()
+    lam, W = G.dev_sym_eig(A)
+    assert torch.equal(A, A0)  # input untouched
+    ref = torch.linalg.eigvalsh(A).flip(0)
+    nrm = ref.abs().max().item()
+    assert bool((lam[:-1] >= lam[1:]).all())  # descending
+    assert (lam - ref).abs().max().item() <= 1e-12 * nrm
+    assert ((A @ W - W * lam).norm(dim=0)).max().item() <= 1e-12 * nrm
+    assert (W.T @ W - torch.eye(r, dtype=torch.float64, device="cuda")).abs().max().item() <= 1e-11
+
+
 # ---- device-side sample-set construction (csrc/build.cu) ----------------------
 def _skewed_csr(seed):
     """Rows and columns longer than one 512-entry segment, empty rows and
