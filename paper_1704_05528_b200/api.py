@@ -24,7 +24,7 @@ from ._abi import (OBSERVER_FN, Backend, InvalidArgument, IterationRecord, Sketc
                    raise_for)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsvt_b200.so")
+LIB_PATH = os.environ.get("SVTB_LIB") or os.path.join(_HERE, "lib", "libsvt_b200.so")  # SVTB_LIB: A/B builds
 _lib = None
 
 P_I64 = C.POINTER(C.c_int64)

@@ -168,6 +168,147 @@ __global__ void triplet_fill_kernel(long long cnt, long long lo, long long n, co
     val[k] = vals[perm[lo + k]];
 }
 
+
+// ---- shared-memory-tiled view (TilePlanView, common.hpp) -----------------
+// keys[k] = (block of k's row) << 32 | gather index; rid[k] = row (one warp
+// per row)
+__global__ void tile_keys_kernel(long long rows, const long long* __restrict__ ptr, const int* __restrict__ idx,
+                                 unsigned long long* __restrict__ keys, int* __restrict__ iota,
+                                 int* __restrict__ rid) {
+    const long long r = (blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= rows) return;
+    const unsigned long long hi = static_cast<unsigned long long>(r / kTileRows) << 32;
+    for (long long k = ptr[r] + lane; k < ptr[r + 1]; k += 32) {
+        keys[k] = hi | static_cast<unsigned int>(idx[k]);
+        iota[k] = static_cast<int>(k);
+        rid[k] = static_cast<int>(r);
+    }
+}
+
+__global__ void tile_newcol_kernel(long long nnz, const unsigned long long* __restrict__ skeys,
+                                   int* __restrict__ newcol) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p >= nnz) return;
+    newcol[p] = (p == 0 || skeys[p] != skeys[p - 1]) ? 1 : 0;
+}
+
+// coarse tile starts: the block's first entry, or where dix / kTileSlots
+// changes (dix = distinct gather index within the block)
+__global__ void tile_start_kernel(long long nnz, long long rows, const unsigned long long* __restrict__ skeys,
+                                  const long long* __restrict__ ptr, const int* __restrict__ G,
+                                  int* __restrict__ ts) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p >= nnz) return;
+    const long long blk = static_cast<long long>(skeys[p] >> 32);
+    const long long bstart = ptr[blk * kTileRows];
+    const int ct = (G[p] - G[bstart]) / kTileSlots;
+    const bool st = (p == bstart) || ct != (G[p - 1] - G[bstart]) / kTileSlots;
+    ts[p] = st ? 1 : 0;
+}
+
+__global__ void tile_coarse_start_kernel(long long nnz, const int* __restrict__ ts, const int* __restrict__ TI,
+                                         long long* __restrict__ cstart) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p >= nnz) return;
+    if (ts[p]) cstart[TI[p] - 1] = p;
+}
+
+__global__ void tile_nsub_kernel(long long nc, const long long* __restrict__ cstart, int* __restrict__ nsub) {
+    const long long c = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (c >= nc) return;
+    nsub[c] = static_cast<int>((cstart[c + 1] - cstart[c] + kTileEnts - 1) / kTileEnts);
+}
+
+// per entry: its (sub-)tile, slot and the (tile, local row) sort key; tile
+// starts, blocks and the slots' gather indices (duplicates write equal values)
+__global__ void tile_assign_kernel(long long nnz, const int* __restrict__ TI, const long long* __restrict__ cstart,
+                                   const int* __restrict__ sub_base, const int* __restrict__ G,
+                                   const int* __restrict__ sp, const int* __restrict__ rid,
+                                   const unsigned long long* __restrict__ skeys, int* __restrict__ slot_of,
+                                   unsigned long long* __restrict__ key2, long long* __restrict__ tile_e,
+                                   int* __restrict__ tile_blk) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p >= nnz) return;
+    const int c = TI[p] - 1;
+    const long long q = p - cstart[c];
+    const long long sub = sub_base[c] + q / kTileEnts;
+    const long long substart = cstart[c] + (q / kTileEnts) * kTileEnts;
+    slot_of[p] = G[p] - G[substart];
+    key2[p] = (static_cast<unsigned long long>(sub) << 9) | static_cast<unsigned long long>(rid[sp[p]] % kTileRows);
+    if (p == substart) {
+        tile_e[sub] = p;
+        tile_blk[sub] = static_cast<int>(skeys[p] >> 32);
+    }
+}
+
+__global__ void tile_nslot_kernel(long long nt, const long long* __restrict__ tile_e, const int* __restrict__ G,
+                                  int* __restrict__ nslot) {
+    const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (t >= nt) return;
+    nslot[t] = G[tile_e[t + 1] - 1] - G[tile_e[t]] + 1;
+}
+
+__global__ void tile_ucol_kernel(long long nnz, const long long* __restrict__ cstart, const int* __restrict__ TI, const int* __restrict__ sub_base,
+                                 const int* __restrict__ slot_of, const int* __restrict__ sp,
+                                 const int* __restrict__ idx, const int* __restrict__ tile_u, int* __restrict__ ucol) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p >= nnz) return;
+    const int c = TI[p] - 1;
+    const long long sub = sub_base[c] + (p - cstart[c]) / kTileEnts;
+    ucol[tile_u[sub] + slot_of[p]] = idx[sp[p]];
+}
+
+// final (tile, row)-ordered entries: slot, and the CSR position of the value
+__global__ void tile_fill_kernel(long long nnz, const int* __restrict__ o, const int* __restrict__ slot_of,
+                                 const int* __restrict__ sp, const int* __restrict__ map, TileEnt* __restrict__ ent,
+                                 int* __restrict__ perm) {
+    const long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (f >= nnz) return;
+    const int p = o[f];
+    TileEnt t;
+    t.v = 0.0;
+    t.slot = slot_of[p];
+    t.pad = 0;
+    ent[f] = t;
+    const int srcpos = sp[p];
+    perm[f] = map ? map[srcpos] : srcpos;
+}
+
+// roff[t * stride + r] = first entry of local row r in tile t (relative)
+__global__ void tile_roff_kernel(long long nt, const long long* __restrict__ tile_e,
+                                 const unsigned long long* __restrict__ skey2, unsigned short* __restrict__ roff) {
+    const long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (g >= nt * kTileRoffStride) return;
+    const long long t = g / kTileRoffStride;
+    const int r = static_cast<int>(g - t * kTileRoffStride);
+    const long long b = tile_e[t], e = tile_e[t + 1];
+    if (r > kTileRows) {
+        roff[g] = static_cast<unsigned short>(e - b);
+        return;
+    }
+    const unsigned long long key = (static_cast<unsigned long long>(t) << 9) + static_cast<unsigned long long>(r);
+    long long lo = b, hi = e;
+    while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (skey2[mid] < key)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    roff[g] = static_cast<unsigned short>(lo - b);
+}
+
+__global__ void invert_perm_kernel(long long n, const int* __restrict__ fwd, int* __restrict__ inv) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p < n) inv[fwd[p]] = static_cast<int>(p);
+}
+
+__global__ void iota_kernel(long long n, int* __restrict__ out) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p < n) out[p] = static_cast<int>(p);
+}
+
 inline unsigned nb(long long n, int t = 256) { return static_cast<unsigned>((n + t - 1) / t); }
 
 // exclusive scan of n ints into out (n + 1 entries; out[n] = total)
@@ -358,6 +499,217 @@ void build_from_triplets_device(svt_ctx* ctx, svt_mat* M, i64 nnz, const i64* ro
     }
     const int code = build_sampled_device(ctx, M, col64.get());
     if (code != 0) throw std::invalid_argument("SampledMatrix: invalid entry");
+}
+
+
+// Tiled view of a CSR-like pattern (ptr: rows + 1, idx: gather index per
+// entry, sorted within each row).  map (optional) sends a source position to
+// the CSR position holding its value (the CSC view passes csc2csr).
+void build_tile_plan(svt_ctx* ctx, const long long* ptr, const int* idx, i64 rows, i64 nnz, const int* map,
+                     TilePlan& P) {
+    cudaStream_t s = ctx->stream;
+    const i64 nblocks = (rows + kTileRows - 1) / kTileRows;
+    P.v = TilePlanView{};
+    P.v.nrows = rows;
+    P.v.nnz = nnz;
+    P.src = nullptr;
+    std::vector<long long> h_te(1, 0);
+    std::vector<int> h_tb;
+    i64 nt = 0;
+    if (nnz > 0) {
+        const size_t N = static_cast<size_t>(nnz);
+        DevBuf<unsigned long long> keys(N), skeys(N);
+        DevBuf<int> iota(N), sp(N), rid(N), A1(N), G(N), TI(N);
+        DevBuf<unsigned char> tmp;
+        {
+            LaunchScope ls(ctx, K_OTHER, 16.0 * nnz, 0.0);
+            tile_keys_kernel<<<nb(rows * 32), 256, 0, s>>>(rows, ptr, idx, keys.get(), iota.get(), rid.get());
+        }
+        int end_bit = 33;
+        while ((1LL << (end_bit - 32)) < nblocks + 1) ++end_bit;
+        size_t bytes = 0;
+        SVT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.get(), skeys.get(), iota.get(), sp.get(),
+                                                 static_cast<int>(nnz), 0, end_bit, s));
+        tmp.ensure(bytes);
+        SVT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, keys.get(), skeys.get(), iota.get(), sp.get(),
+                                                 static_cast<int>(nnz), 0, end_bit, s));
+        tile_newcol_kernel<<<nb(nnz), 256, 0, s>>>(nnz, skeys.get(), A1.get());
+        SVT_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, A1.get(), G.get(), static_cast<int>(nnz), s));
+        tmp.ensure(bytes);
+        SVT_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), bytes, A1.get(), G.get(), static_cast<int>(nnz), s));
+        tile_start_kernel<<<nb(nnz), 256, 0, s>>>(nnz, rows, skeys.get(), ptr, G.get(), A1.get());
+        SVT_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, A1.get(), TI.get(), static_cast<int>(nnz), s));
+        tmp.ensure(bytes);
+        SVT_CUDA(cub::DeviceScan::InclusiveSum(tmp.get(), bytes, A1.get(), TI.get(), static_cast<int>(nnz), s));
+        int nc = 0;
+        SVT_CUDA(cudaMemcpyAsync(&nc, TI.get() + nnz - 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+        sync_stream(ctx);
+        DevBuf<long long> cstart(static_cast<size_t>(nc) + 1);
+        tile_coarse_start_kernel<<<nb(nnz), 256, 0, s>>>(nnz, A1.get(), TI.get(), cstart.get());
+        const long long nn = nnz;
+        SVT_CUDA(cudaMemcpyAsync(cstart.get() + nc, &nn, sizeof(long long), cudaMemcpyHostToDevice, s));
+        DevBuf<int> nsub(static_cast<size_t>(nc) + 1), sub_base(static_cast<size_t>(nc) + 1);
+        tile_nsub_kernel<<<nb(nc), 256, 0, s>>>(nc, cstart.get(), nsub.get());
+        exclusive_scan(ctx, nsub.get(), sub_base.get(), nc, tmp);
+        int ntot = 0;
+        SVT_CUDA(cudaMemcpyAsync(&ntot, sub_base.get() + nc, sizeof(int), cudaMemcpyDeviceToHost, s));
+        sync_stream(ctx);
+        nt = ntot;
+        P.tile_e.alloc(static_cast<size_t>(nt) + 1);
+        P.tile_u.alloc(static_cast<size_t>(nt) + 1);
+        DevBuf<int> tile_blk(static_cast<size_t>(nt)), nslot(static_cast<size_t>(nt) + 1), tu32(static_cast<size_t>(nt) + 1);
+        DevBuf<unsigned long long>& key2 = keys;  // keys are dead after the first sort
+        DevBuf<int>& slot_of = iota;
+        {
+            LaunchScope ls(ctx, K_OTHER, 40.0 * nnz, 0.0);
+            tile_assign_kernel<<<nb(nnz), 256, 0, s>>>(nnz, TI.get(), cstart.get(), sub_base.get(), G.get(),
+                                                       sp.get(), rid.get(), skeys.get(), slot_of.get(), key2.get(),
+                                                       P.tile_e.get(), tile_blk.get());
+        }
+        SVT_CUDA(cudaMemcpyAsync(P.tile_e.get() + nt, &nn, sizeof(long long), cudaMemcpyHostToDevice, s));
+        tile_nslot_kernel<<<nb(nt), 256, 0, s>>>(nt, P.tile_e.get(), G.get(), nslot.get());
+        exclusive_scan(ctx, nslot.get(), tu32.get(), nt, tmp);
+        int nuc = 0;
+        SVT_CUDA(cudaMemcpyAsync(&nuc, tu32.get() + nt, sizeof(int), cudaMemcpyDeviceToHost, s));
+        sync_stream(ctx);
+        P.ucol.alloc(static_cast<size_t>(nuc) + kTileSlots);  // padded: slot loads run past a tile's end
+        SVT_CUDA(cudaMemsetAsync(P.ucol.get(), 0, sizeof(int) * (static_cast<size_t>(nuc) + kTileSlots), s));
+        tile_ucol_kernel<<<nb(nnz), 256, 0, s>>>(nnz, cstart.get(), TI.get(), sub_base.get(), slot_of.get(),
+                                                 sp.get(), idx, tu32.get(), P.ucol.get());
+        {
+            std::vector<int> h(static_cast<size_t>(nt) + 1);
+            std::vector<long long> h64(static_cast<size_t>(nt) + 1);
+            SVT_CUDA(cudaMemcpyAsync(h.data(), tu32.get(), sizeof(int) * (nt + 1), cudaMemcpyDeviceToHost, s));
+            sync_stream(ctx);
+            for (size_t i = 0; i < h.size(); ++i) h64[i] = h[i];
+            SVT_CUDA(cudaMemcpyAsync(P.tile_u.get(), h64.data(), sizeof(long long) * (nt + 1), cudaMemcpyHostToDevice,
+                                     s));
+            sync_stream(ctx);
+        }
+        // (tile, local row) order; slots ascend inside a row (stable sort)
+        int end2 = 10;
+        while ((1LL << (end2 - 9)) < nt + 1) ++end2;
+        DevBuf<unsigned long long>& skey2 = skeys;
+        DevBuf<int>& o = rid;  // rid is dead after tile_assign
+        DevBuf<int>& pos = A1;
+        {
+            LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
+            // pos = iota (reuse tile_keys-free pass: positions 0..nnz-1)
+            iota_kernel<<<nb(nnz), 256, 0, s>>>(nnz, pos.get());
+        }
+        SVT_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key2.get(), skey2.get(), pos.get(), o.get(),
+                                                 static_cast<int>(nnz), 0, end2, s));
+        tmp.ensure(bytes);
+        SVT_CUDA(cub::DeviceRadixSort::SortPairs(tmp.get(), bytes, key2.get(), skey2.get(), pos.get(), o.get(),
+                                                 static_cast<int>(nnz), 0, end2, s));
+        P.ent.alloc(N);
+        P.perm.alloc(N);
+        {
+            LaunchScope ls(ctx, K_OTHER, 32.0 * nnz, 0.0);
+            tile_fill_kernel<<<nb(nnz), 256, 0, s>>>(nnz, o.get(), slot_of.get(), sp.get(), map, P.ent.get(),
+                                                     P.perm.get());
+        }
+        P.roff.alloc(static_cast<size_t>(nt) * kTileRoffStride);
+        tile_roff_kernel<<<nb(nt * kTileRoffStride), 256, 0, s>>>(nt, P.tile_e.get(), skey2.get(), P.roff.get());
+        h_te.resize(static_cast<size_t>(nt) + 1);
+        h_tb.resize(static_cast<size_t>(nt));
+        SVT_CUDA(cudaMemcpyAsync(h_te.data(), P.tile_e.get(), sizeof(long long) * (nt + 1), cudaMemcpyDeviceToHost, s));
+        SVT_CUDA(cudaMemcpyAsync(h_tb.data(), tile_blk.get(), sizeof(int) * nt, cudaMemcpyDeviceToHost, s));
+        sync_stream(ctx);  // temporaries die here
+        SVT_CHECK_LAUNCH();
+    }
+    // work items: each block's tiles in runs of >= target entries; a block
+    // spread over several items writes partial rows, summed in item order
+    const i64 target = std::max<i64>(4LL * kTileEnts, nnz / std::max(1, ctx->num_sms));
+    std::vector<int> it0, it1, iblk, ipart, sblk, sfirst, scount;
+    i64 t = 0, nparts = 0;
+    for (i64 b = 0; b < nblocks; ++b) {
+        const i64 tb0 = t;
+        while (t < nt && h_tb[static_cast<size_t>(t)] == b) ++t;
+        const size_t first_item = it0.size();
+        i64 a = tb0;
+        if (a == t) {  // empty block: one item writes its zero rows
+            it0.push_back(static_cast<int>(a));
+            it1.push_back(static_cast<int>(a));
+            iblk.push_back(static_cast<int>(b));
+        }
+        while (a < t) {
+            i64 e = a;
+            long long ents = 0;
+            while (e < t && (ents < target || e == a) && e - a < kTileItemTiles) {
+                ents += h_te[static_cast<size_t>(e + 1)] - h_te[static_cast<size_t>(e)];
+                ++e;
+            }
+            // do not leave a small remainder behind
+            if (t - e > 0 && t - a <= kTileItemTiles) {
+                long long rest = h_te[static_cast<size_t>(t)] - h_te[static_cast<size_t>(e)];
+                if (rest < target / 2) e = t;
+            }
+            it0.push_back(static_cast<int>(a));
+            it1.push_back(static_cast<int>(e));
+            iblk.push_back(static_cast<int>(b));
+            a = e;
+        }
+        const size_t cnt = it0.size() - first_item;
+        if (cnt == 1) {
+            ipart.push_back(-1);
+        } else {
+            sblk.push_back(static_cast<int>(b));
+            sfirst.push_back(static_cast<int>(nparts));
+            scount.push_back(static_cast<int>(cnt));
+            for (size_t q = 0; q < cnt; ++q) ipart.push_back(static_cast<int>(nparts++));
+        }
+    }
+    auto up = [&](DevBuf<int>& d, const std::vector<int>& h) {
+        d.alloc(std::max<size_t>(1, h.size()));
+        if (!h.empty()) SVT_CUDA(cudaMemcpyAsync(d.get(), h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice, s));
+    };
+    up(P.item_t0, it0);
+    up(P.item_t1, it1);
+    up(P.item_blk, iblk);
+    up(P.item_part, ipart);
+    up(P.split_blk, sblk);
+    up(P.split_first, sfirst);
+    up(P.split_count, scount);
+    sync_stream(ctx);
+    P.v.ntiles = nt;
+    P.v.nitems = static_cast<long long>(it0.size());
+    P.v.nsplit = static_cast<long long>(sblk.size());
+    P.v.nparts = nparts;
+    P.v.tile_e = P.tile_e.get();
+    P.v.tile_u = P.tile_u.get();
+    P.v.ucol = P.ucol.get();
+    P.v.roff = P.roff.get();
+    P.v.ent = P.ent.get();
+    P.v.perm = P.perm.get();
+    P.v.item_t0 = P.item_t0.get();
+    P.v.item_t1 = P.item_t1.get();
+    P.v.item_blk = P.item_blk.get();
+    P.v.item_part = P.item_part.get();
+    P.v.split_blk = P.split_blk.get();
+    P.v.split_first = P.split_first.get();
+    P.v.split_count = P.split_count.get();
+    P.built = true;
+}
+
+
+// Both tiled views of M (lazily, on the first wide product).  The CSC view's
+// values come from the CSR array through csc2csr (built here if the upload
+// path did not keep it).
+void ensure_tile_plans(svt_ctx* ctx, svt_mat* M) {
+    const i64 nnz = M->nnz_local;
+    if (!M->tile_csr.built)
+        build_tile_plan(ctx, reinterpret_cast<const long long*>(M->rowptr.get()), M->col.get(), M->m_local, nnz,
+                        nullptr, M->tile_csr);
+    if (!M->tile_csc.built) {
+        if (M->csc2csr.n < static_cast<size_t>(nnz)) {
+            M->csc2csr.alloc(static_cast<size_t>(std::max<i64>(1, nnz)));
+            if (nnz > 0)
+                invert_perm_kernel<<<nb(nnz), 256, 0, ctx->stream>>>(nnz, M->csr2csc.get(), M->csc2csr.get());
+        }
+        build_tile_plan(ctx, reinterpret_cast<const long long*>(M->colptr.get()), M->cscrow.get(), M->n, nnz,
+                        M->csc2csr.get(), M->tile_csc);
+    }
 }
 
 }  // namespace svtb

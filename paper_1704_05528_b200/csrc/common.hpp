@@ -152,6 +152,41 @@ struct SegPlanView {
     const int* long_first = nullptr;
     const int* long_count = nullptr;
 };
+// Shared-memory-tiled view of the same CSR / CSC pattern for wide panels
+// (build.cu builds it, sparse.cu consumes it).  Output rows are grouped in
+// blocks of kTileRows; a block's entries, ordered by gather index, are cut
+// into tiles of at most kTileSlots distinct gather indices ("slots") and
+// kTileEnts entries.  A tile stages its slots' panel rows in shared memory
+// once and every entry reads them from there, so the L2 -> SM traffic per
+// entry drops by the tile's reuse factor (entries / slots).  Inside a tile
+// the entries are ordered by (row, slot) with per-row offsets, so each
+// output row accumulates in a fixed order (deterministic, no atomics).
+constexpr int kTileRows = 128;
+constexpr int kTileSlots = 80;
+constexpr int kTileEnts = 1024;
+constexpr int kTileRoffStride = 136;  // kTileRows + 1 rounded up to 16 B
+constexpr int kTileItemTiles = 512;   // tiles per work item (metadata staged in shared memory)
+struct TileEnt {
+    double v;  // value (refreshed from the CSR values at each sketch)
+    int slot;  // slot of the entry's gather index in its tile
+    int pad;
+};
+struct TilePlanView {
+    long long nrows = 0, ntiles = 0, nitems = 0, nsplit = 0, nparts = 0, nnz = 0;
+    const long long* tile_e = nullptr;     // ntiles + 1 entry offsets
+    const long long* tile_u = nullptr;     // ntiles + 1 slot offsets into ucol
+    const int* ucol = nullptr;             // gather index of every slot
+    const unsigned short* roff = nullptr;  // ntiles x kTileRoffStride row offsets (tile-relative)
+    TileEnt* ent = nullptr;                // entries in tile order
+    const int* perm = nullptr;             // tile position -> CSR position (value source)
+    const int* item_t0 = nullptr;          // work item = (block, tile range)
+    const int* item_t1 = nullptr;
+    const int* item_blk = nullptr;
+    const int* item_part = nullptr;        // -1: writes its block directly; else partial slot
+    const int* split_blk = nullptr;        // blocks spread over several items
+    const int* split_first = nullptr;
+    const int* split_count = nullptr;
+};
 void nccl_init(Comm& c, int rank, int world, const void* id128);
 
 }  // namespace svtb

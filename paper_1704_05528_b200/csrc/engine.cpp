@@ -199,9 +199,36 @@ double frob_sq(Engine& E) {
     return read_scalar(c, S_FROB);
 }
 
+// The tiled views (wide panels) mirror Y: built on first use, their entry
+// values re-gathered from Y.csr once per sketch.  Only ever called on the
+// main stream (side-stream products follow main-stream work through events).
+static bool tiles_ready(Engine& E, i64 w, cudaStream_t stream) {
+    svt_mat* A = E.mat;
+    if (!E.tiled || w <= 16 || A->nnz_local <= 0 || E.Y.csr == nullptr) return false;
+    if (!E.tiles_fresh || A->tile_csr.src != E.Y.csr || A->tile_csc.src != E.Y.csr) {
+        if (stream && stream != E.ctx->stream) return false;
+        ensure_tile_plans(E.ctx, A);
+        tile_values(E.ctx, A->tile_csr.v, E.Y.csr);
+        tile_values(E.ctx, A->tile_csc.v, E.Y.csr);
+        A->tile_csr.src = E.Y.csr;
+        A->tile_csc.src = E.Y.csr;
+        E.tiles_fresh = true;
+    }
+    return true;
+}
+
+void prepare_tiles(Engine& E) {
+    E.tiles_fresh = false;
+    E.tiled = tile_spmm_enabled();
+    tiles_ready(E, 32, nullptr);
+}
+
 void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo, cudaStream_t stream,
              DevBuf<double>* scratch) {
     svt_mat* A = E.mat;
+    if (tiles_ready(E, w, stream) &&
+        spmm_tiled(E.ctx, K_SPMM, A->tile_csr.v, A->n, w, X, ldx, out, ldo, stream, scratch))
+        return;
     spmm(E.ctx, K_SPMM, A->plan_csr.v, A->m_local, A->col.get(), E.Y.csr, A->nnz_local, A->n, w, X, ldx, out, ldo,
          stream, scratch);
 }
@@ -209,8 +236,10 @@ void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo, c
 void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out, cudaStream_t stream,
                DevBuf<double>* scratch) {
     svt_mat* A = E.mat;
-    spmm(E.ctx, K_SPMMT, A->plan_csc.v, A->n, A->cscrow.get(), E.Y.csc, A->nnz_local, A->m_local, w, X, ldx, out, w,
-         stream, scratch);
+    if (!(tiles_ready(E, w, stream) &&
+          spmm_tiled(E.ctx, K_SPMMT, A->tile_csc.v, A->m_local, w, X, ldx, out, w, stream, scratch)))
+        spmm(E.ctx, K_SPMMT, A->plan_csc.v, A->n, A->cscrow.get(), E.Y.csc, A->nnz_local, A->m_local, w, X, ldx, out,
+             w, stream, scratch);
     E.ctx->comm.allreduce_sum(out, static_cast<size_t>(A->n * w), stream ? stream : E.ctx->stream);
 }
 
@@ -910,6 +939,7 @@ static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, Fina
 // sketch.hpp:188-201
 SketchOut r3svd(Engine& E, const svt_sketch_params& p, FinalizeMode mode, double tau, double frob_y_sq) {
     check_sketch_params(p);
+    prepare_tiles(E);  // Y may have changed since the previous sketch
     QBDev& st = E.qb;
     qb_init(E, st, p.t, p.np, derive_seed_u(p.seed, 0), frob_y_sq);
     return run_loop(E, st, p, mode, tau, 0);
@@ -928,6 +958,7 @@ SketchOut r4svd(Engine& E, const double* U_prev, i64 ldu, i64 s, const svt_sketc
     svt_mat* A = E.mat;
     const i64 min_dim = std::min(A->m, A->n);
     if (s > min_dim) throw std::invalid_argument("r4svd: recycled basis wider than min(m, n)");
+    prepare_tiles(E);
     if (frob_y_sq < 0.0) frob_y_sq = frob_sq(E);
     if (!(frob_y_sq > 0.0)) throw std::domain_error("r4svd: target matrix is all zero");
     const i64 m = A->m_local;
@@ -967,6 +998,7 @@ DevFactors rsvd(Engine& E, i64 k, const svt_sketch_params& p) {
     const i64 min_dim = std::min(A->m, A->n);
     if (k < 1) throw std::invalid_argument("rsvd: k must be >= 1");
     if (p.p < 0 || k + p.p > min_dim) throw std::invalid_argument("rsvd: k + p must not exceed min(m, n)");
+    prepare_tiles(E);
     QBDev st;
     // same kernels as qb_init (sketch.hpp:173-176), no zero-norm check
     const i64 t = k + p.p;

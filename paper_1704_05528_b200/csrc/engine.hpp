@@ -17,11 +17,24 @@ struct SegPlan {
     svtb::SegPlanView v;
 };
 
+// Tiled view storage behind svtb::TilePlanView (built lazily, on the first
+// wide product).  `src` is the CSR value array the entries currently mirror.
+struct TilePlan {
+    svtb::DevBuf<long long> tile_e, tile_u;
+    svtb::DevBuf<int> ucol, perm, item_t0, item_t1, item_blk, item_part, split_blk, split_first, split_count;
+    svtb::DevBuf<unsigned short> roff;
+    svtb::DevBuf<svtb::TileEnt> ent;
+    svtb::TilePlanView v;
+    const double* src = nullptr;
+    bool built = false;
+};
+
 // Device SampledMatrix (sampled.hpp:25-110): this rank's row block as CSR
 // (int64 rowptr, int32 col, fp64 val) plus a CSC view whose value array
 // mirrors the CSR values through csr2csc.
 struct svt_mat {
     SegPlan plan_csr, plan_csc;
+    TilePlan tile_csr, tile_csc;  // shared-memory-tiled views for wide panels
     svt_ctx* ctx = nullptr;
     svtb::i64 m = 0, n = 0, row_begin = 0, row_end = 0, m_local = 0, nnz_local = 0, nnz_global = 0;
     svtb::DevBuf<svtb::i64> rowptr;
@@ -96,6 +109,8 @@ struct Engine {
     bool batching = true;  // speculative multi-round batches (exact-arithmetic equivalent)
     int last_rounds = -1;  // rounds of the previous sketch (batch-size predictor)
     u64 sketch_gen = 0;    // incremented per sketch: a speculative batch never outlives its sketch
+    bool tiled = false;        // shared-memory-tiled SpMM for wide panels (opt-in, per sketch)
+    bool tiles_fresh = false;  // the tiled views mirror Y (cleared at every sketch entry)
     Engine(svt_ctx* c, svt_mat* m, Vals y) : ctx(c), mat(m), Y(y), batching(c->batching != 0) {}
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
@@ -120,7 +135,9 @@ void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out, cudaStre
                DevBuf<double>* scratch = nullptr);
 void qr_orthonormal(Engine& E, double* X, i64 ldx, i64 w, double* Qout, i64 ldq);            // dense.hpp:103
 void qr_orthonormal(Engine& E, i64 rows, bool dist, double* X, i64 ldx, i64 w, double* Qout, i64 ldq);
-double spectral_norm_est(Engine& E, int iters, u64 seed);                                   // sampled.hpp:188
+double spectral_norm_est(Engine& E, int iters, u64 seed);
+// mark the tiled views stale and re-gather them from E.Y (sketch entry)
+void prepare_tiles(Engine& E);                                   // sampled.hpp:188
 
 // sketch.hpp
 void qb_init(Engine& E, QBDev& st, i64 t, int np, u64 seed, double frob_y_sq = -1.0);
@@ -137,6 +154,11 @@ u64 derive_seed_u(u64 seed, u64 stream);
 // build.cu: device-side CSC view / csr2csc / segment plans of an uploaded CSR
 void build_plan_device(svt_ctx* ctx, const long long* ptr, i64 rows, SegPlan& P);
 int build_sampled_device(svt_ctx* ctx, svt_mat* M, const long long* col64);
+// build.cu: the shared-memory-tiled view of a CSR-like pattern (map: source
+// position -> CSR position of its value, or null for the identity)
+void build_tile_plan(svt_ctx* ctx, const long long* ptr, const int* idx, i64 rows, i64 nnz, const int* map,
+                     TilePlan& P);
+void ensure_tile_plans(svt_ctx* ctx, svt_mat* M);
 void build_from_triplets_device(svt_ctx* ctx, svt_mat* M, i64 nnz, const i64* rows, const i64* cols,
                                 const double* vals);
 

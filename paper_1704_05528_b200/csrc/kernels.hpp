@@ -33,6 +33,14 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
           i64 x_rows, i64 w, const double* X, i64 ldx, double* out, i64 ldo, cudaStream_t stream = nullptr,
           DevBuf<double>* scratch = nullptr);
 
+// Shared-memory-tiled variant for wide panels (TilePlanView); returns false
+// when the call is outside its limits (the caller then uses spmm).  The
+// plan's entries must mirror the current values (tile_values).
+bool tile_spmm_enabled();
+bool spmm_tiled(svt_ctx* ctx, int cls, const TilePlanView& P, i64 x_rows, i64 w, const double* X, i64 ldx,
+                double* out, i64 ldo, cudaStream_t stream = nullptr, DevBuf<double>* scratch = nullptr);
+void tile_values(svt_ctx* ctx, const TilePlanView& P, const double* Ycsr);
+
 // Fused SDDMM + Bregman update + reductions (sampled.hpp:148-176,
 // solver.hpp:143-168, 321-323).  For each stored (i, j):
 //   p = U[i,:] . Vs[j,:]   (Vs = V diag(sigma))

@@ -469,6 +469,208 @@ __global__ void densify_kernel(long long m_local, long long n, const long long* 
         out[row * n + col[e]] = val[e];
 }
 
+
+// ---- shared-memory-tiled SpMM for wide panels (TilePlanView) ---------------
+// One CTA (16 warps) per (work item, 32*Q-column chunk of the panel).  A work
+// item is a run of tiles of one kTileRows-row block.  Per tile the CTA stages
+// the tile's distinct panel rows (kTileSlots x 32Q doubles), its entries
+// (value, slot) and row offsets in shared memory with cp.async, double
+// buffered: tile t+1 streams in while tile t is consumed.  Warp q owns rows
+// 8q..8q+7 of the block, lane j columns c0 + Q*j .. c0 + Q*j + Q-1; each row
+// accumulates in registers over its entries in (tile, slot) order — fixed,
+// so the result is deterministic.  The panel row an entry reads comes from
+// shared memory, so the L2 -> SM traffic per entry falls by the tile's reuse
+// (entries per slot); each entry costs one broadcast record load, Q/2
+// 16-byte panel loads and Q FMAs per lane.
+constexpr int kTileThreads = 512;
+constexpr int kTileRowsPerWarp = kTileRows / (kTileThreads / 32);
+static_assert(kTileRowsPerWarp == 8, "row split");
+constexpr size_t kStageX = static_cast<size_t>(kTileSlots) * 128 * sizeof(double);
+constexpr size_t kStageE = static_cast<size_t>(kTileEnts) * sizeof(TileEnt);
+constexpr size_t kStageR = static_cast<size_t>(kTileRoffStride) * sizeof(unsigned short);
+constexpr size_t kStageBytes = kStageX + kStageE + kStageR;
+constexpr size_t kTileSmem = 2 * kStageBytes + 2 * (kTileItemTiles + 1) * sizeof(int);
+static_assert(kStageR % 16 == 0, "roff stage");
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_bytes) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Q columns per lane; V16: 16-byte panel pieces (X 16-byte aligned, ldx and
+// w even)
+template <int Q, bool V16>
+__global__ void __launch_bounds__(kTileThreads, 1)
+    tile_spmm_kernel(TilePlanView P, const double* __restrict__ X, long long ldx, long long w,
+                     double* __restrict__ out, long long ldo, double* __restrict__ partial) {
+    constexpr int WC = 32 * Q;                                  // chunk width
+    constexpr int PIECES = kTileSlots * WC / 2;                 // 16-byte pieces per X stage
+    constexpr int PPT = (PIECES + kTileThreads - 1) / kTileThreads;
+    extern __shared__ __align__(16) unsigned char tsm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int item = blockIdx.x;
+    const long long c0 = static_cast<long long>(blockIdx.y) * WC;
+    const int t0 = P.item_t0[item], nt = P.item_t1[item] - t0;
+    const long long blk = P.item_blk[item];
+    const int part = P.item_part[item];
+    // the item's tile metadata (entry / slot offsets, item-relative) in
+    // shared memory once, so no per-tile global load sits on the critical path
+    int* me = reinterpret_cast<int*>(tsm + 2 * kStageBytes);  // [nt + 1]
+    int* mu = me + (kTileItemTiles + 1);                       // [nt + 1]
+    const long long e_base = P.tile_e[t0], u_base = P.tile_u[t0];
+    for (int i = tid; i <= nt; i += kTileThreads) {
+        me[i] = static_cast<int>(P.tile_e[t0 + i] - e_base);
+        mu[i] = static_cast<int>(P.tile_u[t0 + i] - u_base);
+    }
+    __syncthreads();
+    const TileEnt* ent = P.ent + e_base;
+    const int* ucol = P.ucol + u_base;
+
+    // gather indices of the next tile to stage, loaded one tile ahead so the
+    // cp.async issue never waits on them (ucol is padded by kTileSlots)
+    int ucn[PPT];
+    auto load_ucol = [&](int t) {
+        const int u0 = mu[t];
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+            const int g = tid + j * kTileThreads;
+            ucn[j] = g < PIECES ? __ldg(ucol + u0 + g / (WC / 2)) : 0;
+        }
+    };
+    auto stage = [&](int t, int buf) {
+        unsigned char* base = tsm + static_cast<size_t>(buf) * kStageBytes;
+        double* xs = reinterpret_cast<double*>(base);
+        const int nu = mu[t + 1] - mu[t];
+#pragma unroll
+        for (int j = 0; j < PPT; ++j) {
+            const int g = tid + j * kTileThreads;
+            const int sl = g / (WC / 2), pc = g - sl * (WC / 2);
+            if (g < PIECES && sl < nu) {
+                const double* row = X + static_cast<long long>(ucn[j]) * ldx;
+                const long long col = c0 + 2 * pc;
+                if (V16) {
+                    cp_async16(xs + sl * WC + 2 * pc, row + (col < w ? col : 0), col < w ? 16 : 0);
+                } else {
+                    cp_async8(xs + sl * WC + 2 * pc, row + (col < w ? col : 0), col < w ? 8 : 0);
+                    cp_async8(xs + sl * WC + 2 * pc + 1, row + (col + 1 < w ? col + 1 : 0), col + 1 < w ? 8 : 0);
+                }
+            }
+        }
+        const int e0 = me[t], ne = me[t + 1] - e0;
+        TileEnt* es = reinterpret_cast<TileEnt*>(base + kStageX);
+        for (int k = tid; k < ne; k += kTileThreads) cp_async16(es + k, ent + e0 + k, 16);
+        unsigned short* rs = reinterpret_cast<unsigned short*>(base + kStageX + kStageE);
+        const unsigned short* rsrc = P.roff + static_cast<long long>(t0 + t) * kTileRoffStride;
+        if (tid < static_cast<int>(kStageR / 16)) cp_async16(rs + tid * 8, rsrc + tid * 8, 16);
+        cp_async_commit();
+    };
+
+    double acc[kTileRowsPerWarp][Q];
+#pragma unroll
+    for (int r = 0; r < kTileRowsPerWarp; ++r)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) acc[r][q] = 0.0;
+
+    if (nt > 0) {
+        load_ucol(0);
+        stage(0, 0);
+    }
+#pragma unroll 1
+    for (int t = 0; t < nt; ++t) {
+        const int buf = t & 1;
+        if (t + 1 < nt) {
+            load_ucol(t + 1);
+            stage(t + 1, buf ^ 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const unsigned char* base = tsm + static_cast<size_t>(buf) * kStageBytes;
+        const double* xs = reinterpret_cast<const double*>(base) + lane * Q;
+        const TileEnt* es = reinterpret_cast<const TileEnt*>(base + kStageX);
+        const unsigned short* rs =
+            reinterpret_cast<const unsigned short*>(base + kStageX + kStageE) + warp * kTileRowsPerWarp;
+        const int rb = lane <= kTileRowsPerWarp ? rs[lane] : 0;
+        int k = __shfl_sync(0xffffffffu, rb, 0);
+#pragma unroll
+        for (int r = 0; r < kTileRowsPerWarp; ++r) {
+            const int e = __shfl_sync(0xffffffffu, rb, r + 1);
+#pragma unroll 2
+            for (; k < e; ++k) {
+                const TileEnt p = es[k];
+                const double* xr = xs + p.slot * WC;
+                if (Q == 4) {
+                    const double2 a = *reinterpret_cast<const double2*>(xr);
+                    const double2 b = *reinterpret_cast<const double2*>(xr + 2);
+                    acc[r][0] = fma(p.v, a.x, acc[r][0]);
+                    acc[r][1 % Q] = fma(p.v, a.y, acc[r][1 % Q]);
+                    acc[r][2 % Q] = fma(p.v, b.x, acc[r][2 % Q]);
+                    acc[r][3 % Q] = fma(p.v, b.y, acc[r][3 % Q]);
+                } else if (Q == 2) {
+                    const double2 a = *reinterpret_cast<const double2*>(xr);
+                    acc[r][0] = fma(p.v, a.x, acc[r][0]);
+                    acc[r][1 % Q] = fma(p.v, a.y, acc[r][1 % Q]);
+                } else {
+                    acc[r][0] = fma(p.v, xr[0], acc[r][0]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    const long long row0 = blk * kTileRows + warp * kTileRowsPerWarp;
+#pragma unroll
+    for (int r = 0; r < kTileRowsPerWarp; ++r) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const long long col = c0 + lane * Q + q;
+            if (col >= w) continue;
+            if (part < 0) {
+                const long long row = row0 + r;
+                if (row < P.nrows) out[row * ldo + col] = acc[r][q];
+            } else {
+                partial[(static_cast<long long>(part) * kTileRows + warp * kTileRowsPerWarp + r) * w + col] =
+                    acc[r][q];
+            }
+        }
+    }
+}
+
+// blocks spread over several items: out rows = sum of the items' partial
+// rows in item order (deterministic); grid (nsplit, column chunks)
+__global__ void __launch_bounds__(256) tile_split_reduce_kernel(TilePlanView P, long long w,
+                                                                const double* __restrict__ partial,
+                                                                double* __restrict__ out, long long ldo) {
+    const int sidx = blockIdx.x;
+    const long long col = static_cast<long long>(blockIdx.y) * 32 + (threadIdx.x & 31);
+    if (col >= w) return;
+    const long long blk = P.split_blk[sidx];
+    const int first = P.split_first[sidx], cnt = P.split_count[sidx];
+    for (int r = threadIdx.x >> 5; r < kTileRows; r += 8) {
+        const long long row = blk * kTileRows + r;
+        if (row >= P.nrows) break;
+        double s = 0.0;
+        for (int q = 0; q < cnt; ++q) s += partial[(static_cast<long long>(first + q) * kTileRows + r) * w + col];
+        out[row * ldo + col] = s;
+    }
+}
+
+// tile-ordered values from the CSR value array
+__global__ void tile_values_kernel(long long nnz, const int* __restrict__ perm, const double* __restrict__ Y,
+                                   TileEnt* __restrict__ ent) {
+    const long long f = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (f < nnz) ent[f].v = __ldg(Y + __ldg(perm + f));
+}
+
 }  // namespace
 
 void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* idx, const double* val, i64 nnz,
@@ -532,6 +734,68 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
                                                                                               out, ldo);
         }
     }
+}
+
+
+// opt-in (SVTB_TILED_SPMM=1, read per sketch): measured slower than the
+// segment kernel on the BASELINE patterns (at ~1 % density a
+// staged slot serves 2-3 entries, so the per-tile staging / barrier cost
+// outweighs the saved L2 gathers)
+bool tile_spmm_enabled() {
+    const char* e = std::getenv("SVTB_TILED_SPMM");
+    return e != nullptr && std::atoi(e) != 0;
+}
+
+void tile_values(svt_ctx* ctx, const TilePlanView& P, const double* Ycsr) {
+    if (P.nnz <= 0) return;
+    LaunchScope ls(ctx, K_OTHER, 24.0 * P.nnz, 0.0);
+    tile_values_kernel<<<static_cast<unsigned>((P.nnz + 255) / 256), 256, 0, ctx->stream>>>(P.nnz, P.perm, Ycsr,
+                                                                                           P.ent);
+}
+
+bool spmm_tiled(svt_ctx* ctx, int cls, const TilePlanView& P, i64 x_rows, i64 w, const double* X, i64 ldx,
+                double* out, i64 ldo, cudaStream_t stream, DevBuf<double>* scratch) {
+    if (P.nrows <= 0 || w <= 0) return true;
+    const i64 chunks = (w + 31) / 32;
+    // partial rows of split blocks: bounded (very wide panels of a split
+    // pattern fall back to the segment kernel)
+    const double part_bytes = 8.0 * static_cast<double>(P.nparts) * kTileRows * static_cast<double>(w);
+    if (part_bytes > 4e9 || chunks > 65535) return false;
+    cudaStream_t s = stream ? stream : ctx->stream;
+    DevBuf<double>& part = scratch ? *scratch : ctx->ws_spmm;
+    double* partial = nullptr;
+    if (P.nparts > 0) {
+        part.ensure(static_cast<size_t>(P.nparts) * kTileRows * static_cast<size_t>(w));
+        partial = part.get();
+    }
+    const bool v16 = (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (ldx % 2 == 0) && (w % 2 == 0);
+    const int Q = w > 64 ? 4 : (w > 32 ? 2 : 1);
+    static bool attr = false;
+    if (!attr) {
+#define SVT_TATTR(QQ, VV)                                                                                 \
+    SVT_CUDA(cudaFuncSetAttribute(tile_spmm_kernel<QQ, VV>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                  static_cast<int>(kTileSmem)))
+        SVT_TATTR(1, true); SVT_TATTR(1, false); SVT_TATTR(2, true); SVT_TATTR(2, false);
+        SVT_TATTR(4, true); SVT_TATTR(4, false);
+#undef SVT_TATTR
+        attr = true;
+    }
+    LaunchScope ls(ctx, cls, 12.0 * P.nnz + 8.0 * (P.nrows + 1) + 8.0 * w * (x_rows + P.nrows), 2.0 * P.nnz * w, s);
+    const dim3 grid(static_cast<unsigned>(P.nitems), static_cast<unsigned>((w + 32 * Q - 1) / (32 * Q)));
+#define SVT_TL(QQ)                                                                                       \
+    (v16 ? tile_spmm_kernel<QQ, true><<<grid, kTileThreads, kTileSmem, s>>>(P, X, ldx, w, out, ldo, partial) \
+         : tile_spmm_kernel<QQ, false><<<grid, kTileThreads, kTileSmem, s>>>(P, X, ldx, w, out, ldo, partial))
+    if (Q == 4)
+        SVT_TL(4);
+    else if (Q == 2)
+        SVT_TL(2);
+    else
+        SVT_TL(1);
+#undef SVT_TL
+    if (P.nsplit > 0)
+        tile_split_reduce_kernel<<<dim3(static_cast<unsigned>(P.nsplit), static_cast<unsigned>(chunks)), 256, 0, s>>>(
+            P, w, partial, out, ldo);
+    return true;
 }
 
 void sddmm_update(svt_ctx* ctx, const SegPlanView& plan, i64 m_local, const int* col, const double* A, double* Y,
