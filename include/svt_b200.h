@@ -235,6 +235,13 @@ int svt_dev_gemm(svt_ctx* ctx, int transA, int64_t M, int64_t N, int64_t K, doub
  * (SVD of B through its Gram), exposed for its own parity tests.  G is not
  * modified.  Synchronous. */
 int svt_dev_sym_eig(svt_ctx* ctx, const double* G, int64_t r, double* W, double* lambda);
+/* C (M x N, row-major, ld ldc) = A^T B for row-major FP64 device operands A
+ * (K x M, ld lda) and B (K x N, ld ldb), computed on the INT8 tensor cores
+ * by the Ozaki digit-splitting scheme (slices = int8 digits per entry, 6..8;
+ * 8 carries the FP64 GEMM error bound).  The FP64 contraction of the
+ * Gram-Schmidt step (sketch.hpp:133-141, Q^T X) in this form. */
+int svt_dev_gemm_tn_ozaki(svt_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                          const double* B, int64_t ldb, double* C, int64_t ldc, int slices);
 
 /* Device-pointer sparse products on the context stream (row-major panels):
  * out (m_local x w) = S * X (X: n x w) or, transpose != 0, out (n x w) = S^T * X

@@ -172,6 +172,26 @@ def dev_gemm(a, b, c, trans_a=False, alpha=1.0, beta=0.0, ctx: Context | None = 
     return c
 
 
+def dev_gemm_tn_ozaki(a, b, slices: int = 8, ctx: Context | None = None):
+    """a.T @ b for row-major float64 CUDA tensors a (K x M), b (K x N) on the
+    INT8 tensor cores (Ozaki digit slices; svt_dev_gemm_tn_ozaki)."""
+    import torch
+    ctx = ctx or default_context()
+    for t in (a, b):
+        if not (t.is_cuda and t.dtype == torch.float64 and t.dim() == 2 and t.stride(1) == 1):
+            raise InvalidArgument("dev_gemm_tn_ozaki: row-major float64 CUDA matrices required")
+    if a.shape[0] != b.shape[0]:
+        raise InvalidArgument("dev_gemm_tn_ozaki: K mismatch")
+    K, M = a.shape
+    N = b.shape[1]
+    c = torch.empty((M, N), dtype=torch.float64, device=a.device)
+    torch.cuda.synchronize()
+    _check(lib().svt_dev_gemm_tn_ozaki(ctx.h, C.c_int64(M), C.c_int64(N), C.c_int64(K), C.c_void_p(a.data_ptr()),
+                                       C.c_int64(a.stride(0)), C.c_void_p(b.data_ptr()), C.c_int64(b.stride(0)),
+                                       C.c_void_p(c.data_ptr()), C.c_int64(N), C.c_int(slices)))
+    return c
+
+
 def dev_sym_eig(g, ctx: Context | None = None):
     """(lambda descending, W) with g = W diag(lambda) W^T for a symmetric
     row-major contiguous float64 CUDA tensor (svt_dev_sym_eig; the Gram

@@ -11,7 +11,7 @@ OUT_DIR = os.path.join(HERE, "lib")
 OUT = os.path.join(OUT_DIR, "libsvt_b200.so")
 OBJ = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["rng.cu", "sparse.cu", "dense.cu", "build.cu", "io.cpp", "runtime.cpp", "host.cpp", "engine.cpp", "solver.cpp", "capi.cpp",
+SOURCES = ["rng.cu", "sparse.cu", "dense.cu", "ozaki.cu", "build.cu", "io.cpp", "runtime.cpp", "host.cpp", "engine.cpp", "solver.cpp", "capi.cpp",
            "synth.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",

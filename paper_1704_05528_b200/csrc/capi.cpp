@@ -118,10 +118,14 @@ int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, sv
         SVT_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
         SVT_CUDA(cudaMallocHost(&c->h_scalars, 64 * sizeof(double)));
         SVT_CUDA(cudaMallocHost(&c->h_flags, 64 * sizeof(int)));
+        c->h_stage_n = 1 << 16;
+        SVT_CUDA(cudaMallocHost(&c->h_stage, c->h_stage_n * sizeof(double)));
         SVT_CUDA(cudaMalloc(&c->d_scalars, 64 * sizeof(double)));
         SVT_CUDA(cudaMalloc(&c->d_flags, 64 * sizeof(int)));
         SVT_CUDA(cudaMemsetAsync(c->d_scalars, 0, 64 * sizeof(double), c->stream));
         SVT_CUDA(cudaMemsetAsync(c->d_flags, 0, 64 * sizeof(int), c->stream));
+        c->d_tickets.alloc(kTickets);
+        SVT_CUDA(cudaMemsetAsync(c->d_tickets.get(), 0, kTickets * sizeof(unsigned), c->stream));
         nccl_init(c->comm, rank, world, nccl_id);
         sync_stream(c.get());
         *out = c.release();
@@ -160,6 +164,7 @@ int svt_ctx_destroy(svt_ctx* ctx) {
         cudaFree(ctx->d_flags);
         cudaFreeHost(ctx->h_scalars);
         cudaFreeHost(ctx->h_flags);
+        if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
         cudaStreamDestroy(ctx->stream);
         if (ctx->side) cudaStreamDestroy(ctx->side);
         delete ctx;
@@ -654,6 +659,19 @@ int svt_dev_sym_eig(svt_ctx* ctx, const double* G, int64_t r, double* W, double*
         DevBuf<double> Gc(static_cast<size_t>(r * r));
         SVT_CUDA(cudaMemcpyAsync(Gc.get(), G, sizeof(double) * r * r, cudaMemcpyDeviceToDevice, ctx->stream));
         sym_eig(ctx, Gc.get(), r, W, lambda);
+        sync_stream(ctx);
+    });
+}
+
+int svt_dev_gemm_tn_ozaki(svt_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                          const double* B, int64_t ldb, double* C, int64_t ldc, int slices) {
+    return guard([&] {
+        need(ctx, "svt_dev_gemm_tn_ozaki");
+        if (M < 0 || N < 0 || K < 0 || lda < M || ldb < N || ldc < N || slices < 6 || slices > 8)
+            throw std::invalid_argument("dev_gemm_tn_ozaki: bad shape or slice count");
+        if (M == 0 || N == 0) return;
+        if (!A || !B || !C) throw std::invalid_argument("dev_gemm_tn_ozaki: null operand");
+        gemm_tn_ozaki(ctx, M, N, K, 1.0, A, lda, B, ldb, 0.0, C, ldc, slices);
         sync_stream(ctx);
     });
 }

@@ -115,6 +115,9 @@ struct DevBuf {
     T* get() const { return p; }
 };
 
+// arrival counters of the single-launch column reductions (one per 32-column block)
+constexpr size_t kTickets = 4096;
+
 // Kernel classes for instrumentation (svt_ctx_kernel_stats).
 enum KClass : int { K_SPMM = 0, K_SPMMT = 1, K_SDDMM = 2, K_GEMM = 3, K_RNG = 4, K_QR = 5, K_FINAL = 6, K_OTHER = 7, K_NCLASS = 8 };
 
@@ -225,8 +228,13 @@ struct svt_ctx {
     double* d_scalars = nullptr;  // device, 64 doubles
     int* d_flags = nullptr;       // device, 64 ints
     int* h_flags = nullptr;       // pinned, 64 ints
+    double* h_stage = nullptr;    // pinned staging for small device -> host reads
+    size_t h_stage_n = 0;
     svtb::DevBuf<double> ws_partial;   // split-K / reduction partials
+    svtb::DevBuf<double> ws_ozaki;     // int8 digit slices of the Ozaki-scheme GEMM (raw bytes)
+    svtb::DevBuf<int> ws_ozexp;        // their per-column exponents
     svtb::DevBuf<double> ws_partial2;  // second partial buffer (reductions)
+    svtb::DevBuf<unsigned> d_tickets;  // self-resetting arrival counters (single-launch reductions)
     svtb::DevBuf<double> ws_spmm;      // long-row partials of the segmented SpMM
     svtb::DevBuf<unsigned> ws_counters;  // last-CTA-reduces counters (self-resetting)
     svtb::DevBuf<unsigned long long> ws_rng;  // raw mt19937_64 draws

@@ -1920,6 +1920,56 @@ __global__ void col_sumsq_partial_kernel(const double* __restrict__ X, long long
     }
 }
 
+// Single-launch variant: every (column block, row part) CTA writes its
+// partial sums; the last CTA to arrive for a column block (arrival counter)
+// adds the parts in part order — the same fixed order as the two-kernel
+// path, so the result is deterministic — and resets the counter.
+__global__ void col_sumsq_fused_kernel(const double* __restrict__ X, long long rows, long long cols, long long ld,
+                                       long long rows_per_block, double* __restrict__ partial,
+                                       double* __restrict__ out, unsigned* __restrict__ tickets) {
+    const long long j = blockIdx.x * 32LL + (threadIdx.x & 31);
+    const int ty = threadIdx.x >> 5;  // 8 row lanes
+    __shared__ double red[8][33];
+    __shared__ bool last;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    const long long r0 = blockIdx.y * rows_per_block;
+    const long long r1 = min(rows, r0 + rows_per_block);
+    if (j < cols) {
+        long long i = r0 + ty;
+        for (; i + 24 < r1; i += 32) {
+            const double a = X[i * ld + j], b = X[(i + 8) * ld + j];
+            const double c = X[(i + 16) * ld + j], d = X[(i + 24) * ld + j];
+            s0 = fma(a, a, s0);
+            s1 = fma(b, b, s1);
+            s2 = fma(c, c, s2);
+            s3 = fma(d, d, s3);
+        }
+        for (; i < r1; i += 8) {
+            const double v = X[i * ld + j];
+            s0 = fma(v, v, s0);
+        }
+    }
+    red[ty][threadIdx.x & 31] = (s0 + s1) + (s2 + s3);
+    __syncthreads();
+    if (ty == 0 && j < cols) {
+        double t = 0.0;
+        for (int q = 0; q < 8; ++q) t += red[q][threadIdx.x & 31];
+        partial[blockIdx.y * cols + j] = t;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(tickets + blockIdx.x, 1u) == gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (ty == 0 && j < cols) {
+        double t = 0.0;
+        for (unsigned p = 0; p < gridDim.y; ++p) t += __ldcg(partial + p * cols + j);
+        out[j] = t;
+    }
+    if (threadIdx.x == 0) tickets[blockIdx.x] = 0;
+}
+
 __global__ void col_sumsq_finish_kernel(const double* __restrict__ partial, long long cols, int nparts,
                                         double* __restrict__ out) {
     const long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -2220,6 +2270,11 @@ void col_sumsq(svt_ctx* ctx, const double* X, i64 rows, i64 cols, i64 ld, double
     ctx->ws_partial2.ensure(static_cast<size_t>(nparts * cols));
     LaunchScope ls(ctx, K_OTHER, 8.0 * rows * cols, 2.0 * rows * cols);
     dim3 grid(static_cast<unsigned>((cols + 31) / 32), static_cast<unsigned>(nparts));
+    if (ctx->d_tickets.get() != nullptr && static_cast<size_t>(grid.x) <= kTickets) {
+        col_sumsq_fused_kernel<<<grid, 256, 0, ctx->stream>>>(X, rows, cols, ld, rpb, ctx->ws_partial2.get(), out,
+                                                              ctx->d_tickets.get());
+        return;
+    }
     col_sumsq_partial_kernel<<<grid, 256, 0, ctx->stream>>>(X, rows, cols, ld, rpb, ctx->ws_partial2.get());
     col_sumsq_finish_kernel<<<nblk(cols), 256, 0, ctx->stream>>>(ctx->ws_partial2.get(), cols,
                                                                  static_cast<int>(nparts), out);

@@ -43,6 +43,34 @@ int read_flag(svt_ctx* c, int i) {
     return c->h_flags[i];
 }
 
+// small device -> host read through the pinned staging buffer (a pageable
+// destination makes the copy a staged, host-synchronous transfer), then one
+// stream synchronization
+void read_doubles(svt_ctx* c, const double* d, size_t count, double* out) {
+    if (count == 0) return;
+    if (count > c->h_stage_n) {
+        SVT_CUDA(cudaMemcpyAsync(out, d, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+        sync_stream(c);
+        return;
+    }
+    SVT_CUDA(cudaMemcpyAsync(c->h_stage, d, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+    sync_stream(c);
+    std::memcpy(out, c->h_stage, sizeof(double) * count);
+}
+void read_doubles2(svt_ctx* c, const double* d1, const double* d2, size_t count, double* o1, double* o2) {
+    if (2 * count > c->h_stage_n) {
+        SVT_CUDA(cudaMemcpyAsync(o1, d1, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+        SVT_CUDA(cudaMemcpyAsync(o2, d2, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+        sync_stream(c);
+        return;
+    }
+    SVT_CUDA(cudaMemcpyAsync(c->h_stage, d1, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+    SVT_CUDA(cudaMemcpyAsync(c->h_stage + count, d2, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+    sync_stream(c);
+    std::memcpy(o1, c->h_stage, sizeof(double) * count);
+    std::memcpy(o2, c->h_stage + count, sizeof(double) * count);
+}
+
 bool debug_batch() {
     static const bool on = std::getenv("SVTB_DEBUG_BATCH") != nullptr;
     return on;
@@ -234,12 +262,14 @@ void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo, c
 }
 
 void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out, cudaStream_t stream,
-               DevBuf<double>* scratch) {
+               DevBuf<double>* scratch, i64 ldo) {
     svt_mat* A = E.mat;
+    if (ldo < 0) ldo = w;
+    if (ldo != w && E.ctx->comm.world > 1) throw std::logic_error("sp_mult_t: strided output needs one rank");
     if (!(tiles_ready(E, w, stream) &&
-          spmm_tiled(E.ctx, K_SPMMT, A->tile_csc.v, A->m_local, w, X, ldx, out, w, stream, scratch)))
+          spmm_tiled(E.ctx, K_SPMMT, A->tile_csc.v, A->m_local, w, X, ldx, out, ldo, stream, scratch)))
         spmm(E.ctx, K_SPMMT, A->plan_csc.v, A->n, A->cscrow.get(), E.Y.csc, A->nnz_local, A->m_local, w, X, ldx, out,
-             w, stream, scratch);
+             ldo, stream, scratch);
     E.ctx->comm.allreduce_sum(out, static_cast<size_t>(A->n * w), stream ? stream : E.ctx->stream);
 }
 
@@ -318,6 +348,11 @@ static void power_iterate(Engine& E, i64 w, int np) {
 // B[r0:r0+w, :] = (Y^T Q[:, r0:r0+w])^T stored as B^T columns; norm_b_sq +=
 static void append_coefficients(Engine& E, QBDev& st, i64 r0, i64 w, int nb_op) {
     svt_ctx* c = E.ctx;
+    if (c->comm.world == 1) {  // straight into the coefficient rows (no staging copy)
+        sp_mult_t(E, w, st.Q.get() + r0, st.cap, st.Bt.get() + r0, nullptr, nullptr, st.cap);
+        sumsq(c, st.Bt.get() + r0, st.n, w, st.cap, dsc(c, S_NB), nb_op);
+        return;
+    }
     E.T.ensure(static_cast<size_t>(st.n * w));
     sp_mult_t(E, w, st.Q.get() + r0, st.cap, E.T.get());
     copy2d(c, E.T.get(), w, st.Bt.get() + r0, st.cap, st.n, w);
@@ -415,8 +450,7 @@ void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFact
     gemm(c, K_FINAL, true, r, r, n, 1.0, st.Bt.get(), st.cap, st.Bt.get(), st.cap, 0.0, E.G.get(), r);
     sym_eig(c, E.G.get(), r, E.W.get(), E.lam.get());
     std::vector<double> lam(static_cast<size_t>(r));
-    SVT_CUDA(cudaMemcpyAsync(lam.data(), E.lam.get(), sizeof(double) * r, cudaMemcpyDeviceToHost, c->stream));
-    sync_stream(c);
+    read_doubles(c, E.lam.get(), static_cast<size_t>(r), lam.data());
     i64 kc = r;
     if (mode == FinalizeMode::Kept) {
         i64 cnt = 0;
@@ -429,8 +463,7 @@ void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFact
     E.lam.ensure(static_cast<size_t>(std::max(r, kc)));
     col_sumsq(c, E.Vraw.get(), n, kc, kc, E.lam.get());
     std::vector<double> s2(static_cast<size_t>(kc));
-    SVT_CUDA(cudaMemcpyAsync(s2.data(), E.lam.get(), sizeof(double) * kc, cudaMemcpyDeviceToHost, c->stream));
-    sync_stream(c);
+    read_doubles(c, E.lam.get(), static_cast<size_t>(kc), s2.data());
     std::vector<double> sig(static_cast<size_t>(kc));
     for (i64 j = 0; j < kc; ++j) sig[static_cast<size_t>(j)] = std::sqrt(s2[static_cast<size_t>(j)]);
     std::vector<int> perm(static_cast<size_t>(kc));
@@ -538,9 +571,7 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
         col_sumsq(c, Zt.get(), r, b, b, res2.get());
         th_h.resize(static_cast<size_t>(b));
         res_h.resize(static_cast<size_t>(b));
-        SVT_CUDA(cudaMemcpyAsync(th_h.data(), th.get(), sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream));
-        SVT_CUDA(cudaMemcpyAsync(res_h.data(), res2.get(), sizeof(double) * b, cudaMemcpyDeviceToHost, c->stream));
-        sync_stream(c);
+        read_doubles2(c, th.get(), res2.get(), static_cast<size_t>(b), th_h.data(), res_h.data());
         kk = 0;
         while (kk < b && th_h[static_cast<size_t>(kk)] > tau2 * (1.0 - 1e-6)) ++kk;
         if (kk == b && b < r) {
@@ -632,8 +663,7 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
     E.lam.ensure(static_cast<size_t>(kc));
     col_sumsq(c, E.Vraw.get(), n, kc, kc, E.lam.get());
     std::vector<double> s2(static_cast<size_t>(kc));
-    SVT_CUDA(cudaMemcpyAsync(s2.data(), E.lam.get(), sizeof(double) * kc, cudaMemcpyDeviceToHost, c->stream));
-    sync_stream(c);
+    read_doubles(c, E.lam.get(), static_cast<size_t>(kc), s2.data());
     std::vector<double> sig(static_cast<size_t>(kc));
     for (i64 j = 0; j < kc; ++j) sig[static_cast<size_t>(j)] = std::sqrt(s2[static_cast<size_t>(j)]);
     std::vector<int> perm(static_cast<size_t>(kc));
@@ -835,12 +865,16 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         return -1;
     }
     // coefficient rows of the whole batch and their per-block energies
-    sp_mult_t(E, W, Q + r0, ldq, E.TW.get());
-    copy2d(c, E.TW.get(), W, st.Bt.get() + r0, ldq, n, W);
-    col_sumsq(c, E.TW.get(), n, W, W, E.eW.get());
+    if (c->comm.world == 1) {  // straight into the coefficient rows (no staging copy)
+        sp_mult_t(E, W, Q + r0, ldq, st.Bt.get() + r0, nullptr, nullptr, ldq);
+        col_sumsq(c, st.Bt.get() + r0, n, W, ldq, E.eW.get());
+    } else {
+        sp_mult_t(E, W, Q + r0, ldq, E.TW.get());
+        copy2d(c, E.TW.get(), W, st.Bt.get() + r0, ldq, n, W);
+        col_sumsq(c, E.TW.get(), n, W, W, E.eW.get());
+    }
     std::vector<double> e(static_cast<size_t>(W));
-    SVT_CUDA(cudaMemcpyAsync(e.data(), E.eW.get(), sizeof(double) * W, cudaMemcpyDeviceToHost, c->stream));
-    sync_stream(c);
+    read_doubles(c, E.eW.get(), static_cast<size_t>(W), e.data());
     // replay the reference's loop test round by round
     int accepted = 0;
     for (int k = 0; k < K; ++k) {

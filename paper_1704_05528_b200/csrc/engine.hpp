@@ -132,7 +132,7 @@ double frob_sq(Engine& E);  // ||Y||_F^2 (all ranks)
 void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo, cudaStream_t stream = nullptr,
              DevBuf<double>* scratch = nullptr);
 void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out, cudaStream_t stream = nullptr,
-               DevBuf<double>* scratch = nullptr);
+               DevBuf<double>* scratch = nullptr, i64 ldo = -1);  // ldo != w: single rank only
 void qr_orthonormal(Engine& E, double* X, i64 ldx, i64 w, double* Qout, i64 ldq);            // dense.hpp:103
 void qr_orthonormal(Engine& E, i64 rows, bool dist, double* X, i64 ldx, i64 w, double* Qout, i64 ldq);
 double spectral_norm_est(Engine& E, int iters, u64 seed);

@@ -64,6 +64,12 @@ void axpy_values(svt_ctx* ctx, i64 nnz, const double* a, double alpha, const dou
 void densify_dev(svt_ctx* ctx, i64 m_local, i64 n, const i64* rowptr, const int* col, const double* val,
                  double* out);
 
+// ---- FP64 on the INT8 tensor cores (ozaki.cu) ----------------------------------
+// C (M x N) = alpha * A^T B + beta * C; A: K x M, B: K x N, row-major FP64;
+// slices = int8 digits per entry (8: FP64-equivalent, 6..8 accepted).
+void gemm_tn_ozaki(svt_ctx* ctx, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
+                   i64 ldb, double beta, double* C, i64 ldc, int slices = 8);
+
 // ---- dense ------------------------------------------------------------------
 // C (M x N) = alpha * op(A) * B + beta * C; op(A) = A^T when transA (A stored
 // K x M row-major), else A (M x K row-major).  B is K x N row-major.  Large K

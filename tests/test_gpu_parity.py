@@ -498,6 +498,27 @@ def test_dev_sym_eig_matches_fp64_reference(r, decay, scalar, monkeypatch):
     assert (W.T @ W - torch.eye(r, dtype=torch.float64, device="cuda")).abs().max().item() <= 1e-11
 
 
+# ---- FP64 contraction on the INT8 tensor cores (csrc/ozaki.cu, tcgen05 kind::i8)
+@pytest.mark.parametrize("K,M,N", [(1, 1, 1), (1000, 100, 37), (20000, 300, 128), (40000, 129, 65)])
+def test_ozaki_tn_matches_fp64(K, M, N):
+    """C = A^T B from int8 digit slices: with 8 slices the error is within
+    the FP64 GEMM scale, |C - C_ref| <= 1e-15 (|A|^T |B|) elementwise
+    (measured 1-3e-16); 7 / 6 slices degrade by 2^7 per slice.  Columns of A
+    span 2^±12 in magnitude (the per-column exponents), one column is zero."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(K + M + N)
+    A = torch.randn(K, M, dtype=torch.float64, device="cuda", generator=g)
+    A *= torch.exp2(torch.randint(-12, 13, (1, M), device="cuda", generator=g).double())
+    A[:, M // 2] = 0.0
+    B = torch.randn(K, N, dtype=torch.float64, device="cuda", generator=g)
+    ref = A.T @ B
+    scale = A.abs().T @ B.abs()
+    for S, tol in ((8, 1e-15), (7, 1.5e-13), (6, 2e-11)):
+        C = G.dev_gemm_tn_ozaki(A, B, S)
+        assert ((C - ref).abs() <= tol * scale + 1e-300).all(), S
+    assert torch.equal(G.dev_gemm_tn_ozaki(A, B, 8), G.dev_gemm_tn_ozaki(A, B, 8))  # deterministic
+
+
 # ---- device-side sample-set construction (csrc/build.cu) ----------------------
 def _skewed_csr(seed):
     """Rows and columns longer than one 512-entry segment, empty rows and
