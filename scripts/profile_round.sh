@@ -24,3 +24,11 @@ echo "full sddmm rc=$?"
 # cfg5 shapes of the CGS contraction in isolation (scripts/gemm_bench.py)
 ncu --set full --clock-control none --import-source on -k regex:dmma --launch-skip 3 -c 1 \
     -o gpurun_out/full_dmma_tn_cfg5 python scripts/gemm_bench.py 4 > gpurun_out/ncu_full5.log 2>&1; echo "full tn5 rc=$?"
+# tcgen05 INT8 (Ozaki) FP64 contraction on the cfg4 CGS shape
+ncu --set full --clock-control none --import-source on -k regex:ozaki_tn -c 1 \
+    -o gpurun_out/full_ozaki_tn python scripts/ozaki_bench.py 69878x1322x120 > gpurun_out/ncu_full6.log 2>&1; echo "full ozaki rc=$?"
+# cfg5 bench line (no CPU leg: an oracle iteration takes hours) and the per-config table
+python bench.py --config 5 --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_cfg5.log 2>&1; echo "bench cfg5 rc=$?"
+tail -1 gpurun_out/bench_cfg5.log > gpurun_out/bench_cfg5.json
+python scripts/config_table.py 1,2,3,4 > gpurun_out/config_table.log 2>&1; echo "table rc=$?"
+cp profiles/r01_config_table.json gpurun_out/config_table.json
