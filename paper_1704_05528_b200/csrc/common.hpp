@@ -233,6 +233,8 @@ struct svt_ctx {
     svtb::DevBuf<double> ws_partial;   // split-K / reduction partials
     svtb::DevBuf<double> ws_ozaki;     // int8 digit slices of the Ozaki-scheme GEMM (raw bytes)
     svtb::DevBuf<int> ws_ozexp;        // their per-column exponents
+    svtb::DevBuf<double> ws_ozakib;    // B-operand slices
+    svtb::DevBuf<int> ws_ozexpb;
     svtb::DevBuf<double> ws_partial2;  // second partial buffer (reductions)
     svtb::DevBuf<unsigned> d_tickets;  // self-resetting arrival counters (single-launch reductions)
     svtb::DevBuf<double> ws_spmm;      // long-row partials of the segmented SpMM

@@ -145,6 +145,7 @@ void reset_qb(QBDev& st, const svt_mat* A) {
     st.n = A->n;
     st.min_dim = std::min(A->m, A->n);
     st.rank = 0;
+    st.qs_valid = 0;
     st.norm_b_sq = 0.0;
     st.frob_y_sq = 0.0;
     st.saturated = false;
@@ -732,6 +733,52 @@ static void finalize_mode(Engine& E, const QBDev& st, FinalizeMode mode, double 
 // -1 when the panel is numerically rank deficient (the caller re-runs the
 // rounds one by one with the exact fallback semantics).
 // Sketch of a batch (Omega for rounds round0 .. round0 + K - 1, then
+// Gram-Schmidt coefficients C (r0 x w) = Q[:, :r0]^T X (sketch.hpp:133) on
+// the INT8 tensor cores from cached digit slices of the basis (ozaki.cu;
+// SVTB_OZAKI=1), else the DMMA GEMM.  The slices of a column are built once,
+// the first time the column takes part in a product.
+static bool ozaki_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SVTB_OZAKI");
+        return e != nullptr && std::atoi(e) != 0;
+    }();
+    return on;
+}
+
+static void basis_tx(Engine& E, QBDev& st, i64 r0, i64 w, const double* X, i64 ldx, double* C) {
+    svt_ctx* c = E.ctx;
+    const i64 m = st.m_local;
+    const double* Q = st.Q.get();
+    if (ozaki_enabled() && m >= 4096 && r0 >= 64 && w > 16) {
+        const i64 tiles = ozaki_rows_pad(st.cap) / 128;
+        const size_t bytes = static_cast<size_t>(8) * tiles * 128 * ozaki_kpad(m);
+        if (st.qs_tiles != tiles) {
+            st.qs.release();
+            st.qe.release();
+            st.qs_tiles = 0;
+            st.qs_valid = 0;
+            size_t free_b = 0, total_b = 0;
+            SVT_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            if (bytes < free_b / 2) {
+                st.qs.alloc(bytes / 8 + 2);
+                st.qe.alloc(static_cast<size_t>(tiles * 128));
+                st.qs_tiles = tiles;
+            }
+        }
+        if (st.qs_tiles == tiles) {
+            int8_t* sl = reinterpret_cast<int8_t*>(st.qs.get());
+            if (st.qs_valid < r0) {
+                ozaki_slice_basis(c, Q + st.qs_valid, m, r0 - st.qs_valid, st.cap, st.qs_valid, sl, tiles,
+                                  st.qe.get());
+                st.qs_valid = r0;
+            }
+            gemm_tn_ozaki_cached(c, r0, w, m, sl, tiles, st.qe.get(), X, ldx, C, w);
+            return;
+        }
+    }
+    gemm(c, K_GEMM, true, r0, w, m, 1.0, Q, st.cap, X, ldx, 0.0, C, w);
+}
+
 // X = Y (Y^T (Y Omega))) into spec slot `slot`, on `stream` (main or side).
 static void batch_sketch(Engine& E, const svt_sketch_params& p, int round0, int K, int slot, bool side) {
     svt_ctx* c = E.ctx;
@@ -816,7 +863,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         E.CW.ensure(static_cast<size_t>(r0 * W));
         E.eW.ensure(static_cast<size_t>(3 * W));
         col_sumsq(c, XW, m, W, W, E.eW.get() + 2 * W);
-        gemm(c, K_GEMM, true, r0, W, m, 1.0, Q, ldq, XW, W, 0.0, E.CW.get(), W);
+        basis_tx(E, st, r0, W, XW, W, E.CW.get());
         allreduce(c, E.CW.get(), static_cast<size_t>(r0 * W));
         gemm(c, K_GEMM, false, m, W, r0, -1.0, Q, ldq, E.CW.get(), W, 1.0, XW, W);
         col_sumsq(c, XW, m, W, W, E.eW.get());

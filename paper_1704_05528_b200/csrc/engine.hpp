@@ -69,6 +69,12 @@ struct DevFactors {
 struct QBDev {
     i64 m_local = 0, n = 0, min_dim = 0, cap = 0, rank = 0;
     DevBuf<double> Q, Bt;
+    // INT8 digit slices of Q's leading columns for the Gram-Schmidt product
+    // Q^T X on the tensor cores (ozaki.cu): valid for columns [0, qs_valid)
+    // of this sketch; extended lazily, reset with the basis
+    DevBuf<double> qs;  // raw int8 tiles
+    DevBuf<int> qe;     // per-column exponents
+    i64 qs_tiles = 0, qs_valid = 0;
     double norm_b_sq = 0.0;
     double frob_y_sq = 0.0;
     bool saturated = false;

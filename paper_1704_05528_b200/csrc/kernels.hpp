@@ -69,6 +69,14 @@ void densify_dev(svt_ctx* ctx, i64 m_local, i64 n, const i64* rowptr, const int*
 // slices = int8 digits per entry (8: FP64-equivalent, 6..8 accepted).
 void gemm_tn_ozaki(svt_ctx* ctx, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
                    i64 ldb, double beta, double* C, i64 ldc, int slices = 8);
+// cached-A form (8 slices): the basis slices live in a 128-row tiled int8
+// array of ctiles row tiles x ozaki_kpad(K) digits per slice
+i64 ozaki_kpad(i64 K);
+i64 ozaki_rows_pad(i64 rows);
+void ozaki_slice_basis(svt_ctx* ctx, const double* X, i64 K, i64 C, i64 ld, i64 c_off, int8_t* tiles, i64 ctiles,
+                       int* e);
+void gemm_tn_ozaki_cached(svt_ctx* ctx, i64 M, i64 N, i64 K, const int8_t* tiles, i64 ctiles, const int* e,
+                          const double* B, i64 ldb, double* C, i64 ldc);
 
 // ---- dense ------------------------------------------------------------------
 // C (M x N) = alpha * op(A) * B + beta * C; op(A) = A^T when transA (A stored

@@ -42,7 +42,8 @@ namespace {
 
 constexpr int OZ_BM = 128;           // output rows per CTA (UMMA M)
 constexpr int OZ_BN = 64;            // output columns per CTA (UMMA N)
-constexpr int OZ_BK = 64;            // K bytes (= digits) per stage row
+constexpr int OZ_BK = 32;            // K bytes (= digits) per stage row: one MMA-K step
+constexpr int OZ_NST = 4;            // pipeline stages
 constexpr int OZ_KC = 16384;         // K per CTA (int32 diagonal sums cannot overflow)
 constexpr int OZ_THREADS = 128;
 
@@ -51,22 +52,22 @@ struct OzTile {
     static constexpr int A_BYTES = OZ_BM * OZ_BK;  // one slice's A tile
     static constexpr int B_BYTES = OZ_BN * OZ_BK;
     static constexpr int STAGE = S * (A_BYTES + B_BYTES);
-    static constexpr size_t SMEM = 2 * static_cast<size_t>(STAGE) + 1024;  // + alignment slack
+    static constexpr size_t SMEM = OZ_NST * static_cast<size_t>(STAGE) + 1024;  // + alignment slack
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
 
-// K-major, 64-byte swizzle (Swizzle<2,4,3>): 16-byte chunk c of row r lives
-// at chunk c ^ ((r >> 1) & 3); 8-row atoms of 512 bytes stacked along M/N.
-__device__ __forceinline__ uint64_t umma_desc_sw64(unsigned saddr) {
+// K-major, 32-byte swizzle (Swizzle<1,4,3>): 16-byte chunk c of row r lives
+// at chunk c ^ ((r >> 2) & 1); 8-row atoms of 256 bytes stacked along M/N.
+__device__ __forceinline__ uint64_t umma_desc_sw32(unsigned saddr) {
     uint64_t d = 0;
     d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);  // start address
     d |= static_cast<uint64_t>(1) << 16;                 // LBO (unused for swizzled K-major)
-    d |= static_cast<uint64_t>(512 >> 4) << 32;          // SBO: next 8-row atom
+    d |= static_cast<uint64_t>(256 >> 4) << 32;          // SBO: next 8-row atom
     d |= static_cast<uint64_t>(1) << 46;                 // descriptor version (sm_100)
-    d |= static_cast<uint64_t>(4) << 61;                 // SWIZZLE_64B
+    d |= static_cast<uint64_t>(6) << 61;                 // SWIZZLE_32B
     return d;
 }
 
@@ -95,13 +96,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
 
 template <int S>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
-    ozaki_tn_kernel(const int8_t* __restrict__ SA, long long a_pitch, long long a_slice,
-                    const int8_t* __restrict__ SB, long long b_pitch, long long b_slice,
-                    const int* __restrict__ eA, const int* __restrict__ eB, long long M, long long N,
-                    long long kchunk, long long Kpad, double* __restrict__ partial) {
+    ozaki_tn_kernel(const int8_t* __restrict__ SA, long long a_tiles, const int8_t* __restrict__ SB,
+                    long long b_tiles, const int* __restrict__ eA, const int* __restrict__ eB, long long M,
+                    long long N, long long kchunk, long long Kpad, double* __restrict__ partial) {
     using T = OzTile<S>;
     extern __shared__ __align__(1024) unsigned char oz_raw[];
-    __shared__ uint64_t mma_done[2];
+    __shared__ uint64_t mma_done[OZ_NST];
     __shared__ uint32_t tmem_base_sh;
     unsigned char* sm = oz_raw + ((1024 - (smem_u32(oz_raw) & 1023)) & 1023);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -111,14 +111,19 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     const long long k1 = min(Kpad, k0 + kchunk);
     const int nkb = static_cast<int>((k1 - k0) / OZ_BK);
 
+    // barriers: full[s] — stage s's bulk copies landed (transaction count);
+    // empty[s] (mma_done) — the MMAs reading stage s completed (tcgen05.commit)
+    __shared__ uint64_t full_bar[OZ_NST];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
             smem_u32(&tmem_base_sh)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (tid == 0) {
-        mbar_init(&mma_done[0], 1);
-        mbar_init(&mma_done[1], 1);
+        for (int q = 0; q < OZ_NST; ++q) {
+            mbar_init(&mma_done[q], 1);
+            mbar_init(&full_bar[q], 1);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -126,86 +131,77 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
     asm volatile("tcgen05.fence::after_thread_sync;\n");
     const uint32_t tmem = tmem_base_sh;
 
-    // stage issue: every thread copies its 16-byte chunks of all S slices
-    auto load = [&](int kb, int st) {
-        unsigned char* base = sm + static_cast<size_t>(st) * T::STAGE;
-        const long long kk = k0 + static_cast<long long>(kb) * OZ_BK;
+    if (warp == 1) {
+        // ---- producer (one thread): per stage one bulk copy per slice tile ----
+        if (lane == 0) {
+            const long long KT = Kpad / OZ_BK, kt0 = k0 / OZ_BK;
+            const long long mt = m0 / OZ_BM, nt = n0 / OZ_BN;
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int st = kb % OZ_NST;
+                if (kb >= OZ_NST) mbar_wait(&mma_done[st], static_cast<unsigned>((kb / OZ_NST - 1) & 1));
+                const unsigned fb = smem_u32(&full_bar[st]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb),
+                             "r"(static_cast<unsigned>(T::STAGE)));
+                unsigned char* base = sm + static_cast<size_t>(st) * T::STAGE;
+                const long long kt = kt0 + kb;
 #pragma unroll 1
-        for (int p = 0; p < S; ++p) {
-            const int8_t* ga = SA + p * a_slice + m0 * a_pitch + kk;
-            const unsigned sa = smem_u32(base + p * T::A_BYTES);
-#pragma unroll
-            for (int j = 0; j < OZ_BM * 4 / OZ_THREADS; ++j) {
-                const int g = tid + j * OZ_THREADS;
-                const int r = g >> 2, c = g & 3;
-                cp16(sa + r * OZ_BK + ((c ^ ((r >> 1) & 3)) << 4), ga + r * a_pitch + (c << 4));
-            }
-            const int8_t* gb = SB + p * b_slice + n0 * b_pitch + kk;
-            const unsigned sb = smem_u32(base + S * T::A_BYTES + p * T::B_BYTES);
-#pragma unroll
-            for (int j = 0; j < OZ_BN * 4 / OZ_THREADS; ++j) {
-                const int g = tid + j * OZ_THREADS;
-                const int r = g >> 2, c = g & 3;
-                cp16(sb + r * OZ_BK + ((c ^ ((r >> 1) & 3)) << 4), gb + r * b_pitch + (c << 4));
+                for (int p = 0; p < S; ++p) {
+                    const int8_t* ga = SA + ((p * a_tiles + mt) * KT + kt) * T::A_BYTES;
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                            smem_u32(base + p * T::A_BYTES)),
+                        "l"(ga), "r"(T::A_BYTES), "r"(fb)
+                        : "memory");
+                    const int8_t* gb = SB + ((p * b_tiles + nt) * KT + kt) * T::B_BYTES;
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                            smem_u32(base + S * T::A_BYTES + p * T::B_BYTES)),
+                        "l"(gb), "r"(T::B_BYTES), "r"(fb)
+                        : "memory");
+                }
             }
         }
-        asm volatile("cp.async.commit_group;\n");
-    };
-
-    unsigned phase[2] = {0u, 0u};
-    unsigned started = 0;  // diagonals that already hold a partial sum (issuing thread)
-    if (nkb > 0) load(0, 0);
-    for (int kb = 0; kb < nkb; ++kb) {
-        const int st = kb & 1;
-        if (kb + 1 < nkb) {
-            // the other stage was last read by the MMAs of k-block kb - 1
-            if (kb >= 1) {
-                mbar_wait(&mma_done[st ^ 1], phase[st ^ 1]);
-                phase[st ^ 1] ^= 1u;
-            }
-            load(kb + 1, st ^ 1);
-            asm volatile("cp.async.wait_group 1;\n");
-        } else {
-            asm volatile("cp.async.wait_group 0;\n");
-        }
-        // generic-proxy smem writes -> visible to the tensor core's async proxy
-        asm volatile("fence.proxy.async.shared::cta;\n");
-        __syncthreads();
-        if (tid == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;\n");
-            unsigned char* base = sm + static_cast<size_t>(st) * T::STAGE;
-            const unsigned sa0 = smem_u32(base), sb0 = smem_u32(base + S * T::A_BYTES);
-#pragma unroll 1
-            for (int p = 1; p <= S; ++p) {
-#pragma unroll 1
-                for (int q = 1; p + q <= S + 1; ++q) {
-                    const int d = p + q - 2;
-                    const uint32_t dt = tmem + static_cast<uint32_t>(d * OZ_BN);
+        __syncwarp();
+    } else if (warp == 0) {
+        // ---- MMA issuer (warp 0, one thread) -------------------------------
+        if (lane == 0) {
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int st = kb % OZ_NST;
+                mbar_wait(&full_bar[st], static_cast<unsigned>((kb / OZ_NST) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;\n");
+                unsigned char* base = sm + static_cast<size_t>(st) * T::STAGE;
+                const uint64_t da0 = umma_desc_sw32(smem_u32(base));
+                const uint64_t db0 = umma_desc_sw32(smem_u32(base + S * T::A_BYTES));
+                // the p = 1 row of pairs opens every diagonal: it overwrites
+                // on the first k-block and accumulates afterwards
+                const unsigned first_acc = kb > 0 ? 1u : 0u;
 #pragma unroll
-                    for (int ks = 0; ks < OZ_BK / 32; ++ks) {
-                        const uint64_t da = umma_desc_sw64(sa0 + (p - 1) * T::A_BYTES + ks * 32);
-                        const uint64_t db = umma_desc_sw64(sb0 + (q - 1) * T::B_BYTES + ks * 32);
-                        const unsigned acc = (started >> d) & 1u;
+                for (int p = 1; p <= S; ++p) {
+#pragma unroll
+                    for (int q = 1; p + q <= S + 1; ++q) {
+                        const uint32_t dt = tmem + static_cast<uint32_t>((p + q - 2) * OZ_BN);
+                        const uint64_t da = da0 + static_cast<uint64_t>(((p - 1) * T::A_BYTES) >> 4);
+                        const uint64_t db = db0 + static_cast<uint64_t>(((q - 1) * T::B_BYTES) >> 4);
                         asm volatile(
                             "{\n"
                             ".reg .pred pa;\n"
                             "setp.ne.b32 pa, %4, 0;\n"
                             "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, pa;\n"
                             "}\n" ::"r"(dt),
-                            "l"(da), "l"(db), "r"(kOzIdesc), "r"(acc));
-                        started |= 1u << d;
+                            "l"(da), "l"(db), "r"(kOzIdesc), "r"(p == 1 ? first_acc : 1u));
                     }
                 }
+                asm volatile(
+                    "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                        smem_u32(&mma_done[st])));
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                smem_u32(&mma_done[st])));
+            // the last commit tracks every MMA issued before it
+            if (nkb > 0)
+                mbar_wait(&mma_done[(nkb - 1) % OZ_NST], static_cast<unsigned>(((nkb - 1) / OZ_NST) & 1));
         }
+        __syncwarp();
     }
-    // all MMAs done: the last commit covers every earlier MMA
-    if (nkb > 0) {
-        const int st = (nkb - 1) & 1;
-        mbar_wait(&mma_done[st], phase[st]);
-    }
+    __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n");
 
     // epilogue: thread (warp, lane) owns output row m0 + 32 warp + lane
@@ -273,35 +269,60 @@ __global__ void oz_fill_int_kernel(int* p, long long n, int v) {
     if (i < n) p[i] = v;
 }
 
-// digit slices, transposed to K-major: out[p][c][k] (pitch Kpad, slice
-// stride Cpad * Kpad), zero outside K x C.  32 x 32 tiles through shared
-// memory so both the FP64 reads and the int8 writes are coalesced.
-template <int S>
-__global__ void oz_slice_kernel(const double* __restrict__ X, long long K, long long C, long long ld,
-                                const int* __restrict__ e, long long Kpad, long long Cpad,
-                                int8_t* __restrict__ out) {
-    __shared__ double tile[32][33];
-    const long long kb = blockIdx.x * 32LL, cb = blockIdx.y * 32LL;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 32
-    for (int r = ty; r < 32; r += 8) {
-        const long long k = kb + r, c = cb + tx;
+// Digit slices in the GEMM's shared-memory image: operand row c (an output
+// row / column), K index k -> tile (c / TR, k / 32) of TR x 32 bytes, stored
+// contiguously (slice p, row tile, k tile) in the 32-byte-swizzled K-major
+// UMMA layout, so a pipeline stage is one contiguous bulk copy per slice.
+// Zero outside K x C.  32 x 32 element tiles through shared memory keep the
+// FP64 reads coalesced.
+template <int S, int TR>
+__global__ void __launch_bounds__(256) oz_slice_kernel(const double* __restrict__ X, long long K, long long C,
+                                                       long long ld, const int* __restrict__ e, long long Kpad,
+                                                       long long Ctiles, long long c_off, int8_t* __restrict__ out) {
+    // block: 128 K values x 32 columns; thread: one column, 16 consecutive K
+    // values -> one 16-byte store per slice (a swizzle chunk of the tile)
+    __shared__ double tile[128][33];
+    const long long kb = blockIdx.x * 128LL, cb = blockIdx.y * 32LL;
+    const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
+    const long long c_rd = cb + tx;
+    const int ex = (c_rd < C) ? e[c_rd] : 0;
+    for (int r = ty; r < 128; r += 8) {
+        const long long k = kb + r;
         double v = 0.0;
-        if (k < K && c < C) v = ldexp(X[k * ld + c], -e[c]);
+        if (k < K && c_rd < C) v = ldexp(X[k * ld + c_rd], -ex);
         tile[r][tx] = v;
     }
     __syncthreads();
-    const long long slice = Cpad * Kpad;
-    for (int r = ty; r < 32; r += 8) {  // r: column within the tile, tx: k within the tile
-        const long long c = cb + r, k = kb + tx;
-        if (c >= Cpad || k >= Kpad) continue;
-        double v = tile[tx][r];
+    const long long c = cb + tx;            // operand row
+    const int kq = ty;                      // 16-wide K group within the block
+    const long long k0 = kb + 16 * kq;
+    if (c >= C || k0 >= Kpad) return;
+    const long long row = c_off + c;
+    const long long ct = row / TR, kt = k0 / 32;
+    const int rr = static_cast<int>(row - ct * TR);
+    const int chunk = static_cast<int>((k0 / 16) & 1);
+    const int inner = rr * 32 + ((chunk ^ ((rr >> 2) & 1)) << 4);
+    const long long KT = Kpad / 32;
+    double v[16];
 #pragma unroll
-        for (int p = 0; p < S; ++p) {
-            v *= 128.0;
-            const double dgt = trunc(v);
-            v -= dgt;
-            out[p * slice + c * Kpad + k] = static_cast<int8_t>(static_cast<int>(dgt));
+    for (int j = 0; j < 16; ++j) v[j] = tile[16 * kq + j][tx];
+#pragma unroll
+    for (int p = 0; p < S; ++p) {
+        unsigned w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            unsigned packed = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                double x = v[4 * q + b] * 128.0;
+                const double dgt = trunc(x);
+                v[4 * q + b] = x - dgt;
+                packed |= (static_cast<unsigned>(static_cast<int>(dgt)) & 0xFFu) << (8 * b);
+            }
+            w[q] = packed;
         }
+        *reinterpret_cast<uint4*>(out + ((p * Ctiles + ct) * KT + kt) * (TR * 32) + inner) =
+            make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
@@ -318,35 +339,37 @@ __global__ void oz_reduce_kernel(long long M, long long N, int splits, const dou
 
 inline long long rup(long long x, long long a) { return (x + a - 1) / a * a; }
 
-template <int S>
-void ozaki_run(svt_ctx* ctx, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
-               i64 ldb, double beta, double* C, i64 ldc) {
+// exponents e[0..C) and digit slices of the C columns of a row-major K x C
+// FP64 matrix into rows [c_off, c_off + C) of a TR-row tiled slice array
+template <int S, int TR>
+void slice_columns(svt_ctx* ctx, const double* X, i64 K, i64 C, i64 ld, i64 Kpad, i64 Ctiles, i64 c_off,
+                   int8_t* tiles, int* e) {
     cudaStream_t s = ctx->stream;
-    const i64 Kpad = rup(std::max<i64>(K, 1), OZ_BK);
+    if (C <= 0) return;
+    LaunchScope ls(ctx, K_GEMM, 16.0 * K * C + 1.0 * S * C * Kpad, 0.0);  // part of the contraction
+    oz_fill_int_kernel<<<static_cast<unsigned>((C + 255) / 256), 256, 0, s>>>(e, C, -2147483647);
+    const i64 xb = (C + 31) / 32;
+    const i64 parts = std::max<i64>(1, std::min<i64>((4 * ctx->num_sms + xb - 1) / xb, (K + 255) / 256));
+    const i64 rpp = (std::max<i64>(K, 1) + parts - 1) / parts;
+    oz_colexp_kernel<<<dim3(static_cast<unsigned>(xb), static_cast<unsigned>(parts)), 256, 0, s>>>(X, K, C, ld, rpp,
+                                                                                                   e);
+    oz_slice_kernel<S, TR><<<dim3(static_cast<unsigned>((Kpad + 127) / 128), static_cast<unsigned>(xb)), 256, 0, s>>>(
+        X, K, C, ld, e, Kpad, Ctiles, c_off, tiles);
+}
+
+// C (M x N) = alpha * A^T B + beta * C from A's slices (a_tiles 128-row
+// tiles, K padded to Kpad) and B (row-major K x N FP64, sliced here)
+template <int S>
+void ozaki_gemm(svt_ctx* ctx, i64 M, i64 N, i64 K, const int8_t* SA, i64 a_tiles, i64 Kpad, const int* eA,
+                double alpha, const double* B, i64 ldb, double beta, double* C, i64 ldc) {
+    cudaStream_t s = ctx->stream;
     const i64 Mpad = rup(M, OZ_BM), Npad = rup(N, OZ_BN);
-    const size_t a_bytes = static_cast<size_t>(S) * Mpad * Kpad, b_bytes = static_cast<size_t>(S) * Npad * Kpad;
-    ctx->ws_ozaki.ensure((a_bytes + b_bytes + 7) / 8 + 2);
-    int8_t* SA = reinterpret_cast<int8_t*>(ctx->ws_ozaki.get());
-    int8_t* SB = SA + a_bytes;
-    ctx->ws_ozexp.ensure(static_cast<size_t>(M + N));
-    int* eA = ctx->ws_ozexp.get();
-    int* eB = eA + M;
-    {
-        LaunchScope ls(ctx, K_OTHER, 8.0 * (M * K + N * K) * 2 + S * 1.0 * (Mpad + Npad) * Kpad, 0.0);
-        oz_fill_int_kernel<<<static_cast<unsigned>((M + N + 255) / 256), 256, 0, s>>>(eA, M + N, -2147483647);
-        for (int q = 0; q < 2; ++q) {
-            const i64 cols = q ? N : M;
-            const i64 xb = (cols + 31) / 32;
-            const i64 parts = std::max<i64>(1, std::min<i64>((4 * ctx->num_sms + xb - 1) / xb, (K + 255) / 256));
-            const i64 rpp = (K + parts - 1) / parts;
-            oz_colexp_kernel<<<dim3(static_cast<unsigned>(xb), static_cast<unsigned>(parts)), 256, 0, s>>>(
-                q ? B : A, K, cols, q ? ldb : lda, rpp, q ? eB : eA);
-        }
-        oz_slice_kernel<S><<<dim3(static_cast<unsigned>(Kpad / 32), static_cast<unsigned>(Mpad / 32)), 256, 0, s>>>(
-            A, K, M, lda, eA, Kpad, Mpad, SA);
-        oz_slice_kernel<S><<<dim3(static_cast<unsigned>(Kpad / 32), static_cast<unsigned>(Npad / 32)), 256, 0, s>>>(
-            B, K, N, ldb, eB, Kpad, Npad, SB);
-    }
+    const size_t b_bytes = static_cast<size_t>(S) * Npad * Kpad;
+    ctx->ws_ozakib.ensure((b_bytes + 7) / 8 + 2);
+    int8_t* SB = reinterpret_cast<int8_t*>(ctx->ws_ozakib.get());
+    ctx->ws_ozexpb.ensure(static_cast<size_t>(N));
+    int* eB = ctx->ws_ozexpb.get();
+    slice_columns<S, OZ_BN>(ctx, B, K, N, ldb, Kpad, Npad / OZ_BN, 0, SB, eB);
     // K split: the int32 diagonal sums bound a chunk at OZ_KC; among the
     // admissible split counts take the one with the fewest waves x chunk
     // depth (one CTA per SM)
@@ -372,17 +395,29 @@ void ozaki_run(svt_ctx* ctx, i64 M, i64 N, i64 K, double alpha, const double* A,
         attr = true;
     }
     {
-        LaunchScope ls(ctx, K_GEMM, static_cast<double>(a_bytes + b_bytes) + 8.0 * splits * M * N,
+        LaunchScope ls(ctx, K_GEMM, static_cast<double>(S) * (Mpad + Npad) * Kpad + 8.0 * splits * M * N,
                        2.0 * M * N * K);
         const dim3 grid(static_cast<unsigned>(Mpad / OZ_BM), static_cast<unsigned>(Npad / OZ_BN),
                         static_cast<unsigned>(splits));
-        ozaki_tn_kernel<S><<<grid, OZ_THREADS, OzTile<S>::SMEM, s>>>(SA, Kpad, Mpad * Kpad, SB, Kpad, Npad * Kpad,
-                                                                     eA, eB, M, N, kchunk, Kpad,
-                                                                     ctx->ws_partial.get());
+        ozaki_tn_kernel<S><<<grid, OZ_THREADS, OzTile<S>::SMEM, s>>>(SA, a_tiles, SB, Npad / OZ_BN, eA, eB, M, N,
+                                                                     kchunk, Kpad, ctx->ws_partial.get());
     }
     LaunchScope ls(ctx, K_OTHER, 8.0 * (splits + 2) * M * N, 0.0);
     oz_reduce_kernel<<<static_cast<unsigned>((M * N + 255) / 256), 256, 0, s>>>(
         M, N, static_cast<int>(splits), ctx->ws_partial.get(), alpha, beta, C, ldc);
+}
+
+template <int S>
+void ozaki_run(svt_ctx* ctx, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
+               i64 ldb, double beta, double* C, i64 ldc) {
+    const i64 Kpad = rup(std::max<i64>(K, 1), OZ_BK);
+    const i64 Mpad = rup(M, OZ_BM);
+    const size_t a_bytes = static_cast<size_t>(S) * Mpad * Kpad;
+    ctx->ws_ozaki.ensure((a_bytes + 7) / 8 + 2);
+    int8_t* SA = reinterpret_cast<int8_t*>(ctx->ws_ozaki.get());
+    ctx->ws_ozexp.ensure(static_cast<size_t>(M));
+    slice_columns<S, OZ_BM>(ctx, A, K, M, lda, Kpad, Mpad / OZ_BM, 0, SA, ctx->ws_ozexp.get());
+    ozaki_gemm<S>(ctx, M, N, K, SA, Mpad / OZ_BM, Kpad, ctx->ws_ozexp.get(), alpha, B, ldb, beta, C, ldc);
 }
 
 }  // namespace
@@ -403,6 +438,22 @@ void gemm_tn_ozaki(svt_ctx* ctx, i64 M, i64 N, i64 K, double alpha, const double
             ozaki_run<8>(ctx, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
             break;
     }
+}
+
+
+// Cached A operand (the Gram-Schmidt basis Q, whose columns only ever get
+// appended during a sketch): slices of columns [c_off, c_off + C) of a
+// row-major K x C block into the 128-row tiled cache, exponents into e.
+i64 ozaki_kpad(i64 K) { return rup(std::max<i64>(K, 1), OZ_BK); }
+i64 ozaki_rows_pad(i64 rows) { return rup(std::max<i64>(rows, 1), OZ_BM); }
+void ozaki_slice_basis(svt_ctx* ctx, const double* X, i64 K, i64 C, i64 ld, i64 c_off, int8_t* tiles, i64 ctiles,
+                       int* e) {
+    slice_columns<8, OZ_BM>(ctx, X, K, C, ld, ozaki_kpad(K), ctiles, c_off, tiles, e + c_off);
+}
+void gemm_tn_ozaki_cached(svt_ctx* ctx, i64 M, i64 N, i64 K, const int8_t* tiles, i64 ctiles, const int* e,
+                          const double* B, i64 ldb, double* C, i64 ldc) {
+    if (M <= 0 || N <= 0) return;
+    ozaki_gemm<8>(ctx, M, N, K, tiles, ctiles, ozaki_kpad(K), e, 1.0, B, ldb, 0.0, C, ldc);
 }
 
 }  // namespace svtb

@@ -702,6 +702,19 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
         }
     } else {
         const unsigned nb = static_cast<unsigned>((plan.nseg + 3) / 4);
+        // the gathers run through L1: ask for the whole unified L1 / shared
+        // array as cache (the kernels use no shared memory)
+        static const bool carve = [] {
+            const char* e = std::getenv("SVTB_SPMM_CARVEOUT");
+            const int pct = e ? std::atoi(e) : -2;
+            if (pct < -1) return false;
+            SVT_CUDA(cudaFuncSetAttribute(spmm_wide_kernel<1, 16>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+            SVT_CUDA(cudaFuncSetAttribute(spmm_wide_kernel<2, 8>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+            SVT_CUDA(cudaFuncSetAttribute(spmm_wide_kernel<3, 5>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+            SVT_CUDA(cudaFuncSetAttribute(spmm_wide_kernel<4, 4>, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+            return true;
+        }();
+        (void)carve;
         if (w <= 32)
             spmm_wide_kernel<1, 16><<<dim3(nb, 1), 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo,
                                                                           partial);
