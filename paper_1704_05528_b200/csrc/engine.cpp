@@ -737,12 +737,9 @@ static void finalize_mode(Engine& E, const QBDev& st, FinalizeMode mode, double 
 // the INT8 tensor cores from cached digit slices of the basis (ozaki.cu;
 // SVTB_OZAKI=1), else the DMMA GEMM.  The slices of a column are built once,
 // the first time the column takes part in a product.
-static bool ozaki_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("SVTB_OZAKI");
-        return e != nullptr && std::atoi(e) != 0;
-    }();
-    return on;
+static bool ozaki_enabled() {  // read per batch (cheap), so tests can toggle it
+    const char* e = std::getenv("SVTB_OZAKI");
+    return e != nullptr && std::atoi(e) != 0;
 }
 
 static void basis_tx(Engine& E, QBDev& st, i64 r0, i64 w, const double* X, i64 ldx, double* C) {

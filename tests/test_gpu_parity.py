@@ -519,6 +519,30 @@ def test_ozaki_tn_matches_fp64(K, M, N):
     assert torch.equal(G.dev_gemm_tn_ozaki(A, B, 8), G.dev_gemm_tn_ozaki(A, B, 8))  # deterministic
 
 
+def test_ozaki_gram_schmidt_in_the_sketch_matches_oracle(monkeypatch):
+    """The batch Gram-Schmidt product Q^T X on the INT8 tensor cores
+    (SVTB_OZAKI=1, cached basis slices): r3svd on a 5000 x 700 sample set
+    reveals the oracle's rank in the same rounds, singular values within
+    1e-8 of the oracle (north-star tolerance) and 1e-10 of the DMMA path."""
+    rng = np.random.default_rng(7)
+    m, n = 5000, 700
+    cells = rng.choice(m * n, int(0.06 * m * n), replace=False)
+    vals = rng.standard_normal(len(cells))
+    S = O.sampled(m, n, cells // n, cells % n, vals)
+    A = G.SampledMatrix.from_csr(m, n, S.rowptr, S.col, S.val)
+    p = params(10, 10, 1, 0.3, 7)
+    base = G.r3svd(A, p)
+    monkeypatch.setenv("SVTB_OZAKI", "1")
+    oz = G.r3svd(A, p)
+    oz2 = G.r3svd(A, p)
+    monkeypatch.delenv("SVTB_OZAKI")
+    o = O.r3svd(S, p)
+    assert oz.rank == base.rank == o.rank and oz.extension_rounds == base.extension_rounds == o.extension_rounds
+    np.testing.assert_allclose(oz.sigma, o.sigma, rtol=1e-8, atol=1e-8 * o.sigma[0])
+    np.testing.assert_allclose(oz.sigma, base.sigma, rtol=1e-10, atol=1e-10 * base.sigma[0])
+    assert np.array_equal(oz.sigma, oz2.sigma)  # deterministic
+
+
 # ---- device-side sample-set construction (csrc/build.cu) ----------------------
 def _skewed_csr(seed):
     """Rows and columns longer than one 512-entry segment, empty rows and
