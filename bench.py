@@ -288,11 +288,12 @@ def main():
     ctx.sync()
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
     ctx.reset_stats()
-    ctx.set_profiling(True)
+    ctx.set_profiling(not os.environ.get("SVTB_BENCH_NOPROF"))  # dev switch: A/B of the per-launch events
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
     clocks.start()
+    al0 = G.Context.alloc_stats()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -305,6 +306,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
+    al1 = G.Context.alloc_stats()
     ms_local = e0.elapsed_time(e1)
     ms = max_over_ranks(ms_local)
     launches = ctx.launch_count()
@@ -421,6 +423,9 @@ def main():
             "gpu_launches": launches,
             "host": {"syncs_per_step": hstats["syncs"] / args.steps,
                      "sync_wait_ms_per_step": hstats["sync_ms"] / args.steps,
+                     "device_allocs_in_timed_region": al1["mallocs"] - al0["mallocs"],
+                     "device_frees_in_timed_region": al1["frees"] - al0["frees"],
+                     "alloc_ms_in_timed_region": al1["ms"] - al0["ms"],
                      "kernel_ms_per_step": sum(v["total_ms"] for v in stats.values()) / args.steps},
             "clocks": clk,
             "e2e": e2e,

@@ -240,6 +240,9 @@ int svt_dev_sym_eig(svt_ctx* ctx, const double* G, int64_t r, double* W, double*
  * by the Ozaki digit-splitting scheme (slices = int8 digits per entry, 6..8;
  * 8 carries the FP64 GEMM error bound).  The FP64 contraction of the
  * Gram-Schmidt step (sketch.hpp:133-141, Q^T X) in this form. */
+/* Process-wide device allocation counters: cudaMalloc calls, cudaFree calls
+ * and host milliseconds spent in them (instrumentation). */
+int svt_alloc_stats(int64_t* mallocs, int64_t* frees, double* ms);
 int svt_dev_gemm_tn_ozaki(svt_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                           const double* B, int64_t ldb, double* C, int64_t ldc, int slices);
 

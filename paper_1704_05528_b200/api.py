@@ -124,6 +124,13 @@ class Context:
         _check(lib().svt_ctx_host_stats(self.h, C.byref(n), C.byref(ms)))
         return dict(syncs=n.value, sync_ms=ms.value)
 
+    @staticmethod
+    def alloc_stats():
+        """Process-wide (cudaMalloc calls, cudaFree calls, host ms in them)."""
+        a, f, ms = C.c_int64(), C.c_int64(), C.c_double()
+        _check(lib().svt_alloc_stats(C.byref(a), C.byref(f), C.byref(ms)))
+        return dict(mallocs=a.value, frees=f.value, ms=ms.value)
+
     def set_batching(self, on: bool):
         """Speculative multi-round batches (default on; same rounds/ranks)."""
         _check(lib().svt_ctx_set_batching(self.h, C.c_int(1 if on else 0)))

@@ -663,6 +663,14 @@ int svt_dev_sym_eig(svt_ctx* ctx, const double* G, int64_t r, double* W, double*
     });
 }
 
+int svt_alloc_stats(int64_t* mallocs, int64_t* frees, double* ms) {
+    return guard([&] {
+        if (mallocs) *mallocs = alloc_stats().count;
+        if (frees) *frees = alloc_stats().frees;
+        if (ms) *ms = alloc_stats().ms;
+    });
+}
+
 int svt_dev_gemm_tn_ozaki(svt_ctx* ctx, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                           const double* B, int64_t ldb, double* C, int64_t ldc, int slices) {
     return guard([&] {

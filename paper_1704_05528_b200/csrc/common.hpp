@@ -115,6 +115,11 @@ struct DevBuf {
     T* get() const { return p; }
 };
 
+// factor buffers (U, V, sigma of a few dozen kept triplets) are sized for at
+// least this many columns, so the kept rank creeping up over SVT iterations
+// does not regrow them (each regrow is a cudaFree: a device-wide sync)
+constexpr long long kFactorCols = 32;
+
 // arrival counters of the single-launch column reductions (one per 32-column block)
 constexpr size_t kTickets = 4096;
 
@@ -236,6 +241,7 @@ struct svt_ctx {
     svtb::DevBuf<double> ws_ozakib;    // B-operand slices
     svtb::DevBuf<int> ws_ozexpb;
     svtb::DevBuf<double> ws_partial2;  // second partial buffer (reductions)
+    svtb::DevBuf<int> ws_perm;         // eigenvector permutation (sym_eig)
     svtb::DevBuf<unsigned> d_tickets;  // self-resetting arrival counters (single-launch reductions)
     svtb::DevBuf<double> ws_spmm;      // long-row partials of the segmented SpMM
     svtb::DevBuf<unsigned> ws_counters;  // last-CTA-reduces counters (self-resetting)

@@ -2250,12 +2250,15 @@ void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
     std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return lh[x] > lh[y]; });
     std::vector<double> ls_sorted(static_cast<size_t>(r));
     for (i64 j = 0; j < r; ++j) ls_sorted[static_cast<size_t>(j)] = lh[static_cast<size_t>(perm[static_cast<size_t>(j)])];
-    DevBuf<int> dperm(static_cast<size_t>(r));
-    SVT_CUDA(cudaMemcpyAsync(dperm.get(), perm.data(), sizeof(int) * r, cudaMemcpyHostToDevice, ctx->stream));
+    // context workspace: a per-call buffer would cudaFree (a device-wide
+    // synchronisation) on every eigensolve
+    ctx->ws_perm.ensure(static_cast<size_t>(r));
+    int* dperm_p = ctx->ws_perm.get();
+    SVT_CUDA(cudaMemcpyAsync(dperm_p, perm.data(), sizeof(int) * r, cudaMemcpyHostToDevice, ctx->stream));
     SVT_CUDA(cudaMemcpyAsync(lambda, ls_sorted.data(), sizeof(double) * r, cudaMemcpyHostToDevice, ctx->stream));
     {
         LaunchScope ls(ctx, K_FINAL, 16.0 * r * r, 0.0);
-        gather_eigvecs_kernel<<<nblk(r * r), 256, 0, ctx->stream>>>(V, rp, dperm.get(), r, W);
+        gather_eigvecs_kernel<<<nblk(r * r), 256, 0, ctx->stream>>>(V, rp, dperm_p, r, W);
     }
     sync_stream(ctx);
 }

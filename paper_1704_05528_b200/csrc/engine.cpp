@@ -205,7 +205,7 @@ void qr_panel(Engine& E, i64 m, bool dist, const double* X, i64 ldx, i64 w, doub
 // it, predicated on flag `f` computed from max|Q^T P| > 1e-8 (sketch.hpp:138).
 void reorth_if_needed(Engine& E, i64 m, bool dist, const double* Q, i64 ldq, i64 r0, double* P, i64 ldp, i64 w) {
     svt_ctx* c = E.ctx;
-    E.D.ensure(static_cast<size_t>(r0 * w));
+    E.D.ensure(static_cast<size_t>(std::max(r0, ldq) * w));  // ldq = basis capacity: no regrow as r0 grows
     gemm(c, K_GEMM, true, r0, w, m, 1.0, Q, ldq, P, ldp, 0.0, E.D.get(), w);
     if (dist) allreduce(c, E.D.get(), static_cast<size_t>(r0 * w));
     maxabs(c, E.D.get(), r0, w, w, 0.0, dsc(c, S_MAXD));
@@ -408,7 +408,7 @@ void qb_extend(Engine& E, QBDev& st, i64 dt, int np, u64 seed, const double* ome
     const i64 ldq = st.cap;
     if (r0 > 0) {
         // classical Gram-Schmidt, conditional second pass (sketch.hpp:133-136)
-        E.C.ensure(static_cast<size_t>(r0 * width));
+        E.C.ensure(static_cast<size_t>(std::max(r0, st.cap) * width));
         gemm(c, K_GEMM, true, r0, width, m, 1.0, Q, ldq, E.X.get(), width, 0.0, E.C.get(), width);
         allreduce(c, E.C.get(), static_cast<size_t>(r0 * width));
         gemm(c, K_GEMM, false, m, width, r0, -1.0, Q, ldq, E.C.get(), width, 1.0, E.X.get(), width);
@@ -459,7 +459,7 @@ void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFact
         while (cnt < r && std::sqrt(std::max(lam[static_cast<size_t>(cnt)], 0.0)) > lim) ++cnt;
         kc = std::min(r, cnt + 1);
     }
-    E.Vraw.ensure(static_cast<size_t>(n * kc));
+    E.Vraw.ensure(static_cast<size_t>(n * std::max<i64>(kc, kFactorCols)));
     gemm(c, K_FINAL, false, n, kc, r, 1.0, st.Bt.get(), st.cap, E.W.get(), r, 0.0, E.Vraw.get(), kc);
     E.lam.ensure(static_cast<size_t>(std::max(r, kc)));
     col_sumsq(c, E.Vraw.get(), n, kc, kc, E.lam.get());
@@ -485,21 +485,21 @@ void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFact
         out.sigma[static_cast<size_t>(j)] = s;
         inv[static_cast<size_t>(j)] = (s > 0.0) ? 1.0 / s : 0.0;
     }
-    E.perm.ensure(static_cast<size_t>(k));
-    out.d_sigma.ensure(static_cast<size_t>(2 * k));
+    E.perm.ensure(static_cast<size_t>(std::max<i64>(k, kFactorCols)));
+    out.d_sigma.ensure(static_cast<size_t>(2 * std::max<i64>(k, kFactorCols)));
     SVT_CUDA(cudaMemcpyAsync(E.perm.get(), perm.data(), sizeof(int) * k, cudaMemcpyHostToDevice, c->stream));
     SVT_CUDA(cudaMemcpyAsync(out.d_sigma.get(), out.sigma.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
                              c->stream));
     SVT_CUDA(cudaMemcpyAsync(out.d_sigma.get() + k, inv.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
                              c->stream));
     // V = (B^T W)[:, perm] / sigma
-    out.V.ensure(static_cast<size_t>(n * k));
+    out.V.ensure(static_cast<size_t>(n * std::max<i64>(k, kFactorCols)));
     permute_cols(c, E.Vraw.get(), n, kc, E.perm.get(), k, out.V.get(), k);
     scale_cols(c, out.V.get(), n, k, k, out.d_sigma.get() + k);
     // U = Q W[:, perm]
-    E.Wk.ensure(static_cast<size_t>(r * k));
+    E.Wk.ensure(static_cast<size_t>(k <= kFactorCols ? std::max(r, st.cap) * kFactorCols : r * k));
     permute_cols(c, E.W.get(), r, r, E.perm.get(), k, E.Wk.get(), k);
-    out.U.ensure(static_cast<size_t>(std::max<i64>(1, m) * k));
+    out.U.ensure(static_cast<size_t>(std::max<i64>(1, m) * std::max<i64>(k, kFactorCols)));
     gemm(c, K_FINAL, false, m, k, r, 1.0, st.Q.get(), st.cap, E.Wk.get(), k, 0.0, out.U.get(), k);
     // keep the host copy of sigma in sync with the stream (the inv upload
     // above reads a host vector that dies with this frame)
@@ -537,16 +537,19 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
     // engine-owned workspaces (grow-only; no per-iteration cudaMalloc/free)
     DevBuf<double>&Z = E.fkZ, &Zq = E.fkZq, &Zt = E.fkZt, &Wn = E.fkWn, &H = E.fkH, &Yh = E.fkYh, &th = E.fkth,
     &ZY = E.fkZY, &Xr = E.fkXr, &res2 = E.fkres;
+    // sized for the basis capacity, not the current rank: the rank grows
+    // every SVT iteration and each regrow is a cudaFree (device-wide sync)
+    const i64 rc = std::max(r, st.cap);
     auto grow = [&](i64 bb) {
-        Z.ensure(static_cast<size_t>(r * bb));
-        Zq.ensure(static_cast<size_t>(r * bb));
-        Zt.ensure(static_cast<size_t>(r * bb));
+        Z.ensure(static_cast<size_t>(rc * bb));
+        Zq.ensure(static_cast<size_t>(rc * bb));
+        Zt.ensure(static_cast<size_t>(rc * bb));
         Wn.ensure(static_cast<size_t>(n * bb));
         H.ensure(static_cast<size_t>(bb * bb));
         Yh.ensure(static_cast<size_t>(bb * bb));
         th.ensure(static_cast<size_t>(bb));
-        ZY.ensure(static_cast<size_t>(r * bb));
-        Xr.ensure(static_cast<size_t>(r * bb));
+        ZY.ensure(static_cast<size_t>(rc * bb));
+        Xr.ensure(static_cast<size_t>(rc * bb));
         res2.ensure(static_cast<size_t>(bb));
     };
     grow(b);
@@ -578,7 +581,7 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
         if (kk == b && b < r) {
             // the block does not reach below the threshold: widen it
             const i64 b2 = std::min<i64>(r, 2 * b);
-            Zt.ensure(static_cast<size_t>(r * b2));
+            Zt.ensure(static_cast<size_t>(rc * b2));
             copy2d(c, Zq.get(), b, Zt.get(), b2, r, b);
             gaussian_block_dev(c, r, b2 - b, derive_seed_u(seed, 0x5EEDF1A2ULL + static_cast<u64>(it)), Zt.get() + b,
                                b2);
@@ -659,7 +662,7 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
     c->stats[K_FINAL].flops += 0.0;
     const i64 kc = std::min(b, kk + 1);
     // V_raw = B^T (Zq Yh) = Wn Yh; sigma = column norms (Rayleigh quotients)
-    E.Vraw.ensure(static_cast<size_t>(n * kc));
+    E.Vraw.ensure(static_cast<size_t>(n * std::max<i64>(kc, kFactorCols)));
     gemm(c, K_FINAL, false, n, kc, b, 1.0, Wn.get(), b, Yh.get(), b, 0.0, E.Vraw.get(), kc);
     E.lam.ensure(static_cast<size_t>(kc));
     col_sumsq(c, E.Vraw.get(), n, kc, kc, E.lam.get());
@@ -681,19 +684,19 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
         out.sigma[static_cast<size_t>(j)] = sig[static_cast<size_t>(perm[static_cast<size_t>(j)])];
         inv[static_cast<size_t>(j)] = 1.0 / out.sigma[static_cast<size_t>(j)];
     }
-    E.perm.ensure(static_cast<size_t>(k));
-    out.d_sigma.ensure(static_cast<size_t>(2 * k));
+    E.perm.ensure(static_cast<size_t>(std::max<i64>(k, kFactorCols)));
+    out.d_sigma.ensure(static_cast<size_t>(2 * std::max<i64>(k, kFactorCols)));
     SVT_CUDA(cudaMemcpyAsync(E.perm.get(), perm.data(), sizeof(int) * k, cudaMemcpyHostToDevice, c->stream));
     SVT_CUDA(cudaMemcpyAsync(out.d_sigma.get(), out.sigma.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
                              c->stream));
     SVT_CUDA(cudaMemcpyAsync(out.d_sigma.get() + k, inv.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
                              c->stream));
-    out.V.ensure(static_cast<size_t>(n * k));
+    out.V.ensure(static_cast<size_t>(n * std::max<i64>(k, kFactorCols)));
     permute_cols(c, E.Vraw.get(), n, kc, E.perm.get(), k, out.V.get(), k);
     scale_cols(c, out.V.get(), n, k, k, out.d_sigma.get() + k);
-    E.Wk.ensure(static_cast<size_t>(r * k));
+    E.Wk.ensure(static_cast<size_t>(k <= kFactorCols ? std::max(r, st.cap) * kFactorCols : r * k));
     permute_cols(c, Xr.get(), r, b, E.perm.get(), k, E.Wk.get(), k);
-    out.U.ensure(static_cast<size_t>(std::max<i64>(1, m) * k));
+    out.U.ensure(static_cast<size_t>(std::max<i64>(1, m) * std::max<i64>(k, kFactorCols)));
     gemm(c, K_FINAL, false, m, k, r, 1.0, st.Q.get(), st.cap, E.Wk.get(), k, 0.0, out.U.get(), k);
     sync_stream(c);
 }
@@ -857,7 +860,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         // keeps more than max(1e-3, 1e8 (m + r0) eps) of every block's norm
         // the test is false with that margin, so the check product Q^T X is
         // only formed when some block lost more (near-dependent rounds).
-        E.CW.ensure(static_cast<size_t>(r0 * W));
+        E.CW.ensure(static_cast<size_t>(std::max(r0, st.cap) * W));  // basis capacity: no regrow as r0 grows
         E.eW.ensure(static_cast<size_t>(3 * W));
         col_sumsq(c, XW, m, W, W, E.eW.get() + 2 * W);
         basis_tx(E, st, r0, W, XW, W, E.CW.get());
@@ -937,6 +940,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
 static SketchOut run_loop(Engine& E, QBDev& st, const svt_sketch_params& p, FinalizeMode mode, double tau,
                           i64 s_warm) {
     SketchOut out;
+    out.f = std::move(E.fpool);  // reuse the previous sketch's factor buffers (no per-sketch cudaMalloc / cudaFree)
     int rounds = 0;
     ++E.sketch_gen;  // speculative batches of an earlier sketch can never be used by this one
     // Omega bank: the Gaussian blocks of the next rounds depend only on

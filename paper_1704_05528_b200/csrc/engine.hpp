@@ -115,6 +115,7 @@ struct Engine {
     bool batching = true;  // speculative multi-round batches (exact-arithmetic equivalent)
     int last_rounds = -1;  // rounds of the previous sketch (batch-size predictor)
     u64 sketch_gen = 0;    // incremented per sketch: a speculative batch never outlives its sketch
+    DevFactors fpool;          // factor buffers handed back by the solver for the next sketch
     bool tiled = false;        // shared-memory-tiled SpMM for wide panels (opt-in, per sketch)
     bool tiles_fresh = false;  // the tiled views mirror Y (cleared at every sketch entry)
     Engine(svt_ctx* c, svt_mat* m, Vals y) : ctx(c), mat(m), Y(y), batching(c->batching != 0) {}

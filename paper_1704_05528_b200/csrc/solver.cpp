@@ -46,8 +46,8 @@ void shrink_into(svt_ctx* c, const DevFactors& f, double tau, DevFactors& out) {
     out.sigma.resize(static_cast<size_t>(keep));
     for (i64 j = 0; j < keep; ++j) out.sigma[static_cast<size_t>(j)] = f.sigma[static_cast<size_t>(j)] - tau;
     if (keep == 0) return;
-    out.U.ensure(static_cast<size_t>(std::max<i64>(1, f.m_local) * keep));
-    out.V.ensure(static_cast<size_t>(f.n * keep));
+    out.U.ensure(static_cast<size_t>(std::max<i64>(1, f.m_local) * std::max<i64>(keep, kFactorCols)));
+    out.V.ensure(static_cast<size_t>(f.n * std::max<i64>(keep, kFactorCols)));
     copy2d(c, f.U.get(), f.k, out.U.get(), keep, f.m_local, keep);
     copy2d(c, f.V.get(), f.k, out.V.get(), keep, f.n, keep);
 }
@@ -58,8 +58,8 @@ void copy_factors(svt_ctx* c, const DevFactors& f, DevFactors& out) {
     out.k = f.k;
     out.sigma = f.sigma;
     if (f.k == 0) return;
-    out.U.ensure(static_cast<size_t>(std::max<i64>(1, f.m_local) * f.k));
-    out.V.ensure(static_cast<size_t>(f.n * f.k));
+    out.U.ensure(static_cast<size_t>(std::max<i64>(1, f.m_local) * std::max<i64>(f.k, kFactorCols)));
+    out.V.ensure(static_cast<size_t>(f.n * std::max<i64>(f.k, kFactorCols)));
     SVT_CUDA(cudaMemcpyAsync(out.U.get(), f.U.get(), sizeof(double) * f.m_local * f.k, cudaMemcpyDeviceToDevice,
                              c->stream));
     SVT_CUDA(cudaMemcpyAsync(out.V.get(), f.V.get(), sizeof(double) * f.n * f.k, cudaMemcpyDeviceToDevice,
@@ -159,6 +159,7 @@ void solver_step(svt_solver* S, svt_observer_fn obs, void* user, svt_record* rec
             revealed = so.rank;
             rounds = so.rounds;
             shrink_into(c, so.f, cfg.tau, S->X);
+            E.fpool = std::move(so.f);  // buffers back to the engine (freed only with it)
             break;
         }
         case SVT_BACKEND_RSVD_FIXED: {
@@ -183,9 +184,9 @@ void solver_step(svt_solver* S, svt_observer_fn obs, void* user, svt_record* rec
     // X = shrink(...): U (m_local x k), sigma - tau, V (n x k); Vs = V diag(sigma - tau)
     DevFactors& X = S->X;
     const i64 k = X.k;
-    X.d_sigma.ensure(static_cast<size_t>(std::max<i64>(1, k)));
+    X.d_sigma.ensure(static_cast<size_t>(std::max<i64>(k, kFactorCols)));
     if (k > 0) {
-        S->Vs.ensure(static_cast<size_t>(A->n * k));
+        S->Vs.ensure(static_cast<size_t>(A->n * std::max<i64>(k, kFactorCols)));
         SVT_CUDA(cudaMemcpyAsync(X.d_sigma.get(), X.sigma.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
                                  c->stream));
         copy2d(c, X.V.get(), k, S->Vs.get(), k, A->n, k);
@@ -267,7 +268,7 @@ void solver_step(svt_solver* S, svt_observer_fn obs, void* user, svt_record* rec
     S->frob_y_sq = sums[3];
     S->s = k;
     if (k > 0) {
-        S->U_prev.ensure(static_cast<size_t>(std::max<i64>(1, A->m_local) * k));
+        S->U_prev.ensure(static_cast<size_t>(std::max<i64>(1, A->m_local) * std::max<i64>(k, kFactorCols)));
         SVT_CUDA(cudaMemcpyAsync(S->U_prev.get(), X.U.get(), sizeof(double) * A->m_local * k,
                                  cudaMemcpyDeviceToDevice, c->stream));
     }
