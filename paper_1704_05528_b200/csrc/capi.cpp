@@ -124,6 +124,10 @@ int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, sv
         SVT_CUDA(cudaMalloc(&c->d_flags, 64 * sizeof(int)));
         SVT_CUDA(cudaMemsetAsync(c->d_scalars, 0, 64 * sizeof(double), c->stream));
         SVT_CUDA(cudaMemsetAsync(c->d_flags, 0, 64 * sizeof(int), c->stream));
+        // reduction / permutation scratch sized once (regrowing inside an SVT
+        // iteration would cudaFree: a device-wide sync)
+        c->ws_partial2.alloc(size_t(4) << 20);
+        c->ws_perm.alloc(4096);
         c->d_tickets.alloc(kTickets);
         SVT_CUDA(cudaMemsetAsync(c->d_tickets.get(), 0, kTickets * sizeof(unsigned), c->stream));
         nccl_init(c->comm, rank, world, nccl_id);

@@ -119,6 +119,12 @@ struct DevBuf {
 // least this many columns, so the kept rank creeping up over SVT iterations
 // does not regrow them (each regrow is a cudaFree: a device-wide sync)
 constexpr long long kFactorCols = 32;
+// ... and, within a 64 MB budget for (rows + n) x columns, for the whole
+// possible kept rank (small problems keep most of their basis: config 2)
+inline long long factor_cols(long long rows_plus_n, long long max_rank) {
+    const long long budget = (64LL << 20) / (8 * std::max<long long>(1, rows_plus_n));
+    return std::max<long long>(kFactorCols, std::min<long long>(max_rank, budget));
+}
 
 // arrival counters of the single-launch column reductions (one per 32-column block)
 constexpr size_t kTickets = 4096;

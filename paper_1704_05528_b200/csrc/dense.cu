@@ -2200,7 +2200,10 @@ void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
     bsz = std::min<i64>(bsz, std::max<i64>(1, r / 64));
     const bool blocked = bsz >= 1 && std::getenv("SVTB_JACOBI_SCALAR") == nullptr;
     const i64 rp = blocked ? (r + 2 * bsz - 1) / (2 * bsz) * (2 * bsz) : (r + 1) & ~1LL;
-    ctx->ws_eig.ensure(static_cast<size_t>(2 * rp * rp + rp));
+    // floor at a 1056-wide problem (the dense-Gram finalize range): the
+    // basis grows every SVT iteration and each regrow is a device-wide sync
+    constexpr i64 kEigFloor = 1056;
+    ctx->ws_eig.ensure(static_cast<size_t>(std::max(2 * rp * rp + rp, 2 * kEigFloor * kEigFloor + kEigFloor)));
     ctx->ws_info.ensure(8);
     double* A = ctx->ws_eig.get();
     double* V = A + rp * rp;

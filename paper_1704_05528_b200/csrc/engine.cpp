@@ -98,7 +98,11 @@ void ensure_cap(Engine& E, QBDev& st, i64 need) {
     const double per_col = 8.0 * static_cast<double>(std::max<i64>(1, st.m_local) + st.n);
     const bool roomy = per_col * static_cast<double>(2 * st.cap) < 0.45 * static_cast<double>(free_b);
     i64 grown = roomy ? st.cap * 2 : st.cap + st.cap / 4;
-    if (st.cap == 0 && E.mat != nullptr && E.mat->nnz_global >= (1LL << 20)) {
+    if (st.cap == 0 && per_col * static_cast<double>(st.min_dim) <= 0.4 * static_cast<double>(free_b)) {
+        // the whole basis range is affordable (small and mid-size problems):
+        // reserve it once, so the basis never regrows inside an SVT iteration
+        grown = st.min_dim;
+    } else if (st.cap == 0 && E.mat != nullptr && E.mat->nnz_global >= (1LL << 20)) {
         // first sketch of a large problem: reserve the whole basis range the
         // panels can take in ~40 % of free HBM (all of min(m, n) for config
         // 4: 6.9 GB), so no multi-GB regrow lands inside an SVT iteration
@@ -445,9 +449,13 @@ void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFact
     out.k = 0;
     out.sigma.clear();
     if (r == 0) return;
-    E.G.ensure(static_cast<size_t>(r * r));
-    E.W.ensure(static_cast<size_t>(r * r));
-    E.lam.ensure(static_cast<size_t>(r));
+    // the dense Gram path runs for bases up to ~1024 wide (finalize_kept):
+    // size for that at once, so the basis growing over SVT iterations does
+    // not regrow these (a cudaFree is a device-wide sync)
+    const i64 rfloor = std::min<i64>(st.min_dim, 1024);
+    E.G.ensure(static_cast<size_t>(std::max(r * r, rfloor * rfloor)));
+    E.W.ensure(static_cast<size_t>(std::max(r * r, rfloor * rfloor)));
+    E.lam.ensure(static_cast<size_t>(std::max(r, rfloor)));
     gemm(c, K_FINAL, true, r, r, n, 1.0, st.Bt.get(), st.cap, st.Bt.get(), st.cap, 0.0, E.G.get(), r);
     sym_eig(c, E.G.get(), r, E.W.get(), E.lam.get());
     std::vector<double> lam(static_cast<size_t>(r));
@@ -459,7 +467,7 @@ void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFact
         while (cnt < r && std::sqrt(std::max(lam[static_cast<size_t>(cnt)], 0.0)) > lim) ++cnt;
         kc = std::min(r, cnt + 1);
     }
-    E.Vraw.ensure(static_cast<size_t>(n * std::max<i64>(kc, kFactorCols)));
+    E.Vraw.ensure(static_cast<size_t>(n * std::max<i64>(kc, factor_cols(m + n, st.min_dim))));
     gemm(c, K_FINAL, false, n, kc, r, 1.0, st.Bt.get(), st.cap, E.W.get(), r, 0.0, E.Vraw.get(), kc);
     E.lam.ensure(static_cast<size_t>(std::max(r, kc)));
     col_sumsq(c, E.Vraw.get(), n, kc, kc, E.lam.get());
@@ -485,21 +493,21 @@ void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFact
         out.sigma[static_cast<size_t>(j)] = s;
         inv[static_cast<size_t>(j)] = (s > 0.0) ? 1.0 / s : 0.0;
     }
-    E.perm.ensure(static_cast<size_t>(std::max<i64>(k, kFactorCols)));
-    out.d_sigma.ensure(static_cast<size_t>(2 * std::max<i64>(k, kFactorCols)));
+    E.perm.ensure(static_cast<size_t>(std::max<i64>(k, factor_cols(m + n, st.min_dim))));
+    out.d_sigma.ensure(static_cast<size_t>(2 * std::max<i64>(k, factor_cols(m + n, st.min_dim))));
     SVT_CUDA(cudaMemcpyAsync(E.perm.get(), perm.data(), sizeof(int) * k, cudaMemcpyHostToDevice, c->stream));
     SVT_CUDA(cudaMemcpyAsync(out.d_sigma.get(), out.sigma.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
                              c->stream));
     SVT_CUDA(cudaMemcpyAsync(out.d_sigma.get() + k, inv.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
                              c->stream));
     // V = (B^T W)[:, perm] / sigma
-    out.V.ensure(static_cast<size_t>(n * std::max<i64>(k, kFactorCols)));
+    out.V.ensure(static_cast<size_t>(n * std::max<i64>(k, factor_cols(m + n, st.min_dim))));
     permute_cols(c, E.Vraw.get(), n, kc, E.perm.get(), k, out.V.get(), k);
     scale_cols(c, out.V.get(), n, k, k, out.d_sigma.get() + k);
     // U = Q W[:, perm]
-    E.Wk.ensure(static_cast<size_t>(k <= kFactorCols ? std::max(r, st.cap) * kFactorCols : r * k));
+    E.Wk.ensure(static_cast<size_t>(std::max<i64>(r * k, std::max(r, st.cap) * factor_cols(m + n, st.min_dim))));
     permute_cols(c, E.W.get(), r, r, E.perm.get(), k, E.Wk.get(), k);
-    out.U.ensure(static_cast<size_t>(std::max<i64>(1, m) * std::max<i64>(k, kFactorCols)));
+    out.U.ensure(static_cast<size_t>(std::max<i64>(1, m) * std::max<i64>(k, factor_cols(m + n, st.min_dim))));
     gemm(c, K_FINAL, false, m, k, r, 1.0, st.Q.get(), st.cap, E.Wk.get(), k, 0.0, out.U.get(), k);
     // keep the host copy of sigma in sync with the stream (the inv upload
     // above reads a host vector that dies with this frame)
@@ -540,11 +548,12 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
     // sized for the basis capacity, not the current rank: the rank grows
     // every SVT iteration and each regrow is a cudaFree (device-wide sync)
     const i64 rc = std::max(r, st.cap);
-    auto grow = [&](i64 bb) {
+    auto grow = [&](i64 bb_need) {
+        const i64 bb = std::max<i64>(bb_need, std::min<i64>(rc, 128));  // the block widens over iterations
         Z.ensure(static_cast<size_t>(rc * bb));
         Zq.ensure(static_cast<size_t>(rc * bb));
         Zt.ensure(static_cast<size_t>(rc * bb));
-        Wn.ensure(static_cast<size_t>(n * bb));
+        Wn.ensure(static_cast<size_t>(n * std::max<i64>(bb, factor_cols(m + n, st.min_dim))));
         H.ensure(static_cast<size_t>(bb * bb));
         Yh.ensure(static_cast<size_t>(bb * bb));
         th.ensure(static_cast<size_t>(bb));
@@ -662,7 +671,7 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
     c->stats[K_FINAL].flops += 0.0;
     const i64 kc = std::min(b, kk + 1);
     // V_raw = B^T (Zq Yh) = Wn Yh; sigma = column norms (Rayleigh quotients)
-    E.Vraw.ensure(static_cast<size_t>(n * std::max<i64>(kc, kFactorCols)));
+    E.Vraw.ensure(static_cast<size_t>(n * std::max<i64>(kc, factor_cols(m + n, st.min_dim))));
     gemm(c, K_FINAL, false, n, kc, b, 1.0, Wn.get(), b, Yh.get(), b, 0.0, E.Vraw.get(), kc);
     E.lam.ensure(static_cast<size_t>(kc));
     col_sumsq(c, E.Vraw.get(), n, kc, kc, E.lam.get());
@@ -684,19 +693,19 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
         out.sigma[static_cast<size_t>(j)] = sig[static_cast<size_t>(perm[static_cast<size_t>(j)])];
         inv[static_cast<size_t>(j)] = 1.0 / out.sigma[static_cast<size_t>(j)];
     }
-    E.perm.ensure(static_cast<size_t>(std::max<i64>(k, kFactorCols)));
-    out.d_sigma.ensure(static_cast<size_t>(2 * std::max<i64>(k, kFactorCols)));
+    E.perm.ensure(static_cast<size_t>(std::max<i64>(k, factor_cols(m + n, st.min_dim))));
+    out.d_sigma.ensure(static_cast<size_t>(2 * std::max<i64>(k, factor_cols(m + n, st.min_dim))));
     SVT_CUDA(cudaMemcpyAsync(E.perm.get(), perm.data(), sizeof(int) * k, cudaMemcpyHostToDevice, c->stream));
     SVT_CUDA(cudaMemcpyAsync(out.d_sigma.get(), out.sigma.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
                              c->stream));
     SVT_CUDA(cudaMemcpyAsync(out.d_sigma.get() + k, inv.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
                              c->stream));
-    out.V.ensure(static_cast<size_t>(n * std::max<i64>(k, kFactorCols)));
+    out.V.ensure(static_cast<size_t>(n * std::max<i64>(k, factor_cols(m + n, st.min_dim))));
     permute_cols(c, E.Vraw.get(), n, kc, E.perm.get(), k, out.V.get(), k);
     scale_cols(c, out.V.get(), n, k, k, out.d_sigma.get() + k);
-    E.Wk.ensure(static_cast<size_t>(k <= kFactorCols ? std::max(r, st.cap) * kFactorCols : r * k));
+    E.Wk.ensure(static_cast<size_t>(std::max<i64>(r * k, std::max(r, st.cap) * factor_cols(m + n, st.min_dim))));
     permute_cols(c, Xr.get(), r, b, E.perm.get(), k, E.Wk.get(), k);
-    out.U.ensure(static_cast<size_t>(std::max<i64>(1, m) * std::max<i64>(k, kFactorCols)));
+    out.U.ensure(static_cast<size_t>(std::max<i64>(1, m) * std::max<i64>(k, factor_cols(m + n, st.min_dim))));
     gemm(c, K_FINAL, false, m, k, r, 1.0, st.Q.get(), st.cap, E.Wk.get(), k, 0.0, out.U.get(), k);
     sync_stream(c);
 }
@@ -789,9 +798,12 @@ static void batch_sketch(Engine& E, const svt_sketch_params& p, int round0, int 
     DevBuf<double>* part = side ? &sp.part : nullptr;
     u64 seeds[kMaxOmegaBatch];
     for (int k = 0; k < K; ++k) seeds[k] = derive_seed_u(p.seed, static_cast<u64>(round0 + k));
-    sp.om[slot].ensure(static_cast<size_t>(n * W));
-    sp.x[slot].ensure(static_cast<size_t>(std::max<i64>(1, m) * W));
-    sp.t[slot].ensure(static_cast<size_t>(n * W));
+    // batch panels sized for the widest batch at once (W grows over the first
+    // batches; a regrow inside an SVT iteration is a device-wide sync)
+    const i64 Wc = std::max<i64>(W, kMaxBatchW);
+    sp.om[slot].ensure(static_cast<size_t>(n * Wc));
+    sp.x[slot].ensure(static_cast<size_t>(std::max<i64>(1, m) * Wc));
+    sp.t[slot].ensure(static_cast<size_t>(n * Wc));
     gaussian_blocks_dev(c, n, w, seeds, K, sp.om[slot].get(), w, W, side);
     sp_mult(E, W, sp.om[slot].get(), W, sp.x[slot].get(), W, s, part);
     for (int j = 0; j < p.np; ++j) {  // np <= 1 on this path
@@ -849,7 +861,8 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         sp.slot = ns;
     }
     double* XW = sp.x[slot].get();
-    E.TW.ensure(static_cast<size_t>(n * W));
+    const i64 Wc = std::max<i64>(W, kMaxBatchW);
+    E.TW.ensure(static_cast<size_t>(n * Wc));
     double* Q = st.Q.get();
     const i64 ldq = st.cap;
     if (r0 > 0) {
@@ -860,8 +873,8 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         // keeps more than max(1e-3, 1e8 (m + r0) eps) of every block's norm
         // the test is false with that margin, so the check product Q^T X is
         // only formed when some block lost more (near-dependent rounds).
-        E.CW.ensure(static_cast<size_t>(std::max(r0, st.cap) * W));  // basis capacity: no regrow as r0 grows
-        E.eW.ensure(static_cast<size_t>(3 * W));
+        E.CW.ensure(static_cast<size_t>(std::max(r0, st.cap) * Wc));  // basis capacity: no regrow as r0 grows
+        E.eW.ensure(static_cast<size_t>(3 * Wc));
         col_sumsq(c, XW, m, W, W, E.eW.get() + 2 * W);
         basis_tx(E, st, r0, W, XW, W, E.CW.get());
         allreduce(c, E.CW.get(), static_cast<size_t>(r0 * W));
@@ -886,9 +899,9 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
                          static_cast<long long>(r0), read_flag(c, F_CHECK), read_flag(c, F_SECOND));
     }
     // one Cholesky QR (twice) of the whole panel: nested spans per block
-    E.GW.ensure(static_cast<size_t>(W * W));
-    E.RW.ensure(static_cast<size_t>(W * W));
-    E.X2.ensure(static_cast<size_t>(std::max<i64>(1, m) * W));
+    E.GW.ensure(static_cast<size_t>(Wc * Wc));
+    E.RW.ensure(static_cast<size_t>(Wc * Wc));
+    E.X2.ensure(static_cast<size_t>(std::max<i64>(1, m) * Wc));
     zero_flag(c, F_QRSTAT);
     int* status = dfl(c, F_QRSTAT);
     gemm(c, K_QR, true, W, W, m, 1.0, XW, W, XW, W, 0.0, E.GW.get(), W);

@@ -89,6 +89,9 @@ struct SketchOut {
     int rounds = 0;
 };
 
+// widest speculative round batch (the 128-column Cholesky panel)
+constexpr i64 kMaxBatchW = 128;
+
 // Per-context reusable workspaces of the sketch engines.
 struct Engine {
     svt_ctx* ctx;

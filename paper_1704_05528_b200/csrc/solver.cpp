@@ -46,8 +46,8 @@ void shrink_into(svt_ctx* c, const DevFactors& f, double tau, DevFactors& out) {
     out.sigma.resize(static_cast<size_t>(keep));
     for (i64 j = 0; j < keep; ++j) out.sigma[static_cast<size_t>(j)] = f.sigma[static_cast<size_t>(j)] - tau;
     if (keep == 0) return;
-    out.U.ensure(static_cast<size_t>(std::max<i64>(1, f.m_local) * std::max<i64>(keep, kFactorCols)));
-    out.V.ensure(static_cast<size_t>(f.n * std::max<i64>(keep, kFactorCols)));
+    out.U.ensure(static_cast<size_t>(std::max<i64>(1, f.m_local) * std::max<i64>(keep, factor_cols(f.m_local + f.n, f.n))));
+    out.V.ensure(static_cast<size_t>(f.n * std::max<i64>(keep, factor_cols(f.m_local + f.n, f.n))));
     copy2d(c, f.U.get(), f.k, out.U.get(), keep, f.m_local, keep);
     copy2d(c, f.V.get(), f.k, out.V.get(), keep, f.n, keep);
 }
@@ -58,8 +58,8 @@ void copy_factors(svt_ctx* c, const DevFactors& f, DevFactors& out) {
     out.k = f.k;
     out.sigma = f.sigma;
     if (f.k == 0) return;
-    out.U.ensure(static_cast<size_t>(std::max<i64>(1, f.m_local) * std::max<i64>(f.k, kFactorCols)));
-    out.V.ensure(static_cast<size_t>(f.n * std::max<i64>(f.k, kFactorCols)));
+    out.U.ensure(static_cast<size_t>(std::max<i64>(1, f.m_local) * std::max<i64>(f.k, factor_cols(f.m_local + f.n, f.n))));
+    out.V.ensure(static_cast<size_t>(f.n * std::max<i64>(f.k, factor_cols(f.m_local + f.n, f.n))));
     SVT_CUDA(cudaMemcpyAsync(out.U.get(), f.U.get(), sizeof(double) * f.m_local * f.k, cudaMemcpyDeviceToDevice,
                              c->stream));
     SVT_CUDA(cudaMemcpyAsync(out.V.get(), f.V.get(), sizeof(double) * f.n * f.k, cudaMemcpyDeviceToDevice,
@@ -184,9 +184,9 @@ void solver_step(svt_solver* S, svt_observer_fn obs, void* user, svt_record* rec
     // X = shrink(...): U (m_local x k), sigma - tau, V (n x k); Vs = V diag(sigma - tau)
     DevFactors& X = S->X;
     const i64 k = X.k;
-    X.d_sigma.ensure(static_cast<size_t>(std::max<i64>(k, kFactorCols)));
+    X.d_sigma.ensure(static_cast<size_t>(std::max<i64>(k, factor_cols(A->m_local + A->n, std::min(A->m, A->n)))));
     if (k > 0) {
-        S->Vs.ensure(static_cast<size_t>(A->n * std::max<i64>(k, kFactorCols)));
+        S->Vs.ensure(static_cast<size_t>(A->n * std::max<i64>(k, factor_cols(A->m_local + A->n, std::min(A->m, A->n)))));
         SVT_CUDA(cudaMemcpyAsync(X.d_sigma.get(), X.sigma.data(), sizeof(double) * k, cudaMemcpyHostToDevice,
                                  c->stream));
         copy2d(c, X.V.get(), k, S->Vs.get(), k, A->n, k);
@@ -268,7 +268,7 @@ void solver_step(svt_solver* S, svt_observer_fn obs, void* user, svt_record* rec
     S->frob_y_sq = sums[3];
     S->s = k;
     if (k > 0) {
-        S->U_prev.ensure(static_cast<size_t>(std::max<i64>(1, A->m_local) * std::max<i64>(k, kFactorCols)));
+        S->U_prev.ensure(static_cast<size_t>(std::max<i64>(1, A->m_local) * std::max<i64>(k, factor_cols(A->m_local + A->n, std::min(A->m, A->n)))));
         SVT_CUDA(cudaMemcpyAsync(S->U_prev.get(), X.U.get(), sizeof(double) * A->m_local * k,
                                  cudaMemcpyDeviceToDevice, c->stream));
     }
