@@ -128,6 +128,8 @@ int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, sv
         // iteration would cudaFree: a device-wide sync)
         c->ws_partial2.alloc(size_t(4) << 20);
         c->ws_perm.alloc(4096);
+        c->ws_eig.alloc(static_cast<size_t>(2 * 1056 * 1056 + 1056));  // dense Gram eigensolve up to r = 1056
+        c->ws_info.alloc(8);
         c->d_tickets.alloc(kTickets);
         SVT_CUDA(cudaMemsetAsync(c->d_tickets.get(), 0, kTickets * sizeof(unsigned), c->stream));
         nccl_init(c->comm, rank, world, nccl_id);

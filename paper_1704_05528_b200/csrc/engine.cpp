@@ -162,9 +162,10 @@ void qr_panel(Engine& E, i64 m, bool dist, const double* X, i64 ldx, i64 w, doub
               const int* pred) {
     svt_ctx* c = E.ctx;
     dist = dist && c->comm.world > 1;
-    E.G.ensure(static_cast<size_t>(w * w));
-    E.Rinv.ensure(static_cast<size_t>(w * w));
-    E.tmp.ensure(static_cast<size_t>(std::max<i64>(1, m) * w));
+    const i64 wc = std::max<i64>(w, 64);  // panels are <= 64 wide: size once
+    E.G.ensure(static_cast<size_t>(wc * wc));
+    E.Rinv.ensure(static_cast<size_t>(wc * wc));
+    E.tmp.ensure(static_cast<size_t>(std::max<i64>(1, m) * wc));
     int* status = dfl(c, F_QRSTAT);
     zero_flag(c, F_QRSTAT);
     if (!dist && w <= 16) {
@@ -174,7 +175,7 @@ void qr_panel(Engine& E, i64 m, bool dist, const double* X, i64 ldx, i64 w, doub
         gemm(c, K_QR, false, m, w, w, 1.0, X, ldx, E.Rinv.get(), w, 0.0, E.tmp.get(), w, pred);
         gram_chol(c, E.tmp.get(), w, m, w, E.G.get(), E.Rinv.get(), status, pred);
         gemm(c, K_QR, false, m, w, w, 1.0, E.tmp.get(), w, E.Rinv.get(), w, 0.0, Qout, ldq, pred);
-        E.hh.ensure(static_cast<size_t>(std::max<i64>(1, m) * w));
+        E.hh.ensure(static_cast<size_t>(std::max<i64>(1, m) * std::max<i64>(w, 64)));
         householder_qr(c, X, m, w, ldx, Qout, ldq, E.hh.get(), pred, status);
         return;
     }
@@ -189,7 +190,7 @@ void qr_panel(Engine& E, i64 m, bool dist, const double* X, i64 ldx, i64 w, doub
     chol_rinv(c, E.G.get(), w, E.Rinv.get(), status, pred);
     gemm(c, K_QR, false, m, w, w, 1.0, E.tmp.get(), w, E.Rinv.get(), w, 0.0, Qout, ldq, pred);
     if (!dist) {
-        E.hh.ensure(static_cast<size_t>(std::max<i64>(1, m) * w));
+        E.hh.ensure(static_cast<size_t>(std::max<i64>(1, m) * std::max<i64>(w, 64)));
         householder_qr(c, X, m, w, ldx, Qout, ldq, E.hh.get(), pred, status);
         return;
     }
@@ -278,6 +279,9 @@ void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out, cudaStre
     E.ctx->comm.allreduce_sum(out, static_cast<size_t>(A->n * w), stream ? stream : E.ctx->stream);
 }
 
+// basis capacity of the engine's QB state (workspace sizing hint)
+static i64 st_cap_hint(const Engine& E) { return std::max<i64>(E.qb.cap, 64); }
+
 // dense.hpp:103-110 on a panel of any width: CholQR2 (w <= 64) or block
 // CGS2 + CholQR2 over 64-column blocks (the column-ordered QR, same nested
 // spans).  X is clobbered.
@@ -293,7 +297,7 @@ void qr_orthonormal(Engine& E, i64 m, bool dist, double* X, i64 ldx, i64 w, doub
         const i64 wb = std::min(B, w - b0);
         double* Xb = X + b0;
         if (b0 > 0) {
-            E.C.ensure(static_cast<size_t>(b0 * wb));
+            E.C.ensure(static_cast<size_t>(std::max(b0, st_cap_hint(E)) * 64));
             for (int pass = 0; pass < 2; ++pass) {
                 gemm(c, K_QR, true, b0, wb, m, 1.0, Qout, ldq, Xb, ldx, 0.0, E.C.get(), wb);
                 if (dist) allreduce(c, E.C.get(), static_cast<size_t>(b0 * wb));
