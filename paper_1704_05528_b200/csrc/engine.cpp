@@ -750,19 +750,23 @@ static void finalize_mode(Engine& E, const QBDev& st, FinalizeMode mode, double 
 // rounds one by one with the exact fallback semantics).
 // Sketch of a batch (Omega for rounds round0 .. round0 + K - 1, then
 // Gram-Schmidt coefficients C (r0 x w) = Q[:, :r0]^T X (sketch.hpp:133) on
-// the INT8 tensor cores from cached digit slices of the basis (ozaki.cu;
-// SVTB_OZAKI=1), else the DMMA GEMM.  The slices of a column are built once,
-// the first time the column takes part in a product.
-static bool ozaki_enabled() {  // read per batch (cheap), so tests can toggle it
+// the INT8 tensor cores from cached digit slices of the basis (ozaki.cu),
+// else the DMMA GEMM.  The slices of a column are built once, the first time
+// the column takes part in a product.  Default: bases of >= 4096 columns
+// (config 5: +5 % iterations/s; at config 4's ~2,000 columns the INT8 kernel's
+// SM footprint slows the concurrent side-stream SpMM as much as it saves);
+// SVTB_OZAKI=0 / 1 turns it off / on for every basis of >= 64 columns.
+static bool ozaki_enabled(i64 r0) {  // read per batch (cheap), so tests can toggle it
     const char* e = std::getenv("SVTB_OZAKI");
-    return e != nullptr && std::atoi(e) != 0;
+    if (e != nullptr) return std::atoi(e) != 0;
+    return r0 >= 4096;
 }
 
 static void basis_tx(Engine& E, QBDev& st, i64 r0, i64 w, const double* X, i64 ldx, double* C) {
     svt_ctx* c = E.ctx;
     const i64 m = st.m_local;
     const double* Q = st.Q.get();
-    if (ozaki_enabled() && m >= 4096 && r0 >= 64 && w > 16) {
+    if (ozaki_enabled(r0) && m >= 4096 && r0 >= 64 && w > 16) {
         const i64 tiles = ozaki_rows_pad(st.cap) / 128;
         const size_t bytes = static_cast<size_t>(8) * tiles * 128 * ozaki_kpad(m);
         if (st.qs_tiles != tiles) {
