@@ -666,6 +666,28 @@ def _config_solver(config, iters, batching=True):
     return A, recs, res
 
 
+@pytest.mark.parametrize("config", [1, 3, 4])
+def test_no_device_allocation_inside_later_iterations(config):
+    """Every cudaFree is a device-wide synchronisation that drains the
+    speculative side stream, so once the workspaces have reached their size
+    (after the warm-up iterations) an SVT iteration must allocate nothing
+    (DESIGN.md §3).  Configs 1, 3, 4 at full size, iterations 4-7."""
+    d = G.synth_config(config, 1)
+    A = G.SampledMatrix(d["m"], d["n"], *d["train"])
+    frob = float(np.sqrt(G.sp_frob_norm_sq(A)))
+    cfg, stop = G.config_params(config, A.nnz, d["m"], d["n"], frob)
+    S = G.Solver(A, cfg, stop)
+    for _ in range(3):
+        S.step()
+    a0 = G.Context.alloc_stats()
+    for _ in range(4):
+        S.step()
+    a1 = G.Context.alloc_stats()
+    S.close()
+    A.close()
+    assert a1["mallocs"] == a0["mallocs"] and a1["frees"] == a0["frees"], (a0, a1)
+
+
 @pytest.mark.parametrize("config,iters", [(3, 4), (4, 3)])
 def test_full_size_batched_equals_sequential_and_is_deterministic(config, iters):
     """At the BASELINE sizes the oracle is too slow, so parity is checked
