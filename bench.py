@@ -389,8 +389,9 @@ def main():
         d2h = 8 * 8 * nsteps + 8 * (res.U.size + res.V.size + res.sigma.size)
         e2e = {"value": nsteps / el, "unit": "iter/s", "h2d_bytes_per_step": int(h2d / nsteps),
                "d2h_bytes_per_step": int(d2h / nsteps),
-               "note": "public C-ABI path from host buffers: CSR upload + kickstart + the same W+K iterations "
-                       "(each reads its record back) + factor download, wall clock"}
+               "note": "public C-ABI path from host buffers: CSR upload + kickstart + iterations 1..W+K "
+                       "(each reads its record back) + factor download, wall clock; it includes the early, "
+                       "cheaper iterations (smaller bases), while value times iterations W+1..W+K only"}
         s2.close()
         A2.close()
 
