@@ -101,6 +101,20 @@ __global__ void __launch_bounds__(32) mt_twist_kernel(unsigned long long seed, i
     for (int i = lane; i < MT_N; i += 32) state[i] = mt[i];
 }
 
+// normal q of the block lands at (row q % rows, column q / rows) of the
+// row-major panel: one 64-bit division per pair (the second normal is the
+// next row, or the top of the next column)
+__device__ __forceinline__ void store_pair(double* __restrict__ out, long long ld, long long rows, long long total,
+                                           long long q0, double z0, double z1) {
+    const long long c0 = q0 / rows;
+    const long long r0 = q0 - c0 * rows;
+    if (q0 < total) out[r0 * ld + c0] = z0;
+    if (q0 + 1 < total) {
+        const bool wrap = (r0 + 1 == rows);
+        out[(wrap ? 0 : r0 + 1) * ld + (wrap ? c0 + 1 : c0)] = z1;
+    }
+}
+
 // pairs [0, npairs) of this chunk; global normal index q = 2*(pair0 + p) + {0,1}
 __global__ void box_muller_kernel(const unsigned long long* __restrict__ draws, long long npairs, long long pair0,
                                   long long rows, long long total, double* __restrict__ out, long long ld) {
@@ -113,10 +127,9 @@ __global__ void box_muller_kernel(const unsigned long long* __restrict__ draws, 
     const double radius = sqrt(-2.0 * log(u1));
     const double angle = 2.0 * 3.14159265358979323846 * u2;
     const long long q0 = 2 * (pair0 + p);
-    const double z0 = radius * cos(angle);
-    const double z1 = radius * sin(angle);
-    if (q0 < total) out[(q0 % rows) * ld + q0 / rows] = z0;
-    if (q0 + 1 < total) out[((q0 + 1) % rows) * ld + (q0 + 1) / rows] = z1;
+    double sn, cs;
+    sincos(angle, &sn, &cs);
+    store_pair(out, ld, rows, total, q0, radius * cs, radius * sn);
 }
 
 // K independent streams at once: block k seeds std::mt19937_64 with
@@ -188,10 +201,9 @@ __global__ void box_muller_multi_kernel(const unsigned long long* __restrict__ d
     const double radius = sqrt(-2.0 * log(u1));
     const double angle = 2.0 * 3.14159265358979323846 * u2;
     const long long q0 = 2 * p;
-    const double z0 = radius * cos(angle);
-    const double z1 = radius * sin(angle);
-    if (q0 < total) o[(q0 % rows) * ld + q0 / rows] = z0;
-    if (q0 + 1 < total) o[((q0 + 1) % rows) * ld + (q0 + 1) / rows] = z1;
+    double sn, cs;
+    sincos(angle, &sn, &cs);
+    store_pair(o, ld, rows, total, q0, radius * cs, radius * sn);
 }
 
 }  // namespace
