@@ -1,4 +1,6 @@
-# host CPU state around bench runs: load, steal time, process CPU time
+# host CPU state around bench runs (load, steal, process CPU time, context switches):
+# NRUNS=8 bash scripts/host_probe.sh — used to rule out host contention as the
+# cause of the sporadic slow steps (they were device-wide syncs of cudaFree)
 cat /proc/loadavg
 python - <<'PY'
 import json, resource, subprocess, time
