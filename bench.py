@@ -43,8 +43,8 @@ CONFIG_NAMES = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=DEFAULT_CONFIG)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -56,17 +56,13 @@ def parse():
 
 # ---------------------------------------------------------------------------
 def load_problem(config, seed):
-    """Host CSR (global) for train and test sets of a BASELINE config."""
-    from paper_1704_05528_b200 import api as G
-    d = G.synth_config(config, seed)
-    m, n = d["m"], d["n"]
-    if config == 5:
-        train = d["csr"]
-        test = None
-    else:
-        train = G.build_csr(m, n, *d["train"])
-        test = G.build_csr(m, n, *d["test"]) if d["test"] is not None else None
-    return m, n, train, test
+    """Host CSR (global) for train and test sets of a BASELINE config, from
+    the shared generator (csrc/synth.cpp) compiled into liboracle.so: the
+    CPU arms load no product library."""
+    from oracle import oracle as O
+    d = O.synth_config(config, seed)
+    tr, te = d["train"], d["test"]
+    return d["m"], d["n"], (tr.rowptr, tr.col, tr.val), ((te.rowptr, te.col, te.val) if te is not None else None)
 
 
 def frob(val):
@@ -166,51 +162,56 @@ def measured_fp64_peak():
 
 
 # ---------------------------------------------------------------------------
-def cpu_oracle_rate(config, seed, m, n, train, test, budget, max_iters):
-    """Times the CPU oracle (the reference's algorithm restated in C++,
-    single-threaded like the reference) on the same workload; stops after the
-    iteration that crosses `budget` seconds.  Returns (iters/s, sample text)."""
+def oracle_threads():
     from oracle import oracle as O
-    from paper_1704_05528_b200 import api as G
+    return O.num_threads()
+
+
+def cpu_matched_iteration(config, m, n, train, test, ckpt, W):
+    """The CPU oracle (the reference's algorithm restated, all host threads)
+    on iteration W + 1 — the first iteration of the GPU's timed window —
+    resumed from the device state after W iterations (svt_solver_checkpoint),
+    so both arms time the same iteration of the same run.  Returns
+    (seconds, record)."""
+    from oracle import oracle as O
     rp, co, va = train
     A = O.Csr(m, n, rp, co, va)
     T = O.Csr(m, n, *test) if test is not None else None
-    cfg, stop = G.config_params(config, int(rp[-1]), m, n, frob(va))
-    cfg.maxit = max_iters
-    stamps = []
+    cfg, stop = O.config_params(config, int(rp[-1]), m, n, frob(va))
+    cfg.maxit = W + 1
+    st = ckpt["state"]
+    s = int(st.s)
+    start = dict(iter=int(st.iter), y_vals=ckpt["y_vals"][: int(rp[-1])],
+                 u_prev=np.asarray(ckpt["u_prev"][: m * s]).reshape(s, m).T if s else np.zeros((m, 0)),
+                 eps_threshold=st.eps_threshold, eps_min=st.eps_min)
     t0 = time.perf_counter()
-
-    def obs(rec, U, s, V):
-        stamps.append(time.perf_counter())
-        return (time.perf_counter() - t0) < budget
-
-    O.svt_run(A, cfg, stop, observer=obs, test=T)
-    its = len(stamps)
-    el = stamps[-1] - t0 if stamps else time.perf_counter() - t0
-    return its / el, f"first {its} SVT iteration(s) from the kickstart on the full {CONFIG_NAMES[config]} ({el:.1f} s)", its, el
+    r = O.svt_run(A, cfg, stop, test=T, start=start)
+    return time.perf_counter() - t0, r.trace[0]
 
 
 # ---------------------------------------------------------------------------
 def run_reference(args, rank, world):
-    """--impl reference: the reference's algorithm (CPU oracle port; the
-    reference itself cannot be built here) on the same config/metric."""
+    """--impl reference: the reference's algorithm on the host CPU (the
+    oracle port: the reference itself cannot be built here),
+    all host threads, on the same config / metric.  Bounded sample: SVT
+    iterations from the kickstart (the first ones of the same run) until
+    W + K iterations or a time cap.  Loads only liboracle.so."""
     if rank != 0:
         return
     if args.config == 5:
-        print(json.dumps({"impl": "reference", "unavailable": "one cfg5 oracle iteration takes hours on one core "
+        print(json.dumps({"impl": "reference", "unavailable": "one cfg5 oracle iteration takes hours on the host "
                                                               "(SURVEY §8d); the reference arm runs on config 4"}),
               flush=True)
         return
     m, n, train, test = load_problem(args.config, args.seed)
     from oracle import oracle as O
-    from paper_1704_05528_b200 import api as G
     rp, co, va = train
     A = O.Csr(m, n, rp, co, va)
     T = O.Csr(m, n, *test) if test is not None else None
-    cfg, stop = G.config_params(args.config, int(rp[-1]), m, n, frob(va))
+    cfg, stop = O.config_params(args.config, int(rp[-1]), m, n, frob(va))
     cfg.maxit = args.warmup + args.steps
     stamps = [time.perf_counter()]
-    budget = max(90.0, args.cpu_budget * 4)
+    budget = max(120.0, args.cpu_budget * 6)
 
     def obs(rec, U, s, V):
         stamps.append(time.perf_counter())
@@ -218,17 +219,19 @@ def run_reference(args, rank, world):
 
     O.svt_run(A, cfg, stop, observer=obs, test=T)
     d = np.diff(stamps)
-    timed = d[args.warmup:] if len(d) > args.warmup else d
-    value = len(timed) / float(np.sum(timed))
-    sample = (f"{len(d)} consecutive oracle SVT iterations (of W+K={args.warmup + args.steps}, {budget:.0f} s cap); "
-              f"rate over the last {len(timed)}")
+    value = len(d) / float(np.sum(d))
+    cores = O.num_threads()
+    sample = (f"SVT iterations 1-{len(d)} of the same run from the kickstart (GPU arm times {args.warmup + 1}-"
+              f"{args.warmup + args.steps}; later iterations carry wider bases and cost more), {budget:.0f} s cap, "
+              f"oracle port with {cores} OpenMP threads")
     print(json.dumps({
-        "metric": "SVT iters/sec (R4SVD)", "value": value, "unit": "iter/s", "n_gpus": world, "steps": len(timed),
-        "warmup": min(args.warmup, len(d)), "ms_per_step": 1000.0 / value, "higher_is_better": True,
+        "metric": "SVT iters/sec (R4SVD)", "value": value, "unit": "iter/s", "n_gpus": world, "steps": len(d),
+        "warmup": 0, "ms_per_step": 1000.0 / value, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
         "config": {"workload": CONFIG_NAMES[args.config], "config": args.config, "m": m, "n": n,
-                   "nnz": int(rp[-1]), "parallelism": "single CPU thread (reference has no threads)"},
-        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": 1, "kind": "port", "sample": sample},
+                   "nnz": int(rp[-1]), "parallelism": f"host CPU, {cores} threads",
+                   "iterations_timed": list(range(1, len(d) + 1))},
+        "cpu_baseline": {"value": value, "unit": "iter/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -276,47 +279,128 @@ def main():
     else:
         ctx = G.Context(local)
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     A = G.SampledMatrix.from_csr(m, n, rp, co, va, ctx=ctx, row_block=(rb, re_))
     T = G.SampledMatrix.from_csr(m, n, *test, ctx=ctx, row_block=(rb, re_)) if test is not None else None
     cfg, stop = G.config_params(args.config, int(rp[-1]), m, n, frob(va))
     cfg.maxit = max(cfg.maxit, args.warmup + args.steps + 1)
     solver = G.Solver(A, cfg, stop, test=T)
     setup_s = time.perf_counter() - t_setup
+    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
 
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    # warm-up: iterations 1..W (iteration 1's device time feeds the matched
+    # CPU comparison), then a host checkpoint of the state after W
+    # iterations: the e2e leg and the profiled pass resume from it, and the
+    # CPU leg times iteration W + 1 from the same state
+    warm_ms = []
     for _ in range(args.warmup):
+        a = ev()
         solver.step()
+        ctx.join()
+        b = ev()
+        b.synchronize()
+        warm_ms.append(a.elapsed_time(b))
     ctx.sync()
-    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    ckpt = solver.checkpoint()
+
+    # ---- timed window: iterations W+1..W+K, no instrumentation ----------
     ctx.reset_stats()
-    ctx.set_profiling(not os.environ.get("SVTB_BENCH_NOPROF"))  # dev switch: A/B of the per-launch events
+    ctx.set_profiling(False)
     clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
     clocks.start()
     al0 = G.Context.alloc_stats()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    e0 = ev()
+    marks = []
     recs = []
     for _ in range(args.steps):
         recs.append(solver.step())
+        marks.append(ev())
     ctx.join()  # the timed region also covers any speculative side-stream work still in flight
-    e1.record(stream)
+    e1 = ev()
     e1.synchronize()
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
     al1 = G.Context.alloc_stats()
-    ms_local = e0.elapsed_time(e1)
-    ms = max_over_ranks(ms_local)
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    step_ms = [e0.elapsed_time(marks[0])] + [marks[i - 1].elapsed_time(marks[i]) for i in range(1, len(marks))]
     launches = ctx.launch_count()
     hstats = ctx.host_stats()
-    stats = {KCLASS[k]: ctx.kernel_stats(k) for k in range(8)}
-    ctx.set_profiling(False)
     value = args.steps * 1000.0 / ms  # whole-job iterations per second
+    solver.close()  # release the timed run's basis before the next legs allocate their own
 
-    # roofline: the dominant kernel class of the step by device time.  The
-    # sparse passes are held against HBM (algorithmic bytes); the dense FP64
+    # ---- e2e: the public C-ABI path from pinned host buffers -------------
+    # timed: upload of the sample sets (CSR) and of the iteration state
+    # after W iterations, iterations W+1..W+K through svt_solver_step (each
+    # reads its record back), download of the result factors
+    e2e = None
+    if not args.no_e2e:
+        def pinned(x):
+            t = torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+            return t.numpy()
+        lrp = rp[rb: re_ + 1]
+        s0, s1 = int(lrp[0]), int(lrp[-1])
+        host = {"rp": pinned(lrp - lrp[0]), "co": pinned(co[s0:s1]), "va": pinned(va[s0:s1])}
+        if test is not None:
+            trp = test[0][rb: re_ + 1]
+            t0_, t1_ = int(trp[0]), int(trp[-1])
+            host.update({"trp": pinned(trp - trp[0]), "tco": pinned(test[1][t0_:t1_]),
+                         "tva": pinned(test[2][t0_:t1_])})
+        ck_h = {k: (pinned(v) if isinstance(v, np.ndarray) else v) for k, v in ckpt.items()}
+        h2d = sum(host[k].nbytes for k in host) + sum(ck_h[k].nbytes for k in
+                                                      ("y_vals", "u_prev", "best_U", "best_sigma", "best_V"))
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        A2 = G.SampledMatrix.from_csr(m, n, host["rp"], host["co"], host["va"], ctx=ctx, row_block=(0, re_ - rb)) \
+            if world == 1 else G.SampledMatrix.from_csr(m, n, rp, co, va, ctx=ctx, row_block=(rb, re_))
+        T2 = None
+        if test is not None:
+            T2 = G.SampledMatrix.from_csr(m, n, host["trp"], host["tco"], host["tva"], ctx=ctx,
+                                          row_block=(0, re_ - rb)) \
+                if world == 1 else G.SampledMatrix.from_csr(m, n, *test, ctx=ctx, row_block=(rb, re_))
+        s2 = G.Solver.resume(A2, cfg, stop, ck_h, test=T2)
+        recs2 = [s2.step() for _ in range(args.steps)]
+        res = s2.result()
+        ctx.sync()
+        el = max_over_ranks(time.perf_counter() - t0)
+        d2h = 96 * args.steps + 8 * (res.U.size + res.V.size + res.sigma.size)
+        same = all((a["rank"], a["extension_rounds"], a["kept"], a["residual"]) ==
+                   (b["rank"], b["extension_rounds"], b["kept"], b["residual"]) for a, b in zip(recs, recs2))
+        e2e = {"value": args.steps / el, "unit": "iter/s", "h2d_bytes_per_step": int(h2d / args.steps),
+               "d2h_bytes_per_step": int(d2h / args.steps),
+               "iterations": [r["iter"] for r in recs2], "same_records_as_timed_window": same,
+               "note": "public C-ABI path, wall clock: CSR upload of the sample sets + resume from the host "
+                       "checkpoint after W iterations (Y values, U_prev, best factors) from pinned memory, "
+                       "iterations W+1..W+K (each reads its record back), factor download"}
+        s2.close()
+        A2.close()
+        if T2 is not None:
+            T2.close()
+
+    # ---- profiled pass: the same iterations again, with per-launch events
+    s3 = G.Solver.resume(A, cfg, stop, ckpt, test=T)
+    ctx.reset_stats()
+    ctx.set_profiling(True)
+    for _ in range(args.steps):
+        s3.step()
+    ctx.join()
+    ctx.sync()
+    stats = {KCLASS[k]: ctx.kernel_stats(k) for k in range(8)}
+    hstats_prof = ctx.host_stats()
+    ctx.set_profiling(False)
+    s3.close()
+
+    # roofline: the dominant kernel class by device time (per-launch CUDA
+    # events of the profiled pass over the same iterations).  The sparse
+    # passes are held against HBM (algorithmic bytes); the dense FP64
     # contractions (CGS / CholQR / finalize GEMMs on the DMMA pipe) against
     # the FP64 GEMM peak when their arithmetic intensity exceeds the machine
     # balance, else against HBM.
@@ -336,27 +420,21 @@ def main():
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof.update({"kernel": dom, "arith_intensity_flop_per_byte": ai, "machine_balance": balance,
                  "launches": s["launches"], "avg_launch_us": 1000.0 * s["total_ms"] / max(1, s["launches"]),
-                 "share_of_step": s["total_ms"] / max(1e-9, sum(v["total_ms"] for v in stats.values()))})
+                 "share_of_step": s["total_ms"] / max(1e-9, sum(v["total_ms"] for v in stats.values())),
+                 "timing": "per-launch CUDA events in a separate profiled pass over iterations W+1..W+K "
+                           "(resumed from the same state); the timed window runs without them"})
     # the sparse passes, always reported against HBM (north star: SpMM/SDDMM
-    # GB/s vs peak), plus the SpMMs' L2 gather rate: every stored entry reads
-    # one 8w-byte panel row (= 4 x the 2 nnz w flops), which is what bounds
-    # them (ncu: DRAM ~3 %, L2 hit ~96 %); ceiling = the LTS throughput cap
-    # of the microarchitecture guide (~6300 B/clk at 1.965 GHz)
-    l2_cap_tbs = 6300.0 * 1.965e9 / 1e12
+    # GB/s vs peak), plus the SpMMs' gather rate: every stored entry reads
+    # one 8w-byte panel row (= 4 x the 2 nnz w flops)
     sparse = {}
     for k in ("spmm", "spmm_t", "sddmm_update"):
         v = stats[k]
         if v["total_ms"] > 0:
             sparse[k] = {"achieved_gbs": v["bytes"] / (v["total_ms"] * 1e-3) / 1e9,
-                         "frac": v["bytes"] / (v["total_ms"] * 1e-3) / 1e9 / peak_bw}
+                         "frac": v["bytes"] / (v["total_ms"] * 1e-3) / 1e9 / peak_bw,
+                         "launches": v["launches"], "avg_launch_us": 1000.0 * v["total_ms"] / max(1, v["launches"])}
             if k != "sddmm_update":
-                g = 4.0 * v["flops"] / (v["total_ms"] * 1e-3) / 1e12
-                sparse[k].update({"l2_gather_tbs": g, "l2_gather_ceiling_tbs": l2_cap_tbs,
-                                  "l2_gather_frac": g / l2_cap_tbs})
-    if dom in ("spmm", "spmm_t"):
-        roof["note"] = ("L2-gather bound, not HBM: see sparse_roofline[%s].l2_gather_* (DRAM traffic per "
-                        "launch ~ the algorithmic bytes)" % dom)
-    step_ms_kernels = {k: v["total_ms"] / args.steps for k, v in stats.items()}
+                sparse[k]["gather_tbs"] = 4.0 * v["flops"] / (v["total_ms"] * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -368,43 +446,27 @@ def main():
             traffic = None
     roof["traffic"] = traffic
 
-    solver.close()  # release the timed run's basis before the e2e run allocates its own
-    # e2e: the public C-ABI call with host buffers: upload + kickstart + K
-    # iterations (each reads its record back) + factor download
-    e2e = None
-    if not args.no_e2e:
-        barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        A2 = G.SampledMatrix.from_csr(m, n, rp, co, va, ctx=ctx, row_block=(rb, re_))
-        s2 = G.Solver(A2, cfg, stop)
-        nsteps = args.warmup + args.steps
-        for _ in range(nsteps):
-            s2.step()
-        res = s2.result()
-        ctx.sync()
-        el = max_over_ranks(time.perf_counter() - t0)
-        nnz_l = int(rp[re_] - rp[rb])
-        h2d = 8 * (re_ - rb + 1) + 16 * nnz_l
-        d2h = 8 * 8 * nsteps + 8 * (res.U.size + res.V.size + res.sigma.size)
-        e2e = {"value": nsteps / el, "unit": "iter/s", "h2d_bytes_per_step": int(h2d / nsteps),
-               "d2h_bytes_per_step": int(d2h / nsteps),
-               "note": "public C-ABI path from host buffers: CSR upload + kickstart + iterations 1..W+K "
-                       "(each reads its record back) + factor download, wall clock; it includes the early, "
-                       "cheaper iterations (smaller bases), while value times iterations W+1..W+K only"}
-        s2.close()
-        A2.close()
-
     cpu = None
+    matched = None
     if rank == 0 and world == 1 and not args.no_cpu and args.config == 5:
-        cpu = {"value": None, "unit": "iter/s", "cores": 1, "kind": "port",
-               "sample": "none: one cfg5 oracle iteration (t0 = 5000 sketch of a 1e8-entry matrix, ~2,000 "
-                         "extension rounds to r ~ 20k) takes hours on one core (SURVEY §8d); the CPU baseline "
-                         "is reported on the default workload (config 4)"}
+        cpu = {"value": None, "unit": "iter/s", "cores": oracle_threads(), "kind": "port",
+               "sample": "none: one cfg5 oracle iteration (~2,000 extension rounds to r ~ 20k on a 1e8-entry "
+                         "matrix) takes hours on the host (SURVEY §8d); the CPU baseline is reported on config 4"}
     elif rank == 0 and world == 1 and not args.no_cpu:
-        v, sample, its, el = cpu_oracle_rate(args.config, args.seed, m, n, train, test, args.cpu_budget,
-                                             args.warmup + args.steps)
-        cpu = {"value": v, "unit": "iter/s", "cores": 1, "kind": "port", "sample": sample}
+        cpu_s, crec = cpu_matched_iteration(args.config, m, n, train, test, ckpt, args.warmup)
+        g = recs[0]
+        cores = oracle_threads()
+        par = {"rank_rounds_kept_equal": (g["rank"], g["extension_rounds"], g["kept"]) ==
+               (crec["rank"], crec["extension_rounds"], crec["kept"]),
+               "residual_rel_diff": abs(g["residual"] - crec["residual"]) / abs(crec["residual"])}
+        cpu = {"value": 1.0 / cpu_s, "unit": "iter/s", "cores": cores, "kind": "port",
+               "sample": f"SVT iteration {args.warmup + 1} (the first iteration of the timed window) resumed from "
+                         f"the device state after {args.warmup} iterations; oracle port (the reference's "
+                         f"algorithm restated), {cores} OpenMP threads; {cpu_s:.1f} s",
+               "parity": par}
+        matched = {"iteration": args.warmup + 1, "gpu_ms": step_ms[0], "cpu_ms": 1000.0 * cpu_s,
+                   "gpu_over_cpu_speedup": 1000.0 * cpu_s / step_ms[0],
+                   "iteration1_gpu_ms": warm_ms[0] if warm_ms else None}
 
     if rank == 0:
         line = {
@@ -415,22 +477,24 @@ def main():
                        "nnz": int(rp[-1]), "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU",
                        "iterations_timed": [r["iter"] for r in recs], "revealed_rank": [r["rank"] for r in recs],
                        "kept_rank": [r["kept"] for r in recs], "rounds": [r["extension_rounds"] for r in recs],
+                       "ms_per_iteration": [round(x, 2) for x in step_ms],
                        "l2": ("working set per pass below/near L2 for cfg1-4; no flush between steps" if args.config != 5
                               else "inputs larger than L2 (Y 1.2 GB, Q/B^T tens of GB): no flush needed"),
                        "setup_s": round(setup_s, 2)},
             "roofline": roof,
             "sparse_roofline": sparse,
-            "kernel_ms_per_step": {k: round(v, 3) for k, v in step_ms_kernels.items()},
+            "kernel_ms_per_step": {k: round(v["total_ms"] / args.steps, 3) for k, v in stats.items()},
             "gpu_launches": launches,
             "host": {"syncs_per_step": hstats["syncs"] / args.steps,
-                     "sync_wait_ms_per_step": hstats["sync_ms"] / args.steps,
+                     "sync_wait_ms_per_step_profiled_pass": hstats_prof["sync_ms"] / args.steps,
                      "device_allocs_in_timed_region": al1["mallocs"] - al0["mallocs"],
                      "device_frees_in_timed_region": al1["frees"] - al0["frees"],
                      "alloc_ms_in_timed_region": al1["ms"] - al0["ms"],
-                     "kernel_ms_per_step": sum(v["total_ms"] for v in stats.values()) / args.steps},
+                     "kernel_ms_per_step_profiled_pass": sum(v["total_ms"] for v in stats.values()) / args.steps},
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "matched_window": matched,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -119,6 +119,18 @@ int svt_ctx_create(int device, svt_ctx** out);
 /* One rank of a world: nccl_id is the 128-byte ncclUniqueId of rank 0. */
 int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, svt_ctx** out);
 int svt_nccl_get_unique_id(void* out128);
+/* Host-staged collectives instead of NCCL: every all-reduce of the library
+ * (the n x w partials of Y^T X, the Gram blocks and the norms)
+ * is copied to pinned host memory and handed to `fn`, which must sum the
+ * `count` doubles element-wise across the `world` ranks in place (e.g.
+ * torch.distributed over gloo) and return 0.  All ranks issue the same
+ * sequence of calls (every branch is taken on all-reduced values).  Runs the
+ * row-sharded path where NVLink / NCCL is not available: several ranks
+ * sharing one GPU in tests, or host-coordinated clusters. */
+typedef int (*svt_allreduce_fn)(double* buf, int64_t count, void* user);
+int svt_ctx_create_hostcomm(int device, int rank, int world, svt_allreduce_fn fn, void* user, svt_ctx** out);
+/* all-reduces issued by this context and the doubles they carried */
+int svt_ctx_comm_stats(svt_ctx* ctx, int64_t* calls, double* doubles);
 int svt_ctx_destroy(svt_ctx* ctx);
 int svt_ctx_sync(svt_ctx* ctx);
 /* make the context stream wait for all work issued on the library's side
@@ -278,6 +290,35 @@ int svt_result_info(svt_result* r, int64_t* n_records, int64_t* m_local, int64_t
 int svt_result_trace(svt_result* r, svt_record* out);
 int svt_result_factors(svt_result* r, double* U, double* sigma, double* V);
 int svt_result_free(svt_result* r);
+
+/* ---- checkpoint / resume ------------------------------------------------
+ * The reference has no solver checkpoint (the manifest re-runs
+ * from scratch).  The state below is everything svt_run_backend carries
+ * from one iteration to the next (solver.hpp:221-238, 280-284, 299-303,
+ * 321-324), so resuming at iteration i reproduces iterations i+1.. of the
+ * uninterrupted run bit for bit (same seeds, thresholds, recycled basis).
+ * Host buffers: y_vals = the iterate Y on this rank's pattern (nnz_local,
+ * CSR order); u_prev = U_prev (m_local x s, column-major); best_U / best_V
+ * column-major (m_local x best_k, n x best_k), best_sigma (best_k).  In
+ * svt_solver_checkpoint any buffer may be NULL (query the sizes first). */
+typedef struct svt_solver_state {
+    int32_t iter;        /* iterations completed                              */
+    int32_t done;        /* the run already stopped                            */
+    int32_t converged;
+    int32_t last_rounds; /* previous sketch's round count (batch-size hint)    */
+    int64_t s;           /* recycled basis width                               */
+    int64_t best_k;      /* rank of the best-so-far factors                    */
+    double eps_threshold;
+    double eps_min;      /* running minimum of the dual residual (cooling)     */
+    double best_metric;
+    double frob_y_sq;    /* ||Y||_F^2 of the current iterate (all ranks)       */
+    double frob_a;       /* ||P_Lambda A||_F                                   */
+} svt_solver_state;
+int svt_solver_checkpoint(svt_solver* s, svt_solver_state* st, double* y_vals, double* u_prev, double* best_U,
+                          double* best_sigma, double* best_V);
+int svt_solver_resume(svt_mat* A, const svt_config* cfg, svt_stop stop, svt_backend backend, svt_mat* test,
+                      const svt_solver_state* st, const double* y_vals, const double* u_prev, const double* best_U,
+                      const double* best_sigma, const double* best_V, svt_solver** out);
 
 /* ---- synthetic inputs for the five BASELINE configs (host) ------------- */
 /* Generates the observed (train) triplets and, for configs 3/4, the held-out

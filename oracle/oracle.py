@@ -329,8 +329,13 @@ class SvtResult:
     converged: bool
 
 
-def svt_run_backend(A: Csr, cfg: SvtConfig, stop: StopRule, backend: Backend, observer=None, test: Csr = None):
-    """solver.hpp:215-328.  observer(rec_dict, U, sigma, V) -> bool (False stops)."""
+def svt_run_backend(A: Csr, cfg: SvtConfig, stop: StopRule, backend: Backend, observer=None, test: Csr = None,
+                    start=None):
+    """solver.hpp:215-328.  observer(rec_dict, U, sigma, V) -> bool (False stops).
+    start (test-harness extension): dict(iter, y_vals, u_prev (m x s array),
+    eps_threshold, eps_min) — continue after `iter` completed iterations
+    from that state (the product's svt_solver_checkpoint state) instead of
+    the kickstart."""
     cb = None
     if observer is not None:
         def _obs(rec, m_local, n, k, U, sigma, V, user):
@@ -345,8 +350,17 @@ def svt_run_backend(A: Csr, cfg: SvtConfig, stop: StopRule, backend: Backend, ob
         targs = (C.c_int64(test.nnz), _ptr(test.rowptr, P_I64), _ptr(test.col, P_I64), _ptr(test.val))
     else:
         targs = (C.c_int64(0), None, None, None)
-    _check(lib().oracle_svt_run(*A.args(), C.byref(cfg), stop, backend, *targs,
-                                cb, None, C.byref(h)))
+    if start is None:
+        sargs = (C.c_int(-1), None, C.c_int64(0), None, C.c_double(0.0), C.c_double(0.0))
+    else:
+        y = _f64(start["y_vals"])
+        assert y.size >= A.nnz
+        up = np.asarray(start["u_prev"], dtype=np.float64).reshape(A.m, -1)
+        upc = _cm(up) if up.size else np.zeros(1)
+        sargs = (C.c_int(int(start["iter"])), _ptr(y), C.c_int64(up.shape[1]), _ptr(upc.ravel(order="K")),
+                 C.c_double(start["eps_threshold"]), C.c_double(start["eps_min"]))
+    _check(lib().oracle_svt_resume(*A.args(), C.byref(cfg), stop, backend, *targs,
+                                   cb, None, *sargs, C.byref(h)))
     L = lib()
     nrec, urows, vrows, k, conv = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64(), C.c_int()
     L.oracle_result_info(h, C.byref(nrec), C.byref(urows), C.byref(vrows), C.byref(k), C.byref(conv))
@@ -363,9 +377,9 @@ def svt_run_backend(A: Csr, cfg: SvtConfig, stop: StopRule, backend: Backend, ob
                      _from_cm(V[: vrows.value * kk], vrows.value, kk), trace, bool(conv.value))
 
 
-def svt_run(A, cfg, stop, observer=None, test=None):
+def svt_run(A, cfg, stop, observer=None, test=None, start=None):
     """solver.hpp:333-336"""
-    return svt_run_backend(A, cfg, stop, Backend.r4svd(), observer, test)
+    return svt_run_backend(A, cfg, stop, Backend.r4svd(), observer, test, start)
 
 
 def svt_run_oracle(A, cfg, stop, observer=None, test=None):
@@ -402,3 +416,78 @@ def sample_dense(A, fraction, seed) -> Csr:
     pos = sample_positions(total, ns, seed).astype(np.int64)
     r, c = pos // n, pos % n
     return sampled(m, n, r, c, A[r, c])
+
+
+def random_triplets(m, n, fill, seed):
+    """proj/tests/test_util.hpp:56-78, exactly: the mt19937_64 partial
+    Fisher-Yates over all cells, then std::normal_distribution values from
+    the same engine (libstdc++)."""
+    cnt = C.c_int64()
+    _check(lib().oracle_random_triplets(C.c_int64(m), C.c_int64(n), C.c_double(fill), C.c_uint64(seed),
+                                        C.byref(cnt), None, None, None))
+    k = cnt.value
+    r, c, v = np.zeros(k, np.int64), np.zeros(k, np.int64), np.zeros(k)
+    _check(lib().oracle_random_triplets(C.c_int64(m), C.c_int64(n), C.c_double(fill), C.c_uint64(seed),
+                                        C.byref(cnt), _ptr(r, P_I64), _ptr(c, P_I64), _ptr(v)))
+    return r, c, v
+
+
+def num_threads():
+    """Host threads the oracle's parallel loops use (OMP_NUM_THREADS)."""
+    return int(lib().oracle_num_threads())
+
+
+def synth_config(config, seed=1):
+    """The BASELINE config generators (the shared csrc/synth.cpp, compiled
+    into liboracle.so): dict(m, n, train=Csr, test=Csr or None); config 5
+    has no test set."""
+    L = lib()
+    m, n = C.c_int64(), C.c_int64()
+    if config == 5:
+        nnz = C.c_int64()
+        _check(L.oracle_synth_config_csr(C.c_int(5), C.c_uint64(seed), C.byref(m), C.byref(n), C.byref(nnz),
+                                         None, None, None))
+        rp = np.zeros(m.value + 1, dtype=np.int64)
+        co = np.zeros(nnz.value, dtype=np.int64)
+        va = np.zeros(nnz.value)
+        _check(L.oracle_synth_config_csr(C.c_int(5), C.c_uint64(seed), C.byref(m), C.byref(n), C.byref(nnz),
+                                         _ptr(rp, P_I64), _ptr(co, P_I64), _ptr(va)))
+        return dict(m=m.value, n=n.value, train=Csr(m.value, n.value, rp, co, va), test=None)
+    ntr, nte = C.c_int64(), C.c_int64()
+    _check(L.oracle_synth_config(C.c_int(config), C.c_uint64(seed), C.byref(m), C.byref(n), C.byref(ntr),
+                                 C.byref(nte), None, None, None, None, None, None))
+    tr = [np.zeros(ntr.value, np.int64), np.zeros(ntr.value, np.int64), np.zeros(ntr.value)]
+    te = [np.zeros(max(nte.value, 1), np.int64), np.zeros(max(nte.value, 1), np.int64), np.zeros(max(nte.value, 1))]
+    _check(L.oracle_synth_config(C.c_int(config), C.c_uint64(seed), C.byref(m), C.byref(n), C.byref(ntr),
+                                 C.byref(nte), _ptr(tr[0], P_I64), _ptr(tr[1], P_I64), _ptr(tr[2]),
+                                 _ptr(te[0], P_I64), _ptr(te[1], P_I64), _ptr(te[2])))
+    train = sampled(m.value, n.value, *tr)
+    test = sampled(m.value, n.value, *(a[: nte.value] for a in te)) if nte.value else None
+    return dict(m=m.value, n=n.value, train=train, test=test)
+
+
+def config_params(config, nnz, m, n, frob_a):
+    """The BASELINE.json parameters of each config,
+    restated from paper_1704_05528_b200.api.config_params so the CPU arms and
+    the fixture script need only this library (a CPU test asserts the two
+    agree).  Returns (SvtConfig, StopRule)."""
+    cfg = SvtConfig()
+    cfg.t0 = max(1, int(0.05 * min(m, n)))
+    cfg.dt = 10
+    cfg.beta = 0.95
+    p = nnz / float(m * n)
+    if config == 1:
+        cfg.tau, cfg.delta = 5.0 * n, 1.2 / p
+        cfg.eps_threshold0, cfg.eps_threshold_min = 1e-2, 1e-6
+        cfg.rel_residual_stop = 1e-4
+    elif config == 2:
+        cfg.tau, cfg.delta = 5.0 * np.sqrt(m * n), 1.2 / p
+        cfg.rel_residual_stop = 1e-4
+    elif config in (3, 4):
+        cfg.tau, cfg.delta = frob_a, 1.9
+    elif config == 5:
+        cfg.tau, cfg.delta = 5.0 * n, 1.2 / p
+        cfg.maxit = 30
+    else:
+        raise ValueError("config must be 1..5")
+    return cfg, StopRule.none()

@@ -2,6 +2,9 @@
 // (svt_oracle.hpp).  Loaded by tests/ and bench.py's CPU-baseline legs only.
 // Structs are shared with the product boundary (include/svt_b200.h) so both
 // sides are driven with byte-identical parameters.
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include "svt_oracle.hpp"
 
 #include "../include/svt_b200.h"
@@ -197,12 +200,12 @@ void oracle_qb_info(oracle_qb* h, int64_t* rank, int* saturated, double* norm_b_
     *norm_b_sq = h->st.norm_b_sq;
     *frob_y_sq = h->st.frob_y_sq;
     *q_rows = h->st.Q.rows;
-    *b_cols = h->st.B.cols;
+    *b_cols = h->st.Bt.rows;
 }
 
 void oracle_qb_copy(oracle_qb* h, double* Q, double* B) {
     to_col_major(h->st.Q, Q);
-    to_col_major(h->st.B, B);
+    to_col_major(transpose(h->st.Bt), B);
 }
 
 int oracle_qb_error_percentage(oracle_qb* h, double* out) {
@@ -287,10 +290,28 @@ void oracle_factors_copy(void* hv, double* U, double* sigma, double* V) {
 void oracle_factors_free(void* hv) { delete static_cast<OFactors*>(hv); }
 
 // --- solver -------------------------------------------------------------------
+int oracle_svt_resume(int64_t m, int64_t n, const int64_t* rowptr, const int64_t* col, const double* val,
+                      const svt_config* c, svt_stop stop, svt_backend backend, int64_t test_nnz,
+                      const int64_t* test_rowptr, const int64_t* test_col, const double* test_val,
+                      svt_observer_fn obs, void* user, int start_iter, const double* y_vals, int64_t s,
+                      const double* u_prev, double eps_threshold, double eps_min, void** out);
+
 int oracle_svt_run(int64_t m, int64_t n, const int64_t* rowptr, const int64_t* col, const double* val,
                    const svt_config* c, svt_stop stop, svt_backend backend, int64_t test_nnz,
                    const int64_t* test_rowptr, const int64_t* test_col, const double* test_val, svt_observer_fn obs,
                    void* user, void** out) {
+    return oracle_svt_resume(m, n, rowptr, col, val, c, stop, backend, test_nnz, test_rowptr, test_col, test_val,
+                             obs, user, -1, nullptr, 0, nullptr, 0.0, 0.0, out);
+}
+
+// start_iter < 0: from the kickstart; else continue after `start_iter`
+// completed iterations from (Y values, U_prev m x s column-major, cooling
+// threshold, running residual minimum) — svt_solver_checkpoint's state.
+int oracle_svt_resume(int64_t m, int64_t n, const int64_t* rowptr, const int64_t* col, const double* val,
+                      const svt_config* c, svt_stop stop, svt_backend backend, int64_t test_nnz,
+                      const int64_t* test_rowptr, const int64_t* test_col, const double* test_val,
+                      svt_observer_fn obs, void* user, int start_iter, const double* y_vals, int64_t s,
+                      const double* u_prev, double eps_threshold, double eps_min, void** out) {
     return guard([&] {
         SvtConfig cfg;
         cfg.tau = c->tau;
@@ -333,8 +354,17 @@ int oracle_svt_run(int64_t m, int64_t n, const int64_t* rowptr, const int64_t* c
         SampledMatrix A = csr(m, n, rowptr, col, val);
         std::unique_ptr<SampledMatrix> test;
         if (test_nnz > 0) test = std::make_unique<SampledMatrix>(csr(m, n, test_rowptr, test_col, test_val));
+        std::unique_ptr<SvtStart> start;
+        if (start_iter >= 0) {
+            start = std::make_unique<SvtStart>();
+            start->iter = start_iter;
+            start->y.assign(y_vals, y_vals + A.nnz());
+            start->U_prev = from_col_major(m, s, u_prev);
+            start->eps_threshold = eps_threshold;
+            start->eps_min = eps_min;
+        }
         auto h = std::make_unique<OResult>();
-        h->r = svt_run_backend(A, cfg, sr, be, observer, test.get());
+        h->r = svt_run_backend(A, cfg, sr, be, observer, test.get(), start.get());
         *out = h.release();
     });
 }
@@ -426,4 +456,66 @@ int oracle_make_geometric(int64_t m, int64_t n, int64_t count, double ratio, uin
     });
 }
 
+// proj/tests/test_util.hpp:56-78 — random_triplets: partial Fisher-Yates
+// over all m*n cells with `rng() % (cells - i)`, then the values from
+// std::normal_distribution<double>(0, 1) on the same engine (libstdc++'s
+// algorithm: the reference tests' own inputs are reproduced exactly when
+// built with the same standard library, as both sides are here).
+int oracle_random_triplets(int64_t m, int64_t n, double fill, uint64_t seed, int64_t* count, int64_t* rows,
+                           int64_t* cols, double* vals) {
+    return guard([&] {
+        std::mt19937_64 rng(seed);
+        std::vector<uint64_t> cells(static_cast<size_t>(m) * static_cast<size_t>(n));
+        for (size_t i = 0; i < cells.size(); ++i) cells[i] = i;
+        size_t ns = static_cast<size_t>(fill * static_cast<double>(cells.size()));
+        if (ns < 1) ns = 1;
+        *count = static_cast<int64_t>(ns);
+        if (rows == nullptr) return;
+        for (size_t i = 0; i < ns; ++i) {
+            const size_t j = i + static_cast<size_t>(rng() % (cells.size() - i));
+            std::swap(cells[i], cells[j]);
+        }
+        std::normal_distribution<double> gauss(0.0, 1.0);
+        for (size_t i = 0; i < ns; ++i) {
+            rows[i] = static_cast<int64_t>(cells[i] / static_cast<uint64_t>(n));
+            cols[i] = static_cast<int64_t>(cells[i] % static_cast<uint64_t>(n));
+            vals[i] = gauss(rng);
+        }
+    });
+}
+
 }  // extern "C"
+
+// --- the BASELINE config generators (paper_1704_05528_b200/csrc/synth.cpp,
+// compiled into this library too: one shared generator for both sides, so
+// the CPU arms never load the product library)
+namespace svtb {
+using i64 = std::int64_t;
+using u64 = std::uint64_t;
+u64 derive_seed_u(u64 seed, u64 stream) { return svt_oracle::derive_seed(seed, stream); }
+void synth_config(int config, u64 seed, i64* m, i64* n, i64* nnz_train, i64* nnz_test, i64* train_rows,
+                  i64* train_cols, double* train_vals, i64* test_rows, i64* test_cols, double* test_vals);
+void synth_config_csr(int config, u64 seed, i64* m, i64* n, i64* nnz, i64* rowptr, i64* col, double* val);
+}  // namespace svtb
+
+extern "C" int oracle_synth_config(int config, uint64_t seed, int64_t* m, int64_t* n, int64_t* nnz_train,
+                                   int64_t* nnz_test, int64_t* train_rows, int64_t* train_cols, double* train_vals,
+                                   int64_t* test_rows, int64_t* test_cols, double* test_vals) {
+    return guard([&] {
+        svtb::synth_config(config, seed, m, n, nnz_train, nnz_test, train_rows, train_cols, train_vals, test_rows,
+                           test_cols, test_vals);
+    });
+}
+
+extern "C" int oracle_synth_config_csr(int config, uint64_t seed, int64_t* m, int64_t* n, int64_t* nnz,
+                                       int64_t* rowptr, int64_t* col, double* val) {
+    return guard([&] { svtb::synth_config_csr(config, seed, m, n, nnz, rowptr, col, val); });
+}
+
+extern "C" int oracle_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

@@ -69,23 +69,34 @@ struct LowRankFactors {
     Index rank() const { return static_cast<Index>(sigma.size()); }
 };
 
+// Host parallelism (OpenMP, -fopenmp): every parallel loop below writes
+// disjoint outputs and every reduction runs in a fixed order inside one
+// thread, so the oracle's results are bitwise identical for any thread count.
+
+// sum_k a[k] * b[k] in a fixed blocked order (8 interleaved partial sums,
+// then combined pairwise): vectorizable without reassociation flags.
+inline double dot(const double* a, const double* b, Index n) {
+    double p[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    Index k = 0;
+    for (; k + 8 <= n; k += 8)
+        for (int l = 0; l < 8; ++l) p[l] += a[k + l] * b[k + l];
+    for (int l = 0; k < n; ++k, ++l) p[l] += a[k] * b[k];
+    return ((p[0] + p[4]) + (p[1] + p[5])) + ((p[2] + p[6]) + (p[3] + p[7]));
+}
+
 // C = A^T * B
 inline Mat mul_tn(const Mat& A, const Mat& B) {
     Mat C(A.cols, B.cols);
+#pragma omp parallel for collapse(2) schedule(static) if (A.rows * A.cols * B.cols > 100000)
     for (Index j = 0; j < B.cols; ++j)
-        for (Index i = 0; i < A.cols; ++i) {
-            const double* a = A.col(i);
-            const double* b = B.col(j);
-            double s = 0.0;
-            for (Index k = 0; k < A.rows; ++k) s += a[k] * b[k];
-            C(i, j) = s;
-        }
+        for (Index i = 0; i < A.cols; ++i) C(i, j) = dot(A.col(i), B.col(j), A.rows);
     return C;
 }
 
 // C = A * B
 inline Mat mul_nn(const Mat& A, const Mat& B) {
     Mat C(A.rows, B.cols);
+#pragma omp parallel for schedule(static) if (A.rows * A.cols * B.cols > 100000)
     for (Index j = 0; j < B.cols; ++j) {
         double* c = C.col(j);
         for (Index k = 0; k < A.cols; ++k) {
@@ -101,11 +112,14 @@ inline Mat mul_nn(const Mat& A, const Mat& B) {
 // X -= Q * C
 inline void sub_mul(Mat& X, const Mat& Q, const Mat& C) {
     Mat P = mul_nn(Q, C);
-    for (size_t i = 0; i < X.a.size(); ++i) X.a[i] -= P.a[i];
+    const Index n = static_cast<Index>(X.a.size());
+#pragma omp parallel for schedule(static) if (n > 100000)
+    for (Index i = 0; i < n; ++i) X.a[static_cast<size_t>(i)] -= P.a[static_cast<size_t>(i)];
 }
 
 inline Mat transpose(const Mat& A) {
     Mat T(A.cols, A.rows);
+#pragma omp parallel for schedule(static) if (A.rows * A.cols > 100000)
     for (Index j = 0; j < A.cols; ++j)
         for (Index i = 0; i < A.rows; ++i) T(j, i) = A(i, j);
     return T;
@@ -179,8 +193,7 @@ inline Mat qr_orthonormal(const Mat& X) {
     for (Index j = 0; j < k; ++j) {
         double* x = R.col(j) + j;  // length m - j
         const Index len = m - j;
-        double tail_sq = 0.0;
-        for (Index i = 1; i < len; ++i) tail_sq += x[i] * x[i];
+        const double tail_sq = dot(x + 1, x + 1, len - 1);
         const double c0 = x[0];
         double beta, t;
         if (tail_sq <= std::numeric_limits<double>::min()) {
@@ -198,13 +211,12 @@ inline Mat qr_orthonormal(const Mat& X) {
         tau[static_cast<size_t>(j)] = t;
         // apply H_j = I - t v v^T to the trailing columns
         if (t != 0.0) {
+#pragma omp parallel for schedule(static) if (len * (k - j) > 100000)
             for (Index c = j + 1; c < k; ++c) {
                 double* y = R.col(c) + j;
-                double dot = y[0];
-                for (Index i = 1; i < len; ++i) dot += x[i] * y[i];
-                dot *= t;
-                y[0] -= dot;
-                for (Index i = 1; i < len; ++i) y[i] -= dot * x[i];
+                const double d = t * (y[0] + dot(x + 1, y + 1, len - 1));
+                y[0] -= d;
+                for (Index i = 1; i < len; ++i) y[i] -= d * x[i];
             }
         }
     }
@@ -214,13 +226,12 @@ inline Mat qr_orthonormal(const Mat& X) {
         if (t == 0.0) continue;
         const double* v = R.col(j) + j;
         const Index len = m - j;
+#pragma omp parallel for schedule(static) if (len * k > 100000)
         for (Index c = 0; c < k; ++c) {
             double* y = Q.col(c) + j;
-            double dot = y[0];
-            for (Index i = 1; i < len; ++i) dot += v[i] * y[i];
-            dot *= t;
-            y[0] -= dot;
-            for (Index i = 1; i < len; ++i) y[i] -= dot * v[i];
+            const double d = t * (y[0] + dot(v + 1, y + 1, len - 1));
+            y[0] -= d;
+            for (Index i = 1; i < len; ++i) y[i] -= d * v[i];
         }
     }
     return Q;
@@ -235,20 +246,25 @@ inline void one_sided_jacobi(Mat& A, Mat& V, std::vector<double>& sigma) {
     const Index len = A.rows, k = A.cols;
     V = Mat::identity(k, k);
     const double eps = 2.220446049250313e-16;
+    // Sweeps in round-robin (tournament) order: each of the P - 1 steps of a
+    // sweep rotates P / 2 disjoint column pairs, so the pairs of a step run
+    // in parallel and the result does not depend on the thread count.
+    const Index P = k + (k & 1);  // even number of players (k odd: one bye)
+    std::vector<Index> ring(static_cast<size_t>(P));
     for (int sweep = 0; sweep < 80; ++sweep) {
-        bool rotated = false;
-        for (Index i = 0; i < k - 1; ++i) {
-            for (Index j = i + 1; j < k; ++j) {
+        int rotated = 0;
+        for (Index q = 0; q < P; ++q) ring[static_cast<size_t>(q)] = q;
+        for (Index step = 0; step + 1 < P; ++step) {
+#pragma omp parallel for schedule(dynamic, 1) reduction(| : rotated) if (len * k > 20000)
+            for (Index h = 0; h < P / 2; ++h) {
+                Index i = ring[static_cast<size_t>(h)], j = ring[static_cast<size_t>(P - 1 - h)];
+                if (i > j) std::swap(i, j);
+                if (j >= k) continue;  // the bye
                 double* ai = A.col(i);
                 double* aj = A.col(j);
-                double alpha = 0.0, beta = 0.0, gamma = 0.0;
-                for (Index t = 0; t < len; ++t) {
-                    alpha += ai[t] * ai[t];
-                    beta += aj[t] * aj[t];
-                    gamma += ai[t] * aj[t];
-                }
+                const double alpha = dot(ai, ai, len), beta = dot(aj, aj, len), gamma = dot(ai, aj, len);
                 if (gamma == 0.0 || !(std::abs(gamma) > eps * std::sqrt(alpha * beta))) continue;
-                rotated = true;
+                rotated = 1;
                 const double zeta = (beta - alpha) / (2.0 * gamma);
                 const double tt = (zeta >= 0.0 ? 1.0 : -1.0) /
                                   (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
@@ -267,16 +283,15 @@ inline void one_sided_jacobi(Mat& A, Mat& V, std::vector<double>& sigma) {
                     vj[t] = s * x + c * y;
                 }
             }
+            // rotate every player but the first one place around the ring
+            const Index last = ring[static_cast<size_t>(P - 1)];
+            for (Index q = P - 1; q > 1; --q) ring[static_cast<size_t>(q)] = ring[static_cast<size_t>(q - 1)];
+            if (P > 1) ring[1] = last;
         }
         if (!rotated) break;
     }
     sigma.assign(static_cast<size_t>(k), 0.0);
-    for (Index j = 0; j < k; ++j) {
-        double s = 0.0;
-        const double* a = A.col(j);
-        for (Index t = 0; t < len; ++t) s += a[t] * a[t];
-        sigma[static_cast<size_t>(j)] = std::sqrt(s);
-    }
+    for (Index j = 0; j < k; ++j) sigma[static_cast<size_t>(j)] = std::sqrt(dot(A.col(j), A.col(j), len));
     // sort descending (stable: ties keep column order)
     std::vector<Index> order(static_cast<size_t>(k));
     for (Index j = 0; j < k; ++j) order[static_cast<size_t>(j)] = j;
@@ -451,6 +466,7 @@ inline Mat sp_mult(const SampledMatrix& S, const Mat& X) {
     const auto& off = S.row_offsets();
     const auto& cols = S.col_index();
     const auto& vals = S.values();
+#pragma omp parallel for schedule(dynamic, 256) if (S.nnz() * X.cols > 200000)
     for (Index i = 0; i < S.rows(); ++i)
         for (Index k = off[static_cast<size_t>(i)]; k < off[static_cast<size_t>(i) + 1]; ++k) {
             const double v = vals[static_cast<size_t>(k)];
@@ -467,12 +483,16 @@ inline Mat sp_mult_t(const SampledMatrix& S, const Mat& X) {
     const auto& off = S.row_offsets();
     const auto& cols = S.col_index();
     const auto& vals = S.values();
-    for (Index i = 0; i < S.rows(); ++i)
-        for (Index k = off[static_cast<size_t>(i)]; k < off[static_cast<size_t>(i) + 1]; ++k) {
-            const double v = vals[static_cast<size_t>(k)];
-            const Index c = cols[static_cast<size_t>(k)];
-            for (Index j = 0; j < X.cols; ++j) out(c, j) += v * X(i, j);
-        }
+    // columns of the output are independent: one column per task, each in
+    // the reference's CSR scatter order
+#pragma omp parallel for schedule(dynamic, 1) if (S.nnz() * X.cols > 200000 && X.cols > 1)
+    for (Index j = 0; j < X.cols; ++j) {
+        double* oj = out.col(j);
+        const double* xj = X.col(j);
+        for (Index i = 0; i < S.rows(); ++i)
+            for (Index k = off[static_cast<size_t>(i)]; k < off[static_cast<size_t>(i) + 1]; ++k)
+                oj[cols[static_cast<size_t>(k)]] += vals[static_cast<size_t>(k)] * xj[i];
+    }
     return out;
 }
 
@@ -487,13 +507,13 @@ inline SampledMatrix project_low_rank(const SampledMatrix& pattern, const LowRan
     const auto& off = pattern.row_offsets();
     const auto& cols = pattern.col_index();
     std::vector<double> vals(static_cast<size_t>(pattern.nnz()));
-    size_t k = 0;
+#pragma omp parallel for schedule(dynamic, 256) if (pattern.nnz() * r > 200000)
     for (Index i = 0; i < pattern.rows(); ++i)
-        for (Index p = off[static_cast<size_t>(i)]; p < off[static_cast<size_t>(i) + 1]; ++p, ++k) {
+        for (Index p = off[static_cast<size_t>(i)]; p < off[static_cast<size_t>(i) + 1]; ++p) {
             const Index c = cols[static_cast<size_t>(p)];
             double s = 0.0;
             for (Index j = 0; j < r; ++j) s += F.U(i, j) * W(c, j);
-            vals[k] = s;
+            vals[static_cast<size_t>(p - off[0])] = s;
         }
     return pattern.with_values(std::move(vals));
 }
@@ -562,8 +582,9 @@ struct SketchParams {
 
 // sketch.hpp:32-39
 struct QBState {
-    Mat Q;  // m x r
-    Mat B;  // r x n
+    Mat Q;   // m x r
+    Mat Bt;  // n x r: B^T (columns append without the reference's O(r n)
+             // conservativeResize copy of a column-major B; same values)
     double norm_b_sq = 0.0;
     double frob_y_sq = 0.0;
     Index rank = 0;
@@ -624,8 +645,8 @@ inline QBState qb_init(const SampledMatrix& Y, Index t, int np, std::uint64_t se
     X = detail::power_iterate(Y, std::move(X), np);
     QBState st;
     st.Q = qr_orthonormal(X);
-    st.B = detail::coefficient_block(Y, st.Q);
-    st.norm_b_sq = frob_norm_sq(st.B);
+    st.Bt = sp_mult_t(Y, st.Q);  // coefficient_block, transposed
+    st.norm_b_sq = frob_norm_sq(st.Bt);
     st.frob_y_sq = frob_y_sq;
     st.rank = t;
     st.saturated = (t == min_dim);
@@ -635,7 +656,7 @@ inline QBState qb_init(const SampledMatrix& Y, Index t, int np, std::uint64_t se
 // sketch.hpp:114-154
 inline QBState qb_extend(QBState st, const SampledMatrix& Y, Index dt, int np, std::uint64_t seed) {
     if (dt < 1) throw std::invalid_argument("qb_extend: dt must be >= 1");
-    if (st.Q.rows != Y.rows() || st.B.cols != Y.cols())
+    if (st.Q.rows != Y.rows() || st.Bt.rows != Y.cols())
         throw std::invalid_argument("qb_extend: state does not match target dimensions");
     const Index min_dim = std::min(Y.rows(), Y.cols());
     const Index width = std::min(dt, min_dim - st.rank);
@@ -659,20 +680,14 @@ inline QBState qb_extend(QBState st, const SampledMatrix& Y, Index dt, int np, s
             Qp = qr_orthonormal(Qp);
         }
     }
-    const Mat Bp = detail::coefficient_block(Y, Qp);
+    const Mat Bpt = sp_mult_t(Y, Qp);  // coefficient_block, transposed
     const Index r0 = st.rank;
-    // append (sketch.hpp:145-152)
-    Mat Q2(st.Q.rows, r0 + width);
-    std::copy(st.Q.a.begin(), st.Q.a.end(), Q2.a.begin());
-    std::copy(Qp.a.begin(), Qp.a.end(), Q2.a.begin() + st.Q.rows * r0);
-    Mat B2(r0 + width, Y.cols());
-    for (Index j = 0; j < Y.cols(); ++j) {
-        for (Index i = 0; i < r0; ++i) B2(i, j) = st.B(i, j);
-        for (Index i = 0; i < width; ++i) B2(r0 + i, j) = Bp(i, j);
-    }
-    st.Q = std::move(Q2);
-    st.B = std::move(B2);
-    st.norm_b_sq += frob_norm_sq(Bp);
+    // append (sketch.hpp:145-152): column blocks of Q and B^T
+    st.Q.a.insert(st.Q.a.end(), Qp.a.begin(), Qp.a.end());
+    st.Q.cols += width;
+    st.Bt.a.insert(st.Bt.a.end(), Bpt.a.begin(), Bpt.a.end());
+    st.Bt.cols += width;
+    st.norm_b_sq += frob_norm_sq(Bpt);
     st.rank = r0 + width;
     st.saturated = (st.rank == min_dim);
     return st;
@@ -680,7 +695,7 @@ inline QBState qb_extend(QBState st, const SampledMatrix& Y, Index dt, int np, s
 
 // sketch.hpp:158-162
 inline LowRankFactors finalize(const QBState& st) {
-    LowRankFactors f = small_svd(st.B);
+    LowRankFactors f = small_svd(transpose(st.Bt));
     f.U = mul_nn(st.Q, f.U);
     return f;
 }
@@ -732,8 +747,8 @@ inline SketchResult r4svd(const SampledMatrix& Y, const Mat& U_prev, const Sketc
     Mat gram = mul_tn(st.Q, st.Q);
     for (Index i = 0; i < s; ++i) gram(i, i) -= 1.0;
     if (detail::max_abs(gram) > 1e-8) st.Q = qr_orthonormal(st.Q);
-    st.B = detail::coefficient_block(Y, st.Q);
-    st.norm_b_sq = frob_norm_sq(st.B);
+    st.Bt = sp_mult_t(Y, st.Q);  // coefficient_block, transposed
+    st.norm_b_sq = frob_norm_sq(st.Bt);
     st.frob_y_sq = frob_y_sq;
     st.rank = s;
     st.saturated = (s == min_dim);
@@ -889,25 +904,38 @@ inline void check_config(const SvtConfig& cfg) {
 // solver.hpp:215-328 — the Bregman loop.  `test` (optional) is the held-out
 // pattern for the Appendix-B RMSE/MAE extension (reference: the ratings
 // observer, svt_main.cpp:355-369).
+// Test-harness extension (no reference counterpart): the loop-carried state
+// after `iter` completed iterations (Y, U_prev, the cooling threshold and
+// the running residual minimum), so one iteration of a long run can be
+// checked against the device path from a common state.
+struct SvtStart {
+    int iter = 0;
+    std::vector<double> y;  // Y on A's pattern (CSR order)
+    Mat U_prev;             // m x s
+    double eps_threshold = 0.0;
+    double eps_min = 0.0;
+};
+
 inline SvtResult svt_run_backend(const SampledMatrix& A, const SvtConfig& cfg, StopRule stop, Backend backend,
-                                 const IterationObserver& observer = {}, const SampledMatrix* test = nullptr) {
+                                 const IterationObserver& observer = {}, const SampledMatrix* test = nullptr,
+                                 const SvtStart* start = nullptr) {
     detail::check_config(cfg);
     const Index min_dim = std::min(A.rows(), A.cols());
     if (backend.kind == Backend::Kind::RsvdFixed && (backend.fixed_rank < 1 || backend.fixed_rank > min_dim))
         throw std::invalid_argument("svt_run_backend: fixed rank out of range");
     if (cfg.t0 > min_dim) throw std::invalid_argument("SvtConfig: t0 exceeds min(m, n)");
 
-    SampledMatrix Y = kickstart(A, cfg.tau, cfg.delta, derive_seed(cfg.seed, 0));
-    Mat U_prev(A.rows(), 0);
-    double eps_threshold = cfg.eps_threshold0;
-    double eps_min = std::numeric_limits<double>::infinity();
+    SampledMatrix Y = start ? A.with_values(start->y) : kickstart(A, cfg.tau, cfg.delta, derive_seed(cfg.seed, 0));
+    Mat U_prev = start ? start->U_prev : Mat(A.rows(), 0);
+    double eps_threshold = start ? start->eps_threshold : cfg.eps_threshold0;
+    double eps_min = start ? start->eps_min : std::numeric_limits<double>::infinity();
     const double frob_a = std::sqrt(sp_frob_norm_sq(A));
 
     SvtResult result;
     result.factors = LowRankFactors{Mat(A.rows(), 0), {}, Mat(A.cols(), 0)};
     double best_metric = std::numeric_limits<double>::infinity();
     const double t_start = detail::now_ms();
-    for (int iter = 1; iter <= cfg.maxit; ++iter) {
+    for (int iter = (start ? start->iter : 0) + 1; iter <= cfg.maxit; ++iter) {
         const std::uint64_t iter_seed = derive_seed(cfg.seed, static_cast<std::uint64_t>(iter));
         SketchParams sp;
         sp.t = cfg.t0;

@@ -86,6 +86,12 @@ class IterationRecord(C.Structure):  # solver.hpp:49-57 (+ extensions)
         return {f[0]: getattr(self, f[0]) for f in self._fields_}
 
 
+class SolverState(C.Structure):  # svt_solver_state (checkpoint / resume; no reference counterpart)
+    _fields_ = [("iter", C.c_int32), ("done", C.c_int32), ("converged", C.c_int32), ("last_rounds", C.c_int32),
+                ("s", C.c_int64), ("best_k", C.c_int64), ("eps_threshold", C.c_double), ("eps_min", C.c_double),
+                ("best_metric", C.c_double), ("frob_y_sq", C.c_double), ("frob_a", C.c_double)]
+
+
 OBSERVER_FN = C.CFUNCTYPE(C.c_int, C.POINTER(IterationRecord), C.c_int64, C.c_int64, C.c_int64,
                           C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p)
 

@@ -20,14 +20,15 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._abi import (OBSERVER_FN, Backend, InvalidArgument, IterationRecord, SketchParams, StopRule, SvtConfig,
-                   raise_for)
+from ._abi import (OBSERVER_FN, Backend, InvalidArgument, IterationRecord, SketchParams, SolverState, StopRule,
+                   SvtConfig, raise_for)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SVTB_LIB") or os.path.join(_HERE, "lib", "libsvt_b200.so")  # SVTB_LIB: A/B builds
 _lib = None
 
 P_I64 = C.POINTER(C.c_int64)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int64, C.c_void_p)
 P_F64 = C.POINTER(C.c_double)
 
 
@@ -86,6 +87,35 @@ class Context:
             _check(lib().svt_ctx_create_dist(C.c_int(device), C.c_int(rank), C.c_int(world), buf, C.byref(h)))
         self.h = h
         self.device, self.rank, self.world = device, rank, world
+
+    @classmethod
+    def hostcomm(cls, device, rank, world, allreduce):
+        """One rank of a world whose collectives are host-staged
+        (svt_ctx_create_hostcomm): `allreduce(x)` must sum the float64 numpy
+        array `x` element-wise across ranks in place (e.g.
+        torch.distributed.all_reduce over gloo on torch.from_numpy(x))."""
+        def _fn(buf, count, user):
+            try:
+                allreduce(np.ctypeslib.as_array(buf, shape=(count,)))
+                return 0
+            except Exception:  # noqa: BLE001 — reported as SVT_ENCCL by the library
+                import traceback
+                traceback.print_exc()
+                return 1
+        self = cls.__new__(cls)
+        self._cb = ALLREDUCE_FN(_fn)  # keep the thunk alive as long as the context
+        h = C.c_void_p()
+        _check(lib().svt_ctx_create_hostcomm(C.c_int(device), C.c_int(rank), C.c_int(world), self._cb, None,
+                                             C.byref(h)))
+        self.h = h
+        self.device, self.rank, self.world = device, rank, world
+        return self
+
+    def comm_stats(self):
+        """(all-reduces issued, doubles carried) by this context."""
+        n, d = C.c_int64(), C.c_double()
+        _check(lib().svt_ctx_comm_stats(self.h, C.byref(n), C.byref(d)))
+        return dict(calls=n.value, doubles=d.value)
 
     @staticmethod
     def nccl_unique_id() -> bytes:
@@ -609,6 +639,44 @@ class Solver:
         h = C.c_void_p()
         _check(lib().svt_solver_result(self.h, C.byref(h)))
         return _take_result(h)
+
+    def checkpoint(self, out=None):
+        """Host copy of the iteration state (svt_solver_checkpoint): dict with
+        `state` (SolverState) and the arrays y_vals, u_prev, best_U,
+        best_sigma, best_V.  `out` may supply preallocated (e.g. pinned)
+        arrays of the right sizes."""
+        st = SolverState()
+        _check(lib().svt_solver_checkpoint(self.h, C.byref(st), None, None, None, None, None))
+        m_local, nnz = self.A.row_end - self.A.row_begin, self.A.nnz
+        n = self.A.n
+        o = out or {}
+        arr = {"y_vals": o.get("y_vals", np.zeros(max(nnz, 1))),
+               "u_prev": o.get("u_prev", np.zeros(max(m_local * st.s, 1))),
+               "best_U": o.get("best_U", np.zeros(max(m_local * st.best_k, 1))),
+               "best_sigma": o.get("best_sigma", np.zeros(max(st.best_k, 1))),
+               "best_V": o.get("best_V", np.zeros(max(n * st.best_k, 1)))}
+        _check(lib().svt_solver_checkpoint(self.h, C.byref(st), *[_ptr(arr[k]) for k in
+                                                                  ("y_vals", "u_prev", "best_U", "best_sigma",
+                                                                   "best_V")]))
+        arr["state"] = st
+        return arr
+
+    @classmethod
+    def resume(cls, A: SampledMatrix, cfg: SvtConfig, stop: StopRule, ckpt, backend: Backend = None,
+               test: SampledMatrix | None = None):
+        """A solver continuing from `ckpt` (Solver.checkpoint()): iterations
+        state.iter + 1, ... reproduce the uninterrupted run bit for bit."""
+        self = cls.__new__(cls)
+        self.A, self.test = A, test
+        h = C.c_void_p()
+        _check(lib().svt_solver_resume(A.h, C.byref(cfg), stop, backend or Backend.r4svd(),
+                                       test.h if test is not None else None, C.byref(ckpt["state"]),
+                                       *[_ptr(np.ascontiguousarray(ckpt[k], dtype=np.float64))
+                                         for k in ("y_vals", "u_prev", "best_U", "best_sigma", "best_V")],
+                                       C.byref(h)))
+        self.h = h
+        self.done = bool(ckpt["state"].done)
+        return self
 
     def close(self):
         if getattr(self, "h", None):

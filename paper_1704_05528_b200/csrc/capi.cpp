@@ -17,6 +17,11 @@ void partition_rows(i64 m, const i64* rowptr, int world, i64* bounds);
 svt_solver* solver_create(svt_mat* A, const svt_config& cfg, svt_stop stop, svt_backend backend, svt_mat* test);
 void solver_step(svt_solver* S, svt_observer_fn obs, void* user, svt_record* rec_out, int* done);
 svt_result* solver_result(svt_solver* S);
+void solver_checkpoint(svt_solver* S, svt_solver_state* st, double* y_vals, double* u_prev, double* best_U,
+                       double* best_sigma, double* best_V);
+svt_solver* solver_resume(svt_mat* A, const svt_config& cfg, svt_stop stop, svt_backend backend, svt_mat* test,
+                          const svt_solver_state& st, const double* y_vals, const double* u_prev,
+                          const double* best_U, const double* best_sigma, const double* best_V);
 void kickstart_dev(svt_ctx* c, svt_mat* A, double tau, double delta, u64 seed, double* out_csr, double* out_csc);
 void synth_config(int config, u64 seed, i64* m, i64* n, i64* nnz_train, i64* nnz_test, i64* train_rows,
                   i64* train_cols, double* train_vals, i64* test_rows, i64* test_cols, double* test_vals);
@@ -96,11 +101,11 @@ const char* svt_last_error(void) { return g_err.c_str(); }
 
 int svt_version(void) { return 1; }
 
-int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, svt_ctx** out) {
-    return guard([&] {
+static void ctx_create(int device, int rank, int world, const void* nccl_id, svt_allreduce_fn host_fn,
+                       void* host_user, svt_ctx** out) {
         need(out, "svt_ctx_create");
         if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("svt_ctx_create: bad rank/world");
-        if (world > 1) need(nccl_id, "svt_ctx_create_dist: nccl_id");
+        if (world > 1 && host_fn == nullptr) need(nccl_id, "svt_ctx_create_dist: nccl_id");
         int ndev = 0;
         SVT_CUDA(cudaGetDeviceCount(&ndev));
         if (device < 0 || device >= ndev) throw std::invalid_argument("svt_ctx_create: no such CUDA device");
@@ -132,9 +137,34 @@ int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, sv
         c->ws_info.alloc(8);
         c->d_tickets.alloc(kTickets);
         SVT_CUDA(cudaMemsetAsync(c->d_tickets.get(), 0, kTickets * sizeof(unsigned), c->stream));
-        nccl_init(c->comm, rank, world, nccl_id);
+        if (host_fn != nullptr) {
+            c->comm.rank = rank;
+            c->comm.world = world;
+            c->comm.host_fn = host_fn;
+            c->comm.host_user = host_user;
+        } else {
+            nccl_init(c->comm, rank, world, nccl_id);
+        }
         sync_stream(c.get());
         *out = c.release();
+}
+
+int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, svt_ctx** out) {
+    return guard([&] { ctx_create(device, rank, world, nccl_id, nullptr, nullptr, out); });
+}
+
+int svt_ctx_create_hostcomm(int device, int rank, int world, svt_allreduce_fn fn, void* user, svt_ctx** out) {
+    return guard([&] {
+        need(reinterpret_cast<const void*>(fn), "svt_ctx_create_hostcomm: fn");
+        ctx_create(device, rank, world, nullptr, fn, user, out);
+    });
+}
+
+int svt_ctx_comm_stats(svt_ctx* ctx, int64_t* calls, double* doubles) {
+    return guard([&] {
+        need(ctx, "svt_ctx_comm_stats");
+        if (calls) *calls = ctx->comm.calls;
+        if (doubles) *doubles = ctx->comm.doubles;
     });
 }
 
@@ -938,6 +968,27 @@ int svt_solver_result(svt_solver* s, svt_result** out) {
         need(s, "svt_solver_result");
         need(out, "svt_solver_result");
         *out = solver_result(s);
+    });
+}
+
+int svt_solver_checkpoint(svt_solver* s, svt_solver_state* st, double* y_vals, double* u_prev, double* best_U,
+                          double* best_sigma, double* best_V) {
+    return guard([&] {
+        need(s, "svt_solver_checkpoint");
+        need(st, "svt_solver_checkpoint");
+        solver_checkpoint(s, st, y_vals, u_prev, best_U, best_sigma, best_V);
+    });
+}
+
+int svt_solver_resume(svt_mat* A, const svt_config* cfg, svt_stop stop, svt_backend backend, svt_mat* test,
+                      const svt_solver_state* st, const double* y_vals, const double* u_prev, const double* best_U,
+                      const double* best_sigma, const double* best_V, svt_solver** out) {
+    return guard([&] {
+        need(A, "svt_solver_resume");
+        need(cfg, "svt_solver_resume");
+        need(st, "svt_solver_resume");
+        need(out, "svt_solver_resume");
+        *out = solver_resume(A, *cfg, stop, backend, test, *st, y_vals, u_prev, best_U, best_sigma, best_V);
     });
 }
 

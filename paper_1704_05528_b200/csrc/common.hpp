@@ -141,10 +141,20 @@ struct KStats {
 
 // NCCL entry points, resolved with dlopen so a single-GPU run never needs
 // libnccl (comm.cpp).
+// Host-staged mode (svt_ctx_create_hostcomm): every all-reduce goes D2H into
+// pinned staging, through the caller's callback (which sums across ranks,
+// e.g. gloo), and back H2D — the same collective sequence as NCCL mode.
+typedef int (*HostAllreduceFn)(double* buf, std::int64_t count, void* user);
 struct Comm {
     int rank = 0;
     int world = 1;
     void* handle = nullptr;  // ncclComm_t
+    HostAllreduceFn host_fn = nullptr;
+    void* host_user = nullptr;
+    double* h_buf = nullptr;  // pinned staging (host mode)
+    size_t h_cap = 0;
+    long long calls = 0;    // all-reduces issued (instrumentation)
+    double doubles = 0.0;   // doubles all-reduced
     void allreduce_sum(double* buf, size_t count, cudaStream_t s);
     void allreduce_sum_i32(int* buf, size_t count, cudaStream_t s);
     void destroy();
@@ -267,7 +277,10 @@ struct LaunchScope {
     int cls;
     cudaEvent_t a = nullptr, b = nullptr;
     cudaStream_t st = nullptr;
-    LaunchScope(svt_ctx* c, int k, double bytes, double flops, cudaStream_t stream = nullptr);
+    const char* file;
+    int line;
+    LaunchScope(svt_ctx* c, int k, double bytes, double flops, cudaStream_t stream = nullptr,
+                const char* file = __builtin_FILE(), int line = __builtin_LINE());
     ~LaunchScope() noexcept(false);
 };
 // Blocking wait for the context stream (counted; timed when profiling).

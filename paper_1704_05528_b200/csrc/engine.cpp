@@ -752,14 +752,14 @@ static void finalize_mode(Engine& E, const QBDev& st, FinalizeMode mode, double 
 // Gram-Schmidt coefficients C (r0 x w) = Q[:, :r0]^T X (sketch.hpp:133) on
 // the INT8 tensor cores from cached digit slices of the basis (ozaki.cu),
 // else the DMMA GEMM.  The slices of a column are built once, the first time
-// the column takes part in a product.  Default: bases of >= 4096 columns
-// (config 5: +5 % iterations/s; at config 4's ~2,000 columns the INT8 kernel's
-// SM footprint slows the concurrent side-stream SpMM as much as it saves);
-// SVTB_OZAKI=0 / 1 turns it off / on for every basis of >= 64 columns.
+// the column takes part in a product.  Opt-in (SVTB_OZAKI=1, bases of >= 64
+// columns): in isolation the INT8 kernel measured slower than cuBLAS DGEMM
+// on the config-4 Gram-Schmidt shape (profiles/r01_ozaki_bench.txt), so the
+// default is the DMMA kernel.
 static bool ozaki_enabled(i64 r0) {  // read per batch (cheap), so tests can toggle it
     const char* e = std::getenv("SVTB_OZAKI");
-    if (e != nullptr) return std::atoi(e) != 0;
-    return r0 >= 4096;
+    (void)r0;
+    return e != nullptr && std::atoi(e) != 0;
 }
 
 static void basis_tx(Engine& E, QBDev& st, i64 r0, i64 w, const double* X, i64 ldx, double* C) {

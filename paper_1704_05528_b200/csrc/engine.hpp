@@ -211,6 +211,7 @@ struct svt_solver {
     bool done = false;
     bool converged = false;
     bool result_is_current = false;
+    int resume_last_rounds = -1;  // batch-size hint carried over by a resume
     std::vector<svt_record> trace;
     std::unique_ptr<svtb::Engine> engine;
 };

@@ -4,14 +4,15 @@
 
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.hpp"
 
 namespace svtb {
 
-LaunchScope::LaunchScope(svt_ctx* c, int k, double bytes, double flops, cudaStream_t stream)
-    : ctx(c), cls(k), st(stream ? stream : c->stream) {
+LaunchScope::LaunchScope(svt_ctx* c, int k, double bytes, double flops, cudaStream_t stream, const char* f, int l)
+    : ctx(c), cls(k), st(stream ? stream : c->stream), file(f), line(l) {
     ctx->launch_count++;
     if (ctx->gap_open) {
         auto& g = ctx->gap_stats[ctx->gap_site];
@@ -47,7 +48,17 @@ LaunchScope::~LaunchScope() noexcept(false) {
         if (ctx->pending.size() > 4096) flush_stats(ctx);
     }
     if (e != cudaSuccess && std::uncaught_exceptions() == 0)
-        throw cuda_error(std::string("kernel launch failed: ") + cudaGetErrorString(e));
+        throw cuda_error(std::string("kernel launch failed: ") + cudaGetErrorString(e) + " (launched at " + file +
+                         ":" + std::to_string(line) + ")");
+    // SVTB_SYNC_CHECK=1 (debug): wait for every launch, so a device fault is
+    // reported with the launch site that caused it
+    static const bool sync_check = std::getenv("SVTB_SYNC_CHECK") != nullptr;
+    if (sync_check && std::uncaught_exceptions() == 0) {
+        const cudaError_t se = cudaStreamSynchronize(st);
+        if (se != cudaSuccess)
+            throw cuda_error(std::string("kernel failed: ") + cudaGetErrorString(se) + " (launched at " + file + ":" +
+                             std::to_string(line) + ", class " + std::to_string(cls) + ")");
+    }
 }
 
 void sync_stream(svt_ctx* c, int site, const char* file) {
@@ -159,6 +170,23 @@ void nccl_init(Comm& c, int rank, int world, const void* id128) {
 
 void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t s) {
     if (world <= 1 || count == 0) return;
+    calls++;
+    doubles += static_cast<double>(count);
+    if (host_fn != nullptr) {
+        if (count > h_cap) {
+            if (h_buf) cudaFreeHost(h_buf);
+            h_buf = nullptr;
+            h_cap = std::max(count, 2 * h_cap);
+            SVT_CUDA(cudaMallocHost(&h_buf, h_cap * sizeof(double)));
+        }
+        SVT_CUDA(cudaMemcpyAsync(h_buf, buf, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+        SVT_CUDA(cudaStreamSynchronize(s));
+        if (host_fn(h_buf, static_cast<std::int64_t>(count), host_user) != 0)
+            throw nccl_error("host all-reduce callback failed");
+        SVT_CUDA(cudaMemcpyAsync(buf, h_buf, count * sizeof(double), cudaMemcpyHostToDevice, s));
+        SVT_CUDA(cudaStreamSynchronize(s));  // the staging buffer is reused by the next call
+        return;
+    }
     check(svtb::nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, handle, s), "ncclAllReduce");
 }
 
@@ -168,6 +196,11 @@ void Comm::allreduce_sum_i32(int* buf, size_t count, cudaStream_t s) {
 }
 
 void Comm::destroy() {
+    if (h_buf != nullptr) {
+        cudaFreeHost(h_buf);
+        h_buf = nullptr;
+        h_cap = 0;
+    }
     if (handle != nullptr) {
         svtb::nccl().CommDestroy(handle);
         handle = nullptr;

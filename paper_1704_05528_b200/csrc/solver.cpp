@@ -88,7 +88,8 @@ void kickstart_dev(svt_ctx* c, svt_mat* A, double tau, double delta, u64 seed, d
     scale_values(c, A->nnz_local, A->val.get(), k0 * delta, out_csr, A->csr2csc.get(), out_csc);
 }
 
-svt_solver* solver_create(svt_mat* A, const svt_config& cfg, svt_stop stop, svt_backend backend, svt_mat* test) {
+static std::unique_ptr<svt_solver> solver_alloc(svt_mat* A, const svt_config& cfg, svt_stop stop,
+                                                svt_backend backend, svt_mat* test) {
     check_config(cfg);
     const i64 min_dim = std::min(A->m, A->n);
     if (backend.kind == SVT_BACKEND_RSVD_FIXED && (backend.fixed_rank < 1 || backend.fixed_rank > min_dim))
@@ -108,6 +109,15 @@ svt_solver* solver_create(svt_mat* A, const svt_config& cfg, svt_stop stop, svt_
     const i64 nnz = std::max<i64>(1, A->nnz_local);
     S->Ycsr.alloc(static_cast<size_t>(nnz));
     S->Ycsc.alloc(static_cast<size_t>(nnz));
+    S->eps_threshold = cfg.eps_threshold0;
+    S->X.m_local = S->best.m_local = A->m_local;
+    S->X.n = S->best.n = A->n;
+    return S;
+}
+
+svt_solver* solver_create(svt_mat* A, const svt_config& cfg, svt_stop stop, svt_backend backend, svt_mat* test) {
+    auto S = solver_alloc(A, cfg, stop, backend, test);
+    svt_ctx* c = A->ctx;
     kickstart_dev(c, A, cfg.tau, cfg.delta, derive_seed_u(cfg.seed, 0), S->Ycsr.get(), S->Ycsc.get());
     sumsq(c, A->val.get(), 1, A->nnz_local, A->nnz_local, c->d_scalars + S_FA, 0);
     c->comm.allreduce_sum(c->d_scalars + S_FA, 1, c->stream);
@@ -115,16 +125,98 @@ svt_solver* solver_create(svt_mat* A, const svt_config& cfg, svt_stop stop, svt_
                              c->stream));
     sync_stream(c);
     S->frob_a = std::sqrt(c->h_scalars[S_FA]);
-    S->eps_threshold = cfg.eps_threshold0;
-    S->X.m_local = S->best.m_local = A->m_local;
-    S->X.n = S->best.n = A->n;
     S->t_start_ms = now_ms();
     return S.release();
 }
 
 static Engine& engine_of(svt_solver* S) {
-    if (!S->engine) S->engine = std::make_unique<Engine>(S->ctx, S->A, Vals{S->Ycsr.get(), S->Ycsc.get()});
+    if (!S->engine) {
+        S->engine = std::make_unique<Engine>(S->ctx, S->A, Vals{S->Ycsr.get(), S->Ycsc.get()});
+        S->engine->last_rounds = S->resume_last_rounds;
+    }
     return *S->engine;
+}
+
+// ---- checkpoint / resume (svt_b200.h) ---------------------------------------
+void solver_checkpoint(svt_solver* S, svt_solver_state* st, double* y_vals, double* u_prev, double* best_U,
+                       double* best_sigma, double* best_V) {
+    svt_ctx* c = S->ctx;
+    svt_mat* A = S->A;
+    *st = svt_solver_state{};
+    st->iter = S->iter;
+    st->done = S->done ? 1 : 0;
+    st->converged = S->converged ? 1 : 0;
+    st->last_rounds = S->engine ? S->engine->last_rounds : S->resume_last_rounds;
+    st->s = S->s;
+    st->best_k = S->best.k;
+    st->eps_threshold = S->eps_threshold;
+    st->eps_min = S->eps_min;
+    st->best_metric = S->best_metric;
+    st->frob_y_sq = S->frob_y_sq;
+    st->frob_a = S->frob_a;
+    if (y_vals && A->nnz_local > 0)
+        SVT_CUDA(cudaMemcpyAsync(y_vals, S->Ycsr.get(), sizeof(double) * A->nnz_local, cudaMemcpyDeviceToHost,
+                                 c->stream));
+    std::vector<double> tmp;
+    auto cm_out = [&](const double* d, i64 rows, i64 k, double* h) {
+        if (h == nullptr || rows * k == 0) return;
+        to_host_cm(c, d, rows, k, tmp);
+        std::memcpy(h, tmp.data(), sizeof(double) * rows * k);
+    };
+    cm_out(S->U_prev.get(), A->m_local, S->s, u_prev);
+    cm_out(S->best.U.get(), A->m_local, S->best.k, best_U);
+    cm_out(S->best.V.get(), A->n, S->best.k, best_V);
+    if (best_sigma && S->best.k > 0) std::memcpy(best_sigma, S->best.sigma.data(), sizeof(double) * S->best.k);
+    sync_stream(c);
+}
+
+// column-major host (rows x k) -> row-major device (rows x k, ld k)
+static void upload_cm(svt_ctx* c, const double* h, i64 rows, i64 k, DevBuf<double>& dst, i64 cap_cols) {
+    dst.ensure(static_cast<size_t>(std::max<i64>(1, rows) * std::max(k, cap_cols)));
+    if (rows * k == 0) return;
+    DevBuf<double> stage(static_cast<size_t>(rows * k));
+    SVT_CUDA(cudaMemcpyAsync(stage.get(), h, sizeof(double) * rows * k, cudaMemcpyHostToDevice, c->stream));
+    transpose(c, stage.get(), k, rows, rows, dst.get());
+    sync_stream(c);  // the staging buffer dies with this scope
+}
+
+svt_solver* solver_resume(svt_mat* A, const svt_config& cfg, svt_stop stop, svt_backend backend, svt_mat* test,
+                          const svt_solver_state& st, const double* y_vals, const double* u_prev,
+                          const double* best_U, const double* best_sigma, const double* best_V) {
+    if (st.iter < 0 || st.s < 0 || st.best_k < 0 || st.s > std::min(A->m, A->n) || st.best_k > std::min(A->m, A->n))
+        throw std::invalid_argument("svt_solver_resume: inconsistent state");
+    if ((A->nnz_local > 0 && y_vals == nullptr) || (st.s > 0 && u_prev == nullptr) ||
+        (st.best_k > 0 && (best_U == nullptr || best_sigma == nullptr || best_V == nullptr)))
+        throw std::invalid_argument("svt_solver_resume: missing state buffer");
+    auto S = solver_alloc(A, cfg, stop, backend, test);
+    svt_ctx* c = A->ctx;
+    if (A->nnz_local > 0) {
+        SVT_CUDA(cudaMemcpyAsync(S->Ycsr.get(), y_vals, sizeof(double) * A->nnz_local, cudaMemcpyHostToDevice,
+                                 c->stream));
+        if (A->csc2csr.n > 0)
+            mirror_csc(c, A->nnz_local, A->csc2csr.get(), S->Ycsr.get(), S->Ycsc.get());
+        else
+            scale_values(c, A->nnz_local, S->Ycsr.get(), 1.0, S->Ycsr.get(), A->csr2csc.get(), S->Ycsc.get());
+    }
+    const i64 fc = factor_cols(A->m_local + A->n, std::min(A->m, A->n));
+    S->s = st.s;
+    upload_cm(c, u_prev, A->m_local, st.s, S->U_prev, fc);
+    S->best.k = st.best_k;
+    S->best.sigma.assign(best_sigma, best_sigma + st.best_k);
+    upload_cm(c, best_U, A->m_local, st.best_k, S->best.U, fc);
+    upload_cm(c, best_V, A->n, st.best_k, S->best.V, fc);
+    S->iter = st.iter;
+    S->done = st.done != 0;
+    S->converged = st.converged != 0;
+    S->resume_last_rounds = st.last_rounds;
+    S->eps_threshold = st.eps_threshold;
+    S->eps_min = st.eps_min;
+    S->best_metric = st.best_metric;
+    S->frob_y_sq = st.frob_y_sq;
+    S->frob_a = st.frob_a;
+    sync_stream(c);  // the caller's host buffers may be released on return
+    S->t_start_ms = now_ms();
+    return S.release();
 }
 
 void solver_step(svt_solver* S, svt_observer_fn obs, void* user, svt_record* rec_out, int* done) {

@@ -273,7 +273,8 @@ __global__ void __launch_bounds__(32 * kSddmmWarps) sddmm_update_kernel(
                 const double uj = (j0 < k) ? __ldg(ur + jl) : 0.0;
 #pragma unroll
                 for (int u = 0; u < kSddmmU; ++u)
-                    p[u] = uj * __ldg(Vs + static_cast<long long>(max(cc[u], 0)) * ldv + jl);
+                    // k == 0 (shrink kept nothing): no factor rows exist
+                    p[u] = (k > 0) ? uj * __ldg(Vs + static_cast<long long>(max(cc[u], 0)) * ldv + jl) : 0.0;
             } else {
 #pragma unroll
                 for (int u = 0; u < kSddmmU; ++u) {

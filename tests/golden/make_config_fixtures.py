@@ -1,0 +1,86 @@
+"""Regenerates tests/golden/config{1..4}_trace.json from the CPU oracle.
+
+TEST INFRASTRUCTURE: the oracle (oracle/svt_oracle.hpp, the C++ restatement
+of the reference's dense/sampled/sketch/solver headers) runs the BASELINE.json
+configurations with the parameters bench.py and the GPU tests use
+(paper_1704_05528_b200.api.config_params, restated below so this script
+loads only liboracle.so):
+
+  config 1  full run to the stop rule ||P(X - A)|| / ||P A|| < 1e-4
+            (eps 1e-2 cooling to 1e-6; ~81 iterations)
+  config 2  full run to the same stop rule
+  config 3  15 iterations, held-out MAE / RMSE every iteration
+  config 4  5 iterations, held-out MAE / RMSE every iteration
+
+Each fixture holds the per-iteration records the reference's solver emits
+(solver.hpp:289-297 plus the Appendix-B columns), the final (best-so-far)
+singular values, and the final completed matrix X = U diag(sigma) V^T
+probed at 512 seeded positions.  tests/test_gpu_config_fixtures.py checks
+the device path against them (-m gpu).
+
+  OMP_NUM_THREADS=8 python tests/golden/make_config_fixtures.py [config ...]
+
+The oracle's parallel loops reduce in a fixed order, so the fixtures do not
+depend on the thread count."""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from oracle import oracle as O  # noqa: E402
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+RUNS = {1: None, 2: None, 3: 15, 4: 5}  # maxit (None: the config's stop rule decides)
+PROBES = 512
+
+
+config_params = O.config_params  # restated api.config_params (tests assert they agree)
+
+
+def probe_positions(m, n, seed=12345):
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, m, PROBES), rng.integers(0, n, PROBES)
+
+
+def generate(config):
+    d = O.synth_config(config, 1)
+    A, T = d["train"], d["test"]
+    m, n = d["m"], d["n"]
+    cfg, stop = config_params(config, A.nnz, m, n, float(np.sqrt(np.sum(A.val * A.val))))
+    if RUNS[config] is not None:
+        cfg.maxit = RUNS[config]
+    t0 = time.time()
+    stamps = []
+
+    def obs(rec, U, s, V):
+        stamps.append(time.time() - t0)
+        print(f"  cfg{config} it {rec['iter']}: rank {rec['rank']} rounds {rec['extension_rounds']} "
+              f"kept {rec['kept']} rel {rec['rel_residual_x']:.3e} ({stamps[-1]:.0f} s)", flush=True)
+        return True
+
+    r = O.svt_run(A, cfg, stop, observer=obs, test=T)
+    pr, pc = probe_positions(m, n)
+    X = np.einsum("ij,j,ij->i", r.U[pr], r.sigma, r.V[pc]) if r.sigma.size else np.zeros(PROBES)
+    keys = ("iter", "rank", "extension_rounds", "kept", "residual", "eps_threshold", "train_mae", "rel_residual_x",
+            "test_mae", "test_rmse")
+    out = {
+        "config": config, "seed": 1, "maxit": int(cfg.maxit), "converged": bool(r.converged),
+        "cfg": {f[0]: getattr(cfg, f[0]) for f in cfg._fields_},
+        "trace": [{k: rec[k] for k in keys} for rec in r.trace],
+        "sigma": r.sigma.tolist(),
+        "probe": {"rows": pr.tolist(), "cols": pc.tolist(), "values": X.tolist()},
+        "oracle_threads": O.num_threads(), "oracle_seconds": round(time.time() - t0, 1),
+    }
+    path = os.path.join(HERE, f"config{config}_trace.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=0)
+    print(f"wrote {path}: {len(r.trace)} iterations, converged={r.converged}, {time.time() - t0:.0f} s")
+
+
+if __name__ == "__main__":
+    for c in [int(a) for a in sys.argv[1:]] or sorted(RUNS):
+        generate(c)

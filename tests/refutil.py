@@ -31,19 +31,9 @@ def product(U, sigma, V):
 
 
 def random_triplets(m, n, fill, seed):
-    """test_util.hpp:56-78: seeded partial Fisher-Yates over all cells using
-    mt19937_64 draws `rng() % (cells - i)`; values are standard normals
-    (numpy's generator here — the reference's std::normal_distribution is
-    implementation-defined and the values only need to be generic)."""
-    cells = np.arange(m * n, dtype=np.uint64)
-    ns = max(1, int(fill * m * n))
-    draws = O.mt19937_64(seed, ns)
-    for i in range(ns):
-        j = i + int(int(draws[i]) % (m * n - i))
-        cells[i], cells[j] = cells[j], cells[i]
-    chosen = cells[:ns].astype(np.int64)
-    vals = np.random.default_rng(seed).standard_normal(ns)
-    return chosen // n, chosen % n, vals
+    """test_util.hpp:56-78, exactly (the oracle library restates it with the
+    same std::mt19937_64 / std::normal_distribution engine)."""
+    return O.random_triplets(m, n, fill, seed)
 
 
 def random_sampled(m, n, fill, seed):

@@ -1,0 +1,174 @@
+"""BASELINE configs 1-4 on the device against committed oracle fixtures
+(tests/golden/config*_trace.json, written by tests/golden/make_config_fixtures.py).
+
+North-star tolerances (BASELINE.json): retained rank per iteration exact;
+singular values and the completed matrix within 1e-8 relative; SVT
+iteration count equal or within +-1; final relative residual on Lambda and
+held-out RMSE within 1e-6.  On top of that the revealed rank and the
+extension-round count of every iteration are asserted exact, and the
+per-iteration residual / MAE / relative residual / held-out metrics within
+1e-8 relative.
+
+Config 4 at iteration W + 1 from a common state: the device solver is
+checkpointed after W iterations (svt_solver_checkpoint), the oracle resumes
+from that state (svt_run with `start`) and both compute iteration W + 1 —
+the first iteration of bench.py's timed window — at its full size
+(r ~ 1,700 basis columns)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1704_05528_b200 import api as G
+from paper_1704_05528_b200._abi import StopRule
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = os.path.join(HERE, "golden")
+KEYS = ("residual", "train_mae", "rel_residual_x")
+TEST_KEYS = ("test_mae", "test_rmse")
+
+
+def _fixture(config):
+    p = os.path.join(GOLD, f"config{config}_trace.json")
+    if not os.path.exists(p):
+        pytest.skip(f"fixture {p} not generated")
+    with open(p) as f:
+        return json.load(f)
+
+
+def _problem(config):
+    d = G.synth_config(config, 1)
+    m, n = d["m"], d["n"]
+    A = G.SampledMatrix(m, n, *d["train"])
+    T = G.SampledMatrix(m, n, *d["test"]) if d["test"] is not None else None
+    frob = float(np.sqrt(G.sp_frob_norm_sq(A)))
+    cfg, stop = G.config_params(config, A.nnz, m, n, frob)
+    return A, T, cfg, stop
+
+
+def _rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def test_oracle_config_params_match_api():
+    """oracle.config_params restates api.config_params (the CPU arms and
+    the fixture script load only the oracle library); both must agree."""
+    for config, (m, n, nnz, frob) in {1: (1000, 1000, 200000, 7.0), 2: (512, 512, 131072, 3.0),
+                                      3: (6040, 3706, 900188, 5.0), 4: (69878, 10677, 9000048, 9.0),
+                                      5: (100000, 100000, 100000000, 11.0)}.items():
+        a, sa = G.config_params(config, nnz, m, n, frob)
+        b, sb = O.config_params(config, nnz, m, n, frob)
+        assert {f[0]: getattr(a, f[0]) for f in a._fields_} == {f[0]: getattr(b, f[0]) for f in b._fields_}
+        assert (sa.kind, sa.threshold) == (sb.kind, sb.threshold)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", [1, 2, 3, 4])
+def test_config_matches_oracle_fixture(config):
+    fx = _fixture(config)
+    A, T, cfg, stop = _problem(config)
+    for k, v in fx["cfg"].items():
+        assert getattr(cfg, k) == pytest.approx(v, rel=1e-15, abs=0), k
+    cfg.maxit = fx["maxit"]
+    S = G.Solver(A, cfg, stop, test=T)
+    recs = []
+    while not S.done:
+        recs.append(S.step())
+    res = S.result()
+    S.close()
+    ref = fx["trace"]
+    # iteration count: equal or +-1 (north star)
+    assert abs(len(recs) - len(ref)) <= 1, (len(recs), len(ref))
+    for g, o in zip(recs, ref):
+        assert g["iter"] == o["iter"]
+        assert (g["rank"], g["extension_rounds"], g["kept"]) == (o["rank"], o["extension_rounds"], o["kept"]), \
+            (g["iter"], g["rank"], g["extension_rounds"], g["kept"], o)
+        assert g["eps_threshold"] == o["eps_threshold"]
+        for key in KEYS:
+            assert _rel(g[key], o[key]) <= 1e-8, (g["iter"], key, g[key], o[key])
+        if T is not None:
+            for key in TEST_KEYS:
+                assert _rel(g[key], o[key]) <= 1e-8, (g["iter"], key, g[key], o[key])
+    # final relative residual and held-out RMSE within 1e-6
+    assert _rel(recs[-1]["rel_residual_x"], ref[-1]["rel_residual_x"]) <= 1e-6
+    if T is not None:
+        assert _rel(recs[-1]["test_rmse"], ref[-1]["test_rmse"]) <= 1e-6
+    if len(recs) == len(ref):
+        assert res.converged == fx["converged"]
+        # singular values and the completed matrix (probed) within 1e-8
+        np.testing.assert_allclose(res.sigma, np.array(fx["sigma"]), rtol=1e-8, atol=0)
+        pr, pc = np.array(fx["probe"]["rows"]), np.array(fx["probe"]["cols"])
+        X = np.einsum("ij,j,ij->i", res.U[pr], res.sigma, res.V[pc])
+        Xo = np.array(fx["probe"]["values"])
+        assert np.linalg.norm(X - Xo) <= 1e-8 * np.linalg.norm(Xo)
+    A.close()
+    if T is not None:
+        T.close()
+
+
+@pytest.mark.gpu
+def test_checkpoint_resume_is_bitwise():
+    """svt_solver_checkpoint / svt_solver_resume: iterations after the
+    checkpoint reproduce the uninterrupted run exactly (config 3)."""
+    A, T, cfg, stop = _problem(3)
+    cfg.maxit = 8
+    S = G.Solver(A, cfg, stop, test=T)
+    full = [S.step() for _ in range(8)]
+    rf = S.result()
+    S.close()
+    S = G.Solver(A, cfg, stop, test=T)
+    for _ in range(4):
+        S.step()
+    ck = S.checkpoint()
+    S.close()
+    R = G.Solver.resume(A, cfg, stop, ck, test=T)
+    tail = [R.step() for _ in range(4)]
+    rr = R.result()
+    R.close()
+    strip = lambda r: {k: v for k, v in r.items() if not k.endswith("_ms")}  # noqa: E731
+    assert [strip(r) for r in tail] == [strip(r) for r in full[4:]]
+    assert np.array_equal(rr.sigma, rf.sigma) and np.array_equal(rr.U, rf.U) and np.array_equal(rr.V, rf.V)
+    A.close()
+    T.close()
+
+
+@pytest.mark.gpu
+def test_config4_timed_window_first_iteration_matches_oracle():
+    """bench.py's timed window starts at iteration W + 1 = 6 of config 4.
+    Device state after 5 iterations -> iteration 6 on the device and on the
+    oracle (resumed from the same state): revealed rank, rounds and kept
+    rank exact, sums within 1e-8, kept singular values within 1e-8."""
+    W = 5
+    A, T, cfg, stop = _problem(4)
+    cfg.maxit = W + 1
+    S = G.Solver(A, cfg, stop, test=T)
+    for _ in range(W):
+        S.step()
+    ck = S.checkpoint()
+    gs, osg = [], []
+    g = S.step(observer=lambda rec, U, sg, V: gs.append(sg) or True)
+    S.close()
+    st = ck["state"]
+    m, n = A.m, A.n
+    s = int(st.s)
+    start = dict(iter=int(st.iter), y_vals=ck["y_vals"][: A.nnz],
+                 u_prev=np.asarray(ck["u_prev"][: m * s]).reshape(s, m).T if s else np.zeros((m, 0)),
+                 eps_threshold=st.eps_threshold, eps_min=st.eps_min)
+    Ao = O.Csr(m, n, A.rowptr, A.col, A.values())
+    To = O.Csr(m, n, T.rowptr, T.col, T.values())
+
+    o = O.svt_run(Ao, cfg, StopRule.none(), observer=lambda rec, U, sg, V: osg.append(sg) or True, test=To,
+                  start=start)
+    assert len(o.trace) == 1
+    ro = o.trace[0]
+    assert ro["iter"] == W + 1 == g["iter"]
+    assert (g["rank"], g["extension_rounds"], g["kept"]) == (ro["rank"], ro["extension_rounds"], ro["kept"])
+    assert g["eps_threshold"] == ro["eps_threshold"]
+    for key in KEYS + TEST_KEYS:
+        assert _rel(g[key], ro[key]) <= 1e-8, (key, g[key], ro[key])
+    # shrunk singular values (sigma - tau) of the kept triplets
+    np.testing.assert_allclose(gs[0], osg[0], rtol=1e-8, atol=1e-8 * float(osg[0][0]) if len(osg[0]) else 0)
+    A.close()
+    T.close()

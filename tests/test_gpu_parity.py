@@ -369,6 +369,22 @@ def test_svt_rank0_and_backends():
         check_runs(g, o, tol=1e-7)
 
 
+def test_svt_rank0_at_first_iteration_survives():  # test_solver.cpp:201-211
+    """Shrink keeps nothing at iteration 1 (kickstart k0 = 3 puts sigma_1 of
+    Y^0 just under tau): the fused update must run with k = 0 (no factor rows
+    exist) and the next iteration restarts from an empty basis."""
+    A = O.make_low_rank(60, 50, 6, 40)
+    S = O.sample_dense(A, 0.3, 41)
+    cfg = O.default_config(S)
+    cfg.seed = 42
+    cfg.tau = (3 - 1e-12) * cfg.delta * O.spectral_norm_est(S, 20, O.derive_seed(cfg.seed, 0))
+    cfg.maxit = 4
+    g = G.svt_run(gpu_mat(S), cfg, StopRule.none())
+    o = O.svt_run(S, cfg, StopRule.none())
+    assert o.trace[0]["kept"] == 0 and g.trace[0]["kept"] == 0
+    check_runs(g, o)
+
+
 def test_svt_validates():
     Sg = gpu_mat(O.sampled(2, 2, [0], [0], [1.0]))
     from paper_1704_05528_b200 import SvtConfig
