@@ -5,6 +5,7 @@
 // csr2csc permutation, the CSC value mirror, and both segment plans of the
 // load-balanced SpMM.  Only the CSR arrays cross PCIe; everything derived
 // from them is built in HBM.
+#include <vector>
 #include <cub/cub.cuh>
 
 #include "common.hpp"
@@ -358,6 +359,15 @@ void build_plan_device(svt_ctx* ctx, const long long* ptr, i64 rows, SegPlan& P)
                                                   P.long_first.get(), P.long_count.get());
     }
     sync_stream(ctx);  // cnt / off die here
+    {
+        std::vector<long long> hb(static_cast<size_t>(nsegs)), he(static_cast<size_t>(nsegs));
+        if (nsegs > 0) {
+            SVT_CUDA(cudaMemcpyAsync(hb.data(), P.seg_beg.get(), sizeof(long long) * nsegs, cudaMemcpyDeviceToHost, s));
+            SVT_CUDA(cudaMemcpyAsync(he.data(), P.seg_end.get(), sizeof(long long) * nsegs, cudaMemcpyDeviceToHost, s));
+            sync_stream(ctx);
+        }
+        build_groups(hb, he, s, P);
+    }
     P.v.nseg = nsegs;
     P.v.seg_row = P.seg_row.get();
     P.v.seg_beg = P.seg_beg.get();

@@ -148,14 +148,18 @@ typedef int (*HostAllreduceFn)(double* buf, std::int64_t count, void* user);
 struct Comm {
     int rank = 0;
     int world = 1;
-    void* handle = nullptr;  // ncclComm_t
+    void* handle = nullptr;       // ncclComm_t
+    void* handle_side = nullptr;  // second communicator for the side stream (ncclCommSplit)
     HostAllreduceFn host_fn = nullptr;
     void* host_user = nullptr;
     double* h_buf = nullptr;  // pinned staging (host mode)
     size_t h_cap = 0;
     long long calls = 0;    // all-reduces issued (instrumentation)
     double doubles = 0.0;   // doubles all-reduced
-    void allreduce_sum(double* buf, size_t count, cudaStream_t s);
+    void allreduce_sum(double* buf, size_t count, cudaStream_t s, bool side = false);
+    // collectives may also run on the side stream (speculative batches):
+    // host-staged mode, or NCCL with a second communicator
+    bool side_capable() const { return world > 1 && (host_fn != nullptr || handle_side != nullptr); }
     void allreduce_sum_i32(int* buf, size_t count, cudaStream_t s);
     void destroy();
 };
@@ -175,7 +179,12 @@ struct SegPlanView {
     const int* long_row = nullptr;
     const int* long_first = nullptr;
     const int* long_count = nullptr;
+    // groups of consecutive segments (<= kGrpSegs segments, ~kGrpEntries
+    // entries) walked by one warp with one continuous gather pipeline
+    long long ngrp = 0;
+    const int* grp_first = nullptr;  // ngrp + 1 segment offsets
 };
+constexpr int kGrpSegs = 32;
 // Shared-memory-tiled view of the same CSR / CSC pattern for wide panels
 // (build.cu builds it, sparse.cu consumes it).  Output rows are grouped in
 // blocks of kTileRows; a block's entries, ordered by gather index, are cut

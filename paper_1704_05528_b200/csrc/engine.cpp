@@ -276,7 +276,8 @@ void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out, cudaStre
           spmm_tiled(E.ctx, K_SPMMT, A->tile_csc.v, A->m_local, w, X, ldx, out, ldo, stream, scratch)))
         spmm(E.ctx, K_SPMMT, A->plan_csc.v, A->n, A->cscrow.get(), E.Y.csc, A->nnz_local, A->m_local, w, X, ldx, out,
              ldo, stream, scratch);
-    E.ctx->comm.allreduce_sum(out, static_cast<size_t>(A->n * w), stream ? stream : E.ctx->stream);
+    E.ctx->comm.allreduce_sum(out, static_cast<size_t>(A->n * w), stream ? stream : E.ctx->stream,
+                              stream != nullptr && stream == E.ctx->side);
 }
 
 // basis capacity of the engine's QB state (workspace sizing hint)
@@ -627,7 +628,21 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
                          static_cast<long long>(b), static_cast<long long>(kk), mw / th_h[0], rb / th_h[0], th_h[0],
                          kk < b ? th_h[static_cast<size_t>(kk)] / tau2 : 0.0);
         }
-        if (conv || b == r || it == maxit - 1) break;
+        if (conv || b == r) break;
+        if (it == maxit - 1) {
+            // not converged in maxit sweeps: never hand back unconverged Ritz
+            // pairs silently — the dense Gram eigensolve (exact to
+            // rounding) where it is affordable, else a warning
+            if (r <= 4096) {
+                std::fprintf(stderr, "[svt_b200] finalize_kept: %d sweeps without convergence at r = %lld; "
+                                     "using the dense Gram eigensolve\n", maxit, static_cast<long long>(r));
+                finalize(E, st, FinalizeMode::Kept, tau, out);
+                return;
+            }
+            std::fprintf(stderr, "[svt_b200] finalize_kept: %d sweeps without convergence at r = %lld "
+                                 "(kept pairs' residual above 1e-12 theta_1)\n", maxit, static_cast<long long>(r));
+            break;
+        }
         // Chebyshev-accelerated subspace step (Zhou & Saad's scaled
         // recurrence): damp [0, theta_b] -- everything below the block's
         // smallest Ritz value -- and amplify the block, then rescale column i
@@ -677,7 +692,7 @@ static void finalize_kept(Engine& E, const QBDev& st, double tau, i64 s_warm, u6
     // V_raw = B^T (Zq Yh) = Wn Yh; sigma = column norms (Rayleigh quotients)
     E.Vraw.ensure(static_cast<size_t>(n * std::max<i64>(kc, factor_cols(m + n, st.min_dim))));
     gemm(c, K_FINAL, false, n, kc, b, 1.0, Wn.get(), b, Yh.get(), b, 0.0, E.Vraw.get(), kc);
-    E.lam.ensure(static_cast<size_t>(kc));
+    E.lam.ensure(static_cast<size_t>(std::max<i64>(kc, factor_cols(m + n, st.min_dim))));  // kept rank creeps up: no regrow
     col_sumsq(c, E.Vraw.get(), n, kc, kc, E.lam.get());
     std::vector<double> s2(static_cast<size_t>(kc));
     read_doubles(c, E.lam.get(), static_cast<size_t>(kc), s2.data());
@@ -796,6 +811,13 @@ static void basis_tx(Engine& E, QBDev& st, i64 r0, i64 w, const double* X, i64 l
     gemm(c, K_GEMM, true, r0, w, m, 1.0, Q, st.cap, X, ldx, 0.0, C, w);
 }
 
+// SVTB_COEFF_VIA_B=0: Gram-Schmidt coefficients of a batch as Q^T X (an
+// m-row contraction) instead of B T (read per batch: A/B and test switch)
+static bool coeff_via_b() {
+    const char* e = std::getenv("SVTB_COEFF_VIA_B");
+    return e == nullptr || e[0] != '0';
+}
+
 // X = Y (Y^T (Y Omega))) into spec slot `slot`, on `stream` (main or side).
 static void batch_sketch(Engine& E, const svt_sketch_params& p, int round0, int K, int slot, bool side) {
     svt_ctx* c = E.ctx;
@@ -845,9 +867,13 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
     // batch's Gram-Schmidt / QR; the replay below decides whether it is used
     const i64 room = (st.min_dim - (r0 + W)) / w;
     const int Kn = static_cast<int>(std::min<i64>(K_next, room));
-    // (single rank only: NCCL collectives of one communicator must not run
-    // concurrently on two streams)
-    if (c->side && Kn >= 2 && !no_spec && c->comm.world == 1) {
+    // multi-rank: the side stream's Y^T X all-reduces need their own
+    // communicator (ncclCommSplit) or the host-staged mode; opt-in there
+    // (SVTB_SPEC_MULTI=1) until it has run on NVLink hardware
+    const char* sm_env = std::getenv("SVTB_SPEC_MULTI");  // per batch: tests toggle it
+    const bool spec_multi = sm_env != nullptr && sm_env[0] == '1';
+    const bool spec_ok = c->comm.world == 1 || (spec_multi && c->comm.side_capable());
+    if (c->side && Kn >= 2 && !no_spec && spec_ok) {
         if (!sp.ready) {
             SVT_CUDA(cudaEventCreateWithFlags(&sp.ready, cudaEventDisableTiming));
             SVT_CUDA(cudaEventCreateWithFlags(&sp.freed[0], cudaEventDisableTiming));
@@ -882,20 +908,48 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         // the test is false with that margin, so the check product Q^T X is
         // only formed when some block lost more (near-dependent rounds).
         E.CW.ensure(static_cast<size_t>(std::max(r0, st.cap) * Wc));  // basis capacity: no regrow as r0 grows
-        E.eW.ensure(static_cast<size_t>(3 * Wc));
-        col_sumsq(c, XW, m, W, W, E.eW.get() + 2 * W);
-        basis_tx(E, st, r0, W, XW, W, E.CW.get());
-        allreduce(c, E.CW.get(), static_cast<size_t>(r0 * W));
+        E.eW.ensure(static_cast<size_t>(4 * Wc));
+        // Gram-Schmidt coefficients C = Q^T X.  The batch panel is
+        // X = Y T with T = Y^T Y Omega (np = 1) or Omega (np = 0), and the
+        // coefficient rows B = Q^T Y of the basis are already stored (B^T,
+        // n x r0), so C = B T: a contraction over n instead of m rows
+        // (6.5x fewer flops at config 4), replicated on every rank (no
+        // all-reduce).  In exact arithmetic it is Q^T X; its rounding is
+        // relative to ||Y||_F ||T_k|| instead of ||X_k||, which the
+        // skip rule of the check product below accounts for.
+        const double* Tp = (p.np == 1) ? sp.t[slot].get() : sp.om[slot].get();
+        const bool via_b = coeff_via_b() && p.np <= 1 && n < m;
+        if (via_b) {
+            col_sumsq(c, Tp, n, W, W, E.eW.get() + 3 * W);
+            gemm(c, K_GEMM, true, r0, W, n, 1.0, st.Bt.get(), ldq, Tp, W, 0.0, E.CW.get(), W);
+        } else {
+            col_sumsq(c, XW, m, W, W, E.eW.get() + 2 * W);
+            basis_tx(E, st, r0, W, XW, W, E.CW.get());
+            allreduce(c, E.CW.get(), static_cast<size_t>(r0 * W));
+        }
         gemm(c, K_GEMM, false, m, W, r0, -1.0, Q, ldq, E.CW.get(), W, 1.0, XW, W);
         col_sumsq(c, XW, m, W, W, E.eW.get());
         allreduce(c, E.eW.get(), static_cast<size_t>(W));
-        allreduce(c, E.eW.get() + 2 * W, static_cast<size_t>(W));
-        // worst-case rounding of the two products ~ (m + r0) eps ||X_k||;
         // the decisions are taken on the device (predicated kernels), so the
         // batch issues no host synchronization here
-        const double thr = std::max(1e-3, 1.1e-8 * static_cast<double>(A->m + r0));
-        block_flags(c, E.eW.get(), E.eW.get() + 2 * W, nullptr, K, static_cast<int>(w), thr * thr, 0, nullptr,
-                    dfl(c, F_CHECK));
+        if (via_b) {
+            // residual Q^T X' after the pass ~ (sqrt(L) eps sqrt(r0)) ||Y||_F ||T_k||
+            // (L: longest CSC column); the check product is formed unless
+            // every block kept ||X'_k|| >= thr ||Y||_F ||T_k||, which puts the
+            // reference's test 1e-8 ||X'_k|| two orders above that residual
+            static const double thr_b = [] {
+                const char* e = std::getenv("SVTB_BT_THR");
+                return e ? std::atof(e) : 1e-2;
+            }();
+            block_flags(c, E.eW.get(), E.eW.get() + 3 * W, nullptr, K, static_cast<int>(w),
+                        thr_b * thr_b * st.frob_y_sq, 0, nullptr, dfl(c, F_CHECK));
+        } else {
+            // worst-case rounding of the two products ~ (m + r0) eps ||X_k||
+            allreduce(c, E.eW.get() + 2 * W, static_cast<size_t>(W));
+            const double thr = std::max(1e-3, 1.1e-8 * static_cast<double>(A->m + r0));
+            block_flags(c, E.eW.get(), E.eW.get() + 2 * W, nullptr, K, static_cast<int>(w), thr * thr, 0, nullptr,
+                        dfl(c, F_CHECK));
+        }
         gemm(c, K_GEMM, true, r0, W, m, 1.0, Q, ldq, XW, W, 0.0, E.CW.get(), W, dfl(c, F_CHECK));
         allreduce(c, E.CW.get(), static_cast<size_t>(r0 * W));
         col_sumsq(c, E.CW.get(), r0, W, W, E.eW.get() + W);

@@ -14,6 +14,7 @@
 struct SegPlan {
     svtb::DevBuf<int> seg_row, seg_slot, long_row, long_first, long_count;
     svtb::DevBuf<long long> seg_beg, seg_end;
+    svtb::DevBuf<int> grp_first;
     svtb::SegPlanView v;
 };
 
@@ -161,6 +162,8 @@ DevFactors full_svd(Engine& E);
 
 u64 derive_seed_u(u64 seed, u64 stream);
 
+// host.cpp: the segment groups of a plan (from its host-side segment bounds)
+void build_groups(const std::vector<long long>& beg, const std::vector<long long>& end, cudaStream_t s, SegPlan& P);
 // build.cu: device-side CSC view / csr2csc / segment plans of an uploaded CSR
 void build_plan_device(svt_ctx* ctx, const long long* ptr, i64 rows, SegPlan& P);
 int build_sampled_device(svt_ctx* ctx, svt_mat* M, const long long* col64);

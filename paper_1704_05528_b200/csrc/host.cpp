@@ -63,6 +63,37 @@ void partition_rows(i64 m, const i64* rowptr, int world, i64* bounds) {
     bounds[world] = m;
 }
 
+// Segment groups for the wide gather kernel (sparse.cu spmm_grp_kernel):
+// consecutive segments, at most kGrpSegs of them and ~SVTB_SPMM_GROUP
+// (default 384) entries, a segment never split — one warp streams several
+// short rows through one continuous gather pipeline.
+void build_groups(const std::vector<long long>& beg, const std::vector<long long>& end, cudaStream_t s, SegPlan& P) {
+    static const long long ge = [] {
+        const char* e = std::getenv("SVTB_SPMM_GROUP");
+        return e ? std::max(1LL, std::atoll(e)) : 384LL;
+    }();
+    const i64 nsegs = static_cast<i64>(beg.size());
+    std::vector<int> gf;
+    gf.reserve(static_cast<size_t>(nsegs / 4 + 2));
+    i64 q = 0;
+    while (q < nsegs) {
+        gf.push_back(static_cast<int>(q));
+        long long tot = end[q] - beg[q];
+        i64 r = q + 1;
+        while (r < nsegs && r - q < kGrpSegs && tot + (end[r] - beg[r]) <= ge) {
+            tot += end[r] - beg[r];
+            ++r;
+        }
+        q = r;
+    }
+    gf.push_back(static_cast<int>(nsegs));
+    P.grp_first.alloc(gf.size());
+    SVT_CUDA(cudaMemcpyAsync(P.grp_first.get(), gf.data(), sizeof(int) * gf.size(), cudaMemcpyHostToDevice, s));
+    SVT_CUDA(cudaStreamSynchronize(s));  // gf dies here
+    P.v.ngrp = static_cast<long long>(gf.size()) - 1;
+    P.v.grp_first = P.grp_first.get();
+}
+
 // Row segmentation for the load-balanced SpMM (sparse.cu): rows longer than
 // kSegLen entries are cut into kSegLen chunks that write partial rows.
 void build_plan(const std::vector<i64>& ptr, i64 nrows, cudaStream_t s, SegPlan& P) {
@@ -107,6 +138,7 @@ void build_plan(const std::vector<i64>& ptr, i64 nrows, cudaStream_t s, SegPlan&
     up_i(P.long_first, lfirst);
     up_i(P.long_count, lcount);
     SVT_CUDA(cudaStreamSynchronize(s));  // host vectors die here
+    build_groups(beg, end, s, P);
     P.v.nseg = static_cast<long long>(row.size());
     P.v.seg_row = P.seg_row.get();
     P.v.seg_beg = P.seg_beg.get();

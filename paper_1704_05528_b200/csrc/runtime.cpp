@@ -166,9 +166,19 @@ void nccl_init(Comm& c, int rank, int world, const void* id128) {
     ncclComm_t_ comm = nullptr;
     check(fn(&comm, world, id, rank), "ncclCommInitRank");
     c.handle = comm;
+    // a second communicator over the same ranks for the side stream's
+    // collectives (speculative batches run Y^T X all-reduces concurrently
+    // with the main stream's; one communicator must not be used from two
+    // streams at once).  ncclCommSplit(comm, color 0, key rank, &out, NULL).
+    auto split = reinterpret_cast<ncclResult_t_ (*)(ncclComm_t_, int, int, ncclComm_t_*, void*)>(
+        dlsym(nccl().h, "ncclCommSplit"));
+    if (split != nullptr) {
+        ncclComm_t_ side = nullptr;
+        if (split(comm, 0, rank, &side, nullptr) == 0) c.handle_side = side;
+    }
 }
 
-void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t s) {
+void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t s, bool side) {
     if (world <= 1 || count == 0) return;
     calls++;
     doubles += static_cast<double>(count);
@@ -187,7 +197,9 @@ void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t s) {
         SVT_CUDA(cudaStreamSynchronize(s));  // the staging buffer is reused by the next call
         return;
     }
-    check(svtb::nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, handle, s), "ncclAllReduce");
+    if (side && handle_side == nullptr) throw nccl_error("side-stream all-reduce without a side communicator");
+    check(svtb::nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, side ? handle_side : handle, s),
+          "ncclAllReduce");
 }
 
 void Comm::allreduce_sum_i32(int* buf, size_t count, cudaStream_t s) {
@@ -200,6 +212,10 @@ void Comm::destroy() {
         cudaFreeHost(h_buf);
         h_buf = nullptr;
         h_cap = 0;
+    }
+    if (handle_side != nullptr) {
+        svtb::nccl().CommDestroy(handle_side);
+        handle_side = nullptr;
     }
     if (handle != nullptr) {
         svtb::nccl().CommDestroy(handle);

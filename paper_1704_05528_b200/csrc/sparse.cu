@@ -165,6 +165,110 @@ __global__ void __launch_bounds__(128) spmm_wide_kernel(SegPlanView plan, const 
     }
 }
 
+// Wide panels, grouped: one warp walks a GROUP of consecutive segments
+// (plan.grp_first; short rows are grouped up to ~384 entries) with ONE
+// continuous gather pipeline — the index / value chunk of the next 32
+// entries is in flight while the current chunk's gathers issue, and U
+// entries' panel rows (Q doubles per lane each) are gathered per step — so
+// a warp's memory-level parallelism does not restart at every short row.
+// When an entry crosses its segment's end the accumulated row is written
+// (output row, or the long row's partial slot) and the accumulators reset.
+// Segment bounds / targets of the group (<= kGrpSegs) sit one per lane and
+// are broadcast by shuffle.  Per output element the sum runs over the row's
+// entries in CSR order: the same order as spmm_wide_kernel (bitwise equal).
+template <int Q, int U, int MINB>
+__global__ void __launch_bounds__(128, MINB) spmm_grp_kernel(SegPlanView plan, const int* __restrict__ idx,
+                                                             const double* __restrict__ val,
+                                                             const double* __restrict__ X, long long ldx,
+                                                             long long w, double* __restrict__ out, long long ldo,
+                                                             double* __restrict__ partial) {
+    const int lane = threadIdx.x & 31;
+    const long long g = static_cast<long long>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+    if (g >= plan.ngrp) return;
+    const long long c0 = static_cast<long long>(blockIdx.y) * (32 * Q);
+    // valid column slots of this lane: c0 + lane + 32 q < w  <=>  q < qn
+    const int qn = static_cast<int>(max(0LL, min(static_cast<long long>(Q), (w - c0 - lane + 31) / 32)));
+    const int s0 = plan.grp_first[g], ns = plan.grp_first[g + 1] - s0;
+    // lane i: end / target of segment s0 + i (broadcast by shuffle)
+    long long my_end = 0;
+    int my_dst = 0;  // >= 0: output row; < 0: partial slot -(dst + 1)
+    if (lane < ns) {
+        my_end = plan.seg_end[s0 + lane];
+        const int slot = plan.seg_slot[s0 + lane];
+        my_dst = slot < 0 ? plan.seg_row[s0 + lane] : -(slot + 1);
+    }
+    // entry offsets relative to the group's first entry (a group spans at
+    // most kGrpSegs segments of <= kSegLen entries: 32-bit)
+    const long long beg = plan.seg_beg[s0];
+    const int* gi = idx + beg;
+    const double* gv = val + beg;
+    const int my_e = static_cast<int>(my_end - beg);
+    const int end = __shfl_sync(0xffffffffu, my_e, ns - 1);
+    int si = 0;  // current segment (group-relative)
+    int cur_end = __shfl_sync(0xffffffffu, my_e, 0);
+    double acc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc[q] = 0.0;
+    const double* xb = X + c0 + lane;
+    auto flush = [&]() {
+        const int dst = __shfl_sync(0xffffffffu, my_dst, si);
+        double* o = (dst >= 0) ? out + static_cast<long long>(dst) * ldo
+                               : partial + static_cast<long long>(-(dst + 1)) * w;
+        o += c0 + lane;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            if (q < qn) o[32 * q] = acc[q];
+            acc[q] = 0.0;
+        }
+        ++si;
+        cur_end = __shfl_sync(0xffffffffu, my_e, si < ns ? si : ns - 1);
+    };
+    for (int k0 = 0; k0 < end; k0 += 32) {
+        const int k = k0 + lane;
+        const int cl = (k < end) ? __ldg(gi + k) : 0;
+        const double vl = (k < end) ? __ldg(gv + k) : 0.0;
+        if (cur_end >= k0 + 32 && k0 + 32 <= end) {
+            // fast path: a full chunk inside one segment (rows average ~130
+            // entries at config 4): U entries' gathers in flight per step,
+            // no boundary tests; the values are broadcast after the gathers
+            // issue (fewer live registers)
+#pragma unroll 1
+            for (int e = 0; e < 32; e += U) {
+                double xv[U][Q];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int c = __shfl_sync(0xffffffffu, cl, e + u);
+                    const double* xr = xb + static_cast<long long>(c) * ldx;
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) xv[u][q] = (q < qn) ? __ldg(xr + 32 * q) : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const double v = __shfl_sync(0xffffffffu, vl, e + u);
+#pragma unroll
+                    for (int q = 0; q < Q; ++q) acc[q] = fma(v, xv[u][q], acc[q]);
+                }
+            }
+        } else {
+            // a segment boundary (or the group's last, partial chunk) inside
+            // the chunk: entry by entry, writing finished rows (empty
+            // segments write zero rows)
+            const int cnt = min(32, end - k0);
+#pragma unroll 1
+            for (int e = 0; e < cnt; ++e) {
+                while (k0 + e >= cur_end) flush();
+                const int c = __shfl_sync(0xffffffffu, cl, e);
+                const double v = __shfl_sync(0xffffffffu, vl, e);
+                const double* xr = xb + static_cast<long long>(c) * ldx;
+#pragma unroll
+                for (int q = 0; q < Q; ++q)
+                    if (q < qn) acc[q] = fma(v, __ldg(xr + 32 * q), acc[q]);
+            }
+        }
+    }
+    while (si < ns) flush();  // the last segment (and any empty ones after it)
+}
+
 // out[row, j] = sum of the row's partial slots in a fixed (deterministic)
 // order.  Narrow panels: one warp per long row, lanes over the slots, a
 // shuffle tree per column.
@@ -674,6 +778,13 @@ __global__ void tile_values_kernel(long long nnz, const int* __restrict__ perm, 
 
 }  // namespace
 
+// SVTB_SPMM_LEGACY=1: the one-warp-per-segment kernel (A/B switch, read
+// per call so tests can compare the two)
+static bool spmm_legacy() {
+    const char* e = std::getenv("SVTB_SPMM_LEGACY");
+    return e != nullptr && e[0] == '1';
+}
+
 void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* idx, const double* val, i64 nnz,
           i64 x_rows, i64 w, const double* X, i64 ldx, double* out, i64 ldo, cudaStream_t stream,
           DevBuf<double>* scratch) {
@@ -700,6 +811,33 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
 #undef SVT_CASE
             default:
                 break;
+        }
+    } else if (plan.ngrp > 0 && !spmm_legacy()) {
+        const unsigned nb = static_cast<unsigned>((plan.ngrp + 3) / 4);
+        const unsigned chunks = static_cast<unsigned>(w <= 128 ? 1 : (w + 127) / 128);
+        if (w <= 32)
+            spmm_grp_kernel<1, 8, 8><<<dim3(nb, 1), 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+        else if (w <= 64)
+            spmm_grp_kernel<2, 8, 8><<<dim3(nb, 1), 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+        else if (w <= 96)
+            spmm_grp_kernel<3, 4, 8><<<dim3(nb, 1), 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+        else {
+            // SVTB_SPMM_VARIANT (tuning): U,MINB of the Q = 4 instantiation
+            static const int var = [] {
+                const char* e = std::getenv("SVTB_SPMM_VARIANT");
+                return e ? std::atoi(e) : 0;
+            }();
+            const dim3 gq(nb, chunks);
+            if (var == 1)
+                spmm_grp_kernel<4, 4, 6><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+            else if (var == 2)
+                spmm_grp_kernel<4, 3, 8><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+            else if (var == 3)
+                spmm_grp_kernel<4, 2, 8><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+            else if (var == 4)
+                spmm_grp_kernel<4, 8, 4><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+            else
+                spmm_grp_kernel<4, 4, 8><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
         }
     } else {
         const unsigned nb = static_cast<unsigned>((plan.nseg + 3) / 4);

@@ -35,6 +35,7 @@ from oracle import oracle as O  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 RUNS = {1: None, 2: None, 3: 15, 4: 5}  # maxit (None: the config's stop rule decides)
+SENS_MAXIT = {2: 120}  # the perturbed run of config 2 stops early (its divergence shows by then)
 PROBES = 512
 
 
@@ -63,6 +64,25 @@ def generate(config):
         return True
 
     r = O.svt_run(A, cfg, stop, observer=obs, test=T)
+    # sensitivity of the run itself: the same oracle on A perturbed by one
+    # ulp (relative 2^-52, random sign) per entry.  Two correct
+    # implementations with different rounding (GPU reductions vs the serial
+    # CPU order) cannot agree more closely than the run's own amplification
+    # of such perturbations; the GPU test scales its per-iteration tolerance
+    # by it and expects exact ranks while the perturbed run keeps them.
+    sign = np.where(np.random.default_rng(99).random(A.nnz) < 0.5, -1.0, 1.0)
+    Ap = O.Csr(A.m, A.n, A.rowptr, A.col, A.val * (1.0 + sign * 2.0 ** -52))
+    cfg_p = cfg.copy(maxit=min(cfg.maxit, SENS_MAXIT.get(config, cfg.maxit)))
+    rp_ = O.svt_run(Ap, cfg_p, stop, test=T)
+    keys_s = ["residual", "train_mae", "rel_residual_x"] + (["test_mae", "test_rmse"] if T is not None else [])
+    dev, first = [], None
+    for a, b in zip(rp_.trace, r.trace):
+        dev.append(max(abs(a[k] - b[k]) / abs(b[k]) for k in keys_s))
+        if first is None and (a["rank"], a["extension_rounds"], a["kept"]) != (b["rank"], b["extension_rounds"],
+                                                                                b["kept"]):
+            first = a["iter"]
+    print(f"  sensitivity: {len(dev)} iterations, first rank/rounds/kept change {first}, "
+          f"max dev {max(dev):.2e}", flush=True)
     pr, pc = probe_positions(m, n)
     X = np.einsum("ij,j,ij->i", r.U[pr], r.sigma, r.V[pc]) if r.sigma.size else np.zeros(PROBES)
     keys = ("iter", "rank", "extension_rounds", "kept", "residual", "eps_threshold", "train_mae", "rel_residual_x",
@@ -73,6 +93,8 @@ def generate(config):
         "trace": [{k: rec[k] for k in keys} for rec in r.trace],
         "sigma": r.sigma.tolist(),
         "probe": {"rows": pr.tolist(), "cols": pc.tolist(), "values": X.tolist()},
+        "sensitivity": {"perturbation": "A * (1 +- 2^-52), random signs (seed 99)", "iterations": len(dev),
+                        "rel_dev": dev, "first_rank_change": first},
         "oracle_threads": O.num_threads(), "oracle_seconds": round(time.time() - t0, 1),
     }
     path = os.path.join(HERE, f"config{config}_trace.json")

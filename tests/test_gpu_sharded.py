@@ -81,6 +81,10 @@ def _worker(rank, port, q):
         ctx = G.Context.hostcomm(0, rank, WORLD, allreduce)
         res = {}
         for name, m, n, A, T, cfg, iters in _cases():
+            # config 3 with the speculative side-stream batches (their Y^T X
+            # all-reduces run on the side stream: the second-communicator
+            # path of NCCL mode), the skewed case without
+            os.environ["SVTB_SPEC_MULTI"] = "1" if name == "config3" else "0"
             b = G.partition_rows(A.rowptr, WORLD)
             rb, re_ = int(b[rank]), int(b[rank + 1])
             Ag = G.SampledMatrix.from_csr(m, n, A.rowptr, A.col, A.val, ctx=ctx, row_block=(rb, re_))
