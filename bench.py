@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle CPU work for cpu_baseline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=0,
+                    help="iterations of the separate per-launch-event pass (0: all K)")
     return ap.parse_args()
 
 
@@ -389,7 +391,8 @@ def main():
     s3 = G.Solver.resume(A, cfg, stop, ckpt, test=T)
     ctx.reset_stats()
     ctx.set_profiling(True)
-    for _ in range(args.steps):
+    psteps = args.profile_steps if 0 < args.profile_steps < args.steps else args.steps
+    for _ in range(psteps):
         s3.step()
     ctx.join()
     ctx.sync()
@@ -483,14 +486,15 @@ def main():
                        "setup_s": round(setup_s, 2)},
             "roofline": roof,
             "sparse_roofline": sparse,
-            "kernel_ms_per_step": {k: round(v["total_ms"] / args.steps, 3) for k, v in stats.items()},
+            "kernel_ms_per_step": {k: round(v["total_ms"] / psteps, 3) for k, v in stats.items()},
+            "profiled_iterations": list(range(args.warmup + 1, args.warmup + psteps + 1)),
             "gpu_launches": launches,
             "host": {"syncs_per_step": hstats["syncs"] / args.steps,
-                     "sync_wait_ms_per_step_profiled_pass": hstats_prof["sync_ms"] / args.steps,
+                     "sync_wait_ms_per_step_profiled_pass": hstats_prof["sync_ms"] / psteps,
                      "device_allocs_in_timed_region": al1["mallocs"] - al0["mallocs"],
                      "device_frees_in_timed_region": al1["frees"] - al0["frees"],
                      "alloc_ms_in_timed_region": al1["ms"] - al0["ms"],
-                     "kernel_ms_per_step_profiled_pass": sum(v["total_ms"] for v in stats.values()) / args.steps},
+                     "kernel_ms_per_step_profiled_pass": sum(v["total_ms"] for v in stats.values()) / psteps},
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,

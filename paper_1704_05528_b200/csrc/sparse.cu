@@ -186,8 +186,11 @@ __global__ void __launch_bounds__(128, MINB) spmm_grp_kernel(SegPlanView plan, c
     const long long g = static_cast<long long>(blockIdx.x) * 4 + (threadIdx.x >> 5);
     if (g >= plan.ngrp) return;
     const long long c0 = static_cast<long long>(blockIdx.y) * (32 * Q);
-    // valid column slots of this lane: c0 + lane + 32 q < w  <=>  q < qn
-    const int qn = static_cast<int>(max(0LL, min(static_cast<long long>(Q), (w - c0 - lane + 31) / 32)));
+    // valid column slots of this lane: 32 q < wl  (32-bit compares)
+    const int wl = static_cast<int>(min(w - c0, static_cast<long long>(32 * Q))) - lane;
+    // panel row address = base + c * (ldx * 8 bytes): one 32 x 32 -> 64-bit
+    // multiply-add per gathered row
+    const unsigned ldx8 = static_cast<unsigned>(ldx * 8);
     const int s0 = plan.grp_first[g], ns = plan.grp_first[g + 1] - s0;
     // lane i: end / target of segment s0 + i (broadcast by shuffle)
     long long my_end = 0;
@@ -209,7 +212,7 @@ __global__ void __launch_bounds__(128, MINB) spmm_grp_kernel(SegPlanView plan, c
     double acc[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) acc[q] = 0.0;
-    const double* xb = X + c0 + lane;
+    const char* xb = reinterpret_cast<const char*>(X + c0 + lane);
     auto flush = [&]() {
         const int dst = __shfl_sync(0xffffffffu, my_dst, si);
         double* o = (dst >= 0) ? out + static_cast<long long>(dst) * ldo
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(128, MINB) spmm_grp_kernel(SegPlanView plan, c
         o += c0 + lane;
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
-            if (q < qn) o[32 * q] = acc[q];
+            if (32 * q < wl) o[32 * q] = acc[q];
             acc[q] = 0.0;
         }
         ++si;
@@ -237,10 +240,10 @@ __global__ void __launch_bounds__(128, MINB) spmm_grp_kernel(SegPlanView plan, c
                 double xv[U][Q];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int c = __shfl_sync(0xffffffffu, cl, e + u);
-                    const double* xr = xb + static_cast<long long>(c) * ldx;
+                    const unsigned c = static_cast<unsigned>(__shfl_sync(0xffffffffu, cl, e + u));
+                    const double* xr = reinterpret_cast<const double*>(xb + static_cast<unsigned long long>(c) * ldx8);
 #pragma unroll
-                    for (int q = 0; q < Q; ++q) xv[u][q] = (q < qn) ? __ldg(xr + 32 * q) : 0.0;
+                    for (int q = 0; q < Q; ++q) xv[u][q] = (32 * q < wl) ? __ldg(xr + 32 * q) : 0.0;
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -257,12 +260,12 @@ __global__ void __launch_bounds__(128, MINB) spmm_grp_kernel(SegPlanView plan, c
 #pragma unroll 1
             for (int e = 0; e < cnt; ++e) {
                 while (k0 + e >= cur_end) flush();
-                const int c = __shfl_sync(0xffffffffu, cl, e);
+                const unsigned c = static_cast<unsigned>(__shfl_sync(0xffffffffu, cl, e));
                 const double v = __shfl_sync(0xffffffffu, vl, e);
-                const double* xr = xb + static_cast<long long>(c) * ldx;
+                const double* xr = reinterpret_cast<const double*>(xb + static_cast<unsigned long long>(c) * ldx8);
 #pragma unroll
                 for (int q = 0; q < Q; ++q)
-                    if (q < qn) acc[q] = fma(v, __ldg(xr + 32 * q), acc[q]);
+                    if (32 * q < wl) acc[q] = fma(v, __ldg(xr + 32 * q), acc[q]);
             }
         }
     }
@@ -835,7 +838,7 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
             else if (var == 3)
                 spmm_grp_kernel<4, 2, 8><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
             else if (var == 4)
-                spmm_grp_kernel<4, 8, 4><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+                spmm_grp_kernel<4, 4, 10><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
             else
                 spmm_grp_kernel<4, 4, 8><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
         }
