@@ -264,6 +264,16 @@ int svt_dev_gemm_tn_ozaki(svt_ctx* ctx, int64_t M, int64_t N, int64_t K, const d
  * :130 without the host copies.  Asynchronous. */
 int svt_dev_sp_mult(svt_mat* S, int transpose, int64_t w, const double* X, int64_t ldx, double* out,
                     int64_t ldo);
+/* Device-pointer fused SDDMM + Bregman update on A's pattern, the SVT loop's
+ * last step (solver.hpp:321-323 with project_low_rank / sp_axpy,
+ * sampled.hpp:148-176): with P = U Vs^T on Lambda (U: m_local x k, Vs = V
+ * diag(sigma - tau): n x k, row-major), d = A - P and Y_csr += delta * d
+ * (y_csr: nnz_local values in CSR order, updated in place); y_csc (nullable)
+ * receives the CSC-ordered mirror.  sums4 (host, nullable) <- {sum |d|,
+ * sum d^2, sum (A - Y_old)^2, sum Y_new^2} (all-reduced).  Asynchronous
+ * unless sums4 is given. */
+int svt_dev_sddmm_update(svt_mat* A, int64_t k, const double* U, int64_t ldu, const double* Vs, int64_t ldv,
+                         double delta, double* y_csr, double* y_csc, double* sums4);
 
 /* ---- sketch engines (sketch.hpp) -------------------------------------- */
 int svt_rsvd(svt_mat* Y, int64_t k, const svt_sketch_params* p, svt_factors** out);  /* sketch.hpp:165 */

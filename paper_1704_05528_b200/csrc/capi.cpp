@@ -750,6 +750,26 @@ int svt_dev_sp_mult(svt_mat* S, int transpose, int64_t w, const double* X, int64
     });
 }
 
+int svt_dev_sddmm_update(svt_mat* A, int64_t k, const double* U, int64_t ldu, const double* Vs, int64_t ldv,
+                         double delta, double* y_csr, double* y_csc, double* sums4) {
+    return guard([&] {
+        need(A, "svt_dev_sddmm_update");
+        need(y_csr, "svt_dev_sddmm_update: y_csr");
+        if (k < 0 || (k > 0 && (!U || !Vs || ldu < k || ldv < k)))
+            throw std::invalid_argument("dev_sddmm_update: bad factors");
+        svt_ctx* c = A->ctx;
+        const bool gather = y_csc != nullptr && A->csc2csr.n > 0 && A->nnz_local > 0;
+        sddmm_update(c, A->plan_csr.v, A->m_local, A->col.get(), A->val.get(), y_csr, gather ? nullptr : y_csc,
+                     A->csr2csc.get(), A->nnz_local, A->n, U, ldu, Vs, ldv, k, delta, 1, c->d_scalars + 40);
+        if (gather) mirror_csc(c, A->nnz_local, A->csc2csr.get(), y_csr, y_csc);
+        c->comm.allreduce_sum(c->d_scalars + 40, 4, c->stream);
+        if (sums4) {
+            SVT_CUDA(cudaMemcpyAsync(sums4, c->d_scalars + 40, sizeof(double) * 4, cudaMemcpyDeviceToHost, c->stream));
+            sync_stream(c);
+        }
+    });
+}
+
 int svt_sp_mult_t(svt_mat* S, int64_t w, const double* X, double* out) {
     return guard([&] {
         need(S, "svt_sp_mult_t");

@@ -18,7 +18,7 @@ singular values, and the final completed matrix X = U diag(sigma) V^T
 probed at 512 seeded positions.  tests/test_gpu_config_fixtures.py checks
 the device path against them (-m gpu).
 
-  OMP_NUM_THREADS=8 python tests/golden/make_config_fixtures.py [config ...]
+  OMP_NUM_THREADS=8 python tests/golden/make_config_fixtures.py [config ...] [--sensitivity-only]
 
 The oracle's parallel loops reduce in a fixed order, so the fixtures do not
 depend on the thread count."""
@@ -47,6 +47,30 @@ def probe_positions(m, n, seed=12345):
     return rng.integers(0, m, PROBES), rng.integers(0, n, PROBES)
 
 
+def sensitivity(config, A, T, cfg, stop, trace):
+    """Sensitivity of the run itself: the same oracle on A perturbed by one
+    ulp (relative 2^-52, random sign) per entry.  Two correct
+    implementations with different rounding (GPU reductions vs the serial
+    CPU order) cannot agree more closely than the run's own amplification
+    of such perturbations; the GPU test scales its per-iteration tolerance
+    by it and expects exact ranks while the perturbed run keeps them."""
+    sign = np.where(np.random.default_rng(99).random(A.nnz) < 0.5, -1.0, 1.0)
+    Ap = O.Csr(A.m, A.n, A.rowptr, A.col, A.val * (1.0 + sign * 2.0 ** -52))
+    cfg_p = cfg.copy(maxit=min(cfg.maxit, SENS_MAXIT.get(config, cfg.maxit)))
+    rp_ = O.svt_run(Ap, cfg_p, stop, test=T)
+    keys_s = ["residual", "train_mae", "rel_residual_x"] + (["test_mae", "test_rmse"] if T is not None else [])
+    dev, first = [], None
+    for a, b in zip(rp_.trace, trace):
+        dev.append(max(abs(a[k] - b[k]) / abs(b[k]) for k in keys_s))
+        if first is None and (a["rank"], a["extension_rounds"], a["kept"]) != (b["rank"], b["extension_rounds"],
+                                                                                b["kept"]):
+            first = a["iter"]
+    print(f"  sensitivity: {len(dev)} iterations, first rank/rounds/kept change {first}, "
+          f"max dev {max(dev):.2e}", flush=True)
+    return {"perturbation": "A * (1 +- 2^-52), random signs (seed 99)", "iterations": len(dev),
+            "rel_dev": dev, "first_rank_change": first}
+
+
 def generate(config):
     d = O.synth_config(config, 1)
     A, T = d["train"], d["test"]
@@ -64,25 +88,7 @@ def generate(config):
         return True
 
     r = O.svt_run(A, cfg, stop, observer=obs, test=T)
-    # sensitivity of the run itself: the same oracle on A perturbed by one
-    # ulp (relative 2^-52, random sign) per entry.  Two correct
-    # implementations with different rounding (GPU reductions vs the serial
-    # CPU order) cannot agree more closely than the run's own amplification
-    # of such perturbations; the GPU test scales its per-iteration tolerance
-    # by it and expects exact ranks while the perturbed run keeps them.
-    sign = np.where(np.random.default_rng(99).random(A.nnz) < 0.5, -1.0, 1.0)
-    Ap = O.Csr(A.m, A.n, A.rowptr, A.col, A.val * (1.0 + sign * 2.0 ** -52))
-    cfg_p = cfg.copy(maxit=min(cfg.maxit, SENS_MAXIT.get(config, cfg.maxit)))
-    rp_ = O.svt_run(Ap, cfg_p, stop, test=T)
-    keys_s = ["residual", "train_mae", "rel_residual_x"] + (["test_mae", "test_rmse"] if T is not None else [])
-    dev, first = [], None
-    for a, b in zip(rp_.trace, r.trace):
-        dev.append(max(abs(a[k] - b[k]) / abs(b[k]) for k in keys_s))
-        if first is None and (a["rank"], a["extension_rounds"], a["kept"]) != (b["rank"], b["extension_rounds"],
-                                                                                b["kept"]):
-            first = a["iter"]
-    print(f"  sensitivity: {len(dev)} iterations, first rank/rounds/kept change {first}, "
-          f"max dev {max(dev):.2e}", flush=True)
+    sens = sensitivity(config, A, T, cfg, stop, r.trace)
     pr, pc = probe_positions(m, n)
     X = np.einsum("ij,j,ij->i", r.U[pr], r.sigma, r.V[pc]) if r.sigma.size else np.zeros(PROBES)
     keys = ("iter", "rank", "extension_rounds", "kept", "residual", "eps_threshold", "train_mae", "rel_residual_x",
@@ -93,8 +99,7 @@ def generate(config):
         "trace": [{k: rec[k] for k in keys} for rec in r.trace],
         "sigma": r.sigma.tolist(),
         "probe": {"rows": pr.tolist(), "cols": pc.tolist(), "values": X.tolist()},
-        "sensitivity": {"perturbation": "A * (1 +- 2^-52), random signs (seed 99)", "iterations": len(dev),
-                        "rel_dev": dev, "first_rank_change": first},
+        "sensitivity": sens,
         "oracle_threads": O.num_threads(), "oracle_seconds": round(time.time() - t0, 1),
     }
     path = os.path.join(HERE, f"config{config}_trace.json")
@@ -103,6 +108,25 @@ def generate(config):
     print(f"wrote {path}: {len(r.trace)} iterations, converged={r.converged}, {time.time() - t0:.0f} s")
 
 
+def add_sensitivity(config):
+    """Recompute only the fixture's sensitivity block (the perturbed run)
+    against the trace already stored in tests/golden/config{c}_trace.json."""
+    path = os.path.join(HERE, f"config{config}_trace.json")
+    with open(path) as f:
+        out = json.load(f)
+    d = O.synth_config(config, 1)
+    A, T = d["train"], d["test"]
+    cfg, stop = config_params(config, A.nnz, d["m"], d["n"], float(np.sqrt(np.sum(A.val * A.val))))
+    cfg.maxit = out["maxit"]
+    out["sensitivity"] = sensitivity(config, A, T, cfg, stop, out["trace"])
+    with open(path, "w") as f:
+        json.dump(out, f, indent=0)
+    print(f"wrote {path}: sensitivity over {out['sensitivity']['iterations']} iterations")
+
+
 if __name__ == "__main__":
-    for c in [int(a) for a in sys.argv[1:]] or sorted(RUNS):
-        generate(c)
+    args = sys.argv[1:]
+    only_sens = "--sensitivity-only" in args
+    cfgs = [int(a) for a in args if not a.startswith("--")] or sorted(RUNS)
+    for c in cfgs:
+        add_sensitivity(c) if only_sens else generate(c)
