@@ -332,8 +332,9 @@ void launch_narrow(svt_ctx* ctx, cudaStream_t s, const SegPlanView& plan, const 
 constexpr int kSddmmWarps = 8;
 constexpr int kSddmmU = 4;  // entries per lane group in flight
 
-// Fused SDDMM + Bregman update + reductions, one warp per row.  The warp is
-// G = 32 / KP groups of KP lanes (KP = the kept rank k rounded up to a power
+// Fused SDDMM + Bregman update + reductions for kept ranks k > 64 (config 2
+// keeps most of its basis; k <= 64 runs sddmm_warp_kernel below), one warp
+// per row segment.  The warp is G = 32 / KP groups of KP lanes (KP = the kept rank k rounded up to a power
 // of two, at most 32); group g takes every G-th stored entry of the row and
 // its lanes split the k-long dot product U[i,:] . Vs[j,:], so each factor row
 // is read with coalesced loads (a lane-per-entry loop would touch 32
@@ -449,49 +450,68 @@ __global__ void mirror_csc_kernel(long long nnz, const int* __restrict__ csc2csr
     if (p < nnz) Ycsc[p] = Y[__ldg(csc2csr + p)];
 }
 
-// Large kept rank (16 < k <= 64): lane l holds U[i, l] and U[i, l + 32] in
-// registers for the whole segment; 32 entries are processed per step: every
-// lane forms its partial dot product for all 32 (coalesced loads of each
-// factor row across the warp), then a transposing butterfly (reduce-scatter:
-// 16 + 8 + 4 + 2 + 1 shuffles) leaves the full sum of entry e0 + l on lane l,
-// so the 32 updates run lane-parallel with coalesced A / Y accesses.
-__global__ void __launch_bounds__(32 * kSddmmWarps) sddmm_update_wide_kernel(
+// Fused SDDMM + update for k <= 64, one warp per row segment, 32 entries per
+// chunk.  The warp is G = 32 / KP lane groups of KP lanes (KP = k rounded up
+// to a power of two, <= 32); lane j of a group holds U[i, j] (and, TWO,
+// U[i, j + 32]) for the whole segment.  Per chunk the entries' index, A and Y
+// are loaded coalesced (lane = entry) one chunk ahead; step s = 0..KP-1
+// gathers, in every group g, the factor row of entry s*G + g (coalesced
+// across the group's lanes) — the KP steps' loads are independent and all in
+// flight together.  A reduce-scatter butterfly over the group's KP lanes
+// (KP/2 + ... + 1 shuffles) then leaves the complete dot product of step j on
+// lane j of each group, and one shuffle hands it to the lane that owns the
+// entry, so the update, its Y store and the four sums run lane-parallel.
+template <int KP, bool TWO>
+__global__ void __launch_bounds__(32 * kSddmmWarps, (KP >= 16 ? 2 : 3)) sddmm_warp_kernel(
     SegPlanView plan, const int* __restrict__ col, const double* __restrict__ A, double* __restrict__ Y,
     double* __restrict__ Ycsc, const int* __restrict__ csr2csc, const double* __restrict__ U, long long ldu,
     const double* __restrict__ Vs, long long ldv, int k, double delta, int mode, double* __restrict__ partials) {
+    constexpr int G = 32 / KP;
     __shared__ double red[kSddmmWarps][4];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
+    const int g = lane / KP, j = lane % KP;
+    // lane holding the sum of the entry this lane owns (entry l = s * G + g')
+    const int src = (lane % G) * KP + lane / G;
     double s_abs = 0.0, s_sq = 0.0, s_res = 0.0, s_y = 0.0;
-    const bool lo = lane < k, hi = lane + 32 < k;
+    const bool lo = j < k, hi = TWO && j + 32 < k;
+    const int jl0 = lo ? j : 0, jl1 = hi ? j + 32 : 0;  // clamped: unconditional loads, zero weight
     for (long long sg = static_cast<long long>(blockIdx.x) * kSddmmWarps + warp; sg < plan.nseg;
          sg += static_cast<long long>(gridDim.x) * kSddmmWarps) {
         const long long row = plan.seg_row[sg];
         const long long beg = plan.seg_beg[sg], end = plan.seg_end[sg];
         const double* ur = U + row * ldu;
-        const double u0 = lo ? __ldg(ur + lane) : 0.0;
-        const double u1 = hi ? __ldg(ur + lane + 32) : 0.0;
+        const double u0 = lo ? __ldg(ur + j) : 0.0;
+        const double u1 = hi ? __ldg(ur + j + 32) : 0.0;
+        long long e = beg + lane;
+        int cl_n = (e < end) ? __ldg(col + e) : 0;
+        double a_n = (e < end) ? __ldg(A + e) : 0.0;
+        double y_n = (e < end) ? Y[e] : 0.0;
         for (long long e0 = beg; e0 < end; e0 += 32) {
-            const long long e = e0 + lane;
-            const int cl = (e < end) ? __ldg(col + e) : -1;
-            const double a_pre = (e < end) ? __ldg(A + e) : 0.0;
-            const double y_pre = (e < end) ? Y[e] : 0.0;
-            // all 64 factor-row loads are unconditional and independent (a
-            // branch per entry would serialize them on the L2 latency): past
-            // the segment end the row index is clamped to 0 and its product
-            // discarded with the entry
-            double p[32];
-            const int lane_lo = lo ? lane : 0, lane_hi = hi ? lane + 32 : 0;
-#pragma unroll
-            for (int u = 0; u < 32; ++u) {
-                const int c = max(__shfl_sync(0xffffffffu, cl, u), 0);
-                const double* vr = Vs + static_cast<long long>(c) * ldv;
-                p[u] = fma(u1, __ldg(vr + lane_hi), u0 * __ldg(vr + lane_lo));
+            e = e0 + lane;
+            const int cl = cl_n;
+            const double a = a_n, y_old = y_n;
+            const long long en = e + 32;
+            if (en < end) {  // next chunk's stream loads in flight during this chunk
+                cl_n = __ldg(col + en);
+                a_n = __ldg(A + en);
+                y_n = Y[en];
             }
-            // reduce-scatter: after the level of width o, lane l keeps the o
-            // sums of the entries whose index agrees with l on bits >= o
+            double p[KP];
+            if (k > 0) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
+                for (int s = 0; s < KP; ++s) {
+                    const int c = __shfl_sync(0xffffffffu, cl, s * G + g);
+                    const double* vr = Vs + static_cast<long long>(c) * ldv;
+                    p[s] = u0 * __ldg(vr + jl0);
+                    if (TWO) p[s] = fma(u1, __ldg(vr + jl1), p[s]);
+                }
+            } else {  // shrink kept nothing: no factor rows exist
+#pragma unroll
+                for (int s = 0; s < KP; ++s) p[s] = 0.0;
+            }
+#pragma unroll
+            for (int o = KP / 2; o > 0; o >>= 1) {
                 const bool up = (lane & o) != 0;
 #pragma unroll
                 for (int i = 0; i < o; ++i) {
@@ -500,10 +520,8 @@ __global__ void __launch_bounds__(32 * kSddmmWarps) sddmm_update_wide_kernel(
                     p[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
                 }
             }
+            const double pe = __shfl_sync(0xffffffffu, p[0], src);
             if (e < end) {
-                const double pe = p[0];
-                const double a = a_pre;
-                const double y_old = y_pre;
                 const double d = a - pe;
                 s_abs += fabs(d);
                 s_sq = fma(d, d, s_sq);
@@ -965,25 +983,27 @@ void sddmm_update(svt_ctx* ctx, const SegPlanView& plan, i64 m_local, const int*
         const double per = (mode == 1) ? (Ycsc ? 40.0 : 28.0) : 20.0;
         LaunchScope ls(ctx, K_SDDMM, per * nnz + 8.0 * (m_local + 1) + 8.0 * k * (m_local + n), 2.0 * nnz * k);
         double* part = ctx->ws_partial2.get();
-#define SVT_SDDMM(KP)                                                                                       \
-    sddmm_update_kernel<KP><<<blocks, 32 * kSddmmWarps, 0, ctx->stream>>>(plan, col, A, Y, Ycsc, csr2csc,     \
-                                                                         U, ldu, Vs, ldv, k, delta, mode, part)
+#define SVT_SDDMM_W(KP, TWO)                                                                             \
+    sddmm_warp_kernel<KP, TWO><<<blocks, 32 * kSddmmWarps, 0, ctx->stream>>>(                            \
+        plan, col, A, Y, Ycsc, csr2csc, U, ldu, Vs, ldv, static_cast<int>(k), delta, mode, part)
         if (k <= 1)
-            SVT_SDDMM(1);
+            SVT_SDDMM_W(1, false);
         else if (k <= 2)
-            SVT_SDDMM(2);
+            SVT_SDDMM_W(2, false);
         else if (k <= 4)
-            SVT_SDDMM(4);
+            SVT_SDDMM_W(4, false);
         else if (k <= 8)
-            SVT_SDDMM(8);
+            SVT_SDDMM_W(8, false);
         else if (k <= 16)
-            SVT_SDDMM(16);
+            SVT_SDDMM_W(16, false);
+        else if (k <= 32)
+            SVT_SDDMM_W(32, false);
         else if (k <= 64)
-            sddmm_update_wide_kernel<<<blocks, 32 * kSddmmWarps, 0, ctx->stream>>>(
-                plan, col, A, Y, Ycsc, csr2csc, U, ldu, Vs, ldv, static_cast<int>(k), delta, mode, part);
+            SVT_SDDMM_W(32, true);
         else
-            SVT_SDDMM(32);
-#undef SVT_SDDMM
+            sddmm_update_kernel<32><<<blocks, 32 * kSddmmWarps, 0, ctx->stream>>>(plan, col, A, Y, Ycsc, csr2csc,
+                                                                                U, ldu, Vs, ldv, k, delta, mode, part);
+#undef SVT_SDDMM_W
     }
     LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
     reduce4_kernel<<<1, 128, 0, ctx->stream>>>(ctx->ws_partial2.get(), blocks, d_sums4);

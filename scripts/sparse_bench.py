@@ -64,8 +64,13 @@ def main():
                                        C.c_void_p(ot.data_ptr()), C.c_int64(w))
         t, tt = timed(f, st, reps), timed(ft, st, reps)
         ctx.sync()
-        ref = torch.zeros(m, w, dtype=torch.float64, device="cuda").index_add_(0, rows, vals[:, None] * X[cols])
-        reft = torch.zeros(n, w, dtype=torch.float64, device="cuda").index_add_(0, cols, vals[:, None] * Xt[rows])
+        ref = torch.zeros(m, w, dtype=torch.float64, device="cuda")
+        reft = torch.zeros(n, w, dtype=torch.float64, device="cuda")
+        ch = max(1, (1 << 31) // (8 * w))  # entries per chunk (<= 2 GB of gathered rows)
+        for s0 in range(0, nnz, ch):
+            sl = slice(s0, min(nnz, s0 + ch))
+            ref.index_add_(0, rows[sl], vals[sl, None] * X[cols[sl]])
+            reft.index_add_(0, cols[sl], vals[sl, None] * Xt[rows[sl]])
         e = ((o - ref).abs().max() / ref.abs().max()).item()
         et = ((ot - reft).abs().max() / reft.abs().max()).item()
         alg = 12.0 * nnz + 8.0 * (m + 1) + 8.0 * w * (m + n)
@@ -97,12 +102,14 @@ def main():
         L.svt_dev_sddmm_update(A.h, C.c_int64(k), C.c_void_p(U.data_ptr()), C.c_int64(k), C.c_void_p(Vs.data_ptr()),
                                C.c_int64(k), C.c_double(delta), C.c_void_p(Y.data_ptr()), C.c_void_p(Yc.data_ptr()),
                                sums)
-        P = (U[rows] * Vs[cols]).sum(1)
+        P = torch.cat([(U[rows[s0:s0 + (1 << 24)]] * Vs[cols[s0:s0 + (1 << 24)]]).sum(1)
+                       for s0 in range(0, nnz, 1 << 24)])
         dd = A_vals - P
         Yr = Y0 + delta * dd
         e = ((Y - Yr).abs().max() / Yr.abs().max()).item()
         perm = torch.argsort(cols * m + rows)
         ec = (Yc - Yr[perm]).abs().max().item() / Yr.abs().max().item()
+        del perm
         es = abs(sums[1] - float((dd * dd).sum())) / float((dd * dd).sum())
         alg = 48.0 * nnz + 8.0 * (m + 1) + 8.0 * k * (m + n)
         r = {"kernel": "sddmm_update+mirror", "config": cfg, "k": k, "us": round(tm, 1),

@@ -98,3 +98,20 @@ tot_rt = Counter()
 for r0, r1, rn in rt:
     tot_rt[rn] += r1 - r0
 print("runtime call totals:", ", ".join(f"{k} {v/1e3:.1f}ms" for k, v in tot_rt.most_common(10)))
+# per-stream kernel time by name, and how the streams share the span
+byname = {}
+for e in ev:
+    if e.get("cat") == "kernel":
+        s = e.get("args", {}).get("stream")
+        nm = e["name"].split("(")[0].replace("void ", "").replace("svtb::(anonymous namespace)::", "")[:48]
+        d = byname.setdefault(s, {})
+        d[nm] = d.get(nm, 0.0) + e.get("dur", 0)
+for s, d in byname.items():
+    top = sorted(d.items(), key=lambda kv: -kv[1])[:12]
+    print(f"stream {s} top kernels: " + ", ".join(f"{k} {v/1e3:.1f}" for k, v in top))
+if len(ks) >= 2:
+    a, b = streams[ks[0]], streams[ks[1]]
+    ov = inter_len(a, b)
+    ta, tb = sum(y - x for x, y in a), sum(y - x for x, y in b)
+    print(f"span {span/1e3:.1f} ms: only {ks[0]} {(ta-ov)/1e3:.1f}, only {ks[1]} {(tb-ov)/1e3:.1f}, both {ov/1e3:.1f}, "
+          f"idle {(span - (ta + tb - ov))/1e3:.1f}")

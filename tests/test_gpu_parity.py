@@ -846,3 +846,54 @@ def test_grouped_spmm_bitwise_equals_segment_kernel(config, monkeypatch):
                 outs.append(tO.cpu().numpy())
             assert np.array_equal(outs[0], outs[1]), (config, w, tr)
     A.close()
+
+
+@pytest.mark.parametrize("k", [0, 1, 2, 3, 7, 10, 16, 17, 32, 33, 50, 64, 65, 90])
+def test_dev_sddmm_update_matches_fp64_reference(k):
+    """Fused SDDMM + Bregman update (sampled.hpp:148-176, solver.hpp:321-323)
+    through svt_dev_sddmm_update at every kernel variant (warp-group widths
+    1..32, the two-register k <= 64 form, the k > 64 kernel, k = 0): Y' =
+    Y + delta (A - P_Lambda(U Vs^T)) and its CSC mirror against numpy fp64,
+    1e-12 relative; the four sums (|d|, d^2, (A - Y)^2, Y'^2) 1e-12.  Power-law
+    rows (split into several segments) and empty rows are included."""
+    import ctypes as C
+    import torch
+    rng = np.random.default_rng(100 + k)
+    m, n = 700, 450
+    deg = np.minimum(n, (rng.pareto(1.2, m) * 8).astype(np.int64))
+    deg[::37] = 0
+    deg[5] = n  # one full row (> kSegLen entries: several segments)
+    rows = np.repeat(np.arange(m), deg)
+    cols = np.concatenate([np.sort(rng.choice(n, d, replace=False)) for d in deg if d > 0])
+    vals = rng.standard_normal(rows.size)
+    S = O.sampled(m, n, rows, cols, vals)
+    A = gpu_mat(S)
+    nnz = int(S.rowptr[-1])
+    U = rng.standard_normal((m, max(k, 1)))[:, :k]
+    Vs = rng.standard_normal((n, max(k, 1)))[:, :k]
+    Y0 = rng.standard_normal(nnz)
+    delta = 1.7
+    tU = torch.from_numpy(np.ascontiguousarray(U)).cuda()
+    tV = torch.from_numpy(np.ascontiguousarray(Vs)).cuda()
+    tY = torch.from_numpy(Y0.copy()).cuda()
+    tYc = torch.zeros(nnz, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    sums = (C.c_double * 4)()
+    L = G.lib()
+    rc = L.svt_dev_sddmm_update(A.h, C.c_int64(k), C.c_void_p(tU.data_ptr() if k else None), C.c_int64(max(k, 1)),
+                                C.c_void_p(tV.data_ptr() if k else None), C.c_int64(max(k, 1)), C.c_double(delta),
+                                C.c_void_p(tY.data_ptr()), C.c_void_p(tYc.data_ptr()), sums)
+    assert rc == 0
+    r = np.repeat(np.arange(m), np.diff(S.rowptr))
+    c = np.asarray(S.col)
+    P = np.einsum("ij,ij->i", U[r], Vs[c]) if k else np.zeros(nnz)
+    d = np.asarray(S.val) - P
+    Yr = Y0 + delta * d
+    Yg = tY.cpu().numpy()
+    assert np.max(np.abs(Yg - Yr)) <= 1e-12 * np.max(np.abs(Yr))
+    perm = np.lexsort((r, c))  # CSC order: by column, then row
+    assert np.array_equal(tYc.cpu().numpy(), Yg[perm])
+    want = [np.abs(d).sum(), (d * d).sum(), ((np.asarray(S.val) - Y0) ** 2).sum(), (Yr * Yr).sum()]
+    for got, ref in zip(sums, want):
+        assert abs(got - ref) <= 1e-12 * abs(ref), (k, got, ref)
+    A.close()
