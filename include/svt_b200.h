@@ -180,6 +180,13 @@ int svt_matrix_info(svt_mat* mat, int64_t* m, int64_t* n, int64_t* nnz_local, in
                     int64_t* row_end);
 int svt_matrix_set_values(svt_mat* mat, const double* vals);
 int svt_matrix_get_values(svt_mat* mat, double* vals);
+/* The dense-corner split of the sample pattern used by the wide products
+ * (no reference counterpart: a B200 layout of sampled.hpp:113-144's
+ * operand).  Builds it if not tried yet (SVTB_HYBRID=0 disables), then
+ * reports: on (1 when the cost model kept a block), block rows R / columns C,
+ * entries inside the block and outside it. */
+int svt_matrix_hybrid_info(svt_mat* mat, int* on, int64_t* rows, int64_t* cols, int64_t* nnz_block,
+                           int64_t* nnz_cold);
 
 /* ---- formats (io.hpp): readers / writers either side of the path ------ */
 /* Host triplet set: 0-based (row, col, value) in an m x n frame; a ratings

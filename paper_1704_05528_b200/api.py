@@ -376,6 +376,13 @@ class SampledMatrix:
         return SampledMatrix(self.m, self.n, ctx=self.ctx, _csr=(full, co, va),
                              row_block=(self.row_begin, self.row_end))
 
+    def hybrid_info(self):
+        """The dense-corner split the wide products use (svt_matrix_hybrid_info)."""
+        on = C.c_int()
+        r, c, nb, nc = (C.c_int64() for _ in range(4))
+        _check(lib().svt_matrix_hybrid_info(self.h, C.byref(on), C.byref(r), C.byref(c), C.byref(nb), C.byref(nc)))
+        return {"on": bool(on.value), "rows": r.value, "cols": c.value, "nnz_blk": nb.value, "nnz_cold": nc.value}
+
     def row_index(self):
         return np.repeat(np.arange(self.row_begin, self.row_end, dtype=np.int64), np.diff(self.rowptr))
 

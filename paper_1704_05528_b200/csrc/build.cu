@@ -5,6 +5,8 @@
 // csr2csc permutation, the CSC value mirror, and both segment plans of the
 // load-balanced SpMM.  Only the CSR arrays cross PCIe; everything derived
 // from them is built in HBM.
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 #include <cub/cub.cuh>
 
@@ -308,6 +310,106 @@ __global__ void invert_perm_kernel(long long n, const int* __restrict__ fwd, int
 __global__ void iota_kernel(long long n, int* __restrict__ out) {
     const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (p < n) out[p] = static_cast<int>(p);
+}
+
+
+// ---- dense-corner split (HybridPlan) ----------------------------------------
+__global__ void ptr_degree_kernel(long long rows, const long long* __restrict__ ptr, int* __restrict__ deg) {
+    const long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (r < rows) deg[r] = static_cast<int>(ptr[r + 1] - ptr[r]);
+}
+
+__global__ void scatter_rank_kernel(long long n, const int* __restrict__ order, int* __restrict__ rank) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i < n) rank[order[i]] = static_cast<int>(i);
+}
+
+// rank buckets of the cost model: bucket b < kHybB - 1 holds ranks below
+// 256 << b (beyond the previous bucket), the last one the rest
+constexpr int kHybB = 8;
+__device__ __forceinline__ int hyb_bucket(int rank) {
+    int b = 0;
+    while (b < kHybB - 1 && rank >= (256 << b)) ++b;
+    return b;
+}
+
+// entries by (row-rank bucket, column-rank bucket)
+__global__ void hyb_hist_kernel(long long nnz, const int* __restrict__ rid, const int* __restrict__ col,
+                                const int* __restrict__ rrank, const int* __restrict__ crank,
+                                unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int h[kHybB * kHybB];
+    for (int i = threadIdx.x; i < kHybB * kHybB; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < nnz;
+         e += static_cast<long long>(gridDim.x) * blockDim.x)
+        atomicAdd(&h[hyb_bucket(rrank[rid[e]]) * kHybB + hyb_bucket(crank[col[e]])], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kHybB * kHybB; i += blockDim.x)
+        if (h[i]) atomicAdd(hist + i, static_cast<unsigned long long>(h[i]));
+}
+
+__global__ void hyb_flag_kernel(long long nnz, const int* __restrict__ rid, const int* __restrict__ col,
+                                const int* __restrict__ rrank, const int* __restrict__ crank, int R, int C,
+                                int* __restrict__ fl, int* __restrict__ nfl) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= nnz) return;
+    const int f = (rrank[rid[e]] < R && crank[col[e]] < C) ? 1 : 0;
+    fl[e] = f;
+    nfl[e] = 1 - f;
+}
+
+// order-preserving compaction of the CSR entries into block / cold lists
+__global__ void hyb_compact_kernel(long long nnz, const int* __restrict__ fl, const int* __restrict__ bpos,
+                                   const int* __restrict__ cpos, const int* __restrict__ rid,
+                                   const int* __restrict__ col, const int* __restrict__ rrank,
+                                   const int* __restrict__ crank, int C, int* __restrict__ col_c,
+                                   int* __restrict__ map_c, int* __restrict__ blk_map, int* __restrict__ blk_pos) {
+    const long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (e >= nnz) return;
+    if (fl[e]) {
+        const int q = bpos[e];
+        blk_map[q] = static_cast<int>(e);
+        blk_pos[q] = rrank[rid[e]] * C + crank[col[e]];
+    } else {
+        const int p = cpos[e];
+        col_c[p] = col[e];
+        map_c[p] = static_cast<int>(e);
+    }
+}
+
+// pointer array of the compacted pattern: out[i] = pos[ptr[i]] (i <= rows)
+__global__ void hyb_ptr_kernel(long long rows, const long long* __restrict__ ptr, const int* __restrict__ pos,
+                               long long* __restrict__ out) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i <= rows) out[i] = pos[ptr[i]];
+}
+
+__global__ void hyb_flag_csc_kernel(long long nnz, const int* __restrict__ csc2csr, const int* __restrict__ fl,
+                                    int* __restrict__ nflt) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p < nnz) nflt[p] = 1 - fl[csc2csr[p]];
+}
+
+__global__ void hyb_compact_csc_kernel(long long nnz, const int* __restrict__ csc2csr, const int* __restrict__ nflt,
+                                       const int* __restrict__ cpt, const int* __restrict__ cscrow,
+                                       int* __restrict__ row_c, int* __restrict__ mapt_c) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p >= nnz || !nflt[p]) return;
+    const int q = cpt[p];
+    row_c[q] = cscrow[p];
+    mapt_c[q] = csc2csr[p];
+}
+
+__global__ void hyb_gather_vals_kernel(long long n, const int* __restrict__ map, const double* __restrict__ Y,
+                                       double* __restrict__ out) {
+    const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (p < n) out[p] = Y[__ldg(map + p)];
+}
+
+__global__ void hyb_scatter_blk_kernel(long long nb, const int* __restrict__ blk_map, const int* __restrict__ blk_pos,
+                                       const double* __restrict__ Y, double* __restrict__ D) {
+    const long long q = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (q < nb) D[__ldg(blk_pos + q)] = Y[__ldg(blk_map + q)];
 }
 
 inline unsigned nb(long long n, int t = 256) { return static_cast<unsigned>((n + t - 1) / t); }
@@ -720,6 +822,177 @@ void ensure_tile_plans(svt_ctx* ctx, svt_mat* M) {
         build_tile_plan(ctx, reinterpret_cast<const long long*>(M->colptr.get()), M->cscrow.get(), M->n, nnz,
                         M->csc2csr.get(), M->tile_csc);
     }
+}
+
+
+// Dense-corner split (HybridPlan, engine.hpp).  Cost model: a cold entry of
+// a w-wide product costs the gather kernel ~w 8-byte panel loads through the
+// L1 data pipe (its bound, profiles/r02a_ncu_full_spmm_cfg4_w120.txt); a
+// dense block cell costs ~rho of that on the FP64 tensor cores (measured
+// 57.6 ps / entry vs ~8.4 ps / cell at w = 120: rho ~ 0.15), both linear in
+// w, so the block (R, C) that maximises  entries(R, C) - rho R C  is the same
+// at every width.  R and C run over 256, 512, ..., 16384 (rank buckets of
+// the degree orders: rows by local degree, columns by count); the split is
+// kept when it saves at least 5 % of the entries' cost.
+void ensure_hybrid(svt_ctx* ctx, svt_mat* M) {
+    HybridPlan& H = M->hyb;
+    if (H.tried) return;
+    H.tried = true;
+    const char* env = std::getenv("SVTB_HYBRID");
+    if (env != nullptr && env[0] == '0') return;
+    const i64 nnz = M->nnz_local, ml = M->m_local, n = M->n;
+    if (nnz < (1 << 20) || ml < 512 || n < 512 || nnz >= (1LL << 31)) return;
+    const char* rh = std::getenv("SVTB_HYBRID_RHO");
+    const double rho = rh ? std::atof(rh) : 0.15;
+    const bool dbg = std::getenv("SVTB_DEBUG_HYBRID") != nullptr;
+    cudaStream_t s = ctx->stream;
+    DevBuf<unsigned char> tmp;
+    const i64 mx = std::max(ml, n);
+    DevBuf<int> deg(static_cast<size_t>(mx)), sdeg(static_cast<size_t>(mx)), iota(static_cast<size_t>(mx));
+    DevBuf<int> rorder(static_cast<size_t>(ml)), corder(static_cast<size_t>(n));
+    DevBuf<int> rrank(static_cast<size_t>(ml)), crank(static_cast<size_t>(n));
+    auto order_of = [&](const long long* ptr, i64 rows, int* order, int* rank) {
+        ptr_degree_kernel<<<nb(rows), 256, 0, s>>>(rows, ptr, deg.get());
+        iota_kernel<<<nb(rows), 256, 0, s>>>(rows, iota.get());
+        size_t bytes = 0;
+        SVT_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, deg.get(), sdeg.get(), iota.get(), order,
+                                                           static_cast<int>(rows), 0, 32, s));
+        tmp.ensure(bytes);
+        SVT_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp.get(), bytes, deg.get(), sdeg.get(), iota.get(), order,
+                                                           static_cast<int>(rows), 0, 32, s));
+        scatter_rank_kernel<<<nb(rows), 256, 0, s>>>(rows, order, rank);
+    };
+    const long long* rp = reinterpret_cast<const long long*>(M->rowptr.get());
+    const long long* cp = reinterpret_cast<const long long*>(M->colptr.get());
+    {
+        LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
+        order_of(rp, ml, rorder.get(), rrank.get());
+        order_of(cp, n, corder.get(), crank.get());
+    }
+    DevBuf<int> rid(static_cast<size_t>(nnz));
+    DevBuf<unsigned long long> hist(kHybB * kHybB);
+    SVT_CUDA(cudaMemsetAsync(hist.get(), 0, sizeof(unsigned long long) * kHybB * kHybB, s));
+    {
+        LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
+        row_ids_kernel<<<nb(ml * 32), 256, 0, s>>>(ml, rp, rid.get());
+        hyb_hist_kernel<<<ctx->num_sms * 4, 256, 0, s>>>(nnz, rid.get(), M->col.get(), rrank.get(), crank.get(),
+                                                         hist.get());
+    }
+    unsigned long long h[kHybB * kHybB];
+    SVT_CUDA(cudaMemcpyAsync(h, hist.get(), sizeof(h), cudaMemcpyDeviceToHost, s));
+    sync_stream(ctx);
+    double best = 0.0;
+    i64 R = 0, C = 0, E = 0;
+    for (int a = 0; a < kHybB - 1; ++a) {
+        for (int b = 0; b < kHybB - 1; ++b) {
+            // C even: the dense block's rows are cp.async operands (16-byte rows)
+            const i64 r = std::min<i64>(256LL << a, ml), c = std::min<i64>(256LL << b, n) & ~1LL;
+            if (8.0 * static_cast<double>(r) * static_cast<double>(c) > 512e6) continue;
+            i64 e = 0;
+            for (int i = 0; i <= a; ++i)
+                for (int j = 0; j <= b; ++j) e += static_cast<i64>(h[i * kHybB + j]);
+            const double saved = static_cast<double>(e) - rho * static_cast<double>(r) * static_cast<double>(c);
+            if (saved > best) {
+                best = saved;
+                R = r;
+                C = c;
+                E = e;
+            }
+        }
+    }
+    if (dbg)
+        std::fprintf(stderr, "[hybrid] nnz=%lld best R=%lld C=%lld block entries=%lld (%.1f%%, density %.3f) saved %.1f%%\n",
+                     static_cast<long long>(nnz), static_cast<long long>(R), static_cast<long long>(C),
+                     static_cast<long long>(E), 100.0 * E / nnz, R * C > 0 ? static_cast<double>(E) / (R * C) : 0.0,
+                     100.0 * best / nnz);
+    if (best < 0.05 * static_cast<double>(nnz)) return;
+    H.R = R;
+    H.C = C;
+    // flags and the two order-preserving compactions of the CSR entries
+    DevBuf<int> fl(static_cast<size_t>(nnz) + 1), nfl(static_cast<size_t>(nnz) + 1);
+    DevBuf<int> bpos(static_cast<size_t>(nnz) + 1), cpos(static_cast<size_t>(nnz) + 1);
+    {
+        LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
+        hyb_flag_kernel<<<nb(nnz), 256, 0, s>>>(nnz, rid.get(), M->col.get(), rrank.get(), crank.get(),
+                                               static_cast<int>(R), static_cast<int>(C), fl.get(), nfl.get());
+    }
+    exclusive_scan(ctx, fl.get(), bpos.get(), nnz, tmp);
+    exclusive_scan(ctx, nfl.get(), cpos.get(), nnz, tmp);
+    int tots[2];
+    SVT_CUDA(cudaMemcpyAsync(&tots[0], bpos.get() + nnz, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SVT_CUDA(cudaMemcpyAsync(&tots[1], cpos.get() + nnz, sizeof(int), cudaMemcpyDeviceToHost, s));
+    sync_stream(ctx);
+    H.nnz_blk = tots[0];
+    H.nnz_cold = tots[1];
+    const size_t ncold = static_cast<size_t>(std::max<i64>(1, H.nnz_cold));
+    const size_t nblk = static_cast<size_t>(std::max<i64>(1, H.nnz_blk));
+    H.col_c.alloc(ncold);
+    H.map_c.alloc(ncold);
+    H.val_c.alloc(ncold);
+    H.row_c.alloc(ncold);
+    H.mapt_c.alloc(ncold);
+    H.valt_c.alloc(ncold);
+    H.blk_map.alloc(nblk);
+    H.blk_pos.alloc(nblk);
+    H.rowptr_c.alloc(static_cast<size_t>(ml + 1));
+    H.colptr_c.alloc(static_cast<size_t>(n + 1));
+    H.hot_rows.alloc(static_cast<size_t>(R));
+    H.hot_cols.alloc(static_cast<size_t>(C));
+    H.D.alloc(static_cast<size_t>(R * C));
+    SVT_CUDA(cudaMemsetAsync(H.D.get(), 0, sizeof(double) * static_cast<size_t>(R * C), s));
+    SVT_CUDA(cudaMemcpyAsync(H.hot_rows.get(), rorder.get(), sizeof(int) * R, cudaMemcpyDeviceToDevice, s));
+    SVT_CUDA(cudaMemcpyAsync(H.hot_cols.get(), corder.get(), sizeof(int) * C, cudaMemcpyDeviceToDevice, s));
+    {
+        LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
+        hyb_compact_kernel<<<nb(nnz), 256, 0, s>>>(nnz, fl.get(), bpos.get(), cpos.get(), rid.get(), M->col.get(),
+                                                  rrank.get(), crank.get(), static_cast<int>(C), H.col_c.get(),
+                                                  H.map_c.get(), H.blk_map.get(), H.blk_pos.get());
+        hyb_ptr_kernel<<<nb(ml + 1), 256, 0, s>>>(ml, rp, cpos.get(),
+                                                 reinterpret_cast<long long*>(H.rowptr_c.get()));
+    }
+    // the cold CSC view: CSC positions whose CSR entry is cold, in CSC order
+    if (M->csc2csr.n < static_cast<size_t>(nnz)) {
+        M->csc2csr.alloc(static_cast<size_t>(nnz));
+        invert_perm_kernel<<<nb(nnz), 256, 0, s>>>(nnz, M->csr2csc.get(), M->csc2csr.get());
+    }
+    {
+        LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
+        hyb_flag_csc_kernel<<<nb(nnz), 256, 0, s>>>(nnz, M->csc2csr.get(), fl.get(), nfl.get());
+    }
+    exclusive_scan(ctx, nfl.get(), cpos.get(), nnz, tmp);
+    {
+        LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
+        hyb_compact_csc_kernel<<<nb(nnz), 256, 0, s>>>(nnz, M->csc2csr.get(), nfl.get(), cpos.get(), M->cscrow.get(),
+                                                      H.row_c.get(), H.mapt_c.get());
+        hyb_ptr_kernel<<<nb(n + 1), 256, 0, s>>>(n, cp, cpos.get(), reinterpret_cast<long long*>(H.colptr_c.get()));
+    }
+    build_plan_device(ctx, reinterpret_cast<const long long*>(H.rowptr_c.get()), ml, H.plan_c);
+    build_plan_device(ctx, reinterpret_cast<const long long*>(H.colptr_c.get()), n, H.plant_c);
+    // split-K partials of the block product, per stream: sized for panels up
+    // to 128 wide and 8 K-splits (wider calls grow them once)
+    const size_t wsn = static_cast<size_t>(8 * std::max(R, C) * 128);
+    H.ws[0].alloc(wsn);
+    H.ws[1].alloc(wsn);
+    sync_stream(ctx);  // the temporaries die here
+    H.src = nullptr;
+    H.on = true;
+}
+
+// Mirror a CSR value array into the cold CSR / CSC values and the dense block
+// (12 + 12 B per cold entry, 16 B per block entry).
+void hybrid_refresh(svt_ctx* ctx, svt_mat* M, const double* Ycsr) {
+    HybridPlan& H = M->hyb;
+    if (!H.on) return;
+    cudaStream_t s = ctx->stream;
+    LaunchScope ls(ctx, K_OTHER, 24.0 * H.nnz_cold + 16.0 * H.nnz_blk, 0.0);
+    if (H.nnz_cold > 0) {
+        hyb_gather_vals_kernel<<<nb(H.nnz_cold), 256, 0, s>>>(H.nnz_cold, H.map_c.get(), Ycsr, H.val_c.get());
+        hyb_gather_vals_kernel<<<nb(H.nnz_cold), 256, 0, s>>>(H.nnz_cold, H.mapt_c.get(), Ycsr, H.valt_c.get());
+    }
+    if (H.nnz_blk > 0)
+        hyb_scatter_blk_kernel<<<nb(H.nnz_blk), 256, 0, s>>>(H.nnz_blk, H.blk_map.get(), H.blk_pos.get(), Ycsr,
+                                                             H.D.get());
+    H.src = Ycsr;
 }
 
 }  // namespace svtb

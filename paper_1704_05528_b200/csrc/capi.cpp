@@ -203,6 +203,11 @@ int svt_ctx_destroy(svt_ctx* ctx) {
         if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
         cudaStreamDestroy(ctx->stream);
         if (ctx->side) cudaStreamDestroy(ctx->side);
+        for (int k = 0; k < 2; ++k) {
+            if (ctx->aux[k]) cudaStreamDestroy(ctx->aux[k]);
+            if (ctx->aux_fork[k]) cudaEventDestroy(ctx->aux_fork[k]);
+            if (ctx->aux_join[k]) cudaEventDestroy(ctx->aux_join[k]);
+        }
         delete ctx;
     });
 }
@@ -563,6 +568,20 @@ int svt_matrix_info(svt_mat* M, int64_t* m, int64_t* n, int64_t* nnz_local, int6
     });
 }
 
+int svt_matrix_hybrid_info(svt_mat* M, int* on, int64_t* rows, int64_t* cols, int64_t* nnz_block,
+                           int64_t* nnz_cold) {
+    return guard([&] {
+        need(M, "svt_matrix_hybrid_info");
+        ensure_hybrid(M->ctx, M);
+        const HybridPlan& H = M->hyb;
+        if (on) *on = H.on ? 1 : 0;
+        if (rows) *rows = H.R;
+        if (cols) *cols = H.C;
+        if (nnz_block) *nnz_block = H.nnz_blk;
+        if (nnz_cold) *nnz_cold = H.nnz_cold;
+    });
+}
+
 int svt_matrix_set_values(svt_mat* M, const double* vals) {
     return guard([&] {
         need(M, "svt_matrix_set_values");
@@ -573,6 +592,7 @@ int svt_matrix_set_values(svt_mat* M, const double* vals) {
         svt_ctx* c = M->ctx;
         SVT_CUDA(cudaMemcpyAsync(M->val.get(), vals, sizeof(double) * M->nnz_local, cudaMemcpyHostToDevice, c->stream));
         scale_values(c, M->nnz_local, M->val.get(), 1.0, M->val.get(), M->csr2csc.get(), M->val_csc.get());
+        M->val_version++;
         sync_stream(c);
     });
 }

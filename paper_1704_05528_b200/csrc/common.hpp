@@ -229,6 +229,11 @@ struct svt_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // side stream: Omega prefetch for the next round batch
+    // helper streams of the main / side stream: the dense corner of a split
+    // SpMM runs on the tensor cores concurrently with the gather kernel of the
+    // cold entries (forked and joined inside the product)
+    cudaStream_t aux[2] = {nullptr, nullptr};
+    cudaEvent_t aux_fork[2] = {nullptr, nullptr}, aux_join[2] = {nullptr, nullptr};
     int num_sms = 148;
     svtb::Comm comm;
     void* cusolver = nullptr;  // cusolverDnHandle_t

@@ -342,12 +342,17 @@ struct CpTile {
     static constexpr size_t SMEM = sizeof(double) * kCpStages * (A_ELEMS + B_ELEMS);
 };
 
-template <int BN, bool TA>
+// GS (dense corner of a split sparse pattern, engine.cpp): row k of B is row
+// brow[k] of the panel (a gather folded into the cp.async B loads) and every
+// CTA writes its split-K partial tile (the caller's fixed-order reduction
+// scatter-adds the block rows into the sparse product's output).
+template <int BN, bool TA, bool GS = false>
 __global__ void __launch_bounds__(256, 2) dmma_cp_kernel(long long M, long long N, long long K, double alpha,
                                                          const double* __restrict__ A, long long lda,
                                                          const double* __restrict__ B, long long ldb, double beta,
                                                          double* __restrict__ C, long long ldc, long long kchunk,
-                                                         double* __restrict__ partial, const int* __restrict__ pred) {
+                                                         double* __restrict__ partial, const int* __restrict__ pred,
+                                                         const int* __restrict__ brow = nullptr) {
     if (pred != nullptr && *pred == 0) return;
     using T = CpTile<BN, TA>;
     constexpr int BM = T::BM, BK = T::BK, SA = T::SA, SAR = T::SAR, SB = T::SB;
@@ -390,7 +395,8 @@ __global__ void __launch_bounds__(256, 2) dmma_cp_kernel(long long M, long long 
             const int kk = c / (BN / 2), jj = (c % (BN / 2)) * 2;
             const long long k = k0 + kk, j = j0 + jj;
             const int v = (k < kend) ? static_cast<int>(max(0LL, min(2LL, N - j))) : 0;
-            cp_async16(bs + kk * SB + jj, v ? B + k * ldb + j : B, 8 * v);
+            const long long kr = (GS && v) ? static_cast<long long>(__ldg(brow + k)) : k;
+            cp_async16(bs + kk * SB + jj, v ? B + kr * ldb + j : B, 8 * v);
         }
     };
     double acc[4][NT][2];
@@ -437,7 +443,7 @@ __global__ void __launch_bounds__(256, 2) dmma_cp_kernel(long long M, long long 
             for (int h = 0; h < 2; ++h) {
                 const long long j = j0 + wn + b * 8 + 2 * t + h;
                 if (j >= N) continue;
-                if (gridDim.z == 1) {
+                if (gridDim.z == 1 && !GS) {
                     const double o = (beta != 0.0) ? beta * C[i * ldc + j] : 0.0;
                     C[i * ldc + j] = fma(alpha, acc[a][b][h], o);
                 } else {
@@ -522,6 +528,42 @@ void dmma_launch(svt_ctx* ctx, bool transA, i64 M, i64 N, i64 K, double alpha, c
         gemm_reduce_kernel<<<static_cast<unsigned>((tot + 31) / 32), 32 * kRedWarps, 0, ctx->stream>>>(
             M, N, static_cast<int>(splits), ctx->ws_partial.get(), alpha, beta, C, ldc, pred);
     }
+}
+
+// out[orow[i] * ldo + j] += sum_z partial[z][i][j]  (fixed order: deterministic)
+__global__ void block_scatter_add_kernel(long long M, long long N, int S, const double* __restrict__ partial,
+                                         const int* __restrict__ orow, double* __restrict__ out, long long ldo) {
+    const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (t >= M * N) return;
+    const long long i = t / N, j = t - i * N;
+    double acc = 0.0;
+    for (int z = 0; z < S; ++z) acc += partial[(static_cast<long long>(z) * M + i) * N + j];
+    out[static_cast<long long>(__ldg(orow + i)) * ldo + j] += acc;
+}
+
+template <int BN, bool TA>
+int dense_block_launch(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, const double* D, i64 ldd,
+                       const double* B, i64 ldb, const int* brow, DevBuf<double>& ws) {
+    static bool attr = false;
+    if (!attr) {
+        SVT_CUDA(cudaFuncSetAttribute(dmma_cp_kernel<BN, TA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(CpTile<BN, TA>::SMEM)));
+        attr = true;
+    }
+    const i64 mt = (M + kDmmaBM - 1) / kDmmaBM, nt = (N + BN - 1) / BN, tiles = mt * nt;
+    // K splits: as many as fill ONE wave of two resident CTAs per SM (a
+    // second, nearly empty wave would double the time), at least 16 k-steps
+    // per CTA
+    i64 S = std::max<i64>(1, std::min<i64>((2 * ctx->num_sms) / tiles, K / (16 * kCpBK)));
+    if (ws.n < static_cast<size_t>(M * N)) ws.ensure(static_cast<size_t>(M * N * S));  // one-time growth
+    S = std::max<i64>(1, std::min<i64>(S, static_cast<i64>(ws.n / static_cast<size_t>(M * N))));
+    i64 kchunk = (K + S - 1) / S;
+    kchunk = ((kchunk + kCpBK - 1) / kCpBK) * kCpBK;
+    S = (K + kchunk - 1) / kchunk;
+    dim3 grid(static_cast<unsigned>(mt), static_cast<unsigned>(nt), static_cast<unsigned>(S));
+    dmma_cp_kernel<BN, TA, true><<<grid, 256, CpTile<BN, TA>::SMEM, s>>>(M, N, K, 1.0, D, ldd, B, ldb, 0.0, nullptr,
+                                                                        0, kchunk, ws.get(), nullptr, brow);
+    return static_cast<int>(S);
 }
 
 template <int BM, int BN, int BK, int TM, int TN>
@@ -2044,6 +2086,41 @@ inline unsigned nblk(i64 n, int bs = 256) { return static_cast<unsigned>(std::ma
 }  // namespace
 
 // ---------------------------------------------------------------------------
+// Dense corner of a split sparse product (engine.cpp), in two launches so the
+// tensor-core part can run on a helper stream while the gather kernel of the
+// cold entries runs on the caller's: dense_block_mm computes the split-K
+// partials of op(D) B[brow, :] (M x N; D the R x C dense block, op =
+// transpose for Y^T X; the B-row gather folded into the cp.async loads) into
+// ws on stream s and returns the split count; dense_block_add then adds
+// their fixed-order sum into out[orow[i], :] (deterministic).  alg_bytes /
+// alg_flops: the algorithmic cost of the sparse entries the block stands for
+// (the SpMM roofline's accounting).  Operands must be 16-byte aligned rows
+// (returns 0 otherwise, nothing launched).
+int dense_block_mm(svt_ctx* ctx, cudaStream_t s, int cls, bool transA, i64 M, i64 N, i64 K, const double* D,
+                   i64 ldd, const double* B, i64 ldb, const int* brow, DevBuf<double>& ws, double alg_bytes,
+                   double alg_flops) {
+    if (M <= 0 || N <= 0 || K <= 0) return 0;
+    if ((ldb % 2) != 0 || (ldd % 2) != 0 || (reinterpret_cast<uintptr_t>(B) % 16) != 0 ||
+        (reinterpret_cast<uintptr_t>(D) % 16) != 0)
+        return 0;
+    LaunchScope ls(ctx, cls, alg_bytes, alg_flops, s);
+#define SVT_DB(BN_)                                                                                   \
+    return transA ? dense_block_launch<BN_, true>(ctx, s, M, N, K, D, ldd, B, ldb, brow, ws)         \
+                  : dense_block_launch<BN_, false>(ctx, s, M, N, K, D, ldd, B, ldb, brow, ws)
+    if (N <= 32) SVT_DB(32);
+    if (N <= 64) SVT_DB(64);
+    SVT_DB(128);
+#undef SVT_DB
+}
+
+void dense_block_add(svt_ctx* ctx, cudaStream_t s, int cls, i64 M, i64 N, int S, const DevBuf<double>& ws,
+                     const int* orow, double* out, i64 ldo) {
+    if (M <= 0 || N <= 0 || S <= 0) return;
+    LaunchScope ls(ctx, cls, 0.0, 0.0, s);
+    block_scatter_add_kernel<<<static_cast<unsigned>((M * N + 255) / 256), 256, 0, s>>>(M, N, S, ws.get(), orow, out,
+                                                                                       ldo);
+}
+
 void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
           const double* B, i64 ldb, double beta, double* C, i64 ldc, const int* pred) {
     if (M <= 0 || N <= 0) return;

@@ -255,13 +255,84 @@ static bool tiles_ready(Engine& E, i64 w, cudaStream_t stream) {
 
 void prepare_tiles(Engine& E) {
     E.tiles_fresh = false;
+    E.hyb_fresh = false;
     E.tiled = tile_spmm_enabled();
     tiles_ready(E, 32, nullptr);
+}
+
+// The dense-corner split of Y (HybridPlan) for wide panels: built on the
+// first wide product (main stream), its values mirrored from Y.csr once per
+// sketch; side-stream products use it only once it is fresh (they follow the
+// main stream's refresh through the batch events).  The block product's
+// operands must be 16-byte aligned rows.
+constexpr i64 kHybMinW = 24;
+static bool hybrid_ready(Engine& E, i64 w, const double* X, i64 ldx, cudaStream_t stream) {
+    svt_mat* A = E.mat;
+    if (w < kHybMinW || A->nnz_local <= 0 || E.Y.csr == nullptr) return false;
+    const bool main = stream == nullptr || stream == E.ctx->stream;
+    if (!A->hyb.tried) {
+        if (!main) return false;
+        ensure_hybrid(E.ctx, A);
+    }
+    HybridPlan& H = A->hyb;
+    if (!H.on) return false;
+    // fresh: mirrored during this sketch, or the engine works on the
+    // matrix's own values and they have not been rewritten since
+    const bool own = E.Y.csr == A->val.get();
+    const bool fresh = (E.hyb_fresh && H.src == E.Y.csr) ||
+                       (own && H.src == E.Y.csr && H.src_version == A->val_version);
+    if (!fresh) {
+        if (!main) return false;
+        hybrid_refresh(E.ctx, A, E.Y.csr);
+        H.src_version = own ? A->val_version : -1;
+        E.hyb_fresh = true;
+    }
+    return (ldx % 2 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
+}
+
+
+// Y X (tr = false) or Y^T X (tr = true) through the split: the dense block's
+// split-K product on the helper stream of `stream` (forked after everything
+// already queued there), the cold entries' gather kernel on `stream`
+// meanwhile, then the block rows added into the output after the join.
+template <typename Cold>
+static void split_product(Engine& E, int cls, bool tr, i64 w, const double* X, i64 ldx, double* out, i64 ldo,
+                          cudaStream_t stream, Cold&& cold) {
+    svt_ctx* c = E.ctx;
+    HybridPlan& H = E.mat->hyb;
+    cudaStream_t s = stream ? stream : c->stream;
+    const int k = (s == c->side) ? 1 : 0;
+    if (c->aux[k] == nullptr) {
+        int prio = 0;
+        SVT_CUDA(cudaStreamGetPriority(s, &prio));
+        SVT_CUDA(cudaStreamCreateWithPriority(&c->aux[k], cudaStreamNonBlocking, prio));
+        SVT_CUDA(cudaEventCreateWithFlags(&c->aux_fork[k], cudaEventDisableTiming));
+        SVT_CUDA(cudaEventCreateWithFlags(&c->aux_join[k], cudaEventDisableTiming));
+    }
+    SVT_CUDA(cudaEventRecord(c->aux_fork[k], s));
+    SVT_CUDA(cudaStreamWaitEvent(c->aux[k], c->aux_fork[k], 0));
+    const i64 M = tr ? H.C : H.R, K = tr ? H.R : H.C;
+    const int S = dense_block_mm(c, c->aux[k], cls, tr, M, w, K, H.D.get(), H.C, X, ldx,
+                                 tr ? H.hot_rows.get() : H.hot_cols.get(), H.ws[k], 12.0 * H.nnz_blk,
+                                 2.0 * H.nnz_blk * w);
+    SVT_CUDA(cudaEventRecord(c->aux_join[k], c->aux[k]));
+    if (S == 0) throw std::logic_error("split SpMM: dense block operands not aligned");
+    cold();
+    SVT_CUDA(cudaStreamWaitEvent(s, c->aux_join[k], 0));
+    dense_block_add(c, s, cls, M, w, S, H.ws[k], tr ? H.hot_cols.get() : H.hot_rows.get(), out, ldo);
 }
 
 void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo, cudaStream_t stream,
              DevBuf<double>* scratch) {
     svt_mat* A = E.mat;
+    if (hybrid_ready(E, w, X, ldx, stream)) {
+        HybridPlan& H = A->hyb;
+        split_product(E, K_SPMM, false, w, X, ldx, out, ldo, stream, [&] {
+            spmm(E.ctx, K_SPMM, H.plan_c.v, A->m_local, H.col_c.get(), H.val_c.get(), H.nnz_cold, A->n, w, X, ldx,
+                 out, ldo, stream, scratch);
+        });
+        return;
+    }
     if (tiles_ready(E, w, stream) &&
         spmm_tiled(E.ctx, K_SPMM, A->tile_csr.v, A->n, w, X, ldx, out, ldo, stream, scratch))
         return;
@@ -274,10 +345,17 @@ void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out, cudaStre
     svt_mat* A = E.mat;
     if (ldo < 0) ldo = w;
     if (ldo != w && E.ctx->comm.world > 1) throw std::logic_error("sp_mult_t: strided output needs one rank");
-    if (!(tiles_ready(E, w, stream) &&
-          spmm_tiled(E.ctx, K_SPMMT, A->tile_csc.v, A->m_local, w, X, ldx, out, ldo, stream, scratch)))
+    if (hybrid_ready(E, w, X, ldx, stream)) {
+        HybridPlan& H = A->hyb;
+        split_product(E, K_SPMMT, true, w, X, ldx, out, ldo, stream, [&] {
+            spmm(E.ctx, K_SPMMT, H.plant_c.v, A->n, H.row_c.get(), H.valt_c.get(), H.nnz_cold, A->m_local, w, X,
+                 ldx, out, ldo, stream, scratch);
+        });
+    } else if (!(tiles_ready(E, w, stream) &&
+                 spmm_tiled(E.ctx, K_SPMMT, A->tile_csc.v, A->m_local, w, X, ldx, out, ldo, stream, scratch))) {
         spmm(E.ctx, K_SPMMT, A->plan_csc.v, A->n, A->cscrow.get(), E.Y.csc, A->nnz_local, A->m_local, w, X, ldx, out,
              ldo, stream, scratch);
+    }
     E.ctx->comm.allreduce_sum(out, static_cast<size_t>(A->n * w), stream ? stream : E.ctx->stream,
                               stream != nullptr && stream == E.ctx->side);
 }

@@ -30,12 +30,37 @@ struct TilePlan {
     bool built = false;
 };
 
+// Dense-corner split of a power-law sample pattern for the wide products
+// (build.cu builds it, engine.cpp uses it).  Power-law users and Zipf items
+// concentrate a large share of the entries in the block of the R
+// highest-degree local rows x the C highest-degree columns (config 4:
+// 4096 x 2048 holds 37 % of the entries at 40 % density).  That block is held
+// DENSE (R x C, row-major) and multiplied on the FP64 tensor cores; the other
+// ("cold") entries keep the gather kernels through their own CSR / CSC views
+// and segment plans.  Y's values are mirrored into the cold arrays and the
+// block once per sketch (`src` = the CSR value array mirrored).
+struct HybridPlan {
+    bool tried = false, on = false;
+    svtb::i64 R = 0, C = 0, nnz_cold = 0, nnz_blk = 0;
+    svtb::DevBuf<int> hot_rows, hot_cols;  // block row r -> local row, block column c -> column
+    svtb::DevBuf<int> blk_map, blk_pos;    // block entries: CSR position, r * C + c
+    svtb::DevBuf<svtb::i64> rowptr_c, colptr_c;
+    svtb::DevBuf<int> col_c, row_c;        // cold CSR columns / cold CSC local rows
+    svtb::DevBuf<int> map_c, mapt_c;       // their CSR positions (value source)
+    svtb::DevBuf<double> val_c, valt_c, D;
+    SegPlan plan_c, plant_c;
+    const double* src = nullptr;
+    long long src_version = -1;  // the matrix's own values: their version when mirrored
+    svtb::DevBuf<double> ws[2];  // split-K partials of the block product (main / side stream)
+};
+
 // Device SampledMatrix (sampled.hpp:25-110): this rank's row block as CSR
 // (int64 rowptr, int32 col, fp64 val) plus a CSC view whose value array
 // mirrors the CSR values through csr2csc.
 struct svt_mat {
     SegPlan plan_csr, plan_csc;
     TilePlan tile_csr, tile_csc;  // shared-memory-tiled views for wide panels
+    HybridPlan hyb;               // dense-corner split (wide panels, power-law patterns)
     svt_ctx* ctx = nullptr;
     svtb::i64 m = 0, n = 0, row_begin = 0, row_end = 0, m_local = 0, nnz_local = 0, nnz_global = 0;
     svtb::DevBuf<svtb::i64> rowptr;
@@ -46,6 +71,7 @@ struct svt_mat {
     svtb::DevBuf<double> val_csc;
     svtb::DevBuf<int> csr2csc;
     svtb::DevBuf<int> csc2csr;  // inverse permutation (CSC position -> CSR entry)
+    long long val_version = 0;  // bumped whenever val is rewritten (svt_matrix_set_values)
 };
 
 namespace svtb {
@@ -122,6 +148,7 @@ struct Engine {
     DevFactors fpool;          // factor buffers handed back by the solver for the next sketch
     bool tiled = false;        // shared-memory-tiled SpMM for wide panels (opt-in, per sketch)
     bool tiles_fresh = false;  // the tiled views mirror Y (cleared at every sketch entry)
+    bool hyb_fresh = false;    // the dense-corner split mirrors Y (cleared at every sketch entry)
     Engine(svt_ctx* c, svt_mat* m, Vals y) : ctx(c), mat(m), Y(y), batching(c->batching != 0) {}
     Engine(const Engine&) = delete;
     Engine& operator=(const Engine&) = delete;
@@ -172,6 +199,11 @@ int build_sampled_device(svt_ctx* ctx, svt_mat* M, const long long* col64);
 void build_tile_plan(svt_ctx* ctx, const long long* ptr, const int* idx, i64 rows, i64 nnz, const int* map,
                      TilePlan& P);
 void ensure_tile_plans(svt_ctx* ctx, svt_mat* M);
+// build.cu: the dense-corner split of M (once; M->hyb.on says whether the
+// cost model found a block worth splitting off), and the per-sketch value
+// mirror from a CSR value array
+void ensure_hybrid(svt_ctx* ctx, svt_mat* M);
+void hybrid_refresh(svt_ctx* ctx, svt_mat* M, const double* Ycsr);
 void build_from_triplets_device(svt_ctx* ctx, svt_mat* M, i64 nnz, const i64* rows, const i64* cols,
                                 const double* vals);
 

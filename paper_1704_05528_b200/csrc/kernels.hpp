@@ -85,6 +85,15 @@ void gemm_tn_ozaki_cached(svt_ctx* ctx, i64 M, i64 N, i64 K, const int8_t* tiles
 // reduction.  pred (device int, may be null): skip entirely when *pred == 0.
 void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
           const double* B, i64 ldb, double beta, double* C, i64 ldc, const int* pred = nullptr);
+// Dense corner of a split sparse product: split-K partials of op(D) B[brow, :]
+// on the FP64 tensor cores into ws on stream s (returns the split count, 0 =
+// operands not 16-byte aligned, nothing launched); dense_block_add adds their
+// fixed-order sum into out[orow[i], :].
+int dense_block_mm(svt_ctx* ctx, cudaStream_t s, int cls, bool transA, i64 M, i64 N, i64 K, const double* D,
+                   i64 ldd, const double* B, i64 ldb, const int* brow, DevBuf<double>& ws, double alg_bytes,
+                   double alg_flops);
+void dense_block_add(svt_ctx* ctx, cudaStream_t s, int cls, i64 M, i64 N, int S, const DevBuf<double>& ws,
+                     const int* orow, double* out, i64 ldo);
 
 // Fused Cholesky-QR pass head for a narrow panel (w <= 16, single rank):
 // G = X^T X reduced on the device, then Cholesky and Rinv = L^{-T} in the
