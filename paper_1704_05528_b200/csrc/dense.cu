@@ -325,6 +325,10 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int byt
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
 }
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int bytes) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -346,7 +350,7 @@ struct CpTile {
 // brow[k] of the panel (a gather folded into the cp.async B loads) and every
 // CTA writes its split-K partial tile (the caller's fixed-order reduction
 // scatter-adds the block rows into the sparse product's output).
-template <int BN, bool TA, bool GS = false>
+template <int BN, bool TA, bool GS = false, bool B8 = false>
 __global__ void __launch_bounds__(256, 2) dmma_cp_kernel(long long M, long long N, long long K, double alpha,
                                                          const double* __restrict__ A, long long lda,
                                                          const double* __restrict__ B, long long ldb, double beta,
@@ -396,7 +400,12 @@ __global__ void __launch_bounds__(256, 2) dmma_cp_kernel(long long M, long long 
             const long long k = k0 + kk, j = j0 + jj;
             const int v = (k < kend) ? static_cast<int>(max(0LL, min(2LL, N - j))) : 0;
             const long long kr = (GS && v) ? static_cast<long long>(__ldg(brow + k)) : k;
-            cp_async16(bs + kk * SB + jj, v ? B + kr * ldb + j : B, 8 * v);
+            if (B8) {  // B rows not 16-byte aligned (a panel at an odd column offset)
+                cp_async8(bs + kk * SB + jj, v >= 1 ? B + kr * ldb + j : B, v >= 1 ? 8 : 0);
+                cp_async8(bs + kk * SB + jj + 1, v >= 2 ? B + kr * ldb + j + 1 : B, v >= 2 ? 8 : 0);
+            } else {
+                cp_async16(bs + kk * SB + jj, v ? B + kr * ldb + j : B, 8 * v);
+            }
         }
     };
     double acc[4][NT][2];
@@ -541,12 +550,12 @@ __global__ void block_scatter_add_kernel(long long M, long long N, int S, const 
     out[static_cast<long long>(__ldg(orow + i)) * ldo + j] += acc;
 }
 
-template <int BN, bool TA>
+template <int BN, bool TA, bool B8>
 int dense_block_launch(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, const double* D, i64 ldd,
                        const double* B, i64 ldb, const int* brow, DevBuf<double>& ws) {
     static bool attr = false;
     if (!attr) {
-        SVT_CUDA(cudaFuncSetAttribute(dmma_cp_kernel<BN, TA, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        SVT_CUDA(cudaFuncSetAttribute(dmma_cp_kernel<BN, TA, true, B8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(CpTile<BN, TA>::SMEM)));
         attr = true;
     }
@@ -561,8 +570,9 @@ int dense_block_launch(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, const 
     kchunk = ((kchunk + kCpBK - 1) / kCpBK) * kCpBK;
     S = (K + kchunk - 1) / kchunk;
     dim3 grid(static_cast<unsigned>(mt), static_cast<unsigned>(nt), static_cast<unsigned>(S));
-    dmma_cp_kernel<BN, TA, true><<<grid, 256, CpTile<BN, TA>::SMEM, s>>>(M, N, K, 1.0, D, ldd, B, ldb, 0.0, nullptr,
-                                                                        0, kchunk, ws.get(), nullptr, brow);
+    dmma_cp_kernel<BN, TA, true, B8><<<grid, 256, CpTile<BN, TA>::SMEM, s>>>(M, N, K, 1.0, D, ldd, B, ldb, 0.0,
+                                                                            nullptr, 0, kchunk, ws.get(), nullptr,
+                                                                            brow);
     return static_cast<int>(S);
 }
 
@@ -2100,13 +2110,16 @@ int dense_block_mm(svt_ctx* ctx, cudaStream_t s, int cls, bool transA, i64 M, i6
                    i64 ldd, const double* B, i64 ldb, const int* brow, DevBuf<double>& ws, double alg_bytes,
                    double alg_flops) {
     if (M <= 0 || N <= 0 || K <= 0) return 0;
-    if ((ldb % 2) != 0 || (ldd % 2) != 0 || (reinterpret_cast<uintptr_t>(B) % 16) != 0 ||
-        (reinterpret_cast<uintptr_t>(D) % 16) != 0)
+    if ((ldd % 2) != 0 || (reinterpret_cast<uintptr_t>(D) % 16) != 0 || (reinterpret_cast<uintptr_t>(B) % 8) != 0)
         return 0;
+    // 8-byte operand copies when the panel rows are not 16-byte aligned
+    const bool b8 = (ldb % 2) != 0 || (reinterpret_cast<uintptr_t>(B) % 16) != 0;
     LaunchScope ls(ctx, cls, alg_bytes, alg_flops, s);
-#define SVT_DB(BN_)                                                                                   \
-    return transA ? dense_block_launch<BN_, true>(ctx, s, M, N, K, D, ldd, B, ldb, brow, ws)         \
-                  : dense_block_launch<BN_, false>(ctx, s, M, N, K, D, ldd, B, ldb, brow, ws)
+#define SVT_DB(BN_)                                                                                       \
+    return transA ? (b8 ? dense_block_launch<BN_, true, true>(ctx, s, M, N, K, D, ldd, B, ldb, brow, ws)   \
+                        : dense_block_launch<BN_, true, false>(ctx, s, M, N, K, D, ldd, B, ldb, brow, ws)) \
+                  : (b8 ? dense_block_launch<BN_, false, true>(ctx, s, M, N, K, D, ldd, B, ldb, brow, ws)  \
+                        : dense_block_launch<BN_, false, false>(ctx, s, M, N, K, D, ldd, B, ldb, brow, ws))
     if (N <= 32) SVT_DB(32);
     if (N <= 64) SVT_DB(64);
     SVT_DB(128);

@@ -71,6 +71,21 @@ void read_doubles2(svt_ctx* c, const double* d1, const double* d2, size_t count,
     std::memcpy(o2, c->h_stage + count, sizeof(double) * count);
 }
 
+// flag i and `count` doubles with ONE stream synchronization (the batch path
+// reads its QR status together with the block energies)
+int read_flag_and_doubles(svt_ctx* c, int i, const double* d, size_t count, double* out) {
+    SVT_CUDA(cudaMemcpyAsync(c->h_flags + i, c->d_flags + i, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    if (count > c->h_stage_n) {
+        SVT_CUDA(cudaMemcpyAsync(out, d, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+        sync_stream(c);
+        return c->h_flags[i];
+    }
+    SVT_CUDA(cudaMemcpyAsync(c->h_stage, d, sizeof(double) * count, cudaMemcpyDeviceToHost, c->stream));
+    sync_stream(c);
+    std::memcpy(out, c->h_stage, sizeof(double) * count);
+    return c->h_flags[i];
+}
+
 bool debug_batch() {
     static const bool on = std::getenv("SVTB_DEBUG_BATCH") != nullptr;
     return on;
@@ -263,8 +278,7 @@ void prepare_tiles(Engine& E) {
 // The dense-corner split of Y (HybridPlan) for wide panels: built on the
 // first wide product (main stream), its values mirrored from Y.csr once per
 // sketch; side-stream products use it only once it is fresh (they follow the
-// main stream's refresh through the batch events).  The block product's
-// operands must be 16-byte aligned rows.
+// main stream's refresh through the batch events).
 constexpr i64 kHybMinW = 24;
 static bool hybrid_ready(Engine& E, i64 w, const double* X, i64 ldx, cudaStream_t stream) {
     svt_mat* A = E.mat;
@@ -287,7 +301,7 @@ static bool hybrid_ready(Engine& E, i64 w, const double* X, i64 ldx, cudaStream_
         H.src_version = own ? A->val_version : -1;
         E.hyb_fresh = true;
     }
-    return (ldx % 2 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0);
+    return reinterpret_cast<uintptr_t>(X) % 8 == 0;  // 16-byte rows or not: both operand paths exist
 }
 
 
@@ -953,27 +967,35 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
     const char* sm_env = std::getenv("SVTB_SPEC_MULTI");  // per batch: tests toggle it
     const bool spec_multi = sm_env != nullptr && sm_env[0] == '1';
     const bool spec_ok = c->comm.world == 1 || (spec_multi && c->comm.side_capable());
-    if (c->side && Kn >= 2 && !no_spec && spec_ok) {
-        if (!sp.ready) {
-            SVT_CUDA(cudaEventCreateWithFlags(&sp.ready, cudaEventDisableTiming));
-            SVT_CUDA(cudaEventCreateWithFlags(&sp.freed[0], cudaEventDisableTiming));
-            SVT_CUDA(cudaEventCreateWithFlags(&sp.freed[1], cudaEventDisableTiming));
-            SVT_CUDA(cudaEventRecord(sp.freed[0], c->stream));
-            SVT_CUDA(cudaEventRecord(sp.freed[1], c->stream));
+    // enqueued after this batch's first main-stream kernels, so the main
+    // stream (the critical path) restarts as early as possible after the
+    // previous batch's host synchronization
+    bool spec_launched = false;
+    auto launch_spec = [&]() {
+        if (spec_launched) return;
+        spec_launched = true;
+        if (c->side && Kn >= 2 && !no_spec && spec_ok) {
+            if (!sp.ready) {
+                SVT_CUDA(cudaEventCreateWithFlags(&sp.ready, cudaEventDisableTiming));
+                SVT_CUDA(cudaEventCreateWithFlags(&sp.freed[0], cudaEventDisableTiming));
+                SVT_CUDA(cudaEventCreateWithFlags(&sp.freed[1], cudaEventDisableTiming));
+                SVT_CUDA(cudaEventRecord(sp.freed[0], c->stream));
+                SVT_CUDA(cudaEventRecord(sp.freed[1], c->stream));
+            }
+            const int ns = slot ^ 1;
+            // buffers of slot ns are free once the main stream is done with the
+            // batch that used them; regrowth (cudaFree) synchronizes the device
+            SVT_CUDA(cudaStreamWaitEvent(c->side, sp.freed[ns], 0));
+            batch_sketch(E, p, round0 + K, Kn, ns, true);
+            SVT_CUDA(cudaEventRecord(sp.ready, c->side));
+            sp.valid = true;
+            sp.gen = E.sketch_gen;
+            sp.seed = p.seed;
+            sp.round0 = round0 + K;
+            sp.K = Kn;
+            sp.slot = ns;
         }
-        const int ns = slot ^ 1;
-        // buffers of slot ns are free once the main stream is done with the
-        // batch that used them; regrowth (cudaFree) synchronizes the device
-        SVT_CUDA(cudaStreamWaitEvent(c->side, sp.freed[ns], 0));
-        batch_sketch(E, p, round0 + K, Kn, ns, true);
-        SVT_CUDA(cudaEventRecord(sp.ready, c->side));
-        sp.valid = true;
-        sp.gen = E.sketch_gen;
-        sp.seed = p.seed;
-        sp.round0 = round0 + K;
-        sp.K = Kn;
-        sp.slot = ns;
-    }
+    };
     double* XW = sp.x[slot].get();
     const i64 Wc = std::max<i64>(W, kMaxBatchW);
     E.TW.ensure(static_cast<size_t>(n * Wc));
@@ -1010,6 +1032,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
             allreduce(c, E.CW.get(), static_cast<size_t>(r0 * W));
         }
         gemm(c, K_GEMM, false, m, W, r0, -1.0, Q, ldq, E.CW.get(), W, 1.0, XW, W);
+        launch_spec();
         col_sumsq(c, XW, m, W, W, E.eW.get());
         allreduce(c, E.eW.get(), static_cast<size_t>(W));
         if (debug_batch()) {
@@ -1057,6 +1080,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
             std::fprintf(stderr, "[batch] round0=%d K=%d r0=%lld check=%d second_pass=%d\n", round0, K,
                          static_cast<long long>(r0), read_flag(c, F_CHECK), read_flag(c, F_SECOND));
     }
+    launch_spec();  // (r0 == 0: no Gram-Schmidt kernels before it)
     // one Cholesky QR (twice) of the whole panel: nested spans per block
     E.GW.ensure(static_cast<size_t>(Wc * Wc));
     E.RW.ensure(static_cast<size_t>(Wc * Wc));
@@ -1077,13 +1101,10 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
     }
     chol_rinv(c, E.GW.get(), W, E.RW.get(), status, nullptr);
     gemm(c, K_QR, false, m, W, W, 1.0, E.X2.get(), W, E.RW.get(), W, 0.0, Q + r0, ldq);
-    if (read_flag(c, F_QRSTAT) != 0) {
-        if (debug_batch())
-            std::fprintf(stderr, "[batch] round0=%d K=%d W=%lld r0=%lld: Cholesky QR failed, sequential rounds\n",
-                         round0, K, static_cast<long long>(W), static_cast<long long>(r0));
-        return -1;
-    }
-    // coefficient rows of the whole batch and their per-block energies
+    // coefficient rows of the whole batch and their per-block energies,
+    // enqueued before the QR status is known: status and energies come back
+    // with one synchronization (after a failed QR the columns r0.. of Q and
+    // B^T are rewritten by the sequential rounds that replace the batch)
     if (c->comm.world == 1) {  // straight into the coefficient rows (no staging copy)
         sp_mult_t(E, W, Q + r0, ldq, st.Bt.get() + r0, nullptr, nullptr, ldq);
         col_sumsq(c, st.Bt.get() + r0, n, W, ldq, E.eW.get());
@@ -1093,7 +1114,12 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
         col_sumsq(c, E.TW.get(), n, W, W, E.eW.get());
     }
     std::vector<double> e(static_cast<size_t>(W));
-    read_doubles(c, E.eW.get(), static_cast<size_t>(W), e.data());
+    if (read_flag_and_doubles(c, F_QRSTAT, E.eW.get(), static_cast<size_t>(W), e.data()) != 0) {
+        if (debug_batch())
+            std::fprintf(stderr, "[batch] round0=%d K=%d W=%lld r0=%lld: Cholesky QR failed, sequential rounds\n",
+                         round0, K, static_cast<long long>(W), static_cast<long long>(r0));
+        return -1;
+    }
     // replay the reference's loop test round by round
     int accepted = 0;
     for (int k = 0; k < K; ++k) {

@@ -2,10 +2,10 @@
 // (the C++ standard fixes every output) followed by the reference's explicit
 // Box-Muller transform, dense.hpp:52-98.
 //
-// Stage 1 (mt_twist_kernel): one warp owns the 312-word state in shared
-// memory and runs the twist as two data-parallel halves (words 0..155 read
-// only old words; words 156..311 read the new words 0..155), then tempers and
-// streams the raw 64-bit draws to HBM.  The state persists in global memory
+// Stage 1 (mt_twist_kernel): one 160-thread CTA owns the 312-word state in
+// shared memory (ping-pong) and runs each twist as two data-parallel halves
+// (words 0..155 read only old words; words 156..311 read the new words
+// 0..155), tempering and streaming the raw 64-bit draws to HBM as they form.  The state persists in global memory
 // between chunks, so arbitrarily long streams (qb_init at t0 = 5000 needs
 // 5e8 draws) are produced in bounded scratch.
 // Stage 2 (box_muller_kernel): grid-wide; pair p consumes draws 2p (u1 = 1-u)
@@ -42,63 +42,63 @@ __device__ __forceinline__ unsigned long long twist_word(unsigned long long cur,
     return far ^ xa;
 }
 
-// One warp.  init != 0: seed the state (std::mt19937_64 seeding recurrence,
-// f = 6364136223846793005).  Generates ntwists * 312 draws into out.
-__global__ void __launch_bounds__(32) mt_twist_kernel(unsigned long long seed, int init,
-                                                      unsigned long long* state, long long ntwists,
-                                                      unsigned long long* out) {
-    __shared__ unsigned long long mt[MT_N];
-    const int lane = threadIdx.x;
-    if (init) {
-        if (lane == 0) {
-            unsigned long long x = seed;
-            mt[0] = x;
-            for (int i = 1; i < MT_N; ++i) {
-                x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<unsigned long long>(i);
-                mt[i] = x;
-            }
-        }
-    } else {
-        for (int i = lane; i < MT_N; i += 32) mt[i] = state[i];
+// One CTA of 160 threads (thread i < 156 owns words i and i + 156).  The
+// twist x[k + 312] = f(x[k], x[k + 1], x[k + 156]) has dependency distance
+// 156, so each half of a twist is one data-parallel step: words 0..155 read
+// only the previous state, words 156..311 the previous state and the new
+// words 0..155 (word 311 reads the new word 0).  The state is ping-ponged
+// between two shared arrays (no read-before-overwrite hazard), so a twist
+// costs two barriers; every new word is tempered and written out as soon as
+// it is formed.  init != 0: seed the state (std::mt19937_64 seeding
+// recurrence, f = 6364136223846793005); else continue from `state`.
+// Generates ntwists * 312 draws into out and saves the final state.
+constexpr int kMtThreads = 160;
+__device__ __forceinline__ void mt_seed(unsigned long long seed, unsigned long long* mt) {
+    unsigned long long x = seed;
+    mt[0] = x;
+    for (int i = 1; i < MT_N; ++i) {
+        x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<unsigned long long>(i);
+        mt[i] = x;
     }
-    __syncwarp();
+}
+
+__device__ __forceinline__ void mt_run(unsigned long long (*mt)[MT_N], long long ntwists,
+                                       unsigned long long* __restrict__ out, int& cur) {
+    const int i = threadIdx.x;
     for (long long t = 0; t < ntwists; ++t) {
-        // phase 1: words 0..155 (read all inputs, then write)
-        unsigned long long v[5];
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            const int i = lane + 32 * q;
-            if (i < MT_M) v[q] = twist_word(mt[i], mt[i + 1], mt[i + MT_M]);
+        const unsigned long long* o = mt[cur];
+        unsigned long long* nw = mt[cur ^ 1];
+        unsigned long long* dst = out + t * MT_N;
+        if (i < MT_M) {
+            const unsigned long long v = twist_word(o[i], o[i + 1], o[i + MT_M]);
+            nw[i] = v;
+            dst[i] = temper(v);
         }
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            const int i = lane + 32 * q;
-            if (i < MT_M) mt[i] = v[q];
+        __syncthreads();
+        if (i < MT_M) {
+            const int j = i + MT_M;
+            const unsigned long long v = twist_word(o[j], (j + 1 < MT_N) ? o[j + 1] : nw[0], nw[i]);
+            nw[j] = v;
+            dst[j] = temper(v);
         }
-        __syncwarp();
-        // phase 2: words 156..311 (word 311 reads the new word 0)
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            const int i = MT_M + lane + 32 * q;
-            if (i < MT_N) v[q] = twist_word(mt[i], mt[(i + 1) % MT_N], mt[i - MT_M]);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            const int i = MT_M + lane + 32 * q;
-            if (i < MT_N) mt[i] = v[q];
-        }
-        __syncwarp();
-        unsigned long long* o = out + t * MT_N;
-#pragma unroll
-        for (int q = 0; q < 10; ++q) {
-            const int i = lane + 32 * q;
-            if (i < MT_N) o[i] = temper(mt[i]);
-        }
+        __syncthreads();
+        cur ^= 1;
     }
-    __syncwarp();
-    for (int i = lane; i < MT_N; i += 32) state[i] = mt[i];
+}
+
+__global__ void __launch_bounds__(kMtThreads) mt_twist_kernel(unsigned long long seed, int init,
+                                                              unsigned long long* state, long long ntwists,
+                                                              unsigned long long* out) {
+    __shared__ unsigned long long mt[2][MT_N];
+    if (init) {
+        if (threadIdx.x == 0) mt_seed(seed, mt[0]);
+    } else {
+        for (int i = threadIdx.x; i < MT_N; i += blockDim.x) mt[0][i] = state[i];
+    }
+    __syncthreads();
+    int cur = 0;
+    mt_run(mt, ntwists, out, cur);
+    for (int i = threadIdx.x; i < MT_N; i += blockDim.x) state[i] = mt[cur][i];
 }
 
 // normal q of the block lands at (row q % rows, column q / rows) of the
@@ -138,53 +138,14 @@ struct SeedPack {
     unsigned long long s[kMaxOmegaBatch];
 };
 
-__global__ void __launch_bounds__(32) mt_twist_multi_kernel(SeedPack seeds, long long ntwists,
-                                                            unsigned long long* __restrict__ out, long long stride) {
-    __shared__ unsigned long long mt[MT_N];
-    const int lane = threadIdx.x;
-    unsigned long long* o0 = out + blockIdx.x * stride;
-    if (lane == 0) {
-        unsigned long long x = seeds.s[blockIdx.x];
-        mt[0] = x;
-        for (int i = 1; i < MT_N; ++i) {
-            x = 6364136223846793005ULL * (x ^ (x >> 62)) + static_cast<unsigned long long>(i);
-            mt[i] = x;
-        }
-    }
-    __syncwarp();
-    for (long long t = 0; t < ntwists; ++t) {
-        unsigned long long v[5];
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            const int i = lane + 32 * q;
-            if (i < MT_M) v[q] = twist_word(mt[i], mt[i + 1], mt[i + MT_M]);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            const int i = lane + 32 * q;
-            if (i < MT_M) mt[i] = v[q];
-        }
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            const int i = MT_M + lane + 32 * q;
-            if (i < MT_N) v[q] = twist_word(mt[i], mt[(i + 1) % MT_N], mt[i - MT_M]);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int q = 0; q < 5; ++q) {
-            const int i = MT_M + lane + 32 * q;
-            if (i < MT_N) mt[i] = v[q];
-        }
-        __syncwarp();
-        unsigned long long* o = o0 + t * MT_N;
-#pragma unroll
-        for (int q = 0; q < 10; ++q) {
-            const int i = lane + 32 * q;
-            if (i < MT_N) o[i] = temper(mt[i]);
-        }
-    }
+__global__ void __launch_bounds__(kMtThreads) mt_twist_multi_kernel(SeedPack seeds, long long ntwists,
+                                                                    unsigned long long* __restrict__ out,
+                                                                    long long stride) {
+    __shared__ unsigned long long mt[2][MT_N];
+    if (threadIdx.x == 0) mt_seed(seeds.s[blockIdx.x], mt[0]);
+    __syncthreads();
+    int cur = 0;
+    mt_run(mt, ntwists, out + blockIdx.x * stride, cur);
 }
 
 __global__ void box_muller_multi_kernel(const unsigned long long* __restrict__ draws, long long draw_stride,
@@ -224,7 +185,7 @@ void gaussian_blocks_dev(svt_ctx* ctx, i64 rows, i64 cols, const u64* seeds, int
     for (int k = 0; k < K; ++k) pack.s[k] = seeds[k];
     {
         LaunchScope ls(ctx, K_RNG, 8.0 * draw_stride * K, 0.0, stream);
-        mt_twist_multi_kernel<<<K, 32, 0, stream>>>(pack, twists, scratch.get(), draw_stride);
+        mt_twist_multi_kernel<<<K, kMtThreads, 0, stream>>>(pack, twists, scratch.get(), draw_stride);
     }
     LaunchScope ls(ctx, K_RNG, 32.0 * pairs * K, 0.0, stream);
     dim3 grid(static_cast<unsigned>((pairs + 255) / 256), static_cast<unsigned>(K));
@@ -247,7 +208,7 @@ void gaussian_block_dev(svt_ctx* ctx, i64 rows, i64 cols, u64 seed, double* out,
         const i64 nt = std::min<i64>(chunk_twists, twists_needed - done_twists);
         {
             LaunchScope ls(ctx, K_RNG, nt * MT_N * 8.0, 0.0);
-            mt_twist_kernel<<<1, 32, 0, ctx->stream>>>(seed, first ? 1 : 0, ctx->ws_mt.get(), nt, ctx->ws_rng.get());
+            mt_twist_kernel<<<1, kMtThreads, 0, ctx->stream>>>(seed, first ? 1 : 0, ctx->ws_mt.get(), nt, ctx->ws_rng.get());
         }
         first = false;
         const i64 pair0 = done_twists * MT_N / 2;

@@ -61,14 +61,34 @@ LaunchScope::~LaunchScope() noexcept(false) {
     }
 }
 
+// Host wait for the context stream.  SVTB_SYNC_SPIN=1 polls cudaStreamQuery
+// instead of blocking in cudaStreamSynchronize (whose wake-up latency is a
+// device-idle gap on the critical path of the round-batch loop: one such
+// wait per batch).
+static void wait_stream(cudaStream_t s) {
+    static const bool spin = [] {
+        const char* e = std::getenv("SVTB_SYNC_SPIN");
+        return e != nullptr && e[0] == '1';
+    }();
+    if (!spin) {
+        SVT_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    for (;;) {
+        const cudaError_t e = cudaStreamQuery(s);
+        if (e == cudaSuccess) return;
+        if (e != cudaErrorNotReady) SVT_CUDA(e);
+    }
+}
+
 void sync_stream(svt_ctx* c, int site, const char* file) {
     c->host_syncs++;
     if (!c->profiling) {
-        SVT_CUDA(cudaStreamSynchronize(c->stream));
+        wait_stream(c->stream);
         return;
     }
     const auto t0 = std::chrono::steady_clock::now();
-    SVT_CUDA(cudaStreamSynchronize(c->stream));
+    wait_stream(c->stream);
     const auto t1 = std::chrono::steady_clock::now();
     c->host_sync_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
     if (c->gap_debug) {

@@ -103,7 +103,7 @@ byname = {}
 for e in ev:
     if e.get("cat") == "kernel":
         s = e.get("args", {}).get("stream")
-        nm = e["name"].split("(")[0].replace("void ", "").replace("svtb::(anonymous namespace)::", "")[:48]
+        nm = e["name"].replace("void ", "").replace("svtb::(anonymous namespace)::", "").split("(")[0][:48]
         d = byname.setdefault(s, {})
         d[nm] = d.get(nm, 0.0) + e.get("dur", 0)
 for s, d in byname.items():

@@ -905,8 +905,9 @@ def test_dense_corner_split_spmm_matches_plain(config, monkeypatch):
     on the FP64 tensor cores, the cold entries through the gather kernel)
     gives the same Y X and Y^T X as the plain segmented SpMM within 1e-13
     relative (summation order only), at widths through 200 (panels wider than
-    one DMMA column tile), for an unaligned panel (falls back to the plain
-    kernel) and after the values change (the per-sketch mirror)."""
+    one DMMA column tile), for a panel whose rows are not 16-byte aligned
+    (8-byte operand copies) and after the values change (the per-sketch
+    mirror)."""
     import ctypes as C
     import torch
     d = G.synth_config(config, 1)
@@ -948,7 +949,7 @@ def test_dense_corner_split_spmm_matches_plain(config, monkeypatch):
         A.ctx.sync()
         outs.append(tO)
     assert ((outs[0] - outs[1]).abs().max() / outs[1].abs().max()).item() <= 1e-13
-    # an odd leading dimension (unaligned panel rows): the plain kernel runs
+    # an odd leading dimension (panel rows not 16-byte aligned): 8-byte operand copies
     tX = torch.from_numpy(rng.standard_normal((n, 121))).cuda()
     tO = torch.zeros(m, 121, dtype=torch.float64, device="cuda")
     assert L.svt_dev_sp_mult(Ah.h, 0, C.c_int64(121), C.c_void_p(tX.data_ptr()), C.c_int64(121),
