@@ -151,6 +151,24 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
+def gather_ceiling():
+    """Row-gather ceiling (TB/s): the best uniform-index rate of the gather
+    microbenchmark (scripts/gather_probe.cu: random 1 KB panel rows, register
+    accumulation — what one SpMM entry does), profiles/r02_gather_probe.txt."""
+    p = os.path.join(ROOT, "profiles", "r02_gather_probe.txt")
+    best = 0.0
+    try:
+        with open(p) as f:
+            for line in f:
+                if "uniform" in line and "ldg" in line and "TB/s" in line:
+                    best = max(best, float(line.split("gather")[1].split("TB/s")[0]))
+    except Exception:
+        best = 0.0
+    if best <= 0.0:
+        return 20.9, "fallback constant (probe file missing)"
+    return best, "profiles/r02_gather_probe.txt (uniform random 1 KB rows; L1 hits lift Zipf patterns above it)"
+
+
 def measured_fp64_peak():
     """FP64 GEMM peak (TFLOP/s): cuBLAS DGEMM measured on this pool by
     scripts/measure_fp64_peak.py (profiles/fp64_peak.json); else B200's
@@ -438,6 +456,10 @@ def main():
                          "launches": v["launches"], "avg_launch_us": 1000.0 * v["total_ms"] / max(1, v["launches"])}
             if k != "sddmm_update":
                 sparse[k]["gather_tbs"] = 4.0 * v["flops"] / (v["total_ms"] * 1e-3) / 1e12
+                ceil_tbs, ceil_src = gather_ceiling()
+                sparse[k]["gather_ceiling_tbs"] = ceil_tbs
+                sparse[k]["gather_frac"] = sparse[k]["gather_tbs"] / ceil_tbs
+                sparse[k]["gather_ceiling_source"] = ceil_src
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):

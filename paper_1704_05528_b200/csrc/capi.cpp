@@ -117,9 +117,13 @@ static void ctx_create(int device, int rank, int world, const void* nccl_id, svt
         // SMs it leaves idle: give the main stream the higher priority
         int prio_lo = 0, prio_hi = 0;
         SVT_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+        // SVTB_FLAT_PRIORITY / SVTB_SIDE_PRIORITY (A/B switches): equal
+        // priorities / the side stream above the main stream
         static const bool flat = std::getenv("SVTB_FLAT_PRIORITY") != nullptr;
-        SVT_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, flat ? prio_lo : prio_hi));
-        SVT_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_lo));
+        static const bool side_first = std::getenv("SVTB_SIDE_PRIORITY") != nullptr;
+        SVT_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking,
+                                              (flat || side_first) ? prio_lo : prio_hi));
+        SVT_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, side_first ? prio_hi : prio_lo));
         SVT_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
         SVT_CUDA(cudaMallocHost(&c->h_scalars, 64 * sizeof(double)));
         SVT_CUDA(cudaMallocHost(&c->h_flags, 64 * sizeof(int)));
