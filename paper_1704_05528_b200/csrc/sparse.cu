@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(128) spmm_wide_kernel(SegPlanView plan, const 
 // Segment bounds / targets of the group (<= kGrpSegs) sit one per lane and
 // are broadcast by shuffle.  Per output element the sum runs over the row's
 // entries in CSR order: the same order as spmm_wide_kernel (bitwise equal).
-template <int Q, int U, int MINB>
+template <int Q, int U, int MINB, bool CS = false>
 __global__ void __launch_bounds__(128, MINB) spmm_grp_kernel(SegPlanView plan, const int* __restrict__ idx,
                                                              const double* __restrict__ val,
                                                              const double* __restrict__ X, long long ldx,
@@ -228,8 +228,10 @@ __global__ void __launch_bounds__(128, MINB) spmm_grp_kernel(SegPlanView plan, c
     };
     for (int k0 = 0; k0 < end; k0 += 32) {
         const int k = k0 + lane;
-        const int cl = (k < end) ? __ldg(gi + k) : 0;
-        const double vl = (k < end) ? __ldg(gv + k) : 0.0;
+        // CS: the index / value streams are read once per pass, loaded with
+        // the evict-first hint so they do not displace panel rows from L2
+        const int cl = (k < end) ? (CS ? __ldcs(gi + k) : __ldg(gi + k)) : 0;
+        const double vl = (k < end) ? (CS ? __ldcs(gv + k) : __ldg(gv + k)) : 0.0;
         if (cur_end >= k0 + 32 && k0 + 32 <= end) {
             // fast path: a full chunk inside one segment (rows average ~130
             // entries at config 4): U entries' gathers in flight per step,
@@ -837,11 +839,11 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
         const unsigned nb = static_cast<unsigned>((plan.ngrp + 3) / 4);
         const unsigned chunks = static_cast<unsigned>(w <= 128 ? 1 : (w + 127) / 128);
         if (w <= 32)
-            spmm_grp_kernel<1, 8, 8><<<dim3(nb, 1), 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+            spmm_grp_kernel<1, 8, 8, true><<<dim3(nb, 1), 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
         else if (w <= 64)
-            spmm_grp_kernel<2, 8, 8><<<dim3(nb, 1), 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+            spmm_grp_kernel<2, 8, 8, true><<<dim3(nb, 1), 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
         else if (w <= 96)
-            spmm_grp_kernel<3, 4, 8><<<dim3(nb, 1), 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+            spmm_grp_kernel<3, 4, 8, true><<<dim3(nb, 1), 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
         else {
             // SVTB_SPMM_VARIANT (tuning): U,MINB of the Q = 4 instantiation
             static const int var = [] {
@@ -857,8 +859,10 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
                 spmm_grp_kernel<4, 2, 8><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
             else if (var == 4)
                 spmm_grp_kernel<4, 4, 10><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
-            else
+            else if (var == 5)  // plain __ldg index / value loads (A/B of the evict-first hint)
                 spmm_grp_kernel<4, 4, 8><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+            else  // evict-first index / value streams: cfg4 Y^T X DRAM reads 255 -> 217 MB
+                spmm_grp_kernel<4, 4, 8, true><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
         }
     } else {
         const unsigned nb = static_cast<unsigned>((plan.nseg + 3) / 4);
