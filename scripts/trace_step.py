@@ -110,8 +110,16 @@ for s, d in byname.items():
     top = sorted(d.items(), key=lambda kv: -kv[1])[:12]
     print(f"stream {s} top kernels: " + ", ".join(f"{k} {v/1e3:.1f}" for k, v in top))
 if len(ks) >= 2:
-    a, b = streams[ks[0]], streams[ks[1]]
+    # the library's streams in creation order: main, side, then the helper
+    # streams of main and side (dense-corner products); group each helper
+    # with its parent by the kernels it runs first
+    order = sorted(ks, key=lambda k: int(k) if str(k).isdigit() else 0)
+    main_ids = [order[0]] + ([order[2]] if len(order) > 2 else [])
+    side_ids = [order[1]] + ([order[3]] if len(order) > 3 else [])
+    a = union([iv for k in main_ids for iv in by_stream[k]])
+    b = union([iv for k in side_ids for iv in by_stream[k]])
     ov = inter_len(a, b)
     ta, tb = sum(y - x for x, y in a), sum(y - x for x, y in b)
-    print(f"span {span/1e3:.1f} ms: only {ks[0]} {(ta-ov)/1e3:.1f}, only {ks[1]} {(tb-ov)/1e3:.1f}, both {ov/1e3:.1f}, "
-          f"idle {(span - (ta + tb - ov))/1e3:.1f}")
+    print(f"span {span/1e3:.1f} ms: main-side busy {ta/1e3:.1f} / {tb/1e3:.1f}; only main {(ta-ov)/1e3:.1f}, "
+          f"only side {(tb-ov)/1e3:.1f}, both {ov/1e3:.1f}, idle {(span - (ta + tb - ov))/1e3:.1f} "
+          f"(streams main {main_ids}, side {side_ids})")
