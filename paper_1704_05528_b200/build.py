@@ -11,7 +11,7 @@ OUT_DIR = os.path.join(HERE, "lib")
 OUT = os.path.join(OUT_DIR, "libsvt_b200.so")
 OBJ = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["rng.cu", "sparse.cu", "dense.cu", "ozaki.cu", "build.cu", "io.cpp", "runtime.cpp", "host.cpp", "engine.cpp", "solver.cpp", "capi.cpp",
+SOURCES = ["rng.cu", "sparse.cu", "dense.cu", "ozaki.cu", "build.cu", "cutlass_gemm.cu", "io.cpp", "runtime.cpp", "host.cpp", "engine.cpp", "solver.cpp", "capi.cpp",
            "synth.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
@@ -27,12 +27,28 @@ def _needs(obj, src):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def cutlass_include():
+    """The vendored CUTLASS / CuTe header tree (flashinfer's copy, else tilelang's)."""
+    import importlib.util
+    for mod, rel in (("flashinfer", ("data", "cutlass", "include")), ("tilelang", ("3rdparty", "cutlass", "include"))):
+        spec = importlib.util.find_spec(mod)
+        if spec is None or not spec.submodule_search_locations:
+            continue
+        for loc in spec.submodule_search_locations:
+            p = os.path.join(loc, *rel)
+            if os.path.exists(os.path.join(p, "cutlass", "gemm", "device", "gemm.h")):
+                return p
+    raise RuntimeError("CUTLASS headers not found (flashinfer / tilelang site-packages)")
+
+
 def _compile(src):
     s = os.path.join(CSRC, src)
     o = os.path.join(OBJ, src + ".o")
     if not _needs(o, s):
         return o, None
     cmd = [NVCC, *ARCH, *COMMON, "-c", s, "-o", o]
+    if src == "cutlass_gemm.cu":
+        cmd = [NVCC, *ARCH, *COMMON, "-I", cutlass_include(), "-c", s, "-o", o]
     if src.endswith(".cpp"):
         cmd = [NVCC, *ARCH, *COMMON, "-x", "cu", "-c", s, "-o", o]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -1,0 +1,68 @@
+// Tall row-major FP64 products C = alpha A B + beta C (M >> N: the block
+// Gram-Schmidt update X - Q C and the CholQR products X R^-1) through a CUTLASS
+// 2.x device-GEMM template instantiated here (the vendored CuTe/CUTLASS header
+// tree; compiled into this library for sm_100a).  Configuration: 64 x 64
+// threadblock tiles, 32 x 32 warp tiles, DMMA 8x8x4 (SASS DMMA.8x8x4 — the
+// FP64 tensor path of sm_100a), 4-stage multistage mainloop, 8-byte operand
+// alignment (any leading dimension / column offset).  No split-K: the result
+// is deterministic.  Measured against our hand-written 64 x 128 kernel on the
+// config-4 / config-5 Gram-Schmidt shapes in profiles/r02c_gemm_bench*.txt.
+#include <cutlass/gemm/device/gemm.h>
+
+#include "common.hpp"
+#include "kernels.hpp"
+
+namespace svtb {
+
+namespace {
+
+template <int TM, int TN, int WM, int WN, int STG, int AL>
+using GemmNNT = cutlass::gemm::device::Gemm<
+    double, cutlass::layout::RowMajor, double, cutlass::layout::RowMajor, double, cutlass::layout::RowMajor, double,
+    cutlass::arch::OpClassTensorOp, cutlass::arch::Sm80, cutlass::gemm::GemmShape<TM, TN, 16>,
+    cutlass::gemm::GemmShape<WM, WN, 16>, cutlass::gemm::GemmShape<8, 8, 4>,
+    cutlass::epilogue::thread::LinearCombination<double, 1, double, double>,
+    cutlass::gemm::threadblock::GemmIdentityThreadblockSwizzle<>, STG, AL, AL>;
+
+template <typename G>
+bool run(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
+         i64 ldb, double beta, double* C, i64 ldc) {
+    G op;
+    typename G::Arguments args({static_cast<int>(M), static_cast<int>(N), static_cast<int>(K)},
+                               {A, static_cast<int>(lda)}, {B, static_cast<int>(ldb)}, {C, static_cast<int>(ldc)},
+                               {C, static_cast<int>(ldc)}, {alpha, beta});
+    if (op.can_implement(args) != cutlass::Status::kSuccess) return false;
+    const cutlass::Status st = op(args, nullptr, s ? s : ctx->stream);
+    if (st != cutlass::Status::kSuccess) throw cuda_error("CUTLASS DGEMM launch failed");
+    return true;
+}
+
+// SVTB_CUTLASS_CFG (tuning A/B; 8-byte operand alignment throughout — the
+// FP64 tensor-op iterators take no wider access for row-major operands):
+// 1 = 64x32 (warp 32x16, 4 stages), 2 = 64x64 (warp 32x32, 4 stages; default:
+// config-4 X - QC 737 -> 723 us, X R^-1 93 -> 86 us, config-5 X - QC
+// 16.1 -> 14.7 ms = 96 % of the measured DGEMM peak),
+// 3 = 128x64 (warp 64x32, 3 stages), 4 = 128x32 (warp 64x16), 5 = 64x32 with 5 stages
+int cfg() {
+    static const int v = [] {
+        const char* e = std::getenv("SVTB_CUTLASS_CFG");
+        return e ? std::atoi(e) : 2;
+    }();
+    return v;
+}
+
+}  // namespace
+
+bool cutlass_gemm_nn(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+                     const double* B, i64 ldb, double beta, double* C, i64 ldc) {
+    const i64 lim = (1LL << 31) - 1;
+    if (M > lim || N > lim || K > lim || lda > lim || ldb > lim || ldc > lim) return false;
+    const int c = cfg();
+    if (c == 3) return run<GemmNNT<128, 64, 64, 32, 3, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (c == 4) return run<GemmNNT<128, 32, 64, 16, 4, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (c == 5) return run<GemmNNT<64, 32, 32, 16, 5, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (c == 1) return run<GemmNNT<64, 32, 32, 16, 4, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    return run<GemmNNT<64, 64, 32, 32, 4, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
+}  // namespace svtb

@@ -335,7 +335,7 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int BN, bool TA>
+template <int BN, bool TA, int STG = kCpStages>
 struct CpTile {
     static constexpr int BM = kDmmaBM, BK = kCpBK;
     static constexpr int SA = BM + 4;   // TA: [BK][SA]
@@ -343,14 +343,14 @@ struct CpTile {
     static constexpr int SB = BN + 4;   // [BK][SB]; BN + 4 == 4 mod 16 for BN in {32, 64, 128}
     static constexpr int A_ELEMS = TA ? BK * SA : BM * SAR;
     static constexpr int B_ELEMS = BK * SB;
-    static constexpr size_t SMEM = sizeof(double) * kCpStages * (A_ELEMS + B_ELEMS);
+    static constexpr size_t SMEM = sizeof(double) * STG * (A_ELEMS + B_ELEMS);
 };
 
 // GS (dense corner of a split sparse pattern, engine.cpp): row k of B is row
 // brow[k] of the panel (a gather folded into the cp.async B loads) and every
 // CTA writes its split-K partial tile (the caller's fixed-order reduction
 // scatter-adds the block rows into the sparse product's output).
-template <int BN, bool TA, bool GS = false, bool B8 = false>
+template <int BN, bool TA, bool GS = false, bool B8 = false, int STG = kCpStages>
 __global__ void __launch_bounds__(256, 2) dmma_cp_kernel(long long M, long long N, long long K, double alpha,
                                                          const double* __restrict__ A, long long lda,
                                                          const double* __restrict__ B, long long ldb, double beta,
@@ -358,14 +358,14 @@ __global__ void __launch_bounds__(256, 2) dmma_cp_kernel(long long M, long long 
                                                          double* __restrict__ partial, const int* __restrict__ pred,
                                                          const int* __restrict__ brow = nullptr) {
     if (pred != nullptr && *pred == 0) return;
-    using T = CpTile<BN, TA>;
+    using T = CpTile<BN, TA, STG>;
     constexpr int BM = T::BM, BK = T::BK, SA = T::SA, SAR = T::SAR, SB = T::SB;
     constexpr int NT = BN / 32;
     constexpr int A_CH = BM * BK / 2 / 256;  // 16-byte chunks per thread
     constexpr int B_CH = BK * BN / 2 / 256;
     extern __shared__ __align__(16) double smem[];
     double* As = smem;
-    double* Bs = smem + kCpStages * T::A_ELEMS;
+    double* Bs = smem + STG * T::A_ELEMS;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int wm = (warp >> 2) * 32;
@@ -414,17 +414,17 @@ __global__ void __launch_bounds__(256, 2) dmma_cp_kernel(long long M, long long 
 #pragma unroll
         for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 #pragma unroll
-    for (int st = 0; st < kCpStages - 1; ++st) {
+    for (int st = 0; st < STG - 1; ++st) {
         if (st < nk) issue(st, kbeg + st * BK);
         cp_async_commit();
     }
     for (long long it = 0; it < nk; ++it) {
-        cp_async_wait<kCpStages - 2>();
+        cp_async_wait<STG - 2>();
         __syncthreads();
-        const long long nx = it + kCpStages - 1;
-        if (nx < nk) issue(static_cast<int>(nx % kCpStages), kbeg + nx * BK);
+        const long long nx = it + STG - 1;
+        if (nx < nk) issue(static_cast<int>(nx % STG), kbeg + nx * BK);
         cp_async_commit();
-        const int stg = static_cast<int>(it % kCpStages);
+        const int stg = static_cast<int>(it % STG);
         const double* as = As + stg * T::A_ELEMS;
         const double* bs = Bs + stg * T::B_ELEMS;
 #pragma unroll
@@ -461,6 +461,23 @@ __global__ void __launch_bounds__(256, 2) dmma_cp_kernel(long long M, long long 
             }
         }
     }
+}
+
+
+static bool cutlass_nn_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SVTB_CUTLASS_NN");
+        return e == nullptr || e[0] != '0';
+    }();
+    return on;
+}
+
+static int dmma_stages() {
+    static const int v = [] {
+        const char* e = std::getenv("SVTB_DMMA_STAGES");
+        return e ? std::atoi(e) : 3;
+    }();
+    return v;
 }
 
 template <int BN>
@@ -523,7 +540,17 @@ void dmma_launch(svt_ctx* ctx, bool transA, i64 M, i64 N, i64 K, double alpha, c
     if (cp && transA)
         dmma_cp_kernel<BN, true><<<grid, 256, CpTile<BN, true>::SMEM, ctx->stream>>>(
             M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, ctx->ws_partial.get(), pred);
-    else if (cp)
+    else if (cp && dmma_stages() == 4) {  // A/B switch SVTB_DMMA_STAGES=4 (4-stage cp.async pipeline)
+        static bool attr4 = false;
+        if (!attr4) {
+            SVT_CUDA(cudaFuncSetAttribute(dmma_cp_kernel<BN, false, false, false, 4>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(CpTile<BN, false, 4>::SMEM)));
+            attr4 = true;
+        }
+        dmma_cp_kernel<BN, false, false, false, 4><<<grid, 256, CpTile<BN, false, 4>::SMEM, ctx->stream>>>(
+            M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, ctx->ws_partial.get(), pred);
+    } else if (cp)
         dmma_cp_kernel<BN, false><<<grid, 256, CpTile<BN, false>::SMEM, ctx->stream>>>(
             M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, kchunk, ctx->ws_partial.get(), pred);
     else if (transA)
@@ -2171,7 +2198,13 @@ void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha,
                 break;
         }
     }
-    // FP64 tensor cores (DMMA) for everything wider than the skinny paths
+    // FP64 tensor cores (DMMA) for everything wider than the skinny paths.
+    // Tall unpredicated NN products (Gram-Schmidt X - Q C, CholQR X R^-1):
+    // the CUTLASS 64 x 32 multistage template (SVTB_CUTLASS_NN=0: our 64 x 128
+    // kernel)
+    if (!transA && pred == nullptr && N > 32 && M >= 64LL * ctx->num_sms && cutlass_nn_enabled() &&
+        cutlass_gemm_nn(ctx, ctx->stream, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc))
+        return;
     if (N <= 32)
         dmma_launch<32>(ctx, transA, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
     else if (N <= 64)

@@ -85,6 +85,11 @@ void gemm_tn_ozaki_cached(svt_ctx* ctx, i64 M, i64 N, i64 K, const int8_t* tiles
 // reduction.  pred (device int, may be null): skip entirely when *pred == 0.
 void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
           const double* B, i64 ldb, double beta, double* C, i64 ldc, const int* pred = nullptr);
+// Tall row-major C = alpha A B + beta C through the CUTLASS DMMA template
+// (cutlass_gemm.cu); false when the shape is outside its limits (the caller
+// uses its own kernels).
+bool cutlass_gemm_nn(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+                     const double* B, i64 ldb, double beta, double* C, i64 ldc);
 // Dense corner of a split sparse product: split-K partials of op(D) B[brow, :]
 // on the FP64 tensor cores into ws on stream s (returns the split count, 0 =
 // operands not 16-byte aligned, nothing launched); dense_block_add adds their
