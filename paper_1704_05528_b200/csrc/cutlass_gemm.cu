@@ -8,6 +8,7 @@
 // is deterministic.  Measured against our hand-written 64 x 128 kernel on the
 // config-4 / config-5 Gram-Schmidt shapes in profiles/r02c_gemm_bench*.txt.
 #include <cutlass/gemm/device/gemm.h>
+#include <cutlass/gemm/device/gemm_splitk_parallel.h>
 
 #include "common.hpp"
 #include "kernels.hpp"
@@ -51,7 +52,40 @@ int cfg() {
     return v;
 }
 
+// C = alpha A^T B + beta C with A stored K x M row-major (column-major M x K):
+// the Gram-Schmidt coefficients B T and Q^T X, finalize's B W.  Split-K
+// "parallel": each K slice writes its partial tile to a workspace and a
+// reduction kernel adds the slices in order (deterministic) and applies
+// alpha / beta.
+using GemmTNSplit = cutlass::gemm::device::GemmSplitKParallel<
+    double, cutlass::layout::ColumnMajor, double, cutlass::layout::RowMajor, double, cutlass::layout::RowMajor, double,
+    cutlass::arch::OpClassTensorOp, cutlass::arch::Sm80, cutlass::gemm::GemmShape<64, 64, 16>,
+    cutlass::gemm::GemmShape<32, 32, 16>, cutlass::gemm::GemmShape<8, 8, 4>,
+    cutlass::epilogue::thread::LinearCombination<double, 1, double, double>,
+    cutlass::epilogue::thread::Convert<double, 1, double>, cutlass::reduction::thread::ReduceAdd<double, double, 1>,
+    cutlass::gemm::threadblock::GemmSplitKHorizontalThreadblockSwizzle, 4, 1, 1>;
+
 }  // namespace
+
+bool cutlass_gemm_tn(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+                     const double* B, i64 ldb, double beta, double* C, i64 ldc, DevBuf<double>& ws) {
+    const i64 lim = (1LL << 31) - 1;
+    if (M > lim || N > lim || K > lim || lda > lim || ldb > lim || ldc > lim) return false;
+    // K slices: about two waves of 64 x 64 tiles (three resident per SM), at
+    // least 256 of K per slice, partials within the workspace
+    const i64 tiles = ((M + 63) / 64) * ((N + 63) / 64);
+    i64 splits = std::max<i64>(1, std::min<i64>((6 * ctx->num_sms + tiles - 1) / tiles, K / 256));
+    splits = std::max<i64>(1, std::min<i64>(splits, static_cast<i64>(ws.n / static_cast<size_t>(M * N))));
+    GemmTNSplit op;
+    GemmTNSplit::Arguments args({static_cast<int>(M), static_cast<int>(N), static_cast<int>(K)},
+                                {A, static_cast<int>(lda)}, {B, static_cast<int>(ldb)}, {C, static_cast<int>(ldc)},
+                                {C, static_cast<int>(ldc)}, {alpha, beta}, static_cast<int>(splits));
+    if (op.can_implement(args) != cutlass::Status::kSuccess) return false;
+    if (GemmTNSplit::get_workspace_size(args) > ws.n * sizeof(double)) return false;
+    const cutlass::Status st = op(args, ws.get(), s ? s : ctx->stream);
+    if (st != cutlass::Status::kSuccess) throw cuda_error("CUTLASS split-K DGEMM launch failed");
+    return true;
+}
 
 bool cutlass_gemm_nn(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
                      const double* B, i64 ldb, double beta, double* C, i64 ldc) {

@@ -472,6 +472,14 @@ static bool cutlass_nn_enabled() {
     return on;
 }
 
+static bool cutlass_tn_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("SVTB_CUTLASS_TN");
+        return e == nullptr || e[0] != '0';
+    }();
+    return on;
+}
+
 static int dmma_stages() {
     static const int v = [] {
         const char* e = std::getenv("SVTB_DMMA_STAGES");
@@ -2205,6 +2213,13 @@ void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha,
     if (!transA && pred == nullptr && N > 32 && M >= 64LL * ctx->num_sms && cutlass_nn_enabled() &&
         cutlass_gemm_nn(ctx, ctx->stream, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc))
         return;
+    // wide TN contractions (Gram-Schmidt coefficients B T / Q^T X, finalize
+    // B W): the CUTLASS template with parallel split-K (SVTB_CUTLASS_TN=0:
+    // our kernel).  The W x W Gram blocks stay on our split-K kernel.
+    if (transA && pred == nullptr && N > 32 && M >= 512 && K >= 2048 && cutlass_tn_enabled()) {
+        ensure_partial(ctx, 1);
+        if (cutlass_gemm_tn(ctx, ctx->stream, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ctx->ws_partial)) return;
+    }
     if (N <= 32)
         dmma_launch<32>(ctx, transA, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, pred);
     else if (N <= 64)

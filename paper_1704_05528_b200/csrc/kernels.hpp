@@ -90,6 +90,11 @@ void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha,
 // uses its own kernels).
 bool cutlass_gemm_nn(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
                      const double* B, i64 ldb, double beta, double* C, i64 ldc);
+// C = alpha A^T B + beta C (A stored K x M row-major), CUTLASS DMMA template
+// with a deterministic parallel split-K through ws; false when it does not
+// apply (shape limits, workspace)
+bool cutlass_gemm_tn(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
+                     const double* B, i64 ldb, double beta, double* C, i64 ldc, DevBuf<double>& ws);
 // Dense corner of a split sparse product: split-K partials of op(D) B[brow, :]
 // on the FP64 tensor cores into ws on stream s (returns the split count, 0 =
 // operands not 16-byte aligned, nothing launched); dense_block_add adds their
