@@ -859,6 +859,12 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
                 spmm_grp_kernel<4, 2, 8><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
             else if (var == 4)
                 spmm_grp_kernel<4, 4, 10><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+            else if (var == 6)
+                spmm_grp_kernel<4, 4, 10, true><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+            else if (var == 7)
+                spmm_grp_kernel<4, 2, 12, true><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
+            else if (var == 8)
+                spmm_grp_kernel<4, 3, 10, true><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
             else if (var == 5)  // plain __ldg index / value loads (A/B of the evict-first hint)
                 spmm_grp_kernel<4, 4, 8><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
             else  // evict-first index / value streams: cfg4 Y^T X DRAM reads 255 -> 217 MB
