@@ -17,13 +17,15 @@ namespace svtb {
 
 namespace {
 
-template <int TM, int TN, int WM, int WN, int STG, int AL>
+// SW: threadblock swizzle width (2: the two 64-column tiles of one 64-row
+// block run next to each other, so the A tile is read from HBM once)
+template <int TM, int TN, int WM, int WN, int STG, int AL, int SW = 1>
 using GemmNNT = cutlass::gemm::device::Gemm<
     double, cutlass::layout::RowMajor, double, cutlass::layout::RowMajor, double, cutlass::layout::RowMajor, double,
     cutlass::arch::OpClassTensorOp, cutlass::arch::Sm80, cutlass::gemm::GemmShape<TM, TN, 16>,
     cutlass::gemm::GemmShape<WM, WN, 16>, cutlass::gemm::GemmShape<8, 8, 4>,
     cutlass::epilogue::thread::LinearCombination<double, 1, double, double>,
-    cutlass::gemm::threadblock::GemmIdentityThreadblockSwizzle<>, STG, AL, AL>;
+    cutlass::gemm::threadblock::GemmIdentityThreadblockSwizzle<SW>, STG, AL, AL>;
 
 template <typename G>
 bool run(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda, const double* B,
@@ -96,6 +98,8 @@ bool cutlass_gemm_nn(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double a
     if (c == 4) return run<GemmNNT<128, 32, 64, 16, 4, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (c == 5) return run<GemmNNT<64, 32, 32, 16, 5, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (c == 1) return run<GemmNNT<64, 32, 32, 16, 4, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (c == 6) return run<GemmNNT<64, 64, 32, 32, 4, 1, 2>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    if (c == 7) return run<GemmNNT<64, 128, 32, 64, 3, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     return run<GemmNNT<64, 64, 32, 32, 4, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
