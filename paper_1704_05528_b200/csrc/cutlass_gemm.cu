@@ -1,10 +1,11 @@
 // Tall row-major FP64 products C = alpha A B + beta C (M >> N: the block
 // Gram-Schmidt update X - Q C and the CholQR products X R^-1) through a CUTLASS
 // 2.x device-GEMM template instantiated here (the vendored CuTe/CUTLASS header
-// tree; compiled into this library for sm_100a).  Configuration: 64 x 64
-// threadblock tiles, 32 x 32 warp tiles, DMMA 8x8x4 (SASS DMMA.8x8x4 — the
-// FP64 tensor path of sm_100a), 4-stage multistage mainloop, 8-byte operand
-// alignment (any leading dimension / column offset).  No split-K: the result
+// tree; compiled into this library for sm_100a).  Configuration: 64 x 128
+// threadblock tiles with 32 x 64 warp tiles and a 3-stage multistage
+// mainloop for the batch panels (N > 64), 64 x 64 / 32 x 32 / 4 stages below;
+// DMMA 8x8x4 (SASS DMMA.8x8x4 — the FP64 tensor path of sm_100a), 8-byte
+// operand alignment (any leading dimension / column offset).  No split-K: the result
 // is deterministic.  Measured against our hand-written 64 x 128 kernel on the
 // config-4 / config-5 Gram-Schmidt shapes in profiles/r02c_gemm_bench*.txt.
 #include <cutlass/gemm/device/gemm.h>
@@ -42,9 +43,10 @@ bool run(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const 
 
 // SVTB_CUTLASS_CFG (tuning A/B; 8-byte operand alignment throughout — the
 // FP64 tensor-op iterators take no wider access for row-major operands):
-// 1 = 64x32 (warp 32x16, 4 stages), 2 = 64x64 (warp 32x32, 4 stages; default:
-// config-4 X - QC 737 -> 723 us, X R^-1 93 -> 86 us, config-5 X - QC
-// 16.1 -> 14.7 ms = 96 % of the measured DGEMM peak),
+// 1 = 64x32 (warp 32x16, 4 stages), 2 = default: 64x128 (warp 32x64, 3
+// stages) for N > 64, 64x64 (warp 32x32, 4 stages) below (config-4 X - QC
+// 737 -> 716 us, config-5 X - QC 16.1 -> 14.6 ms = 97 % of the measured
+// DGEMM peak), 6 = 64x64 with a 2-wide tile swizzle,
 // 3 = 128x64 (warp 64x32, 3 stages), 4 = 128x32 (warp 64x16), 5 = 64x32 with 5 stages
 int cfg() {
     static const int v = [] {
@@ -99,7 +101,9 @@ bool cutlass_gemm_nn(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double a
     if (c == 5) return run<GemmNNT<64, 32, 32, 16, 5, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (c == 1) return run<GemmNNT<64, 32, 32, 16, 4, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     if (c == 6) return run<GemmNNT<64, 64, 32, 32, 4, 1, 2>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
-    if (c == 7) return run<GemmNNT<64, 128, 32, 64, 3, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+    // default: one 128-column tile for the batch panels (W = 120 / 128: the
+    // A rows are read once), 64-column tiles for narrower products
+    if (N > 64) return run<GemmNNT<64, 128, 32, 64, 3, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
     return run<GemmNNT<64, 64, 32, 32, 4, 1>>(ctx, s, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 

@@ -480,6 +480,14 @@ static bool cutlass_tn_enabled() {
     return on;
 }
 
+static i64 cutlass_tn_min_m() {  // SVTB_CUTLASS_TN_MIN_M (A/B): smallest output height routed to CUTLASS
+    static const i64 v = [] {
+        const char* e = std::getenv("SVTB_CUTLASS_TN_MIN_M");
+        return e ? static_cast<i64>(std::atoll(e)) : static_cast<i64>(512);
+    }();
+    return v;
+}
+
 static int dmma_stages() {
     static const int v = [] {
         const char* e = std::getenv("SVTB_DMMA_STAGES");
@@ -2216,7 +2224,7 @@ void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha,
     // wide TN contractions (Gram-Schmidt coefficients B T / Q^T X, finalize
     // B W): the CUTLASS template with parallel split-K (SVTB_CUTLASS_TN=0:
     // our kernel).  The W x W Gram blocks stay on our split-K kernel.
-    if (transA && pred == nullptr && N > 32 && M >= 512 && K >= 2048 && cutlass_tn_enabled()) {
+    if (transA && pred == nullptr && N > 32 && M >= cutlass_tn_min_m() && K >= 2048 && cutlass_tn_enabled()) {
         ensure_partial(ctx, 1);
         if (cutlass_gemm_tn(ctx, ctx->stream, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, ctx->ws_partial)) return;
     }

@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(128, MINB) spmm_grp_kernel(SegPlanView plan, c
                                                              const double* __restrict__ X, long long ldx,
                                                              long long w, double* __restrict__ out, long long ldo,
                                                              double* __restrict__ partial) {
+    static_assert(32 % U == 0, "the fast path steps through a 32-entry chunk U entries at a time");
     const int lane = threadIdx.x & 31;
     const long long g = static_cast<long long>(blockIdx.x) * 4 + (threadIdx.x >> 5);
     if (g >= plan.ngrp) return;
@@ -853,8 +854,6 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
             const dim3 gq(nb, chunks);
             if (var == 1)
                 spmm_grp_kernel<4, 4, 6><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
-            else if (var == 2)
-                spmm_grp_kernel<4, 3, 8><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
             else if (var == 3)
                 spmm_grp_kernel<4, 2, 8><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
             else if (var == 4)
@@ -863,8 +862,6 @@ void spmm(svt_ctx* ctx, int cls, const SegPlanView& plan, i64 nrows, const int* 
                 spmm_grp_kernel<4, 4, 10, true><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
             else if (var == 7)
                 spmm_grp_kernel<4, 2, 12, true><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
-            else if (var == 8)
-                spmm_grp_kernel<4, 3, 10, true><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
             else if (var == 5)  // plain __ldg index / value loads (A/B of the evict-first hint)
                 spmm_grp_kernel<4, 4, 8><<<gq, 128, 0, s>>>(plan, idx, val, X, ldx, w, out, ldo, partial);
             else  // evict-first index / value streams: cfg4 Y^T X DRAM reads 255 -> 217 MB
