@@ -10,6 +10,7 @@
 // config-4 / config-5 Gram-Schmidt shapes in profiles/r02c_gemm_bench*.txt.
 #include <cutlass/gemm/device/gemm.h>
 #include <cutlass/gemm/device/gemm_splitk_parallel.h>
+#include <cutlass/gemm/device/gemm_universal.h>
 
 #include "common.hpp"
 #include "kernels.hpp"
@@ -69,7 +70,51 @@ using GemmTNSplit = cutlass::gemm::device::GemmSplitKParallel<
     cutlass::epilogue::thread::Convert<double, 1, double>, cutlass::reduction::thread::ReduceAdd<double, double, 1>,
     cutlass::gemm::threadblock::GemmSplitKHorizontalThreadblockSwizzle, 4, 1, 1>;
 
+// The dense corner of a split SpMM (engine.cpp): op(D) B[brow, :] with the
+// panel rows gathered by the operand iterator (GatherB), K split in
+// "parallel" mode into [S][M][N] partial tiles that the caller's fixed-order
+// scatter-add reduces into the output rows.
+template <typename LayoutA>
+using GemmCorner = cutlass::gemm::device::GemmUniversal<
+    double, LayoutA, double, cutlass::layout::RowMajor, double, cutlass::layout::RowMajor, double,
+    cutlass::arch::OpClassTensorOp, cutlass::arch::Sm80, cutlass::gemm::GemmShape<64, 64, 16>,
+    cutlass::gemm::GemmShape<32, 32, 16>, cutlass::gemm::GemmShape<8, 8, 4>,
+    cutlass::epilogue::thread::LinearCombination<double, 1, double, double>,
+    cutlass::gemm::threadblock::GemmIdentityThreadblockSwizzle<>, 4, 1, 1, cutlass::arch::OpMultiplyAdd,
+    cutlass::ComplexTransform::kNone, cutlass::ComplexTransform::kNone, false, true, false>;
+
+template <typename G>
+int corner(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, const double* D, i64 ldd, const double* B, i64 ldb,
+           const int* brow, DevBuf<double>& ws) {
+    const i64 tiles = ((M + 63) / 64) * ((N + 63) / 64);
+    i64 S = std::max<i64>(1, std::min<i64>((3 * ctx->num_sms) / tiles, K / 256));
+    S = std::max<i64>(1, std::min<i64>(S, static_cast<i64>(ws.n / static_cast<size_t>(M * N))));
+    if (static_cast<size_t>(M * N) > ws.n) return 0;
+    // every slice exactly K / S deep (a multiple of 16), so CUTLASS launches
+    // exactly S slices and every partial tile the reduction reads is written
+    while (S > 1 && K % (16 * S) != 0) --S;
+    typename G::Arguments args(cutlass::gemm::GemmUniversalMode::kGemmSplitKParallel,
+                               {static_cast<int>(M), static_cast<int>(N), static_cast<int>(K)}, static_cast<int>(S),
+                               {1.0, 0.0}, D, B, ws.get(), ws.get(), 0, 0, 0, M * N, ldd, ldb, N, N, nullptr, brow,
+                               nullptr);
+    G op;
+    if (op.can_implement(args) != cutlass::Status::kSuccess) return 0;
+    if (G::get_workspace_size(args) != 0) return 0;
+    const cutlass::Status st = op(args, nullptr, s);
+    if (st != cutlass::Status::kSuccess) throw cuda_error("CUTLASS dense-corner launch failed");
+    return static_cast<int>(S);
+}
+
 }  // namespace
+
+int cutlass_dense_block(svt_ctx* ctx, cudaStream_t s, bool transA, i64 M, i64 N, i64 K, const double* D, i64 ldd,
+                        const double* B, i64 ldb, const int* brow, DevBuf<double>& ws) {
+    const i64 lim = (1LL << 31) - 1;
+    if (M > lim || N > lim || K > lim || ldd > lim || ldb > lim) return 0;
+    if (transA)
+        return corner<GemmCorner<cutlass::layout::ColumnMajor>>(ctx, s, M, N, K, D, ldd, B, ldb, brow, ws);
+    return corner<GemmCorner<cutlass::layout::RowMajor>>(ctx, s, M, N, K, D, ldd, B, ldb, brow, ws);
+}
 
 bool cutlass_gemm_tn(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
                      const double* B, i64 ldb, double beta, double* C, i64 ldc, DevBuf<double>& ws) {

@@ -95,6 +95,10 @@ bool cutlass_gemm_nn(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double a
 // apply (shape limits, workspace)
 bool cutlass_gemm_tn(svt_ctx* ctx, cudaStream_t s, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
                      const double* B, i64 ldb, double beta, double* C, i64 ldc, DevBuf<double>& ws);
+// The same partials through a CUTLASS template with the panel-row gather in
+// its operand iterator (returns the split count, 0 = not applicable)
+int cutlass_dense_block(svt_ctx* ctx, cudaStream_t s, bool transA, i64 M, i64 N, i64 K, const double* D, i64 ldd,
+                        const double* B, i64 ldb, const int* brow, DevBuf<double>& ws);
 // Dense corner of a split sparse product: split-K partials of op(D) B[brow, :]
 // on the FP64 tensor cores into ws on stream s (returns the split count, 0 =
 // operands not 16-byte aligned, nothing launched); dense_block_add adds their
