@@ -13,9 +13,12 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/$
 tail -1 gpurun_out/${TAG}_final_ref.log > gpurun_out/${TAG}_final_ref.json
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_final_launches.csv \
     python bench.py --steps 1 --warmup 5 --no-e2e --no-cpu > gpurun_out/${TAG}_final_ncu_launches.log 2>&1; echo "launches rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:spmm_grp --launch-skip 300 -c 2 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:spmm_grp --launch-skip 150 -c 2 \
     -o gpurun_out/${TAG}_final_full_spmm python bench.py --steps 1 --warmup 5 --no-e2e --no-cpu \
     > gpurun_out/${TAG}_final_ncu_full.log 2>&1; echo "full spmm rc=$?"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"dmma_cp_kernel<128, false, false" --launch-skip 200 -c 1 \
-    -o gpurun_out/${TAG}_final_full_dmma python bench.py --steps 1 --warmup 5 --no-e2e --no-cpu \
-    > gpurun_out/${TAG}_final_ncu_full_dmma.log 2>&1; echo "full dmma rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:cutlass --launch-skip 100 -c 1 \
+    -o gpurun_out/${TAG}_final_full_gemm python bench.py --steps 1 --warmup 5 --no-e2e --no-cpu \
+    > gpurun_out/${TAG}_final_ncu_full_gemm.log 2>&1; echo "full gemm rc=$?"
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/${TAG}_final_tests.log 2>&1; echo "gpu tests rc=$?"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_final_smoke.log 2>&1; echo "smoke rc=$?"
+timeout 600 python scripts/trace_step.py --config 4 --warm 8 --iters 2 --out gpurun_out/${TAG}_trace.json > gpurun_out/${TAG}_final_trace.txt 2>&1; rm -f gpurun_out/${TAG}_trace.json
