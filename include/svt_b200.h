@@ -140,6 +140,12 @@ void* svt_ctx_stream(svt_ctx* ctx); /* the cudaStream_t every kernel runs on */
 int svt_ctx_rank(svt_ctx* ctx, int* rank, int* world);
 /* instrumentation: per-kernel-class CUDA-event timing (0 = off) */
 int svt_ctx_set_profiling(svt_ctx* ctx, int on);
+/* speculative side-stream round batches (1 = on, the default).  Off, every
+ * batch is sketched on the main stream after the previous one: the same
+ * results (the batches are identical), kernels serialised — the bench's
+ * per-kernel roofline pass uses it so launch durations are not inflated by
+ * SM sharing with the other stream. */
+int svt_ctx_set_speculation(svt_ctx* ctx, int on);
 int svt_ctx_reset_stats(svt_ctx* ctx);
 /* class: 0 SpMM, 1 SpMM^T, 2 SDDMM+update, 3 CGS/GEMM passes, 4 RNG, 5 QR, 6 finalize, 7 other */
 int svt_ctx_kernel_stats(svt_ctx* ctx, int cls, int64_t* launches, double* total_ms, double* bytes,

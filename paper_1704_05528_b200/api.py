@@ -137,6 +137,9 @@ class Context:
     def set_profiling(self, on: bool):
         _check(lib().svt_ctx_set_profiling(self.h, C.c_int(1 if on else 0)))
 
+    def set_speculation(self, on: bool):
+        _check(lib().svt_ctx_set_speculation(self.h, C.c_int(1 if on else 0)))
+
     def reset_stats(self):
         _check(lib().svt_ctx_reset_stats(self.h))
 

@@ -254,6 +254,13 @@ int svt_ctx_set_profiling(svt_ctx* ctx, int on) {
     });
 }
 
+int svt_ctx_set_speculation(svt_ctx* ctx, int on) {
+    return guard([&] {
+        need(ctx, "svt_ctx_set_speculation");
+        ctx->speculate = on != 0;
+    });
+}
+
 int svt_ctx_reset_stats(svt_ctx* ctx) {
     return guard([&] {
         need(ctx, "svt_ctx_reset_stats");

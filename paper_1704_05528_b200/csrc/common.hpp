@@ -130,7 +130,8 @@ inline long long factor_cols(long long rows_plus_n, long long max_rank) {
 constexpr size_t kTickets = 4096;
 
 // Kernel classes for instrumentation (svt_ctx_kernel_stats).
-enum KClass : int { K_SPMM = 0, K_SPMMT = 1, K_SDDMM = 2, K_GEMM = 3, K_RNG = 4, K_QR = 5, K_FINAL = 6, K_OTHER = 7, K_NCLASS = 8 };
+// K_SUB (-1): counted as a launch, timed by the enclosing operation's scope
+enum KClass : int { K_SUB = -1, K_SPMM = 0, K_SPMMT = 1, K_SDDMM = 2, K_GEMM = 3, K_RNG = 4, K_QR = 5, K_FINAL = 6, K_OTHER = 7, K_NCLASS = 8 };
 
 struct KStats {
     i64 launches = 0;
@@ -240,6 +241,7 @@ struct svt_ctx {
     // instrumentation
     bool profiling = false;
     int batching = 1;  // speculative multi-round batches in the rank-revealing loop
+    bool speculate = true;  // next batch sketched on the side stream (svt_ctx_set_speculation)
     svtb::i64 launch_count = 0;
     svtb::KStats stats[svtb::K_NCLASS];
     svtb::i64 host_syncs = 0;     // stream synchronizations issued by the library

@@ -2195,7 +2195,11 @@ void dense_block_add(svt_ctx* ctx, cudaStream_t s, int cls, i64 M, i64 N, int S,
 void gemm(svt_ctx* ctx, int cls, bool transA, i64 M, i64 N, i64 K, double alpha, const double* A, i64 lda,
           const double* B, i64 ldb, double beta, double* C, i64 ldc, const int* pred) {
     if (M <= 0 || N <= 0) return;
-    LaunchScope ls(ctx, cls, 8.0 * (M * K + K * N + M * N * (beta != 0.0 ? 2 : 1)), 2.0 * M * N * K);
+    // a predicated product (second Gram-Schmidt pass, re-projection check)
+    // usually exits at once: it is timed but its bytes / flops are not
+    // counted (they are unknown when it is queued)
+    LaunchScope ls(ctx, cls, pred ? 0.0 : 8.0 * (M * K + K * N + M * N * (beta != 0.0 ? 2 : 1)),
+                   pred ? 0.0 : 2.0 * M * N * K);
     if (K <= 0) {
         scale2d_kernel<<<nblk(M * N), 256, 0, ctx->stream>>>(C, M, N, ldc, beta, pred);
         return;

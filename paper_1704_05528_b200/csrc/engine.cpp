@@ -313,9 +313,16 @@ template <typename Cold>
 static void split_product(Engine& E, int cls, bool tr, i64 w, const double* X, i64 ldx, double* out, i64 ldo,
                           cudaStream_t stream, Cold&& cold) {
     svt_ctx* c = E.ctx;
-    HybridPlan& H = E.mat->hyb;
+    svt_mat* Am = E.mat;
+    HybridPlan& H = Am->hyb;
     cudaStream_t s = stream ? stream : c->stream;
     const int k = (s == c->side) ? 1 : 0;
+    // the whole split product is ONE timed operation of class cls (its
+    // kernels run on two streams and overlap); algorithmic bytes of the full
+    // product, the inner launches are K_SUB
+    const i64 rows = tr ? Am->n : Am->m_local, x_rows = tr ? Am->m_local : Am->n;
+    LaunchScope op(c, cls, 12.0 * Am->nnz_local + 8.0 * (rows + 1) + 8.0 * w * (x_rows + rows),
+                   2.0 * Am->nnz_local * w, s);
     if (c->aux[k] == nullptr) {
         int prio = 0;
         SVT_CUDA(cudaStreamGetPriority(s, &prio));
@@ -326,14 +333,13 @@ static void split_product(Engine& E, int cls, bool tr, i64 w, const double* X, i
     SVT_CUDA(cudaEventRecord(c->aux_fork[k], s));
     SVT_CUDA(cudaStreamWaitEvent(c->aux[k], c->aux_fork[k], 0));
     const i64 M = tr ? H.C : H.R, K = tr ? H.R : H.C;
-    const int S = dense_block_mm(c, c->aux[k], cls, tr, M, w, K, H.D.get(), H.C, X, ldx,
-                                 tr ? H.hot_rows.get() : H.hot_cols.get(), H.ws[k], 12.0 * H.nnz_blk,
-                                 2.0 * H.nnz_blk * w);
+    const int S = dense_block_mm(c, c->aux[k], K_SUB, tr, M, w, K, H.D.get(), H.C, X, ldx,
+                                 tr ? H.hot_rows.get() : H.hot_cols.get(), H.ws[k], 0.0, 0.0);
     SVT_CUDA(cudaEventRecord(c->aux_join[k], c->aux[k]));
     if (S == 0) throw std::logic_error("split SpMM: dense block operands not aligned");
     cold();
     SVT_CUDA(cudaStreamWaitEvent(s, c->aux_join[k], 0));
-    dense_block_add(c, s, cls, M, w, S, H.ws[k], tr ? H.hot_cols.get() : H.hot_rows.get(), out, ldo);
+    dense_block_add(c, s, K_SUB, M, w, S, H.ws[k], tr ? H.hot_cols.get() : H.hot_rows.get(), out, ldo);
 }
 
 void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo, cudaStream_t stream,
@@ -342,7 +348,7 @@ void sp_mult(Engine& E, i64 w, const double* X, i64 ldx, double* out, i64 ldo, c
     if (hybrid_ready(E, w, X, ldx, stream)) {
         HybridPlan& H = A->hyb;
         split_product(E, K_SPMM, false, w, X, ldx, out, ldo, stream, [&] {
-            spmm(E.ctx, K_SPMM, H.plan_c.v, A->m_local, H.col_c.get(), H.val_c.get(), H.nnz_cold, A->n, w, X, ldx,
+            spmm(E.ctx, K_SUB, H.plan_c.v, A->m_local, H.col_c.get(), H.val_c.get(), H.nnz_cold, A->n, w, X, ldx,
                  out, ldo, stream, scratch);
         });
         return;
@@ -362,7 +368,7 @@ void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out, cudaStre
     if (hybrid_ready(E, w, X, ldx, stream)) {
         HybridPlan& H = A->hyb;
         split_product(E, K_SPMMT, true, w, X, ldx, out, ldo, stream, [&] {
-            spmm(E.ctx, K_SPMMT, H.plant_c.v, A->n, H.row_c.get(), H.valt_c.get(), H.nnz_cold, A->m_local, w, X,
+            spmm(E.ctx, K_SUB, H.plant_c.v, A->n, H.row_c.get(), H.valt_c.get(), H.nnz_cold, A->m_local, w, X,
                  ldx, out, ldo, stream, scratch);
         });
     } else if (!(tiles_ready(E, w, stream) &&
@@ -974,7 +980,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
     auto launch_spec = [&]() {
         if (spec_launched) return;
         spec_launched = true;
-        if (c->side && Kn >= 2 && !no_spec && spec_ok) {
+        if (c->side && Kn >= 2 && !no_spec && spec_ok && c->speculate) {
             if (!sp.ready) {
                 SVT_CUDA(cudaEventCreateWithFlags(&sp.ready, cudaEventDisableTiming));
                 SVT_CUDA(cudaEventCreateWithFlags(&sp.freed[0], cudaEventDisableTiming));

@@ -14,6 +14,7 @@ namespace svtb {
 LaunchScope::LaunchScope(svt_ctx* c, int k, double bytes, double flops, cudaStream_t stream, const char* f, int l)
     : ctx(c), cls(k), st(stream ? stream : c->stream), file(f), line(l) {
     ctx->launch_count++;
+    if (k < 0) return;  // a kernel inside an operation timed as a whole by an enclosing scope
     if (ctx->gap_open) {
         auto& g = ctx->gap_stats[ctx->gap_site];
         g.first++;
