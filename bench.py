@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of oracle CPU work for cpu_baseline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "host"],
+                    help="multi-rank collectives: NCCL (default) or host-staged over gloo (validates the multi-rank "
+                         "path with several ranks on one GPU; never a measurement)")
     ap.add_argument("--profile-steps", type=int, default=0,
                     help="iterations of the separate per-launch-event pass (0: all K)")
     return ap.parse_args()
@@ -292,7 +295,13 @@ def main():
     rp, co, va = train
     bounds = G.partition_rows(rp, world)
     rb, re_ = int(bounds[rank]), int(bounds[rank + 1])
-    if world > 1:
+    if world > 1 and args.comm == "host":
+        def host_allreduce(x):
+            dist.all_reduce(torch.from_numpy(x))  # sums the pinned staging buffer in place
+
+        local = 0 if torch.cuda.device_count() == 1 else local
+        ctx = G.Context.hostcomm(local, rank, world, host_allreduce)
+    elif world > 1:
         obj = [G.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         ctx = G.Context(local, rank, world, obj[0])
