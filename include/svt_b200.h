@@ -116,7 +116,9 @@ typedef struct svt_result svt_result;   /* SvtResult                        */
 const char* svt_last_error(void);
 int svt_version(void);
 int svt_ctx_create(int device, svt_ctx** out);
-/* One rank of a world: nccl_id is the 128-byte ncclUniqueId of rank 0. */
+/* One rank of a world: nccl_id is the 128-byte ncclUniqueId of rank 0.
+ * world = 1 with an id makes a one-rank communicator: the distributed code
+ * path (row-blocked collectives, side communicator) on a single GPU. */
 int svt_ctx_create_dist(int device, int rank, int world, const void* nccl_id, svt_ctx** out);
 int svt_nccl_get_unique_id(void* out128);
 /* Host-staged collectives instead of NCCL: every all-reduce of the library

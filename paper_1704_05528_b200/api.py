@@ -80,7 +80,7 @@ class Context:
 
     def __init__(self, device=0, rank=0, world=1, nccl_id: bytes | None = None):
         h = C.c_void_p()
-        if world == 1:
+        if world == 1 and nccl_id is None:
             _check(lib().svt_ctx_create(C.c_int(device), C.byref(h)))
         else:
             buf = C.create_string_buffer(nccl_id, 128)

@@ -160,8 +160,11 @@ struct Comm {
     void allreduce_sum(double* buf, size_t count, cudaStream_t s, bool side = false);
     // collectives may also run on the side stream (speculative batches):
     // host-staged mode, or NCCL with a second communicator
-    bool side_capable() const { return world > 1 && (host_fn != nullptr || handle_side != nullptr); }
-    void allreduce_sum_i32(int* buf, size_t count, cudaStream_t s);
+    bool side_capable() const { return dist() && (host_fn != nullptr || handle_side != nullptr); }
+    // the distributed code path (row-blocked collectives) runs whenever a
+    // communicator exists, also for a one-rank NCCL world (svt_ctx_create_dist
+    // with world = 1 and an id: the collective sequence on one GPU)
+    bool dist() const { return world > 1 || handle != nullptr || host_fn != nullptr; }
     void destroy();
 };
 void nccl_unique_id(void* out128);

@@ -178,7 +178,7 @@ void reset_qb(QBDev& st, const svt_mat* A) {
 void qr_panel(Engine& E, i64 m, bool dist, const double* X, i64 ldx, i64 w, double* Qout, i64 ldq,
               const int* pred) {
     svt_ctx* c = E.ctx;
-    dist = dist && c->comm.world > 1;
+    dist = dist && c->comm.dist();
     const i64 wc = std::max<i64>(w, 64);  // panels are <= 64 wide: size once
     E.G.ensure(static_cast<size_t>(wc * wc));
     E.Rinv.ensure(static_cast<size_t>(wc * wc));
@@ -364,7 +364,7 @@ void sp_mult_t(Engine& E, i64 w, const double* X, i64 ldx, double* out, cudaStre
                DevBuf<double>* scratch, i64 ldo) {
     svt_mat* A = E.mat;
     if (ldo < 0) ldo = w;
-    if (ldo != w && E.ctx->comm.world > 1) throw std::logic_error("sp_mult_t: strided output needs one rank");
+    if (ldo != w && E.ctx->comm.dist()) throw std::logic_error("sp_mult_t: strided output needs one rank");
     if (hybrid_ready(E, w, X, ldx, stream)) {
         HybridPlan& H = A->hyb;
         split_product(E, K_SPMMT, true, w, X, ldx, out, ldo, stream, [&] {
@@ -392,7 +392,7 @@ void qr_orthonormal(Engine& E, double* X, i64 ldx, i64 w, double* Qout, i64 ldq)
 
 void qr_orthonormal(Engine& E, i64 m, bool dist, double* X, i64 ldx, i64 w, double* Qout, i64 ldq) {
     svt_ctx* c = E.ctx;
-    dist = dist && c->comm.world > 1;
+    dist = dist && c->comm.dist();
     constexpr i64 B = 64;
     for (i64 b0 = 0; b0 < w; b0 += B) {
         const i64 wb = std::min(B, w - b0);
@@ -458,7 +458,7 @@ static void power_iterate(Engine& E, i64 w, int np) {
 // B[r0:r0+w, :] = (Y^T Q[:, r0:r0+w])^T stored as B^T columns; norm_b_sq +=
 static void append_coefficients(Engine& E, QBDev& st, i64 r0, i64 w, int nb_op) {
     svt_ctx* c = E.ctx;
-    if (c->comm.world == 1) {  // straight into the coefficient rows (no staging copy)
+    if (!c->comm.dist()) {  // straight into the coefficient rows (no staging copy)
         sp_mult_t(E, w, st.Q.get() + r0, st.cap, st.Bt.get() + r0, nullptr, nullptr, st.cap);
         sumsq(c, st.Bt.get() + r0, st.n, w, st.cap, dsc(c, S_NB), nb_op);
         return;
@@ -972,7 +972,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
     // (SVTB_SPEC_MULTI=1) until it has run on NVLink hardware
     const char* sm_env = std::getenv("SVTB_SPEC_MULTI");  // per batch: tests toggle it
     const bool spec_multi = sm_env != nullptr && sm_env[0] == '1';
-    const bool spec_ok = c->comm.world == 1 || (spec_multi && c->comm.side_capable());
+    const bool spec_ok = !c->comm.dist() || (spec_multi && c->comm.side_capable());
     // enqueued after this batch's first main-stream kernels, so the main
     // stream (the critical path) restarts as early as possible after the
     // previous batch's host synchronization
@@ -1111,7 +1111,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
     // enqueued before the QR status is known: status and energies come back
     // with one synchronization (after a failed QR the columns r0.. of Q and
     // B^T are rewritten by the sequential rounds that replace the batch)
-    if (c->comm.world == 1) {  // straight into the coefficient rows (no staging copy)
+    if (!c->comm.dist()) {  // straight into the coefficient rows (no staging copy)
         sp_mult_t(E, W, Q + r0, ldq, st.Bt.get() + r0, nullptr, nullptr, ldq);
         col_sumsq(c, st.Bt.get() + r0, n, W, ldq, E.eW.get());
     } else {

@@ -161,7 +161,6 @@ struct UniqueId {
 };
 
 constexpr int kNcclFloat64 = 8;  // ncclDouble
-constexpr int kNcclInt32 = 2;    // ncclInt32
 constexpr int kNcclSum = 0;
 
 void check(ncclResult_t_ r, const char* what) {
@@ -178,7 +177,7 @@ void nccl_unique_id(void* out128) { check(nccl().GetUniqueId(out128), "ncclGetUn
 void nccl_init(Comm& c, int rank, int world, const void* id128) {
     c.rank = rank;
     c.world = world;
-    if (world <= 1) return;
+    if (world <= 1 && id128 == nullptr) return;  // world 1 with an id: a one-rank communicator
     auto fn = reinterpret_cast<ncclResult_t_ (*)(ncclComm_t_*, int, UniqueId, int)>(
         dlsym(nccl().h, "ncclCommInitRank"));
     if (!fn) throw nccl_error("ncclCommInitRank missing");
@@ -200,7 +199,7 @@ void nccl_init(Comm& c, int rank, int world, const void* id128) {
 }
 
 void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t s, bool side) {
-    if (world <= 1 || count == 0) return;
+    if (!dist() || count == 0) return;
     calls++;
     doubles += static_cast<double>(count);
     if (host_fn != nullptr) {
@@ -221,11 +220,6 @@ void Comm::allreduce_sum(double* buf, size_t count, cudaStream_t s, bool side) {
     if (side && handle_side == nullptr) throw nccl_error("side-stream all-reduce without a side communicator");
     check(svtb::nccl().AllReduce(buf, buf, count, kNcclFloat64, kNcclSum, side ? handle_side : handle, s),
           "ncclAllReduce");
-}
-
-void Comm::allreduce_sum_i32(int* buf, size_t count, cudaStream_t s) {
-    if (world <= 1 || count == 0) return;
-    check(svtb::nccl().AllReduce(buf, buf, count, kNcclInt32, kNcclSum, handle, s), "ncclAllReduce");
 }
 
 void Comm::destroy() {

@@ -199,3 +199,47 @@ def test_sharded_rank_deficient_householder_fallback(sharded):
     np.testing.assert_allclose(U.T @ U, np.eye(U.shape[1]), atol=1e-10)
     np.testing.assert_allclose(a["sigma"][:3], o.sigma[:3], rtol=1e-8)
     np.testing.assert_allclose((U[:, :3] * a["sigma"][:3]) @ a["V"][:, :3].T, M, atol=1e-9 * np.abs(M).max())
+
+
+def test_nccl_one_rank_communicator_runs_the_distributed_path():
+    """NCCL mode itself on the one GPU of the test box: a one-rank NCCL
+    communicator (svt_ctx_create_dist with world = 1 and an id) takes every
+    distributed branch of the engine — the row-block all-reduces through
+    ncclAllReduce on the main stream, the speculative batches' Y^T X
+    all-reduces on the side communicator (ncclCommSplit), the sharded QR and
+    its gathered Householder fallback — and must reproduce the plain
+    single-GPU run.  (Two NCCL ranks cannot share one device; the two-rank
+    collective sequence is covered by the host-staged tests above.)"""
+    os.environ["SVTB_SPEC_MULTI"] = "1"
+    try:
+        ctx = G.Context(0, 0, 1, nccl_id=G.Context.nccl_unique_id())
+        for name, m, n, A, T, cfg, iters in _cases():
+            cfg.maxit = iters
+            Ad = G.SampledMatrix.from_csr(m, n, A.rowptr, A.col, A.val, ctx=ctx, row_block=(0, m))
+            c0 = ctx.comm_stats()
+            r = G.svt_run(Ad, cfg, StopRule.none())
+            calls = ctx.comm_stats()["calls"] - c0["calls"]
+            Ad.close()
+            Ap = G.SampledMatrix.from_csr(m, n, A.rowptr, A.col, A.val)
+            one = G.svt_run(Ap, cfg, StopRule.none())
+            Ap.close()
+            assert calls > 0, name
+            assert len(r.trace) == len(one.trace)
+            for it, (a, b) in enumerate(zip(r.trace, one.trace)):
+                assert (a["rank"], a["extension_rounds"], a["kept"]) == (b["rank"], b["extension_rounds"],
+                                                                          b["kept"]), (name, it, a, b)
+                for k in ("residual", "train_mae", "rel_residual_x"):
+                    assert _rel(a[k], b[k]) <= 1e-8, (name, it, k, a[k], b[k])
+            np.testing.assert_allclose(r.sigma, one.sigma, rtol=1e-8)
+        M = O.make_low_rank(80, 60, 3, 17)
+        S = O.to_sampled(M)
+        p = SketchParams(t=2, dt=4, np=1, eps_threshold=1e-12, seed=4)
+        Sd = G.SampledMatrix.from_csr(80, 60, S.rowptr, S.col, S.val, ctx=ctx, row_block=(0, 80))
+        f = G.r3svd(Sd, p)
+        o = O.r3svd(S, p)
+        assert (f.rank, f.extension_rounds, f.saturated) == (o.rank, o.extension_rounds, o.saturated)
+        np.testing.assert_allclose(f.U.T @ f.U, np.eye(f.U.shape[1]), atol=1e-10)
+        Sd.close()
+        ctx.close()
+    finally:
+        os.environ.pop("SVTB_SPEC_MULTI", None)
