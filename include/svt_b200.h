@@ -355,6 +355,18 @@ int svt_synth_config(int config, uint64_t seed, int64_t* m, int64_t* n, int64_t*
 int svt_synth_config_csr(int config, uint64_t seed, int64_t* m, int64_t* n, int64_t* nnz, int64_t* rowptr,
                          int64_t* col, double* val);
 
+/* ---- the reference's experiment generators (proj/include/svt/synth.hpp) --
+ * Host-side, seeded; the inputs of the CLI's --synthetic / bench modes. */
+uint64_t svt_derive_seed(uint64_t seed, uint64_t stream);                                /* dense.hpp:44 */
+int svt_make_low_rank(int64_t m, int64_t n, int64_t rank, uint64_t seed, double* out);   /* synth.hpp:21-28; out m x n column-major */
+int svt_sample_dense(int64_t m, int64_t n, const double* A, double fraction, uint64_t seed,
+                     svt_triplets** out);                                                /* synth.hpp:64-84 */
+int svt_synthetic_image(int64_t size, int64_t rank, uint64_t seed, uint8_t* pixels);     /* synth.hpp:89-114; size*size row-major */
+int svt_synthetic_ratings(int64_t users, int64_t items, int64_t rank, double fill, double noise, uint64_t seed,
+                          svt_triplets** out);                                           /* synth.hpp:119-160 */
+/* default_config (solver.hpp:95-106) from the CSR-ordered values on the host. */
+int svt_default_config_host(int64_t m, int64_t n, int64_t nnz, const double* csr_vals, svt_config* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -77,7 +77,27 @@ def build(verbose=False):
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{r.stdout}{r.stderr}")
+    build_cli()
     return OUT
+
+
+CLI_SRC = os.path.join(HERE, "tools", "svt_main.cpp")
+CLI = os.path.join(HERE, "bin", "svt")
+
+
+def build_cli():
+    """The `svt` front end (tools/svt_main.cpp): plain C++ over the C ABI of
+    libsvt_b200.so, found at run time through an $ORIGIN-relative rpath."""
+    os.makedirs(os.path.dirname(CLI), exist_ok=True)
+    deps = [CLI_SRC, OUT, os.path.join(HERE, "..", "include", "svt_b200.h")]
+    if os.path.exists(CLI) and all(os.path.getmtime(d) <= os.path.getmtime(CLI) for d in deps):
+        return CLI
+    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-Wall", "-Wextra", CLI_SRC, "-o", CLI,
+           "-L", OUT_DIR, "-lsvt_b200", "-Wl,-rpath,$ORIGIN/../lib"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"svt CLI build failed:\n{' '.join(cmd)}\n{r.stdout}{r.stderr}")
+    return CLI
 
 
 if __name__ == "__main__":

@@ -26,6 +26,13 @@ void kickstart_dev(svt_ctx* c, svt_mat* A, double tau, double delta, u64 seed, d
 void synth_config(int config, u64 seed, i64* m, i64* n, i64* nnz_train, i64* nnz_test, i64* train_rows,
                   i64* train_cols, double* train_vals, i64* test_rows, i64* test_cols, double* test_vals);
 void synth_config_csr(int config, u64 seed, i64* m, i64* n, i64* nnz, i64* rowptr, i64* col, double* val);
+std::vector<double> make_low_rank_cm(i64 m, i64 n, i64 rank, u64 seed);
+void sample_dense(i64 m, i64 n, const double* A_cm, double fraction, u64 seed, std::vector<i64>& r,
+                  std::vector<i64>& c, std::vector<double>& v);
+std::vector<unsigned char> synthetic_image(i64 size, i64 rank, u64 seed);
+void synthetic_ratings(i64 users, i64 items, i64 rank, double fill, double noise, u64 seed, std::vector<i64>& r,
+                       std::vector<i64>& c, std::vector<double>& v);
+u64 derive_seed_u(u64 seed, u64 stream);
 }  // namespace svtb
 
 svt_mat* svtb_matrix_upload(svt_ctx* ctx, svtb::i64 m, svtb::i64 n, svtb::i64 row_begin, svtb::i64 row_end,
@@ -1104,6 +1111,79 @@ int svt_synth_config(int config, uint64_t seed, int64_t* m, int64_t* n, int64_t*
 int svt_synth_config_csr(int config, uint64_t seed, int64_t* m, int64_t* n, int64_t* nnz, int64_t* rowptr,
                          int64_t* col, double* val) {
     return guard([&] { synth_config_csr(config, seed, m, n, nnz, rowptr, col, val); });
+}
+
+// ---- the reference's experiment generators (synth.hpp; the CLI's inputs) ----
+uint64_t svt_derive_seed(uint64_t seed, uint64_t stream) { return derive_seed_u(seed, stream); }  // dense.hpp:44
+
+int svt_make_low_rank(int64_t m, int64_t n, int64_t rank, uint64_t seed, double* out) {  // synth.hpp:21-28
+    return guard([&] {
+        need(out, "svt_make_low_rank");
+        const std::vector<double> A = make_low_rank_cm(m, n, rank, seed);
+        std::memcpy(out, A.data(), sizeof(double) * A.size());
+    });
+}
+
+int svt_sample_dense(int64_t m, int64_t n, const double* A, double fraction, uint64_t seed, svt_triplets** out) {
+    return guard([&] {  // synth.hpp:64-84
+        need(A, "svt_sample_dense");
+        need(out, "svt_sample_dense");
+        if (m < 1 || n < 1) throw std::invalid_argument("sample_dense: bad dimensions");
+        auto T = std::make_unique<svt_triplets>();
+        T->t.m = m;
+        T->t.n = n;
+        sample_dense(m, n, A, fraction, seed, T->t.r, T->t.c, T->t.v);
+        *out = T.release();
+    });
+}
+
+int svt_synthetic_image(int64_t size, int64_t rank, uint64_t seed, uint8_t* pixels) {  // synth.hpp:89-114
+    return guard([&] {
+        need(pixels, "svt_synthetic_image");
+        const std::vector<unsigned char> px = synthetic_image(size, rank, seed);
+        std::memcpy(pixels, px.data(), px.size());
+    });
+}
+
+int svt_synthetic_ratings(int64_t users, int64_t items, int64_t rank, double fill, double noise, uint64_t seed,
+                          svt_triplets** out) {  // synth.hpp:119-160
+    return guard([&] {
+        need(out, "svt_synthetic_ratings");
+        auto T = std::make_unique<svt_triplets>();
+        synthetic_ratings(users, items, rank, fill, noise, seed, T->t.r, T->t.c, T->t.v);
+        T->t.m = users;
+        T->t.n = items;
+        T->t.user_ids.resize(static_cast<size_t>(users));
+        T->t.item_ids.resize(static_cast<size_t>(items));
+        for (int64_t u = 0; u < users; ++u) T->t.user_ids[static_cast<size_t>(u)] = u;
+        for (int64_t i = 0; i < items; ++i) T->t.item_ids[static_cast<size_t>(i)] = i;
+        T->t.provenance = "synthetic";
+        *out = T.release();
+    });
+}
+
+// solver.hpp:95-106 on the host: tau from the serial sum in CSR order (the
+// reference's summation order), so a front end can resolve its defaults and
+// reject bad input before a device context exists
+int svt_default_config_host(int64_t m, int64_t n, int64_t nnz, const double* csr_vals, svt_config* out) {
+    return guard([&] {
+        need(out, "svt_default_config_host");
+        if (m < 1 || n < 1 || nnz < 1 || !csr_vals) throw std::invalid_argument("default_config: empty sample set");
+        svt_config c{};
+        c.maxit = 500;
+        c.np = 1;
+        c.eps_stop = 1e-3;
+        c.eps_threshold0 = 0.5;
+        c.seed = 1;
+        double ss = 0.0;
+        for (int64_t k = 0; k < nnz; ++k) ss += csr_vals[k] * csr_vals[k];
+        c.tau = std::sqrt(ss);
+        c.delta = std::sqrt(static_cast<double>(m) * static_cast<double>(n) / static_cast<double>(nnz));
+        c.t0 = std::max<i64>(1, static_cast<i64>(0.05 * static_cast<double>(std::min(m, n))));
+        c.dt = 10;
+        c.beta = 0.95;
+        *out = c;
+    });
 }
 
 }  // extern "C"

@@ -420,6 +420,106 @@ void synth_config_csr(int config, u64 seed, i64* m, i64* n, i64* nnz, i64* rowpt
     if (val) std::memcpy(val, g_cache.val.data(), sizeof(double) * g_cache.val.size());
 }
 
+// --- the reference's experiment generators (synth.hpp), used by the CLI -----
+
+// synth.hpp:21-28: G1 G2^T / sqrt(rank), column-major m x n
+std::vector<double> make_low_rank_cm(i64 m, i64 n, i64 rank, u64 seed) {
+    if (rank < 1 || rank > std::min(m, n)) throw std::invalid_argument("make_low_rank: rank out of range");
+    const std::vector<double> G1 = gaussian_cm(m, rank, derive_seed_u(seed, 0));
+    const std::vector<double> G2 = gaussian_cm(n, rank, derive_seed_u(seed, 1));
+    const double s = std::sqrt(static_cast<double>(rank));
+    std::vector<double> A(static_cast<size_t>(m * n));
+    parallel_for(n, [&](i64 j0, i64 j1) {
+        for (i64 j = j0; j < j1; ++j)
+            for (i64 i = 0; i < m; ++i) {
+                double acc = 0.0;
+                for (i64 k = 0; k < rank; ++k) acc += G1[static_cast<size_t>(i + k * m)] * G2[static_cast<size_t>(j + k * n)];
+                A[static_cast<size_t>(i + j * m)] = acc / s;
+            }
+    });
+    return A;
+}
+
+// synth.hpp:64-84: exactly floor(fraction m n) uniformly drawn cells
+void sample_dense(i64 m, i64 n, const double* A_cm, double fraction, u64 seed, std::vector<i64>& r,
+                  std::vector<i64>& c, std::vector<double>& v) {
+    if (!(fraction > 0.0 && fraction <= 1.0)) throw std::invalid_argument("sample_dense: fraction must lie in (0, 1]");
+    const u64 total = static_cast<u64>(m) * static_cast<u64>(n);
+    const u64 ns = static_cast<u64>(std::floor(fraction * static_cast<double>(total) + 1e-9));
+    if (ns < 1) throw std::invalid_argument("sample_dense: fraction selects no entries");
+    r.clear(), c.clear(), v.clear();
+    for (u64 pos : sample_positions(total, ns, seed)) {
+        const i64 i = static_cast<i64>(pos / static_cast<u64>(n)), j = static_cast<i64>(pos % static_cast<u64>(n));
+        r.push_back(i);
+        c.push_back(j);
+        v.push_back(A_cm[static_cast<size_t>(i + j * m)]);
+    }
+}
+
+// synth.hpp:89-114: sum of rank-1 sine-profile products, rescaled to
+// [0, 255], rounded and clamped (io.hpp:367-381); row-major pixels
+std::vector<unsigned char> synthetic_image(i64 size, i64 rank, u64 seed) {
+    if (size < 2 || rank < 1 || rank > size) throw std::invalid_argument("synthetic_image: bad size/rank");
+    Gauss stream(derive_seed_u(seed, 2));
+    const double pi = 3.14159265358979323846;
+    auto profile = [&](int term) {
+        std::vector<double> v(static_cast<size_t>(size));
+        const double freq = 0.5 + 0.35 * static_cast<double>(term) + 0.25 * std::abs(stream.next());
+        const double phase = pi * stream.next();
+        for (i64 i = 0; i < size; ++i) {
+            const double x = static_cast<double>(i) / static_cast<double>(size - 1);
+            v[static_cast<size_t>(i)] = std::sin(2.0 * pi * freq * x + phase);
+        }
+        return v;
+    };
+    std::vector<double> M(static_cast<size_t>(size * size), 0.0);
+    double weight = 1.0;
+    for (i64 t = 0; t < rank; ++t, weight *= 0.8) {
+        // the reference's expression evaluates its left profile first
+        const std::vector<double> a = profile(static_cast<int>(t));
+        const std::vector<double> b = profile(static_cast<int>(t));
+        for (i64 i = 0; i < size; ++i)
+            for (i64 j = 0; j < size; ++j)
+                M[static_cast<size_t>(i * size + j)] += (weight * a[static_cast<size_t>(i)]) * b[static_cast<size_t>(j)];
+    }
+    double lo = M[0], hi = M[0];
+    for (double x : M) lo = std::min(lo, x), hi = std::max(hi, x);
+    const double span = (hi > lo) ? (hi - lo) : 1.0;
+    std::vector<unsigned char> px(M.size());
+    for (size_t k = 0; k < M.size(); ++k)
+        px[k] = static_cast<unsigned char>(std::clamp(std::round(255.0 * (M[k] - lo) / span), 0.0, 255.0));
+    return px;
+}
+
+// synth.hpp:119-160: 3 + U V^T + noise on a uniform cell subset, half-star
+// steps clipped to [1, 5]
+void synthetic_ratings(i64 users, i64 items, i64 rank, double fill, double noise, u64 seed, std::vector<i64>& r,
+                       std::vector<i64>& c, std::vector<double>& v) {
+    if (users < 1 || items < 1 || rank < 1 || rank > std::min(users, items))
+        throw std::invalid_argument("synthetic_ratings: bad dimensions/rank");
+    if (!(fill > 0.0 && fill <= 1.0)) throw std::invalid_argument("synthetic_ratings: fill must lie in (0, 1]");
+    std::vector<double> U = gaussian_cm(users, rank, derive_seed_u(seed, 0));
+    const double sr = std::sqrt(static_cast<double>(rank));
+    for (double& x : U) x /= sr;
+    const std::vector<double> V = gaussian_cm(items, rank, derive_seed_u(seed, 1));
+    Gauss noise_stream(derive_seed_u(seed, 2));
+    const u64 total = static_cast<u64>(users) * static_cast<u64>(items);
+    const u64 ns = static_cast<u64>(std::floor(fill * static_cast<double>(total) + 1e-9));
+    if (ns < 2) throw std::invalid_argument("synthetic_ratings: fill selects fewer than 2 cells");
+    r.clear(), c.clear(), v.clear();
+    for (u64 pos : sample_positions(total, ns, derive_seed_u(seed, 3))) {
+        const i64 u = static_cast<i64>(pos / static_cast<u64>(items)), i = static_cast<i64>(pos % static_cast<u64>(items));
+        double dot = 0.0;
+        for (i64 k = 0; k < rank; ++k) dot += U[static_cast<size_t>(u + k * users)] * V[static_cast<size_t>(i + k * items)];
+        double x = 3.0 + dot + noise * noise_stream.next();
+        x = std::round(x * 2.0) / 2.0;
+        x = std::clamp(x, 1.0, 5.0);
+        r.push_back(u);
+        c.push_back(i);
+        v.push_back(x);
+    }
+}
+
 // the partial Fisher-Yates sampler for the formats module (io.cpp)
 std::vector<u64> sample_positions_exported(u64 total, u64 ns, u64 seed) { return sample_positions(total, ns, seed); }
 

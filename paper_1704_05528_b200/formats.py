@@ -228,6 +228,58 @@ def split_ratings(ds: RatingsDataset, train_fraction: float, seed: int, ctx: Con
     return ta.to_matrix(ctx), tb.to_matrix(ctx)
 
 
+# ---- the reference's experiment generators (synth.hpp) -------------------------------
+def derive_seed(seed: int, stream: int) -> int:
+    """derive_seed (dense.hpp:44)."""
+    L = _L()
+    L.svt_derive_seed.restype = C.c_uint64
+    return int(L.svt_derive_seed(C.c_uint64(seed), C.c_uint64(stream)))
+
+
+def make_low_rank(m: int, n: int, rank: int, seed: int) -> np.ndarray:
+    """make_low_rank (synth.hpp:21-28): G1 G2^T / sqrt(rank)."""
+    buf = np.zeros(max(m * n, 1))
+    _check(_L().svt_make_low_rank(C.c_int64(m), C.c_int64(n), C.c_int64(rank), C.c_uint64(seed), _ptr(buf)))
+    return buf[: m * n].reshape(n, m).T.copy()
+
+
+def sample_dense_triplets(A, fraction: float, seed: int):
+    """sample_dense (synth.hpp:64-84), host side: (m, n, rows, cols, vals) in draw order."""
+    A = np.asarray(A, dtype=np.float64)
+    buf = np.ascontiguousarray(A.T).ravel()
+    return _new(_L().svt_sample_dense, C.c_int64(A.shape[0]), C.c_int64(A.shape[1]),
+                _ptr(buf if buf.size else np.zeros(1)), C.c_double(fraction), C.c_uint64(seed)).arrays()
+
+
+def sample_dense(A, fraction: float, seed: int, ctx: Context | None = None) -> SampledMatrix:
+    m, n, r, c, v = sample_dense_triplets(A, fraction, seed)
+    return SampledMatrix(m, n, r, c, v, ctx=ctx or default_context())
+
+
+def synthetic_image(size: int, rank: int, seed: int) -> GrayImage:
+    """synthetic_image (synth.hpp:89-114)."""
+    px = np.zeros(max(size * size, 1), np.uint8)
+    _check(_L().svt_synthetic_image(C.c_int64(size), C.c_int64(rank), C.c_uint64(seed), px.ctypes.data_as(P_U8)))
+    return GrayImage(px[: size * size].reshape(size, size))
+
+
+def synthetic_ratings(users: int, items: int, rank: int, fill: float, noise: float, seed: int) -> RatingsDataset:
+    """synthetic_ratings (synth.hpp:119-160)."""
+    t = _new(_L().svt_synthetic_ratings, C.c_int64(users), C.c_int64(items), C.c_int64(rank), C.c_double(fill),
+             C.c_double(noise), C.c_uint64(seed))
+    m, n, r, c, v = t.arrays()
+    return RatingsDataset(m, n, r, c, v, np.arange(m), np.arange(n), "synthetic", t)
+
+
+def write_matrix_market_triplets(path: str, m: int, n: int, rows, cols, vals) -> None:
+    """write_matrix_market (io.hpp:176-193) of host triplets (validated and
+    ordered like the SampledMatrix constructor, sampled.hpp:27-62)."""
+    from .api import build_csr
+    rp, co, va = build_csr(m, n, rows, cols, vals)
+    _check(_L().svt_write_matrix_market(str(path).encode(), C.c_int64(m), C.c_int64(n), _ptr(rp, P_I64),
+                                        _ptr(co, P_I64), _ptr(va)))
+
+
 # ---- trace export ------------------------------------------------------------------------
 def _records(trace):
     from ._abi import IterationRecord

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "svt_b200.h")).read()
-    return sorted(set(re.findall(r"^(?:int|void\*|const char\*|int64_t) (svt_[a-z0-9_]+)\(", src, re.M)))
+    return sorted(set(re.findall(r"^(?:int|void\*|const char\*|int64_t|uint64_t) (svt_[a-z0-9_]+)\(", src, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
