@@ -493,6 +493,18 @@ def main():
                 sparse[k]["gather_ceiling_tbs"] = ceil_tbs
                 sparse[k]["gather_frac"] = sparse[k]["gather_tbs"] / ceil_tbs
                 sparse[k]["gather_ceiling_source"] = ceil_src
+    # the dense FP64 contractions against the measured DGEMM peak (north
+    # star: FP64 tensor-pipe utilisation of the orthogonalisation GEMMs);
+    # predicated products that the device skipped carry no flops
+    dense = {}
+    for k in ("cgs_gemm", "qr", "finalize"):
+        v = stats[k]
+        if v["total_ms"] > 0 and v["flops"] > 0:
+            tf = v["flops"] / (v["total_ms"] * 1e-3) / 1e12
+            dense[k] = {"achieved_tflops": tf, "peak_tflops": peak_f64, "frac": tf / peak_f64, "peak_kind": f64_kind,
+                        "launches": v["launches"], "ms_per_step": v["total_ms"] / psteps,
+                        "note": ("all launches of the class, incl. latency-bound single-CTA factorisations"
+                                 if k != "cgs_gemm" else "block Gram-Schmidt products (DMMA)")}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -550,6 +562,7 @@ def main():
                        "setup_s": round(setup_s, 2)},
             "roofline": roof,
             "sparse_roofline": sparse,
+            "dense_roofline": dense,
             "kernel_ms_per_step": {k: round(v["total_ms"] / psteps, 3) for k, v in stats.items()},
             "kernel_ms_per_step_in_step": {k: round(v["total_ms"] / psteps, 3) for k, v in stats_in_step.items()},
             "profiled_iterations": list(range(args.warmup + 1, args.warmup + psteps + 1)),

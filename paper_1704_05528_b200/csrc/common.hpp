@@ -302,6 +302,15 @@ struct LaunchScope {
                 const char* file = __builtin_FILE(), int line = __builtin_LINE());
     ~LaunchScope() noexcept(false);
 };
+// NVTX range around a host-side phase of the path (iteration, sketch batch,
+// Gram-Schmidt, CholQR, finalize, update): visible in Nsight Systems /
+// Compute timelines; a no-op unless a tool is attached (header-only NVTX3).
+struct NvtxRange {
+    explicit NvtxRange(const char* name);
+    ~NvtxRange();
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 // Blocking wait for the context stream (counted; timed when profiling).
 void print_gap_stats(svt_ctx* c);
 void sync_stream(svt_ctx* c, int site = __builtin_LINE(), const char* file = __builtin_FILE());

@@ -547,6 +547,7 @@ void qb_extend(Engine& E, QBDev& st, i64 dt, int np, u64 seed, const double* ome
 // small values), V = B^T W / sigma, U = Q W.  Kept mode computes only the
 // triplets with sigma > tau (the ones shrink keeps, solver.hpp:110-120).
 void finalize(Engine& E, const QBDev& st, FinalizeMode mode, double tau, DevFactors& out) {
+    NvtxRange nvtx("sketch.finalize");
     svt_ctx* c = E.ctx;
     const i64 r = st.rank, n = st.n, m = st.m_local;
     out.m_local = m;
@@ -925,6 +926,7 @@ static void batch_sketch(Engine& E, const svt_sketch_params& p, int round0, int 
     auto& sp = E.spec;
     const i64 w = p.dt, W = static_cast<i64>(K) * w, m = A->m_local, n = A->n;
     cudaStream_t s = side ? c->side : c->stream;
+    NvtxRange nvtx(side ? "r4svd.batch_sketch (side stream)" : "r4svd.batch_sketch");
     DevBuf<double>* part = side ? &sp.part : nullptr;
     u64 seeds[kMaxOmegaBatch];
     for (int k = 0; k < K; ++k) seeds[k] = derive_seed_u(p.seed, static_cast<u64>(round0 + k));
@@ -1008,6 +1010,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
     double* Q = st.Q.get();
     const i64 ldq = st.cap;
     if (r0 > 0) {
+        NvtxRange nvtx("r4svd.block_gram_schmidt");
         // block Gram-Schmidt against Q, then the reference's per-round test
         // ||Q^T X_k|| > 1e-8 ||X_k|| for a second pass (sketch.hpp:134).
         // After one pass ||Q^T X_k|| is a rounding residual, at most
@@ -1087,6 +1090,7 @@ static int qb_extend_batch(Engine& E, QBDev& st, const svt_sketch_params& p, int
                          static_cast<long long>(r0), read_flag(c, F_CHECK), read_flag(c, F_SECOND));
     }
     launch_spec();  // (r0 == 0: no Gram-Schmidt kernels before it)
+    NvtxRange nvtx_qr("r4svd.cholqr2 + coefficients");
     // one Cholesky QR (twice) of the whole panel: nested spans per block
     E.GW.ensure(static_cast<size_t>(Wc * Wc));
     E.RW.ensure(static_cast<size_t>(Wc * Wc));

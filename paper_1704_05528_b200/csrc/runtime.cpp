@@ -1,5 +1,6 @@
 // Context runtime: launch accounting / CUDA-event instrumentation and the
 // NCCL communicator (resolved with dlopen so single-GPU use never needs it).
+#include <nvtx3/nvToolsExt.h>
 #include <dlfcn.h>
 
 #include <chrono>
@@ -237,5 +238,8 @@ void Comm::destroy() {
         handle = nullptr;
     }
 }
+
+NvtxRange::NvtxRange(const char* name) { nvtxRangePushA(name); }
+NvtxRange::~NvtxRange() { nvtxRangePop(); }
 
 }  // namespace svtb

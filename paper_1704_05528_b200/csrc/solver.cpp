@@ -8,6 +8,7 @@
 // reference's two project_low_rank passes, two sp_axpy passes, residual and
 // train_mae (solver.hpp:279, 287, 321-323).  Cooling, best-so-far, stop rule
 // and observer are host logic in the reference's order.
+#include <nvtx3/nvToolsExt.h>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -229,6 +230,7 @@ void solver_step(svt_solver* S, svt_observer_fn obs, void* user, svt_record* rec
     const svt_config& cfg = S->cfg;
     Engine& E = engine_of(S);
     const int iter = ++S->iter;
+    NvtxRange nvtx_iter("svt.iteration");
     const u64 iter_seed = derive_seed_u(cfg.seed, static_cast<u64>(iter));
     svt_sketch_params sp{};
     sp.t = cfg.t0;
@@ -242,6 +244,8 @@ void solver_step(svt_solver* S, svt_observer_fn obs, void* user, svt_record* rec
     const double t_sketch = now_ms();
     i64 revealed = 0;
     int rounds = 0;
+    nvtxRangePushA("svt.partial_svd + shrink");
+    try {
     switch (S->backend.kind) {
         case SVT_BACKEND_R4SVD:
         case SVT_BACKEND_R3SVD: {
@@ -271,7 +275,13 @@ void solver_step(svt_solver* S, svt_observer_fn obs, void* user, svt_record* rec
         default:
             throw std::invalid_argument("svt_run_backend: unknown backend");
     }
+    } catch (...) {
+        nvtxRangePop();
+        throw;
+    }
+    nvtxRangePop();
     const double sketch_ms = now_ms() - t_sketch;
+    NvtxRange nvtx_update("svt.residual + sddmm_update");
 
     // X = shrink(...): U (m_local x k), sigma - tau, V (n x k); Vs = V diag(sigma - tau)
     DevFactors& X = S->X;
