@@ -2363,6 +2363,10 @@ void sym_eig(svt_ctx* ctx, double* G, i64 r, double* W, double* lambda) {
     constexpr i64 kJbSmem = 200 * 1024;
     i64 bsz = std::min<i64>(16, kJbSmem / (32 * (r + 1)));
     bsz = std::min<i64>(bsz, std::max<i64>(1, r / 64));
+    if (const char* e = std::getenv("SVTB_JACOBI_B")) {  // tuning: block width override (must fit shared memory)
+        const i64 want = std::atoll(e);
+        if (want >= 1 && 32 * want * (r + 2 * want) <= kJbSmem) bsz = want;
+    }
     const bool blocked = bsz >= 1 && std::getenv("SVTB_JACOBI_SCALAR") == nullptr;
     const i64 rp = blocked ? (r + 2 * bsz - 1) / (2 * bsz) * (2 * bsz) : (r + 1) & ~1LL;
     // floor at a 1056-wide problem (the dense-Gram finalize range): the

@@ -383,7 +383,7 @@ struct UsageError : std::runtime_error {
 };
 
 struct Option {
-    enum Type { Flag, Str, Int, Real, Uint, IntList, StrList } type;
+    enum Type { Flag, Str, Int, Int32, Real, Uint, IntList, StrList } type;
     void* target;
     std::string help;
     std::vector<std::string> members;  // allowed values (Str)
@@ -440,13 +440,8 @@ void assign(const std::string& flag, Option& o, const std::string& v) {
                 throw UsageError(kUsageValidation, flag + ": " + v + " not in the allowed set");
             *static_cast<std::string*>(o.target) = v;
             break;
-        case Option::Int:
-            if (o.help == "int32") {
-                *static_cast<int*>(o.target) = static_cast<int>(to_int(flag, v));
-            } else {
-                *static_cast<long long*>(o.target) = to_int(flag, v);
-            }
-            break;
+        case Option::Int: *static_cast<long long*>(o.target) = to_int(flag, v); break;
+        case Option::Int32: *static_cast<int*>(o.target) = static_cast<int>(to_int(flag, v)); break;
         case Option::Uint: {
             if (!v.empty() && v[0] == '-') throw UsageError(kUsageConversion, "could not convert " + flag + " = " + v);
             char* end = nullptr;
@@ -473,26 +468,48 @@ void add_solver_flags(Command& cmd, SolverFlags& f) {
     cmd.add("--delta", Option::Real, &f.delta, "Step size (default sqrt(m n / ns))");
     cmd.add("--dt", Option::Int, &f.dt, "Sampling increment per extension round (default 10)");
     cmd.add("--t0", Option::Int, &f.t0, "Initial sampling size (default floor(0.05 min(m,n)))");
-    cmd.add("--np", Option::Int, &f.np, "int32");
+    cmd.add("--np", Option::Int32, &f.np, "Power iteration passes (default 1)");
     cmd.add("--beta", Option::Real, &f.beta, "Annealing factor (default 0.95)");
     cmd.add("--eps-threshold0", Option::Real, &f.eps_threshold0, "Initial sketch error-percentage target (default 0.5)");
     cmd.add("--stop-mae", Option::Real, &f.stop_mae, "Stop when train MAE drops below this");
     cmd.add("--stop-residual", Option::Real, &f.stop_residual, "Stop when the sample-set residual drops below this");
     cmd.add("--maxit", Option::Int, &f.maxit, "Iteration cap (default 500)");
     cmd.add("--seed", Option::Uint, &f.seed, "Master seed");
-    cmd.add("--threads", Option::Int, &f.threads, "int32");
+    cmd.add("--threads", Option::Int32, &f.threads, "Kernel thread cap; 1 is bit-reproducible");
     cmd.add("--out-prefix", Option::Str, &f.out_prefix, "Artifact path prefix");
     cmd.add("--trace-out", Option::Str, &f.trace_out, "Trace CSV path (default <prefix>.trace.csv)");
 }
 
-std::string usage(const std::vector<Command*>& cmds) {
+std::string usage(const std::vector<Command*>& cmds, const Command* cur = nullptr) {
     std::string out =
-        "Low-rank matrix completion via singular value thresholding with adaptive randomized partial SVD\n"
-        "Usage: svt [--manifest FILE] [SUBCOMMAND] [OPTIONS]\n\nSubcommands:\n";
-    for (const Command* c : cmds) out += "  " + c->name + "  " + c->help + "\n";
-    out += "\nSolver options (every subcommand):\n";
-    for (const auto& o : cmds.front()->options)
-        if (o.first.rfind("--", 0) == 0) out += "  " + o.first + "\n";
+        "Low-rank matrix completion via singular value thresholding with adaptive randomized partial SVD\n";
+    auto options_of = [&](const Command& c) {
+        for (const auto& o : c.options) {
+            std::string line = "  " + o.first;
+            if (o.second.type != Option::Flag) line += " VALUE";
+            if (!o.second.members.empty()) {
+                line += " {";
+                for (std::size_t k = 0; k < o.second.members.size(); ++k) line += (k ? "," : "") + o.second.members[k];
+                line += "}";
+            }
+            if (line.size() < 34) line.resize(34, ' ');
+            out += line + " " + o.second.help + "\n";
+        }
+    };
+    if (cur != nullptr) {
+        out += "Usage: svt " + cur->name + (cur->positional ? " [" + cur->positional_name + "]" : "") + " [OPTIONS]\n  " +
+               cur->help + "\n\nOptions:\n";
+        options_of(*cur);
+        return out;
+    }
+    out += "Usage: svt [--manifest FILE] [SUBCOMMAND] [OPTIONS]\n\nOptions:\n"
+           "  --manifest FILE                   Re-execute a previously written run manifest\n\nSubcommands:\n";
+    for (const Command* c : cmds) {
+        std::string line = "  " + c->name;
+        line.resize(12, ' ');
+        out += line + c->help + "\n";
+    }
+    out += "\nRun `svt SUBCOMMAND --help` for the subcommand's options.\n";
     return out;
 }
 
@@ -1129,14 +1146,15 @@ int main(int argc, char** argv) {
 
     std::vector<Command*> cmds{&complete, &image, &ratings, &bench};
     bool help = false;
+    Command* parsed = nullptr;
     try {
-        parse_args(argc, argv, cmds, manifest_path, help);
+        parsed = parse_args(argc, argv, cmds, manifest_path, help);
     } catch (const UsageError& e) {
         std::fprintf(stderr, "%s\nRun with --help for more information.\n", e.what());
         return e.code;
     }
     if (help) {
-        std::printf("%s", usage(cmds).c_str());
+        std::printf("%s", usage(cmds, parsed).c_str());
         return 0;
     }
 
