@@ -187,6 +187,11 @@ struct SegPlanView {
     // entries) walked by one warp with one continuous gather pipeline
     long long ngrp = 0;
     const int* grp_first = nullptr;  // ngrp + 1 segment offsets
+    // 32-entry chunks of the segments, as an exclusive prefix over the
+    // segments (nseg + 1 values): the chunk-balanced static partition of the
+    // fused SDDMM update
+    long long nchunks = 0;
+    const long long* chunk_off = nullptr;
 };
 constexpr int kGrpSegs = 32;
 // Shared-memory-tiled view of the same CSR / CSC pattern for wide panels

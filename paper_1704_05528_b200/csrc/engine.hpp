@@ -15,6 +15,7 @@ struct SegPlan {
     svtb::DevBuf<int> seg_row, seg_slot, long_row, long_first, long_count;
     svtb::DevBuf<long long> seg_beg, seg_end;
     svtb::DevBuf<int> grp_first;
+    svtb::DevBuf<long long> chunk_off;
     svtb::SegPlanView v;
 };
 

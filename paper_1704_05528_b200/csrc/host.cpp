@@ -89,9 +89,18 @@ void build_groups(const std::vector<long long>& beg, const std::vector<long long
     gf.push_back(static_cast<int>(nsegs));
     P.grp_first.alloc(gf.size());
     SVT_CUDA(cudaMemcpyAsync(P.grp_first.get(), gf.data(), sizeof(int) * gf.size(), cudaMemcpyHostToDevice, s));
-    SVT_CUDA(cudaStreamSynchronize(s));  // gf dies here
+    // 32-entry chunks per segment, exclusive prefix (sddmm_warp_kernel's partition)
+    std::vector<long long> co(static_cast<size_t>(nsegs) + 1);
+    co[0] = 0;
+    for (i64 k = 0; k < nsegs; ++k)
+        co[static_cast<size_t>(k) + 1] = co[static_cast<size_t>(k)] + (end[static_cast<size_t>(k)] - beg[static_cast<size_t>(k)] + 31) / 32;
+    P.chunk_off.alloc(co.size());
+    SVT_CUDA(cudaMemcpyAsync(P.chunk_off.get(), co.data(), sizeof(long long) * co.size(), cudaMemcpyHostToDevice, s));
+    SVT_CUDA(cudaStreamSynchronize(s));  // gf / co die here
     P.v.ngrp = static_cast<long long>(gf.size()) - 1;
     P.v.grp_first = P.grp_first.get();
+    P.v.nchunks = co.back();
+    P.v.chunk_off = P.chunk_off.get();
 }
 
 // Row segmentation for the load-balanced SpMM (sparse.cu): rows longer than

@@ -333,6 +333,10 @@ void launch_narrow(svt_ctx* ctx, cudaStream_t s, const SegPlanView& plan, const 
 
 // ---- fused SDDMM + Bregman update + reductions ------------------------------
 constexpr int kSddmmWarps = 8;
+#ifndef SVTB_SDDMM_MINB
+#define SVTB_SDDMM_MINB 4
+#endif
+constexpr int kSddmmMinBlocksSmallK = SVTB_SDDMM_MINB;  // resident CTAs asked of the compiler for k <= 4
 constexpr int kSddmmU = 4;  // entries per lane group in flight
 
 // Fused SDDMM + Bregman update + reductions for kept ranks k > 64 (config 2
@@ -465,7 +469,7 @@ __global__ void mirror_csc_kernel(long long nnz, const int* __restrict__ csc2csr
 // lane j of each group, and one shuffle hands it to the lane that owns the
 // entry, so the update, its Y store and the four sums run lane-parallel.
 template <int KP, bool TWO>
-__global__ void __launch_bounds__(32 * kSddmmWarps, (KP >= 16 ? 2 : 3)) sddmm_warp_kernel(
+__global__ void __launch_bounds__(32 * kSddmmWarps, (KP >= 16 ? 2 : (KP >= 8 ? 3 : kSddmmMinBlocksSmallK))) sddmm_warp_kernel(
     SegPlanView plan, const int* __restrict__ col, const double* __restrict__ A, double* __restrict__ Y,
     double* __restrict__ Ycsc, const int* __restrict__ csr2csc, const double* __restrict__ U, long long ldu,
     const double* __restrict__ Vs, long long ldv, int k, double delta, int mode, double* __restrict__ partials) {
@@ -479,10 +483,9 @@ __global__ void __launch_bounds__(32 * kSddmmWarps, (KP >= 16 ? 2 : 3)) sddmm_wa
     double s_abs = 0.0, s_sq = 0.0, s_res = 0.0, s_y = 0.0;
     const bool lo = j < k, hi = TWO && j + 32 < k;
     const int jl0 = lo ? j : 0, jl1 = hi ? j + 32 : 0;  // clamped: unconditional loads, zero weight
-    for (long long sg = static_cast<long long>(blockIdx.x) * kSddmmWarps + warp; sg < plan.nseg;
-         sg += static_cast<long long>(gridDim.x) * kSddmmWarps) {
-        const long long row = plan.seg_row[sg];
-        const long long beg = plan.seg_beg[sg], end = plan.seg_end[sg];
+    // entries [beg, end) of one row (a segment or a part of one): 32-entry
+    // chunks with the next chunk's stream loads in flight
+    auto run = [&](long long row, long long beg, long long end) {
         const double* ur = U + row * ldu;
         const double u0 = lo ? __ldg(ur + j) : 0.0;
         const double u1 = hi ? __ldg(ur + j + 32) : 0.0;
@@ -541,6 +544,50 @@ __global__ void __launch_bounds__(32 * kSddmmWarps, (KP >= 16 ? 2 : 3)) sddmm_wa
                 } else {
                     s_y = fma(y_old, y_old, s_y);
                 }
+            }
+        }
+        };
+    if (plan.chunk_off == nullptr) {  // static partition by segments
+        for (long long sg = static_cast<long long>(blockIdx.x) * kSddmmWarps + warp; sg < plan.nseg;
+             sg += static_cast<long long>(gridDim.x) * kSddmmWarps)
+            run(plan.seg_row[sg], plan.seg_beg[sg], plan.seg_end[sg]);
+    } else {
+        // Chunk-balanced static partition: warp w of W owns the chunks
+        // [C w / W, C (w + 1) / W) of the segments' 32-entry chunks in
+        // segment order (a segment may be shared by two warps: the update
+        // has no reduction along a row).  Power-law patterns give the
+        // per-segment partition warps of very different loads; every warp of
+        // a CTA then waits at the final barrier for the slowest one (ncu:
+        // a third of the stall cycles).  Static, so the sums stay
+        // deterministic.
+        const long long W = static_cast<long long>(gridDim.x) * kSddmmWarps;
+        const long long gw = static_cast<long long>(blockIdx.x) * kSddmmWarps + warp;
+        const long long C = plan.nchunks;
+        long long c = C / W * gw + min(gw, C % W);
+        const long long c1 = c + C / W + (gw < C % W ? 1 : 0);
+        if (c < c1) {
+            // last segment sg with chunk_off[sg] <= c: 32-ary search, one probe per lane
+            long long lo_s = 0, hi_s = plan.nseg;  // answer in [lo_s, hi_s)
+            while (hi_s - lo_s > 1) {
+                const long long step = (hi_s - lo_s + 31) / 32;
+                const long long probe = lo_s + step * lane;
+                const bool ok = probe < hi_s && __ldg(plan.chunk_off + probe) <= c;
+                const unsigned m = __ballot_sync(0xffffffffu, ok);
+                const int top = 31 - __clz(static_cast<int>(m));  // lane 0 always ok (chunk_off[lo_s] <= c)
+                const long long nlo = lo_s + step * top;
+                hi_s = min(hi_s, nlo + step);
+                lo_s = nlo;
+            }
+            long long sg = lo_s;
+            while (c < c1) {
+                const long long off = __ldg(plan.chunk_off + sg), nxt = __ldg(plan.chunk_off + sg + 1);
+                if (nxt > c) {
+                    const long long beg = plan.seg_beg[sg], end = plan.seg_end[sg];
+                    const long long cend = min(nxt, c1);
+                    run(plan.seg_row[sg], beg + 32 * (c - off), min(end, beg + 32 * (cend - off)));
+                    c = cend;
+                }
+                ++sg;
             }
         }
     }
@@ -983,6 +1030,7 @@ void sddmm_update(svt_ctx* ctx, const SegPlanView& plan, i64 m_local, const int*
                   i64 ldv, i64 k, double delta, int mode, double* d_sums4) {
     const int blocks =
         std::max(1, std::min<int>(ctx->num_sms * 8, static_cast<int>((plan.nseg + kSddmmWarps - 1) / kSddmmWarps)));
+    int blocks_launched = blocks;
     ctx->ws_partial2.ensure(static_cast<size_t>(blocks) * 4);
     {
         // col 4 + A 8 + Y in 8 + Y out 8 (+ CSC mirror 4 + 8) per
@@ -990,9 +1038,27 @@ void sddmm_update(svt_ctx* ctx, const SegPlanView& plan, i64 m_local, const int*
         const double per = (mode == 1) ? (Ycsc ? 40.0 : 28.0) : 20.0;
         LaunchScope ls(ctx, K_SDDMM, per * nnz + 8.0 * (m_local + 1) + 8.0 * k * (m_local + n), 2.0 * nnz * k);
         double* part = ctx->ws_partial2.get();
+        // the chunk-balanced partition gives every warp the same load, so the
+        // grid is whole waves of the CTAs resident at once (no part-filled
+        // last wave): SVTB_SDDMM_WAVES x occupancy x SMs
+        static const int waves = [] {
+            const char* e = std::getenv("SVTB_SDDMM_WAVES");
+            return e ? std::max(1, std::atoi(e)) : 1;
+        }();
 #define SVT_SDDMM_W(KP, TWO)                                                                             \
-    sddmm_warp_kernel<KP, TWO><<<blocks, 32 * kSddmmWarps, 0, ctx->stream>>>(                            \
-        plan, col, A, Y, Ycsc, csr2csc, U, ldu, Vs, ldv, static_cast<int>(k), delta, mode, part)
+    do {                                                                                                 \
+        int gridb = blocks;                                                                              \
+        if (plan.chunk_off != nullptr) {                                                                 \
+            static int occ = 0;                                                                          \
+            if (occ == 0)                                                                                \
+                SVT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sddmm_warp_kernel<KP, TWO>,  \
+                                                                       32 * kSddmmWarps, 0));            \
+            gridb = std::max(1, std::min(blocks, waves * std::max(1, occ) * ctx->num_sms));              \
+        }                                                                                                \
+        sddmm_warp_kernel<KP, TWO><<<gridb, 32 * kSddmmWarps, 0, ctx->stream>>>(                         \
+            plan, col, A, Y, Ycsc, csr2csc, U, ldu, Vs, ldv, static_cast<int>(k), delta, mode, part);    \
+        blocks_launched = gridb;                                                                         \
+    } while (0)
         if (k <= 1)
             SVT_SDDMM_W(1, false);
         else if (k <= 2)
@@ -1013,7 +1079,7 @@ void sddmm_update(svt_ctx* ctx, const SegPlanView& plan, i64 m_local, const int*
 #undef SVT_SDDMM_W
     }
     LaunchScope ls(ctx, K_OTHER, 0.0, 0.0);
-    reduce4_kernel<<<1, 128, 0, ctx->stream>>>(ctx->ws_partial2.get(), blocks, d_sums4);
+    reduce4_kernel<<<1, 128, 0, ctx->stream>>>(ctx->ws_partial2.get(), blocks_launched, d_sums4);
 }
 
 void mirror_csc(svt_ctx* ctx, i64 nnz, const int* csc2csr, const double* Y, double* Ycsc) {
