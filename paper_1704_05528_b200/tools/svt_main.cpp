@@ -982,7 +982,7 @@ int run_ratings(const Json& man) {
         out << "iter,train_mae,test_mae\n";
         char buf[96];
         for (std::size_t i = 0; i < result.trace.size(); ++i) {
-            // an iteration that met the stop rule is not shown to the observer
+            // the observer sees every iteration (solver.hpp:311-314); the fallback only guards the index
             const double tm = i < watch.test_maes.size() ? watch.test_maes[i] : result.trace[i].test_mae;
             std::snprintf(buf, sizeof(buf), "%d,%.17g,%.17g\n", result.trace[i].iter, result.trace[i].train_mae, tm);
             out << buf;

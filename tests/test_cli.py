@@ -269,3 +269,40 @@ def test_ratings_early_stop_fires_on_the_test_mae_minimum(tmp_path):  # test_cli
     for r, rec in zip(rows, ref.trace):
         assert abs(float(r[1]) - rec["train_mae"]) <= 1e-8 * rec["train_mae"]
         assert abs(float(r[2]) - rec["test_mae"]) <= 1e-8 * rec["test_mae"]
+
+
+@gpu
+def test_image_and_ratings_from_files(tmp_path):
+    """The file-input modes (svt_main.cpp:597-604, 626-636): a PGM image and
+    a delimited ratings file; the manifests replay from the same files."""
+    img = F.synthetic_image(40, 4, 11)
+    pgm = str(tmp_path / "in.pgm")
+    F.write_pgm(img, pgm)
+    p1 = str(tmp_path / "img")
+    assert run_cli("image", pgm, "--fraction", 0.7, "--maxit", 150, "--seed", 2, "--out-prefix", p1).returncode in (0, 3)
+    assert os.path.exists(p1 + ".recovered.pgm") and not os.path.exists(p1 + ".original.pgm")
+    man = json.load(open(p1 + ".manifest.json"))
+    assert man["input"] == {"kind": "file", "path": pgm, "fraction": 0.7} and man["stop"]["threshold"] == 1.0
+    rec = F.read_pgm(p1 + ".recovered.pgm")
+    assert rec.pixels.shape == img.pixels.shape
+    first = open(p1 + ".sigma.mtx", "rb").read()
+    assert run_cli("--manifest", p1 + ".manifest.json").returncode in (0, 3)
+    assert open(p1 + ".sigma.mtx", "rb").read() == first
+
+    ds = F.synthetic_ratings(60, 45, 3, 0.4, 0.2, 5)
+    path = str(tmp_path / "ratings.dat")
+    with open(path, "w") as f:
+        for u, i, r in zip(ds.rows, ds.cols, ds.vals):
+            f.write(f"{1000 + u}::{77 + 2 * i}::{r:g}::0\n")
+    p2 = str(tmp_path / "rat")
+    rc = run_cli("ratings", path, "--train-fraction", 0.8, "--maxit", 30, "--stop-mae", 0.05, "--seed", 4,
+                 "--out-prefix", p2).returncode
+    assert rc in (0, 3)
+    users = [ln.split("\t") for ln in open(p2 + ".users.tsv").read().splitlines()]
+    items = [ln.split("\t") for ln in open(p2 + ".items.tsv").read().splitlines()]
+    assert len(users) == len(set(ds.rows)) and len(items) == len(set(ds.cols))
+    assert all(int(uid) >= 1000 for _, uid in users) and [int(k) for k, _ in users] == list(range(len(users)))
+    rows = list(open(p2 + ".test_mae.csv"))[1:]
+    assert len(rows) == trace_length(p2 + ".trace.csv") > 0
+    met = json.load(open(p2 + ".metrics.json"))
+    assert met["final_test_mae"] == float(rows[-1].split(",")[2])
