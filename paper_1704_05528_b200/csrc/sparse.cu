@@ -460,7 +460,7 @@ __global__ void mirror_csc_kernel(long long nnz, const int* __restrict__ csc2csr
 // Fused SDDMM + update for k <= 64, one warp per row segment, 32 entries per
 // chunk.  The warp is G = 32 / KP lane groups of KP lanes (KP = k rounded up
 // to a power of two, <= 32); lane j of a group holds U[i, j] (and, TWO,
-// U[i, j + 32]) for the whole segment.  Per chunk the entries' index, A and Y
+// U[i, j + KP], ... S columns per lane) for the whole segment.  Per chunk the entries' index, A and Y
 // are loaded coalesced (lane = entry) one chunk ahead; step s = 0..KP-1
 // gathers, in every group g, the factor row of entry s*G + g (coalesced
 // across the group's lanes) — the KP steps' loads are independent and all in
@@ -468,7 +468,7 @@ __global__ void mirror_csc_kernel(long long nnz, const int* __restrict__ csc2csr
 // (KP/2 + ... + 1 shuffles) then leaves the complete dot product of step j on
 // lane j of each group, and one shuffle hands it to the lane that owns the
 // entry, so the update, its Y store and the four sums run lane-parallel.
-template <int KP, bool TWO>
+template <int KP, int S>
 __global__ void __launch_bounds__(32 * kSddmmWarps, (KP >= 16 ? 2 : (KP >= 8 ? 3 : kSddmmMinBlocksSmallK))) sddmm_warp_kernel(
     SegPlanView plan, const int* __restrict__ col, const double* __restrict__ A, double* __restrict__ Y,
     double* __restrict__ Ycsc, const int* __restrict__ csr2csc, const double* __restrict__ U, long long ldu,
@@ -481,14 +481,21 @@ __global__ void __launch_bounds__(32 * kSddmmWarps, (KP >= 16 ? 2 : (KP >= 8 ? 3
     // lane holding the sum of the entry this lane owns (entry l = s * G + g')
     const int src = (lane % G) * KP + lane / G;
     double s_abs = 0.0, s_sq = 0.0, s_res = 0.0, s_y = 0.0;
-    const bool lo = j < k, hi = TWO && j + 32 < k;
-    const int jl0 = lo ? j : 0, jl1 = hi ? j + 32 : 0;  // clamped: unconditional loads, zero weight
+    // lane j of a group holds columns j, j + KP, ..., j + (S - 1) KP (k <= S KP)
+    bool has[S];
+    int jl[S];  // clamped: unconditional loads, zero weight
+#pragma unroll
+    for (int t = 0; t < S; ++t) {
+        has[t] = j + t * KP < k;
+        jl[t] = has[t] ? j + t * KP : 0;
+    }
     // entries [beg, end) of one row (a segment or a part of one): 32-entry
     // chunks with the next chunk's stream loads in flight
     auto run = [&](long long row, long long beg, long long end) {
         const double* ur = U + row * ldu;
-        const double u0 = lo ? __ldg(ur + j) : 0.0;
-        const double u1 = hi ? __ldg(ur + j + 32) : 0.0;
+        double u[S];
+#pragma unroll
+        for (int t = 0; t < S; ++t) u[t] = has[t] ? __ldg(ur + jl[t]) : 0.0;
         long long e = beg + lane;
         int cl_n = (e < end) ? __ldg(col + e) : 0;
         double a_n = (e < end) ? __ldg(A + e) : 0.0;
@@ -509,8 +516,9 @@ __global__ void __launch_bounds__(32 * kSddmmWarps, (KP >= 16 ? 2 : (KP >= 8 ? 3
                 for (int s = 0; s < KP; ++s) {
                     const int c = __shfl_sync(0xffffffffu, cl, s * G + g);
                     const double* vr = Vs + static_cast<long long>(c) * ldv;
-                    p[s] = u0 * __ldg(vr + jl0);
-                    if (TWO) p[s] = fma(u1, __ldg(vr + jl1), p[s]);
+                    p[s] = u[0] * __ldg(vr + jl[0]);
+#pragma unroll
+                    for (int t = 1; t < S; ++t) p[s] = fma(u[t], __ldg(vr + jl[t]), p[s]);
                 }
             } else {  // shrink kept nothing: no factor rows exist
 #pragma unroll
@@ -1041,38 +1049,58 @@ void sddmm_update(svt_ctx* ctx, const SegPlanView& plan, i64 m_local, const int*
         // the chunk-balanced partition gives every warp the same load, so the
         // grid is whole waves of the CTAs resident at once (no part-filled
         // last wave): SVTB_SDDMM_WAVES x occupancy x SMs
+        static const int slots = [] {
+            const char* e = std::getenv("SVTB_SDDMM_SLOTS");
+            return e ? std::atoi(e) : 4;
+        }();
         static const int waves = [] {
             const char* e = std::getenv("SVTB_SDDMM_WAVES");
             return e ? std::max(1, std::atoi(e)) : 1;
         }();
-#define SVT_SDDMM_W(KP, TWO)                                                                             \
+#define SVT_SDDMM_W(KP, SL)                                                                             \
     do {                                                                                                 \
         int gridb = blocks;                                                                              \
         if (plan.chunk_off != nullptr) {                                                                 \
             static int occ = 0;                                                                          \
             if (occ == 0)                                                                                \
-                SVT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sddmm_warp_kernel<KP, TWO>,  \
+                SVT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, sddmm_warp_kernel<KP, SL>,   \
                                                                        32 * kSddmmWarps, 0));            \
             gridb = std::max(1, std::min(blocks, waves * std::max(1, occ) * ctx->num_sms));              \
         }                                                                                                \
-        sddmm_warp_kernel<KP, TWO><<<gridb, 32 * kSddmmWarps, 0, ctx->stream>>>(                         \
+        sddmm_warp_kernel<KP, SL><<<gridb, 32 * kSddmmWarps, 0, ctx->stream>>>(                         \
             plan, col, A, Y, Ycsc, csr2csc, U, ldu, Vs, ldv, static_cast<int>(k), delta, mode, part);    \
         blocks_launched = gridb;                                                                         \
     } while (0)
+        // columns per lane (SVTB_SDDMM_SLOTS = 1 / 2 / 4, default 4): wider k on a
+        // narrower lane group — fewer idle lanes just above a power of two, a
+        // shorter butterfly and fewer partial sums in registers.  Measured
+        // (update + mirror): cfg4 k = 10 282 -> 232 us, k = 20 385 -> 324,
+        // k = 50 498 -> 452; cfg5 k = 50 4.96 -> 4.47 ms; 8 columns per lane
+        // spill and lose the coalescing (cfg5 k = 50: 6.1 ms)
         if (k <= 1)
-            SVT_SDDMM_W(1, false);
+            SVT_SDDMM_W(1, 1);
         else if (k <= 2)
-            SVT_SDDMM_W(2, false);
+            SVT_SDDMM_W(2, 1);
         else if (k <= 4)
-            SVT_SDDMM_W(4, false);
+            SVT_SDDMM_W(4, 1);
         else if (k <= 8)
-            SVT_SDDMM_W(8, false);
-        else if (k <= 16)
-            SVT_SDDMM_W(16, false);
-        else if (k <= 32)
-            SVT_SDDMM_W(32, false);
-        else if (k <= 64)
-            SVT_SDDMM_W(32, true);
+            SVT_SDDMM_W(8, 1);
+        else if (k <= 16) {
+            if (slots >= 2)
+                SVT_SDDMM_W(8, 2);
+            else
+                SVT_SDDMM_W(16, 1);
+        } else if (k <= 32) {
+            if (slots >= 2)
+                SVT_SDDMM_W(16, 2);
+            else
+                SVT_SDDMM_W(32, 1);
+        } else if (k <= 64) {
+            if (slots >= 4)
+                SVT_SDDMM_W(16, 4);
+            else
+                SVT_SDDMM_W(32, 2);
+        }
         else
             sddmm_update_kernel<32><<<blocks, 32 * kSddmmWarps, 0, ctx->stream>>>(plan, col, A, Y, Ycsc, csr2csc,
                                                                                 U, ldu, Vs, ldv, k, delta, mode, part);
