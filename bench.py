@@ -395,17 +395,28 @@ def main():
             T2 = G.SampledMatrix.from_csr(m, n, host["trp"], host["tco"], host["tva"], ctx=ctx,
                                           row_block=(0, re_ - rb)) \
                 if world == 1 else G.SampledMatrix.from_csr(m, n, *test, ctx=ctx, row_block=(rb, re_))
+        t_up = time.perf_counter()
         s2 = G.Solver.resume(A2, cfg, stop, ck_h, test=T2)
-        recs2 = [s2.step() for _ in range(args.steps)]
+        t_res = time.perf_counter()
+        recs2, t_it = [], []
+        for _ in range(args.steps):
+            recs2.append(s2.step())
+            t_it.append(time.perf_counter())
         res = s2.result()
         ctx.sync()
-        el = max_over_ranks(time.perf_counter() - t0)
+        t_end = time.perf_counter()
+        el = max_over_ranks(t_end - t0)
+        e2e_breakdown = {"upload_and_build_ms": round(1e3 * (t_up - t0), 1), "resume_ms": round(1e3 * (t_res - t_up), 1),
+                         "first_iteration_ms": round(1e3 * (t_it[0] - t_res), 1),
+                         "other_iterations_ms": round(1e3 * (t_it[-1] - t_it[0]), 1),
+                         "result_download_ms": round(1e3 * (t_end - t_it[-1]), 1)}
         d2h = 96 * args.steps + 8 * (res.U.size + res.V.size + res.sigma.size)
         same = all((a["rank"], a["extension_rounds"], a["kept"], a["residual"]) ==
                    (b["rank"], b["extension_rounds"], b["kept"], b["residual"]) for a, b in zip(recs, recs2))
         e2e = {"value": args.steps / el, "unit": "iter/s", "h2d_bytes_per_step": int(h2d / args.steps),
                "d2h_bytes_per_step": int(d2h / args.steps),
                "iterations": [r["iter"] for r in recs2], "same_records_as_timed_window": same,
+               "breakdown_ms": e2e_breakdown,
                "note": "public C-ABI path, wall clock: CSR upload of the sample sets + resume from the host "
                        "checkpoint after W iterations (Y values, U_prev, best factors) from pinned memory, "
                        "iterations W+1..W+K (each reads its record back), factor download"}
